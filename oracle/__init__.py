@@ -1,0 +1,44 @@
+"""Plain, slow, float64 CPU oracle for the FGC entropic Gromov-Wasserstein hot path.
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and the
+``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import anything
+from this package.  The product path (``paper_2404_08970_b200``) never imports it,
+and this package never imports the product path, torch, or any shared helper:
+it is NumPy float64 written from the paper (arXiv 2404.08970, ``PAPER.md``).
+
+Every function cites the passage it follows.  "PAPER.md:N" is a line of the
+paper's LaTeX source; "SPEC.md:N" a line of the CPU-program spec written from it.
+
+Pins (tests/test_oracle_*.py, ``-m "not gpu"``) tie each function to something
+other than itself: worked examples (tests/golden/), closed forms, brute force,
+invariants and finite differences.  Functions without such a pin would say
+"parity unpinned"; in this package only ``ugw`` (not implemented: the paper
+leaves Remark 3's ``g`` undefined) is unpinned.
+"""
+
+from .gw import (  # noqa: F401
+    dist,
+    const_term,
+    grad_entrywise,
+    grad_prescribed,
+    grad_prescribed_dp,
+    grad_realized,
+    ref_dp_lower,
+    ref_dp_upper,
+    ref_dp_distance,
+    triple_product_dp,
+    triple_product_dense,
+    objective,
+    objective_bruteforce,
+    entropy,
+    violation,
+    fgw_grad_prescribed,
+    fgw_objective,
+)
+from .solver import (  # noqa: F401
+    logsumexp,
+    sinkhorn,
+    entropic_gw,
+    entropic_fgw,
+    plan_from_duals,
+)

@@ -1,0 +1,406 @@
+"""Pins for the float64 oracle (-m "not gpu").
+
+Each test ties an oracle function to something other than itself: worked
+examples printed in SPEC.md/PAPER.md (tests/golden/), closed forms derived
+independently here, brute force on tiny inputs, invariants, finite differences
+and an independent convex solver.  A plausible mistake in the oracle (dropped
+term, wrong sign or index, transposed operand, wrong factor 2 or 4, wrong
+schedule) fails at least one of them.
+"""
+
+import itertools
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import workloads as W
+
+GOLDEN = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_examples.json")))
+
+
+def _sorted(rng, n):
+    return np.sort(rng.random(n))
+
+
+def _feasible_plan(rng, p, q, iters=2000):
+    """A strictly positive plan in S(p, q), built by alternating rescaling of a random
+    matrix (input preparation only, independent of the oracle's Sinkhorn)."""
+    Z = rng.random((p.size, q.size)) + 0.1
+    for _ in range(iters):
+        Z *= (p / Z.sum(1))[:, None]
+        Z *= (q / Z.sum(0))[None, :]
+    return Z
+
+
+# --------------------------------------------------------------------------- golden
+
+@pytest.mark.parametrize("ex", GOLDEN["dp"], ids=lambda e: e["id"])
+def test_dp_worked_examples(ex):
+    fn = {"lower": O.ref_dp_lower, "upper": O.ref_dp_upper, "distance": O.ref_dp_distance}[ex["op"]]
+    np.testing.assert_allclose(fn(ex["v"], ex["s"], ex["k"]), ex["expect"], rtol=0, atol=1e-14)
+
+
+@pytest.mark.parametrize("ex", GOLDEN["dist"], ids=lambda e: e["id"])
+def test_dist_worked_examples(ex):
+    np.testing.assert_allclose(O.dist(ex["s"], ex["k"]), ex["expect"], rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("ex", GOLDEN["triple"], ids=lambda e: e["id"])
+def test_triple_product_worked_examples(ex):
+    np.testing.assert_allclose(O.triple_product_dense(ex["x"], ex["y"], ex["T"]), ex["expect"], atol=1e-15)
+    np.testing.assert_allclose(O.triple_product_dp(ex["x"], ex["y"], ex["T"]), ex["expect"], atol=1e-15)
+
+
+@pytest.mark.parametrize("ex", GOLDEN["const_term"], ids=lambda e: e["id"])
+def test_const_term_worked_examples(ex):
+    c, c2 = O.const_term(ex["x"], ex["y"], ex["p"], ex["q"])
+    np.testing.assert_allclose(2 * (c[:, None] + c2[None, :]), ex["expect_C1"], atol=1e-15)
+
+
+@pytest.mark.parametrize("ex", GOLDEN["objective"], ids=lambda e: e["id"])
+def test_objective_worked_examples(ex):
+    assert O.objective(ex["x"], ex["y"], ex["T"]) == pytest.approx(ex["expect"], abs=1e-15)
+    assert O.objective_bruteforce(ex["x"], ex["y"], ex["T"]) == pytest.approx(ex["expect"], abs=1e-15)
+
+
+@pytest.mark.parametrize("ex", GOLDEN["entropy"], ids=lambda e: e["id"])
+def test_entropy_worked_examples(ex):
+    assert O.entropy(ex["T"]) == pytest.approx(ex["expect"], abs=1e-14)
+
+
+def test_sinkhorn_worked_example():
+    ex = GOLDEN["sinkhorn"][0]
+    G = np.array(ex["G"], float)
+    f, g, _ = O.sinkhorn(G, np.array(ex["p"]), np.array(ex["q"]), ex["eps"], 200)
+    T = O.plan_from_duals(G, f, g, ex["eps"])
+    np.testing.assert_allclose(T, ex["expect"], atol=ex["atol"])
+    # the closed form itself: sigma = 1/(1+e^{-1/eps})
+    sig = 1.0 / (1.0 + math.exp(-1.0 / ex["eps"]))
+    np.testing.assert_allclose(T, [[sig / 2, (1 - sig) / 2], [(1 - sig) / 2, sig / 2]], atol=1e-12)
+
+
+# --------------------------------------------------------------------------- DP vs dense
+
+@pytest.mark.parametrize("n", [1, 2, 3, 7, 64])
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_dp_distance_matches_dense(n, k):
+    """the recursion equals the dense product (<= 1e-12 rel)."""
+    rng = np.random.default_rng(n * 10 + k)
+    s = _sorted(rng, n)
+    if n >= 7:
+        s[3] = s[2]  # a tie: zero gap (reading R15)
+    v = rng.random(n)
+    dense = O.dist(s, k) @ v
+    dp = O.ref_dp_distance(v, s, k)
+    assert np.max(np.abs(dp - dense)) <= 1e-12 * max(1.0, np.max(np.abs(dense)))
+    lower = np.array([sum((s[i] - s[j]) ** k * v[j] for j in range(i)) for i in range(n)])
+    np.testing.assert_allclose(O.ref_dp_lower(v, s, k), lower, rtol=1e-12, atol=1e-15)
+
+
+def test_dp_integer_grid_is_paper_recursion():
+    """On the integer grid (h = 1) the gap recursion is the paper's
+    a_{i+1,r} = x_i + sum_s C(r-1,s-1) a_{is}: check against a
+    direct transcription of that integer formula."""
+    n, k = 9, 3
+    v = np.random.default_rng(1).random(n)
+    a = np.zeros((n, k + 1))
+    for i in range(n - 1):
+        for r in range(1, k + 2):
+            a[i + 1, r - 1] = v[i] + sum(math.comb(r - 1, s - 1) * a[i, s - 1] for s in range(1, r + 1))
+    np.testing.assert_allclose(O.ref_dp_lower(v, np.arange(n, dtype=float), k), a[:, k], rtol=1e-14)
+
+
+def test_triple_product_dp_matches_dense():
+    """Paper's exactness claim in fp64: <= 1e-12."""
+    rng = np.random.default_rng(3)
+    for (n, m, k) in [(12, 9, 1), (40, 33, 1), (17, 23, 2)]:
+        x, y = _sorted(rng, n), _sorted(rng, m)
+        T = rng.random((n, m))
+        dense = O.triple_product_dense(x, y, T, k)
+        dp = O.triple_product_dp(x, y, T, k)
+        assert np.linalg.norm(dp - dense) <= 1e-12 * np.linalg.norm(dense)
+
+
+# --------------------------------------------------------------------------- gradient
+
+def test_gradient_three_ways_any_plan():
+    """c2 == c4 for any T: entrywise definition vs decomposition."""
+    rng = np.random.default_rng(4)
+    for (n, m) in [(1, 1), (1, 5), (5, 1), (7, 5), (12, 12)]:
+        x, y = _sorted(rng, n), _sorted(rng, m)
+        T = rng.random((n, m))
+        ge = O.grad_entrywise(x, y, T)
+        gr = O.grad_realized(x, y, T)
+        assert np.max(np.abs(ge - gr)) <= 1e-12 * max(1.0, np.max(np.abs(ge)))
+
+
+def test_gradient_prescribed_on_feasible_plan():
+    """c3 == c2 iff T in S(p, q) (reading R4); and differs for an infeasible T."""
+    rng = np.random.default_rng(5)
+    n, m = 8, 6
+    x, y = _sorted(rng, n), _sorted(rng, m)
+    p, q = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))
+    T = _feasible_plan(rng, p, q)
+    ge = O.grad_entrywise(x, y, T)
+    np.testing.assert_allclose(O.grad_prescribed(x, y, p, q, T), ge, atol=1e-12)
+    np.testing.assert_allclose(O.grad_prescribed_dp(x, y, p, q, T), ge, atol=1e-12)
+    T2 = T * 1.1
+    assert np.max(np.abs(O.grad_prescribed(x, y, p, q, T2) - O.grad_entrywise(x, y, T2))) > 1e-3
+
+
+def test_homogeneity_identity():
+    """<grad E(T), T> = 2 E(T) for every T: catches a wrong factor."""
+    rng = np.random.default_rng(6)
+    x, y = _sorted(rng, 9), _sorted(rng, 7)
+    T = rng.random((9, 7))
+    eb = O.objective_bruteforce(x, y, T)
+    assert np.sum(O.grad_realized(x, y, T) * T) == pytest.approx(2 * eb, rel=1e-12)
+    assert O.objective(x, y, T) == pytest.approx(eb, rel=1e-12)
+
+
+def test_finite_differences():
+    """Central differences of the brute-force E match the gradient."""
+    rng = np.random.default_rng(7)
+    n = 8
+    x, y = _sorted(rng, n), _sorted(rng, n)
+    T = rng.random((n, n)) / n ** 2
+    G = O.grad_realized(x, y, T)
+    d = 1e-6
+    for (i, p) in [(0, 0), (3, 5), (7, 2), (4, 4)]:
+        Tp, Tm = T.copy(), T.copy()
+        Tp[i, p] += d
+        Tm[i, p] -= d
+        fd = (O.objective_bruteforce(x, y, Tp) - O.objective_bruteforce(x, y, Tm)) / (2 * d)
+        assert fd == pytest.approx(G[i, p], rel=1e-5)
+
+
+def test_closed_form_E_of_product_plan():
+    """E(p (x) p) on the uniform grid, X = Y, uniform p:
+    (N+1)/(3(N-1)) - 2((N+1)/(3N))^2, from E[d^2] = 2 Var and E[d] = (N+1)/(3N)
+    of the discrete uniform law (derived from PAPER.md:86)."""
+    printed = {2: 0.5, 3: 0.2716049383, 10: 0.1385185185, 256: 0.1119859882}
+    for n, val in printed.items():
+        x = np.arange(n) / (n - 1)
+        p = np.full(n, 1.0 / n)
+        closed = (n + 1) / (3 * (n - 1)) - 2 * ((n + 1) / (3 * n)) ** 2
+        assert closed == pytest.approx(val, abs=1e-10)
+        assert O.objective(x, x, np.outer(p, p)) == pytest.approx(closed, rel=1e-12)
+
+
+def test_closed_form_first_gradient():
+    """G0 = 2(c_i + c'_p) - 4 (D_X p)_i (D_Y q)_p at T0 = p (x) q,
+    with the integer-index closed forms on a uniform grid and uniform p."""
+    for n in [2, 5, 13]:
+        x = np.arange(n) / (n - 1)
+        p = np.full(n, 1.0 / n)
+        i = np.arange(1, n + 1, dtype=float)
+        DXp = ((i - 1) * i / 2 + (n - i) * (n - i + 1) / 2) / (n * (n - 1))
+        c = ((i - 1) * i * (2 * i - 1) + (n - i) * (n - i + 1) * (2 * n - 2 * i + 1)) / (6 * n * (n - 1) ** 2)
+        G0 = 2 * (c[:, None] + c[None, :]) - 4 * DXp[:, None] * DXp[None, :]
+        np.testing.assert_allclose(O.grad_prescribed(x, x, p, p, np.outer(p, p)), G0, atol=1e-14)
+        np.testing.assert_allclose(O.grad_entrywise(x, x, np.outer(p, p)), G0, atol=1e-14)
+
+
+def test_permutation_couplings_bruteforce():
+    """N <= 6, uniform weights: E(P_sigma) >= 0; E = 0 at the identity when y = x and
+    at the reversal when y = -x (isometries)."""
+    rng = np.random.default_rng(8)
+    for n in [2, 3, 5, 6]:
+        x = _sorted(rng, n)
+        best = np.inf
+        for sig in itertools.permutations(range(n)):
+            P = np.zeros((n, n))
+            P[np.arange(n), sig] = 1.0 / n
+            e = O.objective(x, x, P)
+            assert e >= -1e-15
+            best = min(best, e)
+        P = np.eye(n) / n
+        assert O.objective(x, x, P) == pytest.approx(0.0, abs=1e-15)
+        assert best == pytest.approx(0.0, abs=1e-15)
+        yr = np.sort(-x)
+        R = np.fliplr(np.eye(n)) / n
+        assert O.objective(x, yr, R) == pytest.approx(0.0, abs=1e-14)
+
+
+def test_translation_and_reflection_invariance():
+    """GW is invariant to translation / reflection."""
+    rng = np.random.default_rng(9)
+    n, m = 10, 8
+    x, y = _sorted(rng, n), _sorted(rng, m)
+    p, q = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))
+    T = _feasible_plan(rng, p, q)
+    G = O.grad_prescribed(x, y, p, q, T)
+    np.testing.assert_allclose(O.grad_prescribed(x + 3.7, y - 1.25, p, q, T), G, atol=1e-12)
+    # reflection x -> -x reverses the row order (and p); T -> R T
+    xr = -x[::-1]
+    np.testing.assert_allclose(O.grad_prescribed(xr, y, p[::-1], q, T[::-1]), G[::-1], atol=1e-12)
+    assert O.objective(xr, y, T[::-1]) == pytest.approx(O.objective(x, y, T), rel=1e-12)
+
+
+# --------------------------------------------------------------------------- Sinkhorn
+
+def test_sinkhorn_zero_and_separable_cost():
+    """Zero cost -> p (x) q; separable cost a_i + b_p -> p (x) q."""
+    rng = np.random.default_rng(10)
+    n, m = 6, 4
+    p, q = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))
+    for G in [np.zeros((n, m)), rng.random(n)[:, None] + rng.random(m)[None, :]]:
+        f, g, _ = O.sinkhorn(G, p, q, 0.3, 5)
+        np.testing.assert_allclose(O.plan_from_duals(G, f, g, 0.3), np.outer(p, q), atol=1e-15)
+
+
+def test_sinkhorn_marginals_after_each_half_step():
+    """After the g-update the column sums are exact; after an f-update the row sums
+    are (the two half-steps of PAPER.md:114's Sinkhorn, reading R7)."""
+    rng = np.random.default_rng(11)
+    G = rng.random((7, 5))
+    p, q = rng.dirichlet(np.ones(7)), rng.dirichlet(np.ones(5))
+    eps = 0.05
+    f, g, _ = O.sinkhorn(G, p, q, eps, 3)
+    T = O.plan_from_duals(G, f, g, eps)
+    np.testing.assert_allclose(T.sum(0), q, atol=1e-15)
+    # one more f half-step from (f, g): rows exact
+    f2 = eps * np.log(p) - eps * O.logsumexp((g[None, :] - G) / eps, axis=1)
+    np.testing.assert_allclose(O.plan_from_duals(G, f2, g, eps).sum(1), p, atol=1e-15)
+
+
+def test_sinkhorn_fixed_point_matches_independent_dual_solver():
+    """The Sinkhorn limit equals the maximiser of the entropic-OT dual
+    max_{f,g} <f,p> + <g,q> - eps sum exp((f_i + g_p - G_ip)/eps), found with
+    scipy's L-BFGS (an independent algorithm)."""
+    from scipy.optimize import minimize
+    rng = np.random.default_rng(12)
+    n, m, eps = 4, 3, 0.2
+    G = rng.random((n, m))
+    p, q = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))
+
+    def negdual(z):
+        f, g = z[:n], z[n:]
+        K = np.exp((f[:, None] + g[None, :] - G) / eps)
+        val = f @ p + g @ q - eps * K.sum()
+        grad = np.concatenate([p - K.sum(1), q - K.sum(0)])
+        return -val, -grad
+
+    res = minimize(negdual, np.zeros(n + m), jac=True, method="L-BFGS-B",
+                   options={"gtol": 1e-14, "ftol": 1e-16, "maxiter": 10000})
+    Tref = np.exp((res.x[:n, None] + res.x[None, n:] - G) / eps)
+    f, g, _ = O.sinkhorn(G, p, q, eps, 3000)
+    np.testing.assert_allclose(O.plan_from_duals(G, f, g, eps), Tref, atol=1e-8)
+
+
+def test_sinkhorn_tolerance_rule_stops_on_check():
+    rng = np.random.default_rng(13)
+    G = rng.random((20, 15))
+    p, q = rng.dirichlet(np.ones(20)), rng.dirichlet(np.ones(15))
+    f, g, used = O.sinkhorn(G, p, q, 0.1, 2000, tol=1e-9, check_every=10)
+    assert used % 10 == 0 and used < 2000
+    assert O.violation(O.plan_from_duals(G, f, g, 0.1), p, q) <= 1e-9
+
+
+# --------------------------------------------------------------------------- entropic GW
+
+def test_entropic_gw_single_point():
+    """N = M = 1: G = [[0]], T = [[1]], E = 0."""
+    r = O.entropic_gw([0.3], [0.7], [1.0], [1.0], 0.01, 3, 10, record_grads=True)
+    assert r["T"].tolist() == [[1.0]]
+    assert r["gw_objective"] == 0.0
+    assert r["G"][0].tolist() == [[0.0]]
+
+
+def test_entropic_gw_single_row():
+    """N = 1 < M: T = q as a row and G = 2 c' exactly (P16b)."""
+    rng = np.random.default_rng(14)
+    y = _sorted(rng, 6)
+    q = rng.dirichlet(np.ones(6))
+    r = O.entropic_gw([0.5], y, [1.0], q, 0.01, 2, 20, record_grads=True)
+    np.testing.assert_allclose(r["T"][0], q, atol=1e-15)
+    c2 = (O.dist(y) ** 2) @ q
+    np.testing.assert_allclose(r["G"][1][0], 2 * c2, atol=1e-14)
+
+
+def test_entropic_gw_large_eps_is_product_plan():
+    """eps -> infinity: the entropy term dominates and T -> p (x) q."""
+    P = W.uniform_problem(12, 9, seed=1)
+    r = O.entropic_gw(P.x, P.y, P.p, P.q, 1e6, 3, 20)
+    np.testing.assert_allclose(r["T"], np.outer(P.p, P.q), atol=1e-9)
+
+
+def test_entropic_gw_reversal_equivariance():
+    """Reversing the source (x -> -x reversed, p reversed) gives R T."""
+    P = W.uniform_problem(15, 11, seed=2, eps=0.02)
+    r1 = O.entropic_gw(P.x, P.y, P.p, P.q, P.eps, 4, 50)
+    r2 = O.entropic_gw(-P.x[::-1], P.y, P.p[::-1], P.q, P.eps, 4, 50)
+    np.testing.assert_allclose(r2["T"], r1["T"][::-1], atol=1e-12)
+
+
+def test_entropic_gw_dp_equals_dense_paper_table2():
+    """The paper's central exactness claim (||P_FGC - P||_F =
+    5.12e-15 at N = 500): on its Table 2 workload (uniform grid, U[0,1] weights,
+    k = 1, eps = 0.002, 10 outer iterations), the DP-gradient and dense-gradient
+    solves give plans within 1e-12."""
+    ex = GOLDEN["paper_table2"][0]
+    P = W.table2(ex["N"], seed=0)
+    rd = O.entropic_gw(P.x, P.y, P.p, P.q, P.eps, 10, 30, grad_mode="dense")
+    rp = O.entropic_gw(P.x, P.y, P.p, P.q, P.eps, 10, 30, grad_mode="dp")
+    diff = np.linalg.norm(rd["T"] - rp["T"])
+    assert diff <= ex["bound_used"]
+
+
+def test_entropic_gw_objective_decreases_c1_recipe():
+    """C1 recipe (reduced outer count): E(T^l) falls from E(p (x) q) and the plan is
+    feasible to Sinkhorn precision."""
+    P = W.config1()
+    r = O.entropic_gw(P.x, P.y, P.p, P.q, P.eps, 5, 100)
+    e0 = O.objective(P.x, P.y, np.outer(P.p, P.q))
+    assert r["E"][-1] < r["E"][0] < e0
+    assert r["viol"][-1] < 1e-6
+
+
+# --------------------------------------------------------------------------- FGW
+
+def test_fgw_endpoints():
+    """alpha = 1 is GW; alpha = 0 gives Sinkhorn(C o C) after one outer iteration and
+    a fixed point afterwards."""
+    rng = np.random.default_rng(15)
+    n, m = 9, 7
+    x, y = _sorted(rng, n), _sorted(rng, m)
+    p, q = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))
+    fx, fy = rng.standard_normal(n), rng.standard_normal(m)
+    r1 = O.entropic_fgw(x, y, p, q, fx, fy, 1.0, 0.05, 3, 40)
+    rg = O.entropic_gw(x, y, p, q, 0.05, 3, 40)
+    np.testing.assert_array_equal(r1["T"], rg["T"])
+    r0 = O.entropic_fgw(x, y, p, q, fx, fy, 0.0, 0.05, 3, 40)
+    CC = (fx[:, None] - fy[None, :]) ** 2
+    f, g, _ = O.sinkhorn(CC, p, q, 0.05, 120)
+    np.testing.assert_allclose(r0["T"], O.plan_from_duals(CC, f, g, 0.05), atol=1e-12)
+
+
+def test_fgw_gradient_bruteforce():
+    """grad E_bar = (1-theta) c^2 + theta * 2 sum (d - d)^2 T  on a feasible plan."""
+    rng = np.random.default_rng(16)
+    n, m, th = 6, 5, 0.3
+    x, y = _sorted(rng, n), _sorted(rng, m)
+    p, q = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))
+    fx, fy = rng.standard_normal(n), rng.standard_normal(m)
+    T = _feasible_plan(rng, p, q)
+    brute = (1 - th) * (fx[:, None] - fy[None, :]) ** 2 + th * O.grad_entrywise(x, y, T)
+    np.testing.assert_allclose(O.fgw_grad_prescribed(x, y, p, q, fx, fy, th, T), brute, atol=1e-12)
+
+
+# --------------------------------------------------------------------------- workloads
+
+def test_workloads_deterministic_and_valid():
+    a, b = W.config1(), W.config1()
+    np.testing.assert_array_equal(a.x, b.x)
+    for P in [W.config1(), W.config2(512), W.config4(1024), W.config5(300, 200), W.table2(50)]:
+        assert np.all(np.diff(P.x) >= 0) and np.all(np.diff(P.y) >= 0)
+        assert abs(P.p.sum() - 1) < 1e-12 and abs(P.q.sum() - 1) < 1e-12
+        assert np.all(P.p >= 0) and np.all(P.q >= 0)
+    P3 = W.config3(64)
+    T = P3.extra["T"]
+    assert T.dtype == np.float32 and np.all(T > 0)
+    np.testing.assert_allclose(T.sum(0), P3.q, rtol=1e-5)
