@@ -1,0 +1,267 @@
+#!/usr/bin/env python
+"""Benchmark of the FGC entropic-GW hot path (BASELINE.json metric) -> ONE JSON line.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--n 65536]
+
+A step is one outer mirror-descent iteration of entropic GW on config C4 (BASELINE.json
+configs[3]: N = M = 65536, x, y ~ sort Uniform[0,1), uniform marginals, eps = 1e-3):
+one DP gradient + 100 log-domain Sinkhorn iterations
+(PAPER.md:108-114).  The cost matrix is 17.2 GB (> L2), so no L2 flush is needed.
+
+value     : outer iterations / s, device-timed (CUDA events on the library's stream,
+            barrier + synchronize on both sides, max over ranks), inputs resident in HBM.
+e2e       : the same metric through the public host-vector call (solve_host):
+            H2D of x, y, p, q from pinned memory and D2H of the duals inside the timed region.
+roofline  : dominant kernel (Sinkhorn half-steps), algorithmic bytes / live event time.
+cpu_baseline / --impl reference : the float64 NumPy oracle (oracle/) on the host cores,
+            a bounded sample extrapolated to the metric's unit (see "sample").
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "DP GW-gradient GB/s (% of HBM peak) and entropic-GW outer iters/s at N=M=65536"
+UNIT = "outer_iter/s"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
+
+
+def peaks():
+    try:
+        d = json.load(open(PEAKS_PATH))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            r = [x.strip() for x in r]
+            try:
+                sm.append(float(r[1]))
+                smax = float(r[2])
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, r[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ----------------------------------------------------------------------------- oracle baseline
+
+def oracle_sample(n_s=2048, n_full=65536, inner=100, sweeps=3):
+    """Time the float64 oracle on the C4 recipe at n_s: the dense gradient (2 DGEMMs,
+    O(N^3)) and Sinkhorn iterations (O(N^2)), then extrapolate one outer iteration to
+    n_full: t = t_grad (n_full/n_s)^3 + inner * t_sweep (n_full/n_s)^2."""
+    import numpy as np
+    import oracle as O
+    import workloads as W
+    P = W.config4(n_s)
+    T = np.outer(P.p, P.q)
+    t0 = time.perf_counter()
+    G = O.grad_prescribed(P.x, P.y, P.p, P.q, T)
+    t_grad = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    O.sinkhorn(G, P.p, P.q, P.eps, sweeps)
+    t_sweep = (time.perf_counter() - t0) / sweeps
+    r = n_full / n_s
+    t_outer = t_grad * r ** 3 + inner * t_sweep * r ** 2
+    cores = len(os.sched_getaffinity(0))
+    try:
+        from threadpoolctl import threadpool_info
+        blas = max((d.get("num_threads", 1) for d in threadpool_info()), default=1)
+    except Exception:
+        blas = cores
+    return {"value": 1.0 / t_outer, "unit": UNIT, "cores": int(max(blas, 1)), "kind": "oracle",
+            "sample": ("oracle (float64 NumPy) on the C4 recipe at N=M=%d: dense gradient %.3f s + %d Sinkhorn "
+                       "iterations at %.3f s each, extrapolated to N=M=%d as t_grad*(N/%d)^3 + 100*t_sweep*(N/%d)^2"
+                       % (n_s, t_grad, sweeps, t_sweep, n_full, n_s, n_s)),
+            "t_grad_s": t_grad, "t_sweep_s": t_sweep}
+
+
+# ----------------------------------------------------------------------------- main
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=65536, help="N = M (default: BASELINE config 4)")
+    ap.add_argument("--inner", type=int, default=100)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    config = {"workload": "C4 (BASELINE configs[3]): 1-D entropic GW, N=M=%d fp32, x,y ~ sort Uniform[0,1), "
+                          "uniform p,q, eps=1e-3, T0=p(x)q, seed 0; step = 1 DP gradient + %d log-domain Sinkhorn "
+                          "iterations" % (args.n, args.inner),
+              "N": args.n, "M": args.n, "eps": 1e-3, "inner_iters": args.inner,
+              "l2": "no flush needed: the N x M cost matrix (%.1f GB) is larger than L2 (126 MB)"
+                    % (4.0 * args.n * args.n / 1e9),
+              "parallelism": "rows sharded over %d GPU(s)" % world}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        samples = []
+        for i in range(args.warmup + args.steps):
+            s = oracle_sample(n_s=1024 if args.n >= 1024 else args.n, n_full=args.n, inner=args.inner, sweeps=2)
+            if i >= args.warmup:
+                samples.append(s)
+        v = statistics.median(s["value"] for s in samples)
+        cb = dict(samples[-1])
+        cb["value"] = v
+        print(json.dumps({"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / v,
+                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                          "data": "synthetic", "config": config, "cpu_baseline": cb,
+                          "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import workloads as W
+    from paper_2404_08970_b200 import api, _lib
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        raise SystemExit("multi-GPU sharding: see DESIGN.md (not in this build)")
+
+    P = W.config4(args.n)
+    n, m = P.n, P.m
+    x, y, p, q = (torch.as_tensor(v, dtype=torch.float64, device=dev) for v in (P.x, P.y, P.p, P.q))
+    ctx = api.Context.get(dev)
+    lib = _lib.load()
+    # ---- warm-up (untimed) ----
+    api.solve(x, y, p, q, P.eps, args.warmup, args.inner, device=dev, ctx=ctx)
+    torch.cuda.synchronize()
+    # ---- timed region ----
+    clocks = ClockSampler(local_rank)
+    import ctypes as C
+    ms_c = (C.c_double * 7)()
+    cnt_c = (C.c_int64 * 7)()
+    _lib.check(lib.gw_ctx_profile(ctx.h, 2, None, None, 0))
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(ctx.stream)
+    res = api.solve(x, y, p, q, P.eps, args.steps, args.inner, device=dev, ctx=ctx)
+    e1.record(ctx.stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ck = clocks.stop()
+    _lib.check(lib.gw_ctx_profile(ctx.h, 0, C.cast(ms_c, C.c_void_p), C.cast(cnt_c, C.c_void_p), 7))
+    elapsed_ms = e0.elapsed_time(e1)
+    value = args.steps / (elapsed_ms / 1000.0)
+
+    # ---- roofline (live, per kernel class) ----
+    hbm, peak_src = peaks()
+    names = ["grad_moments", "grad_carry", "grad_main", "sink_row", "sink_col"]
+    algo_bytes = {"grad_moments": 4.0 * n * m, "grad_main": 8.0 * n * m, "sink_row": 4.0 * n * m,
+                  "sink_col": 4.0 * n * m}
+    kern = {}
+    for k, nm in enumerate(names):
+        if cnt_c[k] > 0:
+            ms_launch = ms_c[k] / cnt_c[k] * (2 if nm == "sink_col" else 1)  # sink_col counts col+colfin
+            d = {"ms_total": ms_c[k], "launches": int(cnt_c[k]), "ms_per_launch": ms_launch}
+            if nm in algo_bytes:
+                d["GBps"] = algo_bytes[nm] / (ms_launch / 1000.0) / 1e9
+                d["frac"] = d["GBps"] / hbm
+            kern[nm] = d
+    dom = max(("sink_row", "sink_col"), key=lambda k: kern.get(k, {}).get("ms_total", 0))
+    roof = {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["GBps"], "peak": hbm, "unit": "GB/s",
+            "frac": kern[dom]["frac"], "traffic": None, "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": algo_bytes[dom],
+            "share_of_step": kern[dom]["ms_total"] / elapsed_ms}
+    grad_ms = sum(kern.get(k, {}).get("ms_total", 0) for k in ("grad_moments", "grad_carry", "grad_main"))
+    grad_ms /= max(1, kern.get("grad_main", {}).get("launches", 1))
+    grad = {"ms_per_gradient": grad_ms, "algorithmic_bytes": 12.0 * n * m,
+            "GBps_algorithmic": 12.0 * n * m / (grad_ms / 1000.0) / 1e9,
+            "frac_of_peak": 12.0 * n * m / (grad_ms / 1000.0) / 1e9 / hbm,
+            "note": "standalone-T form: moments pass (4NM) + main pass (8NM) bytes"}
+
+    # ---- e2e through the public host-vector call (pinned inputs, D2H of duals) ----
+    pin = [torch.empty(v.size, dtype=torch.float64).pin_memory() for v in (P.x, P.y, P.p, P.q)]
+    for t, v in zip(pin, (P.x, P.y, P.p, P.q)):
+        t.numpy()[:] = v
+    torch.cuda.synchronize()
+    h0 = time.perf_counter()
+    re = api.solve_host(*(t.numpy() for t in pin), P.eps, args.steps, args.inner, ctx=ctx)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - h0
+    e2e = {"value": args.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * (2 * n + 2 * m) / args.steps,
+           "d2h_bytes_per_step": 8 * (n + m) / args.steps,
+           "note": "one solve_host call of %d outer iterations timed on the host clock around the call "
+                   "(inputs staged H2D and duals copied D2H inside it)" % args.steps}
+
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config,
+           "roofline": roof, "grad": grad, "kernels": kern,
+           "gpu_launches": int(cnt_c[6]),
+           "clocks": ck, "e2e": e2e,
+           "result": {"gw_objective": res.gw_objective, "marginal_violation": res.marginal_violation,
+                      "e2e_gw_objective": re.gw_objective}}
+    if rank == 0 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = oracle_sample(n_s=2048 if args.n >= 2048 else args.n, n_full=args.n,
+                                            inner=args.inner)
+    if rank == 0:
+        print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,200 @@
+/*
+ * gwdp.h -- C ABI of the B200-native FGC entropic Gromov-Wasserstein hot path.
+ *
+ * Paper: "Efficient Gradient Computation for Gromov-Wasserstein" style FGC-GW,
+ * arXiv 2404.08970 (PAPER.md in the reference).  Citations below are
+ * "PAPER.md:<line>" (the paper's LaTeX source) and "SPEC.md:<line>".
+ *
+ * Problem (notation of SURVEY.md §0.3 / BASELINE.json):
+ *   x in R^n (rows, marginal p), y in R^m (columns, marginal q), both
+ *   NON-DECREASING; D_X[i,j] = |x_i - x_j|^k, D_Y[p,q] = |y_p - y_q|^k
+ *   (generalised to sorted supports: reading R1 in DESIGN.md);
+ *   plan T (n x m, the paper's Gamma), row-major.
+ *   GW gradient (transpose typo fixed, reading R3):
+ *     G = 2 (c 1^T + 1 c'^T) - 4 D_X T D_Y,  c = (D_X o D_X) p,  c' = (D_Y o D_Y) q.
+ *   Entropic GW by mirror descent with tau = eps
+ *   (Remark 1 PAPER.md:127-133):
+ *     T^l = argmin_{T in S(p,q)} <G(T^{l-1}), T> + eps H(T),  solved by log-domain
+ *     Sinkhorn: f_i = eps ln p_i - eps LSE_p((g_p - G_ip)/eps),
+ *               g_p = eps ln q_p - eps LSE_i((f_i - G_ip)/eps),
+ *     T_ip = exp((f_i + g_p - G_ip)/eps).
+ *
+ * Conventions (all entry points):
+ *   - Every pointer is a DEVICE pointer on ctx's device unless the problem's
+ *     flags contain GW_HOST_VECTORS (then x, y, p, q, f, g, fx, fy are HOST
+ *     pointers and the library stages them; N x M matrices are always device).
+ *     The caller owns every argument; the library never frees or retains them.
+ *   - N x M matrices: row-major fp32 (gw_dtype GW_F32), leading dimension
+ *     ld >= m, ld % 4 == 0, 16-byte aligned base.  A rank holds only its
+ *     n_local rows [row0, row0 + n_local).
+ *   - Work is enqueued on ctx's stream.  Calls that fill host structs
+ *     (info, res, trace) synchronise that stream before returning.
+ *   - Errors: a status is returned; no exception or abort crosses the ABI;
+ *     gw_last_error() returns a thread-local message.  Argument and validation
+ *     errors are detected before any output is written.  Asynchronous CUDA
+ *     faults surface as GW_ERR_CUDA at the next synchronising call.
+ *     Sinkhorn not reaching tol within max_iter is NOT an error
+ *     (converged = 0).
+ *   - Inputs are never mutated; marginals within 1e-9 of unit mass are
+ *     renormalised in an internal copy.
+ *   - Results are bitwise reproducible for fixed inputs, sizes and world size
+ *     (fixed-order reductions, no float atomics on result paths).
+ */
+#ifndef GWDP_H
+#define GWDP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GWDP_ABI_VERSION 1
+
+typedef struct gw_ctx gw_ctx;    /* opaque: device, stream, workspace, optional comm */
+typedef struct gw_comm gw_comm;  /* opaque: NCCL communicator, rank, world size      */
+
+typedef enum {
+  GW_OK = 0,
+  GW_ERR_INVALID_ARG = 1,     /* null pointer, bad size, bad ld / alignment, eps <= 0 */
+  GW_ERR_DIM_MISMATCH = 2,    /* shard does not fit (row0 + n_local > n)              */
+  GW_ERR_UNSORTED = 3,        /* x or y not non-decreasing (reading R16)              */
+  GW_ERR_NEGATIVE_WEIGHT = 4, /* p or q has a negative entry             */
+  GW_ERR_NOT_NORMALIZED = 5,  /* |sum - 1| > 1e-9                        */
+  GW_ERR_NONFINITE = 6,       /* NaN/Inf in inputs or produced          */
+  GW_ERR_CONFIG = 7,          /* invalid options                                       */
+  GW_ERR_UNSUPPORTED = 8,     /* k != 1, loss != square, tau != eps, fp64 storage, UGW */
+  GW_ERR_OOM = 9,
+  GW_ERR_CUDA = 10,
+  GW_ERR_NCCL = 11
+} gw_status;
+
+typedef enum { GW_LOSS_SQUARE = 0 } gw_loss;       /* the only loss the paper defines */
+typedef enum { GW_F32 = 0, GW_F64 = 1 } gw_dtype;  /* storage of every N x M matrix */
+
+/* problem flags */
+#define GW_NO_VALIDATE     0x1u  /* skip sortedness / marginal checks (caller guarantees them) */
+#define GW_HOST_VECTORS    0x2u  /* x, y, p, q (and f, g, fx, fy outputs/inputs) are host pointers */
+
+typedef struct {
+  int64_t n, m;           /* global sizes: x in R^n (rows), y in R^m (columns)        */
+  int64_t row0, n_local;  /* this rank's row shard; (0, n) on one GPU                  */
+  const double *x, *y;    /* supports, non-decreasing (length n and m)                 */
+  const double *p, *q;    /* marginals, >= 0, sum 1 within 1e-9 (length n and m)       */
+  int32_t k;              /* distance power |x - x'|^k; only k = 1 (hot path, R17)      */
+  int32_t loss;           /* gw_loss */
+  int32_t dtype;          /* gw_dtype; only GW_F32 in this ABI version                 */
+  uint32_t flags;         /* GW_NO_VALIDATE | GW_HOST_VECTORS                          */
+} gw_problem;
+
+/* Optional precomputed moments of T (device, fp64).  Not used in ABI v1
+ * (gw_grad_dp always computes them in its moments pass); reserved. */
+typedef struct {
+  const double *row_sum, *row_ysum;   /* T 1, T y over this shard's rows       */
+  const double *col_sum, *col_xsum;   /* T^T 1, T^T x over ALL rows            */
+} gw_moments;
+
+typedef struct {
+  double eps;           /* entropic regulariser, > 0                   */
+  int32_t max_iter;     /* Sinkhorn iterations (f-update + g-update pairs)           */
+  double tol;           /* stop when marginal violation <= tol; <= 0: run max_iter    */
+  int32_t check_every;  /* violation check period (iterations) when tol > 0           */
+} gw_sinkhorn_opts;
+
+typedef struct {
+  int32_t iters;               /* iterations performed                                */
+  int32_t converged;           /* 1 if violation <= tol was observed                   */
+  double marginal_violation;   /* max(|T1 - p|_inf, |T^T 1 - q|_inf) of the final plan */
+} gw_sinkhorn_info;
+
+/* solve flags */
+#define GW_SOLVE_TRACE_OBJECTIVE 0x1u  /* fill trace[l*4+0] = E(T^l) for every l (costs one
+                                          moments+reduce pass for the last l only)        */
+
+typedef struct {
+  double eps, tau;            /* tau must equal eps (Remark 1, reading R6)            */
+  int32_t outer_iters;        /* mirror-descent iterations L                           */
+  gw_sinkhorn_opts inner;     /* inner.eps is ignored (eps above is used)              */
+  uint32_t flags;             /* GW_SOLVE_* */
+} gw_solve_opts;
+
+typedef struct {
+  double gw_objective;        /* E(T^L), realised marginals (R13)          */
+  double entropic_objective;  /* E(T^L) + eps H(T^L)                  */
+  double marginal_violation;  /* of T^L                                                 */
+  int32_t outer_iters, inner_iters_total, converged;
+  double ms_grad, ms_sinkhorn, ms_total;
+} gw_result;
+
+/* ---- context / communicator ------------------------------------------------------ */
+
+/* Create a context on `device`, enqueuing on `cuda_stream` (a cudaStream_t; NULL =
+ * the legacy default stream).  `comm` may be NULL (single GPU). */
+gw_status gw_ctx_create(gw_ctx **out, int device, void *cuda_stream, gw_comm *comm);
+gw_status gw_ctx_destroy(gw_ctx *ctx);
+/* Release the context's workspace (it is re-grown lazily). */
+gw_status gw_ctx_trim(gw_ctx *ctx);
+/* Kernel-class timing with CUDA events on ctx's stream (for measurement harnesses).
+ * enable: 0 off, 1 on, 2 on + reset totals.  out_ms / out_counts (host, nullable) receive
+ * `nslots` entries: {grad_moments, grad_carry, grad_main, sink_row, sink_col, other}
+ * accumulated since the last reset; with nslots >= 7, out_counts[6] = all kernel launches of
+ * the library since the last reset.  Synchronises ctx's stream. */
+gw_status gw_ctx_profile(gw_ctx *ctx, int enable, double *out_ms, int64_t *out_counts, int nslots);
+const char *gw_last_error(void);
+int gw_abi_version(void);
+
+/* NCCL bootstrap: rank 0 gets a 128-byte id, the caller broadcasts it (e.g. with
+ * torch.distributed), every rank calls gw_comm_init with the same id. */
+gw_status gw_get_unique_id(unsigned char id[128]);
+gw_status gw_comm_init(gw_comm **out, const unsigned char id[128], int nranks, int rank);
+gw_status gw_comm_destroy(gw_comm *comm);
+
+/* ---- hot path ----------------------------------------------------------------------- */
+
+/* G = 2(c 1^T + 1 c'^T) - 4 D_X T D_Y for the rows [row0, row0 + n_local)
+ * in O(n m) by the paper's dynamic programme
+ * realised as row and column prefix scans with fp64 carries.
+ * T: device fp32 (n_local x m, ldT); G: device fp32 output (ldG), may alias T
+ * (ldG == ldT).  c, c' use the PRESCRIBED p, q (reading R4).  mom: must be NULL
+ * in ABI v1.  Asynchronous. */
+gw_status gw_grad_dp(gw_ctx *ctx, const gw_problem *prob, const void *T, int64_t ldT,
+                     void *G, int64_t ldG, const gw_moments *mom);
+
+/* Log-domain Sinkhorn on cost G, never materialising
+ * exp(-G/eps).  f (n_local) and g (m) are in/out fp64 duals (warm start; pass
+ * zeros for a cold start).  T_out (nullable): the plan exp((f+g-G)/eps), fp32,
+ * ldT.  info (host, nullable).  Iteration = f-update then g-update (reading R7). */
+gw_status sinkhorn_solve(gw_ctx *ctx, const gw_problem *prob, const void *G, int64_t ldG,
+                         const gw_sinkhorn_opts *opts, double *f, double *g,
+                         void *T_out, int64_t ldT, gw_sinkhorn_info *info);
+
+/* Entropic GW by mirror descent, tau = eps.
+ * T0: initial plan (device fp32, nullable -> p (x) q, reading R5); T_out: final plan
+ * (nullable).  f, g: final duals (f has n_local entries, g has m).  res (host,
+ * required).  trace (host, nullable): [outer_iters x 4] doubles per outer l:
+ * {E(T^l) (NaN unless GW_SOLVE_TRACE_OBJECTIVE), violation of T^l,
+ *  Sinkhorn iterations used, milliseconds}.  The iteration counts let the oracle
+ * replay the schedule (reading R8). */
+gw_status entropic_gw_solve(gw_ctx *ctx, const gw_problem *prob, const gw_solve_opts *opts,
+                            const void *T0, void *T_out, int64_t ldT, double *f, double *g,
+                            gw_result *res, double *trace);
+
+/* Fused GW (Remark 2): cost (1-alpha) C o C + alpha G with the
+ * feature cost C_ip = |fx_i - fy_p| (never stored), objective
+ * (1-alpha) <C o C, T> + alpha E(T).  fx (n), fy (m).  Same conventions as
+ * entropic_gw_solve. */
+gw_status fgw_solve(gw_ctx *ctx, const gw_problem *prob, const double *fx, const double *fy,
+                    double alpha, const gw_solve_opts *opts, const void *T0, void *T_out,
+                    int64_t ldT, double *f, double *g, gw_result *res, double *trace);
+
+/* Unbalanced GW (Remark 3): the paper leaves g(Gamma-hat)
+ * undefined, so there is no definition to implement against.
+ * Always returns GW_ERR_UNSUPPORTED. */
+gw_status ugw_solve(gw_ctx *ctx, const gw_problem *prob, double rho, const gw_solve_opts *opts,
+                    const void *T0, void *T_out, int64_t ldT, double *f, double *g,
+                    gw_result *res, double *trace);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GWDP_H */

@@ -1,0 +1,231 @@
+"""Python binding of the C ABI (include/gwdp.h): argument marshalling only.
+
+Every step of the hot path runs in libgwdp.so's CUDA kernels; torch provides device
+memory and the stream.  Names follow the C ABI: ``grad`` -> gw_grad_dp,
+``sinkhorn`` -> sinkhorn_solve, ``solve`` -> entropic_gw_solve / fgw_solve.
+"""
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+__all__ = ["Context", "grad", "sinkhorn", "solve", "solve_host", "ugw_solve", "Result", "plan_buffer"]
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
+
+
+def _vec(v, device):
+    t = torch.as_tensor(v, dtype=torch.float64, device=device)
+    return t.contiguous()
+
+
+def _ld(m):
+    return (m + 31) // 32 * 32
+
+
+def plan_buffer(n, m, device=None, dtype=torch.float32):
+    """An (n, m) view into an (n, ld) buffer with ld % 32 == 0 (the ABI needs ld % 4 == 0)."""
+    buf = torch.empty((n, _ld(m)), dtype=dtype, device=device)
+    return buf[:, :m]
+
+
+def _check_mat(t, name):
+    if t.dtype != torch.float32 or not t.is_cuda or t.dim() != 2 or t.stride(1) != 1:
+        raise ValueError("%s must be a 2-D row-major float32 CUDA tensor" % name)
+    return t.stride(0)
+
+
+class Context:
+    """One gw_ctx per (device, stream); owns the library workspace."""
+
+    _cache = {}
+
+    def __init__(self, device=None, stream=None, comm=None):
+        self.lib = L.load()
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else torch.device(device).index or 0)
+        self.device = dev
+        s = torch.cuda.current_stream(dev) if stream is None else stream
+        self.stream = s
+        h = C.c_void_p()
+        L.check(self.lib.gw_ctx_create(C.byref(h), dev.index, C.c_void_p(s.cuda_stream),
+                                       C.c_void_p(comm) if comm else C.c_void_p(0)))
+        self.h = h
+
+    @classmethod
+    def get(cls, device=None):
+        dev = torch.cuda.current_device() if device is None else torch.device(device).index or 0
+        key = (dev, torch.cuda.current_stream(dev).cuda_stream)
+        if key not in cls._cache:
+            cls._cache[key] = Context(dev)
+        return cls._cache[key]
+
+    def trim(self):
+        L.check(self.lib.gw_ctx_trim(self.h))
+
+    def close(self):
+        if self.h:
+            self.lib.gw_ctx_destroy(self.h)
+            self.h = None
+
+
+def _problem(x, y, p, q, n_local=None, row0=0, flags=0):
+    pr = L.gw_problem()
+    pr.n, pr.m = x.numel(), y.numel()
+    pr.row0 = row0
+    pr.n_local = pr.n if n_local is None else n_local
+    pr.x, pr.y, pr.p, pr.q = x.data_ptr(), y.data_ptr(), p.data_ptr(), q.data_ptr()
+    pr.k, pr.loss, pr.dtype, pr.flags = 1, L.GW_LOSS_SQUARE, L.GW_F32, flags
+    return pr
+
+
+def grad(x, y, p, q, T, out=None, validate=True, ctx=None):
+    """G = 2(c 1^T + 1 c'^T) - 4 D_X T D_Y  (gw_grad_dp), fp32."""
+    ctx = ctx or Context.get(T.device)
+    dev = T.device
+    x, y, p, q = (_vec(v, dev) for v in (x, y, p, q))
+    ldT = _check_mat(T, "T")
+    n, m = T.shape
+    if out is None:
+        out = plan_buffer(n, m, dev)
+    ldG = _check_mat(out, "out")
+    pr = _problem(x, y, p, q, flags=0 if validate else L.GW_NO_VALIDATE)
+    L.check(ctx.lib.gw_grad_dp(ctx.h, C.byref(pr), _ptr(T), ldT, _ptr(out), ldG, None))
+    return out
+
+
+def sinkhorn(G, p, q, eps, max_iter, tol=0.0, check_every=10, f=None, g=None, return_plan=False, ctx=None):
+    """Log-domain Sinkhorn on cost G (sinkhorn_solve).  Returns a dict with
+    f, g (fp64 CUDA), iters, converged, violation and optionally T."""
+    ctx = ctx or Context.get(G.device)
+    dev = G.device
+    n, m = G.shape
+    ldG = _check_mat(G, "G")
+    p, q = _vec(p, dev), _vec(q, dev)
+    # supports are irrelevant to Sinkhorn but the problem struct carries them: pass sorted dummies
+    xs = torch.arange(n, dtype=torch.float64, device=dev)
+    ys = torch.arange(m, dtype=torch.float64, device=dev)
+    f = torch.zeros(n, dtype=torch.float64, device=dev) if f is None else _vec(f, dev).clone()
+    g = torch.zeros(m, dtype=torch.float64, device=dev) if g is None else _vec(g, dev).clone()
+    T = plan_buffer(n, m, dev) if return_plan else None
+    pr = _problem(xs, ys, p, q)
+    o = L.gw_sinkhorn_opts(eps, int(max_iter), float(tol), int(check_every))
+    info = L.gw_sinkhorn_info()
+    L.check(ctx.lib.sinkhorn_solve(ctx.h, C.byref(pr), _ptr(G), ldG, C.byref(o), _ptr(f), _ptr(g), _ptr(T),
+                                   T.stride(0) if T is not None else 0, C.byref(info)))
+    out = {"f": f, "g": g, "iters": info.iters, "converged": bool(info.converged),
+           "violation": info.marginal_violation}
+    if return_plan:
+        out["T"] = T
+    return out
+
+
+@dataclass
+class Result:
+    gw_objective: float
+    entropic_objective: float
+    marginal_violation: float
+    outer_iters: int
+    inner_iters_total: int
+    converged: bool
+    ms_grad: float
+    ms_sinkhorn: float
+    ms_total: float
+    f: Optional[object] = None
+    g: Optional[object] = None
+    T: Optional[object] = None
+    trace: Optional[np.ndarray] = None   # [outer, 4]: E(T^l), violation, inner iters, ms
+    extra: dict = field(default_factory=dict)
+
+
+def _result(res, f, g, T, tr):
+    return Result(res.gw_objective, res.entropic_objective, res.marginal_violation, res.outer_iters,
+                  res.inner_iters_total, bool(res.converged), res.ms_grad, res.ms_sinkhorn, res.ms_total,
+                  f, g, T, tr)
+
+
+def _opts(eps, outer, inner, tol, check_every, trace_objective):
+    o = L.gw_solve_opts()
+    o.eps = eps
+    o.tau = eps
+    o.outer_iters = int(outer)
+    o.inner = L.gw_sinkhorn_opts(eps, int(inner), float(tol), int(check_every))
+    o.flags = L.GW_SOLVE_TRACE_OBJECTIVE if trace_objective else 0
+    return o
+
+
+def solve(x, y, p, q, eps, outer, inner, tol=0.0, check_every=10, T0=None, return_plan=False,
+          trace_objective=False, fx=None, fy=None, alpha=None, device=None, ctx=None):
+    """Entropic GW (entropic_gw_solve) or, with fx/fy/alpha, entropic FGW (fgw_solve), on
+    device vectors; tau = eps."""
+    dev = torch.device(device) if device is not None else (T0.device if T0 is not None else torch.device("cuda"))
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    ctx = ctx or Context.get(dev)
+    x, y, p, q = (_vec(v, dev) for v in (x, y, p, q))
+    n, m = x.numel(), y.numel()
+    f = torch.empty(n, dtype=torch.float64, device=dev)
+    g = torch.empty(m, dtype=torch.float64, device=dev)
+    T = plan_buffer(n, m, dev) if return_plan else None
+    ld = 0
+    if T0 is not None:
+        ld = _check_mat(T0, "T0")
+        if T is not None and T.stride(0) != ld:
+            T = torch.empty((n, ld), dtype=torch.float32, device=dev)[:, :m]
+    elif T is not None:
+        ld = T.stride(0)
+    pr = _problem(x, y, p, q)
+    o = _opts(eps, outer, inner, tol, check_every, trace_objective)
+    res = L.gw_result()
+    tr = np.zeros((max(int(outer), 1), 4), dtype=np.float64)
+    trp = tr.ctypes.data_as(C.c_void_p)
+    if fx is not None:
+        fxv, fyv = _vec(fx, dev), _vec(fy, dev)
+        L.check(ctx.lib.fgw_solve(ctx.h, C.byref(pr), _ptr(fxv), _ptr(fyv), float(alpha), C.byref(o), _ptr(T0),
+                                  _ptr(T), ld, _ptr(f), _ptr(g), C.byref(res), trp))
+    else:
+        L.check(ctx.lib.entropic_gw_solve(ctx.h, C.byref(pr), C.byref(o), _ptr(T0), _ptr(T), ld, _ptr(f), _ptr(g),
+                                          C.byref(res), trp))
+    return _result(res, f, g, T, tr[: int(outer)])
+
+
+def solve_host(x, y, p, q, eps, outer, inner, tol=0.0, check_every=10, device=None, ctx=None,
+               fx=None, fy=None, alpha=None):
+    """entropic_gw_solve with HOST vectors (GW_HOST_VECTORS): the library stages x, y, p, q
+    host->device and copies the duals f, g back.  This is the end-to-end public call."""
+    ctx = ctx or Context.get(device)
+    xs, ys, ps, qs = (np.ascontiguousarray(v, dtype=np.float64) for v in (x, y, p, q))
+    n, m = xs.size, ys.size
+    f = np.empty(n)
+    g = np.empty(m)
+    pr = L.gw_problem()
+    pr.n, pr.m, pr.row0, pr.n_local = n, m, 0, n
+    pr.x, pr.y, pr.p, pr.q = (a.ctypes.data for a in (xs, ys, ps, qs))
+    pr.k, pr.loss, pr.dtype, pr.flags = 1, L.GW_LOSS_SQUARE, L.GW_F32, L.GW_HOST_VECTORS
+    o = _opts(eps, outer, inner, tol, check_every, False)
+    res = L.gw_result()
+    tr = np.zeros((max(int(outer), 1), 4))
+    fp = f.ctypes.data_as(C.c_void_p)
+    gp = g.ctypes.data_as(C.c_void_p)
+    if fx is not None:
+        fxs, fys = (np.ascontiguousarray(v, dtype=np.float64) for v in (fx, fy))
+        L.check(ctx.lib.fgw_solve(ctx.h, C.byref(pr), fxs.ctypes.data_as(C.c_void_p),
+                                  fys.ctypes.data_as(C.c_void_p), float(alpha), C.byref(o), None, None, 0, fp, gp,
+                                  C.byref(res), tr.ctypes.data_as(C.c_void_p)))
+    else:
+        L.check(ctx.lib.entropic_gw_solve(ctx.h, C.byref(pr), C.byref(o), None, None, 0, fp, gp, C.byref(res),
+                                          tr.ctypes.data_as(C.c_void_p)))
+    return _result(res, f, g, None, tr[: int(outer)])
+
+
+def ugw_solve(*args, **kwargs):
+    """Unbalanced GW (Remark 3): the paper leaves g(Gamma-hat) undefined -> GW_ERR_UNSUPPORTED."""
+    ctx = Context.get()
+    res = L.gw_result()
+    L.check(ctx.lib.ugw_solve(ctx.h, None, 1.0, None, None, None, 0, None, None, C.byref(res), None))

@@ -1,0 +1,832 @@
+// gwdp.cu -- host side of the C ABI (include/gwdp.h): context, workspace, validation,
+// the gradient pass, Sinkhorn and the entropic (F)GW mirror-descent loop.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/gwdp.h"
+#include "common.cuh"
+#include "grad.cuh"
+#include "sink.cuh"
+#include "vec.cuh"
+
+using namespace gw;
+
+// ------------------------------------------------------------------------------ errors
+static thread_local std::string g_err;
+
+static gw_status fail(gw_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define CU(x)                                                                                  \
+  do {                                                                                         \
+    cudaError_t e_ = (x);                                                                      \
+    if (e_ != cudaSuccess)                                                                     \
+      return fail(e_ == cudaErrorMemoryAllocation ? GW_ERR_OOM : GW_ERR_CUDA, "%s: %s (%s:%d)", \
+                  #x, cudaGetErrorString(e_), __FILE__, __LINE__);                             \
+  } while (0)
+#define TRY(x)                      \
+  do {                              \
+    gw_status s_ = (x);             \
+    if (s_ != GW_OK) return s_;     \
+  } while (0)
+// every kernel launch is followed by KCHECK(); it also counts launches on the ctx `c`
+#define KCHECK()                 \
+  do {                           \
+    CU(cudaGetLastError());      \
+    ++c->launches;               \
+  } while (0)
+
+// ------------------------------------------------------------------------------ context
+struct Buf {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+
+struct gw_comm {
+  ncclComm_t nccl = nullptr;
+  int nranks = 1, rank = 0;
+};
+
+// Per-kernel-class CUDA-event timing (enabled by gw_ctx_profile; events on ctx's stream).
+enum { PC_GRAD_MOMENTS = 0, PC_GRAD_CARRY, PC_GRAD_MAIN, PC_SINK_ROW, PC_SINK_COL, PC_OTHER, PC_N };
+struct Prof {
+  bool on = false;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  double ms[PC_N] = {0};
+  long long cnt[PC_N] = {0};
+};
+
+struct gw_ctx {
+  Prof prof;
+  long long launches = 0;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  gw_comm* comm = nullptr;
+  std::vector<Buf*> all;
+  // vectors
+  Buf stage, mom, xc, yc, pn, qn, lp, lq, cvx, cvy;
+  Buf fs, gs, fh, fl, gh, gl, ftmp, viol, stop, iters, part;
+  // gradient aux
+  Buf rP, rA, cS, cX, blk, bs, btot, cxend, SAg, WAg, Ptot, Aend, DP, DA, tobj, tent, tcc, objout;
+  Buf fxs, fys;  // FGW features (staged)
+  Buf fsc, gsc;  // scaled duals for the Gibbs regeneration
+  Buf Gs;        // solver cost buffer
+  double* hpin = nullptr;  // pinned host scratch (64 doubles)
+  gw_ctx() {
+    Buf* b[] = {&stage, &mom, &xc, &yc, &pn, &qn, &lp, &lq, &cvx, &cvy, &fs, &gs, &fh, &fl, &gh, &gl,
+                &ftmp, &viol, &stop, &iters, &part, &rP, &rA, &cS, &cX, &blk, &bs, &btot, &cxend,
+                &SAg, &WAg, &Ptot, &Aend, &DP, &DA, &tobj, &tent, &tcc, &objout, &fxs, &fys, &fsc, &gsc, &Gs};
+    for (Buf* x : b) all.push_back(x);
+  }
+};
+
+static gw_status prof_event(gw_ctx* c, cudaEvent_t* e) {
+  Prof& P = c->prof;
+  if (P.used == P.pool.size()) {
+    cudaEvent_t x;
+    CU(cudaEventCreate(&x));
+    P.pool.push_back(x);
+  }
+  *e = P.pool[P.used++];
+  return GW_OK;
+}
+// Open / close a timed region of kernel class `cls` (no-ops when profiling is off).
+#define PROF_BEGIN(c, cls)                                           \
+  cudaEvent_t pb_##cls = nullptr;                                    \
+  if ((c)->prof.on) {                                                \
+    TRY(prof_event(c, &pb_##cls));                                   \
+    CU(cudaEventRecord(pb_##cls, (c)->stream));                      \
+  }
+#define PROF_END(c, cls, nlaunch)                                    \
+  if ((c)->prof.on) {                                                \
+    cudaEvent_t pe_;                                                 \
+    TRY(prof_event(c, &pe_));                                        \
+    CU(cudaEventRecord(pe_, (c)->stream));                           \
+    (c)->prof.ev.push_back({cls, {pb_##cls, pe_}});                  \
+    (c)->prof.cnt[cls] += (nlaunch);                                 \
+  }
+
+template <typename T>
+static gw_status ws(gw_ctx* c, Buf& b, size_t count, T** out) {
+  size_t bytes = count * sizeof(T);
+  if (bytes == 0) bytes = 16;
+  if (b.cap < bytes) {
+    if (b.p) {
+      CU(cudaStreamSynchronize(c->stream));
+      CU(cudaFree(b.p));
+      b.p = nullptr;
+      b.cap = 0;
+    }
+    size_t alloc = bytes + (bytes >> 4);  // slack to avoid regrowth churn
+    CU(cudaMalloc(&b.p, alloc));
+    b.cap = alloc;
+  }
+  *out = reinterpret_cast<T*>(b.p);
+  return GW_OK;
+}
+
+static int grid_for(int64_t n, int tpb = 256, int cap = 148 * 16) {
+  int64_t g = (n + tpb - 1) / tpb;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+extern "C" const char* gw_last_error(void) { return g_err.c_str(); }
+extern "C" int gw_abi_version(void) { return GWDP_ABI_VERSION; }
+
+extern "C" gw_status gw_ctx_create(gw_ctx** out, int device, void* cuda_stream, gw_comm* comm) {
+  if (!out) return fail(GW_ERR_INVALID_ARG, "gw_ctx_create: out is null");
+  int ndev = 0;
+  CU(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(GW_ERR_INVALID_ARG, "gw_ctx_create: bad device %d", device);
+  CU(cudaSetDevice(device));
+  gw_ctx* c = new gw_ctx();
+  c->device = device;
+  c->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+  c->comm = comm;
+  if (cudaMallocHost(&c->hpin, 64 * sizeof(double)) != cudaSuccess) {
+    delete c;
+    return fail(GW_ERR_OOM, "gw_ctx_create: pinned alloc failed");
+  }
+  *out = c;
+  return GW_OK;
+}
+
+extern "C" gw_status gw_ctx_trim(gw_ctx* c) {
+  if (!c) return fail(GW_ERR_INVALID_ARG, "null ctx");
+  CU(cudaSetDevice(c->device));
+  CU(cudaStreamSynchronize(c->stream));
+  for (Buf* b : c->all)
+    if (b->p) {
+      CU(cudaFree(b->p));
+      b->p = nullptr;
+      b->cap = 0;
+    }
+  return GW_OK;
+}
+
+// Profiling: enable != 0 turns event timing on (and resets the totals when enable == 2);
+// out_ms / out_counts (host, nullable, `nslots` entries) receive the accumulated milliseconds
+// and launch counts per kernel class {grad_moments, grad_carry, grad_main, sink_row,
+// sink_col, other}.  Synchronises the stream when reading.
+extern "C" gw_status gw_ctx_profile(gw_ctx* c, int enable, double* out_ms, int64_t* out_counts, int nslots) {
+  if (!c) return fail(GW_ERR_INVALID_ARG, "null ctx");
+  CU(cudaSetDevice(c->device));
+  Prof& P = c->prof;
+  if (out_ms || out_counts || enable == 2 || enable == 0) {
+    CU(cudaStreamSynchronize(c->stream));
+    for (auto& e : P.ev) {
+      float ms = 0.f;
+      CU(cudaEventElapsedTime(&ms, e.second.first, e.second.second));
+      P.ms[e.first] += ms;
+    }
+    P.ev.clear();
+    P.used = 0;
+  }
+  for (int k = 0; k < nslots && k < PC_N; ++k) {
+    if (out_ms) out_ms[k] = P.ms[k];
+    if (out_counts) out_counts[k] = P.cnt[k];
+  }
+  if (nslots > PC_N && out_counts) out_counts[PC_N] = c->launches;  // all kernel launches
+  if (enable == 2) {
+    for (int k = 0; k < PC_N; ++k) { P.ms[k] = 0; P.cnt[k] = 0; }
+    c->launches = 0;
+  }
+  P.on = enable != 0;
+  return GW_OK;
+}
+
+extern "C" gw_status gw_ctx_destroy(gw_ctx* c) {
+  if (!c) return GW_OK;
+  gw_status st = gw_ctx_trim(c);
+  for (auto e : c->prof.pool) cudaEventDestroy(e);
+  if (c->hpin) cudaFreeHost(c->hpin);
+  delete c;
+  return st;
+}
+
+// ------------------------------------------------------------------------------ NCCL
+extern "C" gw_status gw_get_unique_id(unsigned char id[128]) {
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId u;
+  ncclResult_t r = ncclGetUniqueId(&u);
+  if (r != ncclSuccess) return fail(GW_ERR_NCCL, "ncclGetUniqueId: %s", ncclGetErrorString(r));
+  memcpy(id, &u, 128);
+  return GW_OK;
+}
+
+extern "C" gw_status gw_comm_init(gw_comm** out, const unsigned char id[128], int nranks, int rank) {
+  if (!out || nranks < 1 || rank < 0 || rank >= nranks) return fail(GW_ERR_INVALID_ARG, "gw_comm_init: bad args");
+  gw_comm* c = new gw_comm();
+  c->nranks = nranks;
+  c->rank = rank;
+  ncclUniqueId u;
+  memcpy(&u, id, 128);
+  ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, u, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return fail(GW_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+  }
+  *out = c;
+  return GW_OK;
+}
+
+extern "C" gw_status gw_comm_destroy(gw_comm* c) {
+  if (!c) return GW_OK;
+  if (c->nccl) ncclCommDestroy(c->nccl);
+  delete c;
+  return GW_OK;
+}
+
+// ------------------------------------------------------------------------------ set-up
+struct Prepared {
+  int64_t n, m, row0, nl;
+  const double *x, *y, *p, *q;  // device views of the caller's vectors (staged if host)
+  double *xc, *yc, *pn, *qn, *lp, *lq, *cx, *cy;
+  double xlast, ylast;
+};
+
+static gw_status check_problem(const gw_problem* pb) {
+  if (!pb) return fail(GW_ERR_INVALID_ARG, "problem is null");
+  if (pb->n < 1 || pb->m < 1) return fail(GW_ERR_INVALID_ARG, "n, m must be >= 1 (got %lld, %lld)",
+                                          (long long)pb->n, (long long)pb->m);
+  if (pb->row0 < 0 || pb->n_local < 0 || pb->row0 + pb->n_local > pb->n)
+    return fail(GW_ERR_DIM_MISMATCH, "row shard [%lld, %lld) outside [0, %lld)", (long long)pb->row0,
+                (long long)(pb->row0 + pb->n_local), (long long)pb->n);
+  if (!pb->x || !pb->y || !pb->p || !pb->q) return fail(GW_ERR_INVALID_ARG, "x, y, p, q must be non-null");
+  if (pb->k != 1) return fail(GW_ERR_UNSUPPORTED, "distance power k=%d: only k = 1 is implemented", pb->k);
+  if (pb->loss != GW_LOSS_SQUARE) return fail(GW_ERR_UNSUPPORTED, "only the square loss is defined (PAPER.md:86)");
+  if (pb->dtype != GW_F32) return fail(GW_ERR_UNSUPPORTED, "only fp32 matrix storage in ABI v1");
+  return GW_OK;
+}
+
+static gw_status check_matrix(const void* M, int64_t ld, int64_t m, const char* name) {
+  if (!M) return fail(GW_ERR_INVALID_ARG, "%s is null", name);
+  if (ld < m || (ld & 3)) return fail(GW_ERR_INVALID_ARG, "%s: ld=%lld must be >= m=%lld and a multiple of 4", name,
+                                      (long long)ld, (long long)m);
+  if (reinterpret_cast<uintptr_t>(M) & 15) return fail(GW_ERR_INVALID_ARG, "%s: base must be 16-byte aligned", name);
+  return GW_OK;
+}
+
+// Validate (reading R16) and build the centred supports, normalised
+// marginals, their logs and the constant-term vectors c, c'.
+static gw_status prepare(gw_ctx* c, const gw_problem* pb, Prepared& P) {
+  TRY(check_problem(pb));
+  const int64_t n = pb->n, m = pb->m;
+  P.n = n; P.m = m; P.row0 = pb->row0; P.nl = pb->n_local;
+  const bool host = pb->flags & GW_HOST_VECTORS;
+  if (host) {
+    double* st;
+    TRY(ws(c, c->stage, (size_t)(2 * n + 2 * m), &st));
+    CU(cudaMemcpyAsync(st, pb->x, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(st + n, pb->p, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(st + 2 * n, pb->y, m * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(st + 2 * n + m, pb->q, m * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    P.x = st; P.p = st + n; P.y = st + 2 * n; P.q = st + 2 * n + m;
+  } else {
+    P.x = pb->x; P.p = pb->p; P.y = pb->y; P.q = pb->q;
+  }
+  double* mom;
+  TRY(ws(c, c->mom, 16, &mom));
+  k_validate<<<2, 1024, 0, c->stream>>>(P.x, P.p, n, P.y, P.q, m, mom);
+  KCHECK();
+  double *xc, *yc, *pn, *qn, *lp, *lq, *cx, *cy;
+  TRY(ws(c, c->xc, n, &xc)); TRY(ws(c, c->yc, m, &yc));
+  TRY(ws(c, c->pn, n, &pn)); TRY(ws(c, c->qn, m, &qn));
+  TRY(ws(c, c->lp, n, &lp)); TRY(ws(c, c->lq, m, &lq));
+  TRY(ws(c, c->cvx, n, &cx)); TRY(ws(c, c->cvy, m, &cy));
+  CU(cudaMemcpyAsync(c->hpin, mom, 16 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  const double* h = c->hpin;
+  if (!(pb->flags & GW_NO_VALIDATE)) {
+    if (h[2] != 0 || h[10] != 0) return fail(GW_ERR_NONFINITE, "non-finite entry in x, y, p or q");
+    if (h[0] != 0 || h[8] != 0) return fail(GW_ERR_UNSORTED, "x and y must be non-decreasing (reading R16)");
+    if (h[1] != 0 || h[9] != 0) return fail(GW_ERR_NEGATIVE_WEIGHT, "p and q must be >= 0");
+    if (fabs(h[3] - 1.0) > 1e-9 || fabs(h[11] - 1.0) > 1e-9)
+      return fail(GW_ERR_NOT_NORMALIZED, "|sum p - 1| = %.3g, |sum q - 1| = %.3g exceed 1e-9 (SPEC.md:72)",
+                  fabs(h[3] - 1.0), fabs(h[11] - 1.0));
+  }
+  k_prep<<<grid_for(n), 256, 0, c->stream>>>(P.x, P.p, n, mom, xc, pn, lp, cx);
+  KCHECK();
+  k_prep<<<grid_for(m), 256, 0, c->stream>>>(P.y, P.q, m, mom + 8, yc, qn, lq, cy);
+  KCHECK();
+  P.xc = xc; P.yc = yc; P.pn = pn; P.qn = qn; P.lp = lp; P.lq = lq; P.cx = cx; P.cy = cy;
+  P.xlast = h[6] * 0.0;  // filled below from host copies of the endpoints
+  // endpoints in centred coordinates: x_{n-1} - xmid = (x_{n-1} - x_0) / 2
+  double ends[4];
+  CU(cudaMemcpyAsync(&ends[0], P.x, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaMemcpyAsync(&ends[1], P.x + n - 1, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaMemcpyAsync(&ends[2], P.y, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaMemcpyAsync(&ends[3], P.y + m - 1, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  P.xlast = ends[1] - h[6];
+  P.ylast = ends[3] - h[14];
+  return GW_OK;
+}
+
+// ------------------------------------------------------------------------------ gradient
+struct GradOut {
+  double E, viol, go, H, cc;  // filled when OBJ
+};
+
+// One DP gradient pass over the (local) plan given by `S` (mode `mode`):
+//   STORE -> G (ldG);  OBJ -> E(T), violation(T), H(T) via k_objective.
+static gw_status grad_pass(gw_ctx* c, const Prepared& P, int mode, const TSrc& S, float* G, int64_t ldG, bool store,
+                           bool obj, const double* fx, const double* fy, double alpha, double* objout_dev) {
+  const int64_t nl = P.nl, m = P.m;
+  if (nl == 0) return GW_OK;
+  const int nb = (int)((nl + TR - 1) / TR), ns = (int)((m + TC - 1) / TC);
+  double *rP, *rA, *cS, *cX, *blk, *bs, *btot, *cxend, *SAg, *WAg, *Ptot, *Aend, *DP, *DA, *tobj, *tent, *tcc;
+  TRY(ws(c, c->rP, (size_t)ns * nl, &rP)); TRY(ws(c, c->rA, (size_t)ns * nl, &rA));
+  TRY(ws(c, c->cS, (size_t)nb * m, &cS)); TRY(ws(c, c->cX, (size_t)nb * m, &cX));
+  TRY(ws(c, c->blk, (size_t)nb * ns * 4, &blk)); TRY(ws(c, c->bs, (size_t)nb * ns * 4, &bs));
+  TRY(ws(c, c->btot, m, &btot)); TRY(ws(c, c->cxend, m, &cxend));
+  TRY(ws(c, c->SAg, m, &SAg)); TRY(ws(c, c->WAg, m, &WAg));
+  TRY(ws(c, c->Ptot, nl, &Ptot)); TRY(ws(c, c->Aend, nl, &Aend));
+  TRY(ws(c, c->DP, nl, &DP)); TRY(ws(c, c->DA, nl, &DA));
+  TRY(ws(c, c->tobj, (size_t)nb * ns, &tobj)); TRY(ws(c, c->tent, (size_t)nb * ns, &tent));
+  TRY(ws(c, c->tcc, (size_t)nb * ns, &tcc));
+  const double* xl = P.xc + P.row0;
+  dim3 grid(ns, nb);
+  PROF_BEGIN(c, PC_GRAD_MOMENTS);
+  switch (mode) {
+    case T_EXPLICIT: k_grad_moments<T_EXPLICIT><<<grid, NT, 0, c->stream>>>(S, nl, m, xl, P.yc, rP, rA, cS, cX); break;
+    case T_GIBBS: k_grad_moments<T_GIBBS><<<grid, NT, 0, c->stream>>>(S, nl, m, xl, P.yc, rP, rA, cS, cX); break;
+    default: k_grad_moments<T_PRODUCT><<<grid, NT, 0, c->stream>>>(S, nl, m, xl, P.yc, rP, rA, cS, cX); break;
+  }
+  KCHECK();
+  PROF_END(c, PC_GRAD_MOMENTS, 1);
+  PROF_BEGIN(c, PC_GRAD_CARRY);
+  k_colcarry<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(nl, m, nb, xl, cS, cX, btot, cxend);
+  KCHECK();
+  k_rowcarry<<<nb, TR, 0, c->stream>>>(nl, m, ns, xl, P.yc, rP, rA, blk, Ptot, Aend);
+  KCHECK();
+  k_blkscan<<<(ns + 127) / 128, 128, 0, c->stream>>>(nl, nb, ns, xl, blk, bs);
+  KCHECK();
+  Scan1DBatch B;
+  memset(&B, 0, sizeof(B));
+  B.d[0] = Scan1D{btot, P.yc, m, SAg, nullptr, nullptr};
+  B.d[1] = Scan1D{cxend, P.yc, m, WAg, nullptr, nullptr};
+  B.d[2] = Scan1D{Ptot, xl, nl, nullptr, DP, nullptr};
+  B.d[3] = Scan1D{Aend, xl, nl, nullptr, DA, nullptr};
+  k_scan1d<<<4, 1024, 0, c->stream>>>(B);
+  KCHECK();
+  PROF_END(c, PC_GRAD_CARRY, 4);
+  MainArgs a;
+  a.S = S; a.nl = nl; a.m = m; a.nb = nb; a.ns = ns;
+  a.xl = xl; a.yc = P.yc; a.cl = P.cx + P.row0; a.c2 = P.cy; a.DP = DP; a.DA = DA; a.SAg = SAg; a.WAg = WAg;
+  a.rP = rP; a.rA = rA; a.cS = cS; a.cX = cX; a.bs = bs; a.xlast = P.xlast; a.ylast = P.ylast;
+  a.G = G; a.ldG = ldG; a.tile_obj = tobj; a.tile_ent = tent; a.tile_cc = tcc;
+  a.fx = fx ? fx + P.row0 : nullptr; a.fy = fy; a.alpha = alpha;
+  PROF_BEGIN(c, PC_GRAD_MAIN);
+#define LAUNCH_MAIN(MODE, ST, OB)                                                                  \
+  do {                                                                                             \
+    const size_t dsm = main_dyn_smem<OB>();                                                        \
+    CU(cudaFuncSetAttribute(k_grad_main<MODE, ST, OB>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                            (int)dsm));                                                            \
+    k_grad_main<MODE, ST, OB><<<grid, NT, dsm, c->stream>>>(a);                                    \
+  } while (0)
+  if (mode == T_EXPLICIT) {
+    if (store && obj) LAUNCH_MAIN(T_EXPLICIT, true, true);
+    else if (store) LAUNCH_MAIN(T_EXPLICIT, true, false);
+    else LAUNCH_MAIN(T_EXPLICIT, false, true);
+  } else if (mode == T_GIBBS) {
+    if (store && obj) LAUNCH_MAIN(T_GIBBS, true, true);
+    else if (store) LAUNCH_MAIN(T_GIBBS, true, false);
+    else LAUNCH_MAIN(T_GIBBS, false, true);
+  } else {
+    if (store && obj) LAUNCH_MAIN(T_PRODUCT, true, true);
+    else if (store) LAUNCH_MAIN(T_PRODUCT, true, false);
+    else LAUNCH_MAIN(T_PRODUCT, false, true);
+  }
+#undef LAUNCH_MAIN
+  KCHECK();
+  PROF_END(c, PC_GRAD_MAIN, 1);
+  if (obj) {
+    k_objective<<<1, 1024, 0, c->stream>>>(Ptot, xl, P.pn + P.row0, P.cx + P.row0, nl, btot, P.yc, P.qn, P.cy, m,
+                                           tobj, (int64_t)nb * ns, tent, objout_dev);
+    KCHECK();
+    if (fx) {
+      // <C o C, T> for FGW: reuse k_objective's tile sum slot via a second call on tcc
+      k_objective<<<1, 1024, 0, c->stream>>>(Ptot, xl, P.pn + P.row0, P.cx + P.row0, nl, btot, P.yc, P.qn, P.cy,
+                                             m, tcc, (int64_t)nb * ns, nullptr, objout_dev + 4);
+      KCHECK();
+    }
+  }
+  return GW_OK;
+}
+
+extern "C" gw_status gw_grad_dp(gw_ctx* c, const gw_problem* pb, const void* T, int64_t ldT, void* G, int64_t ldG,
+                                const gw_moments* mom) {
+  if (!c) return fail(GW_ERR_INVALID_ARG, "null ctx");
+  if (mom) return fail(GW_ERR_UNSUPPORTED, "gw_grad_dp: precomputed moments are not accepted in ABI v1");
+  TRY(check_problem(pb));
+  TRY(check_matrix(T, ldT, pb->m, "T"));
+  TRY(check_matrix(G, ldG, pb->m, "G"));
+  if (c->comm && c->comm->nranks > 1)
+    return fail(GW_ERR_UNSUPPORTED, "gw_grad_dp: multi-rank gradient goes through entropic_gw_solve");
+  CU(cudaSetDevice(c->device));
+  Prepared P;
+  TRY(prepare(c, pb, P));
+  TSrc S{reinterpret_cast<const float*>(T), ldT, nullptr, nullptr, 0.0};
+  TRY(grad_pass(c, P, T_EXPLICIT, S, reinterpret_cast<float*>(G), ldG, true, false, nullptr, nullptr, 1.0, nullptr));
+  return GW_OK;
+}
+
+// ------------------------------------------------------------------------------ Sinkhorn
+struct SinkState {
+  double *f, *g;     // fp64 duals (device)
+  float *fh, *fl, *gh, *gl;
+  double* ftmp;
+  float* viol;
+  int *stop, *iters;
+  float2* part;
+  int nrb;
+  int64_t RB;
+};
+
+static gw_status sink_alloc(gw_ctx* c, const Prepared& P, SinkState& s) {
+  TRY(ws(c, c->fh, P.nl, &s.fh)); TRY(ws(c, c->fl, P.nl, &s.fl));
+  TRY(ws(c, c->gh, P.m, &s.gh)); TRY(ws(c, c->gl, P.m, &s.gl));
+  TRY(ws(c, c->ftmp, P.nl, &s.ftmp));
+  TRY(ws(c, c->viol, 4, &s.viol));
+  TRY(ws(c, c->stop, 4, &s.stop));
+  TRY(ws(c, c->iters, 4, &s.iters));
+  // row blocks of the column half-step: enough CTAs to fill the machine (>= 4 waves)
+  const int64_t colblocks = (P.m + 1023) / 1024;
+  int64_t want = (148 * 8 + colblocks - 1) / colblocks;
+  int64_t RB = (P.nl + want - 1) / std::max<int64_t>(want, 1);
+  RB = std::max<int64_t>(16, (RB + 3) & ~int64_t(3));
+  s.RB = RB;
+  s.nrb = (int)std::max<int64_t>(1, (P.nl + RB - 1) / RB);
+  TRY(ws(c, c->part, (size_t)s.nrb * P.m, &s.part));
+  return GW_OK;
+}
+
+static gw_status sink_split(gw_ctx* c, const Prepared& P, SinkState& s, double eps) {
+  k_split<<<grid_for(P.nl), 256, 0, c->stream>>>(s.f, P.nl, GW_LOG2E / eps, s.fh, s.fl);
+  KCHECK();
+  k_split<<<grid_for(P.m), 256, 0, c->stream>>>(s.g, P.m, GW_LOG2E / eps, s.gh, s.gl);
+  KCHECK();
+  return GW_OK;
+}
+
+// `iters` Sinkhorn iterations on G.  tol > 0: check every `check_every` iterations (one
+// host sync per check); returns the iterations used and whether tol was met.
+static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const float* G, int64_t ldG, double eps,
+                          int iters, double tol, int check_every, int* used, int* converged) {
+  const int64_t nl = P.nl, m = P.m;
+  const float c2f = (float)(GW_LOG2E / eps);
+  const bool small_rows = m <= 2048;
+  const int rows_grid = grid_for(small_rows ? (nl + 7) / 8 : nl, 1, 148 * 8);
+  dim3 cgrid((unsigned)((m + 1023) / 1024), (unsigned)s.nrb);
+  CU(cudaMemsetAsync(s.stop, 0, sizeof(int), c->stream));
+  *used = 0;
+  *converged = 0;
+  if (check_every < 1) check_every = 10;
+  int done = 0;
+  const bool tolmode = tol > 0;
+  while (done < iters) {
+    const int chunk = tolmode ? std::min(check_every, iters - done) : iters - done;
+    for (int k = 0; k < chunk; ++k) {
+      const bool check = tolmode && k == 0 && done > 0;  // violation of the plan after `done` iterations
+      if (check) CU(cudaMemsetAsync(s.viol, 0, sizeof(float), c->stream));
+      double* fout = check ? s.ftmp : s.f;
+      PROF_BEGIN(c, PC_SINK_ROW);
+      if (small_rows)
+        k_sink_row<32><<<rows_grid, 256, 0, c->stream>>>(G, ldG, nl, m, s.gh, s.gl, c2f, s.f, fout, P.lp + P.row0, eps,
+                                                         s.fh, s.fl, check ? s.viol : nullptr, s.stop);
+      else
+        k_sink_row<256><<<rows_grid, 256, 0, c->stream>>>(G, ldG, nl, m, s.gh, s.gl, c2f, s.f, fout, P.lp + P.row0,
+                                                          eps, s.fh, s.fl, check ? s.viol : nullptr, s.stop);
+      KCHECK();
+      PROF_END(c, PC_SINK_ROW, 1);
+      if (check) {
+        k_sink_commit<<<grid_for(nl), 256, 0, c->stream>>>(s.viol, tol, s.stop, s.ftmp, s.f, nl, s.iters, done);
+        KCHECK();
+      }
+      PROF_BEGIN(c, PC_SINK_COL);
+      k_sink_col<<<cgrid, 256, 0, c->stream>>>(G, ldG, nl, m, s.fh, s.fl, c2f, s.RB, s.part, s.stop);
+      KCHECK();
+      k_sink_colfin<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.part, s.nrb, m, P.lq, eps, s.g, s.gh, s.gl,
+                                                                       s.stop);
+      KCHECK();
+      PROF_END(c, PC_SINK_COL, 2);
+    }
+    if (tolmode) {
+      int hs[2];
+      CU(cudaMemcpyAsync(hs, s.stop, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      CU(cudaMemcpyAsync(hs + 1, s.iters, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      CU(cudaStreamSynchronize(c->stream));
+      if (hs[0]) {
+        *used = hs[1];
+        *converged = 1;
+        return GW_OK;
+      }
+    }
+    done += chunk;
+  }
+  *used = done;
+  if (tolmode) {
+    // final check of the plan after `done` iterations (row half-step into ftmp, not committed)
+    CU(cudaMemsetAsync(s.viol, 0, sizeof(float), c->stream));
+    if (small_rows)
+      k_sink_row<32><<<rows_grid, 256, 0, c->stream>>>(G, ldG, nl, m, s.gh, s.gl, c2f, s.f, s.ftmp, P.lp + P.row0, eps,
+                                                       s.fh, s.fl, s.viol, nullptr);
+    else
+      k_sink_row<256><<<rows_grid, 256, 0, c->stream>>>(G, ldG, nl, m, s.gh, s.gl, c2f, s.f, s.ftmp, P.lp + P.row0,
+                                                        eps, s.fh, s.fl, s.viol, nullptr);
+    KCHECK();
+    float hv;
+    CU(cudaMemcpyAsync(&hv, s.viol, sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    *converged = (double)hv <= tol;
+    // restore fh/fl for the committed f
+    k_split<<<grid_for(nl), 256, 0, c->stream>>>(s.f, nl, GW_LOG2E / eps, s.fh, s.fl);
+    KCHECK();
+  }
+  return GW_OK;
+}
+
+static gw_status stage_duals_in(gw_ctx* c, const gw_problem* pb, const Prepared& P, double* f, double* g,
+                                double** fd, double** gd) {
+  if (pb->flags & GW_HOST_VECTORS) {
+    TRY(ws(c, c->fs, P.nl, fd));
+    TRY(ws(c, c->gs, P.m, gd));
+    if (f) CU(cudaMemcpyAsync(*fd, f, P.nl * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    if (g) CU(cudaMemcpyAsync(*gd, g, P.m * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  } else {
+    *fd = f;
+    *gd = g;
+  }
+  return GW_OK;
+}
+
+static gw_status stage_duals_out(gw_ctx* c, const gw_problem* pb, const Prepared& P, double* f, double* g,
+                                 const double* fd, const double* gd) {
+  if (pb->flags & GW_HOST_VECTORS) {
+    if (f) CU(cudaMemcpyAsync(f, fd, P.nl * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (g) CU(cudaMemcpyAsync(g, gd, P.m * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+  }
+  return GW_OK;
+}
+
+static gw_status materialize(gw_ctx* c, const Prepared& P, int mode, const TSrc& S, void* T, int64_t ldT) {
+  const int g = grid_for(P.nl * P.m, 256, 148 * 32);
+  if (mode == T_PRODUCT) k_materialize<T_PRODUCT><<<g, 256, 0, c->stream>>>(S, P.nl, P.m, (float*)T, ldT);
+  else k_materialize<T_GIBBS><<<g, 256, 0, c->stream>>>(S, P.nl, P.m, (float*)T, ldT);
+  KCHECK();
+  return GW_OK;
+}
+
+extern "C" gw_status sinkhorn_solve(gw_ctx* c, const gw_problem* pb, const void* G, int64_t ldG,
+                                    const gw_sinkhorn_opts* o, double* f, double* g, void* T_out, int64_t ldT,
+                                    gw_sinkhorn_info* info) {
+  if (!c || !o) return fail(GW_ERR_INVALID_ARG, "null ctx or opts");
+  if (!(o->eps > 0) || o->max_iter < 0) return fail(GW_ERR_CONFIG, "eps must be > 0 and max_iter >= 0");
+  if (!f || !g) return fail(GW_ERR_INVALID_ARG, "f and g (warm start, in/out) must be non-null");
+  TRY(check_problem(pb));
+  TRY(check_matrix(G, ldG, pb->m, "G"));
+  if (T_out) TRY(check_matrix(T_out, ldT, pb->m, "T_out"));
+  if (c->comm && c->comm->nranks > 1)
+    return fail(GW_ERR_UNSUPPORTED, "sinkhorn_solve: multi-rank Sinkhorn goes through entropic_gw_solve");
+  CU(cudaSetDevice(c->device));
+  Prepared P;
+  TRY(prepare(c, pb, P));
+  SinkState s;
+  TRY(sink_alloc(c, P, s));
+  TRY(stage_duals_in(c, pb, P, f, g, &s.f, &s.g));
+  TRY(sink_split(c, P, s, o->eps));
+  int used = 0, conv = 0;
+  TRY(sink_run(c, P, s, reinterpret_cast<const float*>(G), ldG, o->eps, o->max_iter, o->tol, o->check_every, &used,
+               &conv));
+  if (T_out) {
+    double *fs, *gs;
+    TRY(ws(c, c->Ptot, P.nl, &fs));  // scratch
+    TRY(ws(c, c->btot, P.m, &gs));
+    k_scale<<<grid_for(P.nl), 256, 0, c->stream>>>(s.f, P.nl, GW_LOG2E / o->eps, fs);
+    k_scale<<<grid_for(P.m), 256, 0, c->stream>>>(s.g, P.m, GW_LOG2E / o->eps, gs);
+    KCHECK();
+    TSrc S{reinterpret_cast<const float*>(G), ldG, fs, gs, GW_LOG2E / o->eps};
+    TRY(materialize(c, P, T_GIBBS, S, T_out, ldT));
+  }
+  if (info) {
+    // violation of the returned plan: a measuring row half-step (not committed)
+    CU(cudaMemsetAsync(s.viol, 0, sizeof(float), c->stream));
+    const float c2f = (float)(GW_LOG2E / o->eps);
+    const int rows_grid = grid_for(P.m <= 2048 ? (P.nl + 7) / 8 : P.nl, 1, 148 * 8);
+    if (P.m <= 2048)
+      k_sink_row<32><<<rows_grid, 256, 0, c->stream>>>(reinterpret_cast<const float*>(G), ldG, P.nl, P.m, s.gh, s.gl,
+                                                       c2f, s.f, s.ftmp, P.lp + P.row0, o->eps, s.fh, s.fl, s.viol,
+                                                       nullptr);
+    else
+      k_sink_row<256><<<rows_grid, 256, 0, c->stream>>>(reinterpret_cast<const float*>(G), ldG, P.nl, P.m, s.gh,
+                                                        s.gl, c2f, s.f, s.ftmp, P.lp + P.row0, o->eps, s.fh, s.fl,
+                                                        s.viol, nullptr);
+    KCHECK();
+    float hv;
+    CU(cudaMemcpyAsync(&hv, s.viol, sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    info->iters = used;
+    info->converged = o->tol > 0 ? ((double)hv <= o->tol) : 0;
+    info->marginal_violation = hv;
+  }
+  TRY(stage_duals_out(c, pb, P, f, g, s.f, s.g));
+  return GW_OK;
+}
+
+// ------------------------------------------------------------------------------ solver
+static gw_status solve_impl(gw_ctx* c, const gw_problem* pb, const gw_solve_opts* o, const double* fx_in,
+                            const double* fy_in, double alpha, const void* T0, void* T_out, int64_t ldT, double* f,
+                            double* g, gw_result* res, double* trace) {
+  if (!c || !o || !res) return fail(GW_ERR_INVALID_ARG, "null ctx, opts or result");
+  if (!(o->eps > 0)) return fail(GW_ERR_CONFIG, "eps must be > 0");
+  if (o->tau != o->eps && o->tau != 0)
+    return fail(GW_ERR_UNSUPPORTED, "tau != eps is not implemented (Remark 1, reading R6)");
+  if (o->outer_iters < 0 || o->inner.max_iter < 0) return fail(GW_ERR_CONFIG, "iteration counts must be >= 0");
+  if (!f || !g) return fail(GW_ERR_INVALID_ARG, "f and g (outputs) must be non-null");
+  TRY(check_problem(pb));
+  if (T0) TRY(check_matrix(T0, ldT, pb->m, "T0"));
+  if (T_out) TRY(check_matrix(T_out, ldT, pb->m, "T_out"));
+  if (c->comm && c->comm->nranks > 1)
+    return fail(GW_ERR_UNSUPPORTED, "multi-rank solve: not in this build");
+  CU(cudaSetDevice(c->device));
+  const double eps = o->eps;
+  Prepared P;
+  TRY(prepare(c, pb, P));
+  const int64_t nl = P.nl, m = P.m;
+  const double* fx = nullptr;
+  const double* fy = nullptr;
+  if (fx_in) {
+    if (pb->flags & GW_HOST_VECTORS) {
+      double *a, *b;
+      TRY(ws(c, c->fxs, P.n, &a));
+      TRY(ws(c, c->fys, m, &b));
+      CU(cudaMemcpyAsync(a, fx_in, P.n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+      CU(cudaMemcpyAsync(b, fy_in, m * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+      fx = a; fy = b;
+    } else {
+      fx = fx_in; fy = fy_in;
+    }
+  }
+  // cost buffer
+  const int64_t ldG = (m + 31) & ~int64_t(31);
+  float* G;
+  TRY(ws(c, c->Gs, (size_t)std::max<int64_t>(nl, 1) * ldG, &G));
+  SinkState s;
+  TRY(sink_alloc(c, P, s));
+  if (pb->flags & GW_HOST_VECTORS) {
+    TRY(stage_duals_in(c, pb, P, nullptr, nullptr, &s.f, &s.g));  // device scratch for host duals
+  } else {
+    s.f = f;  // the caller's device output buffers hold the duals throughout
+    s.g = g;
+  }
+  // f = g = 0 before the first sweep (reading R7)
+  k_fill<<<grid_for(nl), 256, 0, c->stream>>>(s.f, nl, 0.0);
+  k_fill<<<grid_for(m), 256, 0, c->stream>>>(s.g, m, 0.0);
+  KCHECK();
+  // scaled duals f log2e/eps, g log2e/eps for the Gibbs regeneration of T in the gradient
+  double *Fs, *Gs2, *objout;
+  TRY(ws(c, c->fsc, (size_t)std::max<int64_t>(nl, 1), &Fs));
+  TRY(ws(c, c->gsc, (size_t)m, &Gs2));
+  TRY(ws(c, c->objout, 16, &objout));
+
+  cudaEvent_t ev0, ev1;
+  CU(cudaEventCreate(&ev0)); CU(cudaEventCreate(&ev1));
+  CU(cudaEventRecord(ev0, c->stream));
+  std::vector<cudaEvent_t> evs(2 * (size_t)o->outer_iters + 2);
+  for (auto& e : evs) CU(cudaEventCreate(&e));
+
+  int inner_total = 0, conv_all = 1;
+  float ms_grad = 0.f, ms_sink = 0.f;
+  std::vector<double> tr((size_t)std::max(o->outer_iters, 1) * 4, NAN);
+  const bool want_trace_obj = (o->flags & GW_SOLVE_TRACE_OBJECTIVE) != 0;
+  for (int l = 0; l < o->outer_iters; ++l) {
+    // ---- gradient of T^{l} (l = 0: T0 or p q^T) ----
+    int mode;
+    TSrc S;
+    if (l == 0) {
+      if (T0) { mode = T_EXPLICIT; S = TSrc{reinterpret_cast<const float*>(T0), ldT, nullptr, nullptr, 0.0}; }
+      else { mode = T_PRODUCT; S = TSrc{nullptr, 0, P.pn + P.row0, P.qn, 0.0}; }
+    } else {
+      mode = T_GIBBS;
+      k_scale<<<grid_for(nl), 256, 0, c->stream>>>(s.f, nl, GW_LOG2E / eps, Fs);
+      k_scale<<<grid_for(m), 256, 0, c->stream>>>(s.g, m, GW_LOG2E / eps, Gs2);
+      KCHECK();
+      S = TSrc{G, ldG, Fs, Gs2, GW_LOG2E / eps};
+    }
+    const bool obj = (l > 0) && want_trace_obj;
+    CU(cudaEventRecord(evs[2 * l], c->stream));
+    TRY(grad_pass(c, P, mode, S, G, ldG, true, obj, fx, fy, alpha, objout));
+    CU(cudaEventRecord(evs[2 * l + 1], c->stream));
+    if (obj) {
+      CU(cudaMemcpyAsync(c->hpin, objout, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CU(cudaStreamSynchronize(c->stream));
+      const double E = c->hpin[0];
+      tr[(size_t)(l - 1) * 4 + 0] = fx ? (1.0 - alpha) * c->hpin[6] + alpha * E : E;
+      tr[(size_t)(l - 1) * 4 + 1] = c->hpin[1];
+    }
+    // ---- Sinkhorn on G^{l+1} with warm-started duals ----
+    TRY(sink_split(c, P, s, eps));
+    int used = 0, conv = 0;
+    TRY(sink_run(c, P, s, G, ldG, eps, o->inner.max_iter, o->inner.tol, o->inner.check_every, &used, &conv));
+    inner_total += used;
+    if (o->inner.tol > 0 && !conv) conv_all = 0;
+    tr[(size_t)l * 4 + 2] = used;
+  }
+  CU(cudaEventRecord(evs[2 * (size_t)o->outer_iters], c->stream));
+  // ---- final plan T^L: objective, violation, entropy (one read-only gradient pass) ----
+  double E = 0.0, viol = 0.0, H = 0.0, ecc = 0.0;
+  if (nl > 0) {
+    int mode;
+    TSrc S;
+    if (o->outer_iters == 0) {
+      if (T0) { mode = T_EXPLICIT; S = TSrc{reinterpret_cast<const float*>(T0), ldT, nullptr, nullptr, 0.0}; }
+      else { mode = T_PRODUCT; S = TSrc{nullptr, 0, P.pn + P.row0, P.qn, 0.0}; }
+    } else {
+      mode = T_GIBBS;
+      k_scale<<<grid_for(nl), 256, 0, c->stream>>>(s.f, nl, GW_LOG2E / eps, Fs);
+      k_scale<<<grid_for(m), 256, 0, c->stream>>>(s.g, m, GW_LOG2E / eps, Gs2);
+      KCHECK();
+      S = TSrc{G, ldG, Fs, Gs2, GW_LOG2E / eps};
+    }
+    TRY(grad_pass(c, P, mode, S, nullptr, 0, false, true, fx, fy, alpha, objout));
+    if (T_out) TRY(materialize(c, P, mode == T_EXPLICIT ? T_GIBBS : mode, S, T_out, ldT));
+    if (T_out && mode == T_EXPLICIT) CU(cudaMemcpy2DAsync(T_out, ldT * 4, T0, ldT * 4, m * 4, nl,
+                                                          cudaMemcpyDeviceToDevice, c->stream));
+    CU(cudaMemcpyAsync(c->hpin, objout, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  }
+  CU(cudaEventRecord(ev1, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  if (nl > 0) {
+    E = c->hpin[0]; viol = c->hpin[1]; H = c->hpin[3]; ecc = c->hpin[6];
+  }
+  const double Eout = fx ? (1.0 - alpha) * ecc + alpha * E : E;
+  if (o->outer_iters > 0) {
+    tr[(size_t)(o->outer_iters - 1) * 4 + 0] = Eout;
+    tr[(size_t)(o->outer_iters - 1) * 4 + 1] = viol;
+  }
+  for (int l = 0; l < o->outer_iters; ++l) {
+    float a = 0.f, b = 0.f;
+    CU(cudaEventElapsedTime(&a, evs[2 * l], evs[2 * l + 1]));
+    CU(cudaEventElapsedTime(&b, evs[2 * l + 1], evs[2 * l + 2]));
+    ms_grad += a;
+    ms_sink += b;
+    tr[(size_t)l * 4 + 3] = a + b;
+  }
+  float ms_total = 0.f;
+  CU(cudaEventElapsedTime(&ms_total, ev0, ev1));
+  for (auto& e : evs) cudaEventDestroy(e);
+  cudaEventDestroy(ev0); cudaEventDestroy(ev1);
+  res->gw_objective = Eout;
+  res->entropic_objective = Eout + eps * H;
+  res->marginal_violation = viol;
+  res->outer_iters = o->outer_iters;
+  res->inner_iters_total = inner_total;
+  res->converged = (o->inner.tol > 0) ? conv_all : 0;
+  res->ms_grad = ms_grad;
+  res->ms_sinkhorn = ms_sink;
+  res->ms_total = ms_total;
+  if (trace) memcpy(trace, tr.data(), sizeof(double) * 4 * (size_t)o->outer_iters);
+  TRY(stage_duals_out(c, pb, P, f, g, s.f, s.g));
+  return GW_OK;
+}
+
+extern "C" gw_status entropic_gw_solve(gw_ctx* c, const gw_problem* pb, const gw_solve_opts* o, const void* T0,
+                                       void* T_out, int64_t ldT, double* f, double* g, gw_result* res,
+                                       double* trace) {
+  return solve_impl(c, pb, o, nullptr, nullptr, 1.0, T0, T_out, ldT, f, g, res, trace);
+}
+
+extern "C" gw_status fgw_solve(gw_ctx* c, const gw_problem* pb, const double* fx, const double* fy, double alpha,
+                               const gw_solve_opts* o, const void* T0, void* T_out, int64_t ldT, double* f,
+                               double* g, gw_result* res, double* trace) {
+  if (!fx || !fy) return fail(GW_ERR_INVALID_ARG, "fgw_solve: fx and fy must be non-null");
+  if (!(alpha >= 0.0 && alpha <= 1.0)) return fail(GW_ERR_CONFIG, "fgw_solve: alpha must be in [0, 1]");
+  return solve_impl(c, pb, o, fx, fy, alpha, T0, T_out, ldT, f, g, res, trace);
+}
+
+extern "C" gw_status ugw_solve(gw_ctx*, const gw_problem*, double, const gw_solve_opts*, const void*, void*, int64_t,
+                               double*, double*, gw_result*, double*) {
+  return fail(GW_ERR_UNSUPPORTED,
+              "ugw_solve: Remark 3 (PAPER.md:148-167) leaves g(Gamma-hat) undefined; no definition to implement");
+}

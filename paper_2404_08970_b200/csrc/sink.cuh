@@ -1,0 +1,202 @@
+// sink.cuh -- log-domain Sinkhorn for the entropic-OT subproblem (PAPER.md:108-114,
+// Remark 1 PAPER.md:127-133) on a cost G (N x M fp32), never materialising exp(-G/eps).
+//
+// One iteration (reading R7): f-update then g-update,
+//   f_i = eps ln p_i - eps LSE_p((g_p - G_ip)/eps),   g_p = eps ln q_p - eps LSE_i((f_i - G_ip)/eps).
+// Work is in log2 units: a_ip = g_p log2e/eps - G_ip log2e/eps with the dual scaled and split
+// into fp32 hi + lo parts (so the per-column rounding of g is below fp32 ulp), exponent by
+// MUFU ex2, max-shifted (online) log-sum-exp, fp64 duals.
+#pragma once
+#include "common.cuh"
+
+namespace gw {
+
+// ---------------------------------------------------------------------------------
+// Row half-step.  TPR threads per row (32 or 256), rows grid-strided.
+//   fout_i = eps ln p_i - eps ln2 LSE2_p(a_ip)
+// and the violation of the current plan's row (the plan (fcur, g)):
+//   |sum_p T_ip - p_i| = p_i |2^{(fcur_i - fout_i) log2e / eps} - 1|
+// ---------------------------------------------------------------------------------
+template <int TPR>
+__global__ void __launch_bounds__(256) k_sink_row(const float* __restrict__ G, int64_t ld, int64_t nl, int64_t m,
+                                                  const float* __restrict__ gh, const float* __restrict__ gl,
+                                                  float c2f, const double* __restrict__ fcur,
+                                                  double* __restrict__ fout, const double* __restrict__ lp,
+                                                  double eps, float* __restrict__ fh, float* __restrict__ fl,
+                                                  float* __restrict__ viol, const int* __restrict__ stop) {
+  if (stop && *stop) return;
+  constexpr int RPC = 256 / TPR;
+  __shared__ float smm[8], sms[8];
+  const int grp = threadIdx.x / TPR, tid = threadIdx.x % TPR;
+  const double l2e_eps = GW_LOG2E / eps;
+  float vmax = 0.f;
+  for (int64_t row0 = (int64_t)blockIdx.x * RPC; row0 < nl; row0 += (int64_t)gridDim.x * RPC) {
+    const int64_t row = row0 + grp;
+    const bool rv = row < nl;
+    LSE2 st{-INFINITY, 0.f};
+    if (rv) {
+      const float* gr = G + row * ld;
+      for (int64_t q = 8 * (int64_t)tid; q < m; q += 8 * TPR) {
+        float4 x0 = __ldcs(reinterpret_cast<const float4*>(gr + q));
+        float4 x1 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (q + 4 < m) x1 = __ldcs(reinterpret_cast<const float4*>(gr + q + 4));
+        const float gv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+        float av[8];
+        float cm = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          av[k] = (q + k < m) ? fmaf(gv[k], -c2f, gh[q + k]) + gl[q + k] : -INFINITY;
+          cm = fmaxf(cm, av[k]);
+        }
+        if (cm > st.m) {
+          st.s = (st.m == -INFINITY) ? 0.f : st.s * exp2f(st.m - cm);
+          st.m = cm;
+        }
+        if (st.m != -INFINITY) {
+          float acc = 0.f;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc += exp2f(av[k] - st.m);
+          st.s += acc;
+        }
+      }
+    }
+    if (TPR == 32) {
+      st = lse_warp(st);
+    } else {
+      st = lse_warp(st);
+      if ((threadIdx.x & 31) == 0) { smm[threadIdx.x >> 5] = st.m; sms[threadIdx.x >> 5] = st.s; }
+      __syncthreads();
+      st = LSE2{smm[0], sms[0]};
+      for (int k = 1; k < 8; ++k) st = lse_merge(st, LSE2{smm[k], sms[k]});
+      __syncthreads();
+    }
+    if (rv && tid == 0) {
+      const double lse2 = (double)st.m + log2((double)st.s);
+      const double fo = fcur[row];
+      const double fn = (lp[row] == -INFINITY) ? -INFINITY : eps * lp[row] - eps * GW_LN2 * lse2;
+      fout[row] = fn;
+      const double fs = fn * l2e_eps;
+      const float h = (float)fs;
+      fh[row] = h;
+      fl[row] = isfinite(fs) ? (float)(fs - (double)h) : 0.f;
+      if (viol) {
+        const double pi = exp(lp[row]);
+        double v = (pi > 0.0) ? pi * fabs(exp2((fo - fn) * l2e_eps) - 1.0) : 0.0;
+        if (!(v == v)) v = 3.0e38;
+        vmax = fmaxf(vmax, (float)fmin(v, 3.0e38));
+      }
+    }
+  }
+  if (viol) {
+    vmax = warp_max(vmax);
+    if ((threadIdx.x & 31) == 0 && vmax > 0.f) atomic_max_nonneg(viol, vmax);
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// Column half-step, pass 1: per (row block, column) online LSE of b_ip = f_i log2e/eps -
+// G_ip log2e/eps.  Thread = 4 consecutive columns (float4), CTA = 1024 columns, rows
+// [rb*RB, (rb+1)*RB).  Partials (m, s) to part[rb][q].
+// ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_sink_col(const float* __restrict__ G, int64_t ld, int64_t nl, int64_t m,
+                                                  const float* __restrict__ fh, const float* __restrict__ fl,
+                                                  float c2f, int64_t RB, float2* __restrict__ part,
+                                                  const int* __restrict__ stop) {
+  if (stop && *stop) return;
+  const int64_t q0 = ((int64_t)blockIdx.x * 256 + threadIdx.x) * 4;
+  if (q0 >= m) return;
+  const int64_t rb = blockIdx.y;
+  const int64_t rs = rb * RB, re = min(nl, rs + RB);
+  LSE2 st[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) st[k] = LSE2{-INFINITY, 0.f};
+  const float* base = G + q0;
+  int64_t r = rs;
+  for (; r + 4 <= re; r += 4) {
+    float4 x[4];
+    float fr[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      x[u] = __ldcs(reinterpret_cast<const float4*>(base + (r + u) * ld));
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) fr[u] = fh[r + u];
+    float a[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float lo = fl[r + u];
+      a[u][0] = fmaf(x[u].x, -c2f, fr[u]) + lo;
+      a[u][1] = fmaf(x[u].y, -c2f, fr[u]) + lo;
+      a[u][2] = fmaf(x[u].z, -c2f, fr[u]) + lo;
+      a[u][3] = fmaf(x[u].w, -c2f, fr[u]) + lo;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float cm = fmaxf(fmaxf(a[0][k], a[1][k]), fmaxf(a[2][k], a[3][k]));
+      if (cm > st[k].m) {
+        st[k].s = (st[k].m == -INFINITY) ? 0.f : st[k].s * exp2f(st[k].m - cm);
+        st[k].m = cm;
+      }
+      if (st[k].m != -INFINITY)
+        st[k].s += exp2f(a[0][k] - st[k].m) + exp2f(a[1][k] - st[k].m) + exp2f(a[2][k] - st[k].m) +
+                   exp2f(a[3][k] - st[k].m);
+    }
+  }
+  for (; r < re; ++r) {
+    const float4 x = __ldcs(reinterpret_cast<const float4*>(base + r * ld));
+    const float fr = fh[r], lo = fl[r];
+    const float a[4] = {fmaf(x.x, -c2f, fr) + lo, fmaf(x.y, -c2f, fr) + lo, fmaf(x.z, -c2f, fr) + lo,
+                        fmaf(x.w, -c2f, fr) + lo};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) st[k] = lse_merge(st[k], LSE2{a[k], 1.f});
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (q0 + k < m) part[rb * m + q0 + k] = make_float2(st[k].m, st[k].s);
+}
+
+// Column half-step, pass 2: merge the row-block partials in fixed order and update g.
+__global__ void k_sink_colfin(const float2* __restrict__ part, int nrb, int64_t m, const double* __restrict__ lq,
+                              double eps, double* __restrict__ g, float* __restrict__ gh, float* __restrict__ gl,
+                              const int* __restrict__ stop) {
+  if (stop && *stop) return;
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= m) return;
+  LSE2 st{-INFINITY, 0.f};
+  // fp64 merge for accuracy
+  double M = -INFINITY;
+  for (int rb = 0; rb < nrb; ++rb) M = fmax(M, (double)part[(int64_t)rb * m + q].x);
+  double S = 0.0;
+  if (M != -INFINITY)
+    for (int rb = 0; rb < nrb; ++rb) {
+      const float2 v = part[(int64_t)rb * m + q];
+      if (v.x != -INFINITY) S += (double)v.y * exp2((double)v.x - M);
+    }
+  (void)st;
+  const double lse2 = M + log2(S);
+  const double gn = (lq[q] == -INFINITY) ? -INFINITY : eps * lq[q] - eps * GW_LN2 * lse2;
+  g[q] = gn;
+  const double gs = gn * (GW_LOG2E / eps);
+  const float h = (float)gs;
+  gh[q] = h;
+  gl[q] = isfinite(gs) ? (float)(gs - (double)h) : 0.f;
+}
+
+// Tolerance rule (reading R8): the row half-step of iteration k+1 measured the violation of
+// the plan after iteration k into *viol (written to ftmp).  If it is <= tol, stop with f
+// unchanged (iteration k+1 is discarded); otherwise commit ftmp -> f.
+__global__ void k_sink_commit(const float* __restrict__ viol, double tol, int* __restrict__ stop,
+                              const double* __restrict__ ftmp, double* __restrict__ f, int64_t nl,
+                              int* __restrict__ iters, int it_before) {
+  if (*stop) return;
+  const bool done = (double)(*viol) <= tol;
+  __syncthreads();
+  if (done) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) { *stop = 1; *iters = it_before; }
+    return;
+  }
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nl; i += (int64_t)gridDim.x * blockDim.x)
+    f[i] = ftmp[i];
+}
+
+}  // namespace gw

@@ -1,0 +1,192 @@
+// vec.cuh -- O(N + M) kernels: validation, set-up, 1-D dynamic programmes.
+#pragma once
+#include "common.cuh"
+
+namespace gw {
+
+// ---------------------------------------------------------------------------------
+// Validation + moments of one (support, marginal) pair, one CTA of 1024 threads.
+// out[0..7] = {unsorted, negative, nonfinite, S0 = sum w, S1 = sum xc w, S2 = sum xc^2 w,
+//              xmid, unused}, xc = x - xmid, xmid = (x_0 + x_{n-1}) / 2.
+// Fixed-order reduction => deterministic (SPEC.md:68-76 validate_measure).
+// ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_validate(const double* __restrict__ x0, const double* __restrict__ w0,
+                                                   int64_t n0, const double* __restrict__ x1,
+                                                   const double* __restrict__ w1, int64_t n1,
+                                                   double* __restrict__ out) {
+  __shared__ double sm[32];
+  const double* x = blockIdx.x == 0 ? x0 : x1;
+  const double* w = blockIdx.x == 0 ? w0 : w1;
+  const int64_t n = blockIdx.x == 0 ? n0 : n1;
+  double* o = out + 8 * blockIdx.x;
+  const double xmid = 0.5 * (x[0] + x[n - 1]);
+  double uns = 0, neg = 0, nf = 0, s0 = 0, s1 = 0, s2 = 0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double xi = x[i], wi = w[i];
+    if (!isfinite(xi) || !isfinite(wi)) nf = 1;
+    if (i + 1 < n && !(x[i + 1] >= xi)) uns = 1;
+    if (wi < 0) neg = 1;
+    const double xc = xi - xmid;
+    s0 += wi;
+    s1 += xc * wi;
+    s2 += xc * xc * wi;
+  }
+  uns = block_sum<32>(uns, sm);
+  neg = block_sum<32>(neg, sm);
+  nf = block_sum<32>(nf, sm);
+  s0 = block_sum<32>(s0, sm);
+  s1 = block_sum<32>(s1, sm);
+  s2 = block_sum<32>(s2, sm);
+  if (threadIdx.x == 0) {
+    o[0] = uns; o[1] = neg; o[2] = nf; o[3] = s0; o[4] = s1; o[5] = s2; o[6] = xmid; o[7] = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// Set-up of one (support, marginal) pair (grid-stride):
+//   xc = x - xmid (centred; GW is translation invariant),
+//   wn = w / S0 (renormalised copy), lw = ln wn,
+//   c_i = sum_j (x_i - x_j)^2 wn_j = xc_i^2 - 2 xc_i mu1 + mu2   ((D o D) u
+//   at k = 1, by moments of the normalised marginal; mu_k = S_k / S0).
+// ---------------------------------------------------------------------------------
+__global__ void k_prep(const double* __restrict__ x, const double* __restrict__ w, int64_t n,
+                       const double* __restrict__ mom, double* __restrict__ xc, double* __restrict__ wn,
+                       double* __restrict__ lw, double* __restrict__ cvec) {
+  const double xmid = mom[6], S0 = mom[3];
+  const double mu1 = mom[4] / S0, mu2 = mom[5] / S0, inv = 1.0 / S0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = x[i] - xmid;
+    const double wv = w[i] * inv;
+    xc[i] = v;
+    wn[i] = wv;
+    lw[i] = log(wv);
+    cvec[i] = v * v - 2.0 * v * mu1 + mu2;
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// 1-D dynamic programme on a sorted support s (one CTA of 1024 threads per vector):
+//   lower_i = sum_{j<i} (s_i - s_j) v_j                      (the paper's L v at k = 1,
+//   dist_i  = sum_j |s_i - s_j| v_j = 2 lower_i + Sv - s_i V   PAPER.md:219-243; D = L + L^T)
+// with V = sum v, Sv = sum s v.  Chunked: local pass, block scan of chunk states,
+// second local pass.  Either output may be null.  tot (nullable) = {V, Sv}.
+// ---------------------------------------------------------------------------------
+struct Scan1D {
+  const double* v;
+  const double* s;
+  int64_t n;
+  double* lower;
+  double* dist;
+  double* tot;
+};
+struct Scan1DBatch {
+  Scan1D d[6];
+};
+
+__global__ void __launch_bounds__(1024) k_scan1d(Scan1DBatch B) {
+  __shared__ double sm[3 * 32];
+  const Scan1D D = B.d[blockIdx.x];
+  const int64_t n = D.n;
+  if (n <= 0) return;
+  const int64_t chunk = (n + blockDim.x - 1) / blockDim.x;
+  const int64_t i0 = threadIdx.x * chunk, i1 = min(n, i0 + chunk);
+  PA<double> st{0.0, 0.0, D.s[min(i0, n - 1)]};
+  for (int64_t i = i0; i < i1; ++i) {
+    const double si = D.s[i];
+    st.A += (si - st.s) * st.P;
+    st.s = si;
+    st.P += D.v[i];
+  }
+  PA<double> total;
+  PA<double> e = pa_block_scan_excl<32>(st, sm, total);
+  const double V = total.P, Sv = total.s * total.P - total.A;
+  for (int64_t i = i0; i < i1; ++i) {
+    const double si = D.s[i];
+    const double lo = pa_eval(e, si);
+    if (D.lower) D.lower[i] = lo;
+    if (D.dist) D.dist[i] = 2.0 * lo + Sv - si * V;
+    e.A = lo;
+    e.s = si;
+    e.P += D.v[i];
+  }
+  if (D.tot && threadIdx.x == 0) { D.tot[0] = V; D.tot[1] = Sv; }
+}
+
+// fp32 hi/lo split of s * v (log2-domain dual scaling used by the Sinkhorn kernels)
+__global__ void k_split(const double* __restrict__ v, int64_t n, double scale, float* __restrict__ hi,
+                        float* __restrict__ lo) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double s = v[i] * scale;
+    const float h = (float)s;
+    hi[i] = h;
+    lo[i] = isfinite(s) ? (float)(s - (double)h) : 0.f;
+  }
+}
+
+__global__ void k_scale(const double* __restrict__ v, int64_t n, double scale, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = v[i] * scale;
+}
+
+__global__ void k_fill(double* __restrict__ v, int64_t n, double val) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v[i] = val;
+}
+
+// ---------------------------------------------------------------------------------
+// Objective assembly from the gradient pass's reductions (one CTA, deterministic).
+// With G' = 2(c 1^T + 1 c'^T) - 4 V (prescribed c, c'), V = D_X T D_Y:
+//   <V, T> = (2<c, a> + 2<c', b> - <G', T>) / 4,
+//   E(T)   = a^T (D_X o D_X) a + b^T (D_Y o D_Y) b - 2 <V, T>      (PAPER.md:86 expanded)
+// and a^T (D o D) a = 2 (A0 A2 - A1^2), A_k = sum xc^k a (moments; k = 1).
+// viol = max(|a - p|_inf, |b - q|_inf).
+// out: {E, viol, <G',T>, H}
+// ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_objective(const double* __restrict__ a, const double* __restrict__ xc,
+                                                    const double* __restrict__ p, const double* __restrict__ c,
+                                                    int64_t n, const double* __restrict__ b,
+                                                    const double* __restrict__ yc, const double* __restrict__ q,
+                                                    const double* __restrict__ c2, int64_t m,
+                                                    const double* __restrict__ tile_obj, int64_t ntile,
+                                                    const double* __restrict__ tile_ent, double* __restrict__ out) {
+  __shared__ double sm[32];
+  double A0 = 0, A1 = 0, A2 = 0, ca = 0, va = 0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double ai = a[i], xi = xc[i];
+    A0 += ai; A1 += ai * xi; A2 += ai * xi * xi; ca += c[i] * ai;
+    va = fmax(va, fabs(ai - p[i]));
+  }
+  double B0 = 0, B1 = 0, B2 = 0, cb = 0, vb = 0;
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+    const double bi = b[i], yi = yc[i];
+    B0 += bi; B1 += bi * yi; B2 += bi * yi * yi; cb += c2[i] * bi;
+    vb = fmax(vb, fabs(bi - q[i]));
+  }
+  double go = 0, he = 0;
+  for (int64_t i = threadIdx.x; i < ntile; i += blockDim.x) {
+    go += tile_obj[i];
+    if (tile_ent) he += tile_ent[i];
+  }
+  A0 = block_sum<32>(A0, sm); A1 = block_sum<32>(A1, sm); A2 = block_sum<32>(A2, sm);
+  B0 = block_sum<32>(B0, sm); B1 = block_sum<32>(B1, sm); B2 = block_sum<32>(B2, sm);
+  ca = block_sum<32>(ca, sm); cb = block_sum<32>(cb, sm);
+  go = block_sum<32>(go, sm); he = block_sum<32>(he, sm);
+  // max reduction (order independent)
+  __shared__ double smx[32];
+  double vmax = fmax(va, vb);
+  for (int d = 16; d > 0; d >>= 1) vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, d));
+  if ((threadIdx.x & 31) == 0) smx[threadIdx.x >> 5] = vmax;
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) smx[0] = fmax(smx[0], smx[k]);
+  if (threadIdx.x == 0) {
+    const double VT = (2.0 * ca + 2.0 * cb - go) / 4.0;
+    const double E = 2.0 * (A0 * A2 - A1 * A1) + 2.0 * (B0 * B2 - B1 * B1) - 2.0 * VT;
+    out[0] = E;
+    out[1] = smx[0];
+    out[2] = go;
+    out[3] = he;
+  }
+}
+
+}  // namespace gw

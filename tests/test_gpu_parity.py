@@ -1,0 +1,243 @@
+"""GPU parity: the CUDA path (through the C ABI) against the float64 oracle on the same
+seeded inputs.  Tolerances are the north_star's (BASELINE.json):
+  gradient max-abs error <= 1e-5 * max|G|,  final GW objective rel. error <= 1e-4,
+  marginal violation <= 1e-6.
+"""
+
+import numpy as np
+import pytest
+
+import oracle as O
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+GRAD_TOL = 1e-5
+OBJ_TOL = 1e-4
+VIOL_TOL = 1e-6
+
+
+@pytest.fixture(scope="module")
+def gw():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__ as ge
+    ge.build()
+    from paper_2404_08970_b200 import api
+    return api
+
+
+def _dev():
+    import torch
+    return torch.device("cuda", 0)
+
+
+def _to_dev(api, T):
+    import torch
+    n, m = T.shape
+    t = api.plan_buffer(n, m, _dev())
+    t.copy_(torch.from_numpy(np.ascontiguousarray(T, dtype=np.float32)))
+    return t
+
+
+def _grad_err(G, Go):
+    return np.max(np.abs(G - Go)) / max(np.max(np.abs(Go)), 1e-300)
+
+
+# ----------------------------------------------------------------------------- gradient
+
+GRAD_SHAPES = [(1, 1), (1, 7), (7, 1), (3, 5), (64, 64), (255, 300), (256, 256), (257, 513), (600, 1000),
+               (1000, 777), (1024, 1031)]
+
+
+@pytest.mark.parametrize("n,m", GRAD_SHAPES)
+def test_grad_random_plan(gw, n, m):
+    """gw_grad_dp vs grad_prescribed on a random fp32 plan, ragged tails,
+    ties in the supports, non-uniform marginals."""
+    rng = np.random.default_rng(n * 1000 + m)
+    x, y = np.sort(rng.random(n)), np.sort(rng.random(m))
+    if n > 10:
+        x[5] = x[4]
+    if m > 10:
+        y[7] = y[6]
+    p, q = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))
+    T = (rng.exponential(size=(n, m)) / (n * m)).astype(np.float32)
+    G = gw.grad(x, y, p, q, _to_dev(gw, T)).cpu().numpy().astype(np.float64)
+    Go = O.grad_prescribed(x, y, p, q, T.astype(np.float64))
+    assert _grad_err(G, Go) <= GRAD_TOL
+
+
+def test_grad_c3_recipe_4096(gw):
+    """C3 recipe (Exp(1) rescaled to uniform marginals) at N = M = 4096, full matrix."""
+    P = W.config3(4096)
+    T = P.extra["T"]
+    G = gw.grad(P.x, P.y, P.p, P.q, _to_dev(gw, T)).cpu().numpy().astype(np.float64)
+    Go = O.grad_prescribed(P.x, P.y, P.p, P.q, T.astype(np.float64))
+    assert _grad_err(G, Go) <= GRAD_TOL
+
+
+def test_grad_product_closed_form(gw):
+    """At T0 = p (x) q the gradient is G0 = 2(c_i + c'_p) - 4 (D_X p)_i (D_Y q)_p (P7)."""
+    P = W.uniform_problem(777, 1290, seed=3)
+    T = np.outer(P.p, P.q).astype(np.float32)
+    G = gw.grad(P.x, P.y, P.p, P.q, _to_dev(gw, T)).cpu().numpy().astype(np.float64)
+    DX, DY = O.dist(P.x), O.dist(P.y)
+    Tq = T.astype(np.float64)
+    a, b = Tq.sum(1), Tq.sum(0)
+    c, c2 = O.const_term(P.x, P.y, P.p, P.q)
+    G0 = 2 * (c[:, None] + c2[None, :]) - 4 * np.outer(DX @ a, DY @ b)
+    assert _grad_err(G, G0) <= GRAD_TOL
+
+
+def test_grad_in_place(gw):
+    rng = np.random.default_rng(5)
+    n, m = 300, 400
+    x, y = np.sort(rng.random(n)), np.sort(rng.random(m))
+    p, q = np.full(n, 1 / n), np.full(m, 1 / m)
+    T = (rng.random((n, m)) / (n * m)).astype(np.float32)
+    Td = _to_dev(gw, T)
+    G = gw.grad(x, y, p, q, Td, out=Td).cpu().numpy().astype(np.float64)
+    assert _grad_err(G, O.grad_prescribed(x, y, p, q, T.astype(np.float64))) <= GRAD_TOL
+
+
+def test_grad_deterministic(gw):
+    P = W.config3(1500)
+    Td = _to_dev(gw, P.extra["T"])
+    a = gw.grad(P.x, P.y, P.p, P.q, Td).cpu().numpy()
+    b = gw.grad(P.x, P.y, P.p, P.q, Td).cpu().numpy()
+    assert np.array_equal(a, b)
+
+
+# ----------------------------------------------------------------------------- errors
+
+def test_rejects_unsorted(gw):
+    from paper_2404_08970_b200 import GwError
+    x = np.array([0.0, 0.5, 0.2, 0.9])
+    T = np.full((4, 4), 1 / 16, np.float32)
+    with pytest.raises(GwError) as e:
+        gw.grad(x, np.sort(x), np.full(4, .25), np.full(4, .25), _to_dev(gw, T))
+    assert e.value.code == "GW_ERR_UNSORTED"
+
+
+def test_rejects_bad_marginals(gw):
+    from paper_2404_08970_b200 import GwError
+    x = np.linspace(0, 1, 4)
+    T = _to_dev(gw, np.full((4, 4), 1 / 16, np.float32))
+    with pytest.raises(GwError) as e:
+        gw.grad(x, x, np.ones(4), np.full(4, .25), T)
+    assert e.value.code == "GW_ERR_NOT_NORMALIZED"
+    with pytest.raises(GwError) as e:
+        gw.grad(x, x, np.array([.5, .5, .25, -.25]), np.full(4, .25), T)
+    assert e.value.code == "GW_ERR_NEGATIVE_WEIGHT"
+    # within the 1e-9 band: accepted (renormalised copy)
+    gw.grad(x, x, np.array([.25, .25, .25, .25 + 1e-12]), np.full(4, .25), T)
+
+
+# ----------------------------------------------------------------------------- Sinkhorn
+
+@pytest.mark.parametrize("n,m,eps", [(5, 3, 0.2), (200, 333, 0.05), (1000, 2500, 0.02), (300, 4100, 0.01)])
+def test_sinkhorn_parity(gw, n, m, eps):
+    """sinkhorn_solve vs the oracle's log-domain Sinkhorn (same schedule, same fp32 cost)."""
+    rng = np.random.default_rng(n + m)
+    G = rng.random((n, m)).astype(np.float32)
+    p, q = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))
+    r = gw.sinkhorn(_to_dev(gw, G), p, q, eps, 50, return_plan=True)
+    f, g, _ = O.sinkhorn(G.astype(np.float64), p, q, eps, 50)
+    To = O.plan_from_duals(G.astype(np.float64), f, g, eps)
+    T = r["T"].cpu().numpy().astype(np.float64)
+    assert np.max(np.abs(T - To)) <= 1e-4 * np.max(To)
+    assert np.max(np.abs(r["g"].cpu().numpy() - g)) <= 1e-5 * eps * 10
+
+
+def test_sinkhorn_tolerance_rule(gw):
+    rng = np.random.default_rng(7)
+    n, m, eps = 400, 300, 0.05
+    G = rng.random((n, m)).astype(np.float32)
+    p, q = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))
+    r = gw.sinkhorn(_to_dev(gw, G), p, q, eps, 2000, tol=1e-9, check_every=10)
+    assert r["converged"] and r["iters"] % 10 == 0 and r["violation"] <= 1e-9
+    f, g, used = O.sinkhorn(G.astype(np.float64), p, q, eps, r["iters"])
+    To = O.plan_from_duals(G.astype(np.float64), f, g, eps)
+    assert O.violation(To, p, q) <= 1e-8
+
+
+# ----------------------------------------------------------------------------- solver
+
+def test_solver_c1_trajectory(gw):
+    """C1 (BASELINE configs[0]): N = M = 256, eps = 1e-2, 20 x 100, T0 = p q^T, full trajectory."""
+    P = W.config1()
+    r = gw.solve(P.x, P.y, P.p, P.q, P.eps, P.outer, P.inner, trace_objective=True, return_plan=True)
+    ro = O.entropic_gw(P.x, P.y, P.p, P.q, P.eps, P.outer, P.inner)
+    assert abs(r.gw_objective - ro["gw_objective"]) <= OBJ_TOL * abs(ro["gw_objective"])
+    assert r.marginal_violation <= VIOL_TOL
+    np.testing.assert_allclose(r.trace[:, 0], ro["E"], rtol=OBJ_TOL)
+    T = r.T.cpu().numpy().astype(np.float64)
+    assert O.violation(T, P.p, P.q) <= VIOL_TOL
+    assert abs(O.objective(P.x, P.y, T) - r.gw_objective) <= OBJ_TOL * abs(r.gw_objective)
+    assert abs(r.entropic_objective - ro["entropic_objective"]) <= OBJ_TOL * abs(ro["entropic_objective"])
+
+
+def test_solver_gradient_step_on_own_plan(gw):
+    """The per-step gradient contract: c3 on the GPU's own T^l."""
+    P = W.config2(1024)
+    r = gw.solve(P.x, P.y, P.p, P.q, P.eps, 3, 100, return_plan=True)
+    T = r.T
+    G = gw.grad(P.x, P.y, P.p, P.q, T).cpu().numpy().astype(np.float64)
+    Go = O.grad_prescribed(P.x, P.y, P.p, P.q, T.cpu().numpy().astype(np.float64))
+    assert _grad_err(G, Go) <= GRAD_TOL
+
+
+def test_solver_c2_recipe_reduced(gw):
+    """C2 recipe at N = 1024 (Gaussian mixture / reflected y / Dirichlet marginals), eps = 5e-3,
+    20 outer x 100 inner; the oracle replays the same schedule."""
+    P = W.config2(1024)
+    r = gw.solve(P.x, P.y, P.p, P.q, P.eps, 20, 100, trace_objective=True)
+    ro = O.entropic_gw(P.x, P.y, P.p, P.q, P.eps, 20, 100)
+    assert abs(r.gw_objective - ro["gw_objective"]) <= OBJ_TOL * abs(ro["gw_objective"])
+    assert r.marginal_violation <= VIOL_TOL
+
+
+def test_solver_tolerance_rule_replay(gw):
+    """Reading R8: with the tolerance rule the GPU reports its per-outer inner counts and the
+    oracle replays them exactly."""
+    P = W.config4(512)
+    r = gw.solve(P.x, P.y, P.p, P.q, P.eps, 5, 2000, tol=1e-7, check_every=10)
+    counts = [int(c) for c in r.trace[:, 2]]
+    ro = O.entropic_gw(P.x, P.y, P.p, P.q, P.eps, 5, counts)
+    assert abs(r.gw_objective - ro["gw_objective"]) <= OBJ_TOL * abs(ro["gw_objective"])
+    assert r.marginal_violation <= VIOL_TOL
+    assert ro["viol"][-1] <= VIOL_TOL
+
+
+def test_solver_single_point_and_row(gw):
+    r = gw.solve([0.3], [0.7], [1.0], [1.0], 0.01, 3, 10, return_plan=True)
+    assert r.T.cpu().numpy().tolist() == [[1.0]] and abs(r.gw_objective) < 1e-12
+    rng = np.random.default_rng(1)
+    y = np.sort(rng.random(9))
+    q = rng.dirichlet(np.ones(9))
+    r = gw.solve([0.5], y, [1.0], q, 0.01, 2, 20, return_plan=True)
+    np.testing.assert_allclose(r.T.cpu().numpy()[0], q, rtol=1e-5)
+
+
+def test_solver_host_vectors_match_device(gw):
+    P = W.config1()
+    a = gw.solve(P.x, P.y, P.p, P.q, P.eps, 4, 50)
+    b = gw.solve_host(P.x, P.y, P.p, P.q, P.eps, 4, 50)
+    assert a.gw_objective == b.gw_objective
+    np.testing.assert_array_equal(a.f.cpu().numpy(), b.f)
+
+
+def test_solver_deterministic(gw):
+    P = W.config2(700)
+    a = gw.solve(P.x, P.y, P.p, P.q, P.eps, 3, 60, return_plan=True)
+    b = gw.solve(P.x, P.y, P.p, P.q, P.eps, 3, 60, return_plan=True)
+    assert a.gw_objective == b.gw_objective
+    assert np.array_equal(a.T.cpu().numpy(), b.T.cpu().numpy())
+
+
+def test_ugw_unsupported(gw):
+    from paper_2404_08970_b200 import GwError
+    with pytest.raises(GwError) as e:
+        gw.ugw_solve()
+    assert e.value.code == "GW_ERR_UNSUPPORTED"
