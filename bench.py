@@ -210,19 +210,19 @@ def main():
 
     # ---- roofline (live, per kernel class) ----
     hbm, peak_src = peaks()
-    names = ["grad_moments", "grad_carry", "grad_main", "sink_row", "sink_col"]
+    names = ["grad_moments", "grad_carry", "grad_main", "sink_row", "sink_col", "sink_fused"]
     algo_bytes = {"grad_moments": 4.0 * n * m, "grad_main": 8.0 * n * m, "sink_row": 4.0 * n * m,
-                  "sink_col": 4.0 * n * m}
+                  "sink_col": 4.0 * n * m, "sink_fused": 4.0 * n * m}
     kern = {}
     for k, nm in enumerate(names):
         if cnt_c[k] > 0:
-            ms_launch = ms_c[k] / cnt_c[k] * (2 if nm == "sink_col" else 1)  # sink_col counts col+colfin
+            ms_launch = ms_c[k] / cnt_c[k] * (2 if nm in ("sink_col", "sink_fused") else 1)  # 2 launches/class
             d = {"ms_total": ms_c[k], "launches": int(cnt_c[k]), "ms_per_launch": ms_launch}
             if nm in algo_bytes:
                 d["GBps"] = algo_bytes[nm] / (ms_launch / 1000.0) / 1e9
                 d["frac"] = d["GBps"] / hbm
             kern[nm] = d
-    dom = max(("sink_row", "sink_col"), key=lambda k: kern.get(k, {}).get("ms_total", 0))
+    dom = max(("sink_row", "sink_col", "sink_fused"), key=lambda k: kern.get(k, {}).get("ms_total", 0))
     roof = {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["GBps"], "peak": hbm, "unit": "GB/s",
             "frac": kern[dom]["frac"], "traffic": None, "peak_source": peak_src,
             "algorithmic_bytes_per_launch": algo_bytes[dom],
@@ -255,7 +255,8 @@ def main():
            "gpu_launches": int(cnt_c[6]),
            "clocks": ck, "e2e": e2e,
            "result": {"gw_objective": res.gw_objective, "marginal_violation": res.marginal_violation,
-                      "e2e_gw_objective": re.gw_objective}}
+                      "e2e_gw_objective": re.gw_objective, "inner_iters": res.inner_iters_total,
+                      "inner_fused": res.inner_fused_total}}
     if rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = oracle_sample(n_s=2048 if args.n >= 2048 else args.n, n_full=args.n,
                                             inner=args.inner)

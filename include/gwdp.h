@@ -104,6 +104,7 @@ typedef struct {
 typedef struct {
   int32_t iters;               /* iterations performed                                */
   int32_t converged;           /* 1 if violation <= tol was observed                   */
+  int32_t fused_iters;         /* iterations that ran the fused one-read path            */
   double marginal_violation;   /* max(|T1 - p|_inf, |T^T 1 - q|_inf) of the final plan */
 } gw_sinkhorn_info;
 
@@ -123,6 +124,7 @@ typedef struct {
   double entropic_objective;  /* E(T^L) + eps H(T^L)                  */
   double marginal_violation;  /* of T^L                                                 */
   int32_t outer_iters, inner_iters_total, converged;
+  int32_t inner_fused_total;  /* Sinkhorn iterations that ran the fused one-read path    */
   double ms_grad, ms_sinkhorn, ms_total;
 } gw_result;
 

@@ -53,7 +53,8 @@ class gw_sinkhorn_opts(C.Structure):
 
 
 class gw_sinkhorn_info(C.Structure):
-    _fields_ = [("iters", C.c_int32), ("converged", C.c_int32), ("marginal_violation", C.c_double)]
+    _fields_ = [("iters", C.c_int32), ("converged", C.c_int32), ("fused_iters", C.c_int32),
+                ("marginal_violation", C.c_double)]
 
 
 class gw_solve_opts(C.Structure):
@@ -64,7 +65,7 @@ class gw_solve_opts(C.Structure):
 class gw_result(C.Structure):
     _fields_ = [("gw_objective", C.c_double), ("entropic_objective", C.c_double),
                 ("marginal_violation", C.c_double), ("outer_iters", C.c_int32),
-                ("inner_iters_total", C.c_int32), ("converged", C.c_int32),
+                ("inner_iters_total", C.c_int32), ("converged", C.c_int32), ("inner_fused_total", C.c_int32),
                 ("ms_grad", C.c_double), ("ms_sinkhorn", C.c_double), ("ms_total", C.c_double)]
 
 

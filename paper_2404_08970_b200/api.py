@@ -120,7 +120,7 @@ def sinkhorn(G, p, q, eps, max_iter, tol=0.0, check_every=10, f=None, g=None, re
     L.check(ctx.lib.sinkhorn_solve(ctx.h, C.byref(pr), _ptr(G), ldG, C.byref(o), _ptr(f), _ptr(g), _ptr(T),
                                    T.stride(0) if T is not None else 0, C.byref(info)))
     out = {"f": f, "g": g, "iters": info.iters, "converged": bool(info.converged),
-           "violation": info.marginal_violation}
+           "violation": info.marginal_violation, "fused_iters": info.fused_iters}
     if return_plan:
         out["T"] = T
     return out
@@ -141,13 +141,14 @@ class Result:
     g: Optional[object] = None
     T: Optional[object] = None
     trace: Optional[np.ndarray] = None   # [outer, 4]: E(T^l), violation, inner iters, ms
+    inner_fused_total: int = 0
     extra: dict = field(default_factory=dict)
 
 
 def _result(res, f, g, T, tr):
     return Result(res.gw_objective, res.entropic_objective, res.marginal_violation, res.outer_iters,
                   res.inner_iters_total, bool(res.converged), res.ms_grad, res.ms_sinkhorn, res.ms_total,
-                  f, g, T, tr)
+                  f, g, T, tr, res.inner_fused_total)
 
 
 def _opts(eps, outer, inner, tol, check_every, trace_objective):

@@ -13,6 +13,7 @@
 
 #include "../../include/gwdp.h"
 #include "common.cuh"
+#include "fused.cuh"
 #include "grad.cuh"
 #include "sink.cuh"
 #include "vec.cuh"
@@ -63,7 +64,7 @@ struct gw_comm {
 };
 
 // Per-kernel-class CUDA-event timing (enabled by gw_ctx_profile; events on ctx's stream).
-enum { PC_GRAD_MOMENTS = 0, PC_GRAD_CARRY, PC_GRAD_MAIN, PC_SINK_ROW, PC_SINK_COL, PC_OTHER, PC_N };
+enum { PC_GRAD_MOMENTS = 0, PC_GRAD_CARRY, PC_GRAD_MAIN, PC_SINK_ROW, PC_SINK_COL, PC_SINK_FUSED, PC_N };
 struct Prof {
   bool on = false;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
@@ -82,7 +83,7 @@ struct gw_ctx {
   std::vector<Buf*> all;
   // vectors
   Buf stage, mom, xc, yc, pn, qn, lp, lq, cvx, cvy;
-  Buf fs, gs, fh, fl, gh, gl, ftmp, viol, stop, iters, part;
+  Buf fs, gs, fh, fl, gh, gl, ftmp, viol, stop, iters, part, fpart, mode, srow, pfl;
   // gradient aux
   Buf rP, rA, cS, cX, blk, bs, btot, cxend, SAg, WAg, Ptot, Aend, DP, DA, tobj, tent, tcc, objout;
   Buf fxs, fys;  // FGW features (staged)
@@ -91,7 +92,7 @@ struct gw_ctx {
   double* hpin = nullptr;  // pinned host scratch (64 doubles)
   gw_ctx() {
     Buf* b[] = {&stage, &mom, &xc, &yc, &pn, &qn, &lp, &lq, &cvx, &cvy, &fs, &gs, &fh, &fl, &gh, &gl,
-                &ftmp, &viol, &stop, &iters, &part, &rP, &rA, &cS, &cX, &blk, &bs, &btot, &cxend,
+                &ftmp, &viol, &stop, &iters, &part, &fpart, &mode, &srow, &pfl, &rP, &rA, &cS, &cX, &blk, &bs, &btot, &cxend,
                 &SAg, &WAg, &Ptot, &Aend, &DP, &DA, &tobj, &tent, &tcc, &objout, &fxs, &fys, &fsc, &gsc, &Gs};
     for (Buf* x : b) all.push_back(x);
   }
@@ -461,7 +462,66 @@ struct SinkState {
   float2* part;
   int nrb;
   int64_t RB;
+  // fused fast path
+  int* mode;      // [0] = path of the current iteration (1 = fused), [1] = fused iterations run
+  float* dev;     // max |log2(colsum/q)| of the last column half-step
+  double* fpart;  // [ncl][m]
+  float* Srow;    // [nl]
+  float* pf;      // [nl] p as fp32
+  int fK = 0, fCL = 0, fncl = 0;  // fK == 0: fast path unavailable for this shape
+  int64_t frpc = 0;
 };
+
+template <int K, int CL>
+static gw_status fused_config_t(gw_ctx* c, int* ncl) {
+  auto kern = k_sink_fused<K, CL>;
+  const size_t dsm = fused_dyn_smem<K>();
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(148 * CL);
+  cfg.blockDim = dim3(FT);
+  cfg.dynamicSmemBytes = dsm;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CU(cudaOccupancyMaxActiveClusters(ncl, (void*)kern, &cfg));
+  return GW_OK;
+}
+
+template <int K, int CL>
+static gw_status fused_launch_t(gw_ctx* c, const FusedArgs& fa, int ncl) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ncl * CL);
+  cfg.blockDim = dim3(FT);
+  cfg.dynamicSmemBytes = fused_dyn_smem<K>();
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CU(cudaLaunchKernelEx(&cfg, k_sink_fused<K, CL>, fa));
+  return GW_OK;
+}
+
+// (K, CL) dispatch: K in 1..4 with CL = 1 (m <= 8192), K = 4 with CL in {2, 4, 8}
+#define FUSED_DISPATCH(FN, ...)                                                   \
+  switch (K * 16 + CL) {                                                          \
+    case 1 * 16 + 1: return FN<1, 1>(__VA_ARGS__);                                \
+    case 2 * 16 + 1: return FN<2, 1>(__VA_ARGS__);                                \
+    case 3 * 16 + 1: return FN<3, 1>(__VA_ARGS__);                                \
+    case 4 * 16 + 1: return FN<4, 1>(__VA_ARGS__);                                \
+    case 4 * 16 + 2: return FN<4, 2>(__VA_ARGS__);                                \
+    case 4 * 16 + 4: return FN<4, 4>(__VA_ARGS__);                                \
+    case 4 * 16 + 8: return FN<4, 8>(__VA_ARGS__);                                \
+    default: return fail(GW_ERR_UNSUPPORTED, "fused path: no instance K=%d CL=%d", K, CL); \
+  }
+static gw_status fused_config(gw_ctx* c, int K, int CL, int* ncl) { FUSED_DISPATCH(fused_config_t, c, ncl) }
+static gw_status fused_launch(gw_ctx* c, int K, int CL, const FusedArgs& fa, int ncl) {
+  FUSED_DISPATCH(fused_launch_t, c, fa, ncl)
+}
 
 static gw_status sink_alloc(gw_ctx* c, const Prepared& P, SinkState& s) {
   TRY(ws(c, c->fh, P.nl, &s.fh)); TRY(ws(c, c->fl, P.nl, &s.fl));
@@ -478,6 +538,34 @@ static gw_status sink_alloc(gw_ctx* c, const Prepared& P, SinkState& s) {
   s.RB = RB;
   s.nrb = (int)std::max<int64_t>(1, (P.nl + RB - 1) / RB);
   TRY(ws(c, c->part, (size_t)s.nrb * P.m, &s.part));
+  // fused fast path: cluster of CL CTAs x W = 2048 K columns spans a row
+  int* md;
+  TRY(ws(c, c->mode, 4, &md));
+  s.mode = md;
+  s.dev = reinterpret_cast<float*>(md + 2);
+  s.fK = 0;
+  const char* env = getenv("GWDP_NO_FUSED");
+  if (!(env && env[0] == '1') && P.nl > 0) {
+    int K, CL;
+    if (P.m <= 8192) { K = (int)((P.m + 2047) / 2048); CL = 1; }
+    else { K = 4; CL = (int)((P.m + 8191) / 8192); }
+    if (CL == 3) CL = 4;
+    if (CL > 4 && CL < 8) CL = 8;
+    if (CL <= 8) {
+      int ncl = 0;
+      TRY(fused_config(c, K, CL, &ncl));
+      if (ncl > 0) {
+        ncl = (int)std::min<int64_t>(ncl, P.nl);
+        s.fK = K; s.fCL = CL; s.fncl = ncl;
+        s.frpc = (P.nl + ncl - 1) / ncl;
+        TRY(ws(c, c->fpart, (size_t)ncl * P.m, &s.fpart));
+        TRY(ws(c, c->srow, (size_t)P.nl, &s.Srow));
+        TRY(ws(c, c->pfl, (size_t)P.nl, &s.pf));
+        k_to_float<<<grid_for(P.nl), 256, 0, c->stream>>>(P.pn + P.row0, P.nl, s.pf);
+        KCHECK();
+      }
+    }
+  }
   return GW_OK;
 }
 
@@ -492,31 +580,35 @@ static gw_status sink_split(gw_ctx* c, const Prepared& P, SinkState& s, double e
 // `iters` Sinkhorn iterations on G.  tol > 0: check every `check_every` iterations (one
 // host sync per check); returns the iterations used and whether tol was met.
 static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const float* G, int64_t ldG, double eps,
-                          int iters, double tol, int check_every, int* used, int* converged) {
+                          int iters, double tol, int check_every, int* used, int* converged, bool reset_count = true) {
   const int64_t nl = P.nl, m = P.m;
   const float c2f = (float)(GW_LOG2E / eps);
-  const bool small_rows = m <= 2048;
-  const int rows_grid = grid_for(small_rows ? (nl + 7) / 8 : nl, 1, 148 * 8);
   dim3 cgrid((unsigned)((m + 1023) / 1024), (unsigned)s.nrb);
   CU(cudaMemsetAsync(s.stop, 0, sizeof(int), c->stream));
+  if (reset_count) CU(cudaMemsetAsync(s.mode, 0, 4 * sizeof(int), c->stream));  // safe path; dev = 0; count = 0
+  else CU(cudaMemsetAsync(s.mode, 0, sizeof(int), c->stream));                   // safe path first
   *used = 0;
   *converged = 0;
   if (check_every < 1) check_every = 10;
   int done = 0;
   const bool tolmode = tol > 0;
+  FusedArgs fa;
+  fa.G = G; fa.ld = ldG; fa.nl = nl; fa.m = m; fa.c2f = c2f; fa.gh = s.gh; fa.gl = s.gl; fa.fh = s.fh;
+  fa.fl = s.fl; fa.pf = s.pf; fa.Srow = s.Srow; fa.part = s.fpart; fa.rows_per_cluster = s.frpc;
+  fa.mode = s.mode; fa.stop = s.stop;
   while (done < iters) {
     const int chunk = tolmode ? std::min(check_every, iters - done) : iters - done;
     for (int k = 0; k < chunk; ++k) {
       const bool check = tolmode && k == 0 && done > 0;  // violation of the plan after `done` iterations
+      // iterations run the robust two-kernel path while *mode == 0 and the fused one-read
+      // path once *mode == 1 (decided on the device by k_sink_mode; no host sync)
+      const int* skip = check ? nullptr : s.mode;
       if (check) CU(cudaMemsetAsync(s.viol, 0, sizeof(float), c->stream));
       double* fout = check ? s.ftmp : s.f;
       PROF_BEGIN(c, PC_SINK_ROW);
-      if (small_rows)
-        k_sink_row<32><<<rows_grid, 256, 0, c->stream>>>(G, ldG, nl, m, s.gh, s.gl, c2f, s.f, fout, P.lp + P.row0, eps,
-                                                         s.fh, s.fl, check ? s.viol : nullptr, s.stop);
-      else
-        k_sink_row<256><<<rows_grid, 256, 0, c->stream>>>(G, ldG, nl, m, s.gh, s.gl, c2f, s.f, fout, P.lp + P.row0,
-                                                          eps, s.fh, s.fl, check ? s.viol : nullptr, s.stop);
+      k_sink_row<<<(unsigned)((nl + RROWS - 1) / RROWS), 256, 0, c->stream>>>(
+          G, ldG, nl, m, s.gh, s.gl, c2f, s.f, fout, P.lp + P.row0, eps, s.fh, s.fl, check ? s.viol : nullptr, s.stop,
+          skip);
       KCHECK();
       PROF_END(c, PC_SINK_ROW, 1);
       if (check) {
@@ -524,12 +616,24 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
         KCHECK();
       }
       PROF_BEGIN(c, PC_SINK_COL);
-      k_sink_col<<<cgrid, 256, 0, c->stream>>>(G, ldG, nl, m, s.fh, s.fl, c2f, s.RB, s.part, s.stop);
+      k_sink_col<<<cgrid, 256, 0, c->stream>>>(G, ldG, nl, m, s.fh, s.fl, c2f, s.RB, s.part, s.stop, skip);
       KCHECK();
       k_sink_colfin<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.part, s.nrb, m, P.lq, eps, s.g, s.gh, s.gl,
-                                                                       s.stop);
+                                                                       s.stop, skip, s.dev);
       KCHECK();
       PROF_END(c, PC_SINK_COL, 2);
+      if (!check && s.fK > 0) {
+        PROF_BEGIN(c, PC_SINK_FUSED);
+        TRY(fused_launch(c, s.fK, s.fCL, fa, s.fncl));
+        KCHECK();
+        k_sink_fin_fast<<<grid_for(std::max(m, nl), 256, 1 << 30), 256, 0, c->stream>>>(
+            s.Srow, nl, P.lp + P.row0, s.f, s.fh, s.fl, nullptr, s.fpart, s.fncl, m, P.lq, eps, s.g, s.gh, s.gl,
+            s.mode, s.stop, s.dev);
+        KCHECK();
+        PROF_END(c, PC_SINK_FUSED, 2);
+      }
+      k_sink_mode<<<1, 32, 0, c->stream>>>(s.dev, s.mode, s.fK > 0 ? 20.f : -1.f);
+      KCHECK();
     }
     if (tolmode) {
       int hs[2];
@@ -548,12 +652,8 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
   if (tolmode) {
     // final check of the plan after `done` iterations (row half-step into ftmp, not committed)
     CU(cudaMemsetAsync(s.viol, 0, sizeof(float), c->stream));
-    if (small_rows)
-      k_sink_row<32><<<rows_grid, 256, 0, c->stream>>>(G, ldG, nl, m, s.gh, s.gl, c2f, s.f, s.ftmp, P.lp + P.row0, eps,
-                                                       s.fh, s.fl, s.viol, nullptr);
-    else
-      k_sink_row<256><<<rows_grid, 256, 0, c->stream>>>(G, ldG, nl, m, s.gh, s.gl, c2f, s.f, s.ftmp, P.lp + P.row0,
-                                                        eps, s.fh, s.fl, s.viol, nullptr);
+    k_sink_row<<<(unsigned)((nl + RROWS - 1) / RROWS), 256, 0, c->stream>>>(
+        G, ldG, nl, m, s.gh, s.gl, c2f, s.f, s.ftmp, P.lp + P.row0, eps, s.fh, s.fl, s.viol, nullptr, nullptr);
     KCHECK();
     float hv;
     CU(cudaMemcpyAsync(&hv, s.viol, sizeof(float), cudaMemcpyDeviceToHost, c->stream));
@@ -633,21 +733,19 @@ extern "C" gw_status sinkhorn_solve(gw_ctx* c, const gw_problem* pb, const void*
     // violation of the returned plan: a measuring row half-step (not committed)
     CU(cudaMemsetAsync(s.viol, 0, sizeof(float), c->stream));
     const float c2f = (float)(GW_LOG2E / o->eps);
-    const int rows_grid = grid_for(P.m <= 2048 ? (P.nl + 7) / 8 : P.nl, 1, 148 * 8);
-    if (P.m <= 2048)
-      k_sink_row<32><<<rows_grid, 256, 0, c->stream>>>(reinterpret_cast<const float*>(G), ldG, P.nl, P.m, s.gh, s.gl,
-                                                       c2f, s.f, s.ftmp, P.lp + P.row0, o->eps, s.fh, s.fl, s.viol,
-                                                       nullptr);
-    else
-      k_sink_row<256><<<rows_grid, 256, 0, c->stream>>>(reinterpret_cast<const float*>(G), ldG, P.nl, P.m, s.gh,
-                                                        s.gl, c2f, s.f, s.ftmp, P.lp + P.row0, o->eps, s.fh, s.fl,
-                                                        s.viol, nullptr);
+    k_sink_row<<<(unsigned)((P.nl + RROWS - 1) / RROWS), 256, 0, c->stream>>>(
+        reinterpret_cast<const float*>(G), ldG, P.nl, P.m, s.gh, s.gl, c2f, s.f, s.ftmp, P.lp + P.row0, o->eps, s.fh,
+        s.fl, s.viol, nullptr, nullptr);
     KCHECK();
     float hv;
     CU(cudaMemcpyAsync(&hv, s.viol, sizeof(float), cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
+    int* md = reinterpret_cast<int*>(c->hpin + 40);
+    CU(cudaMemcpyAsync(md, s.mode, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
     info->iters = used;
     info->converged = o->tol > 0 ? ((double)hv <= o->tol) : 0;
+    info->fused_iters = md[1];
     info->marginal_violation = hv;
   }
   TRY(stage_duals_out(c, pb, P, f, g, s.f, s.g));
@@ -748,7 +846,8 @@ static gw_status solve_impl(gw_ctx* c, const gw_problem* pb, const gw_solve_opts
     // ---- Sinkhorn on G^{l+1} with warm-started duals ----
     TRY(sink_split(c, P, s, eps));
     int used = 0, conv = 0;
-    TRY(sink_run(c, P, s, G, ldG, eps, o->inner.max_iter, o->inner.tol, o->inner.check_every, &used, &conv));
+    TRY(sink_run(c, P, s, G, ldG, eps, o->inner.max_iter, o->inner.tol, o->inner.check_every, &used, &conv,
+                 l == 0));
     inner_total += used;
     if (o->inner.tol > 0 && !conv) conv_all = 0;
     tr[(size_t)l * 4 + 2] = used;
@@ -775,8 +874,11 @@ static gw_status solve_impl(gw_ctx* c, const gw_problem* pb, const gw_solve_opts
                                                           cudaMemcpyDeviceToDevice, c->stream));
     CU(cudaMemcpyAsync(c->hpin, objout, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   }
+  int fused_total = 0;
+  if (o->outer_iters > 0) CU(cudaMemcpyAsync(c->hpin + 32, s.mode, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CU(cudaEventRecord(ev1, c->stream));
   CU(cudaStreamSynchronize(c->stream));
+  if (o->outer_iters > 0) fused_total = reinterpret_cast<int*>(c->hpin + 32)[1];
   if (nl > 0) {
     E = c->hpin[0]; viol = c->hpin[1]; H = c->hpin[3]; ecc = c->hpin[6];
   }
@@ -803,6 +905,7 @@ static gw_status solve_impl(gw_ctx* c, const gw_problem* pb, const gw_solve_opts
   res->outer_iters = o->outer_iters;
   res->inner_iters_total = inner_total;
   res->converged = (o->inner.tol > 0) ? conv_all : 0;
+  res->inner_fused_total = fused_total;
   res->ms_grad = ms_grad;
   res->ms_sinkhorn = ms_sink;
   res->ms_total = ms_total;

@@ -12,84 +12,97 @@
 namespace gw {
 
 // ---------------------------------------------------------------------------------
-// Row half-step.  TPR threads per row (32 or 256), rows grid-strided.
-//   fout_i = eps ln p_i - eps ln2 LSE2_p(a_ip)
+// Row half-step (robust "safe" path).  A CTA of 256 threads owns RROWS rows and walks
+// the columns in chunks of 2048 (8 per thread), so each chunk's dual constants gh/gl are
+// loaded once per RROWS rows (L2 traffic 8/RROWS B per element on top of the 4 B of G).
+// Online max-shifted LSE per row in registers.
+//   fout_i = eps ln p_i - eps ln2 LSE2_p(a_ip),   a_ip = g_p log2e/eps - G_ip log2e/eps
 // and the violation of the current plan's row (the plan (fcur, g)):
 //   |sum_p T_ip - p_i| = p_i |2^{(fcur_i - fout_i) log2e / eps} - 1|
 // ---------------------------------------------------------------------------------
-template <int TPR>
+constexpr int RROWS = 16;
+
 __global__ void __launch_bounds__(256) k_sink_row(const float* __restrict__ G, int64_t ld, int64_t nl, int64_t m,
                                                   const float* __restrict__ gh, const float* __restrict__ gl,
                                                   float c2f, const double* __restrict__ fcur,
                                                   double* __restrict__ fout, const double* __restrict__ lp,
                                                   double eps, float* __restrict__ fh, float* __restrict__ fl,
-                                                  float* __restrict__ viol, const int* __restrict__ stop) {
+                                                  float* __restrict__ viol, const int* __restrict__ stop,
+                                                  const int* __restrict__ skip_if_fast) {
   if (stop && *stop) return;
-  constexpr int RPC = 256 / TPR;
-  __shared__ float smm[8], sms[8];
-  const int grp = threadIdx.x / TPR, tid = threadIdx.x % TPR;
-  const double l2e_eps = GW_LOG2E / eps;
-  float vmax = 0.f;
-  for (int64_t row0 = (int64_t)blockIdx.x * RPC; row0 < nl; row0 += (int64_t)gridDim.x * RPC) {
-    const int64_t row = row0 + grp;
-    const bool rv = row < nl;
-    LSE2 st{-INFINITY, 0.f};
-    if (rv) {
-      const float* gr = G + row * ld;
-      for (int64_t q = 8 * (int64_t)tid; q < m; q += 8 * TPR) {
-        float4 x0 = __ldcs(reinterpret_cast<const float4*>(gr + q));
+  if (skip_if_fast && *skip_if_fast) return;
+  __shared__ float smm[RROWS][8], sms[RROWS][8];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t r0 = (int64_t)blockIdx.x * RROWS;
+  const int nr = (int)min((int64_t)RROWS, nl - r0);
+  if (nr <= 0) return;
+  LSE2 st[RROWS];
+#pragma unroll
+  for (int r = 0; r < RROWS; ++r) st[r] = LSE2{-INFINITY, 0.f};
+  for (int64_t q = 8 * (int64_t)threadIdx.x; q < m; q += 8 * 256) {
+    float hv[8], lv[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const bool v = q + k < m;
+      hv[k] = v ? gh[q + k] : -INFINITY;
+      lv[k] = v ? gl[q + k] : 0.f;
+    }
+#pragma unroll
+    for (int r = 0; r < RROWS; ++r) {
+      if (r < nr) {
+        const float* gr = G + (r0 + r) * ld + q;
+        const float4 x0 = __ldcs(reinterpret_cast<const float4*>(gr));
         float4 x1 = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (q + 4 < m) x1 = __ldcs(reinterpret_cast<const float4*>(gr + q + 4));
+        if (q + 4 < m) x1 = __ldcs(reinterpret_cast<const float4*>(gr + 4));
         const float gv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
         float av[8];
         float cm = -INFINITY;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          av[k] = (q + k < m) ? fmaf(gv[k], -c2f, gh[q + k]) + gl[q + k] : -INFINITY;
+          av[k] = (q + k < m) ? fmaf(gv[k], -c2f, hv[k]) + lv[k] : -INFINITY;
           cm = fmaxf(cm, av[k]);
         }
-        if (cm > st.m) {
-          st.s = (st.m == -INFINITY) ? 0.f : st.s * exp2f(st.m - cm);
-          st.m = cm;
+        LSE2 s = st[r];
+        if (cm > s.m) {
+          s.s = (s.m == -INFINITY) ? 0.f : s.s * exp2f(s.m - cm);
+          s.m = cm;
         }
-        if (st.m != -INFINITY) {
+        if (s.m != -INFINITY) {
           float acc = 0.f;
 #pragma unroll
-          for (int k = 0; k < 8; ++k) acc += exp2f(av[k] - st.m);
-          st.s += acc;
+          for (int k = 0; k < 8; ++k) acc += exp2f(av[k] - s.m);
+          s.s += acc;
         }
-      }
-    }
-    if (TPR == 32) {
-      st = lse_warp(st);
-    } else {
-      st = lse_warp(st);
-      if ((threadIdx.x & 31) == 0) { smm[threadIdx.x >> 5] = st.m; sms[threadIdx.x >> 5] = st.s; }
-      __syncthreads();
-      st = LSE2{smm[0], sms[0]};
-      for (int k = 1; k < 8; ++k) st = lse_merge(st, LSE2{smm[k], sms[k]});
-      __syncthreads();
-    }
-    if (rv && tid == 0) {
-      const double lse2 = (double)st.m + log2((double)st.s);
-      const double fo = fcur[row];
-      const double fn = (lp[row] == -INFINITY) ? -INFINITY : eps * lp[row] - eps * GW_LN2 * lse2;
-      fout[row] = fn;
-      const double fs = fn * l2e_eps;
-      const float h = (float)fs;
-      fh[row] = h;
-      fl[row] = isfinite(fs) ? (float)(fs - (double)h) : 0.f;
-      if (viol) {
-        const double pi = exp(lp[row]);
-        double v = (pi > 0.0) ? pi * fabs(exp2((fo - fn) * l2e_eps) - 1.0) : 0.0;
-        if (!(v == v)) v = 3.0e38;
-        vmax = fmaxf(vmax, (float)fmin(v, 3.0e38));
+        st[r] = s;
       }
     }
   }
-  if (viol) {
-    vmax = warp_max(vmax);
-    if ((threadIdx.x & 31) == 0 && vmax > 0.f) atomic_max_nonneg(viol, vmax);
+#pragma unroll
+  for (int r = 0; r < RROWS; ++r) {
+    LSE2 s = lse_warp(st[r]);
+    if (lane == 0) { smm[r][w] = s.m; sms[r][w] = s.s; }
+  }
+  __syncthreads();
+  if (threadIdx.x < nr) {
+    const int r = threadIdx.x;
+    const int64_t row = r0 + r;
+    LSE2 s{smm[r][0], sms[r][0]};
+    for (int k = 1; k < 8; ++k) s = lse_merge(s, LSE2{smm[r][k], sms[r][k]});
+    const double l2e_eps = GW_LOG2E / eps;
+    const double lse2 = (double)s.m + log2((double)s.s);
+    const double fo = fcur[row];
+    const double fn = (lp[row] == -INFINITY) ? -INFINITY : eps * lp[row] - eps * GW_LN2 * lse2;
+    fout[row] = fn;
+    const double fs = fn * l2e_eps;
+    const float h = (float)fs;
+    fh[row] = h;
+    fl[row] = isfinite(fs) ? (float)(fs - (double)h) : 0.f;
+    if (viol) {
+      const double pi = exp(lp[row]);
+      double v = (pi > 0.0) ? pi * fabs(exp2((fo - fn) * l2e_eps) - 1.0) : 0.0;
+      if (!(v == v)) v = 3.0e38;
+      atomic_max_nonneg(viol, (float)fmin(v, 3.0e38));
+    }
   }
 }
 
@@ -101,8 +114,9 @@ __global__ void __launch_bounds__(256) k_sink_row(const float* __restrict__ G, i
 __global__ void __launch_bounds__(256) k_sink_col(const float* __restrict__ G, int64_t ld, int64_t nl, int64_t m,
                                                   const float* __restrict__ fh, const float* __restrict__ fl,
                                                   float c2f, int64_t RB, float2* __restrict__ part,
-                                                  const int* __restrict__ stop) {
+                                                  const int* __restrict__ stop, const int* __restrict__ skip_if_fast) {
   if (stop && *stop) return;
+  if (skip_if_fast && *skip_if_fast) return;
   const int64_t q0 = ((int64_t)blockIdx.x * 256 + threadIdx.x) * 4;
   if (q0 >= m) return;
   const int64_t rb = blockIdx.y;
@@ -158,11 +172,12 @@ __global__ void __launch_bounds__(256) k_sink_col(const float* __restrict__ G, i
 // Column half-step, pass 2: merge the row-block partials in fixed order and update g.
 __global__ void k_sink_colfin(const float2* __restrict__ part, int nrb, int64_t m, const double* __restrict__ lq,
                               double eps, double* __restrict__ g, float* __restrict__ gh, float* __restrict__ gl,
-                              const int* __restrict__ stop) {
+                              const int* __restrict__ stop, const int* __restrict__ skip_if_fast,
+                              float* __restrict__ dev) {
   if (stop && *stop) return;
+  if (skip_if_fast && *skip_if_fast) return;
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (q >= m) return;
-  LSE2 st{-INFINITY, 0.f};
   // fp64 merge for accuracy
   double M = -INFINITY;
   for (int rb = 0; rb < nrb; ++rb) M = fmax(M, (double)part[(int64_t)rb * m + q].x);
@@ -172,9 +187,15 @@ __global__ void k_sink_colfin(const float2* __restrict__ part, int nrb, int64_t 
       const float2 v = part[(int64_t)rb * m + q];
       if (v.x != -INFINITY) S += (double)v.y * exp2((double)v.x - M);
     }
-  (void)st;
   const double lse2 = M + log2(S);
   const double gn = (lq[q] == -INFINITY) ? -INFINITY : eps * lq[q] - eps * GW_LN2 * lse2;
+  if (dev) {  // |log2(colsum / q)| of the half-step plan: decides the next iteration's path
+    double d = fabs((gn - g[q]) * (GW_LOG2E / eps));
+    if (!(d == d)) d = 3.0e38;
+    float dv = (float)fmin(d, 3.0e38);
+    dv = warp_max(dv);
+    if ((threadIdx.x & 31) == 0) atomic_max_nonneg(dev, dv);
+  }
   g[q] = gn;
   const double gs = gn * (GW_LOG2E / eps);
   const float h = (float)gs;
