@@ -9,25 +9,22 @@
 // so every element of G is read ONCE per iteration and exponentiated ONCE.
 //
 // Layout: a thread-block cluster of CL CTAs spans a row (CTA rank r owns columns
-// [r W, (r+1) W), W = 4 K FT); clusters own contiguous row ranges.  Per row:
+// [r W, (r+1) W), W = 4 K NT); clusters own contiguous row ranges.  Per row:
 //   TMA bulk copy (cp.async.bulk, mbarrier complete_tx) of the CTA's row slice into a
-//   FSTAGES-deep shared-memory ring -> e values in registers -> CTA partial of S_i ->
-//   DSMEM store of the partial into every peer CTA (mapa + st.shared::cluster) ->
-//   split cluster barrier (arrive.release now, wait.acquire one row later, so the exchange
-//   latency hides behind the next row) -> S_i (fixed rank order: identical in all CTAs)
-//   -> column accumulation e_ip w_i (fp32 per 32 rows, then fp64).
+//   FSTAGES-deep shared-memory ring -> e values in registers (packed fp32x2 FFMA2/FADD2,
+//   MUFU.EX2) -> warp partial of S_i -> st.async of the partial into every peer CTA
+//   (complete_tx on the receiver's slot mbarrier) -> consumed one row later, so the exchange
+//   latency hides behind the next row -> S_i (fixed order: identical in all warps and CTAs)
+//   -> column accumulation e_ip w_i (fp32 per FFLUSH rows, then fp64 in shared memory).
 // Column partials per cluster -> part[cluster][col] (fp64), merged in fixed order by
-// k_sink_colfin_fast: deterministic, no float atomics.
+// k_sink_fin_fast: deterministic, no float atomics.
 #pragma once
 #include "common.cuh"
 
 namespace gw {
 
-constexpr int FT = 512;       // threads per CTA
-constexpr int FNW = FT / 32;  // warps per CTA
-constexpr int FSTAGES = 4;    // TMA ring depth (rows)
-constexpr int FFLUSH = 32;    // rows between fp32 -> fp64 column-accumulator flushes
-constexpr int FPF = 8;        // L2 prefetch distance (rows) beyond the shared-memory ring
+constexpr int FSTAGES = 5;             // TMA ring depth (rows)
+constexpr int FFLUSH = 32;             // rows between fp32 -> fp64 column-accumulator flushes
 
 struct FusedArgs {
   const float* G;
@@ -41,6 +38,7 @@ struct FusedArgs {
   float* Srow;                // out: S_i = row sums of the plan entering the iteration
   double* part;               // [nclusters][m] column sums of the half-step plan
   int64_t rows_per_cluster;
+  int l2_ahead;               // rows beyond the ring to prefetch into L2 (0: none)
   const int* mode;            // run only if *mode == 1
   const int* stop;
 };
@@ -76,6 +74,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!P bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
 }
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -116,73 +125,103 @@ __device__ __forceinline__ void st_async_f32(uint32_t raddr, float v, uint32_t r
                "r"(__float_as_uint(v)), "r"(rbar)
                : "memory");
 }
-// fixed-order warp sum (tree to lane 0, then broadcast): bit-identical in every lane and warp
-__device__ __forceinline__ float warp_sum_fixed(float v) {
+// Butterfly warp sum: every lane ends with the same bits (each step adds the same two values,
+// only in commuted order), so lanes 0..CL-1 can send identical partials to the CL ranks.
+__device__ __forceinline__ float warp_sum_bfly(float v) {
 #pragma unroll
-  for (int d = 16; d > 0; d >>= 1) v += __shfl_down_sync(0xffffffffu, v, d);
-  return __shfl_sync(0xffffffffu, v, 0);
+  for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+  return v;
 }
 
-// dynamic shared memory: the TMA ring [FSTAGES][W] fp32 + fp64 column accumulators [W]
-template <int K>
+// packed fp32x2 arithmetic (sm_100: FFMA2 / FADD2 -- two lanes per instruction)
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+
+// W = 4 K NT columns per CTA.  Dynamic shared memory: the TMA ring [FSTAGES][W] fp32, then the
+// fp64 column accumulators [K][4][NT] (conflict-free: lane-contiguous doubles).
+template <int K, int NT>
 constexpr size_t fused_dyn_smem() {
-  return (size_t)FSTAGES * 4 * K * FT * sizeof(float) + (size_t)4 * K * FT * sizeof(double);
+  return (size_t)FSTAGES * 4 * K * NT * sizeof(float) + (size_t)4 * K * NT * sizeof(double);
 }
 
-// Per row, no CTA-wide barrier: every warp (a) exponentiates its 4K columns from the ring
-// stage, (b) releases the stage (empty mbarrier), (c) sends its partial of S_i to every
-// cluster rank with st.async (complete_tx on the receiver's slot mbarrier), then (d) waits
-// for the previous row's CL x FNW partials, reduces them in a fixed order (bit-identical in
-// every warp of every CTA) and accumulates e_ip w_i for its columns.  Warp 0 lane 0 refills
-// ring stages one row behind and prefetches FPF further rows into L2.
-//
-// Exponent (log2 units): a = fma(G_ip, -log2e/eps, gh_p) + F_i with the fp32 hi parts of the
-// scaled duals only: the fma carries the one rounding of the large terms and "+ F" cancels
-// exactly.  Dropping the lo parts (|lo| <= ulp/2 ~ 2^-20 relative) biases each row by 2^{Fl_i}
-// and each column by 2^{gl_p}; the row / column normalisations of the iteration absorb both, so
-// the fp64 duals' plan differs from the fixed point by <= 2^-19 relative per entry (marginal
-// violation ~1e-5 * p_i).
-template <int K, bool FULL>
-__device__ __forceinline__ float fused_exp_row(const float4* __restrict__ st, const float (&ghv)[K][4], float c2f,
-                                               float F, float (&ec)[K][4], int t, int64_t c0, int64_t m) {
-  float ps[4] = {0.f, 0.f, 0.f, 0.f};
+// Exponentiate one row slice: e = 2^(fma(G, -log2e/eps, gh) + F) for the thread's 4K columns
+// (K float4 from the ring stage), packed fp32x2; returns the thread's partial row sum (pairwise
+// tree, so the dependent-add chain is log2(K) deep instead of K).
+template <int K, int NT, bool FULL>
+__device__ __forceinline__ float fused_exp_row(const float4* __restrict__ sp, const float2 (&ghv)[K][2], float2 nc2,
+                                               float2 F2, float2 (&ec)[K][2], int t, int64_t c0, int64_t m) {
+  float2 ps[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) {
-    const float4 gv = st[t + FT * k];
-    const float g4[4] = {gv.x, gv.y, gv.z, gv.w};
-#pragma unroll
-    for (int jj = 0; jj < 4; ++jj) {
-      float e = ex2_ftz(fmaf(g4[jj], -c2f, ghv[k][jj]) + F);
-      if (!FULL && c0 + 4 * (t + FT * k) + jj >= m) e = 0.f;
-      ec[k][jj] = e;
-      ps[jj] += e;
+    const float4 gv = sp[t + NT * k];
+    const float2 a0 = fadd2(ffma2(make_float2(gv.x, gv.y), nc2, ghv[k][0]), F2);
+    const float2 a1 = fadd2(ffma2(make_float2(gv.z, gv.w), nc2, ghv[k][1]), F2);
+    float2 e0 = make_float2(ex2_ftz(a0.x), ex2_ftz(a0.y));
+    float2 e1 = make_float2(ex2_ftz(a1.x), ex2_ftz(a1.y));
+    if (!FULL) {
+      const int64_t col = c0 + 4 * (t + NT * k);
+      if (col >= m) e0.x = 0.f;
+      if (col + 1 >= m) e0.y = 0.f;
+      if (col + 2 >= m) e1.x = 0.f;
+      if (col + 3 >= m) e1.y = 0.f;
     }
+    ec[k][0] = e0;
+    ec[k][1] = e1;
+    ps[k] = fadd2(e0, e1);
   }
-  return (ps[0] + ps[1]) + (ps[2] + ps[3]);
+#pragma unroll
+  for (int w = 1; w < K; w <<= 1)
+#pragma unroll
+    for (int k = 0; k + w < K; k += 2 * w) ps[k] = fadd2(ps[k], ps[k + w]);
+  return ps[0].x + ps[0].y;
 }
 
-template <int K, int CL>
-struct FusedCtx {
-  static constexpr int W = 4 * K * FT;
-  static constexpr int NSLOT = 4;           // exchange slots (power of 2)
-  static constexpr int NX = CL * FNW;       // partials per row
-};
-
-template <int K, int CL>
-__global__ void __launch_bounds__(FT, 1) k_sink_fused(FusedArgs a) {
+// One CTA = NT threads (NT/32 warps), each owning 4K columns (K float4 per row).  Per row j and
+// without any CTA-wide barrier every warp (a) exponentiates its columns from the ring stage,
+// (b) releases the stage -- the LAST warp to release it (shared counter) refills it by TMA with
+// the row FSTAGES further on, so FSTAGES-1 rows stay in flight whatever the warps' relative
+// progress -- (c) sends its partial of S_j to every cluster rank with st.async, then (d) waits
+// for row j-1's CL x NW partials, reduces them in a fixed order (bit-identical in every warp
+// of every CTA) and accumulates e_{j-1,p} w_{j-1}.
+//
+// Exponent (log2 units): a = fma(G_ip, -log2e/eps, gh_p) + F_i with the fp32 hi parts of the
+// scaled duals only (reading R30): the fma carries the one rounding of the large terms and
+// "+ F" cancels exactly; the dropped lo parts are per-row / per-column scalings that the
+// iteration's normalisations absorb.
+template <int K, int CL, int NT>
+__global__ void __launch_bounds__(NT, 1) k_sink_fused(FusedArgs a) {
   if (*a.mode != 1 || (a.stop && *a.stop)) return;  // uniform across the cluster
-  constexpr int W = FusedCtx<K, CL>::W;
-  constexpr int NSLOT = FusedCtx<K, CL>::NSLOT;
-  constexpr int NX = FusedCtx<K, CL>::NX;
-  extern __shared__ __align__(128) float ring[];  // [FSTAGES][W], then acc64 [W] (fp64)
+  constexpr int NW = NT / 32;
+  constexpr int W = 4 * K * NT;
+  constexpr int NSLOT = 4;       // exchange slots (power of 2)
+  constexpr int NX = CL * NW;    // partials per row
+  extern __shared__ __align__(128) float ring[];  // [FSTAGES][W], then acc64 [K][4][NT] (fp64)
   double* acc64 = reinterpret_cast<double*>(ring + (size_t)FSTAGES * W);
-  __shared__ __align__(8) uint64_t full[FSTAGES], empty[FSTAGES];
+  __shared__ __align__(8) uint64_t full[FSTAGES];
+  __shared__ unsigned int scnt[FSTAGES];
   __shared__ __align__(8) uint64_t xbar[NSLOT];
-  __shared__ __align__(16) float xs[NSLOT][NX];  // [slot][rank * FNW + warp]
+  __shared__ __align__(16) float xs[NSLOT][NX];  // [slot][rank * NW + warp]
 
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
-  const uint32_t cr = cluster_rank();
-  const int64_t cid = cluster_id();
+  // 1-D grid of 1-D clusters: rank and cluster index from blockIdx (provably warp-uniform)
+  const uint32_t cr = blockIdx.x % CL;
+  const int64_t cid = blockIdx.x / CL;
   const int64_t m = a.m;
   const int64_t c0 = (int64_t)cr * W;
   const int64_t ncol = max((int64_t)0, min((int64_t)W, m - c0));  // valid columns of this CTA
@@ -191,25 +230,13 @@ __global__ void __launch_bounds__(FT, 1) k_sink_fused(FusedArgs a) {
   const int64_t re = min(a.nl, rb + a.rows_per_cluster);
   const int nrows = (int)max((int64_t)0, re - rb);
   constexpr uint32_t xbytes = 4u * NX;
-  const float* __restrict__ fh = a.fh + rb;
-  const float* __restrict__ pf = a.pf + rb;
-  float* __restrict__ Srow = a.Srow + rb;
   const float* __restrict__ Gbase = a.G + rb * a.ld + c0;
   const int64_t ld = a.ld;
 
-  float ghv[K][4];
-  const bool full_tile = (ncol == W);
-#pragma unroll
-  for (int k = 0; k < K; ++k)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int64_t col = c0 + 4 * (t + FT * k) + j;
-      ghv[k][j] = col < m ? a.gh[col] : 0.f;
-    }
   if (t == 0) {
     for (int s = 0; s < FSTAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], FNW);
+      scnt[s] = 0u;
     }
     for (int s = 0; s < NSLOT; ++s) mbar_init(&xbar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -218,63 +245,85 @@ __global__ void __launch_bounds__(FT, 1) k_sink_fused(FusedArgs a) {
   __syncthreads();
   cluster_arrive();
   cluster_wait();  // every CTA's barriers are initialised and armed before any DSMEM traffic
+
   if (t == 0 && bytes > 0) {
-    for (int s = 0; s < FSTAGES && s < nrows; ++s) {
-      mbar_expect_tx(&full[s], bytes);
-      tma_load_1d(ring + (size_t)s * W, Gbase + (int64_t)s * ld, bytes, &full[s]);
+    for (int r = 0; r < FSTAGES && r < nrows; ++r) {
+      mbar_expect_tx(&full[r], bytes);
+      tma_load_1d(ring + (size_t)r * W, Gbase + (int64_t)r * ld, bytes, &full[r]);
     }
-    for (int r = FSTAGES; r < FSTAGES + FPF && r < nrows; ++r) prefetch_l2_bulk(Gbase + (int64_t)r * ld, bytes);
+    for (int r = FSTAGES; r < FSTAGES + a.l2_ahead && r < nrows; ++r) prefetch_l2_bulk(Gbase + (int64_t)r * ld, bytes);
   }
+  const float* __restrict__ fh = a.fh + rb;
+  const float* __restrict__ pf = a.pf + rb;
+  float* __restrict__ Srow = a.Srow + rb;
   // lane c < CL of every warp sends to rank c: remote address of this warp's slot-0 entry and
   // of the slot-0 barrier (slot s sits at a fixed byte offset from slot 0 in every CTA)
   const uint32_t peer = (uint32_t)min(lane, CL - 1);
-  const uint32_t rx0 = mapa(&xs[0][cr * FNW + wid], peer), rb0 = mapa(&xbar[0], peer);
+  const uint32_t rx0 = mapa(&xs[0][cr * NW + wid], peer), rb0 = mapa(&xbar[0], peer);
   constexpr uint32_t XSTRIDE = sizeof(xs[0]), BSTRIDE = sizeof(uint64_t);
-  float acc32[K][4];
+  const bool full_tile = (ncol == W);
+
+  float2 ghv[K][2], acc[K][2];
 #pragma unroll
   for (int k = 0; k < K; ++k)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) { acc32[k][j] = 0.f; acc64[4 * (t + FT * k) + j] = 0.0; }
-  const float c2f = a.c2f;
-  float eA[K][4], eB[K][4];
+    for (int h = 0; h < 2; ++h) {
+      const int64_t col = c0 + 4 * (t + NT * k) + 2 * h;
+      ghv[k][h].x = col < m ? a.gh[col] : 0.f;
+      ghv[k][h].y = col + 1 < m ? a.gh[col + 1] : 0.f;
+      acc[k][h] = make_float2(0.f, 0.f);
+      acc64[(k * 4 + 2 * h) * NT + t] = 0.0;
+      acc64[(k * 4 + 2 * h + 1) * NT + t] = 0.0;
+    }
+  const float2 nc2 = make_float2(-a.c2f, -a.c2f);
+  float2 eA[K][2], eB[K][2];
   float pA = 0.f, pB = 0.f;
+  // the row's dual and marginal are loaded one row ahead (their L2 latency would otherwise sit on
+  // every row's critical path)
+  float Fnx = nrows > 0 ? fh[0] : 0.f, pnx = nrows > 0 ? pf[0] : 0.f;
 
-  // one row: exponentiate + send (row j), then consume the previous row (j - 1)
-  auto step = [&](int j, float (&ecur)[K][4], float& pcur, float (&eprv)[K][4], float pprv) {
-    const int st = j & (FSTAGES - 1);
+  // Step j: exponentiate row j and send its partial row sums, then consume row j-1 (its
+  // partials were sent one step ago, so the exchange latency hides behind row j's work).
+  auto step = [&](int j, float2 (&ecur)[K][2], float& pcur, float2 (&eprv)[K][2], float pprv) {
     if (j < nrows) {
-      const float F = fh[j];
-      pcur = pf[j];
+      const int st = j % FSTAGES;
+      const float F = Fnx;
+      pcur = pnx;
+      if (j + 1 < nrows) {
+        Fnx = fh[j + 1];
+        pnx = pf[j + 1];
+      }
       float psum = 0.f;
       if (bytes > 0) {
         mbar_wait(&full[st], (uint32_t)((j / FSTAGES) & 1));
         const float4* sp = reinterpret_cast<const float4*>(ring + (size_t)st * W);
-        psum = full_tile ? fused_exp_row<K, true>(sp, ghv, c2f, F, ecur, t, c0, m)
-                         : fused_exp_row<K, false>(sp, ghv, c2f, F, ecur, t, c0, m);
+        psum = full_tile ? fused_exp_row<K, NT, true>(sp, ghv, nc2, make_float2(F, F), ecur, t, c0, m)
+                         : fused_exp_row<K, NT, false>(sp, ghv, nc2, make_float2(F, F), ecur, t, c0, m);
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with stage st
+        if (lane == 0) {  // this warp is done with stage st; the last one refills it
+          const int nxt = j + FSTAGES;
+          if (atomicAdd(&scnt[st], 1u) == NW - 1) {
+            scnt[st] = 0u;
+            if (nxt < nrows) {
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              mbar_expect_tx(&full[st], bytes);
+              tma_load_1d(ring + (size_t)st * W, Gbase + (int64_t)nxt * ld, bytes, &full[st]);
+              if (a.l2_ahead > 0 && nxt + a.l2_ahead < nrows)
+                prefetch_l2_bulk(Gbase + (int64_t)(nxt + a.l2_ahead) * ld, bytes);
+            }
+          }
+        }
       } else {
 #pragma unroll
-        for (int k = 0; k < K; ++k)
-#pragma unroll
-          for (int jj = 0; jj < 4; ++jj) ecur[k][jj] = 0.f;
+        for (int k = 0; k < K; ++k) { ecur[k][0] = make_float2(0.f, 0.f); ecur[k][1] = ecur[k][0]; }
       }
-      psum = warp_sum_fixed(psum);
+      psum = warp_sum_bfly(psum);
       const int xsl = j & (NSLOT - 1);
       if (lane < CL) st_async_f32(rx0 + XSTRIDE * xsl, psum, rb0 + BSTRIDE * xsl);
     }
     if (j > 0) {
       const int jp = j - 1;
-      // warp 0 lane 0 refills the stage of row j-1 with row j-1+FSTAGES (+ L2 prefetch)
-      if (t == 0 && bytes > 0 && jp + FSTAGES < nrows) {
-        const int rs = jp & (FSTAGES - 1);
-        mbar_wait(&empty[rs], (uint32_t)((jp / FSTAGES) & 1));
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&full[rs], bytes);
-        tma_load_1d(ring + (size_t)rs * W, Gbase + (int64_t)(jp + FSTAGES) * ld, bytes, &full[rs]);
-        if (jp + FSTAGES + FPF < nrows) prefetch_l2_bulk(Gbase + (int64_t)(jp + FSTAGES + FPF) * ld, bytes);
-      }
-      // row j-1: wait for its CL x FNW partials and reduce them in a fixed order
+      // row j-1: wait for its CL x NW partials and reduce them in a fixed order
       const int psl = jp & (NSLOT - 1);
       mbar_wait(&xbar[psl], (uint32_t)((jp / NSLOT) & 1));
       float S = 0.f;
@@ -284,23 +333,26 @@ __global__ void __launch_bounds__(FT, 1) k_sink_fused(FusedArgs a) {
       } else {
         S = lane < NX ? xs[psl][lane] : 0.f;
       }
-      S = warp_sum_fixed(S);
+      S = warp_sum_bfly(S);
       if (t == 0) {
         Srow[jp] = S;
         if (jp + NSLOT < nrows) mbar_expect_tx(&xbar[psl], xbytes);  // the slot now serves row j+3
       }
       const float wv = pprv * rcp_ftz(S);
+      const float2 w2 = make_float2(wv, wv);
 #pragma unroll
-      for (int k = 0; k < K; ++k)
-#pragma unroll
-        for (int jj = 0; jj < 4; ++jj) acc32[k][jj] = fmaf(eprv[k][jj], wv, acc32[k][jj]);
-      if ((j & (FFLUSH - 1)) == 0) {
+      for (int k = 0; k < K; ++k) {
+        acc[k][0] = ffma2(eprv[k][0], w2, acc[k][0]);
+        acc[k][1] = ffma2(eprv[k][1], w2, acc[k][1]);
+      }
+      if ((jp & (FFLUSH - 1)) == FFLUSH - 1) {
 #pragma unroll
         for (int k = 0; k < K; ++k)
 #pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
-            acc64[4 * (t + FT * k) + jj] += (double)acc32[k][jj];
-            acc32[k][jj] = 0.f;
+          for (int h = 0; h < 2; ++h) {
+            acc64[(k * 4 + 2 * h) * NT + t] += (double)acc[k][h].x;
+            acc64[(k * 4 + 2 * h + 1) * NT + t] += (double)acc[k][h].y;
+            acc[k][h] = make_float2(0.f, 0.f);
           }
       }
     }
@@ -313,10 +365,12 @@ __global__ void __launch_bounds__(FT, 1) k_sink_fused(FusedArgs a) {
 #pragma unroll
   for (int k = 0; k < K; ++k)
 #pragma unroll
-    for (int jj = 0; jj < 4; ++jj) {
-      const double v = acc64[4 * (t + FT * k) + jj] + (double)acc32[k][jj];
-      const int64_t col = c0 + 4 * (t + FT * k) + jj;
-      if (col < m) a.part[cid * m + col] = v;
+    for (int h = 0; h < 2; ++h) {
+      const int64_t col = c0 + 4 * (t + NT * k) + 2 * h;
+      const double v0 = acc64[(k * 4 + 2 * h) * NT + t] + (double)acc[k][h].x;
+      const double v1 = acc64[(k * 4 + 2 * h + 1) * NT + t] + (double)acc[k][h].y;
+      if (col < m) a.part[cid * m + col] = v0;
+      if (col + 1 < m) a.part[cid * m + col + 1] = v1;
     }
   // no CTA may exit while a peer can still address its shared memory
   cluster_arrive();

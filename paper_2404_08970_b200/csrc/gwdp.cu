@@ -468,18 +468,18 @@ struct SinkState {
   double* fpart;  // [ncl][m]
   float* Srow;    // [nl]
   float* pf;      // [nl] p as fp32
-  int fK = 0, fCL = 0, fncl = 0;  // fK == 0: fast path unavailable for this shape
+  int fK = 0, fCL = 0, fNT = 256, fncl = 0;  // fK == 0: fast path unavailable for this shape
   int64_t frpc = 0;
 };
 
-template <int K, int CL>
+template <int K, int CL, int NT>
 static gw_status fused_config_t(gw_ctx* c, int* ncl) {
-  auto kern = k_sink_fused<K, CL>;
-  const size_t dsm = fused_dyn_smem<K>();
+  auto kern = k_sink_fused<K, CL, NT>;
+  const size_t dsm = fused_dyn_smem<K, NT>();
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(148 * CL);
-  cfg.blockDim = dim3(FT);
+  cfg.blockDim = dim3(NT);
   cfg.dynamicSmemBytes = dsm;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -490,36 +490,44 @@ static gw_status fused_config_t(gw_ctx* c, int* ncl) {
   return GW_OK;
 }
 
-template <int K, int CL>
+template <int K, int CL, int NT>
 static gw_status fused_launch_t(gw_ctx* c, const FusedArgs& fa, int ncl) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(ncl * CL);
-  cfg.blockDim = dim3(FT);
-  cfg.dynamicSmemBytes = fused_dyn_smem<K>();
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = fused_dyn_smem<K, NT>();
   cfg.stream = c->stream;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  CU(cudaLaunchKernelEx(&cfg, k_sink_fused<K, CL>, fa));
+  CU(cudaLaunchKernelEx(&cfg, k_sink_fused<K, CL, NT>, fa));
   return GW_OK;
 }
 
-// (K, CL) dispatch: K in 1..4 with CL = 1 (m <= 8192), K = 4 with CL in {2, 4, 8}
+// (K, CL, NT) dispatch: W = 4 K NT columns per CTA (W <= 8192); one cluster of CL CTAs spans a row.
+//   NT = 256: K in {1, 2, 4, 8} with CL = 1, K = 8 with CL in {2, 4, 8}
+//   NT = 512: K in {1, 2, 4} with CL = 1, K = 4 with CL in {2, 4, 8}
 #define FUSED_DISPATCH(FN, ...)                                                   \
-  switch (K * 16 + CL) {                                                          \
-    case 1 * 16 + 1: return FN<1, 1>(__VA_ARGS__);                                \
-    case 2 * 16 + 1: return FN<2, 1>(__VA_ARGS__);                                \
-    case 3 * 16 + 1: return FN<3, 1>(__VA_ARGS__);                                \
-    case 4 * 16 + 1: return FN<4, 1>(__VA_ARGS__);                                \
-    case 4 * 16 + 2: return FN<4, 2>(__VA_ARGS__);                                \
-    case 4 * 16 + 4: return FN<4, 4>(__VA_ARGS__);                                \
-    case 4 * 16 + 8: return FN<4, 8>(__VA_ARGS__);                                \
-    default: return fail(GW_ERR_UNSUPPORTED, "fused path: no instance K=%d CL=%d", K, CL); \
+  switch ((NT / 256) * 256 + K * 16 + CL) {                                       \
+    case 256 + 1 * 16 + 1: return FN<1, 1, 256>(__VA_ARGS__);                     \
+    case 256 + 2 * 16 + 1: return FN<2, 1, 256>(__VA_ARGS__);                     \
+    case 256 + 4 * 16 + 1: return FN<4, 1, 256>(__VA_ARGS__);                     \
+    case 256 + 8 * 16 + 1: return FN<8, 1, 256>(__VA_ARGS__);                     \
+    case 256 + 8 * 16 + 2: return FN<8, 2, 256>(__VA_ARGS__);                     \
+    case 256 + 8 * 16 + 4: return FN<8, 4, 256>(__VA_ARGS__);                     \
+    case 256 + 8 * 16 + 8: return FN<8, 8, 256>(__VA_ARGS__);                     \
+    case 512 + 1 * 16 + 1: return FN<1, 1, 512>(__VA_ARGS__);                     \
+    case 512 + 2 * 16 + 1: return FN<2, 1, 512>(__VA_ARGS__);                     \
+    case 512 + 4 * 16 + 1: return FN<4, 1, 512>(__VA_ARGS__);                     \
+    case 512 + 4 * 16 + 2: return FN<4, 2, 512>(__VA_ARGS__);                     \
+    case 512 + 4 * 16 + 4: return FN<4, 4, 512>(__VA_ARGS__);                     \
+    case 512 + 4 * 16 + 8: return FN<4, 8, 512>(__VA_ARGS__);                     \
+    default: return fail(GW_ERR_UNSUPPORTED, "fused path: no instance K=%d CL=%d NT=%d", K, CL, NT); \
   }
-static gw_status fused_config(gw_ctx* c, int K, int CL, int* ncl) { FUSED_DISPATCH(fused_config_t, c, ncl) }
-static gw_status fused_launch(gw_ctx* c, int K, int CL, const FusedArgs& fa, int ncl) {
+static gw_status fused_config(gw_ctx* c, int K, int CL, int NT, int* ncl) { FUSED_DISPATCH(fused_config_t, c, ncl) }
+static gw_status fused_launch(gw_ctx* c, int K, int CL, int NT, const FusedArgs& fa, int ncl) {
   FUSED_DISPATCH(fused_launch_t, c, fa, ncl)
 }
 
@@ -538,7 +546,7 @@ static gw_status sink_alloc(gw_ctx* c, const Prepared& P, SinkState& s) {
   s.RB = RB;
   s.nrb = (int)std::max<int64_t>(1, (P.nl + RB - 1) / RB);
   TRY(ws(c, c->part, (size_t)s.nrb * P.m, &s.part));
-  // fused fast path: cluster of CL CTAs x W = 2048 K columns spans a row
+  // fused fast path: cluster of CL CTAs x W = 1024 K columns spans a row
   int* md;
   TRY(ws(c, c->mode, 4, &md));
   s.mode = md;
@@ -546,17 +554,27 @@ static gw_status sink_alloc(gw_ctx* c, const Prepared& P, SinkState& s) {
   s.fK = 0;
   const char* env = getenv("GWDP_NO_FUSED");
   if (!(env && env[0] == '1') && P.nl > 0) {
+    const char* nte = getenv("GWDP_FUSED_NT");
+    const int NT = (nte && atoi(nte) == 256) ? 256 : 512;
+    const int kmax = 8192 / (4 * NT);  // K at W = 8192 columns per CTA
     int K, CL;
-    if (P.m <= 8192) { K = (int)((P.m + 2047) / 2048); CL = 1; }
-    else { K = 4; CL = (int)((P.m + 8191) / 8192); }
+    if (P.m <= 8192) {
+      K = (int)((P.m + 4 * NT - 1) / (4 * NT));
+      K = K <= 1 ? 1 : K <= 2 ? 2 : K <= 4 ? 4 : 8;
+      if (K > kmax) K = kmax;
+      CL = 1;
+    } else {
+      K = kmax;
+      CL = (int)((P.m + 8191) / 8192);
+    }
     if (CL == 3) CL = 4;
     if (CL > 4 && CL < 8) CL = 8;
     if (CL <= 8) {
       int ncl = 0;
-      TRY(fused_config(c, K, CL, &ncl));
+      TRY(fused_config(c, K, CL, NT, &ncl));
       if (ncl > 0) {
         ncl = (int)std::min<int64_t>(ncl, P.nl);
-        s.fK = K; s.fCL = CL; s.fncl = ncl;
+        s.fK = K; s.fCL = CL; s.fNT = NT; s.fncl = ncl;
         s.frpc = (P.nl + ncl - 1) / ncl;
         TRY(ws(c, c->fpart, (size_t)ncl * P.m, &s.fpart));
         TRY(ws(c, c->srow, (size_t)P.nl, &s.Srow));
@@ -596,6 +614,10 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
   fa.G = G; fa.ld = ldG; fa.nl = nl; fa.m = m; fa.c2f = c2f; fa.gh = s.gh; fa.gl = s.gl; fa.fh = s.fh;
   fa.fl = s.fl; fa.pf = s.pf; fa.Srow = s.Srow; fa.part = s.fpart; fa.rows_per_cluster = s.frpc;
   fa.mode = s.mode; fa.stop = s.stop;
+  {
+    const char* pf = getenv("GWDP_L2_AHEAD");
+    fa.l2_ahead = pf ? atoi(pf) : 0;
+  }
   while (done < iters) {
     const int chunk = tolmode ? std::min(check_every, iters - done) : iters - done;
     for (int k = 0; k < chunk; ++k) {
@@ -624,7 +646,7 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
       PROF_END(c, PC_SINK_COL, 2);
       if (!check && s.fK > 0) {
         PROF_BEGIN(c, PC_SINK_FUSED);
-        TRY(fused_launch(c, s.fK, s.fCL, fa, s.fncl));
+        TRY(fused_launch(c, s.fK, s.fCL, s.fNT, fa, s.fncl));
         KCHECK();
         k_sink_fin_fast<<<grid_for(std::max(m, nl), 256, 1 << 30), 256, 0, c->stream>>>(
             s.Srow, nl, P.lp + P.row0, s.f, s.fh, s.fl, nullptr, s.fpart, s.fncl, m, P.lq, eps, s.g, s.gh, s.gl,
