@@ -189,8 +189,8 @@ def main():
     # ---- timed region ----
     clocks = ClockSampler(local_rank)
     import ctypes as C
-    ms_c = (C.c_double * 7)()
-    cnt_c = (C.c_int64 * 7)()
+    ms_c = (C.c_double * 8)()
+    cnt_c = (C.c_int64 * 8)()
     _lib.check(lib.gw_ctx_profile(ctx.h, 2, None, None, 0))
     clocks.start()
     if world > 1:
@@ -204,7 +204,7 @@ def main():
     if world > 1:
         dist.barrier()
     ck = clocks.stop()
-    _lib.check(lib.gw_ctx_profile(ctx.h, 0, C.cast(ms_c, C.c_void_p), C.cast(cnt_c, C.c_void_p), 7))
+    _lib.check(lib.gw_ctx_profile(ctx.h, 0, C.cast(ms_c, C.c_void_p), C.cast(cnt_c, C.c_void_p), 8))
     elapsed_ms = e0.elapsed_time(e1)
     value = args.steps / (elapsed_ms / 1000.0)
 
@@ -252,7 +252,7 @@ def main():
            "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config,
            "roofline": roof, "grad": grad, "kernels": kern,
-           "gpu_launches": int(cnt_c[6]),
+           "gpu_launches": int(cnt_c[7]),
            "clocks": ck, "e2e": e2e,
            "result": {"gw_objective": res.gw_objective, "marginal_violation": res.marginal_violation,
                       "e2e_gw_objective": re.gw_objective, "inner_iters": res.inner_iters_total,

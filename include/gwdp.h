@@ -138,9 +138,11 @@ gw_status gw_ctx_destroy(gw_ctx *ctx);
 gw_status gw_ctx_trim(gw_ctx *ctx);
 /* Kernel-class timing with CUDA events on ctx's stream (for measurement harnesses).
  * enable: 0 off, 1 on, 2 on + reset totals.  out_ms / out_counts (host, nullable) receive
- * `nslots` entries: {grad_moments, grad_carry, grad_main, sink_row, sink_col, other}
- * accumulated since the last reset; with nslots >= 7, out_counts[6] = all kernel launches of
- * the library since the last reset.  Synchronises ctx's stream. */
+ * `nslots` entries: {grad_moments, grad_carry, grad_main, sink_row, sink_col, sink_fused,
+ * objective_pass} accumulated since the last reset (sink_col and sink_fused count their two
+ * launches per iteration; objective_pass counts one per final-objective pass); with
+ * nslots >= 8, out_counts[7] = all kernel launches of the library since the last reset.
+ * Synchronises ctx's stream. */
 gw_status gw_ctx_profile(gw_ctx *ctx, int enable, double *out_ms, int64_t *out_counts, int nslots);
 const char *gw_last_error(void);
 int gw_abi_version(void);

@@ -156,20 +156,33 @@ __global__ void k_colcarry(int64_t nl, int64_t m, int nb, const double* __restri
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (q >= m) return;
   double CP = 0.0, CX = 0.0;
-  for (int b = 0; b < nb; ++b) {
-    const double s1 = cS[(int64_t)b * m + q], sx = cX[(int64_t)b * m + q];
-    cS[(int64_t)b * m + q] = CP;
-    cX[(int64_t)b * m + q] = CX;
-    const double xa = xl[(int64_t)b * TR], xb = xl[min((int64_t)(b + 1) * TR, nl - 1)];
-    CX = CX + (xb - xa) * CP + sx;
-    CP += s1;
+  constexpr int U = 16;  // blocks in flight: the loads of a group are independent, the recursion is not
+  for (int b0 = 0; b0 < nb; b0 += U) {
+    double s1[U], sx[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int b = b0 + u;
+      s1[u] = b < nb ? cS[(int64_t)b * m + q] : 0.0;
+      sx[u] = b < nb ? cX[(int64_t)b * m + q] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int b = b0 + u;
+      if (b < nb) {
+        cS[(int64_t)b * m + q] = CP;
+        cX[(int64_t)b * m + q] = CX;
+        const double xa = xl[(int64_t)b * TR], xb = xl[min((int64_t)(b + 1) * TR, nl - 1)];
+        CX = CX + (xb - xa) * CP + sx[u];
+        CP += s1[u];
+      }
+    }
   }
   btot[q] = CP;
   cxend[q] = CX;
 }
 
 // Row carries, one CTA per row block (thread = row), walking the strips s:
-//   P_c0(j) = sum_{q < c0(s)} T_jq,   A_c0(j) = sum_{q < c0(s)} (y_{c0(s)} - y_q) T_jq
+//   P_c0(j) = sum_{q < c0} T_jq,   A_c0(j) = sum_{q < c0} (y_{c0} - y_q) T_jq
 // plus per-(block, strip) sums over the block's rows of {P_c0, A_c0, (xe_b - x_j) P_c0,
 // (xe_b - x_j) A_c0} -> blk (the column-direction carry of the row carries).
 // Totals: Ptot = T 1, Aend = sum_q (y_{m-1} - y_q) T_jq.
@@ -177,7 +190,8 @@ __global__ void __launch_bounds__(TR) k_rowcarry(int64_t nl, int64_t m, int ns, 
                                                  const double* __restrict__ yc, double* __restrict__ rP,
                                                  double* __restrict__ rA, double* __restrict__ blk,
                                                  double* __restrict__ Ptot, double* __restrict__ Aend) {
-  __shared__ double red[32][NWARP][4];
+  constexpr int U = 16;  // strips in flight
+  __shared__ double red[U][NWARP][4];
   const int b = blockIdx.x;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const int64_t j = (int64_t)b * TR + t;
@@ -185,22 +199,28 @@ __global__ void __launch_bounds__(TR) k_rowcarry(int64_t nl, int64_t m, int ns, 
   const double xe = xl[min((int64_t)(b + 1) * TR, nl - 1)];
   const double dxe = jv ? xe - xl[j] : 0.0;
   double P = 0.0, A = 0.0;
-  for (int sc = 0; sc < ns; sc += 32) {
-    const int cnt = min(32, ns - sc);
-    for (int k = 0; k < cnt; ++k) {
-      const int s = sc + k;
-      double rp = 0.0, ra = 0.0;
-      if (jv) {
-        rp = rP[(int64_t)s * nl + j];
-        ra = rA[(int64_t)s * nl + j];
-        rP[(int64_t)s * nl + j] = P;
-        rA[(int64_t)s * nl + j] = A;
+  for (int sc = 0; sc < ns; sc += U) {
+    const int cnt = min(U, ns - sc);
+    double rp[U], ra[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      rp[k] = (jv && k < cnt) ? rP[(int64_t)(sc + k) * nl + j] : 0.0;
+      ra[k] = (jv && k < cnt) ? rA[(int64_t)(sc + k) * nl + j] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      if (k < cnt) {
+        const int s = sc + k;
+        if (jv) {
+          rP[(int64_t)s * nl + j] = P;
+          rA[(int64_t)s * nl + j] = A;
+        }
+        const double v0 = warp_sum(P), v1 = warp_sum(A), v2 = warp_sum(dxe * P), v3 = warp_sum(dxe * A);
+        if (lane == 0) { red[k][w][0] = v0; red[k][w][1] = v1; red[k][w][2] = v2; red[k][w][3] = v3; }
+        const double ya = yc[(int64_t)s * TC], yb = yc[min((int64_t)(s + 1) * TC, m - 1)];
+        A = A + (yb - ya) * P + ra[k];
+        P += rp[k];
       }
-      double v0 = warp_sum(P), v1 = warp_sum(A), v2 = warp_sum(dxe * P), v3 = warp_sum(dxe * A);
-      if (lane == 0) { red[k][w][0] = v0; red[k][w][1] = v1; red[k][w][2] = v2; red[k][w][3] = v3; }
-      const double ya = yc[(int64_t)s * TC], yb = yc[min((int64_t)(s + 1) * TC, m - 1)];
-      A = A + (yb - ya) * P + ra;
-      P += rp;
     }
     __syncthreads();
     if (t < cnt * 4) {
@@ -222,15 +242,26 @@ __global__ void k_blkscan(int64_t nl, int nb, int ns, const double* __restrict__
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= ns) return;
   double SP = 0, SA = 0, XP = 0, XA = 0;
-  for (int b = 0; b < nb; ++b) {
-    const double* t = blk + ((int64_t)b * ns + s) * 4;
-    double* o = bs + ((int64_t)b * ns + s) * 4;
-    o[0] = SP; o[1] = SA; o[2] = XP; o[3] = XA;
-    const double dx = xl[min((int64_t)(b + 1) * TR, nl - 1)] - xl[(int64_t)b * TR];
-    XP = XP + dx * SP + t[2];
-    XA = XA + dx * SA + t[3];
-    SP += t[0];
-    SA += t[1];
+  constexpr int U = 16;
+  for (int b0 = 0; b0 < nb; b0 += U) {
+    double4 tv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int b = b0 + u;
+      tv[u] = b < nb ? *reinterpret_cast<const double4*>(blk + ((int64_t)b * ns + s) * 4) : make_double4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int b = b0 + u;
+      if (b < nb) {
+        *reinterpret_cast<double4*>(bs + ((int64_t)b * ns + s) * 4) = make_double4(SP, SA, XP, XA);
+        const double dx = xl[min((int64_t)(b + 1) * TR, nl - 1)] - xl[(int64_t)b * TR];
+        XP = XP + dx * SP + tv[u].z;
+        XA = XA + dx * SA + tv[u].w;
+        SP += tv[u].x;
+        SA += tv[u].y;
+      }
+    }
   }
 }
 

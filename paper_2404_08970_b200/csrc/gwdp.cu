@@ -15,6 +15,7 @@
 #include "common.cuh"
 #include "fused.cuh"
 #include "grad.cuh"
+#include "grad2.cuh"
 #include "sink.cuh"
 #include "vec.cuh"
 
@@ -64,7 +65,7 @@ struct gw_comm {
 };
 
 // Per-kernel-class CUDA-event timing (enabled by gw_ctx_profile; events on ctx's stream).
-enum { PC_GRAD_MOMENTS = 0, PC_GRAD_CARRY, PC_GRAD_MAIN, PC_SINK_ROW, PC_SINK_COL, PC_SINK_FUSED, PC_N };
+enum { PC_GRAD_MOMENTS = 0, PC_GRAD_CARRY, PC_GRAD_MAIN, PC_SINK_ROW, PC_SINK_COL, PC_SINK_FUSED, PC_OBJ, PC_N };
 struct Prof {
   bool on = false;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
@@ -87,13 +88,15 @@ struct gw_ctx {
   // gradient aux
   Buf rP, rA, cS, cX, blk, bs, btot, cxend, SAg, WAg, Ptot, Aend, DP, DA, tobj, tent, tcc, objout;
   Buf fxs, fys;  // FGW features (staged)
+  Buf pnf, qnf;  // fp32 marginals
   Buf fsc, gsc;  // scaled duals for the Gibbs regeneration
   Buf Gs;        // solver cost buffer
   double* hpin = nullptr;  // pinned host scratch (64 doubles)
   gw_ctx() {
     Buf* b[] = {&stage, &mom, &xc, &yc, &pn, &qn, &lp, &lq, &cvx, &cvy, &fs, &gs, &fh, &fl, &gh, &gl,
                 &ftmp, &viol, &stop, &iters, &part, &fpart, &mode, &srow, &pfl, &rP, &rA, &cS, &cX, &blk, &bs, &btot, &cxend,
-                &SAg, &WAg, &Ptot, &Aend, &DP, &DA, &tobj, &tent, &tcc, &objout, &fxs, &fys, &fsc, &gsc, &Gs};
+                &SAg, &WAg, &Ptot, &Aend, &DP, &DA, &tobj, &tent, &tcc, &objout, &fxs, &fys, &fsc, &gsc, &Gs,
+                &pnf, &qnf};
     for (Buf* x : b) all.push_back(x);
   }
 };
@@ -262,6 +265,7 @@ struct Prepared {
   int64_t n, m, row0, nl;
   const double *x, *y, *p, *q;  // device views of the caller's vectors (staged if host)
   double *xc, *yc, *pn, *qn, *lp, *lq, *cx, *cy;
+  float *pnf, *qnf;  // fp32 copies of the normalised marginals (T^0 = p q^T on the fp32 gradient path)
   double xlast, ylast;
 };
 
@@ -330,6 +334,11 @@ static gw_status prepare(gw_ctx* c, const gw_problem* pb, Prepared& P) {
   k_prep<<<grid_for(m), 256, 0, c->stream>>>(P.y, P.q, m, mom + 8, yc, qn, lq, cy);
   KCHECK();
   P.xc = xc; P.yc = yc; P.pn = pn; P.qn = qn; P.lp = lp; P.lq = lq; P.cx = cx; P.cy = cy;
+  TRY(ws(c, c->pnf, n, &P.pnf)); TRY(ws(c, c->qnf, m, &P.qnf));
+  k_to_float<<<grid_for(n), 256, 0, c->stream>>>(pn, n, P.pnf);
+  KCHECK();
+  k_to_float<<<grid_for(m), 256, 0, c->stream>>>(qn, m, P.qnf);
+  KCHECK();
   P.xlast = h[6] * 0.0;  // filled below from host copies of the endpoints
   // endpoints in centred coordinates: x_{n-1} - xmid = (x_{n-1} - x_0) / 2
   double ends[4];
@@ -350,8 +359,12 @@ struct GradOut {
 
 // One DP gradient pass over the (local) plan given by `S` (mode `mode`):
 //   STORE -> G (ldG);  OBJ -> E(T), violation(T), H(T) via k_objective.
-static gw_status grad_pass(gw_ctx* c, const Prepared& P, int mode, const TSrc& S, float* G, int64_t ldG, bool store,
-                           bool obj, const double* fx, const double* fy, double alpha, double* objout_dev) {
+// The STORE-only pass (every gradient of the solver and gw_grad_dp) runs the streaming fp32 kernels of
+// grad2.cuh with T supplied by S2; the objective pass (OBJ) runs grad.cuh's kernels with S (fp64
+// regeneration) so that its moments and its tile sums see bit-identical T values.
+static gw_status grad_pass(gw_ctx* c, const Prepared& P, int mode, const TSrc& S, const TSrc2& S2, float* G,
+                           int64_t ldG, bool store, bool obj, const double* fx, const double* fy, double alpha,
+                           double* objout_dev) {
   const int64_t nl = P.nl, m = P.m;
   if (nl == 0) return GW_OK;
   const int nb = (int)((nl + TR - 1) / TR), ns = (int)((m + TC - 1) / TC);
@@ -367,20 +380,31 @@ static gw_status grad_pass(gw_ctx* c, const Prepared& P, int mode, const TSrc& S
   TRY(ws(c, c->tcc, (size_t)nb * ns, &tcc));
   const double* xl = P.xc + P.row0;
   dim3 grid(ns, nb);
-  PROF_BEGIN(c, PC_GRAD_MOMENTS);
-  switch (mode) {
-    case T_EXPLICIT: k_grad_moments<T_EXPLICIT><<<grid, NT, 0, c->stream>>>(S, nl, m, xl, P.yc, rP, rA, cS, cX); break;
-    case T_GIBBS: k_grad_moments<T_GIBBS><<<grid, NT, 0, c->stream>>>(S, nl, m, xl, P.yc, rP, rA, cS, cX); break;
-    default: k_grad_moments<T_PRODUCT><<<grid, NT, 0, c->stream>>>(S, nl, m, xl, P.yc, rP, rA, cS, cX); break;
+  const bool fast = store && !obj;
+  // the objective pass (old fp64-regeneration kernels) is timed as its own class
+  const int pc_mom = fast ? PC_GRAD_MOMENTS : PC_OBJ, pc_main = fast ? PC_GRAD_MAIN : PC_OBJ;
+  PROF_BEGIN(c, pc_mom);
+  if (fast) {
+    switch (mode) {
+      case T_EXPLICIT: k_grad_moments2<T_EXPLICIT><<<grid, G2T, 0, c->stream>>>(S2, nl, m, xl, P.yc, rP, rA, cS, cX); break;
+      case T_GIBBS: k_grad_moments2<T_GIBBS><<<grid, G2T, 0, c->stream>>>(S2, nl, m, xl, P.yc, rP, rA, cS, cX); break;
+      default: k_grad_moments2<T_PRODUCT><<<grid, G2T, 0, c->stream>>>(S2, nl, m, xl, P.yc, rP, rA, cS, cX); break;
+    }
+  } else {
+    switch (mode) {
+      case T_EXPLICIT: k_grad_moments<T_EXPLICIT><<<grid, NT, 0, c->stream>>>(S, nl, m, xl, P.yc, rP, rA, cS, cX); break;
+      case T_GIBBS: k_grad_moments<T_GIBBS><<<grid, NT, 0, c->stream>>>(S, nl, m, xl, P.yc, rP, rA, cS, cX); break;
+      default: k_grad_moments<T_PRODUCT><<<grid, NT, 0, c->stream>>>(S, nl, m, xl, P.yc, rP, rA, cS, cX); break;
+    }
   }
   KCHECK();
-  PROF_END(c, PC_GRAD_MOMENTS, 1);
+  PROF_END(c, pc_mom, fast ? 1 : 0);
   PROF_BEGIN(c, PC_GRAD_CARRY);
   k_colcarry<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(nl, m, nb, xl, cS, cX, btot, cxend);
   KCHECK();
   k_rowcarry<<<nb, TR, 0, c->stream>>>(nl, m, ns, xl, P.yc, rP, rA, blk, Ptot, Aend);
   KCHECK();
-  k_blkscan<<<(ns + 127) / 128, 128, 0, c->stream>>>(nl, nb, ns, xl, blk, bs);
+  k_blkscan<<<(ns + 31) / 32, 32, 0, c->stream>>>(nl, nb, ns, xl, blk, bs);
   KCHECK();
   Scan1DBatch B;
   memset(&B, 0, sizeof(B));
@@ -397,7 +421,7 @@ static gw_status grad_pass(gw_ctx* c, const Prepared& P, int mode, const TSrc& S
   a.rP = rP; a.rA = rA; a.cS = cS; a.cX = cX; a.bs = bs; a.xlast = P.xlast; a.ylast = P.ylast;
   a.G = G; a.ldG = ldG; a.tile_obj = tobj; a.tile_ent = tent; a.tile_cc = tcc;
   a.fx = fx ? fx + P.row0 : nullptr; a.fy = fy; a.alpha = alpha;
-  PROF_BEGIN(c, PC_GRAD_MAIN);
+  PROF_BEGIN(c, pc_main);
 #define LAUNCH_MAIN(MODE, ST, OB)                                                                  \
   do {                                                                                             \
     const size_t dsm = main_dyn_smem<OB>();                                                        \
@@ -405,7 +429,16 @@ static gw_status grad_pass(gw_ctx* c, const Prepared& P, int mode, const TSrc& S
                             (int)dsm));                                                            \
     k_grad_main<MODE, ST, OB><<<grid, NT, dsm, c->stream>>>(a);                                    \
   } while (0)
-  if (mode == T_EXPLICIT) {
+#define LAUNCH_STORE2(MODE)                                                                           \
+  do {                                                                                                \
+    if (fx) k_grad_store2<MODE, true><<<grid, G2T, 0, c->stream>>>(a, S2);                            \
+    else k_grad_store2<MODE, false><<<grid, G2T, 0, c->stream>>>(a, S2);                              \
+  } while (0)
+  if (fast) {
+    if (mode == T_EXPLICIT) LAUNCH_STORE2(T_EXPLICIT);
+    else if (mode == T_GIBBS) LAUNCH_STORE2(T_GIBBS);
+    else LAUNCH_STORE2(T_PRODUCT);
+  } else if (mode == T_EXPLICIT) {
     if (store && obj) LAUNCH_MAIN(T_EXPLICIT, true, true);
     else if (store) LAUNCH_MAIN(T_EXPLICIT, true, false);
     else LAUNCH_MAIN(T_EXPLICIT, false, true);
@@ -419,8 +452,9 @@ static gw_status grad_pass(gw_ctx* c, const Prepared& P, int mode, const TSrc& S
     else LAUNCH_MAIN(T_PRODUCT, false, true);
   }
 #undef LAUNCH_MAIN
+#undef LAUNCH_STORE2
   KCHECK();
-  PROF_END(c, PC_GRAD_MAIN, 1);
+  PROF_END(c, pc_main, 1);
   if (obj) {
     k_objective<<<1, 1024, 0, c->stream>>>(Ptot, xl, P.pn + P.row0, P.cx + P.row0, nl, btot, P.yc, P.qn, P.cy, m,
                                            tobj, (int64_t)nb * ns, tent, objout_dev);
@@ -448,7 +482,9 @@ extern "C" gw_status gw_grad_dp(gw_ctx* c, const gw_problem* pb, const void* T, 
   Prepared P;
   TRY(prepare(c, pb, P));
   TSrc S{reinterpret_cast<const float*>(T), ldT, nullptr, nullptr, 0.0};
-  TRY(grad_pass(c, P, T_EXPLICIT, S, reinterpret_cast<float*>(G), ldG, true, false, nullptr, nullptr, 1.0, nullptr));
+  TSrc2 S2{reinterpret_cast<const float*>(T), ldT, nullptr, nullptr, nullptr, nullptr, 0.f, 0.f};
+  TRY(grad_pass(c, P, T_EXPLICIT, S, S2, reinterpret_cast<float*>(G), ldG, true, false, nullptr, nullptr, 1.0,
+                nullptr));
   return GW_OK;
 }
 
@@ -844,19 +880,31 @@ static gw_status solve_impl(gw_ctx* c, const gw_problem* pb, const gw_solve_opts
     // ---- gradient of T^{l} (l = 0: T0 or p q^T) ----
     int mode;
     TSrc S;
+    TSrc2 S2;
     if (l == 0) {
-      if (T0) { mode = T_EXPLICIT; S = TSrc{reinterpret_cast<const float*>(T0), ldT, nullptr, nullptr, 0.0}; }
-      else { mode = T_PRODUCT; S = TSrc{nullptr, 0, P.pn + P.row0, P.qn, 0.0}; }
+      if (T0) {
+        mode = T_EXPLICIT;
+        S = TSrc{reinterpret_cast<const float*>(T0), ldT, nullptr, nullptr, 0.0};
+        S2 = TSrc2{reinterpret_cast<const float*>(T0), ldT, nullptr, nullptr, nullptr, nullptr, 0.f, 0.f};
+      } else {
+        mode = T_PRODUCT;
+        S = TSrc{nullptr, 0, P.pn + P.row0, P.qn, 0.0};
+        S2 = TSrc2{nullptr, 0, P.pnf + P.row0, nullptr, P.qnf, nullptr, 0.f, 0.f};
+      }
     } else {
       mode = T_GIBBS;
       k_scale<<<grid_for(nl), 256, 0, c->stream>>>(s.f, nl, GW_LOG2E / eps, Fs);
       k_scale<<<grid_for(m), 256, 0, c->stream>>>(s.g, m, GW_LOG2E / eps, Gs2);
       KCHECK();
       S = TSrc{G, ldG, Fs, Gs2, GW_LOG2E / eps};
+      // fp32 hi/lo split of the duals: the Sinkhorn state (fh, fl, gh, gl) is consistent with (f, g)
+      const double cc = GW_LOG2E / eps;
+      const float ch = (float)cc;
+      S2 = TSrc2{G, ldG, s.fh, s.fl, s.gh, s.gl, ch, (float)(cc - (double)ch)};
     }
     const bool obj = (l > 0) && want_trace_obj;
     CU(cudaEventRecord(evs[2 * l], c->stream));
-    TRY(grad_pass(c, P, mode, S, G, ldG, true, obj, fx, fy, alpha, objout));
+    TRY(grad_pass(c, P, mode, S, S2, G, ldG, true, obj, fx, fy, alpha, objout));
     CU(cudaEventRecord(evs[2 * l + 1], c->stream));
     if (obj) {
       CU(cudaMemcpyAsync(c->hpin, objout, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -890,7 +938,8 @@ static gw_status solve_impl(gw_ctx* c, const gw_problem* pb, const gw_solve_opts
       KCHECK();
       S = TSrc{G, ldG, Fs, Gs2, GW_LOG2E / eps};
     }
-    TRY(grad_pass(c, P, mode, S, nullptr, 0, false, true, fx, fy, alpha, objout));
+    const TSrc2 S2{};
+    TRY(grad_pass(c, P, mode, S, S2, nullptr, 0, false, true, fx, fy, alpha, objout));
     if (T_out) TRY(materialize(c, P, mode == T_EXPLICIT ? T_GIBBS : mode, S, T_out, ldT));
     if (T_out && mode == T_EXPLICIT) CU(cudaMemcpy2DAsync(T_out, ldT * 4, T0, ldT * 4, m * 4, nl,
                                                           cudaMemcpyDeviceToDevice, c->stream));

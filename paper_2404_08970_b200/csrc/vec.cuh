@@ -91,6 +91,7 @@ __global__ void __launch_bounds__(1024) k_scan1d(Scan1DBatch B) {
   const int64_t chunk = (n + blockDim.x - 1) / blockDim.x;
   const int64_t i0 = threadIdx.x * chunk, i1 = min(n, i0 + chunk);
   PA<double> st{0.0, 0.0, D.s[min(i0, n - 1)]};
+#pragma unroll 8
   for (int64_t i = i0; i < i1; ++i) {
     const double si = D.s[i];
     st.A += (si - st.s) * st.P;
@@ -100,6 +101,7 @@ __global__ void __launch_bounds__(1024) k_scan1d(Scan1DBatch B) {
   PA<double> total;
   PA<double> e = pa_block_scan_excl<32>(st, sm, total);
   const double V = total.P, Sv = total.s * total.P - total.A;
+#pragma unroll 8
   for (int64_t i = i0; i < i1; ++i) {
     const double si = D.s[i];
     const double lo = pa_eval(e, si);
