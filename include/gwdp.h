@@ -147,17 +147,43 @@ gw_status gw_ctx_profile(gw_ctx *ctx, int enable, double *out_ms, int64_t *out_c
 const char *gw_last_error(void);
 int gw_abi_version(void);
 
-/* NCCL bootstrap: rank 0 gets a 128-byte id, the caller broadcasts it (e.g. with
- * torch.distributed), every rank calls gw_comm_init with the same id. */
+/* ---- row sharding ------------------------------------------
+ * Rank r of R owns rows [row0_r, row0_r + n_local_r) of every N x M matrix (its gw_problem's
+ * row0 / n_local); shards must be non-empty and consecutive in rank order.  x, y, p, q and g are
+ * replicated, f is per shard.  Every rank calls the same entry points in the same order with
+ * identical n, m, x, y, p, q and options (collective semantics).  The only collective the library
+ * issues is an all-gather of equal-sized per-rank payloads (column sums per Sinkhorn iteration,
+ * column / block-strip carries and row moments per gradient, a few scalars per objective);
+ * payloads are combined in rank order, so results are identical on every rank and do not
+ * depend on the transport. */
+
+/* NCCL transport: rank 0 gets a 128-byte id, the caller broadcasts it (e.g. with
+ * torch.distributed), every rank calls gw_comm_init with the same id.  Collectives are
+ * enqueued on the ctx stream (asynchronous). */
 gw_status gw_get_unique_id(unsigned char id[128]);
 gw_status gw_comm_init(gw_comm **out, const unsigned char id[128], int nranks, int rank);
+
+/* Host-callback transport (same sharded code path; used for testing without NVLink and for
+ * any host-side process group): `allgather` receives `bytes` bytes from this rank in `send`
+ * (host memory) and must fill `recv` with nranks * bytes bytes, rank r's contribution at offset
+ * r * bytes; it returns 0 on success.  Called synchronously from the thread driving the ctx,
+ * after the ctx stream has been synchronised. */
+typedef int (*gw_allgather_fn)(const void *send, void *recv, int64_t bytes, void *user);
+gw_status gw_comm_init_host(gw_comm **out, int nranks, int rank, gw_allgather_fn allgather, void *user);
 gw_status gw_comm_destroy(gw_comm *comm);
+
+/* Balanced row shard: the first n % nranks ranks get one more row.  Host only (no GPU). */
+gw_status gw_shard_rows(int64_t n, int nranks, int rank, int64_t *row0, int64_t *n_local);
+/* Validate a shard table (table[2r] = row0_r, table[2r+1] = n_local_r): consecutive in rank order
+ * and covering [0, n).  GW_ERR_DIM_MISMATCH otherwise.  Host only. */
+gw_status gw_check_shards(const int64_t *table, int nranks, int64_t n);
 
 /* ---- hot path ----------------------------------------------------------------------- */
 
 /* G = 2(c 1^T + 1 c'^T) - 4 D_X T D_Y for the rows [row0, row0 + n_local)
  * in O(n m) by the paper's dynamic programme
- * realised as row and column prefix scans with fp64 carries.
+ * realised as row and column prefix scans with fp64 carries.  With a multi-rank ctx every rank
+ * passes its own rows of T and receives its rows of G.
  * T: device fp32 (n_local x m, ldT); G: device fp32 output (ldG), may alias T
  * (ldG == ldT).  c, c' use the PRESCRIBED p, q (reading R4).  mom: must be NULL
  * in ABI v1.  Asynchronous. */

@@ -25,7 +25,7 @@ GW_SOLVE_TRACE_OBJECTIVE = 0x1
 # exported symbols (include/gwdp.h) -- checked by tests/test_abi.py
 SYMBOLS = [
     "gw_ctx_create", "gw_ctx_destroy", "gw_ctx_trim", "gw_ctx_profile", "gw_last_error", "gw_abi_version",
-    "gw_get_unique_id", "gw_comm_init", "gw_comm_destroy",
+    "gw_get_unique_id", "gw_comm_init", "gw_comm_init_host", "gw_comm_destroy", "gw_shard_rows", "gw_check_shards",
     "gw_grad_dp", "sinkhorn_solve", "entropic_gw_solve", "fgw_solve", "ugw_solve",
 ]
 
@@ -69,6 +69,9 @@ class gw_result(C.Structure):
                 ("ms_grad", C.c_double), ("ms_sinkhorn", C.c_double), ("ms_total", C.c_double)]
 
 
+# int (*gw_allgather_fn)(const void *send, void *recv, int64_t bytes, void *user)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
+
 _lib = None
 
 
@@ -92,6 +95,9 @@ def load(path=LIB_PATH):
     lib.gw_get_unique_id.argtypes = [C.c_char_p]
     lib.gw_comm_init.argtypes = [C.POINTER(P), C.c_char_p, C.c_int, C.c_int]
     lib.gw_comm_destroy.argtypes = [P]
+    lib.gw_comm_init_host.argtypes = [C.POINTER(P), C.c_int, C.c_int, ALLGATHER_FN, P]
+    lib.gw_shard_rows.argtypes = [i64, C.c_int, C.c_int, C.POINTER(i64), C.POINTER(i64)]
+    lib.gw_check_shards.argtypes = [C.POINTER(i64), C.c_int, i64]
     lib.gw_grad_dp.argtypes = [P, C.POINTER(gw_problem), P, i64, P, i64, C.POINTER(gw_moments)]
     lib.sinkhorn_solve.argtypes = [P, C.POINTER(gw_problem), P, i64, C.POINTER(gw_sinkhorn_opts), P, P, P, i64,
                                    C.POINTER(gw_sinkhorn_info)]

@@ -43,11 +43,15 @@ def _check_mat(t, name):
 
 
 class Context:
-    """One gw_ctx per (device, stream); owns the library workspace."""
+    """One gw_ctx per (device, stream[, comm]); owns the library workspace.  `comm` is a
+    dist.Comm (multi-rank) or None."""
 
     _cache = {}
 
     def __init__(self, device=None, stream=None, comm=None):
+        if comm is not None and hasattr(comm, "ptr"):
+            self.comm = comm
+            comm = comm.ptr
         self.lib = L.load()
         dev = torch.device("cuda", torch.cuda.current_device() if device is None else torch.device(device).index or 0)
         self.device = dev
@@ -85,8 +89,10 @@ def _problem(x, y, p, q, n_local=None, row0=0, flags=0):
     return pr
 
 
-def grad(x, y, p, q, T, out=None, validate=True, ctx=None):
-    """G = 2(c 1^T + 1 c'^T) - 4 D_X T D_Y  (gw_grad_dp), fp32."""
+def grad(x, y, p, q, T, out=None, validate=True, ctx=None, row0=0):
+    """G = 2(c 1^T + 1 c'^T) - 4 D_X T D_Y  (gw_grad_dp), fp32.
+    Sharded (ctx with a multi-rank comm): x, p are the full supports/marginals, T holds this
+    rank's rows [row0, row0 + T.shape[0]) and the result holds the same rows of G."""
     ctx = ctx or Context.get(T.device)
     dev = T.device
     x, y, p, q = (_vec(v, dev) for v in (x, y, p, q))
@@ -95,7 +101,7 @@ def grad(x, y, p, q, T, out=None, validate=True, ctx=None):
     if out is None:
         out = plan_buffer(n, m, dev)
     ldG = _check_mat(out, "out")
-    pr = _problem(x, y, p, q, flags=0 if validate else L.GW_NO_VALIDATE)
+    pr = _problem(x, y, p, q, n_local=n, row0=row0, flags=0 if validate else L.GW_NO_VALIDATE)
     L.check(ctx.lib.gw_grad_dp(ctx.h, C.byref(pr), _ptr(T), ldT, _ptr(out), ldG, None))
     return out
 
@@ -162,15 +168,19 @@ def _opts(eps, outer, inner, tol, check_every, trace_objective):
 
 
 def solve(x, y, p, q, eps, outer, inner, tol=0.0, check_every=10, T0=None, return_plan=False,
-          trace_objective=False, fx=None, fy=None, alpha=None, device=None, ctx=None):
+          trace_objective=False, fx=None, fy=None, alpha=None, device=None, ctx=None, row0=0, n_local=None):
     """Entropic GW (entropic_gw_solve) or, with fx/fy/alpha, entropic FGW (fgw_solve), on
-    device vectors; tau = eps."""
+    device vectors; tau = eps.  Sharded (ctx with a multi-rank
+    comm): x, p (and fx) are full; this rank owns rows [row0, row0 + n_local): f, T0 and the
+    returned plan hold those rows, g is replicated, the objective and violation are global."""
     dev = torch.device(device) if device is not None else (T0.device if T0 is not None else torch.device("cuda"))
     if dev.index is None:
         dev = torch.device("cuda", torch.cuda.current_device())
     ctx = ctx or Context.get(dev)
     x, y, p, q = (_vec(v, dev) for v in (x, y, p, q))
     n, m = x.numel(), y.numel()
+    if n_local is not None:
+        n = int(n_local)
     f = torch.empty(n, dtype=torch.float64, device=dev)
     g = torch.empty(m, dtype=torch.float64, device=dev)
     T = plan_buffer(n, m, dev) if return_plan else None
@@ -181,7 +191,7 @@ def solve(x, y, p, q, eps, outer, inner, tol=0.0, check_every=10, T0=None, retur
             T = torch.empty((n, ld), dtype=torch.float32, device=dev)[:, :m]
     elif T is not None:
         ld = T.stride(0)
-    pr = _problem(x, y, p, q)
+    pr = _problem(x, y, p, q, n_local=n, row0=row0)
     o = _opts(eps, outer, inner, tol, check_every, trace_objective)
     res = L.gw_result()
     tr = np.zeros((max(int(outer), 1), 4), dtype=np.float64)

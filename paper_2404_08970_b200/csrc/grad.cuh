@@ -237,8 +237,10 @@ __global__ void __launch_bounds__(TR) k_rowcarry(int64_t nl, int64_t m, int ns, 
 // Block-strip carries: for each strip s, exclusive prefix over row blocks of blk,
 //   bs[b][s] = { sum_{j<r0} P_c0(j), sum_{j<r0} A_c0(j),
 //                sum_{j<r0} (x_{r0} - x_j) P_c0(j), sum_{j<r0} (x_{r0} - x_j) A_c0(j) }.
+// tail (nullable): [ns][4] the state after the last block (referenced at the last local row), the
+// per-rank payload of the multi-rank exchange (shard.cuh).
 __global__ void k_blkscan(int64_t nl, int nb, int ns, const double* __restrict__ xl, const double* __restrict__ blk,
-                          double* __restrict__ bs) {
+                          double* __restrict__ bs, double* __restrict__ tail) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= ns) return;
   double SP = 0, SA = 0, XP = 0, XA = 0;
@@ -263,6 +265,7 @@ __global__ void k_blkscan(int64_t nl, int nb, int ns, const double* __restrict__
       }
     }
   }
+  if (tail) *reinterpret_cast<double4*>(tail + 4 * (int64_t)s) = make_double4(SP, SA, XP, XA);
 }
 
 // ---------------------------------------------------------------------------------

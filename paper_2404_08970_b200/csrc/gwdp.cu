@@ -16,6 +16,7 @@
 #include "fused.cuh"
 #include "grad.cuh"
 #include "grad2.cuh"
+#include "shard.cuh"
 #include "sink.cuh"
 #include "vec.cuh"
 
@@ -59,9 +60,17 @@ struct Buf {
   size_t cap = 0;
 };
 
+// Communicator: NCCL (gw_comm_init) or host callbacks (gw_comm_init_host).  The library uses a
+// single collective, an all-gather of equal-sized per-rank payloads (shard.cuh combines them in
+// rank order), so both transports give bit-identical results.
 struct gw_comm {
   ncclComm_t nccl = nullptr;
   int nranks = 1, rank = 0;
+  gw_allgather_fn host_ag = nullptr;
+  void* user = nullptr;
+  unsigned char* hsend = nullptr;  // pinned staging for the host transport
+  unsigned char* hrecv = nullptr;
+  size_t hcap = 0;
 };
 
 // Per-kernel-class CUDA-event timing (enabled by gw_ctx_profile; events on ctx's stream).
@@ -89,6 +98,8 @@ struct gw_ctx {
   Buf rP, rA, cS, cX, blk, bs, btot, cxend, SAg, WAg, Ptot, Aend, DP, DA, tobj, tent, tcc, objout;
   Buf fxs, fys;  // FGW features (staged)
   Buf pnf, qnf;  // fp32 marginals
+  Buf xtab, xg1, xg2, xin, xvec, xtail, xpart;  // multi-rank exchange buffers
+  Buf slse, slseg, scsl, scsg, sviolg;          // Sinkhorn column-sum exchange
   Buf fsc, gsc;  // scaled duals for the Gibbs regeneration
   Buf Gs;        // solver cost buffer
   double* hpin = nullptr;  // pinned host scratch (64 doubles)
@@ -96,7 +107,8 @@ struct gw_ctx {
     Buf* b[] = {&stage, &mom, &xc, &yc, &pn, &qn, &lp, &lq, &cvx, &cvy, &fs, &gs, &fh, &fl, &gh, &gl,
                 &ftmp, &viol, &stop, &iters, &part, &fpart, &mode, &srow, &pfl, &rP, &rA, &cS, &cX, &blk, &bs, &btot, &cxend,
                 &SAg, &WAg, &Ptot, &Aend, &DP, &DA, &tobj, &tent, &tcc, &objout, &fxs, &fys, &fsc, &gsc, &Gs,
-                &pnf, &qnf};
+                &pnf, &qnf, &xtab, &xg1, &xg2, &xin, &xvec, &xtail, &xpart, &slse, &slseg, &scsl, &scsg,
+                &sviolg};
     for (Buf* x : b) all.push_back(x);
   }
 };
@@ -253,10 +265,80 @@ extern "C" gw_status gw_comm_init(gw_comm** out, const unsigned char id[128], in
   return GW_OK;
 }
 
+extern "C" gw_status gw_comm_init_host(gw_comm** out, int nranks, int rank, gw_allgather_fn allgather, void* user) {
+  if (!out || nranks < 1 || rank < 0 || rank >= nranks || (nranks > 1 && !allgather))
+    return fail(GW_ERR_INVALID_ARG, "gw_comm_init_host: bad args");
+  gw_comm* c = new gw_comm();
+  c->nranks = nranks;
+  c->rank = rank;
+  c->host_ag = allgather;
+  c->user = user;
+  *out = c;
+  return GW_OK;
+}
+
 extern "C" gw_status gw_comm_destroy(gw_comm* c) {
   if (!c) return GW_OK;
   if (c->nccl) ncclCommDestroy(c->nccl);
+  if (c->hsend) cudaFreeHost(c->hsend);
+  if (c->hrecv) cudaFreeHost(c->hrecv);
   delete c;
+  return GW_OK;
+}
+
+extern "C" gw_status gw_shard_rows(int64_t n, int nranks, int rank, int64_t* row0, int64_t* n_local) {
+  if (n < 0 || nranks < 1 || rank < 0 || rank >= nranks || !row0 || !n_local)
+    return fail(GW_ERR_INVALID_ARG, "gw_shard_rows: bad args");
+  const int64_t base = n / nranks, extra = n % nranks;
+  *n_local = base + (rank < extra ? 1 : 0);
+  *row0 = rank * base + std::min<int64_t>(rank, extra);
+  return GW_OK;
+}
+
+extern "C" gw_status gw_check_shards(const int64_t* table, int nranks, int64_t n) {
+  if (!table || nranks < 1) return fail(GW_ERR_INVALID_ARG, "gw_check_shards: bad args");
+  int64_t next = 0;
+  for (int r = 0; r < nranks; ++r) {
+    const int64_t r0 = table[2 * r], nl = table[2 * r + 1];
+    if (nl < 0 || r0 != next)
+      return fail(GW_ERR_DIM_MISMATCH, "rank %d holds rows [%lld, %lld): shards must be consecutive in rank order",
+                  r, (long long)r0, (long long)(r0 + nl));
+    next = r0 + nl;
+  }
+  if (next != n) return fail(GW_ERR_DIM_MISMATCH, "shards cover %lld rows, n = %lld", (long long)next, (long long)n);
+  return GW_OK;
+}
+
+static int nranks_of(const gw_ctx* c) { return c->comm ? c->comm->nranks : 1; }
+
+// All-gather of `bytes` per rank from device `dsend` into device `drecv` ([nranks][bytes], rank
+// order), ordered on ctx's stream.  Host transport: synchronises the stream around the callback.
+static gw_status comm_allgather(gw_ctx* c, const void* dsend, void* drecv, size_t bytes) {
+  gw_comm* k = c->comm;
+  if (!k || k->nranks == 1) {
+    if (dsend != drecv) CU(cudaMemcpyAsync(drecv, dsend, bytes, cudaMemcpyDeviceToDevice, c->stream));
+    return GW_OK;
+  }
+  if (k->nccl) {
+    ncclResult_t r = ncclAllGather(dsend, drecv, bytes, ncclInt8, k->nccl, c->stream);
+    if (r != ncclSuccess) return fail(GW_ERR_NCCL, "ncclAllGather: %s", ncclGetErrorString(r));
+    return GW_OK;
+  }
+  const size_t need = bytes * (size_t)k->nranks;
+  if (k->hcap < need) {
+    if (k->hsend) cudaFreeHost(k->hsend);
+    if (k->hrecv) cudaFreeHost(k->hrecv);
+    k->hsend = k->hrecv = nullptr;
+    k->hcap = 0;
+    CU(cudaMallocHost(&k->hsend, need));
+    CU(cudaMallocHost(&k->hrecv, need));
+    k->hcap = need;
+  }
+  CU(cudaMemcpyAsync(k->hsend, dsend, bytes, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  if (k->host_ag(k->hsend, k->hrecv, (int64_t)bytes, k->user) != 0)
+    return fail(GW_ERR_NCCL, "host all-gather callback failed");
+  CU(cudaMemcpyAsync(drecv, k->hrecv, need, cudaMemcpyHostToDevice, c->stream));
   return GW_OK;
 }
 
@@ -267,6 +349,11 @@ struct Prepared {
   double *xc, *yc, *pn, *qn, *lp, *lq, *cx, *cy;
   float *pnf, *qnf;  // fp32 copies of the normalised marginals (T^0 = p q^T on the fp32 gradient path)
   double xlast, ylast;
+  // row shards of all ranks (multi-rank only): tab[2r] = row0_r, tab[2r+1] = nl_r
+  int R = 1, rank = 0;
+  int64_t maxnl = 0;
+  std::vector<int64_t> tab;
+  int64_t* dtab = nullptr;
 };
 
 static gw_status check_problem(const gw_problem* pb) {
@@ -349,6 +436,27 @@ static gw_status prepare(gw_ctx* c, const gw_problem* pb, Prepared& P) {
   CU(cudaStreamSynchronize(c->stream));
   P.xlast = ends[1] - h[6];
   P.ylast = ends[3] - h[14];
+  P.R = nranks_of(c);
+  P.rank = c->comm ? c->comm->rank : 0;
+  P.tab.assign(2 * (size_t)P.R, 0);
+  if (P.R > 1) {
+    int64_t* dt;
+    TRY(ws(c, c->xtab, 2 * (size_t)P.R + 2, &dt));
+    const int64_t mine[2] = {P.row0, P.nl};
+    CU(cudaMemcpyAsync(dt + 2 * P.R, mine, sizeof(mine), cudaMemcpyHostToDevice, c->stream));
+    TRY(comm_allgather(c, dt + 2 * P.R, dt, 2 * sizeof(int64_t)));
+    CU(cudaMemcpyAsync(P.tab.data(), dt, 2 * sizeof(int64_t) * P.R, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    TRY(gw_check_shards(P.tab.data(), P.R, n));
+    for (int r = 0; r < P.R; ++r)
+      if (P.tab[2 * r + 1] == 0) return fail(GW_ERR_DIM_MISMATCH, "rank %d holds no rows (n >= nranks required)", r);
+    P.dtab = dt;
+    for (int r = 0; r < P.R; ++r) P.maxnl = std::max(P.maxnl, P.tab[2 * r + 1]);
+  } else {
+    P.tab[0] = P.row0;
+    P.tab[1] = P.nl;
+    P.maxnl = P.nl;
+  }
   return GW_OK;
 }
 
@@ -365,17 +473,20 @@ struct GradOut {
 static gw_status grad_pass(gw_ctx* c, const Prepared& P, int mode, const TSrc& S, const TSrc2& S2, float* G,
                            int64_t ldG, bool store, bool obj, const double* fx, const double* fy, double alpha,
                            double* objout_dev) {
-  const int64_t nl = P.nl, m = P.m;
-  if (nl == 0) return GW_OK;
+  const int64_t nl = P.nl, m = P.m, n = P.n;
+  const int R = P.R;
+  if (nl == 0) return GW_OK;  // single rank only: prepare() rejects empty shards when R > 1
   const int nb = (int)((nl + TR - 1) / TR), ns = (int)((m + TC - 1) / TC);
   double *rP, *rA, *cS, *cX, *blk, *bs, *btot, *cxend, *SAg, *WAg, *Ptot, *Aend, *DP, *DA, *tobj, *tent, *tcc;
   TRY(ws(c, c->rP, (size_t)ns * nl, &rP)); TRY(ws(c, c->rA, (size_t)ns * nl, &rA));
   TRY(ws(c, c->cS, (size_t)nb * m, &cS)); TRY(ws(c, c->cX, (size_t)nb * m, &cX));
   TRY(ws(c, c->blk, (size_t)nb * ns * 4, &blk)); TRY(ws(c, c->bs, (size_t)nb * ns * 4, &bs));
-  TRY(ws(c, c->btot, m, &btot)); TRY(ws(c, c->cxend, m, &cxend));
+  TRY(ws(c, c->btot, 2 * (size_t)m, &btot));  // {btot | cxend}: one all-gather payload
+  cxend = btot + m;
   TRY(ws(c, c->SAg, m, &SAg)); TRY(ws(c, c->WAg, m, &WAg));
-  TRY(ws(c, c->Ptot, nl, &Ptot)); TRY(ws(c, c->Aend, nl, &Aend));
-  TRY(ws(c, c->DP, nl, &DP)); TRY(ws(c, c->DA, nl, &DA));
+  TRY(ws(c, c->Ptot, 2 * (size_t)P.maxnl, &Ptot));  // {Ptot | Aend}, padded to the largest shard
+  Aend = Ptot + P.maxnl;
+  TRY(ws(c, c->DP, (size_t)(R > 1 ? n : nl), &DP)); TRY(ws(c, c->DA, (size_t)(R > 1 ? n : nl), &DA));
   TRY(ws(c, c->tobj, (size_t)nb * ns, &tobj)); TRY(ws(c, c->tent, (size_t)nb * ns, &tent));
   TRY(ws(c, c->tcc, (size_t)nb * ns, &tcc));
   const double* xl = P.xc + P.row0;
@@ -404,20 +515,60 @@ static gw_status grad_pass(gw_ctx* c, const Prepared& P, int mode, const TSrc& S
   KCHECK();
   k_rowcarry<<<nb, TR, 0, c->stream>>>(nl, m, ns, xl, P.yc, rP, rA, blk, Ptot, Aend);
   KCHECK();
-  k_blkscan<<<(ns + 31) / 32, 32, 0, c->stream>>>(nl, nb, ns, xl, blk, bs);
+  double* tail = nullptr;
+  if (R > 1) TRY(ws(c, c->xtail, 8 * (size_t)ns, &tail));
+  k_blkscan<<<(ns + 31) / 32, 32, 0, c->stream>>>(nl, nb, ns, xl, blk, bs, tail);
   KCHECK();
+  const double* DPsrc = Ptot;
+  const double* DAsrc = Aend;
+  const double* xs_rows = xl;
+  int64_t nrows_dp = nl;
+  if (R > 1) {
+    // (1) column state of the ranks above + global column totals
+    double *g1, *in;
+    TRY(ws(c, c->xg1, 2 * (size_t)m * R, &g1));
+    TRY(ws(c, c->xin, 2 * (size_t)m, &in));
+    TRY(comm_allgather(c, btot, g1, 2 * sizeof(double) * (size_t)m));
+    k_cols_ranks<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(g1, R, P.rank, P.dtab, P.xc, m, in, in + m, btot,
+                                                                   cxend);
+    KCHECK();
+    k_cols_apply<<<grid_for((int64_t)nb * m, 256, 148 * 16), 256, 0, c->stream>>>(nb, m, xl, in, in + m, cS, cX);
+    KCHECK();
+    // (2) block-strip sums of the row carries of the ranks above
+    double* g3;
+    TRY(ws(c, c->xg2, std::max<size_t>(4 * (size_t)ns * R, 2 * (size_t)P.maxnl * R), &g3));
+    TRY(comm_allgather(c, tail, g3, 4 * sizeof(double) * (size_t)ns));
+    k_bs_ranks<<<(ns + 127) / 128, 128, 0, c->stream>>>(g3, R, P.rank, P.dtab, P.xc, ns, tail + 4 * ns);
+    KCHECK();
+    k_bs_apply<<<grid_for((int64_t)nb * ns, 256, 148 * 8), 256, 0, c->stream>>>(nb, ns, xl, tail + 4 * ns, bs);
+    KCHECK();
+    // (3) row totals of every rank -> the 1-D DPs D_X(.) over the global support
+    double* vg;
+    TRY(ws(c, c->xvec, 2 * (size_t)n, &vg));
+    TRY(comm_allgather(c, Ptot, g3, 2 * sizeof(double) * (size_t)P.maxnl));
+    k_unpad<<<grid_for(P.maxnl), 256, 0, c->stream>>>(g3, R, 2 * P.maxnl, P.dtab, vg);
+    KCHECK();
+    k_unpad<<<grid_for(P.maxnl), 256, 0, c->stream>>>(g3 + P.maxnl, R, 2 * P.maxnl, P.dtab, vg + n);
+    KCHECK();
+    DPsrc = vg;
+    DAsrc = vg + n;
+    xs_rows = P.xc;
+    nrows_dp = n;
+  }
   Scan1DBatch B;
   memset(&B, 0, sizeof(B));
   B.d[0] = Scan1D{btot, P.yc, m, SAg, nullptr, nullptr};
   B.d[1] = Scan1D{cxend, P.yc, m, WAg, nullptr, nullptr};
-  B.d[2] = Scan1D{Ptot, xl, nl, nullptr, DP, nullptr};
-  B.d[3] = Scan1D{Aend, xl, nl, nullptr, DA, nullptr};
+  B.d[2] = Scan1D{DPsrc, xs_rows, nrows_dp, nullptr, DP, nullptr};
+  B.d[3] = Scan1D{DAsrc, xs_rows, nrows_dp, nullptr, DA, nullptr};
   k_scan1d<<<4, 1024, 0, c->stream>>>(B);
   KCHECK();
   PROF_END(c, PC_GRAD_CARRY, 4);
   MainArgs a;
   a.S = S; a.nl = nl; a.m = m; a.nb = nb; a.ns = ns;
-  a.xl = xl; a.yc = P.yc; a.cl = P.cx + P.row0; a.c2 = P.cy; a.DP = DP; a.DA = DA; a.SAg = SAg; a.WAg = WAg;
+  a.xl = xl; a.yc = P.yc; a.cl = P.cx + P.row0; a.c2 = P.cy;
+  a.DP = R > 1 ? DP + P.row0 : DP; a.DA = R > 1 ? DA + P.row0 : DA;
+  a.SAg = SAg; a.WAg = WAg;
   a.rP = rP; a.rA = rA; a.cS = cS; a.cX = cX; a.bs = bs; a.xlast = P.xlast; a.ylast = P.ylast;
   a.G = G; a.ldG = ldG; a.tile_obj = tobj; a.tile_ent = tent; a.tile_cc = tcc;
   a.fx = fx ? fx + P.row0 : nullptr; a.fy = fy; a.alpha = alpha;
@@ -456,15 +607,15 @@ static gw_status grad_pass(gw_ctx* c, const Prepared& P, int mode, const TSrc& S
   KCHECK();
   PROF_END(c, pc_main, 1);
   if (obj) {
-    k_objective<<<1, 1024, 0, c->stream>>>(Ptot, xl, P.pn + P.row0, P.cx + P.row0, nl, btot, P.yc, P.qn, P.cy, m,
-                                           tobj, (int64_t)nb * ns, tent, objout_dev);
+    double *part, *gpart;
+    TRY(ws(c, c->xpart, 8 * (size_t)(R + 1), &part));
+    gpart = part + 8;
+    k_obj_partial<<<1, 1024, 0, c->stream>>>(Ptot, xl, P.pn + P.row0, P.cx + P.row0, nl, tobj, (int64_t)nb * ns,
+                                             tent, fx ? tcc : nullptr, part);
     KCHECK();
-    if (fx) {
-      // <C o C, T> for FGW: reuse k_objective's tile sum slot via a second call on tcc
-      k_objective<<<1, 1024, 0, c->stream>>>(Ptot, xl, P.pn + P.row0, P.cx + P.row0, nl, btot, P.yc, P.qn, P.cy,
-                                             m, tcc, (int64_t)nb * ns, nullptr, objout_dev + 4);
-      KCHECK();
-    }
+    TRY(comm_allgather(c, part, gpart, 8 * sizeof(double)));
+    k_obj_final<<<1, 1024, 0, c->stream>>>(gpart, R, btot, P.yc, P.qn, P.cy, m, objout_dev);
+    KCHECK();
   }
   return GW_OK;
 }
@@ -476,8 +627,6 @@ extern "C" gw_status gw_grad_dp(gw_ctx* c, const gw_problem* pb, const void* T, 
   TRY(check_problem(pb));
   TRY(check_matrix(T, ldT, pb->m, "T"));
   TRY(check_matrix(G, ldG, pb->m, "G"));
-  if (c->comm && c->comm->nranks > 1)
-    return fail(GW_ERR_UNSUPPORTED, "gw_grad_dp: multi-rank gradient goes through entropic_gw_solve");
   CU(cudaSetDevice(c->device));
   Prepared P;
   TRY(prepare(c, pb, P));
@@ -506,6 +655,9 @@ struct SinkState {
   float* pf;      // [nl] p as fp32
   int fK = 0, fCL = 0, fNT = 256, fncl = 0;  // fK == 0: fast path unavailable for this shape
   int64_t frpc = 0;
+  // column-sum exchange: this rank's column LSE pairs / column sums, and all ranks' (gathered)
+  double *lse, *lseg, *csl, *csg;
+  float* violg;
 };
 
 template <int K, int CL, int NT>
@@ -582,6 +734,17 @@ static gw_status sink_alloc(gw_ctx* c, const Prepared& P, SinkState& s) {
   s.RB = RB;
   s.nrb = (int)std::max<int64_t>(1, (P.nl + RB - 1) / RB);
   TRY(ws(c, c->part, (size_t)s.nrb * P.m, &s.part));
+  TRY(ws(c, c->slse, 2 * (size_t)P.m, &s.lse));
+  TRY(ws(c, c->scsl, (size_t)P.m, &s.csl));
+  if (P.R > 1) {
+    TRY(ws(c, c->slseg, 2 * (size_t)P.m * P.R, &s.lseg));
+    TRY(ws(c, c->scsg, (size_t)P.m * P.R, &s.csg));
+    TRY(ws(c, c->sviolg, (size_t)P.R, &s.violg));
+  } else {
+    s.lseg = s.lse;
+    s.csg = s.csl;
+    s.violg = nullptr;
+  }
   // fused fast path: cluster of CL CTAs x W = 1024 K columns spans a row
   int* md;
   TRY(ws(c, c->mode, 4, &md));
@@ -631,8 +794,19 @@ static gw_status sink_split(gw_ctx* c, const Prepared& P, SinkState& s, double e
   return GW_OK;
 }
 
+// Violation measured by a row half-step is a per-rank max: make it global (all ranks agree).
+static gw_status sink_viol_global(gw_ctx* c, const Prepared& P, SinkState& s) {
+  if (P.R == 1) return GW_OK;
+  TRY(comm_allgather(c, s.viol, s.violg, sizeof(float)));
+  k_max_f<<<1, 32, 0, c->stream>>>(s.violg, P.R, s.viol);
+  KCHECK();
+  return GW_OK;
+}
+
 // `iters` Sinkhorn iterations on G.  tol > 0: check every `check_every` iterations (one
 // host sync per check); returns the iterations used and whether tol was met.
+// Multi-rank: f is per-shard, g replicated; every column half-step gathers the ranks' column
+// sums (the only exchange), and every rank reaches the same path decision and stop flag.
 static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const float* G, int64_t ldG, double eps,
                           int iters, double tol, int check_every, int* used, int* converged, bool reset_count = true) {
   const int64_t nl = P.nl, m = P.m;
@@ -670,13 +844,17 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
       KCHECK();
       PROF_END(c, PC_SINK_ROW, 1);
       if (check) {
+        TRY(sink_viol_global(c, P, s));
         k_sink_commit<<<grid_for(nl), 256, 0, c->stream>>>(s.viol, tol, s.stop, s.ftmp, s.f, nl, s.iters, done);
         KCHECK();
       }
       PROF_BEGIN(c, PC_SINK_COL);
       k_sink_col<<<cgrid, 256, 0, c->stream>>>(G, ldG, nl, m, s.fh, s.fl, c2f, s.RB, s.part, s.stop, skip);
       KCHECK();
-      k_sink_colfin<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.part, s.nrb, m, P.lq, eps, s.g, s.gh, s.gl,
+      k_sink_colmerge<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.part, s.nrb, m, s.lse, s.stop, skip);
+      KCHECK();
+      TRY(comm_allgather(c, s.lse, s.lseg, 2 * sizeof(double) * (size_t)m));
+      k_sink_colfin<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.lseg, P.R, m, P.lq, eps, s.g, s.gh, s.gl,
                                                                        s.stop, skip, s.dev);
       KCHECK();
       PROF_END(c, PC_SINK_COL, 2);
@@ -684,8 +862,11 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
         PROF_BEGIN(c, PC_SINK_FUSED);
         TRY(fused_launch(c, s.fK, s.fCL, s.fNT, fa, s.fncl));
         KCHECK();
+        k_sink_colsum<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.fpart, s.fncl, m, s.csl, s.mode, s.stop);
+        KCHECK();
+        TRY(comm_allgather(c, s.csl, s.csg, sizeof(double) * (size_t)m));
         k_sink_fin_fast<<<grid_for(std::max(m, nl), 256, 1 << 30), 256, 0, c->stream>>>(
-            s.Srow, nl, P.lp + P.row0, s.f, s.fh, s.fl, nullptr, s.fpart, s.fncl, m, P.lq, eps, s.g, s.gh, s.gl,
+            s.Srow, nl, P.lp + P.row0, s.f, s.fh, s.fl, nullptr, s.csg, P.R, m, P.lq, eps, s.g, s.gh, s.gl,
             s.mode, s.stop, s.dev);
         KCHECK();
         PROF_END(c, PC_SINK_FUSED, 2);
@@ -713,6 +894,7 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
     k_sink_row<<<(unsigned)((nl + RROWS - 1) / RROWS), 256, 0, c->stream>>>(
         G, ldG, nl, m, s.gh, s.gl, c2f, s.f, s.ftmp, P.lp + P.row0, eps, s.fh, s.fl, s.viol, nullptr, nullptr);
     KCHECK();
+    TRY(sink_viol_global(c, P, s));
     float hv;
     CU(cudaMemcpyAsync(&hv, s.viol, sizeof(float), cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
@@ -765,8 +947,6 @@ extern "C" gw_status sinkhorn_solve(gw_ctx* c, const gw_problem* pb, const void*
   TRY(check_problem(pb));
   TRY(check_matrix(G, ldG, pb->m, "G"));
   if (T_out) TRY(check_matrix(T_out, ldT, pb->m, "T_out"));
-  if (c->comm && c->comm->nranks > 1)
-    return fail(GW_ERR_UNSUPPORTED, "sinkhorn_solve: multi-rank Sinkhorn goes through entropic_gw_solve");
   CU(cudaSetDevice(c->device));
   Prepared P;
   TRY(prepare(c, pb, P));
@@ -795,6 +975,7 @@ extern "C" gw_status sinkhorn_solve(gw_ctx* c, const gw_problem* pb, const void*
         reinterpret_cast<const float*>(G), ldG, P.nl, P.m, s.gh, s.gl, c2f, s.f, s.ftmp, P.lp + P.row0, o->eps, s.fh,
         s.fl, s.viol, nullptr, nullptr);
     KCHECK();
+    TRY(sink_viol_global(c, P, s));
     float hv;
     CU(cudaMemcpyAsync(&hv, s.viol, sizeof(float), cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
@@ -823,8 +1004,6 @@ static gw_status solve_impl(gw_ctx* c, const gw_problem* pb, const gw_solve_opts
   TRY(check_problem(pb));
   if (T0) TRY(check_matrix(T0, ldT, pb->m, "T0"));
   if (T_out) TRY(check_matrix(T_out, ldT, pb->m, "T_out"));
-  if (c->comm && c->comm->nranks > 1)
-    return fail(GW_ERR_UNSUPPORTED, "multi-rank solve: not in this build");
   CU(cudaSetDevice(c->device));
   const double eps = o->eps;
   Prepared P;

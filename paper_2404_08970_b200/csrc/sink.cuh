@@ -169,16 +169,14 @@ __global__ void __launch_bounds__(256) k_sink_col(const float* __restrict__ G, i
     if (q0 + k < m) part[rb * m + q0 + k] = make_float2(st[k].m, st[k].s);
 }
 
-// Column half-step, pass 2: merge the row-block partials in fixed order and update g.
-__global__ void k_sink_colfin(const float2* __restrict__ part, int nrb, int64_t m, const double* __restrict__ lq,
-                              double eps, double* __restrict__ g, float* __restrict__ gh, float* __restrict__ gl,
-                              const int* __restrict__ stop, const int* __restrict__ skip_if_fast,
-                              float* __restrict__ dev) {
+// Column half-step, pass 2a: merge this rank's row-block partials in fixed order, in fp64:
+// lse[q] = max_rb M, lse[m + q] = sum_rb S_rb 2^(M_rb - max).
+__global__ void k_sink_colmerge(const float2* __restrict__ part, int nrb, int64_t m, double* __restrict__ lse,
+                                const int* __restrict__ stop, const int* __restrict__ skip_if_fast) {
   if (stop && *stop) return;
   if (skip_if_fast && *skip_if_fast) return;
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (q >= m) return;
-  // fp64 merge for accuracy
   double M = -INFINITY;
   for (int rb = 0; rb < nrb; ++rb) M = fmax(M, (double)part[(int64_t)rb * m + q].x);
   double S = 0.0;
@@ -186,6 +184,28 @@ __global__ void k_sink_colfin(const float2* __restrict__ part, int nrb, int64_t 
     for (int rb = 0; rb < nrb; ++rb) {
       const float2 v = part[(int64_t)rb * m + q];
       if (v.x != -INFINITY) S += (double)v.y * exp2((double)v.x - M);
+    }
+  lse[q] = M;
+  lse[m + q] = S;
+}
+
+// Column half-step, pass 2b: merge the R ranks' (M, S) pairs (gath [R][2m]) in rank order and
+// update g (identical on every rank).
+__global__ void k_sink_colfin(const double* __restrict__ gath, int R, int64_t m, const double* __restrict__ lq,
+                              double eps, double* __restrict__ g, float* __restrict__ gh, float* __restrict__ gl,
+                              const int* __restrict__ stop, const int* __restrict__ skip_if_fast,
+                              float* __restrict__ dev) {
+  if (stop && *stop) return;
+  if (skip_if_fast && *skip_if_fast) return;
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= m) return;
+  double M = -INFINITY;
+  for (int r = 0; r < R; ++r) M = fmax(M, gath[(int64_t)r * 2 * m + q]);
+  double S = 0.0;
+  if (M != -INFINITY)
+    for (int r = 0; r < R; ++r) {
+      const double Mr = gath[(int64_t)r * 2 * m + q];
+      if (Mr != -INFINITY) S += gath[(int64_t)r * 2 * m + m + q] * exp2(Mr - M);
     }
   const double lse2 = M + log2(S);
   const double gn = (lq[q] == -INFINITY) ? -INFINITY : eps * lq[q] - eps * GW_LN2 * lse2;
@@ -201,6 +221,17 @@ __global__ void k_sink_colfin(const float2* __restrict__ part, int nrb, int64_t 
   const float h = (float)gs;
   gh[q] = h;
   gl[q] = isfinite(gs) ? (float)(gs - (double)h) : 0.f;
+}
+
+// Fused path: this rank's column sums of the half-step plan, clusters summed in fixed order.
+__global__ void k_sink_colsum(const double* __restrict__ part, int ncl, int64_t m, double* __restrict__ out,
+                              const int* __restrict__ mode, const int* __restrict__ stop) {
+  if (*mode != 1 || (stop && *stop)) return;
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= m) return;
+  double CS = 0.0;
+  for (int c = 0; c < ncl; ++c) CS += part[(int64_t)c * m + q];
+  out[q] = CS;
 }
 
 // Tolerance rule (reading R8): the row half-step of iteration k+1 measured the violation of

@@ -141,21 +141,22 @@ __global__ void k_fill(double* __restrict__ v, int64_t n, double val) {
 }
 
 // ---------------------------------------------------------------------------------
-// Objective assembly from the gradient pass's reductions (one CTA, deterministic).
+// Objective assembly from the gradient pass's reductions (deterministic, fixed order).
 // With G' = 2(c 1^T + 1 c'^T) - 4 V (prescribed c, c'), V = D_X T D_Y:
 //   <V, T> = (2<c, a> + 2<c', b> - <G', T>) / 4,
 //   E(T)   = a^T (D_X o D_X) a + b^T (D_Y o D_Y) b - 2 <V, T>      (PAPER.md:86 expanded)
 // and a^T (D o D) a = 2 (A0 A2 - A1^2), A_k = sum xc^k a (moments; k = 1).
 // viol = max(|a - p|_inf, |b - q|_inf).
-// out: {E, viol, <G',T>, H}
+// k_obj_partial: this rank's row sums a = T 1 (local rows) and tile sums ->
+//   part[8] = {A0, A1, A2, <c, a>, max|a - p|, <G', T>, H, <C o C, T>}
+// k_obj_final: sums the R ranks' partials in rank order, adds the column part (b = T^T 1 is
+// global) -> out = {E, viol, <G', T>, H, -, -, <C o C, T>, -}.
 // ---------------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) k_objective(const double* __restrict__ a, const double* __restrict__ xc,
-                                                    const double* __restrict__ p, const double* __restrict__ c,
-                                                    int64_t n, const double* __restrict__ b,
-                                                    const double* __restrict__ yc, const double* __restrict__ q,
-                                                    const double* __restrict__ c2, int64_t m,
-                                                    const double* __restrict__ tile_obj, int64_t ntile,
-                                                    const double* __restrict__ tile_ent, double* __restrict__ out) {
+__global__ void __launch_bounds__(1024) k_obj_partial(const double* __restrict__ a, const double* __restrict__ xc,
+                                                      const double* __restrict__ p, const double* __restrict__ c,
+                                                      int64_t n, const double* __restrict__ tile_obj, int64_t ntile,
+                                                      const double* __restrict__ tile_ent,
+                                                      const double* __restrict__ tile_cc, double* __restrict__ part) {
   __shared__ double sm[32];
   double A0 = 0, A1 = 0, A2 = 0, ca = 0, va = 0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
@@ -163,36 +164,60 @@ __global__ void __launch_bounds__(1024) k_objective(const double* __restrict__ a
     A0 += ai; A1 += ai * xi; A2 += ai * xi * xi; ca += c[i] * ai;
     va = fmax(va, fabs(ai - p[i]));
   }
+  double go = 0, he = 0, cc = 0;
+  for (int64_t i = threadIdx.x; i < ntile; i += blockDim.x) {
+    go += tile_obj[i];
+    if (tile_ent) he += tile_ent[i];
+    if (tile_cc) cc += tile_cc[i];
+  }
+  A0 = block_sum<32>(A0, sm); A1 = block_sum<32>(A1, sm); A2 = block_sum<32>(A2, sm);
+  ca = block_sum<32>(ca, sm);
+  go = block_sum<32>(go, sm); he = block_sum<32>(he, sm); cc = block_sum<32>(cc, sm);
+  __shared__ double smx[32];
+  double vmax = va;
+  for (int d = 16; d > 0; d >>= 1) vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, d));
+  if ((threadIdx.x & 31) == 0) smx[threadIdx.x >> 5] = vmax;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) smx[0] = fmax(smx[0], smx[k]);
+    part[0] = A0; part[1] = A1; part[2] = A2; part[3] = ca; part[4] = smx[0];
+    part[5] = go; part[6] = he; part[7] = cc;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_obj_final(const double* __restrict__ parts, int R,
+                                                    const double* __restrict__ b, const double* __restrict__ yc,
+                                                    const double* __restrict__ q, const double* __restrict__ c2,
+                                                    int64_t m, double* __restrict__ out) {
+  __shared__ double sm[32];
   double B0 = 0, B1 = 0, B2 = 0, cb = 0, vb = 0;
   for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
     const double bi = b[i], yi = yc[i];
     B0 += bi; B1 += bi * yi; B2 += bi * yi * yi; cb += c2[i] * bi;
     vb = fmax(vb, fabs(bi - q[i]));
   }
-  double go = 0, he = 0;
-  for (int64_t i = threadIdx.x; i < ntile; i += blockDim.x) {
-    go += tile_obj[i];
-    if (tile_ent) he += tile_ent[i];
-  }
-  A0 = block_sum<32>(A0, sm); A1 = block_sum<32>(A1, sm); A2 = block_sum<32>(A2, sm);
   B0 = block_sum<32>(B0, sm); B1 = block_sum<32>(B1, sm); B2 = block_sum<32>(B2, sm);
-  ca = block_sum<32>(ca, sm); cb = block_sum<32>(cb, sm);
-  go = block_sum<32>(go, sm); he = block_sum<32>(he, sm);
-  // max reduction (order independent)
+  cb = block_sum<32>(cb, sm);
   __shared__ double smx[32];
-  double vmax = fmax(va, vb);
+  double vmax = vb;
   for (int d = 16; d > 0; d >>= 1) vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, d));
   if ((threadIdx.x & 31) == 0) smx[threadIdx.x >> 5] = vmax;
   __syncthreads();
-  if (threadIdx.x == 0)
-    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) smx[0] = fmax(smx[0], smx[k]);
   if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) smx[0] = fmax(smx[0], smx[k]);
+    double A0 = 0, A1 = 0, A2 = 0, ca = 0, va = 0, go = 0, he = 0, cc = 0;
+    for (int r = 0; r < R; ++r) {
+      const double* pr = parts + 8 * r;
+      A0 += pr[0]; A1 += pr[1]; A2 += pr[2]; ca += pr[3]; va = fmax(va, pr[4]);
+      go += pr[5]; he += pr[6]; cc += pr[7];
+    }
     const double VT = (2.0 * ca + 2.0 * cb - go) / 4.0;
     const double E = 2.0 * (A0 * A2 - A1 * A1) + 2.0 * (B0 * B2 - B1 * B1) - 2.0 * VT;
     out[0] = E;
-    out[1] = smx[0];
+    out[1] = fmax(va, smx[0]);
     out[2] = go;
     out[3] = he;
+    out[6] = cc;
   }
 }
 

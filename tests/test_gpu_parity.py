@@ -283,3 +283,33 @@ def test_solver_uses_fused_path(gw):
     assert r.inner_fused_total > 200
     ro = O.entropic_gw(P.x, P.y, P.p, P.q, P.eps, 4, 100)
     assert abs(r.gw_objective - ro["gw_objective"]) <= OBJ_TOL * abs(ro["gw_objective"])
+
+
+# ----------------------------------------------------------------------------- FGW (Remark 2)
+
+def _c5_small(n=512, m=384, outer=5, inner=100):
+    P = W.config5(n, m)
+    P.outer, P.inner = outer, inner
+    return P
+
+
+@pytest.mark.parametrize("alpha", [0.5, 0.0, 1.0])
+def test_fgw_solver_c5_recipe_reduced(gw, alpha):
+    """fgw_solve vs oracle.entropic_fgw (reading R29) on C5's distributions at
+    a reduced size: objective trajectory and final violation."""
+    P = _c5_small()
+    r = gw.solve(P.x, P.y, P.p, P.q, P.eps, P.outer, P.inner, fx=P.fx, fy=P.fy, alpha=alpha,
+                 trace_objective=True, device=_dev())
+    ro = O.entropic_fgw(P.x, P.y, P.p, P.q, P.fx, P.fy, alpha, P.eps, P.outer, P.inner)
+    E = np.asarray(ro["E"])
+    assert np.max(np.abs(r.trace[:, 0] - E) / np.abs(E)) <= OBJ_TOL
+    assert abs(r.gw_objective - ro["gw_objective"]) <= OBJ_TOL * abs(ro["gw_objective"])
+    assert r.marginal_violation <= max(VIOL_TOL, 2 * ro["viol"][-1])
+
+
+def test_fgw_alpha_one_is_gw(gw):
+    """alpha = 1 reduces FGW to GW (Remark 2): same trajectory as entropic_gw_solve."""
+    P = _c5_small(300, 256, 4, 60)
+    a = gw.solve(P.x, P.y, P.p, P.q, P.eps, P.outer, P.inner, fx=P.fx, fy=P.fy, alpha=1.0, device=_dev())
+    b = gw.solve(P.x, P.y, P.p, P.q, P.eps, P.outer, P.inner, device=_dev())
+    assert abs(a.gw_objective - b.gw_objective) <= 1e-6 * abs(b.gw_objective)
