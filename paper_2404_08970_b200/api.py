@@ -207,16 +207,18 @@ def solve(x, y, p, q, eps, outer, inner, tol=0.0, check_every=10, T0=None, retur
 
 
 def solve_host(x, y, p, q, eps, outer, inner, tol=0.0, check_every=10, device=None, ctx=None,
-               fx=None, fy=None, alpha=None):
+               fx=None, fy=None, alpha=None, row0=0, n_local=None):
     """entropic_gw_solve with HOST vectors (GW_HOST_VECTORS): the library stages x, y, p, q
-    host->device and copies the duals f, g back.  This is the end-to-end public call."""
+    host->device and copies the duals f, g back.  This is the end-to-end public call.
+    Sharded: as solve() (f holds this rank's n_local rows)."""
     ctx = ctx or Context.get(device)
     xs, ys, ps, qs = (np.ascontiguousarray(v, dtype=np.float64) for v in (x, y, p, q))
     n, m = xs.size, ys.size
-    f = np.empty(n)
+    nl = n if n_local is None else int(n_local)
+    f = np.empty(nl)
     g = np.empty(m)
     pr = L.gw_problem()
-    pr.n, pr.m, pr.row0, pr.n_local = n, m, 0, n
+    pr.n, pr.m, pr.row0, pr.n_local = n, m, int(row0), nl
     pr.x, pr.y, pr.p, pr.q = (a.ctypes.data for a in (xs, ys, ps, qs))
     pr.k, pr.loss, pr.dtype, pr.flags = 1, L.GW_LOSS_SQUARE, L.GW_F32, L.GW_HOST_VECTORS
     o = _opts(eps, outer, inner, tol, check_every, False)
