@@ -377,6 +377,210 @@ __global__ void __launch_bounds__(NT, 1) k_sink_fused(FusedArgs a) {
   cluster_wait();
 }
 
+__device__ __forceinline__ void st_async_v2f32(uint32_t raddr, float v0, float v1, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+               "f"(v0), "f"(v1), "r"(rbar)
+               : "memory");
+}
+
+// Row-pair variant of k_sink_fused: one step exponentiates TWO rows and exchanges both partial
+// row sums in one 8-byte st.async per peer, and the consumer reduces both in one pass, so the
+// per-row exchange, barrier and loop overhead (~2/3 of a warp's instructions per row at
+// K = 4) is paid once per two rows.  Same arithmetic per element, same fixed reduction order.
+template <int K, int CL, int NT>
+__global__ void __launch_bounds__(NT, 1) k_sink_fused2(FusedArgs a) {
+  if (*a.mode != 1 || (a.stop && *a.stop)) return;  // uniform across the cluster
+  constexpr int NW = NT / 32;
+  constexpr int W = 4 * K * NT;
+  constexpr int NSLOT = 4;       // exchange slots (pairs; power of 2)
+  constexpr int NX = CL * NW;    // partial pairs per row pair
+  extern __shared__ __align__(128) float ring[];  // [FSTAGES][W], then acc64 [K][4][NT] (fp64)
+  double* acc64 = reinterpret_cast<double*>(ring + (size_t)FSTAGES * W);
+  __shared__ __align__(8) uint64_t full[FSTAGES];
+  __shared__ unsigned int scnt[FSTAGES];
+  __shared__ __align__(8) uint64_t xbar[NSLOT];
+  __shared__ __align__(16) float2 xs[NSLOT][NX];  // [slot][rank * NW + warp] = {S_j0 part, S_j1 part}
+
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const uint32_t cr = blockIdx.x % CL;
+  const int64_t cid = blockIdx.x / CL;
+  const int64_t m = a.m;
+  const int64_t c0 = (int64_t)cr * W;
+  const int64_t ncol = max((int64_t)0, min((int64_t)W, m - c0));
+  const uint32_t bytes = (uint32_t)(((ncol + 3) & ~int64_t(3)) * 4);
+  const int64_t rb = cid * a.rows_per_cluster;
+  const int64_t re = min(a.nl, rb + a.rows_per_cluster);
+  const int nrows = (int)max((int64_t)0, re - rb);
+  const int npairs = (nrows + 1) >> 1;
+  constexpr uint32_t xbytes = 8u * NX;
+  const float* __restrict__ Gbase = a.G + rb * a.ld + c0;
+  const int64_t ld = a.ld;
+
+  if (t == 0) {
+    for (int s = 0; s < FSTAGES; ++s) {
+      mbar_init(&full[s], 1);
+      scnt[s] = 0u;
+    }
+    for (int s = 0; s < NSLOT; ++s) mbar_init(&xbar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < NSLOT && s < npairs; ++s) mbar_expect_tx(&xbar[s], xbytes);
+  }
+  __syncthreads();
+  cluster_arrive();
+  cluster_wait();
+
+  if (t == 0 && bytes > 0) {
+    for (int r = 0; r < FSTAGES && r < nrows; ++r) {
+      mbar_expect_tx(&full[r], bytes);
+      tma_load_1d(ring + (size_t)r * W, Gbase + (int64_t)r * ld, bytes, &full[r]);
+    }
+  }
+  const float* __restrict__ fh = a.fh + rb;
+  const float* __restrict__ pf = a.pf + rb;
+  float* __restrict__ Srow = a.Srow + rb;
+  const uint32_t peer = (uint32_t)min(lane, CL - 1);
+  const uint32_t rx0 = mapa(&xs[0][cr * NW + wid], peer), rb0 = mapa(&xbar[0], peer);
+  constexpr uint32_t XSTRIDE = sizeof(xs[0]), BSTRIDE = sizeof(uint64_t);
+  const bool full_tile = (ncol == W);
+
+  float2 ghv[K][2], acc[K][2];
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t col = c0 + 4 * (t + NT * k) + 2 * h;
+      ghv[k][h].x = col < m ? a.gh[col] : 0.f;
+      ghv[k][h].y = col + 1 < m ? a.gh[col + 1] : 0.f;
+      acc[k][h] = make_float2(0.f, 0.f);
+      acc64[(k * 4 + 2 * h) * NT + t] = 0.0;
+      acc64[(k * 4 + 2 * h + 1) * NT + t] = 0.0;
+    }
+  const float2 nc2 = make_float2(-a.c2f, -a.c2f);
+  float2 eA0[K][2], eA1[K][2], eB0[K][2], eB1[K][2];
+  float2 pA = make_float2(0.f, 0.f), pB = pA;  // marginals of the pair's two rows
+  float2 Fnx = make_float2(nrows > 0 ? fh[0] : 0.f, nrows > 1 ? fh[1] : 0.f);
+  float2 pnx = make_float2(nrows > 0 ? pf[0] : 0.f, nrows > 1 ? pf[1] : 0.f);
+
+  // exponentiate row j into e (returns the thread's partial row sum) and release its stage
+  auto do_row = [&](int j, float F, float2 (&e)[K][2]) -> float {
+    float psum = 0.f;
+    if (bytes > 0) {
+      const int st = j % FSTAGES;
+      mbar_wait(&full[st], (uint32_t)((j / FSTAGES) & 1));
+      const float4* sp = reinterpret_cast<const float4*>(ring + (size_t)st * W);
+      psum = full_tile ? fused_exp_row<K, NT, true>(sp, ghv, nc2, make_float2(F, F), e, t, c0, m)
+                       : fused_exp_row<K, NT, false>(sp, ghv, nc2, make_float2(F, F), e, t, c0, m);
+      __syncwarp();
+      if (lane == 0) {  // the last warp to release a stage refills it
+        const int nxt = j + FSTAGES;
+        if (atomicAdd(&scnt[st], 1u) == NW - 1) {
+          scnt[st] = 0u;
+          if (nxt < nrows) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(&full[st], bytes);
+            tma_load_1d(ring + (size_t)st * W, Gbase + (int64_t)nxt * ld, bytes, &full[st]);
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < K; ++k) { e[k][0] = make_float2(0.f, 0.f); e[k][1] = e[k][0]; }
+    }
+    return psum;
+  };
+
+  // Step P: rows 2P, 2P+1 (exponentiate + send), then consume pair P-1.
+  auto step = [&](int P, float2 (&c0e)[K][2], float2 (&c1e)[K][2], float2& pcur, float2 (&v0)[K][2],
+                  float2 (&v1)[K][2], float2 pprv) {
+    const int j0 = 2 * P, j1 = 2 * P + 1;
+    if (j0 < nrows) {
+      const float2 F = Fnx;
+      pcur = pnx;
+      if (j0 + 2 < nrows) Fnx.x = fh[j0 + 2], pnx.x = pf[j0 + 2];
+      if (j1 + 2 < nrows) Fnx.y = fh[j1 + 2], pnx.y = pf[j1 + 2];
+      float s0 = do_row(j0, F.x, c0e);
+      float s1 = 0.f;
+      if (j1 < nrows) {
+        s1 = do_row(j1, F.y, c1e);
+      } else {
+#pragma unroll
+        for (int k = 0; k < K; ++k) { c1e[k][0] = make_float2(0.f, 0.f); c1e[k][1] = c1e[k][0]; }
+        pcur.y = 0.f;
+      }
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) {
+        s0 += __shfl_xor_sync(0xffffffffu, s0, d);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, d);
+      }
+      const int xsl = P & (NSLOT - 1);
+      if (lane < CL) st_async_v2f32(rx0 + XSTRIDE * xsl, s0, s1, rb0 + BSTRIDE * xsl);
+    }
+    if (P > 0) {
+      const int Pp = P - 1;
+      const int psl = Pp & (NSLOT - 1);
+      mbar_wait(&xbar[psl], (uint32_t)((Pp / NSLOT) & 1));
+      float S0 = 0.f, S1 = 0.f;
+      if (NX >= 32) {
+#pragma unroll
+        for (int i = 0; i < NX / 32; ++i) {
+          const float2 v = xs[psl][lane + 32 * i];
+          S0 += v.x;
+          S1 += v.y;
+        }
+      } else if (lane < NX) {
+        const float2 v = xs[psl][lane];
+        S0 = v.x;
+        S1 = v.y;
+      }
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) {
+        S0 += __shfl_xor_sync(0xffffffffu, S0, d);
+        S1 += __shfl_xor_sync(0xffffffffu, S1, d);
+      }
+      const int jp0 = 2 * Pp, jp1 = 2 * Pp + 1;
+      if (t == 0) {
+        Srow[jp0] = S0;
+        if (jp1 < nrows) Srow[jp1] = S1;
+        if (Pp + NSLOT < npairs) mbar_expect_tx(&xbar[psl], xbytes);
+      }
+      const float w0 = pprv.x * rcp_ftz(S0);
+      const float w1 = jp1 < nrows ? pprv.y * rcp_ftz(S1) : 0.f;
+      const float2 w02 = make_float2(w0, w0), w12 = make_float2(w1, w1);
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        acc[k][0] = ffma2(v1[k][0], w12, ffma2(v0[k][0], w02, acc[k][0]));
+        acc[k][1] = ffma2(v1[k][1], w12, ffma2(v0[k][1], w02, acc[k][1]));
+      }
+      if ((Pp & (FFLUSH / 2 - 1)) == FFLUSH / 2 - 1) {
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            acc64[(k * 4 + 2 * h) * NT + t] += (double)acc[k][h].x;
+            acc64[(k * 4 + 2 * h + 1) * NT + t] += (double)acc[k][h].y;
+            acc[k][h] = make_float2(0.f, 0.f);
+          }
+      }
+    }
+  };
+  for (int P = 0; P <= npairs; P += 2) {
+    step(P, eA0, eA1, pA, eB0, eB1, pB);
+    if (P + 1 <= npairs) step(P + 1, eB0, eB1, pB, eA0, eA1, pA);
+  }
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t col = c0 + 4 * (t + NT * k) + 2 * h;
+      const double v0 = acc64[(k * 4 + 2 * h) * NT + t] + (double)acc[k][h].x;
+      const double v1 = acc64[(k * 4 + 2 * h + 1) * NT + t] + (double)acc[k][h].y;
+      if (col < m) a.part[cid * m + col] = v0;
+      if (col + 1 < m) a.part[cid * m + col + 1] = v1;
+    }
+  cluster_arrive();
+  cluster_wait();
+}
+
 // Finish of the fused iteration (one thread per row and per column, fixed order):
 //   rows    f_i <- f_i + eps (ln p_i - ln S_i);  viol = max_i |S_i - p_i|
 //   columns CS_p = sum over clusters, g_p <- g_p + eps (ln q_p - ln CS_p);

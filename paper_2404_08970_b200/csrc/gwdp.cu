@@ -665,6 +665,7 @@ static gw_status fused_config_t(gw_ctx* c, int* ncl) {
   auto kern = k_sink_fused<K, CL, NT>;
   const size_t dsm = fused_dyn_smem<K, NT>();
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+  CU(cudaFuncSetAttribute(k_sink_fused2<K, CL, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(148 * CL);
   cfg.blockDim = dim3(NT);
@@ -690,7 +691,9 @@ static gw_status fused_launch_t(gw_ctx* c, const FusedArgs& fa, int ncl) {
   at[0].val.clusterDim.x = CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  CU(cudaLaunchKernelEx(&cfg, k_sink_fused<K, CL, NT>, fa));
+  static const bool v1 = getenv("GWDP_FUSED_V1") != nullptr;  // single-row variant (comparison)
+  if (v1) CU(cudaLaunchKernelEx(&cfg, k_sink_fused<K, CL, NT>, fa));
+  else CU(cudaLaunchKernelEx(&cfg, k_sink_fused2<K, CL, NT>, fa));
   return GW_OK;
 }
 
@@ -754,7 +757,7 @@ static gw_status sink_alloc(gw_ctx* c, const Prepared& P, SinkState& s) {
   const char* env = getenv("GWDP_NO_FUSED");
   if (!(env && env[0] == '1') && P.nl > 0) {
     const char* nte = getenv("GWDP_FUSED_NT");
-    const int NT = (nte && atoi(nte) == 256) ? 256 : 512;
+    const int NT = (nte && atoi(nte) == 512) ? 512 : 256;
     const int kmax = 8192 / (4 * NT);  // K at W = 8192 columns per CTA
     int K, CL;
     if (P.m <= 8192) {
