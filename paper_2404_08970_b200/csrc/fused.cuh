@@ -23,7 +23,10 @@
 
 namespace gw {
 
-constexpr int FSTAGES = 5;             // TMA ring depth (rows)
+// TMA ring depth (rows): 5 stages of 32 KB at 256 threads; 4 at 512 threads, whose larger exchange
+// slots would not leave room for a fifth next to the 64 KB of fp64 column accumulators
+template <int NT>
+__host__ __device__ constexpr int fstages() { return NT >= 512 ? 4 : 5; }
 constexpr int FFLUSH = 32;             // rows between fp32 -> fp64 column-accumulator flushes
 
 struct FusedArgs {
@@ -157,7 +160,7 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
 // fp64 column accumulators [K][4][NT] (conflict-free: lane-contiguous doubles).
 template <int K, int NT>
 constexpr size_t fused_dyn_smem() {
-  return (size_t)FSTAGES * 4 * K * NT * sizeof(float) + (size_t)4 * K * NT * sizeof(double);
+  return (size_t)fstages<NT>() * 4 * K * NT * sizeof(float) + (size_t)4 * K * NT * sizeof(double);
 }
 
 // Exponentiate one row slice: e = 2^(fma(G, -log2e/eps, gh) + F) for the thread's 4K columns
@@ -209,6 +212,7 @@ __global__ void __launch_bounds__(NT, 1) k_sink_fused(FusedArgs a) {
   if (*a.mode != 1 || (a.stop && *a.stop)) return;  // uniform across the cluster
   constexpr int NW = NT / 32;
   constexpr int W = 4 * K * NT;
+  constexpr int FSTAGES = fstages<NT>();
   constexpr int NSLOT = 4;       // exchange slots (power of 2)
   constexpr int NX = CL * NW;    // partials per row
   extern __shared__ __align__(128) float ring[];  // [FSTAGES][W], then acc64 [K][4][NT] (fp64)
@@ -392,6 +396,7 @@ __global__ void __launch_bounds__(NT, 1) k_sink_fused2(FusedArgs a) {
   if (*a.mode != 1 || (a.stop && *a.stop)) return;  // uniform across the cluster
   constexpr int NW = NT / 32;
   constexpr int W = 4 * K * NT;
+  constexpr int FSTAGES = fstages<NT>();
   constexpr int NSLOT = 4;       // exchange slots (pairs; power of 2)
   constexpr int NX = CL * NW;    // partial pairs per row pair
   extern __shared__ __align__(128) float ring[];  // [FSTAGES][W], then acc64 [K][4][NT] (fp64)
@@ -585,13 +590,50 @@ __global__ void __launch_bounds__(NT, 1) k_sink_fused2(FusedArgs a) {
 //   rows    f_i <- f_i + eps (ln p_i - ln S_i);  viol = max_i |S_i - p_i|
 //   columns CS_p = sum over clusters, g_p <- g_p + eps (ln q_p - ln CS_p);
 //           |log2(CS_p / q_p)| -> dev (path decision).
+// Validity of a (speculative) fused iteration, before anything is committed: every row sum S_i and
+// every column sum CS_p must be finite and above 2^-100 (no overflow of an exponential, no row or
+// column whose terms all underflowed).  Then the absorbed-dual update equals the log-domain one up
+// to fp32 rounding of sums of positive terms.  flag |= 1 otherwise (order-independent OR).
+__global__ void k_sink_fast_check(const float* __restrict__ Srow, int64_t nl, const double* __restrict__ part,
+                                  int ncl, int64_t m, const double* __restrict__ lq, int* __restrict__ flag,
+                                  const int* __restrict__ mode, const int* __restrict__ stop) {
+  if (*mode != 1 || (stop && *stop)) return;
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  bool bad = false;
+  if (q < nl) {
+    const float S = Srow[q];
+    bad |= !(S > 7.9e-31f && S < 3.0e38f);
+  }
+  if (q < m && lq[q] != -INFINITY) {
+    double CS = 0.0;
+    for (int c = 0; c < ncl; ++c) CS += part[(int64_t)c * m + q];
+    bad |= !(CS > 7.9e-31 && CS < 1e300);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+// OR of the ranks' gathered validity flags (multi-rank), in place into flag[0]
+__global__ void k_or_flags(int* __restrict__ flag, const int* __restrict__ gath, int R) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    int v = 0;
+    for (int r = 0; r < R; ++r) v |= gath[r];
+    *flag = v;
+  }
+}
+
 __global__ void k_sink_fin_fast(const float* __restrict__ Srow, int64_t nl, const double* __restrict__ lp,
                                 double* __restrict__ f, float* __restrict__ fh, float* __restrict__ fl,
                                 float* __restrict__ viol, const double* __restrict__ part, int ncl, int64_t m,
                                 const double* __restrict__ lq, double eps, double* __restrict__ g,
                                 float* __restrict__ gh, float* __restrict__ gl, int* __restrict__ mode,
-                                const int* __restrict__ stop, float* __restrict__ dev) {
+                                const int* __restrict__ stop, float* __restrict__ dev, const int* __restrict__ flag) {
   if (*mode != 1 || (stop && *stop)) return;
+  if (*flag) {
+    // speculation failed: nothing is committed and this iteration runs the safe path instead
+    __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x == 0) *mode = 0;
+    return;
+  }
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   float dv = 0.f, vv = 0.f;
   if (q < m) {

@@ -100,6 +100,7 @@ struct gw_ctx {
   Buf pnf, qnf;  // fp32 marginals
   Buf xtab, xg1, xg2, xin, xvec, xtail, xpart;  // multi-rank exchange buffers
   Buf slse, slseg, scsl, scsg, sviolg;          // Sinkhorn column-sum exchange
+  Buf sflag, sflagg;
   Buf fsc, gsc;  // scaled duals for the Gibbs regeneration
   Buf Gs;        // solver cost buffer
   double* hpin = nullptr;  // pinned host scratch (64 doubles)
@@ -108,7 +109,7 @@ struct gw_ctx {
                 &ftmp, &viol, &stop, &iters, &part, &fpart, &mode, &srow, &pfl, &rP, &rA, &cS, &cX, &blk, &bs, &btot, &cxend,
                 &SAg, &WAg, &Ptot, &Aend, &DP, &DA, &tobj, &tent, &tcc, &objout, &fxs, &fys, &fsc, &gsc, &Gs,
                 &pnf, &qnf, &xtab, &xg1, &xg2, &xin, &xvec, &xtail, &xpart, &slse, &slseg, &scsl, &scsg,
-                &sviolg};
+                &sviolg, &sflag, &sflagg};
     for (Buf* x : b) all.push_back(x);
   }
 };
@@ -658,6 +659,7 @@ struct SinkState {
   // column-sum exchange: this rank's column LSE pairs / column sums, and all ranks' (gathered)
   double *lse, *lseg, *csl, *csg;
   float* violg;
+  int *flag, *flagg;  // speculation validity flag (and the ranks' flags)
 };
 
 template <int K, int CL, int NT>
@@ -739,6 +741,8 @@ static gw_status sink_alloc(gw_ctx* c, const Prepared& P, SinkState& s) {
   TRY(ws(c, c->part, (size_t)s.nrb * P.m, &s.part));
   TRY(ws(c, c->slse, 2 * (size_t)P.m, &s.lse));
   TRY(ws(c, c->scsl, (size_t)P.m, &s.csl));
+  TRY(ws(c, c->sflag, 4, &s.flag));
+  TRY(ws(c, c->sflagg, (size_t)P.R + 4, &s.flagg));
   if (P.R > 1) {
     TRY(ws(c, c->slseg, 2 * (size_t)P.m * P.R, &s.lseg));
     TRY(ws(c, c->scsg, (size_t)P.m * P.R, &s.csg));
@@ -816,8 +820,10 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
   const float c2f = (float)(GW_LOG2E / eps);
   dim3 cgrid((unsigned)((m + 1023) / 1024), (unsigned)s.nrb);
   CU(cudaMemsetAsync(s.stop, 0, sizeof(int), c->stream));
-  if (reset_count) CU(cudaMemsetAsync(s.mode, 0, 4 * sizeof(int), c->stream));  // safe path; dev = 0; count = 0
-  else CU(cudaMemsetAsync(s.mode, 0, sizeof(int), c->stream));                   // safe path first
+  if (reset_count) CU(cudaMemsetAsync(s.mode, 0, 4 * sizeof(int), c->stream));  // dev = 0; count = 0
+  // first iteration: speculative fused path if available (validated before commit), else safe
+  k_fill_int<<<1, 32, 0, c->stream>>>(s.mode, s.fK > 0 ? 1 : 0);
+  KCHECK();
   *used = 0;
   *converged = 0;
   if (check_every < 1) check_every = 10;
@@ -835,8 +841,33 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
     const int chunk = tolmode ? std::min(check_every, iters - done) : iters - done;
     for (int k = 0; k < chunk; ++k) {
       const bool check = tolmode && k == 0 && done > 0;  // violation of the plan after `done` iterations
-      // iterations run the robust two-kernel path while *mode == 0 and the fused one-read
-      // path once *mode == 1 (decided on the device by k_sink_mode; no host sync)
+      // Every iteration first tries the fused one-read path when *mode == 1 (speculatively at the
+      // start of a solve); k_sink_fast_check validates it before anything is committed, and on
+      // failure k_sink_fin_fast leaves f, g untouched and sets *mode = 0 so that the robust
+      // two-kernel path below runs this same iteration.  No host sync.
+      if (!check && s.fK > 0) {
+        PROF_BEGIN(c, PC_SINK_FUSED);
+        TRY(fused_launch(c, s.fK, s.fCL, s.fNT, fa, s.fncl));
+        KCHECK();
+        k_sink_colsum<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.fpart, s.fncl, m, s.csl, s.mode, s.stop);
+        KCHECK();
+        TRY(comm_allgather(c, s.csl, s.csg, sizeof(double) * (size_t)m));
+        CU(cudaMemsetAsync(s.flag, 0, sizeof(int), c->stream));
+        k_sink_fast_check<<<grid_for(std::max(m, nl), 256, 1 << 30), 256, 0, c->stream>>>(
+            s.Srow, nl, s.csg, P.R, m, P.lq, s.flag, s.mode, s.stop);
+        KCHECK();
+        if (P.R > 1) {
+          TRY(comm_allgather(c, s.flag, s.flagg, sizeof(int)));
+          k_or_flags<<<1, 32, 0, c->stream>>>(s.flag, s.flagg, P.R);
+          KCHECK();
+        }
+        k_sink_fin_fast<<<grid_for(std::max(m, nl), 256, 1 << 30), 256, 0, c->stream>>>(
+            s.Srow, nl, P.lp + P.row0, s.f, s.fh, s.fl, nullptr, s.csg, P.R, m, P.lq, eps, s.g, s.gh, s.gl,
+            s.mode, s.stop, s.dev, s.flag);
+        KCHECK();
+        PROF_END(c, PC_SINK_FUSED, 2);
+      }
+      // iterations run the robust two-kernel path while *mode == 0 (decided on the device)
       const int* skip = check ? nullptr : s.mode;
       if (check) CU(cudaMemsetAsync(s.viol, 0, sizeof(float), c->stream));
       double* fout = check ? s.ftmp : s.f;
@@ -861,19 +892,6 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
                                                                        s.stop, skip, s.dev);
       KCHECK();
       PROF_END(c, PC_SINK_COL, 2);
-      if (!check && s.fK > 0) {
-        PROF_BEGIN(c, PC_SINK_FUSED);
-        TRY(fused_launch(c, s.fK, s.fCL, s.fNT, fa, s.fncl));
-        KCHECK();
-        k_sink_colsum<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.fpart, s.fncl, m, s.csl, s.mode, s.stop);
-        KCHECK();
-        TRY(comm_allgather(c, s.csl, s.csg, sizeof(double) * (size_t)m));
-        k_sink_fin_fast<<<grid_for(std::max(m, nl), 256, 1 << 30), 256, 0, c->stream>>>(
-            s.Srow, nl, P.lp + P.row0, s.f, s.fh, s.fl, nullptr, s.csg, P.R, m, P.lq, eps, s.g, s.gh, s.gl,
-            s.mode, s.stop, s.dev);
-        KCHECK();
-        PROF_END(c, PC_SINK_FUSED, 2);
-      }
       k_sink_mode<<<1, 32, 0, c->stream>>>(s.dev, s.mode, s.fK > 0 ? 20.f : -1.f);
       KCHECK();
     }

@@ -135,6 +135,10 @@ __global__ void k_to_float(const double* __restrict__ v, int64_t n, float* __res
     out[i] = (float)v[i];
 }
 
+__global__ void k_fill_int(int* __restrict__ v, int val) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *v = val;
+}
+
 __global__ void k_fill(double* __restrict__ v, int64_t n, double val) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     v[i] = val;
