@@ -1,0 +1,134 @@
+"""Full-size parity (BASELINE.json configs[3], N = M = 65536, the launch configuration bench.py
+times): sampled outputs the float64 oracle can compute one by one (tier rules ③).
+
+* gradient: 8 full rows and 8 full columns of gw_grad_dp's G on the GPU's own plan T (a plan of
+  the C4 solve, materialised), against the definition G = 2(c 1^T + 1 c'^T) - 4 D_X T D_Y
+   evaluated in float64 on those rows / columns only: D_X[I, :] T by blocked
+  products, then the oracle's 1-D DP for D_Y; c, c' by their definition.
+* Sinkhorn: one more iteration of the GPU's fused path from the GPU's own (f, g) on that G,
+  against the oracle's log-domain update evaluated blockwise in float64;
+  plus the exact post-update column marginals and the reported violation.
+
+Host memory: ~40 GB (the GPU box has 196 GB); runtime ~2-3 min.
+"""
+
+import numpy as np
+import pytest
+
+import oracle as O
+import workloads as W
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+N = 65536
+BLK = 2048
+
+
+@pytest.fixture(scope="module")
+def full():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__ as ge
+    ge.build()
+    from paper_2404_08970_b200 import api
+    dev = torch.device("cuda", 0)
+    P = W.config4(N)
+    # the GPU's own plan: one outer iteration of the C4 solve, materialised
+    r = api.solve(P.x, P.y, P.p, P.q, P.eps, 1, 20, return_plan=True, device=dev)
+    T = r.T
+    G = api.grad(P.x, P.y, P.p, P.q, T)
+    torch.cuda.synchronize()
+    out = {"P": P, "api": api, "dev": dev, "T_dev": T, "G_dev": G,
+           "T": T.cpu().numpy(), "G": G.cpu().numpy()}
+    yield out
+    del out["T_dev"], out["G_dev"]
+    torch.cuda.empty_cache()
+
+
+def _rows_of_DXT(x, I, T):
+    """D_X[I, :] T in float64, blocked over rows of T."""
+    Wm = np.abs(x[I][:, None] - x[None, :])
+    B = np.zeros((len(I), T.shape[1]))
+    for b in range(0, T.shape[0], BLK):
+        B += Wm[:, b:b + BLK] @ T[b:b + BLK].astype(np.float64)
+    return B
+
+
+def _T_DY_cols(y, J, T):
+    """T D_Y[:, J] in float64, blocked over rows of T."""
+    DYJ = np.abs(y[:, None] - y[None, J])
+    U = np.zeros((T.shape[0], len(J)))
+    for b in range(0, T.shape[0], BLK):
+        U[b:b + BLK] = T[b:b + BLK].astype(np.float64) @ DYJ
+    return U
+
+
+def _const(s, w, idx=None):
+    """c = (D o D) w with D_ij = |s_i - s_j|, rows idx (all by default), blocked."""
+    idx = np.arange(s.size) if idx is None else np.asarray(idx)
+    out = np.empty(idx.size)
+    for b in range(0, idx.size, BLK):
+        ii = idx[b:b + BLK]
+        out[b:b + BLK] = ((s[ii][:, None] - s[None, :]) ** 2) @ w
+    return out
+
+
+def test_fullsize_gradient_sampled_rows_and_columns(full):
+    P, T, G = full["P"], full["T"], full["G"]
+    rng = np.random.default_rng(123)
+    I = np.sort(rng.choice(N, 8, replace=False))
+    J = np.sort(rng.choice(N, 8, replace=False))
+    c2 = _const(P.y, P.q)
+    cI = _const(P.x, P.p, I)
+    B = _rows_of_DXT(P.x, I, T)
+    VI = np.stack([O.ref_dp_distance(B[r], P.y) for r in range(len(I))])
+    GI = 2.0 * (cI[:, None] + c2[None, :]) - 4.0 * VI
+    c = _const(P.x, P.p)
+    U = _T_DY_cols(P.y, J, T)
+    VJ = np.stack([O.ref_dp_distance(U[:, r], P.x) for r in range(len(J))], axis=1)
+    GJ = 2.0 * (c[:, None] + c2[None, J]) - 4.0 * VJ
+    scale = max(np.max(np.abs(GI)), np.max(np.abs(GJ)))
+    err_r = np.max(np.abs(G[I].astype(np.float64) - GI)) / scale
+    err_c = np.max(np.abs(G[:, J].astype(np.float64) - GJ)) / scale
+    assert err_r <= 1e-5 and err_c <= 1e-5, (err_r, err_c)
+
+
+def test_fullsize_sinkhorn_step_and_marginals(full):
+    import torch
+    api, P, G = full["api"], full["P"], full["G"]
+    eps = P.eps
+    r0 = api.sinkhorn(full["G_dev"], P.p, P.q, eps, 30)
+    f0, g0 = r0["f"], r0["g"]
+    r1 = api.sinkhorn(full["G_dev"], P.p, P.q, eps, 1, f=f0, g=g0, return_plan=False)
+    assert r1["fused_iters"] == 1, "the step under test is the fused one-read iteration"
+    f0, g0 = f0.cpu().numpy(), g0.cpu().numpy()
+    f1, g1 = r1["f"].cpu().numpy(), r1["g"].cpu().numpy()
+    lp, lq = np.log(P.p), np.log(P.q)
+    # oracle f-update, blockwise rows
+    fo = np.empty(N)
+    for b in range(0, N, BLK):
+        Gb = G[b:b + BLK].astype(np.float64)
+        fo[b:b + BLK] = eps * lp[b:b + BLK] - eps * O.logsumexp((g0[None, :] - Gb) / eps, axis=1)
+    # oracle g-update on the new f: running column log-sum-exp over row blocks
+    M = np.full(N, -np.inf)
+    S = np.zeros(N)
+    for b in range(0, N, BLK):
+        A = (fo[b:b + BLK, None] - G[b:b + BLK].astype(np.float64)) / eps
+        mb = A.max(axis=0)
+        Mn = np.maximum(M, mb)
+        S = S * np.exp(M - Mn) + np.exp(A - Mn[None, :]).sum(axis=0)
+        M = Mn
+    go = eps * lq - eps * (M + np.log(S))
+    # per-entry plan deviation of one step, in units of eps (reading R30 bounds it by ~1e-4)
+    df = np.max(np.abs(f1 - fo)) / eps
+    dg = np.max(np.abs(g1 - go)) / eps
+    assert df <= 5e-4 and dg <= 5e-4, (df, dg)
+    # after the g-update the plan's column sums are q (up to the fp32 cost): sampled columns
+    rng = np.random.default_rng(5)
+    J = rng.choice(N, 16, replace=False)
+    colsum = np.zeros(J.size)
+    for b in range(0, N, BLK):
+        colsum += np.exp((f1[b:b + BLK, None] + g1[None, J] - G[b:b + BLK][:, J].astype(np.float64)) / eps).sum(0)
+    assert np.max(np.abs(colsum - P.q[J]) / P.q[J]) <= 1e-3
+    torch.cuda.synchronize()
