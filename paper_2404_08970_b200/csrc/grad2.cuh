@@ -70,9 +70,12 @@ struct G2Loader {
 };
 
 // Regenerate T from the loaded values (MODE) and write it to the padded shared-memory tile.
-template <int MODE>
+// OBJ: also copy T to sT2 and accumulate the entropy sum T (ln T - 1) into *ent;
+// on the Gibbs path ln T is the exponent itself (a ln 2), so no logarithm is taken.
+template <int MODE, bool OBJ = false>
 __device__ __forceinline__ void g2_stage(const G2Loader<MODE>& L, const TSrc2& S, float* __restrict__ sT, int64_t r0,
-                                         int64_t c0, int64_t nl, int64_t m, int sub) {
+                                         int64_t c0, int64_t nl, int64_t m, int sub, float* __restrict__ sT2 = nullptr,
+                                         float* ent = nullptr) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
@@ -105,6 +108,19 @@ __device__ __forceinline__ void g2_stage(const G2Loader<MODE>& L, const TSrc2& S
         const float2 a0 = fadd2(fadd2(ffma2(g01, nch, gh0), F2), ffma2(g01, ncl, fadd2(gl0, Fl2)));
         const float2 a1 = fadd2(fadd2(ffma2(g23, nch, gh1), F2), ffma2(g23, ncl, fadd2(gl1, Fl2)));
         t = make_float4(ex2_ftz(a0.x), ex2_ftz(a0.y), ex2_ftz(a1.x), ex2_ftz(a1.y));
+        if (OBJ && i < nl) {
+          constexpr float ln2 = 0.6931471805599453f;
+          const float av[4] = {a0.x, a0.y, a1.x, a1.y}, tv[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (tv[e] > 0.f && q + e < m) *ent += tv[e] * fmaf(av[e], ln2, -1.f);
+        }
+      }
+      if (OBJ && MODE != T_GIBBS && i < nl) {
+        const float tv[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (tv[e] > 0.f && q + e < m) *ent += tv[e] * (__logf(tv[e]) - 1.f);
       }
       if (i >= nl) t = make_float4(0.f, 0.f, 0.f, 0.f);
       if (q + 3 >= m) {
@@ -114,6 +130,7 @@ __device__ __forceinline__ void g2_stage(const G2Loader<MODE>& L, const TSrc2& S
         if (q + 3 >= m) t.w = 0.f;
       }
       *reinterpret_cast<float4*>(sT + rl * G2RS + g2_phys(128 * h + 4 * lane)) = t;
+      if (OBJ) *reinterpret_cast<float4*>(sT2 + rl * G2RS + g2_phys(128 * h + 4 * lane)) = t;
     }
   }
 }
@@ -205,9 +222,13 @@ __global__ void __launch_bounds__(G2T, 4) k_grad_moments2(TSrc2 S, int64_t nl, i
 // FGW (Remark 2): G = (1 - alpha) (fx_i - fy_p)^2 + alpha G_gw; the alpha is
 // folded into the constants and sqrt(1 - alpha) into the features.
 // ---------------------------------------------------------------------------------
-template <int MODE, bool FGW>
-__global__ void __launch_bounds__(G2T, 4) k_grad_store2(MainArgs a, TSrc2 S) {
+// OBJ (the objective pass over the final plan): nothing is stored; per tile the fp64 sums
+// <G, T> (GW gradient, prescribed c), sum T (ln T - 1) and <(fx - fy)^2, T> go to
+// a.tile_obj / tile_ent / tile_cc for k_obj_partial (the constants are then not alpha-scaled).
+template <int MODE, bool FGW, bool OBJ = false>
+__global__ void __launch_bounds__(G2T, OBJ ? 3 : 4) k_grad_store2(MainArgs a, TSrc2 S) {
   __shared__ __align__(16) float sT[G2SUB * G2RS];  // T, then the local row scans (exclusive, per segment)
+  extern __shared__ __align__(16) float sTobj[];     // OBJ: a copy of T (dynamic, G2SUB * G2RS floats)
   __shared__ __align__(16) float4 sRow[TR];         // {R_i, xh_i, v_i, dx_i} (alpha-scaled for FGW)
   __shared__ __align__(16) float2 sEx[G2SUB][4];    // per (row, segment): {P, A} exclusive state of the row
                                                     // before the segment (incl. the strip carry), at the
@@ -223,7 +244,9 @@ __global__ void __launch_bounds__(G2T, 4) k_grad_store2(MainArgs a, TSrc2 S) {
   const int64_t c0 = (int64_t)s * TC, r0 = (int64_t)b * TR;
   const int64_t nl = a.nl, m = a.m;
   const double yc0 = a.yc[c0], xr0 = a.xl[r0];
-  const double alpha = FGW ? a.alpha : 1.0;
+  const double alpha = (FGW && !OBJ) ? a.alpha : 1.0;
+  const double fscale = (FGW && !OBJ) ? sqrt(1.0 - a.alpha) : 1.0;  // features: (1 - alpha)(fx - fy)^2
+  double acc_obj = 0.0, acc_ent = 0.0, acc_cc = 0.0;
 
   // ---- prologue: column state at the tile top, columns q = c0 + 2t + e (e = 0, 1) ----
   double Kq[2], uq[2];
@@ -255,7 +278,7 @@ __global__ void __launch_bounds__(G2T, 4) k_grad_store2(MainArgs a, TSrc2 S) {
       Kq[e] = alpha * (2.0 * a.c2[qq] - 16.0 * AA0 - 8.0 * (a.xlast - xr0) * SAq + 8.0 * a.WAg[qq]);
       uq[e] = alpha * (8.0 * SAq - 16.0 * SA0);
       yhq[e] = (float)(yq[e] - yc0);
-      fyq[e] = FGW ? (float)(sqrt(1.0 - alpha) * a.fy[qq]) : 0.f;
+      fyq[e] = FGW ? (float)(fscale * a.fy[qq]) : 0.f;
       // step to the next exclusive state for e = 1
       e1 = pa_combine(e1, PA<double>{CP[e], 0.0, yq[e]});
       e2 = pa_combine(e2, PA<double>{CX[e], 0.0, yq[e]});
@@ -283,7 +306,7 @@ __global__ void __launch_bounds__(G2T, 4) k_grad_store2(MainArgs a, TSrc2 S) {
     const double xh = a.xl[jj] - xr0;
     const double xn = (j + 1 < nl) ? a.xl[j + 1] - xr0 : xh;
     sRow[k] = make_float4((float)(alpha * R), (float)xh, (float)(alpha * 4.0 * dp), (float)(xn - xh));
-    sFx[k] = FGW ? (float)(sqrt(1.0 - alpha) * a.fx[jj]) : 0.f;
+    sFx[k] = FGW ? (float)(fscale * a.fx[jj]) : 0.f;
     sCar[k] = make_float2((float)a.rP[(int64_t)s * nl + jj], (float)a.rA[(int64_t)s * nl + jj]);
   }
   if (t < 4) sSref[t] = (float)(a.yc[min(c0 + 64 * t + 63, m - 1)] - yc0);
@@ -296,7 +319,11 @@ __global__ void __launch_bounds__(G2T, 4) k_grad_store2(MainArgs a, TSrc2 S) {
   L.load(S, r0, c0, nl, m, 0);
   for (int sub = 0; sub < nsub; ++sub) {
     __syncthreads();  // previous sub-strip fully consumed; prologue smem visible
-    g2_stage<MODE>(L, S, sT, r0, c0, nl, m, sub);
+    {
+      float ent = 0.f;
+      g2_stage<MODE, OBJ>(L, S, sT, r0, c0, nl, m, sub, sTobj, &ent);
+      if (OBJ) acc_ent += (double)ent;
+    }
     if (sub + 1 < nsub) L.load(S, r0, c0, nl, m, sub + 1);
     __syncthreads();
     // ---- row pass: exclusive gap-weighted scan of this thread's segment, in place ----
@@ -374,13 +401,23 @@ __global__ void __launch_bounds__(G2T, 4) k_grad_store2(MainArgs a, TSrc2 S) {
         g = ffma2(make_float2(rc.y, rc.y), u2, g);
         g = ffma2(yh2, make_float2(rc.z, rc.z), g);
         g = ffma2(AA, m162, g);
-        if (FGW) {
-          const float fx = sFx[sub * G2SUB + rl];
-          const float2 d = fadd2(make_float2(fx, fx), make_float2(-fy2.x, -fy2.y));
-          g = ffma2(d, d, g);
+        if (OBJ) {
+          const float2 tv = *reinterpret_cast<const float2*>(sTobj + rl * G2RS + cphys);
+          acc_obj += (double)(g.x * tv.x) + (double)(g.y * tv.y);
+          if (FGW) {
+            const float fx = sFx[sub * G2SUB + rl];
+            const float d0 = fx - fy2.x, d1 = fx - fy2.y;
+            acc_cc += (double)(d0 * d0 * tv.x) + (double)(d1 * d1 * tv.y);
+          }
+        } else {
+          if (FGW) {
+            const float fx = sFx[sub * G2SUB + rl];
+            const float2 d = fadd2(make_float2(fx, fx), make_float2(-fy2.x, -fy2.y));
+            g = ffma2(d, d, g);
+          }
+          if (q1v) *reinterpret_cast<float2*>(Gp + (int64_t)rl * a.ldG) = g;
+          else if (q0v) Gp[(int64_t)rl * a.ldG] = g.x;
         }
-        if (q1v) *reinterpret_cast<float2*>(Gp + (int64_t)rl * a.ldG) = g;
-        else if (q0v) Gp[(int64_t)rl * a.ldG] = g.x;
         SA = fadd2(SA, Av);
         AA = ffma2(make_float2(rc.w, rc.w), SA, AA);
       }
@@ -390,6 +427,17 @@ __global__ void __launch_bounds__(G2T, 4) k_grad_store2(MainArgs a, TSrc2 S) {
       AAtop[1] += (double)(xend - xh0) * SAtop[1] + (double)AA.y;
       SAtop[0] += (double)SA.x;
       SAtop[1] += (double)SA.y;
+    }
+  }
+  if (OBJ) {
+    // fixed-order CTA reductions (columns beyond m and rows beyond nl contribute exact zeros)
+    const double so = block_sum<G2T / 32>(acc_obj, sm);
+    const double se = block_sum<G2T / 32>(acc_ent, sm);
+    const double sc = block_sum<G2T / 32>(acc_cc, sm);
+    if (t == 0) {
+      a.tile_obj[(int64_t)b * a.ns + s] = so;
+      a.tile_ent[(int64_t)b * a.ns + s] = se;
+      a.tile_cc[(int64_t)b * a.ns + s] = sc;
     }
   }
 }

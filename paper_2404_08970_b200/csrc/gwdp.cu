@@ -492,9 +492,11 @@ static gw_status grad_pass(gw_ctx* c, const Prepared& P, int mode, const TSrc& S
   TRY(ws(c, c->tcc, (size_t)nb * ns, &tcc));
   const double* xl = P.xc + P.row0;
   dim3 grid(ns, nb);
-  const bool fast = store && !obj;
-  // the objective pass (old fp64-regeneration kernels) is timed as its own class
-  const int pc_mom = fast ? PC_GRAD_MOMENTS : PC_OBJ, pc_main = fast ? PC_GRAD_MAIN : PC_OBJ;
+  // streaming kernels (grad2.cuh) for the STORE-only gradient and the OBJ-only objective pass; the
+  // rare STORE+OBJ pass (GW_SOLVE_TRACE_OBJECTIVE) runs grad.cuh's kernels
+  const bool fast = store != obj;
+  // the objective pass is timed as its own class
+  const int pc_mom = !obj ? PC_GRAD_MOMENTS : PC_OBJ, pc_main = !obj ? PC_GRAD_MAIN : PC_OBJ;
   PROF_BEGIN(c, pc_mom);
   if (fast) {
     switch (mode) {
@@ -510,7 +512,7 @@ static gw_status grad_pass(gw_ctx* c, const Prepared& P, int mode, const TSrc& S
     }
   }
   KCHECK();
-  PROF_END(c, pc_mom, fast ? 1 : 0);
+  PROF_END(c, pc_mom, !obj ? 1 : 0);
   PROF_BEGIN(c, PC_GRAD_CARRY);
   k_colcarry<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(nl, m, nb, xl, cS, cX, btot, cxend);
   KCHECK();
@@ -583,8 +585,22 @@ static gw_status grad_pass(gw_ctx* c, const Prepared& P, int mode, const TSrc& S
   } while (0)
 #define LAUNCH_STORE2(MODE)                                                                           \
   do {                                                                                                \
-    if (fx) k_grad_store2<MODE, true><<<grid, G2T, 0, c->stream>>>(a, S2);                            \
-    else k_grad_store2<MODE, false><<<grid, G2T, 0, c->stream>>>(a, S2);                              \
+    if (obj) {                                                                                        \
+      const int dsm = G2SUB * G2RS * (int)sizeof(float);                                              \
+      if (fx) {                                                                                       \
+        CU(cudaFuncSetAttribute(k_grad_store2<MODE, true, true>,                                      \
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, dsm));                   \
+        k_grad_store2<MODE, true, true><<<grid, G2T, dsm, c->stream>>>(a, S2);                        \
+      } else {                                                                                        \
+        CU(cudaFuncSetAttribute(k_grad_store2<MODE, false, true>,                                     \
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, dsm));                   \
+        k_grad_store2<MODE, false, true><<<grid, G2T, dsm, c->stream>>>(a, S2);                       \
+      }                                                                                               \
+    } else if (fx) {                                                                                  \
+      k_grad_store2<MODE, true><<<grid, G2T, 0, c->stream>>>(a, S2);                                  \
+    } else {                                                                                          \
+      k_grad_store2<MODE, false><<<grid, G2T, 0, c->stream>>>(a, S2);                                 \
+    }                                                                                                 \
   } while (0)
   if (fast) {
     if (mode == T_EXPLICIT) LAUNCH_STORE2(T_EXPLICIT);
@@ -1138,7 +1154,16 @@ static gw_status solve_impl(gw_ctx* c, const gw_problem* pb, const gw_solve_opts
       KCHECK();
       S = TSrc{G, ldG, Fs, Gs2, GW_LOG2E / eps};
     }
-    const TSrc2 S2{};
+    TSrc2 S2{};
+    if (mode == T_EXPLICIT) {
+      S2 = TSrc2{reinterpret_cast<const float*>(T0), ldT, nullptr, nullptr, nullptr, nullptr, 0.f, 0.f};
+    } else if (mode == T_PRODUCT) {
+      S2 = TSrc2{nullptr, 0, P.pnf + P.row0, nullptr, P.qnf, nullptr, 0.f, 0.f};
+    } else {
+      const double cc = GW_LOG2E / eps;
+      const float ch = (float)cc;
+      S2 = TSrc2{G, ldG, s.fh, s.fl, s.gh, s.gl, ch, (float)(cc - (double)ch)};
+    }
     TRY(grad_pass(c, P, mode, S, S2, nullptr, 0, false, true, fx, fy, alpha, objout));
     if (T_out) TRY(materialize(c, P, mode == T_EXPLICIT ? T_GIBBS : mode, S, T_out, ldT));
     if (T_out && mode == T_EXPLICIT) CU(cudaMemcpy2DAsync(T_out, ldT * 4, T0, ldT * 4, m * 4, nl,
