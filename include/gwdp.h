@@ -63,7 +63,7 @@ typedef enum {
   GW_ERR_NOT_NORMALIZED = 5,  /* |sum - 1| > 1e-9                        */
   GW_ERR_NONFINITE = 6,       /* NaN/Inf in inputs or produced          */
   GW_ERR_CONFIG = 7,          /* invalid options                                       */
-  GW_ERR_UNSUPPORTED = 8,     /* k != 1, loss != square, tau != eps, fp64 storage, UGW */
+  GW_ERR_UNSUPPORTED = 8,     /* k not in {1, 2}, loss != square, tau != eps, fp64 storage, UGW */
   GW_ERR_OOM = 9,
   GW_ERR_CUDA = 10,
   GW_ERR_NCCL = 11
@@ -81,7 +81,7 @@ typedef struct {
   int64_t row0, n_local;  /* this rank's row shard; (0, n) on one GPU                  */
   const double *x, *y;    /* supports, non-decreasing (length n and m)                 */
   const double *p, *q;    /* marginals, >= 0, sum 1 within 1e-9 (length n and m)       */
-  int32_t k;              /* distance power |x - x'|^k; only k = 1 (hot path, R17)      */
+  int32_t k;              /* distance power |x - x'|^k: 1 (hot path) or 2 (R17, f2)     */
   int32_t loss;           /* gw_loss */
   int32_t dtype;          /* gw_dtype; only GW_F32 in this ABI version                 */
   uint32_t flags;         /* GW_NO_VALIDATE | GW_HOST_VECTORS                          */

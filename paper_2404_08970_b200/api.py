@@ -79,17 +79,17 @@ class Context:
             self.h = None
 
 
-def _problem(x, y, p, q, n_local=None, row0=0, flags=0):
+def _problem(x, y, p, q, n_local=None, row0=0, flags=0, k=1):
     pr = L.gw_problem()
     pr.n, pr.m = x.numel(), y.numel()
     pr.row0 = row0
     pr.n_local = pr.n if n_local is None else n_local
     pr.x, pr.y, pr.p, pr.q = x.data_ptr(), y.data_ptr(), p.data_ptr(), q.data_ptr()
-    pr.k, pr.loss, pr.dtype, pr.flags = 1, L.GW_LOSS_SQUARE, L.GW_F32, flags
+    pr.k, pr.loss, pr.dtype, pr.flags = int(k), L.GW_LOSS_SQUARE, L.GW_F32, flags
     return pr
 
 
-def grad(x, y, p, q, T, out=None, validate=True, ctx=None, row0=0):
+def grad(x, y, p, q, T, out=None, validate=True, ctx=None, row0=0, k=1):
     """G = 2(c 1^T + 1 c'^T) - 4 D_X T D_Y  (gw_grad_dp), fp32.
     Sharded (ctx with a multi-rank comm): x, p are the full supports/marginals, T holds this
     rank's rows [row0, row0 + T.shape[0]) and the result holds the same rows of G."""
@@ -101,7 +101,7 @@ def grad(x, y, p, q, T, out=None, validate=True, ctx=None, row0=0):
     if out is None:
         out = plan_buffer(n, m, dev)
     ldG = _check_mat(out, "out")
-    pr = _problem(x, y, p, q, n_local=n, row0=row0, flags=0 if validate else L.GW_NO_VALIDATE)
+    pr = _problem(x, y, p, q, n_local=n, row0=row0, flags=0 if validate else L.GW_NO_VALIDATE, k=k)
     L.check(ctx.lib.gw_grad_dp(ctx.h, C.byref(pr), _ptr(T), ldT, _ptr(out), ldG, None))
     return out
 
@@ -168,7 +168,7 @@ def _opts(eps, outer, inner, tol, check_every, trace_objective):
 
 
 def solve(x, y, p, q, eps, outer, inner, tol=0.0, check_every=10, T0=None, return_plan=False,
-          trace_objective=False, fx=None, fy=None, alpha=None, device=None, ctx=None, row0=0, n_local=None):
+          trace_objective=False, fx=None, fy=None, alpha=None, device=None, ctx=None, row0=0, n_local=None, k=1):
     """Entropic GW (entropic_gw_solve) or, with fx/fy/alpha, entropic FGW (fgw_solve), on
     device vectors; tau = eps.  Sharded (ctx with a multi-rank
     comm): x, p (and fx) are full; this rank owns rows [row0, row0 + n_local): f, T0 and the
@@ -191,7 +191,7 @@ def solve(x, y, p, q, eps, outer, inner, tol=0.0, check_every=10, T0=None, retur
             T = torch.empty((n, ld), dtype=torch.float32, device=dev)[:, :m]
     elif T is not None:
         ld = T.stride(0)
-    pr = _problem(x, y, p, q, n_local=n, row0=row0)
+    pr = _problem(x, y, p, q, n_local=n, row0=row0, k=k)
     o = _opts(eps, outer, inner, tol, check_every, trace_objective)
     res = L.gw_result()
     tr = np.zeros((max(int(outer), 1), 4), dtype=np.float64)
@@ -207,7 +207,7 @@ def solve(x, y, p, q, eps, outer, inner, tol=0.0, check_every=10, T0=None, retur
 
 
 def solve_host(x, y, p, q, eps, outer, inner, tol=0.0, check_every=10, device=None, ctx=None,
-               fx=None, fy=None, alpha=None, row0=0, n_local=None):
+               fx=None, fy=None, alpha=None, row0=0, n_local=None, k=1):
     """entropic_gw_solve with HOST vectors (GW_HOST_VECTORS): the library stages x, y, p, q
     host->device and copies the duals f, g back.  This is the end-to-end public call.
     Sharded: as solve() (f holds this rank's n_local rows)."""
@@ -220,7 +220,7 @@ def solve_host(x, y, p, q, eps, outer, inner, tol=0.0, check_every=10, device=No
     pr = L.gw_problem()
     pr.n, pr.m, pr.row0, pr.n_local = n, m, int(row0), nl
     pr.x, pr.y, pr.p, pr.q = (a.ctypes.data for a in (xs, ys, ps, qs))
-    pr.k, pr.loss, pr.dtype, pr.flags = 1, L.GW_LOSS_SQUARE, L.GW_F32, L.GW_HOST_VECTORS
+    pr.k, pr.loss, pr.dtype, pr.flags = int(k), L.GW_LOSS_SQUARE, L.GW_F32, L.GW_HOST_VECTORS
     o = _opts(eps, outer, inner, tol, check_every, False)
     res = L.gw_result()
     tr = np.zeros((max(int(outer), 1), 4))

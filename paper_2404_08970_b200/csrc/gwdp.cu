@@ -17,6 +17,7 @@
 #include "grad.cuh"
 #include "grad2.cuh"
 #include "shard.cuh"
+#include "poly.cuh"
 #include "sink.cuh"
 #include "vec.cuh"
 
@@ -98,6 +99,7 @@ struct gw_ctx {
   Buf rP, rA, cS, cX, blk, bs, btot, cxend, SAg, WAg, Ptot, Aend, DP, DA, tobj, tent, tcc, objout;
   Buf fxs, fys;  // FGW features (staged)
   Buf pnf, qnf;  // fp32 marginals
+  Buf yfb, pcoef, pc2s, pfx, pfy, ppart, pM;  // k = 2 path
   Buf xtab, xg1, xg2, xin, xvec, xtail, xpart;  // multi-rank exchange buffers
   Buf slse, slseg, scsl, scsg, sviolg;          // Sinkhorn column-sum exchange
   Buf sflag, sflagg;
@@ -109,7 +111,7 @@ struct gw_ctx {
                 &ftmp, &viol, &stop, &iters, &part, &fpart, &mode, &srow, &pfl, &rP, &rA, &cS, &cX, &blk, &bs, &btot, &cxend,
                 &SAg, &WAg, &Ptot, &Aend, &DP, &DA, &tobj, &tent, &tcc, &objout, &fxs, &fys, &fsc, &gsc, &Gs,
                 &pnf, &qnf, &xtab, &xg1, &xg2, &xin, &xvec, &xtail, &xpart, &slse, &slseg, &scsl, &scsg,
-                &sviolg, &sflag, &sflagg};
+                &sviolg, &sflag, &sflagg, &yfb, &pcoef, &pc2s, &pfx, &pfy, &ppart, &pM};
     for (Buf* x : b) all.push_back(x);
   }
 };
@@ -349,7 +351,9 @@ struct Prepared {
   const double *x, *y, *p, *q;  // device views of the caller's vectors (staged if host)
   double *xc, *yc, *pn, *qn, *lp, *lq, *cx, *cy;
   float *pnf, *qnf;  // fp32 copies of the normalised marginals (T^0 = p q^T on the fp32 gradient path)
+  float* yf;         // fp32 centred y (k = 2 path)
   double xlast, ylast;
+  int k = 1;         // distance power
   // row shards of all ranks (multi-rank only): tab[2r] = row0_r, tab[2r+1] = nl_r
   int R = 1, rank = 0;
   int64_t maxnl = 0;
@@ -365,7 +369,8 @@ static gw_status check_problem(const gw_problem* pb) {
     return fail(GW_ERR_DIM_MISMATCH, "row shard [%lld, %lld) outside [0, %lld)", (long long)pb->row0,
                 (long long)(pb->row0 + pb->n_local), (long long)pb->n);
   if (!pb->x || !pb->y || !pb->p || !pb->q) return fail(GW_ERR_INVALID_ARG, "x, y, p, q must be non-null");
-  if (pb->k != 1) return fail(GW_ERR_UNSUPPORTED, "distance power k=%d: only k = 1 is implemented", pb->k);
+  if (pb->k != 1 && pb->k != 2)
+    return fail(GW_ERR_UNSUPPORTED, "distance power k=%d: k = 1 and k = 2 are implemented (R17)", pb->k);
   if (pb->loss != GW_LOSS_SQUARE) return fail(GW_ERR_UNSUPPORTED, "only the square loss is defined (PAPER.md:86)");
   if (pb->dtype != GW_F32) return fail(GW_ERR_UNSUPPORTED, "only fp32 matrix storage in ABI v1");
   return GW_OK;
@@ -422,6 +427,16 @@ static gw_status prepare(gw_ctx* c, const gw_problem* pb, Prepared& P) {
   k_prep<<<grid_for(m), 256, 0, c->stream>>>(P.y, P.q, m, mom + 8, yc, qn, lq, cy);
   KCHECK();
   P.xc = xc; P.yc = yc; P.pn = pn; P.qn = qn; P.lp = lp; P.lq = lq; P.cx = cx; P.cy = cy;
+  P.k = pb->k;
+  if (P.k == 2) {  // c = (D o D) p with D = |x - x'|^2, by moments up to order 4
+    k_poly_const<<<1, 1024, 0, c->stream>>>(xc, pn, n, cx);
+    KCHECK();
+    k_poly_const<<<1, 1024, 0, c->stream>>>(yc, qn, m, cy);
+    KCHECK();
+  }
+  TRY(ws(c, c->yfb, m, &P.yf));
+  k_to_float<<<grid_for(m), 256, 0, c->stream>>>(yc, m, P.yf);
+  KCHECK();
   TRY(ws(c, c->pnf, n, &P.pnf)); TRY(ws(c, c->qnf, m, &P.qnf));
   k_to_float<<<grid_for(n), 256, 0, c->stream>>>(pn, n, P.pnf);
   KCHECK();
@@ -471,9 +486,9 @@ struct GradOut {
 // The STORE-only pass (every gradient of the solver and gw_grad_dp) runs the streaming fp32 kernels of
 // grad2.cuh with T supplied by S2; the objective pass (OBJ) runs grad.cuh's kernels with S (fp64
 // regeneration) so that its moments and its tile sums see bit-identical T values.
-static gw_status grad_pass(gw_ctx* c, const Prepared& P, int mode, const TSrc& S, const TSrc2& S2, float* G,
-                           int64_t ldG, bool store, bool obj, const double* fx, const double* fy, double alpha,
-                           double* objout_dev) {
+static gw_status grad_pass_k1(gw_ctx* c, const Prepared& P, int mode, const TSrc& S, const TSrc2& S2, float* G,
+                              int64_t ldG, bool store, bool obj, const double* fx, const double* fy, double alpha,
+                              double* objout_dev) {
   const int64_t nl = P.nl, m = P.m, n = P.n;
   const int R = P.R;
   if (nl == 0) return GW_OK;  // single rank only: prepare() rejects empty shards when R > 1
@@ -633,6 +648,90 @@ static gw_status grad_pass(gw_ctx* c, const Prepared& P, int mode, const TSrc& S
     TRY(comm_allgather(c, part, gpart, 8 * sizeof(double)));
     k_obj_final<<<1, 1024, 0, c->stream>>>(gpart, R, btot, P.yc, P.qn, P.cy, m, objout_dev);
     KCHECK();
+  }
+  return GW_OK;
+}
+
+// k = 2 (poly.cuh): global moments M_rt of the plan (one read), then G by rows (one write) and/or
+// E(T) from the moments.  Multi-rank: the per-CTA moment partials are all-gathered and summed in
+// rank order.
+static gw_status poly_moments(gw_ctx* c, const Prepared& P, int mode, const TSrc2& S2, bool obj, double** Mout) {
+  const int64_t nl = P.nl, m = P.m;
+  const int64_t rows_per_cta = (PT / 32) * PRPW;
+  const int ncta = (int)std::max<int64_t>(1, (nl + rows_per_cta - 1) / rows_per_cta);
+  // equal all-gather payloads: pad every rank's partials to the largest shard's CTA count
+  const int maxcta = (int)std::max<int64_t>(ncta, (P.maxnl + rows_per_cta - 1) / rows_per_cta);
+  double *part, *M;
+  TRY(ws(c, c->ppart, (size_t)(PNM + 1) * maxcta * (P.R + 1), &part));
+  TRY(ws(c, c->pM, PNM + 1, &M));
+  if (maxcta > ncta)
+    CU(cudaMemsetAsync(part + (size_t)(PNM + 1) * ncta, 0, sizeof(double) * (PNM + 1) * (maxcta - ncta), c->stream));
+  const double* xl = P.xc + P.row0;
+#define LAUNCH_PM(MODE)                                                                                    \
+  do {                                                                                                     \
+    if (obj) k_poly_moments<MODE, true><<<ncta, PT, 0, c->stream>>>(S2, nl, m, xl, P.yf, part);            \
+    else k_poly_moments<MODE, false><<<ncta, PT, 0, c->stream>>>(S2, nl, m, xl, P.yf, part);               \
+  } while (0)
+  if (mode == T_EXPLICIT) LAUNCH_PM(T_EXPLICIT);
+  else if (mode == T_GIBBS) LAUNCH_PM(T_GIBBS);
+  else LAUNCH_PM(T_PRODUCT);
+#undef LAUNCH_PM
+  KCHECK();
+  if (P.R > 1) {
+    double* all = part + (size_t)(PNM + 1) * maxcta;
+    TRY(comm_allgather(c, part, all, sizeof(double) * (PNM + 1) * (size_t)maxcta));
+    k_poly_reduce<<<1, 32, 0, c->stream>>>(all, maxcta * P.R, M);
+  } else {
+    k_poly_reduce<<<1, 32, 0, c->stream>>>(part, ncta, M);
+  }
+  KCHECK();
+  *Mout = M;
+  return GW_OK;
+}
+
+static gw_status grad_pass(gw_ctx* c, const Prepared& P, int mode, const TSrc& S, const TSrc2& S2, float* G,
+                           int64_t ldG, bool store, bool obj, const double* fx, const double* fy, double alpha,
+                           double* objout_dev) {
+  if (P.k == 1) return grad_pass_k1(c, P, mode, S, S2, G, ldG, store, obj, fx, fy, alpha, objout_dev);
+  const int64_t nl = P.nl, m = P.m;
+  if (obj) {
+    // violation, entropy and <C o C, T> do not depend on k: the k = 1 objective machinery supplies
+    // them; E(T) at k = 2 comes from the plan's moments.  Runs before the store: on the solver
+    // path the plan is regenerated from the cost that the store overwrites.
+    TRY(grad_pass_k1(c, P, mode, S, S2, nullptr, 0, false, true, fx, fy, alpha, objout_dev));
+    double* M;
+    TRY(poly_moments(c, P, mode, S2, true, &M));
+    k_poly_objective<<<1, 32, 0, c->stream>>>(M, objout_dev);
+    KCHECK();
+  }
+  if (store) {
+    double* M;
+    PROF_BEGIN(c, PC_GRAD_MOMENTS);
+    TRY(poly_moments(c, P, mode, S2, false, &M));
+    PROF_END(c, PC_GRAD_MOMENTS, 1);
+    PROF_BEGIN(c, PC_GRAD_MAIN);
+    float4* coef;
+    float *c2s, *fxs = nullptr, *fys = nullptr;
+    TRY(ws(c, c->pcoef, std::max<int64_t>(nl, 1), &coef));
+    TRY(ws(c, c->pc2s, m, &c2s));
+    k_poly_rowcoef<<<grid_for(nl), 256, 0, c->stream>>>(M, P.xc + P.row0, P.cx + P.row0, nl, alpha, coef);
+    KCHECK();
+    k_scale_f<<<grid_for(m), 256, 0, c->stream>>>(P.cy, m, 2.0 * alpha, c2s);
+    KCHECK();
+    if (fx) {
+      TRY(ws(c, c->pfx, std::max<int64_t>(nl, 1), &fxs));
+      TRY(ws(c, c->pfy, m, &fys));
+      k_scale_f<<<grid_for(nl), 256, 0, c->stream>>>(fx + P.row0, nl, sqrt(1.0 - alpha), fxs);
+      k_scale_f<<<grid_for(m), 256, 0, c->stream>>>(fy, m, sqrt(1.0 - alpha), fys);
+      KCHECK();
+      k_poly_store<true><<<grid_for(nl * ((m + 3) / 4), 256, 148 * 16), 256, 0, c->stream>>>(
+          coef, c2s, P.yf, fxs, fys, nl, m, G, ldG);
+    } else {
+      k_poly_store<false><<<grid_for(nl * ((m + 3) / 4), 256, 148 * 16), 256, 0, c->stream>>>(
+          coef, c2s, P.yf, nullptr, nullptr, nl, m, G, ldG);
+    }
+    KCHECK();
+    PROF_END(c, PC_GRAD_MAIN, 1);
   }
   return GW_OK;
 }

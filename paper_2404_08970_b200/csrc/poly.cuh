@@ -1,0 +1,222 @@
+// poly.cuh -- the gradient for the distance power k = 2 (PAPER.md:65-80 with
+// k = 2, generalised to sorted supports by reading R1).
+//
+// At k = 2 the distance is a polynomial: D_ij = (x_i - x_j)^2 = sum_r a_r(x_i) x_j^r with
+// a = (x^2, -2x, 1), so D_X T D_Y = sum_{r,t} a_r(x_i) M_rt a_t(y_p) with the 2-D moments
+// M_rt = sum_{j,q} x_j^r T_jq y_q^t of the plan: the O(N M) evaluation needs ONE reduction pass
+// (the moments) and ONE write pass, no scans (the paper's recursion, at k = 2
+// carries the same three power sums).  With centred supports (|x|, |y| <= 1/2) every term is
+// O(0.1) and the expansion cancels by at most ~10x: fp32 per element, fp64 moments.
+//   G_ip = 2 c_i + 2 c'_p - 4 [u_2(i) - 2 u_1(i) y_p + u_0(i) y_p^2],   u_t(i) = sum_r a_r(x_i) M_rt
+// The objective needs moments up to order 4: m_r(a) = M_r0, n_t(b) = M_0t (r, t <= 4) and
+// <D_X T D_Y, T> = sum_{r,t} M_rt atil_r atil_t M_{2-r,2-t},  atil = (1, -2, 1).
+#pragma once
+#include "common.cuh"
+#include "fused.cuh"  // ex2_ftz
+#include "grad2.cuh"  // TSrc2, T_* modes
+
+namespace gw {
+
+constexpr int PM = 5;            // powers 0..4
+constexpr int PNM = PM * PM;     // moments per reduction
+constexpr int PRPW = 64;         // rows per warp
+constexpr int PT = 256;          // threads per CTA (8 warps) -> 512 rows per CTA
+
+__device__ __forceinline__ float p_regen(int MODE, const TSrc2& S, float g, float Fh, float Fl, int64_t q) {
+  if (MODE == T_EXPLICIT) return g;
+  if (MODE == T_PRODUCT) return Fh * S.gh[q];
+  const float a = (fmaf(g, -S.ch, S.gh[q]) + Fh) + fmaf(g, -S.cl, S.gl[q] + Fl);
+  return ex2_ftz(a);
+}
+
+// Moments M_rt (r, t <= 4) of this rank's rows (+ the entropy sum when OBJ): warp per row,
+// lanes stride the columns with float4 loads; fp32 partial sums per lane flushed to fp64 every
+// 256 columns; fixed-order warp and CTA reductions -> part[cta][PNM + 1].
+template <int MODE, bool OBJ>
+__global__ void __launch_bounds__(PT) k_poly_moments(TSrc2 S, int64_t nl, int64_t m, const double* __restrict__ xl,
+                                                     const float* __restrict__ yf, double* __restrict__ part) {
+  __shared__ double red[PT / 32][PNM + 1];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t r0 = ((int64_t)blockIdx.x * (PT / 32) + w) * PRPW;
+  double mom[PNM + 1];  // lane-private accumulators of sum_j x_j^r s_t(j) (+ H)
+#pragma unroll
+  for (int k = 0; k <= PNM; ++k) mom[k] = 0.0;
+  for (int rr = 0; rr < PRPW; ++rr) {
+    const int64_t j = r0 + rr;
+    if (j >= nl) break;
+    float Fh = 0.f, Fl = 0.f;
+    if (MODE == T_GIBBS) { Fh = S.fh[j]; Fl = S.fl[j]; }
+    if (MODE == T_PRODUCT) Fh = S.fh[j];
+    double s64[PM + 1] = {0, 0, 0, 0, 0, 0};
+    const float* row = S.T + j * S.ld;
+    for (int64_t c0 = 4 * (int64_t)lane; c0 < m; c0 += 32 * 4 * 64) {
+      float s32[PM + 1] = {0, 0, 0, 0, 0, 0};
+#pragma unroll 4
+      for (int u = 0; u < 64; ++u) {
+        const int64_t q = c0 + 128 * u;
+        if (q >= m) break;
+        float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (MODE != T_PRODUCT) g = __ldcs(reinterpret_cast<const float4*>(row + q));
+        const float gv[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (q + e < m) {
+            const float t = p_regen(MODE, S, gv[e], Fh, Fl, q + e);
+            const float y = yf[q + e];
+            float yp = t;
+            s32[0] += yp;
+            yp *= y; s32[1] += yp;
+            yp *= y; s32[2] += yp;
+            yp *= y; s32[3] += yp;
+            yp *= y; s32[4] += yp;
+            if (OBJ && t > 0.f) {
+              float lt;
+              if (MODE == T_GIBBS) {
+                lt = ((fmaf(gv[e], -S.ch, S.gh[q + e]) + Fh) + fmaf(gv[e], -S.cl, S.gl[q + e] + Fl)) *
+                     0.6931471805599453f;
+              } else {
+                lt = __logf(t);
+              }
+              s32[5] += t * (lt - 1.f);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k <= PM; ++k) s64[k] += (double)s32[k];
+    }
+    // fixed-order warp sums (butterfly: identical in every lane)
+#pragma unroll
+    for (int k = 0; k <= PM; ++k)
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) s64[k] += __shfl_xor_sync(0xffffffffu, s64[k], d);
+    const double xj = xl[j];
+    double xr = 1.0;
+#pragma unroll
+    for (int r = 0; r < PM; ++r) {
+#pragma unroll
+      for (int t = 0; t < PM; ++t) mom[r * PM + t] += xr * s64[t];
+      xr *= xj;
+    }
+    mom[PNM] += s64[PM];
+  }
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k <= PNM; ++k) red[w][k] = mom[k];
+  __syncthreads();
+  if (threadIdx.x <= PNM) {
+    double v = 0.0;
+    for (int ww = 0; ww < PT / 32; ++ww) v += red[ww][threadIdx.x];
+    part[(int64_t)blockIdx.x * (PNM + 1) + threadIdx.x] = v;
+  }
+}
+
+// Sum the per-CTA partials (of all ranks, gathered [R][ncta][PNM + 1]) in fixed order -> M[PNM + 1].
+__global__ void k_poly_reduce(const double* __restrict__ part, int nparts, double* __restrict__ M) {
+  if (threadIdx.x <= PNM && blockIdx.x == 0) {
+    double v = 0.0;
+    for (int c = 0; c < nparts; ++c) v += part[(int64_t)c * (PNM + 1) + threadIdx.x];
+    M[threadIdx.x] = v;
+  }
+}
+
+// Per-row coefficients of G_ip = A_i + 2c'_p + y_p (B_i + C_i y_p) (alpha-scaled for FGW).
+__global__ void k_poly_rowcoef(const double* __restrict__ M, const double* __restrict__ xl,
+                               const double* __restrict__ cl, int64_t nl, double alpha, float4* __restrict__ coef) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nl; i += (int64_t)gridDim.x * blockDim.x) {
+    const double x = xl[i];
+    const double a[3] = {x * x, -2.0 * x, 1.0};
+    double u[3];
+#pragma unroll
+    for (int t = 0; t < 3; ++t) u[t] = a[0] * M[0 * PM + t] + a[1] * M[1 * PM + t] + a[2] * M[2 * PM + t];
+    const double A = 2.0 * cl[i] - 4.0 * u[2], B = 8.0 * u[1], C = -4.0 * u[0];
+    coef[i] = make_float4((float)(alpha * A), (float)(alpha * B), (float)(alpha * C), 0.f);
+  }
+}
+
+// G_ip = A_i + 2 alpha c'_p + y_p (B_i + C_i y_p) [+ (1 - alpha)(fx_i - fy_p)^2], float4 stores.
+template <bool FGW>
+__global__ void k_poly_store(const float4* __restrict__ coef, const float* __restrict__ c2s,
+                             const float* __restrict__ yf, const float* __restrict__ fxs, const float* __restrict__ fys,
+                             int64_t nl, int64_t m, float* __restrict__ G, int64_t ldG) {
+  const int64_t m4 = (m + 3) / 4;
+  const int64_t total = nl * m4;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / m4, q = 4 * (e - i * m4);
+    const float4 cf = coef[i];
+    float o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t qq = min(q + k, m - 1);
+      const float y = yf[qq];
+      float v = cf.x + c2s[qq] + y * fmaf(cf.z, y, cf.y);
+      if (FGW) {
+        const float d = fxs[i] - fys[qq];
+        v = fmaf(d, d, v);
+      }
+      o[k] = v;
+    }
+    float* dst = G + i * ldG + q;
+    if (q + 3 < m) {
+      *reinterpret_cast<float4*>(dst) = make_float4(o[0], o[1], o[2], o[3]);
+    } else {
+      for (int k = 0; k < 4 && q + k < m; ++k) dst[k] = o[k];
+    }
+  }
+}
+
+// Objective at k = 2 from the global moments (k_obj_final supplies the violation and H):
+//   a^T (D_X o D_X) a = sum_r C(4,r) (-1)^r M_r0 M_{4-r,0},   b^T (D_Y o D_Y) b likewise with M_0t,
+//   <D_X T D_Y, T> = sum_{r,t<=2} M_rt atil_r atil_t M_{2-r,2-t}.   out[0] = E.
+__global__ void k_poly_objective(const double* __restrict__ M, double* __restrict__ out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    const double C4[5] = {1, -4, 6, -4, 1};
+    double Ea = 0.0, Eb = 0.0;
+    for (int r = 0; r <= 4; ++r) {
+      Ea += C4[r] * M[r * PM + 0] * M[(4 - r) * PM + 0];
+      Eb += C4[r] * M[0 * PM + r] * M[0 * PM + (4 - r)];
+    }
+    const double at[3] = {1.0, -2.0, 1.0};
+    double VT = 0.0;
+    for (int r = 0; r <= 2; ++r)
+      for (int t = 0; t <= 2; ++t) VT += M[r * PM + t] * at[r] * at[t] * M[(2 - r) * PM + (2 - t)];
+    out[0] = Ea + Eb - 2.0 * VT;
+  }
+}
+
+// c = (D o D) w at k = 2: sum_j (s_i - s_j)^4 w_j = sum_r C(4,r) (-1)^r s_i^{4-r} mu_r,
+// mu_r = sum_j s_j^r w_j (centred supports, fixed-order reduction in one CTA).
+__global__ void __launch_bounds__(1024) k_poly_const(const double* __restrict__ s, const double* __restrict__ w,
+                                                     int64_t n, double* __restrict__ c) {
+  __shared__ double sm[32];
+  __shared__ double mu[PM];
+  double acc[PM] = {0, 0, 0, 0, 0};
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    double sp = w[i];
+    const double si = s[i];
+#pragma unroll
+    for (int r = 0; r < PM; ++r) {
+      acc[r] += sp;
+      sp *= si;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < PM; ++r) {
+    const double v = block_sum<32>(acc[r], sm);
+    if (threadIdx.x == 0) mu[r] = v;
+  }
+  __syncthreads();
+  const double C4[5] = {1, -4, 6, -4, 1};
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double si = s[i];
+    double v = 0.0, sp = 1.0;
+    // sum_r C(4,r) (-1)^r mu_r s_i^{4-r}: Horner from r = 4 down
+    for (int r = 4; r >= 0; --r) {
+      v += C4[r] * mu[r] * sp;
+      sp *= si;
+    }
+    c[i] = v;
+  }
+}
+
+}  // namespace gw

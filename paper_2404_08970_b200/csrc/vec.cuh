@@ -130,6 +130,11 @@ __global__ void k_scale(const double* __restrict__ v, int64_t n, double scale, d
     out[i] = v[i] * scale;
 }
 
+__global__ void k_scale_f(const double* __restrict__ v, int64_t n, double scale, float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (float)(v[i] * scale);
+}
+
 __global__ void k_to_float(const double* __restrict__ v, int64_t n, float* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = (float)v[i];

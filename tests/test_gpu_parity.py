@@ -313,3 +313,77 @@ def test_fgw_alpha_one_is_gw(gw):
     a = gw.solve(P.x, P.y, P.p, P.q, P.eps, P.outer, P.inner, fx=P.fx, fy=P.fy, alpha=1.0, device=_dev())
     b = gw.solve(P.x, P.y, P.p, P.q, P.eps, P.outer, P.inner, device=_dev())
     assert abs(a.gw_objective - b.gw_objective) <= 1e-6 * abs(b.gw_objective)
+
+
+# ----------------------------------------------------------------------------- full-size configs
+
+@pytest.mark.slow
+def test_grad_c3_fullsize_full_matrix(gw):
+    """C3 (BASELINE configs[2]) at its full size N = M = 16384: the whole gradient matrix against
+    the dense definition (two float64 DGEMMs)."""
+    P = W.config3(16384)
+    T = P.extra["T"]
+    G = gw.grad(P.x, P.y, P.p, P.q, _to_dev(gw, T)).cpu().numpy()
+    Go = O.grad_prescribed(P.x, P.y, P.p, P.q, T.astype(np.float64))
+    err = np.max(np.abs(G.astype(np.float64) - Go)) / np.max(np.abs(Go))
+    assert err <= GRAD_TOL, err
+
+
+@pytest.mark.slow
+def test_solver_c2_fullsize_trajectory(gw):
+    """C2 (BASELINE configs[1]) at its full size N = M = 4096, 20 outer x 100 inner: the GPU's
+    objective trajectory against the oracle's (tests/golden/c2_n4096_trajectory.json, written
+    by scripts/make_golden.py from oracle/ only)."""
+    import json
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "c2_n4096_trajectory.json")
+    ref = json.load(open(path))
+    P = W.config2(4096)
+    r = gw.solve(P.x, P.y, P.p, P.q, P.eps, 20, 100, trace_objective=True, device=_dev())
+    E = np.asarray(ref["E"])
+    assert np.max(np.abs(r.trace[:, 0] - E) / np.abs(E)) <= OBJ_TOL
+    assert abs(r.gw_objective - ref["gw_objective"]) <= OBJ_TOL * abs(ref["gw_objective"])
+    assert r.marginal_violation <= max(VIOL_TOL, 2 * ref["viol"][-1])
+
+
+# ----------------------------------------------------------------------------- distance power k = 2 (f2)
+
+@pytest.mark.parametrize("n,m", [(1, 5), (64, 64), (300, 517), (1024, 777)])
+def test_grad_k2_random_plan(gw, n, m):
+    """gw_grad_dp at k = 2 (D = |x - x'|^2) vs grad_prescribed(k=2)."""
+    rng = np.random.default_rng(n + 7 * m)
+    x, y = np.sort(rng.random(n)), np.sort(rng.random(m))
+    p, q = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))
+    T = (rng.random((n, m)) / (n * m)).astype(np.float32)
+    G = gw.grad(x, y, p, q, _to_dev(gw, T), k=2).cpu().numpy().astype(np.float64)
+    Go = O.grad_prescribed(x, y, p, q, T.astype(np.float64), k=2)
+    assert _grad_err(G, Go) <= GRAD_TOL
+
+
+def test_solver_k2_trajectory(gw):
+    """Entropic GW at k = 2 on C5's distributions (reduced): objective trajectory vs the oracle."""
+    P = _c5_small(400, 300, 5, 100)
+    r = gw.solve(P.x, P.y, P.p, P.q, P.eps, P.outer, P.inner, trace_objective=True, device=_dev(), k=2)
+    ro = O.entropic_gw(P.x, P.y, P.p, P.q, P.eps, P.outer, P.inner, k=2)
+    E = np.asarray(ro["E"])
+    assert np.max(np.abs(r.trace[:, 0] - E) / np.abs(E)) <= OBJ_TOL
+    assert abs(r.gw_objective - ro["gw_objective"]) <= OBJ_TOL * abs(ro["gw_objective"])
+    assert r.marginal_violation <= max(VIOL_TOL, 2 * ro["viol"][-1])
+
+
+def test_fgw_k2(gw):
+    P = _c5_small(300, 256, 4, 60)
+    r = gw.solve(P.x, P.y, P.p, P.q, P.eps, P.outer, P.inner, fx=P.fx, fy=P.fy, alpha=0.5, device=_dev(), k=2)
+    ro = O.entropic_fgw(P.x, P.y, P.p, P.q, P.fx, P.fy, 0.5, P.eps, P.outer, P.inner, k=2)
+    assert abs(r.gw_objective - ro["gw_objective"]) <= OBJ_TOL * abs(ro["gw_objective"])
+
+
+def test_k3_unsupported(gw):
+    from paper_2404_08970_b200 import GwError
+    rng = np.random.default_rng(0)
+    x = np.sort(rng.random(16))
+    p = np.full(16, 1 / 16)
+    T = _to_dev(gw, np.full((16, 16), 1 / 256, dtype=np.float32))
+    with pytest.raises(GwError) as e:
+        gw.grad(x, x, p, p, T, k=3)
+    assert e.value.code == "GW_ERR_UNSUPPORTED"

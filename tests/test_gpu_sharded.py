@@ -153,3 +153,18 @@ def test_sharded_rejects_bad_shards(gw):
         return "ok"
 
     assert _run_ranks(2, fn) == ["GW_ERR_DIM_MISMATCH", "GW_ERR_DIM_MISMATCH"]
+
+
+def test_sharded_k2_solve(gw):
+    api, dist = gw
+    P = _c5(300, 260, 4, 60)
+    r1 = api.solve(P.x, P.y, P.p, P.q, P.eps, P.outer, P.inner, k=2)
+
+    def fn(r, ctx, st):
+        r0, nl = dist.shard_rows(P.x.size, 3, r)
+        return api.solve(P.x, P.y, P.p, P.q, P.eps, P.outer, P.inner, ctx=ctx, row0=r0, n_local=nl,
+                         device=ctx.device, k=2).gw_objective
+
+    out = _run_ranks(3, fn)
+    assert out[0] == out[1] == out[2]
+    assert abs(out[0] - r1.gw_objective) <= 1e-6 * abs(r1.gw_objective)
