@@ -933,7 +933,9 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
                           int iters, double tol, int check_every, int* used, int* converged, bool reset_count = true) {
   const int64_t nl = P.nl, m = P.m;
   const float c2f = (float)(GW_LOG2E / eps);
-  dim3 cgrid((unsigned)((m + 1023) / 1024), (unsigned)s.nrb);
+  // grid-stride launches: when the fused path runs, the skipped safe-path kernels cost one small wave
+  const unsigned cgrid = (unsigned)std::min<int64_t>(((m + 1023) / 1024) * s.nrb, 148 * 4);
+  const unsigned rgrid = (unsigned)std::min<int64_t>((nl + RROWS - 1) / RROWS, 148 * 4);
   CU(cudaMemsetAsync(s.stop, 0, sizeof(int), c->stream));
   if (reset_count) CU(cudaMemsetAsync(s.mode, 0, 4 * sizeof(int), c->stream));  // dev = 0; count = 0
   // first iteration: speculative fused path if available (validated before commit), else safe
@@ -987,7 +989,7 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
       if (check) CU(cudaMemsetAsync(s.viol, 0, sizeof(float), c->stream));
       double* fout = check ? s.ftmp : s.f;
       PROF_BEGIN(c, PC_SINK_ROW);
-      k_sink_row<<<(unsigned)((nl + RROWS - 1) / RROWS), 256, 0, c->stream>>>(
+      k_sink_row<<<rgrid, 256, 0, c->stream>>>(
           G, ldG, nl, m, s.gh, s.gl, c2f, s.f, fout, P.lp + P.row0, eps, s.fh, s.fl, check ? s.viol : nullptr, s.stop,
           skip);
       KCHECK();
@@ -1027,7 +1029,7 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
   if (tolmode) {
     // final check of the plan after `done` iterations (row half-step into ftmp, not committed)
     CU(cudaMemsetAsync(s.viol, 0, sizeof(float), c->stream));
-    k_sink_row<<<(unsigned)((nl + RROWS - 1) / RROWS), 256, 0, c->stream>>>(
+    k_sink_row<<<rgrid, 256, 0, c->stream>>>(
         G, ldG, nl, m, s.gh, s.gl, c2f, s.f, s.ftmp, P.lp + P.row0, eps, s.fh, s.fl, s.viol, nullptr, nullptr);
     KCHECK();
     TRY(sink_viol_global(c, P, s));

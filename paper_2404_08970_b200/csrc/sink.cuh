@@ -30,12 +30,11 @@ __global__ void __launch_bounds__(256) k_sink_row(const float* __restrict__ G, i
                                                   float* __restrict__ viol, const int* __restrict__ stop,
                                                   const int* __restrict__ skip_if_fast) {
   if (stop && *stop) return;
-  if (skip_if_fast && *skip_if_fast) return;
+  if (skip_if_fast && *skip_if_fast) return;  // a skipped launch costs one small wave (grid-stride)
   __shared__ float smm[RROWS][8], sms[RROWS][8];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t r0 = (int64_t)blockIdx.x * RROWS;
+  for (int64_t r0 = (int64_t)blockIdx.x * RROWS; r0 < nl; r0 += (int64_t)gridDim.x * RROWS) {
   const int nr = (int)min((int64_t)RROWS, nl - r0);
-  if (nr <= 0) return;
   LSE2 st[RROWS];
 #pragma unroll
   for (int r = 0; r < RROWS; ++r) st[r] = LSE2{-INFINITY, 0.f};
@@ -104,6 +103,8 @@ __global__ void __launch_bounds__(256) k_sink_row(const float* __restrict__ G, i
       atomic_max_nonneg(viol, (float)fmin(v, 3.0e38));
     }
   }
+  __syncthreads();  // smm / sms are reused by the next row group
+  }
 }
 
 // ---------------------------------------------------------------------------------
@@ -116,10 +117,12 @@ __global__ void __launch_bounds__(256) k_sink_col(const float* __restrict__ G, i
                                                   float c2f, int64_t RB, float2* __restrict__ part,
                                                   const int* __restrict__ stop, const int* __restrict__ skip_if_fast) {
   if (stop && *stop) return;
-  if (skip_if_fast && *skip_if_fast) return;
-  const int64_t q0 = ((int64_t)blockIdx.x * 256 + threadIdx.x) * 4;
-  if (q0 >= m) return;
-  const int64_t rb = blockIdx.y;
+  if (skip_if_fast && *skip_if_fast) return;  // a skipped launch costs one small wave (grid-stride)
+  const int64_t ncb = (m + 1023) / 1024, nrb = (nl + RB - 1) / RB;
+  for (int64_t item = blockIdx.x; item < ncb * nrb; item += gridDim.x) {
+  const int64_t q0 = ((item % ncb) * 256 + threadIdx.x) * 4;
+  if (q0 >= m) continue;
+  const int64_t rb = item / ncb;
   const int64_t rs = rb * RB, re = min(nl, rs + RB);
   LSE2 st[4];
 #pragma unroll
@@ -167,6 +170,7 @@ __global__ void __launch_bounds__(256) k_sink_col(const float* __restrict__ G, i
 #pragma unroll
   for (int k = 0; k < 4; ++k)
     if (q0 + k < m) part[rb * m + q0 + k] = make_float2(st[k].m, st[k].s);
+  }
 }
 
 // Column half-step, pass 2a: merge this rank's row-block partials in fixed order, in fp64:
