@@ -503,11 +503,53 @@ __global__ void __launch_bounds__(NT, 1) k_sink_fused2(FusedArgs a) {
       pcur = pnx;
       if (j0 + 2 < nrows) Fnx.x = fh[j0 + 2], pnx.x = pf[j0 + 2];
       if (j1 + 2 < nrows) Fnx.y = fh[j1 + 2], pnx.y = pf[j1 + 2];
-      float s0 = do_row(j0, F.x, c0e);
-      float s1 = 0.f;
-      if (j1 < nrows) {
+      float s0, s1 = 0.f;
+      if (bytes > 0 && full_tile && j1 < nrows) {
+        // common case: wait for both stages, then exponentiate the two rows in one block so the
+        // scheduler can interleave their independent chains
+        const int st0 = j0 % FSTAGES, st1 = j1 % FSTAGES;
+        mbar_wait(&full[st0], (uint32_t)((j0 / FSTAGES) & 1));
+        mbar_wait(&full[st1], (uint32_t)((j1 / FSTAGES) & 1));
+        const float4* sp0 = reinterpret_cast<const float4*>(ring + (size_t)st0 * W);
+        const float4* sp1 = reinterpret_cast<const float4*>(ring + (size_t)st1 * W);
+        float2 q0 = make_float2(0.f, 0.f), q1 = q0;
+        const float2 F0 = make_float2(F.x, F.x), F1 = make_float2(F.y, F.y);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const float4 g0 = sp0[t + NT * k], g1 = sp1[t + NT * k];
+          const float2 a00 = fadd2(ffma2(make_float2(g0.x, g0.y), nc2, ghv[k][0]), F0);
+          const float2 a01 = fadd2(ffma2(make_float2(g0.z, g0.w), nc2, ghv[k][1]), F0);
+          const float2 a10 = fadd2(ffma2(make_float2(g1.x, g1.y), nc2, ghv[k][0]), F1);
+          const float2 a11 = fadd2(ffma2(make_float2(g1.z, g1.w), nc2, ghv[k][1]), F1);
+          c0e[k][0] = make_float2(ex2_ftz(a00.x), ex2_ftz(a00.y));
+          c0e[k][1] = make_float2(ex2_ftz(a01.x), ex2_ftz(a01.y));
+          c1e[k][0] = make_float2(ex2_ftz(a10.x), ex2_ftz(a10.y));
+          c1e[k][1] = make_float2(ex2_ftz(a11.x), ex2_ftz(a11.y));
+          q0 = fadd2(q0, fadd2(c0e[k][0], c0e[k][1]));
+          q1 = fadd2(q1, fadd2(c1e[k][0], c1e[k][1]));
+        }
+        s0 = q0.x + q0.y;
+        s1 = q1.x + q1.y;
+        __syncwarp();
+        if (lane == 0) {  // release both stages; the last warp to release a stage refills it
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int st = h ? st1 : st0, nxt = (h ? j1 : j0) + FSTAGES;
+            if (atomicAdd(&scnt[st], 1u) == NW - 1) {
+              scnt[st] = 0u;
+              if (nxt < nrows) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(&full[st], bytes);
+                tma_load_1d(ring + (size_t)st * W, Gbase + (int64_t)nxt * ld, bytes, &full[st]);
+              }
+            }
+          }
+        }
+      } else if (j1 < nrows) {
+        s0 = do_row(j0, F.x, c0e);
         s1 = do_row(j1, F.y, c1e);
       } else {
+        s0 = do_row(j0, F.x, c0e);
 #pragma unroll
         for (int k = 0; k < K; ++k) { c1e[k][0] = make_float2(0.f, 0.f); c1e[k][1] = c1e[k][0]; }
         pcur.y = 0.f;
