@@ -42,6 +42,7 @@ struct FusedArgs {
   double* part;               // [nclusters][m] column sums of the half-step plan
   int64_t rows_per_cluster;
   int l2_ahead;               // rows beyond the ring to prefetch into L2 (0: none)
+  int64_t wcol;               // columns per CTA (k_sink_fused2; <= the stage capacity 4 K NT)
   const int* mode;            // run only if *mode == 1
   const int* stop;
 };
@@ -333,7 +334,8 @@ __global__ void __launch_bounds__(NT, 1) k_sink_fused(FusedArgs a) {
       float S = 0.f;
       if (NX >= 32) {
 #pragma unroll
-        for (int i = 0; i < NX / 32; ++i) S += xs[psl][lane + 32 * i];
+        for (int i = 0; i < (NX + 31) / 32; ++i)
+          if (lane + 32 * i < NX) S += xs[psl][lane + 32 * i];
       } else {
         S = lane < NX ? xs[psl][lane] : 0.f;
       }
@@ -410,8 +412,8 @@ __global__ void __launch_bounds__(NT, 1) k_sink_fused2(FusedArgs a) {
   const uint32_t cr = blockIdx.x % CL;
   const int64_t cid = blockIdx.x / CL;
   const int64_t m = a.m;
-  const int64_t c0 = (int64_t)cr * W;
-  const int64_t ncol = max((int64_t)0, min((int64_t)W, m - c0));
+  const int64_t c0 = (int64_t)cr * a.wcol;
+  const int64_t ncol = max((int64_t)0, min(a.wcol, m - c0));  // this CTA's columns (<= W)
   const uint32_t bytes = (uint32_t)(((ncol + 3) & ~int64_t(3)) * 4);
   const int64_t rb = cid * a.rows_per_cluster;
   const int64_t re = min(a.nl, rb + a.rows_per_cluster);
@@ -421,6 +423,13 @@ __global__ void __launch_bounds__(NT, 1) k_sink_fused2(FusedArgs a) {
   const float* __restrict__ Gbase = a.G + rb * a.ld + c0;
   const int64_t ld = a.ld;
 
+  // A CTA slice narrower than the stage (wcol < W): stage slots beyond the loaded bytes are never
+  // written by TMA; zero them once so that with g_hi = -inf on every column the CTA does not own,
+  // e = 2^(0 c - inf + F) = 0 there.
+  if (ncol < W) {
+    for (int i = t; i < FSTAGES * W; i += NT) ring[i] = 0.f;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
   if (t == 0) {
     for (int s = 0; s < FSTAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -446,16 +455,19 @@ __global__ void __launch_bounds__(NT, 1) k_sink_fused2(FusedArgs a) {
   const uint32_t peer = (uint32_t)min(lane, CL - 1);
   const uint32_t rx0 = mapa(&xs[0][cr * NW + wid], peer), rb0 = mapa(&xbar[0], peer);
   constexpr uint32_t XSTRIDE = sizeof(xs[0]), BSTRIDE = sizeof(uint64_t);
-  const bool full_tile = (ncol == W);
+  // per-element masks are only needed where the last loaded float4 straddles m (m % 4 != 0);
+  // elsewhere every slot is a real column of this CTA or a zeroed slot with g_hi = -inf
+  const bool full_tile = !((c0 + ncol >= m) && (m & 3));
 
   float2 ghv[K][2], acc[K][2];
 #pragma unroll
   for (int k = 0; k < K; ++k)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int64_t col = c0 + 4 * (t + NT * k) + 2 * h;
-      ghv[k][h].x = col < m ? a.gh[col] : 0.f;
-      ghv[k][h].y = col + 1 < m ? a.gh[col + 1] : 0.f;
+      const int64_t lc = 4 * (t + NT * k) + 2 * h;  // column inside the CTA slice
+      const int64_t col = c0 + lc;
+      ghv[k][h].x = (lc < ncol && col < m) ? a.gh[col] : -INFINITY;
+      ghv[k][h].y = (lc + 1 < ncol && col + 1 < m) ? a.gh[col + 1] : -INFINITY;
       acc[k][h] = make_float2(0.f, 0.f);
       acc64[(k * 4 + 2 * h) * NT + t] = 0.0;
       acc64[(k * 4 + 2 * h + 1) * NT + t] = 0.0;
@@ -569,10 +581,12 @@ __global__ void __launch_bounds__(NT, 1) k_sink_fused2(FusedArgs a) {
       float S0 = 0.f, S1 = 0.f;
       if (NX >= 32) {
 #pragma unroll
-        for (int i = 0; i < NX / 32; ++i) {
-          const float2 v = xs[psl][lane + 32 * i];
-          S0 += v.x;
-          S1 += v.y;
+        for (int i = 0; i < (NX + 31) / 32; ++i) {
+          if (lane + 32 * i < NX) {
+            const float2 v = xs[psl][lane + 32 * i];
+            S0 += v.x;
+            S1 += v.y;
+          }
         }
       } else if (lane < NX) {
         const float2 v = xs[psl][lane];
@@ -618,11 +632,12 @@ __global__ void __launch_bounds__(NT, 1) k_sink_fused2(FusedArgs a) {
   for (int k = 0; k < K; ++k)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int64_t col = c0 + 4 * (t + NT * k) + 2 * h;
+      const int64_t lc = 4 * (t + NT * k) + 2 * h;
+      const int64_t col = c0 + lc;
       const double v0 = acc64[(k * 4 + 2 * h) * NT + t] + (double)acc[k][h].x;
       const double v1 = acc64[(k * 4 + 2 * h + 1) * NT + t] + (double)acc[k][h].y;
-      if (col < m) a.part[cid * m + col] = v0;
-      if (col + 1 < m) a.part[cid * m + col + 1] = v1;
+      if (lc < ncol && col < m) a.part[cid * m + col] = v0;
+      if (lc + 1 < ncol && col + 1 < m) a.part[cid * m + col + 1] = v1;
     }
   cluster_arrive();
   cluster_wait();

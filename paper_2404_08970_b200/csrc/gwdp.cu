@@ -770,6 +770,7 @@ struct SinkState {
   float* Srow;    // [nl]
   float* pf;      // [nl] p as fp32
   int fK = 0, fCL = 0, fNT = 256, fncl = 0;  // fK == 0: fast path unavailable for this shape
+  int64_t fW = 0;                            // columns per CTA
   int64_t frpc = 0;
   // column-sum exchange: this rank's column LSE pairs / column sums, and all ranks' (gathered)
   double *lse, *lseg, *csl, *csg;
@@ -783,6 +784,10 @@ static gw_status fused_config_t(gw_ctx* c, int* ncl) {
   const size_t dsm = fused_dyn_smem<K, NT>();
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
   CU(cudaFuncSetAttribute(k_sink_fused2<K, CL, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+  if (CL > 8) {  // non-portable cluster sizes (B200 allows up to 16)
+    CU(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CU(cudaFuncSetAttribute(k_sink_fused2<K, CL, NT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(148 * CL);
   cfg.blockDim = dim3(NT);
@@ -832,6 +837,7 @@ static gw_status fused_launch_t(gw_ctx* c, const FusedArgs& fa, int ncl) {
     case 512 + 4 * 16 + 2: return FN<4, 2, 512>(__VA_ARGS__);                     \
     case 512 + 4 * 16 + 4: return FN<4, 4, 512>(__VA_ARGS__);                     \
     case 512 + 4 * 16 + 8: return FN<4, 8, 512>(__VA_ARGS__);                     \
+    case 256 + 8 * 16 + 9: return FN<8, 9, 256>(__VA_ARGS__);                     \
     default: return fail(GW_ERR_UNSUPPORTED, "fused path: no instance K=%d CL=%d NT=%d", K, CL, NT); \
   }
 static gw_status fused_config(gw_ctx* c, int K, int CL, int NT, int* ncl) { FUSED_DISPATCH(fused_config_t, c, ncl) }
@@ -890,12 +896,21 @@ static gw_status sink_alloc(gw_ctx* c, const Prepared& P, SinkState& s) {
     }
     if (CL == 3) CL = 4;
     if (CL > 4 && CL < 8) CL = 8;
-    if (CL <= 8) {
+    int64_t wcol = 4 * (int64_t)K * NT;
+    // Clusters must fit in a GPC: on B200 clusters of 8 leave 28 SMs idle (15 clusters); clusters of
+    // 9 narrower CTAs (wcol = m / 9) use 135 SMs but still 15 clusters, and the per-row cost is set
+    // by the warp count, so it measured no faster (5.73 vs 5.79 TB/s at m = 65536): opt-in only.
+    const char* c9 = getenv("GWDP_FUSED_CL9");
+    if (c9 && c9[0] == '1' && !getenv("GWDP_FUSED_V1") && NT == 256 && CL == 8 && 9 * (wcol - 4) >= P.m) {
+      CL = 9;
+      wcol = ((P.m + 8) / 9 + 3) & ~int64_t(3);
+    }
+    if (CL <= 9) {
       int ncl = 0;
       TRY(fused_config(c, K, CL, NT, &ncl));
       if (ncl > 0) {
         ncl = (int)std::min<int64_t>(ncl, P.nl);
-        s.fK = K; s.fCL = CL; s.fNT = NT; s.fncl = ncl;
+        s.fK = K; s.fCL = CL; s.fNT = NT; s.fncl = ncl; s.fW = wcol;
         s.frpc = (P.nl + ncl - 1) / ncl;
         TRY(ws(c, c->fpart, (size_t)ncl * P.m, &s.fpart));
         TRY(ws(c, c->srow, (size_t)P.nl, &s.Srow));
@@ -949,7 +964,7 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
   FusedArgs fa;
   fa.G = G; fa.ld = ldG; fa.nl = nl; fa.m = m; fa.c2f = c2f; fa.gh = s.gh; fa.gl = s.gl; fa.fh = s.fh;
   fa.fl = s.fl; fa.pf = s.pf; fa.Srow = s.Srow; fa.part = s.fpart; fa.rows_per_cluster = s.frpc;
-  fa.mode = s.mode; fa.stop = s.stop;
+  fa.mode = s.mode; fa.stop = s.stop; fa.wcol = s.fW;
   {
     const char* pf = getenv("GWDP_L2_AHEAD");
     fa.l2_ahead = pf ? atoi(pf) : 0;
