@@ -443,3 +443,153 @@ __global__ void __launch_bounds__(G2T, OBJ ? 3 : 4) k_grad_store2(MainArgs a, TS
 }
 
 }  // namespace gw
+
+namespace gw {
+
+// ---------------------------------------------------------------------------------
+// Moments without shared-memory staging (outputs as k_grad_moments / k_grad_moments2).
+// CTA = 256 threads, tile 256 x 256: warp w owns rows w, w+8, ..., lane L owns columns
+// c0 + 8L .. c0 + 8L + 7 (two coalesced float4 per row).  Per row the lane's 8 values give its
+// partial (P, A) of the row and feed its 8 column accumulators (fp32 over the tile's rows).
+// Rows are taken 4 at a time: the 8 lane partials (4 rows x {P, A}) are reduced over the warp by
+// recursive halving (9 shuffles instead of 40); fixed lane structure => deterministic.
+// ---------------------------------------------------------------------------------
+template <int MODE>
+__global__ void __launch_bounds__(256) k_grad_moments3(TSrc2 S, int64_t nl, int64_t m, const double* __restrict__ xl,
+                                                       const double* __restrict__ yc, double* __restrict__ rP,
+                                                       double* __restrict__ rA, double* __restrict__ cS,
+                                                       double* __restrict__ cX) {
+  __shared__ float red[2][8][TC];
+  const int s = blockIdx.x, b = blockIdx.y;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t c0 = (int64_t)s * TC, r0 = (int64_t)b * TR;
+  const int64_t q0 = c0 + 8 * lane;
+  const double ye = yc[min(c0 + TC, m - 1)];
+  const double xe = xl[min(r0 + TR, nl - 1)];
+  float2 dy[4], gh[4], gl[4], cs[4], cx[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int64_t q = q0 + 2 * k;
+    dy[k] = make_float2(q < m ? (float)(ye - yc[q]) : 0.f, q + 1 < m ? (float)(ye - yc[q + 1]) : 0.f);
+    gh[k] = make_float2(0.f, 0.f);
+    gl[k] = gh[k];
+    if (MODE != T_EXPLICIT) {
+      gh[k] = make_float2(q < m ? S.gh[q] : 0.f, q + 1 < m ? S.gh[q + 1] : 0.f);
+      if (MODE == T_GIBBS) gl[k] = make_float2(q < m ? S.gl[q] : 0.f, q + 1 < m ? S.gl[q + 1] : 0.f);
+    }
+    cs[k] = make_float2(0.f, 0.f);
+    cx[k] = cs[k];
+  }
+  const float2 nch = make_float2(-S.ch, -S.ch), ncl = make_float2(-S.cl, -S.cl);
+  const bool colsok = q0 + 8 <= m;  // all 8 columns of this lane are real
+  const int nrows = (int)min((int64_t)TR, nl - r0);
+  for (int rr = 0; rr < TR; rr += 32) {  // 4 rows per warp per group (8 warps x 4 = 32 rows)
+    if (rr >= nrows) break;              // uniform
+    float v[8];
+    float2 tv[4][4];                     // [row u][float2 k]
+    float F[4], Fl[4], dxr[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int rl = rr + w + 8 * u;
+      const int64_t j = r0 + rl;
+      const bool jv = rl < nrows;
+      F[u] = 0.f; Fl[u] = 0.f;
+      if (MODE != T_EXPLICIT && jv) {
+        F[u] = S.fh[j];
+        if (MODE == T_GIBBS) Fl[u] = S.fl[j];
+      }
+      dxr[u] = jv ? (float)(xe - xl[j]) : 0.f;
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), c = a;
+      if (MODE != T_PRODUCT && jv) {
+        const float* row = S.T + j * S.ld + q0;
+        if (q0 < m) a = __ldcs(reinterpret_cast<const float4*>(row));
+        if (q0 + 4 < m) c = __ldcs(reinterpret_cast<const float4*>(row + 4));
+      }
+      tv[u][0] = make_float2(a.x, a.y); tv[u][1] = make_float2(a.z, a.w);
+      tv[u][2] = make_float2(c.x, c.y); tv[u][3] = make_float2(c.z, c.w);
+    }
+    float part[8];  // [u][P, A]
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int rl = rr + w + 8 * u;
+      const bool jv = rl < nrows;
+      float2 P2 = make_float2(0.f, 0.f), A2 = P2;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float2 t = tv[u][k];
+        if (MODE == T_GIBBS) {
+          const float2 aa = fadd2(fadd2(ffma2(t, nch, gh[k]), make_float2(F[u], F[u])),
+                                  ffma2(t, ncl, fadd2(gl[k], make_float2(Fl[u], Fl[u]))));
+          t = make_float2(ex2_ftz(aa.x), ex2_ftz(aa.y));
+        } else if (MODE == T_PRODUCT) {
+          t = make_float2(F[u] * gh[k].x, F[u] * gh[k].y);
+        }
+        if (!jv) t = make_float2(0.f, 0.f);
+        if (!colsok) {
+          const int64_t q = q0 + 2 * k;
+          if (q >= m) t.x = 0.f;
+          if (q + 1 >= m) t.y = 0.f;
+        }
+        P2 = fadd2(P2, t);
+        A2 = ffma2(dy[k], t, A2);
+        cs[k] = fadd2(cs[k], t);
+        cx[k] = ffma2(make_float2(dxr[u], dxr[u]), t, cx[k]);
+      }
+      part[2 * u] = P2.x + P2.y;
+      part[2 * u + 1] = A2.x + A2.y;
+    }
+    // recursive halving over the warp: 8 values -> lanes with (lane & 3) == 0 hold value lane >> 2
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const bool hi = lane & 16;
+      const float send = hi ? part[i] : part[4 + i];
+      const float keep = hi ? part[4 + i] : part[i];
+      part[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const bool hi = lane & 8;
+      const float send = hi ? part[i] : part[2 + i];
+      const float keep = hi ? part[2 + i] : part[i];
+      part[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    {
+      const bool hi = lane & 4;
+      const float send = hi ? part[0] : part[1];
+      const float keep = hi ? part[1] : part[0];
+      part[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    part[0] += __shfl_xor_sync(0xffffffffu, part[0], 2);
+    part[0] += __shfl_xor_sync(0xffffffffu, part[0], 1);
+    if ((lane & 3) == 0) {
+      const int idx = lane >> 2;  // = 4 bit4 + 2 bit3 + bit2
+      const int u = idx >> 1;
+      const int rl = rr + w + 8 * u;
+      const int64_t j = r0 + rl;
+      if (rl < nrows) {
+        if (idx & 1) rA[(int64_t)s * nl + j] = (double)part[0];
+        else rP[(int64_t)s * nl + j] = (double)part[0];
+      }
+    }
+  }
+  // column partials: fixed-order sum over the 8 warps
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    red[0][w][8 * lane + 2 * k] = cs[k].x;
+    red[0][w][8 * lane + 2 * k + 1] = cs[k].y;
+    red[1][w][8 * lane + 2 * k] = cx[k].x;
+    red[1][w][8 * lane + 2 * k + 1] = cx[k].y;
+  }
+  __syncthreads();
+  const int t = threadIdx.x;
+  const int64_t q = c0 + t;
+  if (q < m) {
+    double a = 0.0, bx = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < 8; ++ww) { a += red[0][ww][t]; bx += red[1][ww][t]; }
+    cS[b * m + q] = a;
+    cX[b * m + q] = bx;
+  }
+}
+
+}  // namespace gw

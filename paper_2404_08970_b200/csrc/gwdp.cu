@@ -513,7 +513,14 @@ static gw_status grad_pass_k1(gw_ctx* c, const Prepared& P, int mode, const TSrc
   // the objective pass is timed as its own class
   const int pc_mom = !obj ? PC_GRAD_MOMENTS : PC_OBJ, pc_main = !obj ? PC_GRAD_MAIN : PC_OBJ;
   PROF_BEGIN(c, pc_mom);
-  if (fast) {
+  static const bool mom2 = getenv("GWDP_MOMENTS2") != nullptr;  // smem-staged variant (comparison)
+  if (fast && !mom2) {
+    switch (mode) {
+      case T_EXPLICIT: k_grad_moments3<T_EXPLICIT><<<grid, 256, 0, c->stream>>>(S2, nl, m, xl, P.yc, rP, rA, cS, cX); break;
+      case T_GIBBS: k_grad_moments3<T_GIBBS><<<grid, 256, 0, c->stream>>>(S2, nl, m, xl, P.yc, rP, rA, cS, cX); break;
+      default: k_grad_moments3<T_PRODUCT><<<grid, 256, 0, c->stream>>>(S2, nl, m, xl, P.yc, rP, rA, cS, cX); break;
+    }
+  } else if (fast) {
     switch (mode) {
       case T_EXPLICIT: k_grad_moments2<T_EXPLICIT><<<grid, G2T, 0, c->stream>>>(S2, nl, m, xl, P.yc, rP, rA, cS, cX); break;
       case T_GIBBS: k_grad_moments2<T_GIBBS><<<grid, G2T, 0, c->stream>>>(S2, nl, m, xl, P.yc, rP, rA, cS, cX); break;
