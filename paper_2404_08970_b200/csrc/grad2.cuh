@@ -135,6 +135,71 @@ __device__ __forceinline__ void g2_stage(const G2Loader<MODE>& L, const TSrc2& S
   }
 }
 
+// Interior tiles (all 256 rows and columns real): loads with a running row pointer, T
+// regeneration with the tile's column duals held in registers (gq: g_hi, gq2: g_lo of the
+// lane's 8 columns) and the row duals from shared memory, no masks.
+template <int MODE>
+__device__ __forceinline__ void g2_load_fast(G2Loader<MODE>& L, const TSrc2& S, int64_t r0, int64_t c0, int sub) {
+  if constexpr (MODE != T_PRODUCT) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const float* p = S.T + (r0 + sub * G2SUB + w) * S.ld + c0 + 4 * lane;
+    const int64_t step = 4 * S.ld;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      L.v[2 * u] = __ldcs(reinterpret_cast<const float4*>(p));
+      L.v[2 * u + 1] = __ldcs(reinterpret_cast<const float4*>(p + 128));
+      p += step;
+    }
+  }
+}
+
+template <int MODE, bool OBJ>
+__device__ __forceinline__ void g2_stage_fast(const G2Loader<MODE>& L, const TSrc2& S, float* __restrict__ sT,
+                                              const float2 (&gq)[2][2], const float2 (&gq2)[2][2],
+                                              const float* __restrict__ sF, const float* __restrict__ sFl, int sub,
+                                              float* __restrict__ sT2, float* ent) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int phys = g2_phys(128 * h + 4 * lane);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int rl = w + 4 * u;
+      float4 t;
+      if (MODE == T_EXPLICIT) {
+        t = L.v[2 * u + h];
+      } else if (MODE == T_PRODUCT) {
+        const float pi = sF[sub * G2SUB + rl];
+        t = make_float4(pi * gq[h][0].x, pi * gq[h][0].y, pi * gq[h][1].x, pi * gq[h][1].y);
+      } else {
+        const float4 g = L.v[2 * u + h];
+        const float Fh = sF[sub * G2SUB + rl], Fl = sFl[sub * G2SUB + rl];
+        const float2 F2 = make_float2(Fh, Fh), Fl2 = make_float2(Fl, Fl);
+        const float2 nch = make_float2(-S.ch, -S.ch), ncl = make_float2(-S.cl, -S.cl);
+        const float2 g01 = make_float2(g.x, g.y), g23 = make_float2(g.z, g.w);
+        const float2 a0 = fadd2(fadd2(ffma2(g01, nch, gq[h][0]), F2), ffma2(g01, ncl, fadd2(gq2[h][0], Fl2)));
+        const float2 a1 = fadd2(fadd2(ffma2(g23, nch, gq[h][1]), F2), ffma2(g23, ncl, fadd2(gq2[h][1], Fl2)));
+        t = make_float4(ex2_ftz(a0.x), ex2_ftz(a0.y), ex2_ftz(a1.x), ex2_ftz(a1.y));
+        if (OBJ) {
+          constexpr float ln2 = 0.6931471805599453f;
+          const float av[4] = {a0.x, a0.y, a1.x, a1.y}, tv[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (tv[e] > 0.f) *ent += tv[e] * fmaf(av[e], ln2, -1.f);
+        }
+      }
+      if (OBJ && MODE != T_GIBBS) {
+        const float tv[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (tv[e] > 0.f) *ent += tv[e] * (__logf(tv[e]) - 1.f);
+      }
+      *reinterpret_cast<float4*>(sT + rl * G2RS + phys) = t;
+      if (OBJ) *reinterpret_cast<float4*>(sT2 + rl * G2RS + phys) = t;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------------
 // Moments (outputs as k_grad_moments in grad.cuh):
 //   rP[s][j] = sum_{q in s} T_jq,   rA[s][j] = sum_{q in s} (ye_s - y_q) T_jq
@@ -226,7 +291,7 @@ __global__ void __launch_bounds__(G2T, 4) k_grad_moments2(TSrc2 S, int64_t nl, i
 // <G, T> (GW gradient, prescribed c), sum T (ln T - 1) and <(fx - fy)^2, T> go to
 // a.tile_obj / tile_ent / tile_cc for k_obj_partial (the constants are then not alpha-scaled).
 template <int MODE, bool FGW, bool OBJ = false>
-__global__ void __launch_bounds__(G2T, OBJ ? 3 : 4) k_grad_store2(MainArgs a, TSrc2 S) {
+__global__ void __launch_bounds__(G2T, 3) k_grad_store2(MainArgs a, TSrc2 S) {
   __shared__ __align__(16) float sT[G2SUB * G2RS];  // T, then the local row scans (exclusive, per segment)
   extern __shared__ __align__(16) float sTobj[];     // OBJ: a copy of T (dynamic, G2SUB * G2RS floats)
   __shared__ __align__(16) float4 sRow[TR];         // {R_i, xh_i, v_i, dx_i} (alpha-scaled for FGW)
@@ -237,12 +302,28 @@ __global__ void __launch_bounds__(G2T, OBJ ? 3 : 4) k_grad_store2(MainArgs a, TS
   __shared__ float sFx[TR];
   __shared__ __align__(8) float2 sCar[TR];          // strip carry of each row: {P_c0, A_c0} (fp32)
   __shared__ float sSref[4];                        // y (tile-relative) of each segment's last column
+  __shared__ float sF[TR], sFl[TR];                 // row duals (hi, lo) / p (product) of the tile's rows
   __shared__ double sm[3 * (G2T / 32)];
 
   const int s = blockIdx.x, b = blockIdx.y;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const int64_t c0 = (int64_t)s * TC, r0 = (int64_t)b * TR;
   const int64_t nl = a.nl, m = a.m;
+  const bool interior = (r0 + TR <= nl) && (c0 + TC <= m);  // uniform: no masks on this tile
+  float2 gq[2][2], gq2[2][2];                       // column duals of the lane's staging columns
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int64_t q = c0 + 128 * h + 4 * lane;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      gq[h][e] = make_float2(0.f, 0.f);
+      gq2[h][e] = gq[h][e];
+      if (MODE != T_EXPLICIT && interior) {
+        gq[h][e] = make_float2(S.gh[q + 2 * e], S.gh[q + 2 * e + 1]);
+        if (MODE == T_GIBBS) gq2[h][e] = make_float2(S.gl[q + 2 * e], S.gl[q + 2 * e + 1]);
+      }
+    }
+  }
   const double yc0 = a.yc[c0], xr0 = a.xl[r0];
   const double alpha = (FGW && !OBJ) ? a.alpha : 1.0;
   const double fscale = (FGW && !OBJ) ? sqrt(1.0 - a.alpha) : 1.0;  // features: (1 - alpha)(fx - fy)^2
@@ -308,6 +389,8 @@ __global__ void __launch_bounds__(G2T, OBJ ? 3 : 4) k_grad_store2(MainArgs a, TS
     sRow[k] = make_float4((float)(alpha * R), (float)xh, (float)(alpha * 4.0 * dp), (float)(xn - xh));
     sFx[k] = FGW ? (float)(fscale * a.fx[jj]) : 0.f;
     sCar[k] = make_float2((float)a.rP[(int64_t)s * nl + jj], (float)a.rA[(int64_t)s * nl + jj]);
+    sF[k] = (MODE != T_EXPLICIT) ? S.fh[jj] : 0.f;
+    sFl[k] = (MODE == T_GIBBS) ? S.fl[jj] : 0.f;
   }
   if (t < 4) sSref[t] = (float)(a.yc[min(c0 + 64 * t + 63, m - 1)] - yc0);
   const int nsub = (int)min((int64_t)(TR / G2SUB), (nl - r0 + G2SUB - 1) / G2SUB);
@@ -316,15 +399,20 @@ __global__ void __launch_bounds__(G2T, OBJ ? 3 : 4) k_grad_store2(MainArgs a, TS
   const float m16 = (float)(-16.0 * alpha);
   double SAtop[2] = {0.0, 0.0}, AAtop[2] = {0.0, 0.0};
   G2Loader<MODE> L;
-  L.load(S, r0, c0, nl, m, 0);
+  if (interior) g2_load_fast<MODE>(L, S, r0, c0, 0);
+  else L.load(S, r0, c0, nl, m, 0);
   for (int sub = 0; sub < nsub; ++sub) {
     __syncthreads();  // previous sub-strip fully consumed; prologue smem visible
     {
       float ent = 0.f;
-      g2_stage<MODE, OBJ>(L, S, sT, r0, c0, nl, m, sub, sTobj, &ent);
+      if (interior) g2_stage_fast<MODE, OBJ>(L, S, sT, gq, gq2, sF, sFl, sub, sTobj, &ent);
+      else g2_stage<MODE, OBJ>(L, S, sT, r0, c0, nl, m, sub, sTobj, &ent);
       if (OBJ) acc_ent += (double)ent;
     }
-    if (sub + 1 < nsub) L.load(S, r0, c0, nl, m, sub + 1);
+    if (sub + 1 < nsub) {
+      if (interior) g2_load_fast<MODE>(L, S, r0, c0, sub + 1);
+      else L.load(S, r0, c0, nl, m, sub + 1);
+    }
     __syncthreads();
     // ---- row pass: exclusive gap-weighted scan of this thread's segment, in place ----
     {
@@ -415,8 +503,9 @@ __global__ void __launch_bounds__(G2T, OBJ ? 3 : 4) k_grad_store2(MainArgs a, TS
             const float2 d = fadd2(make_float2(fx, fx), make_float2(-fy2.x, -fy2.y));
             g = ffma2(d, d, g);
           }
-          if (q1v) *reinterpret_cast<float2*>(Gp + (int64_t)rl * a.ldG) = g;
-          else if (q0v) Gp[(int64_t)rl * a.ldG] = g.x;
+            if (q1v) *reinterpret_cast<float2*>(Gp) = g;
+          else if (q0v) Gp[0] = g.x;
+          Gp += a.ldG;
         }
         SA = fadd2(SA, Av);
         AA = ffma2(make_float2(rc.w, rc.w), SA, AA);
