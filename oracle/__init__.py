@@ -42,3 +42,11 @@ from .solver import (  # noqa: F401
     entropic_fgw,
     plan_from_duals,
 )
+from .grid2d import (  # noqa: F401
+    grid_points,
+    dist2d,
+    apply_distance_2d,
+    grad_prescribed_2d,
+    objective_2d,
+    entropic_gw_2d,
+)

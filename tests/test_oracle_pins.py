@@ -404,3 +404,69 @@ def test_workloads_deterministic_and_valid():
     T = P3.extra["T"]
     assert T.dtype == np.float32 and np.all(T > 0)
     np.testing.assert_allclose(T.sum(0), P3.q, rtol=1e-5)
+
+
+# --------------------------------------------------------------------------- 2-D grids (f3)
+
+@pytest.mark.parametrize("ex", GOLDEN["grid2d"], ids=lambda e: e["id"])
+def test_grid2d_worked_examples(ex):
+    np.testing.assert_allclose(O.apply_distance_2d(ex["v"], ex["axis"], ex["k"]), ex["expect"], atol=1e-15)
+    np.testing.assert_allclose(O.dist2d(ex["axis"], ex["k"]) @ np.asarray(ex["v"], float), ex["expect"], atol=1e-15)
+
+
+def test_dist2d_is_kronecker_sum_at_k1():
+    """k = 1: D-hat = D1 (x) J + J (x) D1 (PAPER.md:348 with k = 1), built with np.kron independently."""
+    rng = np.random.default_rng(0)
+    s = np.sort(rng.random(6))
+    D1 = np.abs(s[:, None] - s[None, :])
+    J = np.ones((6, 6))
+    np.testing.assert_allclose(O.dist2d(s, 1), np.kron(D1, J) + np.kron(J, D1), atol=1e-15)
+    # uniform grid: h (|a - a'| + |b - b'|)
+    h = 0.25
+    g = h * np.arange(5)
+    idx = np.array([(a, b) for a in range(5) for b in range(5)])
+    man = np.abs(idx[:, None, 0] - idx[None, :, 0]) + np.abs(idx[:, None, 1] - idx[None, :, 1])
+    np.testing.assert_allclose(O.dist2d(g, 2), (h * man) ** 2, atol=1e-14)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_apply_distance_2d_matches_dense(k):
+    rng = np.random.default_rng(k)
+    s = np.sort(rng.random(9))
+    v = rng.random(81)
+    np.testing.assert_allclose(O.apply_distance_2d(v, s, k), O.dist2d(s, k) @ v, rtol=1e-12)
+
+
+def test_grad_2d_bruteforce_and_objective():
+    """2-D gradient: against the entrywise definition 2 sum_{jq} (d_ij - d_pq)^2 T_jq
+     on a feasible plan, brute force; <G, T> = 2E (P8)."""
+    rng = np.random.default_rng(4)
+    sx, sy = np.sort(rng.random(3)), np.sort(rng.random(2))
+    N, M = 9, 4
+    p, q = rng.dirichlet(np.ones(N)), rng.dirichlet(np.ones(M))
+    T = _feasible_plan(rng, p, q)
+    DX, DY = O.dist2d(sx), O.dist2d(sy)
+    Gb = np.zeros((N, M))
+    for i in range(N):
+        for pp in range(M):
+            Gb[i, pp] = 2.0 * np.sum((DX[i][:, None] - DY[pp][None, :]) ** 2 * T)
+    G = O.grad_prescribed_2d(sx, sy, p, q, T)
+    np.testing.assert_allclose(G, Gb, rtol=1e-12, atol=1e-13)
+    E = O.objective_2d(sx, sy, T)
+    Eb = sum(((DX[i, j] - DY[a, b]) ** 2) * T[i, a] * T[j, b]
+             for i in range(N) for j in range(N) for a in range(M) for b in range(M))
+    assert abs(E - Eb) <= 1e-12 * max(1.0, abs(Eb))
+    assert abs(np.sum(G * T) - 2.0 * E) <= 1e-12
+
+
+def test_entropic_gw_2d_grid_reflection_equivariance():
+    """Reflecting one axis of the x grid (a -> n-1-a, with the marginal permuted alike) leaves the
+    objective trajectory unchanged (GW is invariant under isometries)."""
+    rng = np.random.default_rng(9)
+    n = 4
+    s = np.arange(n) / (n - 1.0)
+    p, q = rng.dirichlet(np.ones(n * n)), rng.dirichlet(np.ones(n * n))
+    r1 = O.entropic_gw_2d(s, s, p, q, 0.05, 3, 40)
+    perm = np.array([(n - 1 - a) * n + b for a in range(n) for b in range(n)])
+    r2 = O.entropic_gw_2d(s, s, p[perm], q, 0.05, 3, 40)
+    np.testing.assert_allclose(r1["E"], r2["E"], rtol=1e-9)
