@@ -75,6 +75,11 @@ typedef enum { GW_F32 = 0, GW_F64 = 1 } gw_dtype;  /* storage of every N x M mat
 /* problem flags */
 #define GW_NO_VALIDATE     0x1u  /* skip sortedness / marginal checks (caller guarantees them) */
 #define GW_HOST_VECTORS    0x2u  /* x, y, p, q (and f, g, fx, fy outputs/inputs) are host pointers */
+/* 2-D tensor grids (Table 3): n = nx^2 points (a, b) -> row a nx + b
+ * at (x[a], x[b]) with x the SORTED axis of length nx (likewise y with ny, m = ny^2), Manhattan
+ * distance |x_a - x_a'| + |x_b - x_b'| (reading R31; the paper's uniform grid is x_a = a h).
+ * k = 1, nx, ny <= 256, one rank; p (n) and q (m) as usual. */
+#define GW_GRID2D          0x4u
 
 typedef struct {
   int64_t n, m;           /* global sizes: x in R^n (rows), y in R^m (columns)        */

@@ -47,6 +47,9 @@ from .grid2d import (  # noqa: F401
     dist2d,
     apply_distance_2d,
     grad_prescribed_2d,
+    fgw_grad_prescribed_2d,
+    fgw_objective_2d,
+    entropic_fgw_2d,
     objective_2d,
     entropic_gw_2d,
 )

@@ -20,6 +20,7 @@ GW_LOSS_SQUARE = 0
 GW_F32, GW_F64 = 0, 1
 GW_NO_VALIDATE = 0x1
 GW_HOST_VECTORS = 0x2
+GW_GRID2D = 0x4
 GW_SOLVE_TRACE_OBJECTIVE = 0x1
 
 # exported symbols (include/gwdp.h) -- checked by tests/test_abi.py

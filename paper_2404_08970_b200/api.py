@@ -79,9 +79,15 @@ class Context:
             self.h = None
 
 
-def _problem(x, y, p, q, n_local=None, row0=0, flags=0, k=1):
+def _problem(x, y, p, q, n_local=None, row0=0, flags=0, k=1, grid2d=False):
     pr = L.gw_problem()
-    pr.n, pr.m = x.numel(), y.numel()
+    if grid2d:  # x, y are the grid axes (GW_GRID2D): n = len(p) = len(x)^2
+        if p.numel() != x.numel() ** 2 or q.numel() != y.numel() ** 2:
+            raise ValueError("grid2d: len(p) must be len(x)**2 and len(q) len(y)**2")
+        flags |= L.GW_GRID2D
+        pr.n, pr.m = p.numel(), q.numel()
+    else:
+        pr.n, pr.m = x.numel(), y.numel()
     pr.row0 = row0
     pr.n_local = pr.n if n_local is None else n_local
     pr.x, pr.y, pr.p, pr.q = x.data_ptr(), y.data_ptr(), p.data_ptr(), q.data_ptr()
@@ -89,10 +95,11 @@ def _problem(x, y, p, q, n_local=None, row0=0, flags=0, k=1):
     return pr
 
 
-def grad(x, y, p, q, T, out=None, validate=True, ctx=None, row0=0, k=1):
+def grad(x, y, p, q, T, out=None, validate=True, ctx=None, row0=0, k=1, grid2d=False):
     """G = 2(c 1^T + 1 c'^T) - 4 D_X T D_Y  (gw_grad_dp), fp32.
     Sharded (ctx with a multi-rank comm): x, p are the full supports/marginals, T holds this
-    rank's rows [row0, row0 + T.shape[0]) and the result holds the same rows of G."""
+    rank's rows [row0, row0 + T.shape[0]) and the result holds the same rows of G.
+    grid2d: x, y are the axes of 2-D grids with the Manhattan distance (GW_GRID2D)."""
     ctx = ctx or Context.get(T.device)
     dev = T.device
     x, y, p, q = (_vec(v, dev) for v in (x, y, p, q))
@@ -101,7 +108,7 @@ def grad(x, y, p, q, T, out=None, validate=True, ctx=None, row0=0, k=1):
     if out is None:
         out = plan_buffer(n, m, dev)
     ldG = _check_mat(out, "out")
-    pr = _problem(x, y, p, q, n_local=n, row0=row0, flags=0 if validate else L.GW_NO_VALIDATE, k=k)
+    pr = _problem(x, y, p, q, n_local=n, row0=row0, flags=0 if validate else L.GW_NO_VALIDATE, k=k, grid2d=grid2d)
     L.check(ctx.lib.gw_grad_dp(ctx.h, C.byref(pr), _ptr(T), ldT, _ptr(out), ldG, None))
     return out
 
@@ -168,17 +175,19 @@ def _opts(eps, outer, inner, tol, check_every, trace_objective):
 
 
 def solve(x, y, p, q, eps, outer, inner, tol=0.0, check_every=10, T0=None, return_plan=False,
-          trace_objective=False, fx=None, fy=None, alpha=None, device=None, ctx=None, row0=0, n_local=None, k=1):
+          trace_objective=False, fx=None, fy=None, alpha=None, device=None, ctx=None, row0=0, n_local=None, k=1,
+          grid2d=False):
     """Entropic GW (entropic_gw_solve) or, with fx/fy/alpha, entropic FGW (fgw_solve), on
     device vectors; tau = eps.  Sharded (ctx with a multi-rank
     comm): x, p (and fx) are full; this rank owns rows [row0, row0 + n_local): f, T0 and the
-    returned plan hold those rows, g is replicated, the objective and violation are global."""
+    returned plan hold those rows, g is replicated, the objective and violation are global.
+    grid2d: x, y are 2-D grid axes (GW_GRID2D); p, q have len(x)**2, len(y)**2 entries."""
     dev = torch.device(device) if device is not None else (T0.device if T0 is not None else torch.device("cuda"))
     if dev.index is None:
         dev = torch.device("cuda", torch.cuda.current_device())
     ctx = ctx or Context.get(dev)
     x, y, p, q = (_vec(v, dev) for v in (x, y, p, q))
-    n, m = x.numel(), y.numel()
+    n, m = p.numel(), q.numel()
     if n_local is not None:
         n = int(n_local)
     f = torch.empty(n, dtype=torch.float64, device=dev)
@@ -191,7 +200,7 @@ def solve(x, y, p, q, eps, outer, inner, tol=0.0, check_every=10, T0=None, retur
             T = torch.empty((n, ld), dtype=torch.float32, device=dev)[:, :m]
     elif T is not None:
         ld = T.stride(0)
-    pr = _problem(x, y, p, q, n_local=n, row0=row0, k=k)
+    pr = _problem(x, y, p, q, n_local=n, row0=row0, k=k, grid2d=grid2d)
     o = _opts(eps, outer, inner, tol, check_every, trace_objective)
     res = L.gw_result()
     tr = np.zeros((max(int(outer), 1), 4), dtype=np.float64)
@@ -207,20 +216,23 @@ def solve(x, y, p, q, eps, outer, inner, tol=0.0, check_every=10, T0=None, retur
 
 
 def solve_host(x, y, p, q, eps, outer, inner, tol=0.0, check_every=10, device=None, ctx=None,
-               fx=None, fy=None, alpha=None, row0=0, n_local=None, k=1):
+               fx=None, fy=None, alpha=None, row0=0, n_local=None, k=1, grid2d=False):
     """entropic_gw_solve with HOST vectors (GW_HOST_VECTORS): the library stages x, y, p, q
     host->device and copies the duals f, g back.  This is the end-to-end public call.
     Sharded: as solve() (f holds this rank's n_local rows)."""
     ctx = ctx or Context.get(device)
     xs, ys, ps, qs = (np.ascontiguousarray(v, dtype=np.float64) for v in (x, y, p, q))
-    n, m = xs.size, ys.size
+    n, m = ps.size, qs.size
+    if grid2d and (n != xs.size ** 2 or m != ys.size ** 2):
+        raise ValueError("grid2d: len(p) must be len(x)**2 and len(q) len(y)**2")
     nl = n if n_local is None else int(n_local)
     f = np.empty(nl)
     g = np.empty(m)
     pr = L.gw_problem()
     pr.n, pr.m, pr.row0, pr.n_local = n, m, int(row0), nl
     pr.x, pr.y, pr.p, pr.q = (a.ctypes.data for a in (xs, ys, ps, qs))
-    pr.k, pr.loss, pr.dtype, pr.flags = int(k), L.GW_LOSS_SQUARE, L.GW_F32, L.GW_HOST_VECTORS
+    pr.k, pr.loss, pr.dtype = int(k), L.GW_LOSS_SQUARE, L.GW_F32
+    pr.flags = L.GW_HOST_VECTORS | (L.GW_GRID2D if grid2d else 0)
     o = _opts(eps, outer, inner, tol, check_every, False)
     res = L.gw_result()
     tr = np.zeros((max(int(outer), 1), 4))

@@ -1,0 +1,327 @@
+// grid2d.cuh -- the GW gradient on 2-D tensor grids at k = 1 (PAPER.md:280-360,
+// the paper's Table 3 workload).
+//
+// Points i = a nx + b <-> (s_a, s_b) of an nx x nx grid with axis s (reading R31); Manhattan
+// distance D_ij = |s_a - s_a'| + |s_b - s_b'|, i.e. D = D1 (x) J + J (x) D1 (k = 1).
+// Then, with the four marginal matrices of the plan (T as a 4-index tensor T[a][b][c][d],
+// columns q = c ny + d of the ny x ny grid of y)
+//   T^AC[a][c] = sum_{b,d} T,  T^AD[a][d] = sum_{b,c} T,  T^BC[b][c] = sum_{a,d} T,  T^BD[b][d] = sum_{a,c} T,
+//   (D_X T D_Y)[(a,b),(c,d)] = V_AC[a][c] + V_AD[a][d] + V_BC[b][c] + V_BD[b][d],  V_.. = D1x T^.. D1y.
+// So the O(N M) gradient is one reduction pass over T (per-row sums over d and over c), tiny
+// n^3 products, and one write pass; no scans.  The constant term c = (D o D) p and the objective
+// use the same marginals: (D o D) p = sum_a' D1^2 P_A + sum_b' D1^2 P_B + 2 (D1 mat(p) D1).
+#pragma once
+#include "common.cuh"
+#include "fused.cuh"  // ex2_ftz
+#include "grad2.cuh"  // TSrc2, T_* modes
+
+namespace gw {
+
+constexpr int G2D_MAXN = 256;  // axis length limit (M = ny^2 <= 65536 per row)
+
+// axis sortedness / finiteness and weight signs / sum; out[8] like k_validate
+__global__ void __launch_bounds__(1024) k_g2_validate(const double* __restrict__ s, int64_t ns,
+                                                      const double* __restrict__ w, int64_t nw,
+                                                      double* __restrict__ out) {
+  __shared__ double sm[32];
+  double uns = 0, neg = 0, nf = 0, s0 = 0;
+  for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) {
+    if (!isfinite(s[i])) nf = 1;
+    if (i + 1 < ns && !(s[i + 1] >= s[i])) uns = 1;
+  }
+  for (int64_t i = threadIdx.x; i < nw; i += blockDim.x) {
+    const double wi = w[i];
+    if (!isfinite(wi)) nf = 1;
+    if (wi < 0) neg = 1;
+    s0 += wi;
+  }
+  uns = block_sum<32>(uns, sm);
+  neg = block_sum<32>(neg, sm);
+  nf = block_sum<32>(nf, sm);
+  s0 = block_sum<32>(s0, sm);
+  if (threadIdx.x == 0) {
+    out[0] = uns; out[1] = neg; out[2] = nf; out[3] = s0;
+    out[4] = 0; out[5] = 0; out[6] = 0.5 * (s[0] + s[ns - 1]); out[7] = 0;
+  }
+}
+
+// wn = w / S0, lw = ln wn; axc = axis - mid
+__global__ void k_g2_prep(const double* __restrict__ w, int64_t nw, const double* __restrict__ s, int64_t ns,
+                          const double* __restrict__ mom, double* __restrict__ wn, double* __restrict__ lw,
+                          double* __restrict__ sc) {
+  const double inv = 1.0 / mom[3], mid = mom[6];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nw; i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = w[i] * inv;
+    wn[i] = v;
+    lw[i] = log(v);
+    if (i < ns) sc[i] = s[i] - mid;
+  }
+}
+
+// WA[a] = sum_b w[a n + b], WB[b] = sum_a w[a n + b]  (fixed order)
+__global__ void k_g2_wmarg(const double* __restrict__ w, int n, double* __restrict__ WA, double* __restrict__ WB) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) {
+    double v = 0.0;
+    for (int b = 0; b < n; ++b) v += w[(int64_t)t * n + b];
+    WA[t] = v;
+  } else if (t < 2 * n) {
+    const int b = t - n;
+    double v = 0.0;
+    for (int a = 0; a < n; ++a) v += w[(int64_t)a * n + b];
+    WB[b] = v;
+  }
+}
+
+// out[r][c] = sum_{c'} Min[r][c'] |sy_c - sy_c'|     (R x C times the C x C axis distance)
+__global__ void k_g2_mul_right(const double* __restrict__ Min, int R, int C, const double* __restrict__ sy,
+                               double* __restrict__ out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= R * C) return;
+  const int r = e / C, c = e - r * C;
+  const double y = sy[c];
+  double v = 0.0;
+  for (int k = 0; k < C; ++k) v += Min[(int64_t)r * C + k] * fabs(y - sy[k]);
+  out[e] = v;
+}
+
+// out[r][c] = sum_{r'} |sx_r - sx_r'| Min[r'][c]
+__global__ void k_g2_mul_left(const double* __restrict__ sx, int R, const double* __restrict__ Min, int C,
+                              double* __restrict__ out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= R * C) return;
+  const int r = e / C, c = e - r * C;
+  const double x = sx[r];
+  double v = 0.0;
+  for (int k = 0; k < R; ++k) v += fabs(x - sx[k]) * Min[(int64_t)k * C + c];
+  out[e] = v;
+}
+
+// out[a] = sum_a' (s_a - s_a')^2 W[a']
+__global__ void k_g2_sqmv(const double* __restrict__ s, int n, const double* __restrict__ W, double* __restrict__ out) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= n) return;
+  double v = 0.0;
+  for (int k = 0; k < n; ++k) {
+    const double d = s[a] - s[k];
+    v += d * d * W[k];
+  }
+  out[a] = v;
+}
+
+// c[(a,b)] = vA[a] + vB[b] + 2 DWD[a][b]
+__global__ void k_g2_const(const double* __restrict__ vA, const double* __restrict__ vB,
+                           const double* __restrict__ DWD, int n, double* __restrict__ c) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n * n) return;
+  const int a = (int)(i / n), b = (int)(i - (int64_t)a * n);
+  c[i] = vA[a] + vB[b] + 2.0 * DWD[i];
+}
+
+// Per-row reductions of the plan: RC[i][c] = sum_d T[i,(c,d)], RD[i][d] = sum_c T[i,(c,d)]
+// (+ the row's entropy sum T (ln T - 1) when OBJ).  One CTA per row, thread d of the row's
+// ny x ny view (coalesced over d), column sums in fp32 over <= 256 terms, fp64 outputs.
+template <int MODE, bool OBJ>
+__global__ void __launch_bounds__(G2D_MAXN) k_g2_rowred(TSrc2 S, int ny, double* __restrict__ RC,
+                                                        double* __restrict__ RD, double* __restrict__ Hrow,
+                                                        const double* __restrict__ fx, const double* __restrict__ fy,
+                                                        double* __restrict__ CCrow) {
+  __shared__ float wp[G2D_MAXN][G2D_MAXN / 32 + 1];
+  const int64_t i = blockIdx.x;
+  const int d = threadIdx.x, lane = d & 31, w = d >> 5;
+  const bool dv = d < ny;
+  float Fh = 0.f, Fl = 0.f;
+  if (MODE != T_EXPLICIT) Fh = S.fh[i];
+  if (MODE == T_GIBBS) Fl = S.fl[i];
+  const float* row = (MODE == T_PRODUCT) ? nullptr : S.T + i * S.ld;
+  float rd = 0.f, ent = 0.f, cc = 0.f;
+  const float fxi = (OBJ && fx) ? (float)fx[i] : 0.f;
+  for (int c = 0; c < ny; ++c) {
+    float t = 0.f;
+    if (dv) {
+      const int64_t q = (int64_t)c * ny + d;
+      if (MODE == T_EXPLICIT) {
+        t = row[q];
+      } else if (MODE == T_PRODUCT) {
+        t = Fh * S.gh[q];
+      } else {
+        const float g = row[q];
+        const float a = (fmaf(g, -S.ch, S.gh[q]) + Fh) + fmaf(g, -S.cl, S.gl[q] + Fl);
+        t = ex2_ftz(a);
+        if (OBJ && t > 0.f) ent += t * fmaf(a, 0.6931471805599453f, -1.f);
+      }
+      if (OBJ && MODE != T_GIBBS && t > 0.f) ent += t * (__logf(t) - 1.f);
+      if (OBJ && fx) {
+        const float df = fxi - (float)fy[q];
+        cc = fmaf(df * df, t, cc);
+      }
+    }
+    rd += t;
+    float v = t;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) wp[c][w] = v;
+  }
+  __syncthreads();
+  const int nw = (blockDim.x + 31) / 32;
+  if (dv) {
+    double v = 0.0;
+    for (int k = 0; k < nw; ++k) v += (double)wp[d][k];
+    RC[i * ny + d] = v;
+    RD[i * ny + d] = (double)rd;
+  }
+  if (OBJ) {
+    __shared__ double se[G2D_MAXN / 32], sc[G2D_MAXN / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ent += __shfl_xor_sync(0xffffffffu, ent, o);
+      cc += __shfl_xor_sync(0xffffffffu, cc, o);
+    }
+    if (lane == 0) { se[w] = (double)ent; sc[w] = (double)cc; }
+    __syncthreads();
+    if (d == 0) {
+      double h = 0.0, hc = 0.0;
+      for (int k = 0; k < nw; ++k) { h += se[k]; hc += sc[k]; }
+      Hrow[i] = h;
+      if (fx) CCrow[i] = hc;
+    }
+  }
+}
+
+// T^AC[a][c] = sum_b RC[(a,b)][c], T^BC[b][c] = sum_a RC, T^AD[a][d] = sum_b RD, T^BD[b][d] = sum_a RD
+__global__ void k_g2_marg(const double* __restrict__ RC, const double* __restrict__ RD, int nx, int ny,
+                          double* __restrict__ TAC, double* __restrict__ TAD, double* __restrict__ TBC,
+                          double* __restrict__ TBD) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= 4 * nx * ny) return;
+  const int which = e / (nx * ny), k = e - which * nx * ny;
+  const int r = k / ny, col = k - r * ny;
+  const double* src = (which == 0 || which == 2) ? RC : RD;
+  double v = 0.0;
+  if (which < 2) {  // sum over b for fixed a = r
+    for (int b = 0; b < nx; ++b) v += src[((int64_t)r * nx + b) * ny + col];
+  } else {          // sum over a for fixed b = r
+    for (int a = 0; a < nx; ++a) v += src[((int64_t)a * nx + r) * ny + col];
+  }
+  double* dst = which == 0 ? TAC : which == 1 ? TAD : which == 2 ? TBC : TBD;
+  dst[k] = v;
+}
+
+// G[i][q] = alpha (2 c_i + 2 c'_q - 4 (VAC[a][c] + VAD[a][d] + VBC[b][c] + VBD[b][d])) [+ (1-alpha)(fx_i - fy_q)^2]
+// One CTA per row; the row's two ny-vectors are staged in shared memory.  The terms are O(1) and
+// cancel (G near its minimum is much smaller than c_i), so each element is summed in fp64 and
+// rounded to fp32 once (the FP64 adds are well under the store's HBM time).
+template <bool FGW>
+__global__ void __launch_bounds__(256) k_g2_store(const double* __restrict__ cX, const double* __restrict__ cY,
+                                                  const double* __restrict__ VAC, const double* __restrict__ VAD,
+                                                  const double* __restrict__ VBC, const double* __restrict__ VBD,
+                                                  int nx, int ny, int64_t row0, int64_t m, double alpha,
+                                                  const double* __restrict__ fx, const double* __restrict__ fy,
+                                                  float* __restrict__ G, int64_t ldG) {
+  __shared__ double rc[G2D_MAXN], rd[G2D_MAXN];
+  const int64_t il = blockIdx.x, i = row0 + il;
+  const int a = (int)(i / nx), b = (int)(i - (int64_t)a * nx);
+  const double ci = 2.0 * alpha * cX[i];
+  for (int k = threadIdx.x; k < ny; k += blockDim.x) {
+    rc[k] = ci - 4.0 * alpha * (VAC[(int64_t)a * ny + k] + VBC[(int64_t)b * ny + k]);
+    rd[k] = -4.0 * alpha * (VAD[(int64_t)a * ny + k] + VBD[(int64_t)b * ny + k]);
+  }
+  __syncthreads();
+  const double fxi = FGW ? fx[i] : 0.0;
+  const double a2 = 2.0 * alpha, a1 = 1.0 - alpha;
+  float* gr = G + il * ldG;
+  for (int64_t q = threadIdx.x; q < m; q += blockDim.x) {
+    const int c = (int)(q / ny), d = (int)(q - (int64_t)c * ny);
+    double v = rc[c] + rd[d] + a2 * cY[q];
+    if (FGW) {
+      const double df = fxi - fy[q];
+      v = fma(a1 * df, df, v);
+    }
+    gr[q] = (float)v;
+  }
+}
+
+// column sums of the plan (2-D objective / violation): part[chunk][q] over row chunks of 256
+template <int MODE>
+__global__ void __launch_bounds__(256) k_g2_colsum(TSrc2 S, int64_t nl, int64_t m, double* __restrict__ part) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.y * 256;
+  if (q >= m) return;
+  const int64_t r1 = min(nl, r0 + 256);
+  double acc = 0.0;
+  for (int64_t i = r0; i < r1; ++i) {
+    float t;
+    if (MODE == T_EXPLICIT) {
+      t = S.T[i * S.ld + q];
+    } else if (MODE == T_PRODUCT) {
+      t = S.fh[i] * S.gh[q];
+    } else {
+      const float g = S.T[i * S.ld + q];
+      t = ex2_ftz((fmaf(g, -S.ch, S.gh[q]) + S.fh[i]) + fmaf(g, -S.cl, S.gl[q] + S.fl[i]));
+    }
+    acc += (double)t;
+  }
+  part[(int64_t)blockIdx.y * m + q] = acc;
+}
+
+__global__ void k_g2_colsum_reduce(const double* __restrict__ part, int nchunk, int64_t m, double* __restrict__ b) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= m) return;
+  double v = 0.0;
+  for (int k = 0; k < nchunk; ++k) v += part[(int64_t)k * m + q];
+  b[q] = v;
+}
+
+// a_i = sum_c RC[i][c] (row sums of the plan)
+__global__ void k_g2_rowsum(const double* __restrict__ RC, int64_t nl, int ny, double* __restrict__ a) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nl) return;
+  double v = 0.0;
+  for (int c = 0; c < ny; ++c) v += RC[i * ny + c];
+  a[i] = v;
+}
+
+// Objective at 2-D:  out = {E, viol, -, H, -, -, -, -}
+//   E = a^T cA + b^T cB - 2 (<VAC, TAC> + <VAD, TAD> + <VBC, TBC> + <VBD, TBD>)
+// with cA = (D o D) a, cB = (D o D) b computed by the constant-term kernels on the realised marginals.
+__global__ void __launch_bounds__(1024) k_g2_objective(const double* __restrict__ a, const double* __restrict__ cA,
+                                                       const double* __restrict__ p, int64_t n,
+                                                       const double* __restrict__ b, const double* __restrict__ cB,
+                                                       const double* __restrict__ q, int64_t m,
+                                                       const double* __restrict__ VT, const double* __restrict__ TT,
+                                                       int nxny4, const double* __restrict__ Hrow,
+                                                       const double* __restrict__ CCrow, double* __restrict__ out) {
+  __shared__ double sm[32];
+  double ea = 0, eb = 0, vt = 0, h = 0, va = 0, vb = 0, ccs = 0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    ea += a[i] * cA[i];
+    h += Hrow[i];
+    if (CCrow) ccs += CCrow[i];
+    va = fmax(va, fabs(a[i] - p[i]));
+  }
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+    eb += b[i] * cB[i];
+    vb = fmax(vb, fabs(b[i] - q[i]));
+  }
+  for (int i = threadIdx.x; i < nxny4; i += blockDim.x) vt += VT[i] * TT[i];
+  ea = block_sum<32>(ea, sm);
+  eb = block_sum<32>(eb, sm);
+  vt = block_sum<32>(vt, sm);
+  h = block_sum<32>(h, sm);
+  ccs = block_sum<32>(ccs, sm);
+  __shared__ double smx[32];
+  double vmax = fmax(va, vb);
+  for (int o = 16; o > 0; o >>= 1) vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+  if ((threadIdx.x & 31) == 0) smx[threadIdx.x >> 5] = vmax;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) smx[0] = fmax(smx[0], smx[k]);
+    out[0] = ea + eb - 2.0 * vt;
+    out[1] = smx[0];
+    out[2] = vt;
+    out[3] = h;
+    out[6] = ccs;
+  }
+}
+
+}  // namespace gw

@@ -18,6 +18,7 @@
 #include "grad2.cuh"
 #include "shard.cuh"
 #include "poly.cuh"
+#include "grid2d.cuh"
 #include "sink.cuh"
 #include "vec.cuh"
 
@@ -100,6 +101,7 @@ struct gw_ctx {
   Buf fxs, fys;  // FGW features (staged)
   Buf pnf, qnf;  // fp32 marginals
   Buf yfb, pcoef, pc2s, pfx, pfy, ppart, pM;  // k = 2 path
+  Buf g2rc, g2rd, g2h, g2cc, g2tt, g2vt, g2tmp, g2s, g2a, g2b, g2ca, g2cb, g2part;  // 2-D grids
   Buf xtab, xg1, xg2, xin, xvec, xtail, xpart;  // multi-rank exchange buffers
   Buf slse, slseg, scsl, scsg, sviolg;          // Sinkhorn column-sum exchange
   Buf sflag, sflagg;
@@ -111,7 +113,8 @@ struct gw_ctx {
                 &ftmp, &viol, &stop, &iters, &part, &fpart, &mode, &srow, &pfl, &rP, &rA, &cS, &cX, &blk, &bs, &btot, &cxend,
                 &SAg, &WAg, &Ptot, &Aend, &DP, &DA, &tobj, &tent, &tcc, &objout, &fxs, &fys, &fsc, &gsc, &Gs,
                 &pnf, &qnf, &xtab, &xg1, &xg2, &xin, &xvec, &xtail, &xpart, &slse, &slseg, &scsl, &scsg,
-                &sviolg, &sflag, &sflagg, &yfb, &pcoef, &pc2s, &pfx, &pfy, &ppart, &pM};
+                &sviolg, &sflag, &sflagg, &yfb, &pcoef, &pc2s, &pfx, &pfy, &ppart, &pM,
+                &g2rc, &g2rd, &g2h, &g2cc, &g2tt, &g2vt, &g2tmp, &g2s, &g2a, &g2b, &g2ca, &g2cb, &g2part};
     for (Buf* x : b) all.push_back(x);
   }
 };
@@ -354,6 +357,8 @@ struct Prepared {
   float* yf;         // fp32 centred y (k = 2 path)
   double xlast, ylast;
   int k = 1;         // distance power
+  bool grid2d = false;  // GW_GRID2D: xc / yc are the centred axes (nx, ny entries)
+  int nx = 0, ny = 0;
   // row shards of all ranks (multi-rank only): tab[2r] = row0_r, tab[2r+1] = nl_r
   int R = 1, rank = 0;
   int64_t maxnl = 0;
@@ -371,6 +376,18 @@ static gw_status check_problem(const gw_problem* pb) {
   if (!pb->x || !pb->y || !pb->p || !pb->q) return fail(GW_ERR_INVALID_ARG, "x, y, p, q must be non-null");
   if (pb->k != 1 && pb->k != 2)
     return fail(GW_ERR_UNSUPPORTED, "distance power k=%d: k = 1 and k = 2 are implemented (R17)", pb->k);
+  if (pb->flags & GW_GRID2D) {
+    const int64_t nx = (int64_t)llround(sqrt((double)pb->n)), ny = (int64_t)llround(sqrt((double)pb->m));
+    if (nx * nx != pb->n || ny * ny != pb->m)
+      return fail(GW_ERR_INVALID_ARG, "GW_GRID2D: n = %lld and m = %lld must be squares", (long long)pb->n,
+                  (long long)pb->m);
+    if (nx > G2D_MAXN || ny > G2D_MAXN)
+      return fail(GW_ERR_UNSUPPORTED, "GW_GRID2D: grid side %lld / %lld exceeds %d", (long long)nx, (long long)ny,
+                  G2D_MAXN);
+    if (pb->k != 1) return fail(GW_ERR_UNSUPPORTED, "GW_GRID2D: only k = 1 (Manhattan distance) is implemented");
+    if (pb->row0 != 0 || pb->n_local != pb->n)
+      return fail(GW_ERR_UNSUPPORTED, "GW_GRID2D: row sharding is not implemented");
+  }
   if (pb->loss != GW_LOSS_SQUARE) return fail(GW_ERR_UNSUPPORTED, "only the square loss is defined (PAPER.md:86)");
   if (pb->dtype != GW_F32) return fail(GW_ERR_UNSUPPORTED, "only fp32 matrix storage in ABI v1");
   return GW_OK;
@@ -386,8 +403,92 @@ static gw_status check_matrix(const void* M, int64_t ld, int64_t m, const char* 
 
 // Validate (reading R16) and build the centred supports, normalised
 // marginals, their logs and the constant-term vectors c, c'.
+// (D o D) w for a 2-D grid (Manhattan, k = 1): sum_a' D1^2 W_A + sum_b' D1^2 W_B + 2 D1 mat(w) D1
+static gw_status g2_sqconst(gw_ctx* c, const double* axis, int na, const double* w, double* out) {
+  double *WAB, *vAB, *tmp, *dwd;
+  TRY(ws(c, c->g2s, 4 * (size_t)na + 2 * (size_t)na * na, &WAB));
+  vAB = WAB + 2 * na;
+  tmp = vAB + 2 * na;
+  dwd = tmp + (size_t)na * na;
+  k_g2_wmarg<<<(2 * na + 255) / 256, 256, 0, c->stream>>>(w, na, WAB, WAB + na);
+  KCHECK();
+  k_g2_sqmv<<<(na + 255) / 256, 256, 0, c->stream>>>(axis, na, WAB, vAB);
+  KCHECK();
+  k_g2_sqmv<<<(na + 255) / 256, 256, 0, c->stream>>>(axis, na, WAB + na, vAB + na);
+  KCHECK();
+  const int nn = na * na;
+  k_g2_mul_right<<<(nn + 255) / 256, 256, 0, c->stream>>>(w, na, na, axis, tmp);
+  KCHECK();
+  k_g2_mul_left<<<(nn + 255) / 256, 256, 0, c->stream>>>(axis, na, tmp, na, dwd);
+  KCHECK();
+  k_g2_const<<<(nn + 255) / 256, 256, 0, c->stream>>>(vAB, vAB + na, dwd, na, out);
+  KCHECK();
+  return GW_OK;
+}
+
+static gw_status prepare_2d(gw_ctx* c, const gw_problem* pb, Prepared& P) {
+  const int64_t n = pb->n, m = pb->m;
+  const int nx = (int)llround(sqrt((double)n)), ny = (int)llround(sqrt((double)m));
+  P.n = n; P.m = m; P.row0 = 0; P.nl = n; P.k = 1; P.grid2d = true; P.nx = nx; P.ny = ny;
+  if (nranks_of(c) > 1) return fail(GW_ERR_UNSUPPORTED, "GW_GRID2D: multi-rank is not implemented");
+  const bool host = pb->flags & GW_HOST_VECTORS;
+  if (host) {
+    double* st;
+    TRY(ws(c, c->stage, (size_t)(nx + n + ny + m), &st));
+    CU(cudaMemcpyAsync(st, pb->x, nx * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(st + nx, pb->p, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(st + nx + n, pb->y, ny * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(st + nx + n + ny, pb->q, m * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    P.x = st; P.p = st + nx; P.y = st + nx + n; P.q = st + nx + n + ny;
+  } else {
+    P.x = pb->x; P.p = pb->p; P.y = pb->y; P.q = pb->q;
+  }
+  double* mom;
+  TRY(ws(c, c->mom, 16, &mom));
+  k_g2_validate<<<1, 1024, 0, c->stream>>>(P.x, nx, P.p, n, mom);
+  KCHECK();
+  k_g2_validate<<<1, 1024, 0, c->stream>>>(P.y, ny, P.q, m, mom + 8);
+  KCHECK();
+  CU(cudaMemcpyAsync(c->hpin, mom, 16 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  const double* h = c->hpin;
+  if (!(pb->flags & GW_NO_VALIDATE)) {
+    if (h[2] != 0 || h[10] != 0) return fail(GW_ERR_NONFINITE, "non-finite entry in x, y, p or q");
+    if (h[0] != 0 || h[8] != 0) return fail(GW_ERR_UNSORTED, "the grid axes x and y must be non-decreasing");
+    if (h[1] != 0 || h[9] != 0) return fail(GW_ERR_NEGATIVE_WEIGHT, "p and q must be >= 0");
+    if (fabs(h[3] - 1.0) > 1e-9 || fabs(h[11] - 1.0) > 1e-9)
+      return fail(GW_ERR_NOT_NORMALIZED, "|sum p - 1| = %.3g, |sum q - 1| = %.3g exceed 1e-9 (SPEC.md:72)",
+                  fabs(h[3] - 1.0), fabs(h[11] - 1.0));
+  }
+  double *xc, *yc, *pn, *qn, *lp, *lq, *cx, *cy;
+  TRY(ws(c, c->xc, nx, &xc)); TRY(ws(c, c->yc, ny, &yc));
+  TRY(ws(c, c->pn, n, &pn)); TRY(ws(c, c->qn, m, &qn));
+  TRY(ws(c, c->lp, n, &lp)); TRY(ws(c, c->lq, m, &lq));
+  TRY(ws(c, c->cvx, n, &cx)); TRY(ws(c, c->cvy, m, &cy));
+  k_g2_prep<<<grid_for(n), 256, 0, c->stream>>>(P.p, n, P.x, nx, mom, pn, lp, xc);
+  KCHECK();
+  k_g2_prep<<<grid_for(m), 256, 0, c->stream>>>(P.q, m, P.y, ny, mom + 8, qn, lq, yc);
+  KCHECK();
+  TRY(g2_sqconst(c, xc, nx, pn, cx));
+  TRY(g2_sqconst(c, yc, ny, qn, cy));
+  P.xc = xc; P.yc = yc; P.pn = pn; P.qn = qn; P.lp = lp; P.lq = lq; P.cx = cx; P.cy = cy;
+  P.yf = nullptr;
+  TRY(ws(c, c->pnf, n, &P.pnf)); TRY(ws(c, c->qnf, m, &P.qnf));
+  k_to_float<<<grid_for(n), 256, 0, c->stream>>>(pn, n, P.pnf);
+  KCHECK();
+  k_to_float<<<grid_for(m), 256, 0, c->stream>>>(qn, m, P.qnf);
+  KCHECK();
+  P.xlast = P.ylast = 0.0;
+  P.R = 1; P.rank = 0;
+  P.tab.assign(2, 0);
+  P.tab[1] = n;
+  P.maxnl = n;
+  return GW_OK;
+}
+
 static gw_status prepare(gw_ctx* c, const gw_problem* pb, Prepared& P) {
   TRY(check_problem(pb));
+  if (pb->flags & GW_GRID2D) return prepare_2d(c, pb, P);
   const int64_t n = pb->n, m = pb->m;
   P.n = n; P.m = m; P.row0 = pb->row0; P.nl = pb->n_local;
   const bool host = pb->flags & GW_HOST_VECTORS;
@@ -696,9 +797,83 @@ static gw_status poly_moments(gw_ctx* c, const Prepared& P, int mode, const TSrc
   return GW_OK;
 }
 
+// 2-D grids (grid2d.cuh): per-row reductions of the plan -> four marginal matrices -> V = D1x T.. D1y
+// (tiny) -> G by rows; the objective from the same marginals plus the plan's row / column sums.
+static gw_status grad_pass_2d(gw_ctx* c, const Prepared& P, int mode, const TSrc2& S2, float* G, int64_t ldG,
+                              bool store, bool obj, const double* fx, const double* fy, double alpha,
+                              double* objout_dev) {
+  const int nx = P.nx, ny = P.ny;
+  const int64_t n = P.n, m = P.m;
+  const int nn = nx * ny;
+  double *RC, *RD, *Hr, *CCr, *TT, *VT, *tmp;
+  TRY(ws(c, c->g2rc, (size_t)n * ny, &RC)); TRY(ws(c, c->g2rd, (size_t)n * ny, &RD));
+  TRY(ws(c, c->g2h, n, &Hr)); TRY(ws(c, c->g2cc, n, &CCr));
+  TRY(ws(c, c->g2tt, 4 * (size_t)nn, &TT)); TRY(ws(c, c->g2vt, 4 * (size_t)nn, &VT));
+  TRY(ws(c, c->g2tmp, (size_t)nn, &tmp));
+  const int bt = (ny + 31) / 32 * 32;
+  PROF_BEGIN(c, PC_GRAD_MOMENTS);
+#define LAUNCH_RR(MODE, OB)                                                                                   \
+  k_g2_rowred<MODE, OB><<<(unsigned)n, bt, 0, c->stream>>>(S2, ny, RC, RD, Hr, OB ? fx : nullptr, fy, CCr)
+  if (obj) {
+    if (mode == T_EXPLICIT) LAUNCH_RR(T_EXPLICIT, true);
+    else if (mode == T_GIBBS) LAUNCH_RR(T_GIBBS, true);
+    else LAUNCH_RR(T_PRODUCT, true);
+  } else {
+    if (mode == T_EXPLICIT) LAUNCH_RR(T_EXPLICIT, false);
+    else if (mode == T_GIBBS) LAUNCH_RR(T_GIBBS, false);
+    else LAUNCH_RR(T_PRODUCT, false);
+  }
+#undef LAUNCH_RR
+  KCHECK();
+  PROF_END(c, PC_GRAD_MOMENTS, obj ? 0 : 1);
+  PROF_BEGIN(c, PC_GRAD_CARRY);
+  k_g2_marg<<<(4 * nn + 255) / 256, 256, 0, c->stream>>>(RC, RD, nx, ny, TT, TT + nn, TT + 2 * nn, TT + 3 * nn);
+  KCHECK();
+  for (int k = 0; k < 4; ++k) {
+    k_g2_mul_right<<<(nn + 255) / 256, 256, 0, c->stream>>>(TT + (size_t)k * nn, nx, ny, P.yc, tmp);
+    KCHECK();
+    k_g2_mul_left<<<(nn + 255) / 256, 256, 0, c->stream>>>(P.xc, nx, tmp, ny, VT + (size_t)k * nn);
+    KCHECK();
+  }
+  PROF_END(c, PC_GRAD_CARRY, 4);
+  if (obj) {
+    // realised marginals a = T 1 (from the row reductions), b = T^T 1 (column pass)
+    double *av, *bv, *cA, *cB, *part;
+    TRY(ws(c, c->g2a, n, &av)); TRY(ws(c, c->g2b, m, &bv));
+    TRY(ws(c, c->g2ca, n, &cA)); TRY(ws(c, c->g2cb, m, &cB));
+    const int nch = (int)((n + 255) / 256);
+    TRY(ws(c, c->g2part, (size_t)nch * m, &part));
+    k_g2_rowsum<<<grid_for(n), 256, 0, c->stream>>>(RC, n, ny, av);
+    KCHECK();
+    dim3 cg((unsigned)((m + 255) / 256), (unsigned)nch);
+    if (mode == T_EXPLICIT) k_g2_colsum<T_EXPLICIT><<<cg, 256, 0, c->stream>>>(S2, n, m, part);
+    else if (mode == T_GIBBS) k_g2_colsum<T_GIBBS><<<cg, 256, 0, c->stream>>>(S2, n, m, part);
+    else k_g2_colsum<T_PRODUCT><<<cg, 256, 0, c->stream>>>(S2, n, m, part);
+    KCHECK();
+    k_g2_colsum_reduce<<<grid_for(m), 256, 0, c->stream>>>(part, nch, m, bv);
+    KCHECK();
+    TRY(g2_sqconst(c, P.xc, nx, av, cA));
+    TRY(g2_sqconst(c, P.yc, ny, bv, cB));
+    k_g2_objective<<<1, 1024, 0, c->stream>>>(av, cA, P.pn, n, bv, cB, P.qn, m, VT, TT, 4 * nn, Hr,
+                                              fx ? CCr : nullptr, objout_dev);
+    KCHECK();
+  }
+  if (store) {
+    PROF_BEGIN(c, PC_GRAD_MAIN);
+    if (fx) k_g2_store<true><<<(unsigned)n, 256, 0, c->stream>>>(P.cx, P.cy, VT, VT + nn, VT + 2 * nn, VT + 3 * nn, nx,
+                                                                 ny, 0, m, alpha, fx, fy, G, ldG);
+    else k_g2_store<false><<<(unsigned)n, 256, 0, c->stream>>>(P.cx, P.cy, VT, VT + nn, VT + 2 * nn, VT + 3 * nn, nx,
+                                                               ny, 0, m, alpha, nullptr, nullptr, G, ldG);
+    KCHECK();
+    PROF_END(c, PC_GRAD_MAIN, 1);
+  }
+  return GW_OK;
+}
+
 static gw_status grad_pass(gw_ctx* c, const Prepared& P, int mode, const TSrc& S, const TSrc2& S2, float* G,
                            int64_t ldG, bool store, bool obj, const double* fx, const double* fy, double alpha,
                            double* objout_dev) {
+  if (P.grid2d) return grad_pass_2d(c, P, mode, S2, G, ldG, store, obj, fx, fy, alpha, objout_dev);
   if (P.k == 1) return grad_pass_k1(c, P, mode, S, S2, G, ldG, store, obj, fx, fy, alpha, objout_dev);
   const int64_t nl = P.nl, m = P.m;
   if (obj) {

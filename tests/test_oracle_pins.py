@@ -470,3 +470,28 @@ def test_entropic_gw_2d_grid_reflection_equivariance():
     perm = np.array([(n - 1 - a) * n + b for a in range(n) for b in range(n)])
     r2 = O.entropic_gw_2d(s, s, p[perm], q, 0.05, 3, 40)
     np.testing.assert_allclose(r1["E"], r2["E"], rtol=1e-9)
+
+
+def test_fgw_2d_bruteforce_and_reductions():
+    """FGW on 2-D grids (Remark 2): the gradient against the entrywise
+    (1 - a) c_ip^2 + a * 2 sum_{jq} (d_ij - d_pq)^2 T_jq on a feasible plan; alpha = 1 is GW."""
+    rng = np.random.default_rng(14)
+    sx, sy = np.sort(rng.random(3)), np.sort(rng.random(3))
+    N, M = 9, 9
+    p, q = rng.dirichlet(np.ones(N)), rng.dirichlet(np.ones(M))
+    fx, fy = rng.random(N), rng.random(M)
+    T = _feasible_plan(rng, p, q)
+    DX, DY = O.dist2d(sx), O.dist2d(sy)
+    a = 0.3
+    Gb = np.zeros((N, M))
+    for i in range(N):
+        for pp in range(M):
+            Gb[i, pp] = (1 - a) * (fx[i] - fy[pp]) ** 2 + a * 2.0 * np.sum((DX[i][:, None] - DY[pp][None, :]) ** 2 * T)
+    np.testing.assert_allclose(O.fgw_grad_prescribed_2d(sx, sy, p, q, fx, fy, a, T), Gb, rtol=1e-12, atol=1e-13)
+    Eb = sum((1 - a) * (fx[i] - fy[pp]) ** 2 * T[i, pp] for i in range(N) for pp in range(M)) + a * sum(
+        ((DX[i, j] - DY[u, v]) ** 2) * T[i, u] * T[j, v]
+        for i in range(N) for j in range(N) for u in range(M) for v in range(M))
+    assert abs(O.fgw_objective_2d(sx, sy, fx, fy, a, T) - Eb) <= 1e-12
+    r1 = O.entropic_fgw_2d(sx, sy, p, q, fx, fy, 1.0, 0.05, 2, 30)
+    r2 = O.entropic_gw_2d(sx, sy, p, q, 0.05, 2, 30)
+    np.testing.assert_allclose(r1["E"], r2["E"], rtol=1e-12)
