@@ -63,7 +63,7 @@ typedef enum {
   GW_ERR_NOT_NORMALIZED = 5,  /* |sum - 1| > 1e-9                        */
   GW_ERR_NONFINITE = 6,       /* NaN/Inf in inputs or produced          */
   GW_ERR_CONFIG = 7,          /* invalid options                                       */
-  GW_ERR_UNSUPPORTED = 8,     /* k not in {1, 2}, loss != square, tau != eps, fp64 storage, UGW */
+  GW_ERR_UNSUPPORTED = 8,     /* k > GW_MAX_K, loss != square, tau != eps, fp64 storage, UGW */
   GW_ERR_OOM = 9,
   GW_ERR_CUDA = 10,
   GW_ERR_NCCL = 11
@@ -80,13 +80,16 @@ typedef enum { GW_F32 = 0, GW_F64 = 1 } gw_dtype;  /* storage of every N x M mat
  * distance |x_a - x_a'| + |x_b - x_b'| (reading R31; the paper's uniform grid is x_a = a h).
  * k = 1, nx, ny <= 256, one rank; p (n) and q (m) as usual. */
 #define GW_GRID2D          0x4u
+/* largest distance power: k = 1 (gap-weighted scans), k = 2 (moments), 3..5 (power-sum scans,
+ * PAPER.md:229-259; one rank only for k >= 3) */
+#define GW_MAX_K           5
 
 typedef struct {
   int64_t n, m;           /* global sizes: x in R^n (rows), y in R^m (columns)        */
   int64_t row0, n_local;  /* this rank's row shard; (0, n) on one GPU                  */
   const double *x, *y;    /* supports, non-decreasing (length n and m)                 */
   const double *p, *q;    /* marginals, >= 0, sum 1 within 1e-9 (length n and m)       */
-  int32_t k;              /* distance power |x - x'|^k: 1 (hot path) or 2 (R17, f2)     */
+  int32_t k;              /* distance power |x - x'|^k: 1 (hot path) .. GW_MAX_K (R17, f2) */
   int32_t loss;           /* gw_loss */
   int32_t dtype;          /* gw_dtype; only GW_F32 in this ABI version                 */
   uint32_t flags;         /* GW_NO_VALIDATE | GW_HOST_VECTORS                          */

@@ -19,6 +19,7 @@
 #include "shard.cuh"
 #include "poly.cuh"
 #include "grid2d.cuh"
+#include "polyk.cuh"
 #include "sink.cuh"
 #include "vec.cuh"
 
@@ -101,6 +102,7 @@ struct gw_ctx {
   Buf fxs, fys;  // FGW features (staged)
   Buf pnf, qnf;  // fp32 marginals
   Buf yfb, pcoef, pc2s, pfx, pfy, ppart, pM;  // k = 2 path
+  Buf gkrp, gkrt, gkcp, gkz, gkct, gkctt, gkobj;  // k >= 3 path
   Buf g2rc, g2rd, g2h, g2cc, g2tt, g2vt, g2tmp, g2s, g2a, g2b, g2ca, g2cb, g2part;  // 2-D grids
   Buf xtab, xg1, xg2, xin, xvec, xtail, xpart;  // multi-rank exchange buffers
   Buf slse, slseg, scsl, scsg, sviolg;          // Sinkhorn column-sum exchange
@@ -114,6 +116,7 @@ struct gw_ctx {
                 &SAg, &WAg, &Ptot, &Aend, &DP, &DA, &tobj, &tent, &tcc, &objout, &fxs, &fys, &fsc, &gsc, &Gs,
                 &pnf, &qnf, &xtab, &xg1, &xg2, &xin, &xvec, &xtail, &xpart, &slse, &slseg, &scsl, &scsg,
                 &sviolg, &sflag, &sflagg, &yfb, &pcoef, &pc2s, &pfx, &pfy, &ppart, &pM,
+                &gkrp, &gkrt, &gkcp, &gkz, &gkct, &gkctt, &gkobj,
                 &g2rc, &g2rd, &g2h, &g2cc, &g2tt, &g2vt, &g2tmp, &g2s, &g2a, &g2b, &g2ca, &g2cb, &g2part};
     for (Buf* x : b) all.push_back(x);
   }
@@ -374,8 +377,8 @@ static gw_status check_problem(const gw_problem* pb) {
     return fail(GW_ERR_DIM_MISMATCH, "row shard [%lld, %lld) outside [0, %lld)", (long long)pb->row0,
                 (long long)(pb->row0 + pb->n_local), (long long)pb->n);
   if (!pb->x || !pb->y || !pb->p || !pb->q) return fail(GW_ERR_INVALID_ARG, "x, y, p, q must be non-null");
-  if (pb->k != 1 && pb->k != 2)
-    return fail(GW_ERR_UNSUPPORTED, "distance power k=%d: k = 1 and k = 2 are implemented (R17)", pb->k);
+  if (pb->k < 1 || pb->k > GW_MAX_K)
+    return fail(GW_ERR_UNSUPPORTED, "distance power k=%d: 1 <= k <= %d is implemented (R17)", pb->k, GW_MAX_K);
   if (pb->flags & GW_GRID2D) {
     const int64_t nx = (int64_t)llround(sqrt((double)pb->n)), ny = (int64_t)llround(sqrt((double)pb->m));
     if (nx * nx != pb->n || ny * ny != pb->m)
@@ -529,6 +532,14 @@ static gw_status prepare(gw_ctx* c, const gw_problem* pb, Prepared& P) {
   KCHECK();
   P.xc = xc; P.yc = yc; P.pn = pn; P.qn = qn; P.lp = lp; P.lq = lq; P.cx = cx; P.cy = cy;
   P.k = pb->k;
+  if (P.k >= 3) {  // c = (D o D) p, D = |x - x'|^k: the even power 2k by moments (polyk.cuh)
+    switch (P.k) {
+      case 3: k_gk_const<6><<<1, 1024, 0, c->stream>>>(xc, pn, n, cx); k_gk_const<6><<<1, 1024, 0, c->stream>>>(yc, qn, m, cy); break;
+      case 4: k_gk_const<8><<<1, 1024, 0, c->stream>>>(xc, pn, n, cx); k_gk_const<8><<<1, 1024, 0, c->stream>>>(yc, qn, m, cy); break;
+      default: k_gk_const<10><<<1, 1024, 0, c->stream>>>(xc, pn, n, cx); k_gk_const<10><<<1, 1024, 0, c->stream>>>(yc, qn, m, cy); break;
+    }
+    KCHECK();
+  }
   if (P.k == 2) {  // c = (D o D) p with D = |x - x'|^2, by moments up to order 4
     k_poly_const<<<1, 1024, 0, c->stream>>>(xc, pn, n, cx);
     KCHECK();
@@ -555,6 +566,7 @@ static gw_status prepare(gw_ctx* c, const gw_problem* pb, Prepared& P) {
   P.ylast = ends[3] - h[14];
   P.R = nranks_of(c);
   P.rank = c->comm ? c->comm->rank : 0;
+  if (P.k >= 3 && P.R > 1) return fail(GW_ERR_UNSUPPORTED, "k >= 3: row sharding is not implemented");
   P.tab.assign(2 * (size_t)P.R, 0);
   if (P.R > 1) {
     int64_t* dt;
@@ -870,11 +882,95 @@ static gw_status grad_pass_2d(gw_ctx* c, const Prepared& P, int mode, const TSrc
   return GW_OK;
 }
 
+// General distance power k >= 3 (polyk.cuh): tile power sums -> carries -> one main pass.
+template <int K, int MODE, bool STORE, bool OBJ, bool FGW>
+static gw_status gk_main_launch(gw_ctx* c, dim3 grid, const TSrc2& S2, int64_t nl, int64_t m, const double* xl,
+                                const double* yc, const double* rp, const double* rt, const double* Z,
+                                const double* ct, const double* cl, const double* c2, double alpha, const double* fx,
+                                const double* fy, float* G, int64_t ldG, double* tob) {
+  auto kern = k_gk_main<K, MODE, STORE, OBJ, FGW>;
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gk_smem_bytes()));
+  kern<<<grid, GK, gk_smem_bytes(), c->stream>>>(S2, nl, m, xl, yc, rp, rt, Z, ct, cl, c2, alpha, fx, fy, G, ldG,
+                                                    tob);
+  KCHECK();
+  return GW_OK;
+}
+
+template <int K, int MODE>
+static gw_status grad_pass_gk_mode(gw_ctx* c, const Prepared& P, const TSrc2& S2, float* G, int64_t ldG, bool store,
+                                   bool obj, const double* fx, const double* fy, double alpha, double* objout_dev) {
+  const int64_t nl = P.nl, m = P.m;
+  const int ntc = (int)((m + GK - 1) / GK), ntr = (int)((nl + GK - 1) / GK);
+  const size_t K1 = K + 1;
+  double *rp, *rt, *cp, *Z, *ct, *ctt, *tob;
+  TRY(ws(c, c->gkrp, (size_t)ntc * K1 * nl, &rp)); TRY(ws(c, c->gkrt, K1 * nl, &rt));
+  TRY(ws(c, c->gkcp, (size_t)ntr * K1 * m, &cp)); TRY(ws(c, c->gkz, (size_t)ntr * K1 * m, &Z));
+  TRY(ws(c, c->gkct, K1 * m, &ct)); TRY(ws(c, c->gkctt, K1 * m, &ctt));
+  TRY(ws(c, c->gkobj, (size_t)ntc * ntr, &tob));
+  const double* xl = P.xc + P.row0;
+  const dim3 grid((unsigned)ntc, (unsigned)ntr);
+  PROF_BEGIN(c, PC_GRAD_MOMENTS);
+  auto ks = k_gk_sums<K, MODE>;
+  CU(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gk_smem_bytes()));
+  ks<<<grid, GK, gk_smem_bytes(), c->stream>>>(S2, nl, m, xl, P.yc, rp, cp);
+  KCHECK();
+  PROF_END(c, PC_GRAD_MOMENTS, 1);
+  PROF_BEGIN(c, PC_GRAD_CARRY);
+  k_gk_scan_tiles<<<grid_for((int64_t)K1 * nl), 256, 0, c->stream>>>(rp, ntc, (int64_t)K1 * nl, rt);
+  KCHECK();
+  k_gk_apply<K><<<(unsigned)(ntr * K1), 256, 0, c->stream>>>(cp, m, P.yc, Z);
+  KCHECK();
+  k_gk_scan_tiles<<<grid_for((int64_t)K1 * m), 256, 0, c->stream>>>(Z, ntr, (int64_t)K1 * m, ct);
+  KCHECK();
+  PROF_END(c, PC_GRAD_CARRY, 3);
+  const double* cl = P.cx + P.row0;
+  if (obj) {
+    TRY((gk_main_launch<K, MODE, false, true, false>(c, grid, S2, nl, m, xl, P.yc, rp, rt, Z, ct, cl, P.cy, 1.0,
+                                                     nullptr, nullptr, nullptr, 0, tob)));
+    // realised marginals: a = T 1 (row totals, power 0), b = T^T 1 (column totals of the plan)
+    k_gk_scan_tiles<<<grid_for((int64_t)K1 * m), 256, 0, c->stream>>>(cp, ntr, (int64_t)K1 * m, ctt);
+    KCHECK();
+    k_gk_objective<K><<<1, 1024, 0, c->stream>>>(rt, xl, nl, ctt, P.yc, m, tob, (int64_t)ntc * ntr, objout_dev);
+    KCHECK();
+  }
+  if (store) {
+    PROF_BEGIN(c, PC_GRAD_MAIN);
+    if (fx)
+      TRY((gk_main_launch<K, MODE, true, false, true>(c, grid, S2, nl, m, xl, P.yc, rp, rt, Z, ct, cl, P.cy, alpha, fx,
+                                                      fy, G, ldG, nullptr)));
+    else
+      TRY((gk_main_launch<K, MODE, true, false, false>(c, grid, S2, nl, m, xl, P.yc, rp, rt, Z, ct, cl, P.cy, alpha,
+                                                       nullptr, nullptr, G, ldG, nullptr)));
+    PROF_END(c, PC_GRAD_MAIN, 1);
+  }
+  return GW_OK;
+}
+
+template <int K>
+static gw_status grad_pass_gk(gw_ctx* c, const Prepared& P, int mode, const TSrc2& S2, float* G, int64_t ldG,
+                              bool store, bool obj, const double* fx, const double* fy, double alpha,
+                              double* objout_dev) {
+  if (mode == T_EXPLICIT)
+    return grad_pass_gk_mode<K, T_EXPLICIT>(c, P, S2, G, ldG, store, obj, fx, fy, alpha, objout_dev);
+  if (mode == T_GIBBS) return grad_pass_gk_mode<K, T_GIBBS>(c, P, S2, G, ldG, store, obj, fx, fy, alpha, objout_dev);
+  return grad_pass_gk_mode<K, T_PRODUCT>(c, P, S2, G, ldG, store, obj, fx, fy, alpha, objout_dev);
+}
+
 static gw_status grad_pass(gw_ctx* c, const Prepared& P, int mode, const TSrc& S, const TSrc2& S2, float* G,
                            int64_t ldG, bool store, bool obj, const double* fx, const double* fy, double alpha,
                            double* objout_dev) {
   if (P.grid2d) return grad_pass_2d(c, P, mode, S2, G, ldG, store, obj, fx, fy, alpha, objout_dev);
   if (P.k == 1) return grad_pass_k1(c, P, mode, S, S2, G, ldG, store, obj, fx, fy, alpha, objout_dev);
+  if (P.k >= 3) {
+    if (P.nl == 0) return GW_OK;
+    if (obj)  // violation, entropy and <C o C, T> from the k = 1 objective machinery; E(T) below
+      TRY(grad_pass_k1(c, P, mode, S, S2, nullptr, 0, false, true, fx, fy, alpha, objout_dev));
+    switch (P.k) {
+      case 3: return grad_pass_gk<3>(c, P, mode, S2, G, ldG, store, obj, fx, fy, alpha, objout_dev);
+      case 4: return grad_pass_gk<4>(c, P, mode, S2, G, ldG, store, obj, fx, fy, alpha, objout_dev);
+      default: return grad_pass_gk<5>(c, P, mode, S2, G, ldG, store, obj, fx, fy, alpha, objout_dev);
+    }
+  }
   const int64_t nl = P.nl, m = P.m;
   if (obj) {
     // violation, entropy and <C o C, T> do not depend on k: the k = 1 objective machinery supplies
@@ -906,10 +1002,10 @@ static gw_status grad_pass(gw_ctx* c, const Prepared& P, int mode, const TSrc& S
       k_scale_f<<<grid_for(nl), 256, 0, c->stream>>>(fx + P.row0, nl, sqrt(1.0 - alpha), fxs);
       k_scale_f<<<grid_for(m), 256, 0, c->stream>>>(fy, m, sqrt(1.0 - alpha), fys);
       KCHECK();
-      k_poly_store<true><<<grid_for(nl * ((m + 3) / 4), 256, 148 * 16), 256, 0, c->stream>>>(
+      k_poly_store<true><<<dim3((unsigned)((m + 1023) / 1024), (unsigned)((nl + PSR - 1) / PSR)), 256, 0, c->stream>>>(
           coef, c2s, P.yf, fxs, fys, nl, m, G, ldG);
     } else {
-      k_poly_store<false><<<grid_for(nl * ((m + 3) / 4), 256, 148 * 16), 256, 0, c->stream>>>(
+      k_poly_store<false><<<dim3((unsigned)((m + 1023) / 1024), (unsigned)((nl + PSR - 1) / PSR)), 256, 0, c->stream>>>(
           coef, c2s, P.yf, nullptr, nullptr, nl, m, G, ldG);
     }
     KCHECK();

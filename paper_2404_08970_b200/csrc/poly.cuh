@@ -19,7 +19,7 @@ namespace gw {
 
 constexpr int PM = 5;            // powers 0..4
 constexpr int PNM = PM * PM;     // moments per reduction
-constexpr int PRPW = 64;         // rows per warp
+constexpr int PRPW = 8;          // rows per warp (>= 7 CTAs per SM at N = 65536)
 constexpr int PT = 256;          // threads per CTA (8 warps) -> 512 rows per CTA
 
 __device__ __forceinline__ float p_regen(int MODE, const TSrc2& S, float g, float Fh, float Fl, int64_t q) {
@@ -51,18 +51,30 @@ __global__ void __launch_bounds__(PT) k_poly_moments(TSrc2 S, int64_t nl, int64_
     const float* row = S.T + j * S.ld;
     for (int64_t c0 = 4 * (int64_t)lane; c0 < m; c0 += 32 * 4 * 64) {
       float s32[PM + 1] = {0, 0, 0, 0, 0, 0};
-#pragma unroll 4
+#pragma unroll 8
       for (int u = 0; u < 64; ++u) {
         const int64_t q = c0 + 128 * u;
-        if (q >= m) break;
-        float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (MODE != T_PRODUCT) g = __ldcs(reinterpret_cast<const float4*>(row + q));
+        const bool full = q + 3 < m;
+        float4 g = make_float4(0.f, 0.f, 0.f, 0.f), y4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (full) {
+          if (MODE != T_PRODUCT) g = __ldcs(reinterpret_cast<const float4*>(row + q));
+          y4 = *reinterpret_cast<const float4*>(yf + q);
+        } else if (q < m) {
+          float gt[4] = {0.f, 0.f, 0.f, 0.f}, yt[4] = {0.f, 0.f, 0.f, 0.f};
+          for (int e = 0; e < 4 && q + e < m; ++e) {
+            if (MODE != T_PRODUCT) gt[e] = row[q + e];
+            yt[e] = yf[q + e];
+          }
+          g = make_float4(gt[0], gt[1], gt[2], gt[3]);
+          y4 = make_float4(yt[0], yt[1], yt[2], yt[3]);
+        }
         const float gv[4] = {g.x, g.y, g.z, g.w};
+        const float yv[4] = {y4.x, y4.y, y4.z, y4.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           if (q + e < m) {
             const float t = p_regen(MODE, S, gv[e], Fh, Fl, q + e);
-            const float y = yf[q + e];
+            const float y = yv[e];
             float yp = t;
             s32[0] += yp;
             yp *= y; s32[1] += yp;
@@ -134,31 +146,42 @@ __global__ void k_poly_rowcoef(const double* __restrict__ M, const double* __res
   }
 }
 
-// G_ip = A_i + 2 alpha c'_p + y_p (B_i + C_i y_p) [+ (1 - alpha)(fx_i - fy_p)^2], float4 stores.
+// G_ip = A_i + 2 alpha c'_p + y_p (B_i + C_i y_p) [+ (1 - alpha)(fx_i - fy_p)^2]: a CTA covers 1024
+// columns x PSR rows; each thread keeps its 4 columns' y, c' (and fy) in registers across the rows
+// and writes float4s (ld % 4 == 0); the row coefficients are broadcast loads.
+constexpr int PSR = 64;
 template <bool FGW>
-__global__ void k_poly_store(const float4* __restrict__ coef, const float* __restrict__ c2s,
-                             const float* __restrict__ yf, const float* __restrict__ fxs, const float* __restrict__ fys,
-                             int64_t nl, int64_t m, float* __restrict__ G, int64_t ldG) {
-  const int64_t m4 = (m + 3) / 4;
-  const int64_t total = nl * m4;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e / m4, q = 4 * (e - i * m4);
+__global__ void __launch_bounds__(256) k_poly_store(const float4* __restrict__ coef, const float* __restrict__ c2s,
+                                                    const float* __restrict__ yf, const float* __restrict__ fxs,
+                                                    const float* __restrict__ fys, int64_t nl, int64_t m,
+                                                    float* __restrict__ G, int64_t ldG) {
+  const int64_t q = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+  if (q >= m) return;
+  float y[4], c2[4], fy[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int64_t qq = min(q + k, m - 1);
+    y[k] = yf[qq];
+    c2[k] = c2s[qq];
+    fy[k] = FGW ? fys[qq] : 0.f;
+  }
+  const int64_t i0 = (int64_t)blockIdx.y * PSR, i1 = min(nl, i0 + PSR);
+  for (int64_t i = i0; i < i1; ++i) {
     const float4 cf = coef[i];
+    const float fxi = FGW ? fxs[i] : 0.f;
     float o[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const int64_t qq = min(q + k, m - 1);
-      const float y = yf[qq];
-      float v = cf.x + c2s[qq] + y * fmaf(cf.z, y, cf.y);
+      float v = cf.x + c2[k] + y[k] * fmaf(cf.z, y[k], cf.y);
       if (FGW) {
-        const float d = fxs[i] - fys[qq];
+        const float d = fxi - fy[k];
         v = fmaf(d, d, v);
       }
       o[k] = v;
     }
     float* dst = G + i * ldG + q;
     if (q + 3 < m) {
-      *reinterpret_cast<float4*>(dst) = make_float4(o[0], o[1], o[2], o[3]);
+      __stcs(reinterpret_cast<float4*>(dst), make_float4(o[0], o[1], o[2], o[3]));
     } else {
       for (int k = 0; k < 4 && q + k < m; ++k) dst[k] = o[k];
     }

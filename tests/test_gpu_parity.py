@@ -378,12 +378,61 @@ def test_fgw_k2(gw):
     assert abs(r.gw_objective - ro["gw_objective"]) <= OBJ_TOL * abs(ro["gw_objective"])
 
 
-def test_k3_unsupported(gw):
+# ----------------------------------------------------------------------------- distance powers k = 3..5 (f2)
+
+@pytest.mark.parametrize("k", [3, 4, 5])
+@pytest.mark.parametrize("n,m", [(1, 1), (1, 9), (7, 1), (128, 128), (129, 257), (300, 517), (1000, 777)])
+def test_grad_kgen_random_plan(gw, k, n, m):
+    """gw_grad_dp at k = 3..5 (D = |x - x'|^k) vs grad_prescribed(k):
+    tiles of 128 with ragged tails, ties, non-uniform marginals."""
+    rng = np.random.default_rng(13 * n + m + k)
+    x, y = np.sort(rng.random(n)), np.sort(rng.random(m))
+    if n > 10:
+        x[5] = x[4]
+    p, q = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))
+    T = (rng.exponential(size=(n, m)) / (n * m)).astype(np.float32)
+    G = gw.grad(x, y, p, q, _to_dev(gw, T), k=k).cpu().numpy().astype(np.float64)
+    Go = O.grad_prescribed(x, y, p, q, T.astype(np.float64), k=k)
+    assert _grad_err(G, Go) <= GRAD_TOL
+
+
+def test_grad_k3_c3_recipe_2048(gw):
+    """k = 3 on the C3 recipe (Exp(1) plan rescaled to uniform marginals), wide supports."""
+    P = W.config3(2048)
+    T = P.extra["T"]
+    x, y = 10.0 * P.x - 3.0, 4.0 * P.y + 1.0
+    G = gw.grad(x, y, P.p, P.q, _to_dev(gw, T), k=3).cpu().numpy().astype(np.float64)
+    Go = O.grad_prescribed(x, y, P.p, P.q, T.astype(np.float64), k=3)
+    assert _grad_err(G, Go) <= GRAD_TOL
+
+
+@pytest.mark.parametrize("k", [3, 4])
+def test_solver_kgen_trajectory(gw, k):
+    """Entropic GW at k = 3, 4 on C5's distributions (reduced): objective trajectory vs the oracle."""
+    P = _c5_small(400, 300, 5, 100)
+    r = gw.solve(P.x, P.y, P.p, P.q, P.eps, P.outer, P.inner, trace_objective=True, device=_dev(), k=k)
+    ro = O.entropic_gw(P.x, P.y, P.p, P.q, P.eps, P.outer, P.inner, k=k)
+    E = np.asarray(ro["E"])
+    assert np.max(np.abs(r.trace[:, 0] - E) / np.abs(E)) <= OBJ_TOL
+    assert abs(r.gw_objective - ro["gw_objective"]) <= OBJ_TOL * abs(ro["gw_objective"])
+    assert abs(r.entropic_objective - ro["entropic_objective"]) <= OBJ_TOL * abs(ro["entropic_objective"])
+    assert r.marginal_violation <= max(VIOL_TOL, 2 * ro["viol"][-1])
+
+
+def test_fgw_k3(gw):
+    P = _c5_small(300, 256, 4, 60)
+    r = gw.solve(P.x, P.y, P.p, P.q, P.eps, P.outer, P.inner, fx=P.fx, fy=P.fy, alpha=0.5, device=_dev(), k=3)
+    ro = O.entropic_fgw(P.x, P.y, P.p, P.q, P.fx, P.fy, 0.5, P.eps, P.outer, P.inner, k=3)
+    assert abs(r.gw_objective - ro["gw_objective"]) <= OBJ_TOL * abs(ro["gw_objective"])
+
+
+def test_k6_unsupported(gw):
     from paper_2404_08970_b200 import GwError
     rng = np.random.default_rng(0)
     x = np.sort(rng.random(16))
     p = np.full(16, 1 / 16)
     T = _to_dev(gw, np.full((16, 16), 1 / 256, dtype=np.float32))
-    with pytest.raises(GwError) as e:
-        gw.grad(x, x, p, p, T, k=3)
-    assert e.value.code == "GW_ERR_UNSUPPORTED"
+    for k in (0, 6):
+        with pytest.raises(GwError) as e:
+            gw.grad(x, x, p, p, T, k=k)
+        assert e.value.code == "GW_ERR_UNSUPPORTED"

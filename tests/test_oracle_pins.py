@@ -86,7 +86,7 @@ def test_sinkhorn_worked_example():
 # --------------------------------------------------------------------------- DP vs dense
 
 @pytest.mark.parametrize("n", [1, 2, 3, 7, 64])
-@pytest.mark.parametrize("k", [1, 2, 3])
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
 def test_dp_distance_matches_dense(n, k):
     """the recursion equals the dense product (<= 1e-12 rel)."""
     rng = np.random.default_rng(n * 10 + k)
@@ -117,7 +117,7 @@ def test_dp_integer_grid_is_paper_recursion():
 def test_triple_product_dp_matches_dense():
     """Paper's exactness claim in fp64: <= 1e-12."""
     rng = np.random.default_rng(3)
-    for (n, m, k) in [(12, 9, 1), (40, 33, 1), (17, 23, 2)]:
+    for (n, m, k) in [(12, 9, 1), (40, 33, 1), (17, 23, 2), (21, 14, 3), (9, 16, 5)]:
         x, y = _sorted(rng, n), _sorted(rng, m)
         T = rng.random((n, m))
         dense = O.triple_product_dense(x, y, T, k)
