@@ -136,31 +136,45 @@ __global__ void __launch_bounds__(G2D_MAXN) k_g2_rowred(TSrc2 S, int ny, double*
   const float* row = (MODE == T_PRODUCT) ? nullptr : S.T + i * S.ld;
   float rd = 0.f, ent = 0.f, cc = 0.f;
   const float fxi = (OBJ && fx) ? (float)fx[i] : 0.f;
-  for (int c = 0; c < ny; ++c) {
-    float t = 0.f;
-    if (dv) {
-      const int64_t q = (int64_t)c * ny + d;
-      if (MODE == T_EXPLICIT) {
-        t = row[q];
-      } else if (MODE == T_PRODUCT) {
-        t = Fh * S.gh[q];
-      } else {
-        const float g = row[q];
-        const float a = (fmaf(g, -S.ch, S.gh[q]) + Fh) + fmaf(g, -S.cl, S.gl[q] + Fl);
-        t = ex2_ftz(a);
-        if (OBJ && t > 0.f) ent += t * fmaf(a, 0.6931471805599453f, -1.f);
-      }
-      if (OBJ && MODE != T_GIBBS && t > 0.f) ent += t * (__logf(t) - 1.f);
-      if (OBJ && fx) {
-        const float df = fxi - (float)fy[q];
-        cc = fmaf(df * df, t, cc);
-      }
-    }
-    rd += t;
-    float v = t;
+  float gq = 0.f, glq = 0.f;  // (column duals are per q: loaded per element below)
+  constexpr int U = 8;        // loads of U columns c in flight per thread
+  for (int c0 = 0; c0 < ny; c0 += U) {
+    float raw[U];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) wp[c][w] = v;
+    for (int u = 0; u < U; ++u) {
+      const int c = c0 + u;
+      raw[u] = (dv && c < ny && MODE != T_PRODUCT) ? row[(int64_t)c * ny + d] : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int c = c0 + u;
+      if (c >= ny) break;  // uniform across the CTA
+      float t = 0.f;
+      if (dv) {
+        const int64_t q = (int64_t)c * ny + d;
+        if (MODE == T_EXPLICIT) {
+          t = raw[u];
+        } else if (MODE == T_PRODUCT) {
+          t = Fh * S.gh[q];
+        } else {
+          gq = S.gh[q];
+          glq = S.gl[q];
+          const float a = (fmaf(raw[u], -S.ch, gq) + Fh) + fmaf(raw[u], -S.cl, glq + Fl);
+          t = ex2_ftz(a);
+          if (OBJ && t > 0.f) ent += t * fmaf(a, 0.6931471805599453f, -1.f);
+        }
+        if (OBJ && MODE != T_GIBBS && t > 0.f) ent += t * (__logf(t) - 1.f);
+        if (OBJ && fx) {
+          const float df = fxi - (float)fy[q];
+          cc = fmaf(df * df, t, cc);
+        }
+      }
+      rd += t;
+      float v = t;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) wp[c][w] = v;
+    }
   }
   __syncthreads();
   const int nw = (blockDim.x + 31) / 32;
@@ -208,36 +222,75 @@ __global__ void k_g2_marg(const double* __restrict__ RC, const double* __restric
 }
 
 // G[i][q] = alpha (2 c_i + 2 c'_q - 4 (VAC[a][c] + VAD[a][d] + VBC[b][c] + VBD[b][d])) [+ (1-alpha)(fx_i - fy_q)^2]
-// One CTA per row; the row's two ny-vectors are staged in shared memory.  The terms are O(1) and
-// cancel (G near its minimum is much smaller than c_i), so each element is summed in fp64 and
-// rounded to fp32 once (the FP64 adds are well under the store's HBM time).
+// A CTA covers 2048 columns (8 per thread at stride 256: coalesced stores, and the per-row vector
+// reads rd[d] hit consecutive shared-memory words) x G2SR rows; each thread keeps its
+// columns' c'_q (and fy_q) in registers across the rows.  Per row the CTA forms the row's two
+// ny-vectors in shared memory (double-buffered), the next row's V entries already in flight
+// (loaded one row ahead into registers).  The terms are O(1) and cancel (G near its minimum is much
+// smaller than c_i), so each element is summed in fp64 and rounded to fp32 once.
+constexpr int G2SR = 32;
+constexpr int G2SC = 8;  // columns per thread
 template <bool FGW>
 __global__ void __launch_bounds__(256) k_g2_store(const double* __restrict__ cX, const double* __restrict__ cY,
                                                   const double* __restrict__ VAC, const double* __restrict__ VAD,
                                                   const double* __restrict__ VBC, const double* __restrict__ VBD,
-                                                  int nx, int ny, int64_t row0, int64_t m, double alpha,
+                                                  int nx, int ny, int64_t row0, int64_t nl, int64_t m, double alpha,
                                                   const double* __restrict__ fx, const double* __restrict__ fy,
                                                   float* __restrict__ G, int64_t ldG) {
-  __shared__ double rc[G2D_MAXN], rd[G2D_MAXN];
-  const int64_t il = blockIdx.x, i = row0 + il;
-  const int a = (int)(i / nx), b = (int)(i - (int64_t)a * nx);
-  const double ci = 2.0 * alpha * cX[i];
-  for (int k = threadIdx.x; k < ny; k += blockDim.x) {
-    rc[k] = ci - 4.0 * alpha * (VAC[(int64_t)a * ny + k] + VBC[(int64_t)b * ny + k]);
-    rd[k] = -4.0 * alpha * (VAD[(int64_t)a * ny + k] + VBD[(int64_t)b * ny + k]);
+  __shared__ double rc[2][G2D_MAXN], rd[2][G2D_MAXN];
+  const int t = threadIdx.x;
+  const int64_t qb = (int64_t)G2SC * blockIdx.x * blockDim.x + t;  // columns qb + 256 k
+  const bool act = qb < m;
+  const double a2 = 2.0 * alpha, a1 = 1.0 - alpha, a4 = -4.0 * alpha;
+  double cy[G2SC], fyv[G2SC];
+  int cc[G2SC], dd[G2SC];
+#pragma unroll
+  for (int k = 0; k < G2SC; ++k) {
+    const int64_t q = act ? min(qb + 256 * k, m - 1) : 0;
+    cc[k] = (int)(q / ny);
+    dd[k] = (int)(q - (int64_t)cc[k] * ny);
+    cy[k] = a2 * cY[q];
+    fyv[k] = FGW ? fy[q] : 0.0;
   }
-  __syncthreads();
-  const double fxi = FGW ? fx[i] : 0.0;
-  const double a2 = 2.0 * alpha, a1 = 1.0 - alpha;
-  float* gr = G + il * ldG;
-  for (int64_t q = threadIdx.x; q < m; q += blockDim.x) {
-    const int c = (int)(q / ny), d = (int)(q - (int64_t)c * ny);
-    double v = rc[c] + rd[d] + a2 * cY[q];
-    if (FGW) {
-      const double df = fxi - fy[q];
-      v = fma(a1 * df, df, v);
+  const int64_t il0 = (int64_t)blockIdx.y * G2SR, il1 = min(nl, il0 + G2SR);
+  const bool vt = t < ny;  // this thread forms entry t of the row's two vectors
+  double vac = 0, vbc = 0, vad = 0, vbd = 0, cxi = 0;
+  auto fetch = [&](int64_t il) {
+    const int64_t i = row0 + il;
+    const int a = (int)(i / nx), b = (int)(i - (int64_t)a * nx);
+    if (vt) {
+      vac = VAC[(int64_t)a * ny + t]; vbc = VBC[(int64_t)b * ny + t];
+      vad = VAD[(int64_t)a * ny + t]; vbd = VBD[(int64_t)b * ny + t];
+      cxi = cX[i];
     }
-    gr[q] = (float)v;
+  };
+  if (il0 < il1) fetch(il0);
+  for (int64_t il = il0; il < il1; ++il) {
+    const int buf = (int)(il & 1);
+    if (vt) {
+      rc[buf][t] = fma(a4, vac + vbc, a2 * cxi);
+      rd[buf][t] = a4 * (vad + vbd);
+    }
+    if (il + 1 < il1) fetch(il + 1);  // in flight during this row's stores
+    __syncthreads();                  // (double buffer: the next row writes the other half)
+    if (act) {
+      const int64_t i = row0 + il;
+      const double fxi = FGW ? fx[i] : 0.0;
+      float o[G2SC];
+#pragma unroll
+      for (int k = 0; k < G2SC; ++k) {
+        double v = rc[buf][cc[k]] + rd[buf][dd[k]] + cy[k];
+        if (FGW) {
+          const double d = fxi - fyv[k];
+          v = fma(a1 * d, d, v);
+        }
+        o[k] = (float)v;
+      }
+      float* dst = G + il * ldG + qb;
+#pragma unroll
+      for (int k = 0; k < G2SC; ++k)
+        if (qb + 256 * k < m) __stcs(dst + 256 * k, o[k]);
+    }
   }
 }
 

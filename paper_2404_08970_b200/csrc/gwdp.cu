@@ -872,10 +872,11 @@ static gw_status grad_pass_2d(gw_ctx* c, const Prepared& P, int mode, const TSrc
   }
   if (store) {
     PROF_BEGIN(c, PC_GRAD_MAIN);
-    if (fx) k_g2_store<true><<<(unsigned)n, 256, 0, c->stream>>>(P.cx, P.cy, VT, VT + nn, VT + 2 * nn, VT + 3 * nn, nx,
-                                                                 ny, 0, m, alpha, fx, fy, G, ldG);
-    else k_g2_store<false><<<(unsigned)n, 256, 0, c->stream>>>(P.cx, P.cy, VT, VT + nn, VT + 2 * nn, VT + 3 * nn, nx,
-                                                               ny, 0, m, alpha, nullptr, nullptr, G, ldG);
+    const dim3 sg((unsigned)((m + 256 * G2SC - 1) / (256 * G2SC)), (unsigned)((n + G2SR - 1) / G2SR));
+    if (fx) k_g2_store<true><<<sg, 256, 0, c->stream>>>(P.cx, P.cy, VT, VT + nn, VT + 2 * nn, VT + 3 * nn, nx, ny, 0, n,
+                                                       m, alpha, fx, fy, G, ldG);
+    else k_g2_store<false><<<sg, 256, 0, c->stream>>>(P.cx, P.cy, VT, VT + nn, VT + 2 * nn, VT + 3 * nn, nx, ny, 0, n,
+                                                     m, alpha, nullptr, nullptr, G, ldG);
     KCHECK();
     PROF_END(c, PC_GRAD_MAIN, 1);
   }
