@@ -63,7 +63,7 @@ typedef enum {
   GW_ERR_NOT_NORMALIZED = 5,  /* |sum - 1| > 1e-9                        */
   GW_ERR_NONFINITE = 6,       /* NaN/Inf in inputs or produced          */
   GW_ERR_CONFIG = 7,          /* invalid options                                       */
-  GW_ERR_UNSUPPORTED = 8,     /* k > GW_MAX_K, loss != square, tau != eps, fp64 storage, UGW */
+  GW_ERR_UNSUPPORTED = 8,     /* k > GW_MAX_K, loss != square, tau != eps, fp64 storage, ... */
   GW_ERR_OOM = 9,
   GW_ERR_CUDA = 10,
   GW_ERR_NCCL = 11
@@ -225,9 +225,21 @@ gw_status fgw_solve(gw_ctx *ctx, const gw_problem *prob, const double *fx, const
                     double alpha, const gw_solve_opts *opts, const void *T0, void *T_out,
                     int64_t ldT, double *f, double *g, gw_result *res, double *trace);
 
-/* Unbalanced GW (Remark 3): the paper leaves g(Gamma-hat)
- * undefined, so there is no definition to implement against.
- * Always returns GW_ERR_UNSUPPORTED. */
+/* Entropic unbalanced GW (Remark 3).  The paper fixes the functional and the
+ * per-iteration subproblem  min_{G >= 0} <1/2 grad E(G^) + g(G^), G> + m(G^)(rho KL(G1|u) +
+ * rho KL(G^T 1|v) + eps KL(G|u v))  but leaves g(G^) undefined; this build takes readings
+ * R32-R35: g = rho <log(a/u),a> + rho <log(b/v),b> + eps <log(G^/(uv)),G^>, the
+ * gradient with the REALISED marginals a = G^1, b = G^T1, unbalanced Sinkhorn with
+ * kappa = rho~/(rho~+eps~) (opts->inner.max_iter fixed iterations; tol must be 0), G^0 = u v and
+ * the mass rescaling sqrt(m(G^)/m(G)) after each subproblem.
+ *   rho      > 0 (finite); opts->eps > 0, opts->tau = eps or 0; T0 must be NULL.
+ *   T_out    nullable: the final plan (fp32, ldT).  f, g: the subproblem's final duals in R34's
+ *            convention (G = exp((f + g - C)/eps~) u v before the rescaling).
+ *   res      gw_objective = E(G) (realised marginals), entropic_objective = F_eps(G) (R33),
+ *            marginal_violation = max(|G1 - u|, |G^T1 - v|) (informational: G is unbalanced).
+ *   trace    [outer][4] = {F_eps, E, inner iterations, m(G)} per outer iteration (F_eps, E only
+ *            with GW_SOLVE_TRACE_OBJECTIVE, and always for the last one).
+ * One rank, 1-D supports (k = 1..GW_MAX_K); 2-D grids, sharding or tol > 0 -> GW_ERR_UNSUPPORTED. */
 gw_status ugw_solve(gw_ctx *ctx, const gw_problem *prob, double rho, const gw_solve_opts *opts,
                     const void *T0, void *T_out, int64_t ldT, double *f, double *g,
                     gw_result *res, double *trace);

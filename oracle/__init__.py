@@ -12,8 +12,10 @@ paper's LaTeX source; "SPEC.md:N" a line of the CPU-program spec written from it
 Pins (tests/test_oracle_*.py, ``-m "not gpu"``) tie each function to something
 other than itself: worked examples (tests/golden/), closed forms, brute force,
 invariants and finite differences.  Functions without such a pin would say
-"parity unpinned"; in this package only ``ugw`` (not implemented: the paper
-leaves Remark 3's ``g`` undefined) is unpinned.
+"parity unpinned".  ``ugw`` (Remark 3) follows readings R32-R35 (the paper leaves g(G^)
+undefined): its pieces are pinned (finite differences of the functional,
+direct minimisation of the subproblem, the balanced rho -> infinity limit), the reading itself
+is parity unpinned.
 """
 
 from .gw import (  # noqa: F401
@@ -52,4 +54,14 @@ from .grid2d import (  # noqa: F401
     entropic_fgw_2d,
     objective_2d,
     entropic_gw_2d,
+)
+from .ugw import (  # noqa: F401
+    kl,
+    kl_tensor_sq,
+    ugw_functional,
+    ugw_functional_bruteforce,
+    ugw_cost,
+    unbalanced_sinkhorn,
+    unbalanced_plan,
+    entropic_ugw,
 )

@@ -249,8 +249,25 @@ def solve_host(x, y, p, q, eps, outer, inner, tol=0.0, check_every=10, device=No
     return _result(res, f, g, None, tr[: int(outer)])
 
 
-def ugw_solve(*args, **kwargs):
-    """Unbalanced GW (Remark 3): the paper leaves g(Gamma-hat) undefined -> GW_ERR_UNSUPPORTED."""
-    ctx = Context.get()
+def ugw_solve(x, y, u, v, rho, eps, outer, inner, trace_objective=False, return_plan=False, device=None, ctx=None,
+              k=1):
+    """Entropic unbalanced GW (ugw_solve; Remark 3, readings R32-R35 in DESIGN.md)
+    on device vectors.  Returns a Result: gw_objective = E(T), entropic_objective = F_eps(T),
+    trace [outer, 4] = {F_eps, E, inner iterations, mass}."""
+    dev = torch.device(device) if device is not None else torch.device("cuda")
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    ctx = ctx or Context.get(dev)
+    x, y, u, v = (_vec(t, dev) for t in (x, y, u, v))
+    n, m = u.numel(), v.numel()
+    f = torch.empty(n, dtype=torch.float64, device=dev)
+    g = torch.empty(m, dtype=torch.float64, device=dev)
+    T = plan_buffer(n, m, dev) if return_plan else None
+    pr = _problem(x, y, u, v, k=k)
+    o = _opts(eps, outer, inner, 0.0, 10, trace_objective)
     res = L.gw_result()
-    L.check(ctx.lib.ugw_solve(ctx.h, None, 1.0, None, None, None, 0, None, None, C.byref(res), None))
+    tr = np.zeros((max(int(outer), 1), 4), dtype=np.float64)
+    L.check(ctx.lib.ugw_solve(ctx.h, C.byref(pr), float(rho), C.byref(o), None, _ptr(T),
+                              T.stride(0) if T is not None else 0, _ptr(f), _ptr(g), C.byref(res),
+                              tr.ctypes.data_as(C.c_void_p)))
+    return _result(res, f, g, T, tr[: int(outer)])

@@ -20,6 +20,7 @@
 #include "poly.cuh"
 #include "grid2d.cuh"
 #include "polyk.cuh"
+#include "ugw.cuh"
 #include "sink.cuh"
 #include "vec.cuh"
 
@@ -103,6 +104,7 @@ struct gw_ctx {
   Buf pnf, qnf;  // fp32 marginals
   Buf yfb, pcoef, pc2s, pfx, pfy, ppart, pM;  // k = 2 path
   Buf gkrp, gkrt, gkcp, gkz, gkct, gkctt, gkobj;  // k >= 3 path
+  Buf uga, ugb, ugct, ugpart, ugca, ugcb, ugfr, uggr, ugsc;  // UGW
   Buf g2rc, g2rd, g2h, g2cc, g2tt, g2vt, g2tmp, g2s, g2a, g2b, g2ca, g2cb, g2part;  // 2-D grids
   Buf xtab, xg1, xg2, xin, xvec, xtail, xpart;  // multi-rank exchange buffers
   Buf slse, slseg, scsl, scsg, sviolg;          // Sinkhorn column-sum exchange
@@ -117,6 +119,7 @@ struct gw_ctx {
                 &pnf, &qnf, &xtab, &xg1, &xg2, &xin, &xvec, &xtail, &xpart, &slse, &slseg, &scsl, &scsg,
                 &sviolg, &sflag, &sflagg, &yfb, &pcoef, &pc2s, &pfx, &pfy, &ppart, &pM,
                 &gkrp, &gkrt, &gkcp, &gkz, &gkct, &gkctt, &gkobj,
+                &uga, &ugb, &ugct, &ugpart, &ugca, &ugcb, &ugfr, &uggr, &ugsc,
                 &g2rc, &g2rd, &g2h, &g2cc, &g2tt, &g2vt, &g2tmp, &g2s, &g2a, &g2b, &g2ca, &g2cb, &g2part};
     for (Buf* x : b) all.push_back(x);
   }
@@ -1619,8 +1622,255 @@ extern "C" gw_status fgw_solve(gw_ctx* c, const gw_problem* pb, const double* fx
   return solve_impl(c, pb, o, fx, fy, alpha, T0, T_out, ldT, f, g, res, trace);
 }
 
-extern "C" gw_status ugw_solve(gw_ctx*, const gw_problem*, double, const gw_solve_opts*, const void*, void*, int64_t,
-                               double*, double*, gw_result*, double*) {
-  return fail(GW_ERR_UNSUPPORTED,
-              "ugw_solve: Remark 3 (PAPER.md:148-167) leaves g(Gamma-hat) undefined; no definition to implement");
+// ------------------------------------------------------------------------------ UGW (f4)
+// (D o D) w for the 1-D power-k distance: the even power 2k by moments (polyk.cuh)
+static gw_status dd_const(gw_ctx* c, int k, const double* s, const double* w, int64_t n, double* out) {
+  switch (k) {
+    case 1: k_gk_const<2><<<1, 1024, 0, c->stream>>>(s, w, n, out); break;
+    case 2: k_gk_const<4><<<1, 1024, 0, c->stream>>>(s, w, n, out); break;
+    case 3: k_gk_const<6><<<1, 1024, 0, c->stream>>>(s, w, n, out); break;
+    case 4: k_gk_const<8><<<1, 1024, 0, c->stream>>>(s, w, n, out); break;
+    default: k_gk_const<10><<<1, 1024, 0, c->stream>>>(s, w, n, out); break;
+  }
+  KCHECK();
+  return GW_OK;
+}
+
+struct UgwStats {
+  double mass, A1, B1, KL;  // m(T), <a, log(a/u)>, <b, log(b/v)>, <T, log(T/(u v))>
+};
+
+// Statistics of the implicit plan T = 2^(((f' + g' - C) log2e / eps_t)) (absorbed duals in s):
+// a = T 1, b = T^T 1 (device, into a_out / b_out) and the scalars (host).
+static gw_status ugw_stats(gw_ctx* c, const Prepared& P, SinkState& s, const float* C, int64_t ldC, double eps_t,
+                           double* a_out, double* b_out, UgwStats* st) {
+  const int64_t nl = P.nl, m = P.m;
+  const double cc = GW_LOG2E / eps_t;
+  const float ch = (float)cc;
+  const TSrc2 S2{C, ldC, s.fh, s.fl, s.gh, s.gl, ch, (float)(cc - (double)ch)};
+  double *ct, *part, *sc;
+  TRY(ws(c, c->ugct, (size_t)std::max<int64_t>(nl, 1), &ct));
+  const int nch = (int)((nl + 255) / 256);
+  TRY(ws(c, c->ugpart, (size_t)std::max(nch, 1) * m, &part));
+  TRY(ws(c, c->ugsc, 8, &sc));
+  k_ugw_rowstats<<<(unsigned)((nl + 8 * URPW - 1) / (8 * URPW)), 256, 0, c->stream>>>(S2, nl, m, a_out, ct);
+  KCHECK();
+  k_g2_colsum<T_GIBBS><<<dim3((unsigned)((m + 255) / 256), (unsigned)nch), 256, 0, c->stream>>>(S2, nl, m, part);
+  KCHECK();
+  k_g2_colsum_reduce<<<grid_for(m), 256, 0, c->stream>>>(part, nch, m, b_out);
+  KCHECK();
+  k_ugw_scalars<<<1, 1024, 0, c->stream>>>(a_out, P.lp, s.f, ct, nl, b_out, P.lq, s.g, m, sc);
+  KCHECK();
+  CU(cudaMemcpyAsync(c->hpin + 48, sc, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  const double* h = c->hpin + 48;
+  st->mass = h[0];
+  st->A1 = h[1];
+  st->B1 = h[2];
+  st->KL = (h[3] + h[4] - h[5]) / eps_t - h[6] - h[7];
+  return GW_OK;
+}
+
+// F_eps (reading R33) from E and the plan statistics (m(u) = m(v) = 1)
+static double ugw_F(double E, const UgwStats& st, double rho, double eps) {
+  const double mm = st.mass;
+  return E + rho * (2.0 * mm * st.A1 - mm * mm + 1.0) + rho * (2.0 * mm * st.B1 - mm * mm + 1.0) +
+         eps * (2.0 * mm * st.KL - mm * mm + 1.0);
+}
+
+// Entropic UGW (Remark 3) with readings R32-R35: per outer iteration
+//   C = grad E(T^) [realised marginals] + 2 g(T^)   (twice the paper's 1/2 grad E + g: the same
+//       subproblem at 2 m(T^) eps and 2 m(T^) rho)
+//   unbalanced Sinkhorn (kappa = rho / (rho + eps)) on C with warm-started duals, safe path
+//   T^ <- sqrt(m(T^) / m(T)) T.
+static gw_status ugw_impl(gw_ctx* c, const gw_problem* pb, double rho, const gw_solve_opts* o, const void* T0,
+                          void* T_out, int64_t ldT, double* f, double* g, gw_result* res, double* trace) {
+  if (!c || !o || !res) return fail(GW_ERR_INVALID_ARG, "null ctx, opts or result");
+  if (!(o->eps > 0)) return fail(GW_ERR_CONFIG, "eps must be > 0");
+  if (!(rho > 0) || !std::isfinite(rho)) return fail(GW_ERR_CONFIG, "ugw_solve: rho must be finite and > 0");
+  if (o->tau != o->eps && o->tau != 0) return fail(GW_ERR_UNSUPPORTED, "tau != eps is not implemented (R6)");
+  if (o->outer_iters < 0 || o->inner.max_iter < 0) return fail(GW_ERR_CONFIG, "iteration counts must be >= 0");
+  if (!f || !g) return fail(GW_ERR_INVALID_ARG, "f and g (outputs) must be non-null");
+  if (T0) return fail(GW_ERR_UNSUPPORTED, "ugw_solve: the iteration starts from u v (R35); T0 must be null");
+  if (o->inner.tol > 0) return fail(GW_ERR_UNSUPPORTED, "ugw_solve: fixed inner iteration counts only");
+  TRY(check_problem(pb));
+  if (pb->flags & GW_GRID2D) return fail(GW_ERR_UNSUPPORTED, "ugw_solve: 2-D grids are not implemented");
+  if (T_out) TRY(check_matrix(T_out, ldT, pb->m, "T_out"));
+  CU(cudaSetDevice(c->device));
+  const double eps = o->eps;
+  Prepared P;
+  TRY(prepare(c, pb, P));
+  if (P.R > 1) return fail(GW_ERR_UNSUPPORTED, "ugw_solve: row sharding is not implemented");
+  const int64_t nl = P.nl, m = P.m;
+  const int64_t ldG = (m + 31) & ~int64_t(31);
+  float* G;
+  TRY(ws(c, c->Gs, (size_t)std::max<int64_t>(nl, 1) * ldG, &G));
+  SinkState s;
+  TRY(sink_alloc(c, P, s));
+  if (pb->flags & GW_HOST_VECTORS) {
+    TRY(stage_duals_in(c, pb, P, nullptr, nullptr, &s.f, &s.g));
+  } else {
+    s.f = f;
+    s.g = g;
+  }
+  double *av, *bv, *ca, *cb, *fr, *gr, *Fs, *Gs2, *objout;
+  TRY(ws(c, c->uga, (size_t)std::max<int64_t>(nl, 1), &av)); TRY(ws(c, c->ugb, (size_t)m, &bv));
+  TRY(ws(c, c->ugca, (size_t)std::max<int64_t>(nl, 1), &ca)); TRY(ws(c, c->ugcb, (size_t)m, &cb));
+  TRY(ws(c, c->ugfr, (size_t)std::max<int64_t>(nl, 1), &fr)); TRY(ws(c, c->uggr, (size_t)m, &gr));
+  TRY(ws(c, c->fsc, (size_t)std::max<int64_t>(nl, 1), &Fs)); TRY(ws(c, c->gsc, (size_t)m, &Gs2));
+  TRY(ws(c, c->objout, 16, &objout));
+  k_fill<<<grid_for(nl), 256, 0, c->stream>>>(fr, nl, 0.0);
+  k_fill<<<grid_for(m), 256, 0, c->stream>>>(gr, m, 0.0);
+  KCHECK();
+  const bool want_trace_obj = (o->flags & GW_SOLVE_TRACE_OBJECTIVE) != 0;
+  std::vector<double> tr((size_t)std::max(o->outer_iters, 1) * 4, NAN);
+  cudaEvent_t ev0, ev1;
+  CU(cudaEventCreate(&ev0)); CU(cudaEventCreate(&ev1));
+  CU(cudaEventRecord(ev0, c->stream));
+  const unsigned cgrid = (unsigned)std::min<int64_t>(((m + 1023) / 1024) * s.nrb, 148 * 4);
+  const unsigned rgrid = (unsigned)std::min<int64_t>((nl + RROWS - 1) / RROWS, 148 * 4);
+  // T^0 = u v (R35): a = u, b = v, m = 1, every log ratio 0
+  UgwStats st{1.0, 0.0, 0.0, 0.0};
+  double eps_reg = 0.0;  // regulariser of the current implicit plan (l > 0)
+  int inner_total = 0;
+  // E of the current plan (objective pass on the Gibbs form, realised marginals)
+  auto plan_E = [&](double* Eout, double* violout) -> gw_status {
+    const double cc = GW_LOG2E / eps_reg;
+    const float ch = (float)cc;
+    k_scale<<<grid_for(nl), 256, 0, c->stream>>>(s.f, nl, cc, Fs);
+    k_scale<<<grid_for(m), 256, 0, c->stream>>>(s.g, m, cc, Gs2);
+    KCHECK();
+    const TSrc S{G, ldG, Fs, Gs2, cc};
+    const TSrc2 S2{G, ldG, s.fh, s.fl, s.gh, s.gl, ch, (float)(cc - (double)ch)};
+    TRY(grad_pass(c, P, T_GIBBS, S, S2, nullptr, 0, false, true, nullptr, nullptr, 1.0, objout));
+    CU(cudaMemcpyAsync(c->hpin, objout, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    *Eout = c->hpin[0];
+    if (violout) *violout = c->hpin[1];
+    return GW_OK;
+  };
+  for (int l = 0; l < o->outer_iters; ++l) {
+    // ---- cost C = grad E(T^) (realised a, b) + 2 g(T^) (R32) ----
+    const double gconst = rho * st.A1 + rho * st.B1 + eps * st.KL;
+    const double* aw = (l == 0) ? P.pn : av;
+    const double* bw = (l == 0) ? P.qn : bv;
+    TRY(dd_const(c, P.k, P.xc, aw, nl, ca));
+    TRY(dd_const(c, P.k, P.yc, bw, m, cb));
+    k_ugw_addc<<<grid_for(nl), 256, 0, c->stream>>>(ca, gconst, nl);
+    KCHECK();
+    Prepared P2 = P;
+    P2.cx = ca;
+    P2.cy = cb;
+    int mode;
+    TSrc S;
+    TSrc2 S2;
+    if (l == 0) {
+      mode = T_PRODUCT;
+      S = TSrc{nullptr, 0, P.pn, P.qn, 0.0};
+      S2 = TSrc2{nullptr, 0, P.pnf, nullptr, P.qnf, nullptr, 0.f, 0.f};
+    } else {
+      mode = T_GIBBS;
+      const double cc = GW_LOG2E / eps_reg;
+      const float ch = (float)cc;
+      k_scale<<<grid_for(nl), 256, 0, c->stream>>>(s.f, nl, cc, Fs);
+      k_scale<<<grid_for(m), 256, 0, c->stream>>>(s.g, m, cc, Gs2);
+      KCHECK();
+      S = TSrc{G, ldG, Fs, Gs2, cc};
+      S2 = TSrc2{G, ldG, s.fh, s.fl, s.gh, s.gl, ch, (float)(cc - (double)ch)};
+    }
+    TRY(grad_pass(c, P2, mode, S, S2, G, ldG, true, false, nullptr, nullptr, 1.0, nullptr));
+    // ---- unbalanced Sinkhorn at eps~ = 2 m eps, rho~ = 2 m rho (R34), absorbed duals f' = f + eps~ ln u ----
+    const double eps_t = 2.0 * st.mass * eps, rho_t = 2.0 * st.mass * rho;
+    const double kap = rho_t / (rho_t + eps_t);
+    const float c2f = (float)(GW_LOG2E / eps_t);
+    k_ugw_axpy<<<grid_for(nl), 256, 0, c->stream>>>(fr, P.lp, eps_t, nl, s.f);
+    k_ugw_axpy<<<grid_for(m), 256, 0, c->stream>>>(gr, P.lq, eps_t, m, s.g);
+    KCHECK();
+    TRY(sink_split(c, P, s, eps_t));
+    for (int it = 0; it < o->inner.max_iter; ++it) {
+      k_sink_row<<<rgrid, 256, 0, c->stream>>>(G, ldG, nl, m, s.gh, s.gl, c2f, s.f, s.f, P.lp, eps_t, s.fh, s.fl,
+                                                nullptr, nullptr, nullptr, kap);
+      KCHECK();
+      k_sink_col<<<cgrid, 256, 0, c->stream>>>(G, ldG, nl, m, s.fh, s.fl, c2f, s.RB, s.part, nullptr, nullptr);
+      KCHECK();
+      k_sink_colmerge<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.part, s.nrb, m, s.lse, nullptr, nullptr);
+      KCHECK();
+      k_sink_colfin<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.lse, 1, m, P.lq, eps_t, s.g, s.gh, s.gl,
+                                                                       nullptr, nullptr, nullptr, kap);
+      KCHECK();
+    }
+    inner_total += o->inner.max_iter;
+    // relative duals for the warm start (R34), then the mass rescaling (R35)
+    k_ugw_axpy<<<grid_for(nl), 256, 0, c->stream>>>(s.f, P.lp, -eps_t, nl, fr);
+    k_ugw_axpy<<<grid_for(m), 256, 0, c->stream>>>(s.g, P.lq, -eps_t, m, gr);
+    KCHECK();
+    UgwStats sn;
+    TRY(ugw_stats(c, P, s, G, ldG, eps_t, av, bv, &sn));
+    const double scl = std::sqrt(st.mass / sn.mass), lsc = std::log(scl);
+    k_ugw_addc<<<grid_for(nl), 256, 0, c->stream>>>(s.f, eps_t * lsc, nl);
+    k_scale<<<grid_for(nl), 256, 0, c->stream>>>(av, nl, scl, av);
+    k_scale<<<grid_for(m), 256, 0, c->stream>>>(bv, m, scl, bv);
+    KCHECK();
+    k_split<<<grid_for(nl), 256, 0, c->stream>>>(s.f, nl, GW_LOG2E / eps_t, s.fh, s.fl);
+    KCHECK();
+    st.mass = scl * sn.mass;
+    st.A1 = scl * (sn.A1 + lsc * sn.mass);
+    st.B1 = scl * (sn.B1 + lsc * sn.mass);
+    st.KL = scl * (sn.KL + lsc * sn.mass);
+    eps_reg = eps_t;
+    tr[(size_t)l * 4 + 2] = o->inner.max_iter;
+    tr[(size_t)l * 4 + 3] = st.mass;
+    if (want_trace_obj && l + 1 < o->outer_iters) {
+      double E;
+      TRY(plan_E(&E, nullptr));
+      tr[(size_t)l * 4 + 0] = ugw_F(E, st, rho, eps);
+      tr[(size_t)l * 4 + 1] = E;
+    }
+  }
+  // ---- final plan: E, F, violation (vs u, v; informational) ----
+  double E = 0.0, viol = 0.0;
+  if (o->outer_iters == 0) {
+    const TSrc S{nullptr, 0, P.pn, P.qn, 0.0};
+    const TSrc2 S2{nullptr, 0, P.pnf, nullptr, P.qnf, nullptr, 0.f, 0.f};
+    TRY(grad_pass(c, P, T_PRODUCT, S, S2, nullptr, 0, false, true, nullptr, nullptr, 1.0, objout));
+    CU(cudaMemcpyAsync(c->hpin, objout, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    E = c->hpin[0];
+    viol = c->hpin[1];
+    if (T_out) TRY(materialize(c, P, T_PRODUCT, S, T_out, ldT));
+  } else {
+    TRY(plan_E(&E, &viol));
+    if (T_out) TRY(materialize(c, P, T_GIBBS, TSrc{G, ldG, Fs, Gs2, GW_LOG2E / eps_reg}, T_out, ldT));
+  }
+  const double F = ugw_F(E, st, rho, eps);
+  if (o->outer_iters > 0) {
+    tr[(size_t)(o->outer_iters - 1) * 4 + 0] = F;
+    tr[(size_t)(o->outer_iters - 1) * 4 + 1] = E;
+  }
+  // the returned duals are the subproblem's final ones in R34's convention (relative to u v)
+  CU(cudaMemcpyAsync(s.f, fr, nl * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  CU(cudaMemcpyAsync(s.g, gr, m * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  CU(cudaEventRecord(ev1, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  float ms_total = 0.f;
+  CU(cudaEventElapsedTime(&ms_total, ev0, ev1));
+  cudaEventDestroy(ev0); cudaEventDestroy(ev1);
+  res->gw_objective = E;
+  res->entropic_objective = F;
+  res->marginal_violation = viol;
+  res->outer_iters = o->outer_iters;
+  res->inner_iters_total = inner_total;
+  res->converged = 0;
+  res->inner_fused_total = 0;
+  res->ms_grad = 0.0;
+  res->ms_sinkhorn = 0.0;
+  res->ms_total = ms_total;
+  if (trace) memcpy(trace, tr.data(), sizeof(double) * 4 * (size_t)o->outer_iters);
+  TRY(stage_duals_out(c, pb, P, f, g, s.f, s.g));
+  return GW_OK;
+}
+
+extern "C" gw_status ugw_solve(gw_ctx* c, const gw_problem* pb, double rho, const gw_solve_opts* o, const void* T0,
+                               void* T_out, int64_t ldT, double* f, double* g, gw_result* res, double* trace) {
+  return ugw_impl(c, pb, rho, o, T0, T_out, ldT, f, g, res, trace);
 }

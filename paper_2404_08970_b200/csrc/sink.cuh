@@ -12,7 +12,8 @@
 namespace gw {
 
 // ---------------------------------------------------------------------------------
-// Row half-step (robust "safe" path).  A CTA of 256 threads owns RROWS rows and walks
+// Row half-step (robust "safe" path).  kappa = 1 (balanced); kappa = rho/(rho + eps) gives the
+// unbalanced update of UGW's subproblem (reading R34) in the same absorbed form.  A CTA of 256 threads owns RROWS rows and walks
 // the columns in chunks of 2048 (8 per thread), so each chunk's dual constants gh/gl are
 // loaded once per RROWS rows (L2 traffic 8/RROWS B per element on top of the 4 B of G).
 // Online max-shifted LSE per row in registers.
@@ -28,7 +29,7 @@ __global__ void __launch_bounds__(256) k_sink_row(const float* __restrict__ G, i
                                                   double* __restrict__ fout, const double* __restrict__ lp,
                                                   double eps, float* __restrict__ fh, float* __restrict__ fl,
                                                   float* __restrict__ viol, const int* __restrict__ stop,
-                                                  const int* __restrict__ skip_if_fast) {
+                                                  const int* __restrict__ skip_if_fast, double kappa = 1.0) {
   if (stop && *stop) return;
   if (skip_if_fast && *skip_if_fast) return;  // a skipped launch costs one small wave (grid-stride)
   __shared__ float smm[RROWS][8], sms[RROWS][8];
@@ -90,7 +91,7 @@ __global__ void __launch_bounds__(256) k_sink_row(const float* __restrict__ G, i
     const double l2e_eps = GW_LOG2E / eps;
     const double lse2 = (double)s.m + log2((double)s.s);
     const double fo = fcur[row];
-    const double fn = (lp[row] == -INFINITY) ? -INFINITY : eps * lp[row] - eps * GW_LN2 * lse2;
+    const double fn = (lp[row] == -INFINITY) ? -INFINITY : eps * lp[row] - kappa * (eps * GW_LN2 * lse2);
     fout[row] = fn;
     const double fs = fn * l2e_eps;
     const float h = (float)fs;
@@ -198,7 +199,7 @@ __global__ void k_sink_colmerge(const float2* __restrict__ part, int nrb, int64_
 __global__ void k_sink_colfin(const double* __restrict__ gath, int R, int64_t m, const double* __restrict__ lq,
                               double eps, double* __restrict__ g, float* __restrict__ gh, float* __restrict__ gl,
                               const int* __restrict__ stop, const int* __restrict__ skip_if_fast,
-                              float* __restrict__ dev) {
+                              float* __restrict__ dev, double kappa = 1.0) {
   if (stop && *stop) return;
   if (skip_if_fast && *skip_if_fast) return;
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -212,7 +213,7 @@ __global__ void k_sink_colfin(const double* __restrict__ gath, int R, int64_t m,
       if (Mr != -INFINITY) S += gath[(int64_t)r * 2 * m + m + q] * exp2(Mr - M);
     }
   const double lse2 = M + log2(S);
-  const double gn = (lq[q] == -INFINITY) ? -INFINITY : eps * lq[q] - eps * GW_LN2 * lse2;
+  const double gn = (lq[q] == -INFINITY) ? -INFINITY : eps * lq[q] - kappa * (eps * GW_LN2 * lse2);
   if (dev) {  // |log2(colsum / q)| of the half-step plan: decides the next iteration's path
     double d = fabs((gn - g[q]) * (GW_LOG2E / eps));
     if (!(d == d)) d = 3.0e38;

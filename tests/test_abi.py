@@ -53,11 +53,10 @@ def test_library_is_sm100a(lib):
 
 def test_host_only_entry_points(lib):
     assert lib.gw_abi_version() == 1
-    # ugw is defined as unsupported (PAPER.md:156-165 leaves g undefined); no GPU needed
+    # null-argument validation of ugw_solve happens before any device work
     from paper_2404_08970_b200 import _lib
     st = lib.ugw_solve(None, None, 1.0, None, None, None, 0, None, None, None, None)
-    assert _lib.STATUS[st] == "GW_ERR_UNSUPPORTED"
-    assert b"undefined" in lib.gw_last_error()
+    assert _lib.STATUS[st] == "GW_ERR_INVALID_ARG"
     # null-argument validation happens before any device work
     assert _lib.STATUS[lib.gw_grad_dp(None, None, None, 0, None, 0, None)] == "GW_ERR_INVALID_ARG"
 

@@ -237,11 +237,16 @@ def test_solver_deterministic(gw):
     assert np.array_equal(a.T.cpu().numpy(), b.T.cpu().numpy())
 
 
-def test_ugw_unsupported(gw):
+def test_ugw_argument_errors(gw):
     from paper_2404_08970_b200 import GwError
-    with pytest.raises(GwError) as e:
-        gw.ugw_solve()
-    assert e.value.code == "GW_ERR_UNSUPPORTED"
+    P = W.config1()
+    for kw, code in [({"rho": -1.0}, "GW_ERR_CONFIG"), ({"rho": float("inf")}, "GW_ERR_CONFIG"),
+                     ({"eps": 0.0}, "GW_ERR_CONFIG")]:
+        args = dict(rho=1.0, eps=0.01)
+        args.update(kw)
+        with pytest.raises(GwError) as e:
+            gw.ugw_solve(P.x, P.y, P.p, P.q, args["rho"], args["eps"], 2, 10, device=_dev())
+        assert e.value.code == code
 
 
 # ----------------------------------------------------------------------------- fused path

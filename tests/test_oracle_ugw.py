@@ -1,0 +1,103 @@
+"""Pins for the UGW oracle (oracle/ugw.py; Remark 3; readings R32-R35).
+The paper leaves g(G^) undefined, so the reading is parity unpinned; these tests pin every
+piece of it to something other than itself."""
+
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+
+def _problem(seed, n, m):
+    rng = np.random.default_rng(seed)
+    x, y = np.sort(rng.random(n)), np.sort(rng.random(m))
+    u, v = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))
+    return rng, x, y, u, v
+
+
+def test_kl_tensor_closed_form_is_bruteforce():
+    rng = np.random.default_rng(0)
+    a, b = rng.random(5) * 0.3, rng.random(5) * 0.4
+    assert abs(O.kl_tensor_sq(a, b) - O.kl(np.outer(a, a), np.outer(b, b))) <= 1e-13
+    assert O.kl(b, b) == pytest.approx(0.0, abs=1e-15)
+
+
+def test_functional_closed_form_is_bruteforce():
+    rng, x, y, u, v = _problem(1, 4, 3)
+    G = rng.random((4, 3)) * 0.1
+    for k in (1, 2):
+        a = O.ugw_functional(x, y, u, v, G, 0.7, 0.05, k)
+        b = O.ugw_functional_bruteforce(x, y, u, v, G, 0.7, 0.05, k)
+        assert abs(a - b) <= 1e-12 * max(1.0, abs(b))
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_ugw_cost_is_half_gradient_of_functional(k):
+    """R32: the subproblem's linearised objective L(G) = <C(G^), G> + m(G^) (rho KL(G1|u) +
+    rho KL(G^T1|v) + eps KL(G|uv)) has gradient 1/2 grad F_eps at G = G^ (F_eps brute force,
+    central differences): this fixes g(G^) and the realised-marginal 1/2 grad E."""
+    rng, x, y, u, v = _problem(2 + k, 4, 3)
+    Gh = rng.random((4, 3)) * 0.15 + 0.01
+    rho, eps = 0.8, 0.07
+    C = O.ugw_cost(x, y, u, v, Gh, rho, eps, k)
+    a, b = Gh.sum(1), Gh.sum(0)
+    mh = Gh.sum()
+    gradL = C + mh * (rho * np.log(a / u)[:, None] + rho * np.log(b / v)[None, :] + eps * np.log(Gh / np.outer(u, v)))
+    h = 1e-6
+    for _ in range(3):
+        D = rng.standard_normal(Gh.shape)
+        fp = O.ugw_functional_bruteforce(x, y, u, v, Gh + h * D, rho, eps, k)
+        fm = O.ugw_functional_bruteforce(x, y, u, v, Gh - h * D, rho, eps, k)
+        fd = (fp - fm) / (2 * h)
+        assert abs(fd - 2.0 * np.sum(gradL * D)) <= 1e-6 * max(1.0, abs(fd))
+
+
+def test_unbalanced_sinkhorn_solves_the_primal():
+    """R34: the converged unbalanced Sinkhorn plan minimises <C,G> + eps KL(G|uv) + rho KL(G1|u)
+    + rho KL(G^T1|v) (direct L-BFGS minimisation of the primal over log G, tiny instance)."""
+    from scipy.optimize import minimize
+    rng = np.random.default_rng(7)
+    n, m = 3, 4
+    u, v = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m)) * 1.3
+    C = rng.random((n, m))
+    rho, eps = 0.6, 0.2
+    f, g = O.unbalanced_sinkhorn(C, u, v, rho, eps, 3000)
+    Gs = O.unbalanced_plan(C, u, v, f, g, eps)
+
+    def primal(z):
+        G = np.exp(z.reshape(n, m))
+        a, b = G.sum(1), G.sum(0)
+        val = np.sum(C * G) + eps * O.kl(G, np.outer(u, v)) + rho * O.kl(a, u) + rho * O.kl(b, v)
+        dG = C + eps * np.log(G / np.outer(u, v)) + rho * np.log(a / u)[:, None] + rho * np.log(b / v)[None, :]
+        return val, (dG * G).ravel()
+
+    r = minimize(primal, np.log(np.outer(u, v)).ravel(), jac=True, method="L-BFGS-B",
+                 options={"ftol": 1e-15, "gtol": 1e-13, "maxiter": 10000})
+    Gp = np.exp(r.x.reshape(n, m))
+    np.testing.assert_allclose(Gs, Gp, rtol=2e-5, atol=1e-9)
+    assert primal(np.log(Gs).ravel())[0] <= r.fun + 1e-12
+
+
+def test_ugw_balanced_limit_is_entropic_gw_at_twice_eps():
+    """rho -> infinity: kappa -> 1, the subproblem is balanced entropic OT of 1/2 grad E at eps,
+    i.e. of grad E at 2 eps (constants drop out); with converged inner loops the UGW iteration
+    reproduces oracle.entropic_gw(eps = 2 eps) (R32-R35 at their balanced limit)."""
+    _, x, y, u, v = _problem(11, 7, 6)
+    eps = 0.05
+    ru = O.entropic_ugw(x, y, u, v, 1e9, eps, 4, 3000)
+    rg = O.entropic_gw(x, y, u, v, 2 * eps, 4, 3000)
+    np.testing.assert_allclose(ru["E"], rg["E"], rtol=1e-7)
+    np.testing.assert_allclose(ru["T"], rg["T"], atol=1e-9)
+    assert abs(ru["mass"][-1] - 1.0) <= 1e-7
+
+
+def test_ugw_mass_rescaling_and_symmetry():
+    """R35: after each step m(G) = sqrt(m(G^) m(G_sinkhorn)); swapping the spaces transposes the
+    plan (the functional is symmetric in X, Y)."""
+    _, x, y, u, v = _problem(5, 6, 5)
+    r1 = O.entropic_ugw(x, y, u, v, 0.5, 0.05, 3, 200)
+    r2 = O.entropic_ugw(y, x, v, u, 0.5, 0.05, 3, 200)
+    np.testing.assert_allclose(r1["F"], r2["F"], rtol=1e-10)
+    assert all(0.0 < mm < 1.0 + 1e-9 for mm in r1["mass"])
