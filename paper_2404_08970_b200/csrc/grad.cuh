@@ -159,11 +159,13 @@ __global__ void k_colcarry(int64_t nl, int64_t m, int nb, const double* __restri
   constexpr int U = 16;  // blocks in flight: the loads of a group are independent, the recursion is not
   for (int b0 = 0; b0 < nb; b0 += U) {
     double s1[U], sx[U];
+    double dx[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int b = b0 + u;
       s1[u] = b < nb ? cS[(int64_t)b * m + q] : 0.0;
       sx[u] = b < nb ? cX[(int64_t)b * m + q] : 0.0;
+      dx[u] = b < nb ? xl[min((int64_t)(b + 1) * TR, nl - 1)] - xl[(int64_t)b * TR] : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -171,8 +173,7 @@ __global__ void k_colcarry(int64_t nl, int64_t m, int nb, const double* __restri
       if (b < nb) {
         cS[(int64_t)b * m + q] = CP;
         cX[(int64_t)b * m + q] = CX;
-        const double xa = xl[(int64_t)b * TR], xb = xl[min((int64_t)(b + 1) * TR, nl - 1)];
-        CX = CX + (xb - xa) * CP + sx[u];
+        CX = CX + dx[u] * CP + sx[u];
         CP += s1[u];
       }
     }
@@ -190,7 +191,7 @@ __global__ void __launch_bounds__(TR) k_rowcarry(int64_t nl, int64_t m, int ns, 
                                                  const double* __restrict__ yc, double* __restrict__ rP,
                                                  double* __restrict__ rA, double* __restrict__ blk,
                                                  double* __restrict__ Ptot, double* __restrict__ Aend) {
-  constexpr int U = 16;  // strips in flight
+  constexpr int U = 8;  // strips in flight
   __shared__ double red[U][NWARP][4];
   const int b = blockIdx.x;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
@@ -201,11 +202,12 @@ __global__ void __launch_bounds__(TR) k_rowcarry(int64_t nl, int64_t m, int ns, 
   double P = 0.0, A = 0.0;
   for (int sc = 0; sc < ns; sc += U) {
     const int cnt = min(U, ns - sc);
-    double rp[U], ra[U];
+    double rp[U], ra[U], dy[U];
 #pragma unroll
     for (int k = 0; k < U; ++k) {
       rp[k] = (jv && k < cnt) ? rP[(int64_t)(sc + k) * nl + j] : 0.0;
       ra[k] = (jv && k < cnt) ? rA[(int64_t)(sc + k) * nl + j] : 0.0;
+      dy[k] = k < cnt ? yc[min((int64_t)(sc + k + 1) * TC, m - 1)] - yc[(int64_t)(sc + k) * TC] : 0.0;
     }
 #pragma unroll
     for (int k = 0; k < U; ++k) {
@@ -217,8 +219,7 @@ __global__ void __launch_bounds__(TR) k_rowcarry(int64_t nl, int64_t m, int ns, 
         }
         const double v0 = warp_sum(P), v1 = warp_sum(A), v2 = warp_sum(dxe * P), v3 = warp_sum(dxe * A);
         if (lane == 0) { red[k][w][0] = v0; red[k][w][1] = v1; red[k][w][2] = v2; red[k][w][3] = v3; }
-        const double ya = yc[(int64_t)s * TC], yb = yc[min((int64_t)(s + 1) * TC, m - 1)];
-        A = A + (yb - ya) * P + ra[k];
+        A = A + dy[k] * P + ra[k];
         P += rp[k];
       }
     }
@@ -247,17 +248,19 @@ __global__ void k_blkscan(int64_t nl, int nb, int ns, const double* __restrict__
   constexpr int U = 16;
   for (int b0 = 0; b0 < nb; b0 += U) {
     double4 tv[U];
+    double dxv[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int b = b0 + u;
       tv[u] = b < nb ? *reinterpret_cast<const double4*>(blk + ((int64_t)b * ns + s) * 4) : make_double4(0, 0, 0, 0);
+      dxv[u] = b < nb ? xl[min((int64_t)(b + 1) * TR, nl - 1)] - xl[(int64_t)b * TR] : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int b = b0 + u;
       if (b < nb) {
         *reinterpret_cast<double4*>(bs + ((int64_t)b * ns + s) * 4) = make_double4(SP, SA, XP, XA);
-        const double dx = xl[min((int64_t)(b + 1) * TR, nl - 1)] - xl[(int64_t)b * TR];
+        const double dx = dxv[u];
         XP = XP + dx * SP + tv[u].z;
         XA = XA + dx * SA + tv[u].w;
         SP += tv[u].x;

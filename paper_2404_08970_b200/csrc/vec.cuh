@@ -84,32 +84,61 @@ struct Scan1DBatch {
 };
 
 __global__ void __launch_bounds__(1024) k_scan1d(Scan1DBatch B) {
+  // Warp w owns the contiguous chunk [w C, (w+1) C), walked 32 elements at a time (lane =
+  // element: coalesced loads and stores); a warp scan of the elements' states per step, a
+  // fixed-order scan of the 32 warp totals, then the second (output) walk.
   __shared__ double sm[3 * 32];
   const Scan1D D = B.d[blockIdx.x];
   const int64_t n = D.n;
   if (n <= 0) return;
-  const int64_t chunk = (n + blockDim.x - 1) / blockDim.x;
-  const int64_t i0 = threadIdx.x * chunk, i1 = min(n, i0 + chunk);
-  PA<double> st{0.0, 0.0, D.s[min(i0, n - 1)]};
-#pragma unroll 8
-  for (int64_t i = i0; i < i1; ++i) {
-    const double si = D.s[i];
-    st.A += (si - st.s) * st.P;
-    st.s = si;
-    st.P += D.v[i];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  constexpr int NW = 32;
+  const int64_t C = ((n + NW - 1) / NW + 31) / 32 * 32;
+  const int64_t i0 = (int64_t)w * C, i1 = min(n, i0 + C);
+  // pass 1: the warp's total state
+  PA<double> run{0.0, 0.0, i0 < n ? D.s[i0] : D.s[n - 1]};
+  for (int64_t base = i0; base < i1; base += 32) {
+    const int64_t i = base + lane;
+    PA<double> e{0.0, 0.0, D.s[min(i, i1 - 1)]};
+    if (i < i1) e.P = D.v[i];
+    PA<double> ex;
+    const PA<double> inc = pa_warp_scan(e, ex);
+    PA<double> st;  // the step's total (lane 31's inclusive state)
+    st.P = __shfl_sync(0xffffffffu, inc.P, 31);
+    st.A = __shfl_sync(0xffffffffu, inc.A, 31);
+    st.s = __shfl_sync(0xffffffffu, inc.s, 31);
+    run = pa_combine(run, st);
   }
-  PA<double> total;
-  PA<double> e = pa_block_scan_excl<32>(st, sm, total);
-  const double V = total.P, Sv = total.s * total.P - total.A;
-#pragma unroll 8
-  for (int64_t i = i0; i < i1; ++i) {
-    const double si = D.s[i];
-    const double lo = pa_eval(e, si);
-    if (D.lower) D.lower[i] = lo;
-    if (D.dist) D.dist[i] = 2.0 * lo + Sv - si * V;
-    e.A = lo;
-    e.s = si;
-    e.P += D.v[i];
+  if (lane == 0) { sm[w] = run.P; sm[NW + w] = run.A; sm[2 * NW + w] = run.s; }
+  __syncthreads();
+  PA<double> pre{0.0, 0.0, sm[2 * NW]};
+  PA<double> tot = pre;
+  for (int k = 0; k < NW; ++k) {
+    const PA<double> t{sm[k], sm[NW + k], sm[2 * NW + k]};
+    if (k < w) pre = pa_combine(pre, t);
+    tot = pa_combine(tot, t);
+  }
+  const double V = tot.P, Sv = tot.s * tot.P - tot.A;
+  // pass 2: outputs
+  run = pre;
+  for (int64_t base = i0; base < i1; base += 32) {
+    const int64_t i = base + lane;
+    const double si = D.s[min(i, i1 - 1)];
+    PA<double> e{0.0, 0.0, si};
+    if (i < i1) e.P = D.v[i];
+    PA<double> ex;
+    const PA<double> inc = pa_warp_scan(e, ex);
+    const PA<double> mine = pa_combine(run, ex);  // all elements before i
+    const double lo = pa_eval(mine, si);
+    if (i < i1) {
+      if (D.lower) D.lower[i] = lo;
+      if (D.dist) D.dist[i] = 2.0 * lo + Sv - si * V;
+    }
+    PA<double> st;
+    st.P = __shfl_sync(0xffffffffu, inc.P, 31);
+    st.A = __shfl_sync(0xffffffffu, inc.A, 31);
+    st.s = __shfl_sync(0xffffffffu, inc.s, 31);
+    run = pa_combine(run, st);
   }
   if (D.tot && threadIdx.x == 0) { D.tot[0] = V; D.tot[1] = Sv; }
 }
