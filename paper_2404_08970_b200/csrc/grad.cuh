@@ -187,7 +187,7 @@ __global__ void k_colcarry(int64_t nl, int64_t m, int nb, const double* __restri
 // plus per-(block, strip) sums over the block's rows of {P_c0, A_c0, (xe_b - x_j) P_c0,
 // (xe_b - x_j) A_c0} -> blk (the column-direction carry of the row carries).
 // Totals: Ptot = T 1, Aend = sum_q (y_{m-1} - y_q) T_jq.
-__global__ void __launch_bounds__(TR) k_rowcarry(int64_t nl, int64_t m, int ns, const double* __restrict__ xl,
+__global__ void __launch_bounds__(TR, 2) k_rowcarry(int64_t nl, int64_t m, int ns, const double* __restrict__ xl,
                                                  const double* __restrict__ yc, double* __restrict__ rP,
                                                  double* __restrict__ rA, double* __restrict__ blk,
                                                  double* __restrict__ Ptot, double* __restrict__ Aend) {

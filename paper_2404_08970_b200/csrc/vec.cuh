@@ -95,19 +95,29 @@ __global__ void __launch_bounds__(1024) k_scan1d(Scan1DBatch B) {
   constexpr int NW = 32;
   const int64_t C = ((n + NW - 1) / NW + 31) / 32 * 32;
   const int64_t i0 = (int64_t)w * C, i1 = min(n, i0 + C);
-  // pass 1: the warp's total state
+  // pass 1: the warp's total state (the loads of 4 steps issued together)
+  constexpr int SU = 4;
   PA<double> run{0.0, 0.0, i0 < n ? D.s[i0] : D.s[n - 1]};
-  for (int64_t base = i0; base < i1; base += 32) {
-    const int64_t i = base + lane;
-    PA<double> e{0.0, 0.0, D.s[min(i, i1 - 1)]};
-    if (i < i1) e.P = D.v[i];
-    PA<double> ex;
-    const PA<double> inc = pa_warp_scan(e, ex);
-    PA<double> st;  // the step's total (lane 31's inclusive state)
-    st.P = __shfl_sync(0xffffffffu, inc.P, 31);
-    st.A = __shfl_sync(0xffffffffu, inc.A, 31);
-    st.s = __shfl_sync(0xffffffffu, inc.s, 31);
-    run = pa_combine(run, st);
+  for (int64_t b4 = i0; b4 < i1; b4 += 32 * SU) {
+    double sv[SU], vv[SU];
+#pragma unroll
+    for (int u = 0; u < SU; ++u) {
+      const int64_t i = b4 + 32 * u + lane;
+      sv[u] = D.s[min(i, i1 - 1)];
+      vv[u] = i < i1 ? D.v[i] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < SU; ++u) {
+      if (b4 + 32 * u >= i1) break;  // uniform across the warp
+      PA<double> e{vv[u], 0.0, sv[u]};
+      PA<double> ex;
+      const PA<double> inc = pa_warp_scan(e, ex);
+      PA<double> st;  // the step's total (lane 31's inclusive state)
+      st.P = __shfl_sync(0xffffffffu, inc.P, 31);
+      st.A = __shfl_sync(0xffffffffu, inc.A, 31);
+      st.s = __shfl_sync(0xffffffffu, inc.s, 31);
+      run = pa_combine(run, st);
+    }
   }
   if (lane == 0) { sm[w] = run.P; sm[NW + w] = run.A; sm[2 * NW + w] = run.s; }
   __syncthreads();
@@ -121,24 +131,34 @@ __global__ void __launch_bounds__(1024) k_scan1d(Scan1DBatch B) {
   const double V = tot.P, Sv = tot.s * tot.P - tot.A;
   // pass 2: outputs
   run = pre;
-  for (int64_t base = i0; base < i1; base += 32) {
-    const int64_t i = base + lane;
-    const double si = D.s[min(i, i1 - 1)];
-    PA<double> e{0.0, 0.0, si};
-    if (i < i1) e.P = D.v[i];
-    PA<double> ex;
-    const PA<double> inc = pa_warp_scan(e, ex);
-    const PA<double> mine = pa_combine(run, ex);  // all elements before i
-    const double lo = pa_eval(mine, si);
-    if (i < i1) {
-      if (D.lower) D.lower[i] = lo;
-      if (D.dist) D.dist[i] = 2.0 * lo + Sv - si * V;
+  for (int64_t b4 = i0; b4 < i1; b4 += 32 * SU) {
+    double sv[SU], vv[SU];
+#pragma unroll
+    for (int u = 0; u < SU; ++u) {
+      const int64_t i = b4 + 32 * u + lane;
+      sv[u] = D.s[min(i, i1 - 1)];
+      vv[u] = i < i1 ? D.v[i] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < SU; ++u) {
+      if (b4 + 32 * u >= i1) break;  // uniform across the warp
+      const int64_t i = b4 + 32 * u + lane;
+      const double si = sv[u];
+      PA<double> e{vv[u], 0.0, si};
+      PA<double> ex;
+      const PA<double> inc = pa_warp_scan(e, ex);
+      const PA<double> mine = pa_combine(run, ex);  // all elements before i
+      const double lo = pa_eval(mine, si);
+      if (i < i1) {
+        if (D.lower) D.lower[i] = lo;
+        if (D.dist) D.dist[i] = 2.0 * lo + Sv - si * V;
     }
     PA<double> st;
     st.P = __shfl_sync(0xffffffffu, inc.P, 31);
     st.A = __shfl_sync(0xffffffffu, inc.A, 31);
     st.s = __shfl_sync(0xffffffffu, inc.s, 31);
     run = pa_combine(run, st);
+    }
   }
   if (D.tot && threadIdx.x == 0) { D.tot[0] = V; D.tot[1] = Sv; }
 }
