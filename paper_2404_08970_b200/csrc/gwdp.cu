@@ -93,6 +93,7 @@ struct gw_ctx {
   long long launches = 0;
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t cap = nullptr;  // CUDA-graph capture stream (created on first use)
   gw_comm* comm = nullptr;
   std::vector<Buf*> all;
   // vectors
@@ -247,6 +248,7 @@ extern "C" gw_status gw_ctx_destroy(gw_ctx* c) {
   gw_status st = gw_ctx_trim(c);
   for (auto e : c->prof.pool) cudaEventDestroy(e);
   if (c->hpin) cudaFreeHost(c->hpin);
+  if (c->cap) cudaStreamDestroy(c->cap);
   delete c;
   return st;
 }
@@ -1058,6 +1060,16 @@ struct SinkState {
   double *lse, *lseg, *csl, *csg;
   float* violg;
   int *flag, *flagg;  // speculation validity flag (and the ranks' flags)
+  cudaGraphExec_t gexec = nullptr;  // one fixed-count iteration, captured once per solve
+};
+
+static void sink_free(SinkState& s) {
+  if (s.gexec) cudaGraphExecDestroy(s.gexec);
+  s.gexec = nullptr;
+}
+struct SinkGuard {  // releases the captured graph on every exit path of a solve
+  SinkState& s;
+  ~SinkGuard() { sink_free(s); }
 };
 
 template <int K, int CL, int NT>
@@ -1251,63 +1263,95 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
     const char* pf = getenv("GWDP_L2_AHEAD");
     fa.l2_ahead = pf ? atoi(pf) : 0;
   }
+  // one iteration (check: the tolerance rule's violation check of the plan after `done` iterations)
+  auto iteration = [&](bool check, int done) -> gw_status {
+    // Every iteration first tries the fused one-read path when *mode == 1 (speculatively at the
+    // start of a solve); k_sink_fast_check validates it before anything is committed, and on
+    // failure k_sink_fin_fast leaves f, g untouched and sets *mode = 0 so that the robust
+    // two-kernel path below runs this same iteration.  No host sync.
+    if (!check && s.fK > 0) {
+      PROF_BEGIN(c, PC_SINK_FUSED);
+      TRY(fused_launch(c, s.fK, s.fCL, s.fNT, fa, s.fncl));
+      KCHECK();
+      k_sink_colsum<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.fpart, s.fncl, m, s.csl, s.mode, s.stop);
+      KCHECK();
+      TRY(comm_allgather(c, s.csl, s.csg, sizeof(double) * (size_t)m));
+      CU(cudaMemsetAsync(s.flag, 0, sizeof(int), c->stream));
+      k_sink_fast_check<<<grid_for(std::max(m, nl), 256, 1 << 30), 256, 0, c->stream>>>(
+          s.Srow, nl, s.csg, P.R, m, P.lq, s.flag, s.mode, s.stop);
+      KCHECK();
+      if (P.R > 1) {
+        TRY(comm_allgather(c, s.flag, s.flagg, sizeof(int)));
+        k_or_flags<<<1, 32, 0, c->stream>>>(s.flag, s.flagg, P.R);
+        KCHECK();
+      }
+      k_sink_fin_fast<<<grid_for(std::max(m, nl), 256, 1 << 30), 256, 0, c->stream>>>(
+          s.Srow, nl, P.lp + P.row0, s.f, s.fh, s.fl, nullptr, s.csg, P.R, m, P.lq, eps, s.g, s.gh, s.gl,
+          s.mode, s.stop, s.dev, s.flag);
+      KCHECK();
+      PROF_END(c, PC_SINK_FUSED, 2);
+    }
+    // iterations run the robust two-kernel path while *mode == 0 (decided on the device)
+    const int* skip = check ? nullptr : s.mode;
+    if (check) CU(cudaMemsetAsync(s.viol, 0, sizeof(float), c->stream));
+    double* fout = check ? s.ftmp : s.f;
+    PROF_BEGIN(c, PC_SINK_ROW);
+    k_sink_row<<<rgrid, 256, 0, c->stream>>>(
+        G, ldG, nl, m, s.gh, s.gl, c2f, s.f, fout, P.lp + P.row0, eps, s.fh, s.fl, check ? s.viol : nullptr, s.stop,
+        skip);
+    KCHECK();
+    PROF_END(c, PC_SINK_ROW, 1);
+    if (check) {
+      TRY(sink_viol_global(c, P, s));
+      k_sink_commit<<<grid_for(nl), 256, 0, c->stream>>>(s.viol, tol, s.stop, s.ftmp, s.f, nl, s.iters, done);
+      KCHECK();
+    }
+    PROF_BEGIN(c, PC_SINK_COL);
+    k_sink_col<<<cgrid, 256, 0, c->stream>>>(G, ldG, nl, m, s.fh, s.fl, c2f, s.RB, s.part, s.stop, skip);
+    KCHECK();
+    k_sink_colmerge<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.part, s.nrb, m, s.lse, s.stop, skip);
+    KCHECK();
+    TRY(comm_allgather(c, s.lse, s.lseg, 2 * sizeof(double) * (size_t)m));
+    k_sink_colfin<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.lseg, P.R, m, P.lq, eps, s.g, s.gh, s.gl,
+                                                                     s.stop, skip, s.dev);
+    KCHECK();
+    PROF_END(c, PC_SINK_COL, 2);
+    k_sink_mode<<<1, 32, 0, c->stream>>>(s.dev, s.mode, s.fK > 0 ? 20.f : -1.f);
+    KCHECK();
+    return GW_OK;
+  };
+  // Fixed iteration counts on one rank: the iteration's ~10 launches are captured once per solve
+  // into a CUDA graph and replayed (the small configurations are launch-bound; GWDP_NO_GRAPH=1
+  // disables it; not while per-kernel profiling is on, whose events time the launches).
+  static const bool no_graph = getenv("GWDP_NO_GRAPH") != nullptr;
+  if (!tolmode && !no_graph && !c->prof.on && P.R == 1 && iters >= 3) {
+    if (!s.gexec) {
+      if (!c->cap) CU(cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking));
+      CU(cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal));
+      cudaStream_t saved = c->stream;
+      c->stream = c->cap;
+      const gw_status st = iteration(false, 0);
+      c->stream = saved;
+      cudaGraph_t graph = nullptr;
+      const cudaError_t e = cudaStreamEndCapture(c->cap, &graph);
+      if (st != GW_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return st;
+      }
+      if (e != cudaSuccess) return fail(GW_ERR_CUDA, "Sinkhorn graph capture: %s", cudaGetErrorString(e));
+      const cudaError_t ei = cudaGraphInstantiate(&s.gexec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ei != cudaSuccess) return fail(GW_ERR_CUDA, "Sinkhorn graph instantiate: %s", cudaGetErrorString(ei));
+    }
+    for (int k = 0; k < iters; ++k) CU(cudaGraphLaunch(s.gexec, c->stream));
+    *used = iters;
+    return GW_OK;
+  }
   while (done < iters) {
     const int chunk = tolmode ? std::min(check_every, iters - done) : iters - done;
     for (int k = 0; k < chunk; ++k) {
       const bool check = tolmode && k == 0 && done > 0;  // violation of the plan after `done` iterations
-      // Every iteration first tries the fused one-read path when *mode == 1 (speculatively at the
-      // start of a solve); k_sink_fast_check validates it before anything is committed, and on
-      // failure k_sink_fin_fast leaves f, g untouched and sets *mode = 0 so that the robust
-      // two-kernel path below runs this same iteration.  No host sync.
-      if (!check && s.fK > 0) {
-        PROF_BEGIN(c, PC_SINK_FUSED);
-        TRY(fused_launch(c, s.fK, s.fCL, s.fNT, fa, s.fncl));
-        KCHECK();
-        k_sink_colsum<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.fpart, s.fncl, m, s.csl, s.mode, s.stop);
-        KCHECK();
-        TRY(comm_allgather(c, s.csl, s.csg, sizeof(double) * (size_t)m));
-        CU(cudaMemsetAsync(s.flag, 0, sizeof(int), c->stream));
-        k_sink_fast_check<<<grid_for(std::max(m, nl), 256, 1 << 30), 256, 0, c->stream>>>(
-            s.Srow, nl, s.csg, P.R, m, P.lq, s.flag, s.mode, s.stop);
-        KCHECK();
-        if (P.R > 1) {
-          TRY(comm_allgather(c, s.flag, s.flagg, sizeof(int)));
-          k_or_flags<<<1, 32, 0, c->stream>>>(s.flag, s.flagg, P.R);
-          KCHECK();
-        }
-        k_sink_fin_fast<<<grid_for(std::max(m, nl), 256, 1 << 30), 256, 0, c->stream>>>(
-            s.Srow, nl, P.lp + P.row0, s.f, s.fh, s.fl, nullptr, s.csg, P.R, m, P.lq, eps, s.g, s.gh, s.gl,
-            s.mode, s.stop, s.dev, s.flag);
-        KCHECK();
-        PROF_END(c, PC_SINK_FUSED, 2);
-      }
-      // iterations run the robust two-kernel path while *mode == 0 (decided on the device)
-      const int* skip = check ? nullptr : s.mode;
-      if (check) CU(cudaMemsetAsync(s.viol, 0, sizeof(float), c->stream));
-      double* fout = check ? s.ftmp : s.f;
-      PROF_BEGIN(c, PC_SINK_ROW);
-      k_sink_row<<<rgrid, 256, 0, c->stream>>>(
-          G, ldG, nl, m, s.gh, s.gl, c2f, s.f, fout, P.lp + P.row0, eps, s.fh, s.fl, check ? s.viol : nullptr, s.stop,
-          skip);
-      KCHECK();
-      PROF_END(c, PC_SINK_ROW, 1);
-      if (check) {
-        TRY(sink_viol_global(c, P, s));
-        k_sink_commit<<<grid_for(nl), 256, 0, c->stream>>>(s.viol, tol, s.stop, s.ftmp, s.f, nl, s.iters, done);
-        KCHECK();
-      }
-      PROF_BEGIN(c, PC_SINK_COL);
-      k_sink_col<<<cgrid, 256, 0, c->stream>>>(G, ldG, nl, m, s.fh, s.fl, c2f, s.RB, s.part, s.stop, skip);
-      KCHECK();
-      k_sink_colmerge<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.part, s.nrb, m, s.lse, s.stop, skip);
-      KCHECK();
-      TRY(comm_allgather(c, s.lse, s.lseg, 2 * sizeof(double) * (size_t)m));
-      k_sink_colfin<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.lseg, P.R, m, P.lq, eps, s.g, s.gh, s.gl,
-                                                                       s.stop, skip, s.dev);
-      KCHECK();
-      PROF_END(c, PC_SINK_COL, 2);
-      k_sink_mode<<<1, 32, 0, c->stream>>>(s.dev, s.mode, s.fK > 0 ? 20.f : -1.f);
-      KCHECK();
+      TRY(iteration(check, done));
     }
     if (tolmode) {
       int hs[2];
@@ -1386,6 +1430,7 @@ extern "C" gw_status sinkhorn_solve(gw_ctx* c, const gw_problem* pb, const void*
   Prepared P;
   TRY(prepare(c, pb, P));
   SinkState s;
+  SinkGuard sguard{s};
   TRY(sink_alloc(c, P, s));
   TRY(stage_duals_in(c, pb, P, f, g, &s.f, &s.g));
   TRY(sink_split(c, P, s, o->eps));
@@ -1463,6 +1508,7 @@ static gw_status solve_impl(gw_ctx* c, const gw_problem* pb, const gw_solve_opts
   float* G;
   TRY(ws(c, c->Gs, (size_t)std::max<int64_t>(nl, 1) * ldG, &G));
   SinkState s;
+  SinkGuard sguard{s};
   TRY(sink_alloc(c, P, s));
   if (pb->flags & GW_HOST_VECTORS) {
     TRY(stage_duals_in(c, pb, P, nullptr, nullptr, &s.f, &s.g));  // device scratch for host duals
@@ -1706,6 +1752,7 @@ static gw_status ugw_impl(gw_ctx* c, const gw_problem* pb, double rho, const gw_
   float* G;
   TRY(ws(c, c->Gs, (size_t)std::max<int64_t>(nl, 1) * ldG, &G));
   SinkState s;
+  SinkGuard sguard{s};
   TRY(sink_alloc(c, P, s));
   if (pb->flags & GW_HOST_VECTORS) {
     TRY(stage_duals_in(c, pb, P, nullptr, nullptr, &s.f, &s.g));
