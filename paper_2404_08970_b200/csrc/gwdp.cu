@@ -1273,7 +1273,7 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
       PROF_BEGIN(c, PC_SINK_FUSED);
       TRY(fused_launch(c, s.fK, s.fCL, s.fNT, fa, s.fncl));
       KCHECK();
-      k_sink_colsum<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.fpart, s.fncl, m, s.csl, s.mode, s.stop);
+      k_sink_colsum<<<(unsigned)((m + 31) / 32), 256, 0, c->stream>>>(s.fpart, s.fncl, m, s.csl, s.mode, s.stop);
       KCHECK();
       TRY(comm_allgather(c, s.csl, s.csg, sizeof(double) * (size_t)m));
       CU(cudaMemsetAsync(s.flag, 0, sizeof(int), c->stream));
@@ -1309,12 +1309,18 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
     PROF_BEGIN(c, PC_SINK_COL);
     k_sink_col<<<cgrid, 256, 0, c->stream>>>(G, ldG, nl, m, s.fh, s.fl, c2f, s.RB, s.part, s.stop, skip);
     KCHECK();
-    k_sink_colmerge<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.part, s.nrb, m, s.lse, s.stop, skip);
-    KCHECK();
-    TRY(comm_allgather(c, s.lse, s.lseg, 2 * sizeof(double) * (size_t)m));
-    k_sink_colfin<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.lseg, P.R, m, P.lq, eps, s.g, s.gh, s.gl,
-                                                                     s.stop, skip, s.dev);
-    KCHECK();
+    if (P.R == 1) {
+      k_sink_colmergefin<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.part, s.nrb, m, P.lq, eps, s.g, s.gh,
+                                                                            s.gl, s.stop, skip, s.dev);
+      KCHECK();
+    } else {
+      k_sink_colmerge<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.part, s.nrb, m, s.lse, s.stop, skip);
+      KCHECK();
+      TRY(comm_allgather(c, s.lse, s.lseg, 2 * sizeof(double) * (size_t)m));
+      k_sink_colfin<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.lseg, P.R, m, P.lq, eps, s.g, s.gh, s.gl,
+                                                                       s.stop, skip, s.dev);
+      KCHECK();
+    }
     PROF_END(c, PC_SINK_COL, 2);
     k_sink_mode<<<1, 32, 0, c->stream>>>(s.dev, s.mode, s.fK > 0 ? 20.f : -1.f);
     KCHECK();

@@ -228,15 +228,62 @@ __global__ void k_sink_colfin(const double* __restrict__ gath, int R, int64_t m,
   gl[q] = isfinite(gs) ? (float)(gs - (double)h) : 0.f;
 }
 
-// Fused path: this rank's column sums of the half-step plan, clusters summed in fixed order.
-__global__ void k_sink_colsum(const double* __restrict__ part, int ncl, int64_t m, double* __restrict__ out,
-                              const int* __restrict__ mode, const int* __restrict__ stop) {
-  if (*mode != 1 || (stop && *stop)) return;
+// One rank: pass 2a + 2b in one launch (merge the row-block partials, then update g).
+__global__ void k_sink_colmergefin(const float2* __restrict__ part, int nrb, int64_t m, const double* __restrict__ lq,
+                                   double eps, double* __restrict__ g, float* __restrict__ gh, float* __restrict__ gl,
+                                   const int* __restrict__ stop, const int* __restrict__ skip_if_fast,
+                                   float* __restrict__ dev, double kappa = 1.0) {
+  if (stop && *stop) return;
+  if (skip_if_fast && *skip_if_fast) return;
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (q >= m) return;
+  double M = -INFINITY;
+  for (int rb = 0; rb < nrb; ++rb) M = fmax(M, (double)part[(int64_t)rb * m + q].x);
+  double S = 0.0;
+  if (M != -INFINITY)
+    for (int rb = 0; rb < nrb; ++rb) {
+      const float2 v = part[(int64_t)rb * m + q];
+      if (v.x != -INFINITY) S += (double)v.y * exp2((double)v.x - M);
+    }
+  // (M, S) exactly as k_sink_colmerge + k_sink_colfin with R = 1
+  const double lse2 = M + log2(S);
+  const double gn = (lq[q] == -INFINITY) ? -INFINITY : eps * lq[q] - kappa * (eps * GW_LN2 * lse2);
+  if (dev) {
+    double d = fabs((gn - g[q]) * (GW_LOG2E / eps));
+    if (!(d == d)) d = 3.0e38;
+    float dv = (float)fmin(d, 3.0e38);
+    dv = warp_max(dv);
+    if ((threadIdx.x & 31) == 0) atomic_max_nonneg(dev, dv);
+  }
+  g[q] = gn;
+  const double gs = gn * (GW_LOG2E / eps);
+  const float h = (float)gs;
+  gh[q] = h;
+  gl[q] = isfinite(gs) ? (float)(gs - (double)h) : 0.f;
+}
+
+// Fused path: this rank's column sums of the half-step plan, clusters summed in fixed order.
+// CTA = 32 columns x 8 warps: warp w sums clusters w, w + 8, ... for lane's column, then the 8
+// warp sums are added in warp order (deterministic; 8x the parallelism of a thread per column,
+// which matters when there are many clusters, i.e. small problems with one CTA per cluster).
+__global__ void __launch_bounds__(256) k_sink_colsum(const double* __restrict__ part, int ncl, int64_t m,
+                                                     double* __restrict__ out, const int* __restrict__ mode,
+                                                     const int* __restrict__ stop) {
+  if (*mode != 1 || (stop && *stop)) return;
+  __shared__ double red[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t q = blockIdx.x * (int64_t)32 + lane;
   double CS = 0.0;
-  for (int c = 0; c < ncl; ++c) CS += part[(int64_t)c * m + q];
-  out[q] = CS;
+  if (q < m)
+    for (int c = w; c < ncl; c += 8) CS += part[(int64_t)c * m + q];
+  red[w][lane] = CS;
+  __syncthreads();
+  if (w == 0 && q < m) {
+    double v = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v += red[k][lane];
+    out[q] = v;
+  }
 }
 
 // Tolerance rule (reading R8): the row half-step of iteration k+1 measured the violation of
