@@ -63,7 +63,7 @@ typedef enum {
   GW_ERR_NOT_NORMALIZED = 5,  /* |sum - 1| > 1e-9                        */
   GW_ERR_NONFINITE = 6,       /* NaN/Inf in inputs or produced          */
   GW_ERR_CONFIG = 7,          /* invalid options                                       */
-  GW_ERR_UNSUPPORTED = 8,     /* k > GW_MAX_K, loss != square, tau != eps, fp64 storage, ... */
+  GW_ERR_UNSUPPORTED = 8,     /* k > GW_MAX_K, loss != square, fp64 storage, tau != eps off k = 1, ... */
   GW_ERR_OOM = 9,
   GW_ERR_CUDA = 10,
   GW_ERR_NCCL = 11
@@ -121,7 +121,9 @@ typedef struct {
                                           moments+reduce pass for the last l only)        */
 
 typedef struct {
-  double eps, tau;            /* tau must equal eps (Remark 1, reading R6)            */
+  double eps, tau;            /* tau: the step's KL weight; 0 or eps =
+                                 Remark 1's tau = eps; tau != eps (k = 1, 1-D, T0 = NULL):
+                                 cost grad E + (eps - tau) ln T^l at regulariser tau (R6) */
   int32_t outer_iters;        /* mirror-descent iterations L                           */
   gw_sinkhorn_opts inner;     /* inner.eps is ignored (eps above is used)              */
   uint32_t flags;             /* GW_SOLVE_* */
@@ -206,7 +208,7 @@ gw_status sinkhorn_solve(gw_ctx *ctx, const gw_problem *prob, const void *G, int
                          const gw_sinkhorn_opts *opts, double *f, double *g,
                          void *T_out, int64_t ldT, gw_sinkhorn_info *info);
 
-/* Entropic GW by mirror descent, tau = eps.
+/* Entropic GW by mirror descent (tau = eps unless opts->tau says otherwise).
  * T0: initial plan (device fp32, nullable -> p (x) q, reading R5); T_out: final plan
  * (nullable).  f, g: final duals (f has n_local entries, g has m).  res (host,
  * required).  trace (host, nullable): [outer_iters x 4] doubles per outer l:

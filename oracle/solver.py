@@ -69,7 +69,7 @@ def sinkhorn(G, p, q, eps, iters, f0=None, g0=None, tol=None, check_every=10):
 
 
 def entropic_gw(x, y, p, q, eps, outer, inner, k=1, T0=None, tol=None,
-                check_every=10, record_grads=False, grad_mode="dense"):
+                check_every=10, record_grads=False, grad_mode="dense", tau=None):
     """Entropic GW by mirror descent with tau = eps.
 
     PAPER.md:102-114 (eqs. "GW proximal gradient", "GW sinkhorn") and Remark 1
@@ -79,6 +79,12 @@ def entropic_gw(x, y, p, q, eps, outer, inner, k=1, T0=None, tol=None,
     paper's recursion instead of dense products.  ``inner`` is an int (same count every
     outer iteration) or a sequence of per-outer counts (to replay the GPU's
     counts under reading R8).
+
+    ``tau`` (default eps): the general mirror-descent step of PAPER.md:102-110,
+    T^{l+1} = argmin_{T in S(p,q)} <grad E(T^l) + (eps - tau) grad H(T^l), T> + tau H(T),
+    grad H(T) = ln T, i.e. entropic OT of the cost Pi = G + (eps - tau) ln T^l at
+    regulariser tau; ln T^l is the log-domain plan (f + g - Pi_prev)/tau (ln p + ln q for
+    T^0 = p (x) q), never log of an underflowed entry.
 
     Returns a dict: T, f, g, E (list, E(T^l) for l = 1..L), viol (list),
     inner_used (list), gw_objective, entropic_objective, and G (list) when
@@ -93,13 +99,20 @@ def entropic_gw(x, y, p, q, eps, outer, inner, k=1, T0=None, tol=None,
     g = np.zeros(y.size)
     counts = [int(inner)] * outer if np.isscalar(inner) else [int(c) for c in inner]
     out = {"E": [], "viol": [], "inner_used": [], "G": []}
+    tau = eps if tau is None else float(tau)
+    if tau != eps:
+        lnT = _log(T)  # T^0 (p (x) q or T0); afterwards the log-domain plan
     for l in range(outer):
         if grad_mode == "dp":
             G = grad_prescribed_dp(x, y, p, q, T, k)
         else:
             G = grad_prescribed(x, y, p, q, T, k)
-        f, g, used = sinkhorn(G, p, q, eps, counts[l], f, g, tol=tol, check_every=check_every)
-        T = plan_from_duals(G, f, g, eps)
+        if tau != eps:
+            G = G + (eps - tau) * lnT  # the cost Pi of PAPER.md:110
+        f, g, used = sinkhorn(G, p, q, tau, counts[l], f, g, tol=tol, check_every=check_every)
+        T = plan_from_duals(G, f, g, tau)
+        if tau != eps:
+            lnT = (f[:, None] + g[None, :] - G) / tau
         out["E"].append(objective(x, y, T, k))
         out["viol"].append(violation(T, p, q))
         out["inner_used"].append(used)
@@ -111,9 +124,9 @@ def entropic_gw(x, y, p, q, eps, outer, inner, k=1, T0=None, tol=None,
 
 
 def entropic_fgw(x, y, p, q, fx, fy, alpha, eps, outer, inner, k=1, T0=None,
-                 tol=None, check_every=10):
+                 tol=None, check_every=10, tau=None):
     """Entropic FGW: the same iteration with grad E_bar (Remark 2, PAPER.md:134-147:
-    "The iteration formula ... applies to FGW as well")."""
+    "The iteration formula ... applies to FGW as well"); ``tau`` as in entropic_gw."""
     x = np.asarray(x, np.float64)
     y = np.asarray(y, np.float64)
     p = np.asarray(p, np.float64)
@@ -123,10 +136,17 @@ def entropic_fgw(x, y, p, q, fx, fy, alpha, eps, outer, inner, k=1, T0=None,
     g = np.zeros(y.size)
     counts = [int(inner)] * outer if np.isscalar(inner) else [int(c) for c in inner]
     out = {"E": [], "viol": [], "inner_used": []}
+    tau = eps if tau is None else float(tau)
+    if tau != eps:
+        lnT = _log(T)
     for l in range(outer):
         G = fgw_grad_prescribed(x, y, p, q, fx, fy, alpha, T, k)
-        f, g, used = sinkhorn(G, p, q, eps, counts[l], f, g, tol=tol, check_every=check_every)
-        T = plan_from_duals(G, f, g, eps)
+        if tau != eps:
+            G = G + (eps - tau) * lnT
+        f, g, used = sinkhorn(G, p, q, tau, counts[l], f, g, tol=tol, check_every=check_every)
+        T = plan_from_duals(G, f, g, tau)
+        if tau != eps:
+            lnT = (f[:, None] + g[None, :] - G) / tau
         out["E"].append(fgw_objective(x, y, fx, fy, alpha, T, k))
         out["viol"].append(violation(T, p, q))
         out["inner_used"].append(used)

@@ -164,10 +164,10 @@ def _result(res, f, g, T, tr):
                   f, g, T, tr, res.inner_fused_total)
 
 
-def _opts(eps, outer, inner, tol, check_every, trace_objective):
+def _opts(eps, outer, inner, tol, check_every, trace_objective, tau=None):
     o = L.gw_solve_opts()
     o.eps = eps
-    o.tau = eps
+    o.tau = eps if tau is None else float(tau)
     o.outer_iters = int(outer)
     o.inner = L.gw_sinkhorn_opts(eps, int(inner), float(tol), int(check_every))
     o.flags = L.GW_SOLVE_TRACE_OBJECTIVE if trace_objective else 0
@@ -176,12 +176,14 @@ def _opts(eps, outer, inner, tol, check_every, trace_objective):
 
 def solve(x, y, p, q, eps, outer, inner, tol=0.0, check_every=10, T0=None, return_plan=False,
           trace_objective=False, fx=None, fy=None, alpha=None, device=None, ctx=None, row0=0, n_local=None, k=1,
-          grid2d=False):
+          grid2d=False, tau=None):
     """Entropic GW (entropic_gw_solve) or, with fx/fy/alpha, entropic FGW (fgw_solve), on
     device vectors; tau = eps.  Sharded (ctx with a multi-rank
     comm): x, p (and fx) are full; this rank owns rows [row0, row0 + n_local): f, T0 and the
     returned plan hold those rows, g is replicated, the objective and violation are global.
-    grid2d: x, y are 2-D grid axes (GW_GRID2D); p, q have len(x)**2, len(y)**2 entries."""
+    grid2d: x, y are 2-D grid axes (GW_GRID2D); p, q have len(x)**2, len(y)**2 entries.
+    tau: the mirror-descent step's KL weight (default eps, Remark 1): the
+    subproblem is entropic OT of grad E + (eps - tau) ln T^l at regulariser tau (k = 1, 1-D)."""
     dev = torch.device(device) if device is not None else (T0.device if T0 is not None else torch.device("cuda"))
     if dev.index is None:
         dev = torch.device("cuda", torch.cuda.current_device())
@@ -201,7 +203,7 @@ def solve(x, y, p, q, eps, outer, inner, tol=0.0, check_every=10, T0=None, retur
     elif T is not None:
         ld = T.stride(0)
     pr = _problem(x, y, p, q, n_local=n, row0=row0, k=k, grid2d=grid2d)
-    o = _opts(eps, outer, inner, tol, check_every, trace_objective)
+    o = _opts(eps, outer, inner, tol, check_every, trace_objective, tau)
     res = L.gw_result()
     tr = np.zeros((max(int(outer), 1), 4), dtype=np.float64)
     trp = tr.ctypes.data_as(C.c_void_p)

@@ -308,6 +308,9 @@ struct MainArgs {
   const double* fx;    // local rows (nullable -> GW)
   const double* fy;
   double alpha;
+  // tau != eps: the cost gets + beta ln T of the plan it was regenerated
+  // from, beta = eps - tau (k_grad_store2<.., TAU>)
+  double beta;
 };
 
 // dynamic shared memory: sA [SUB][TC] (+ sT [SUB][TC] when OBJ)

@@ -72,7 +72,7 @@ struct G2Loader {
 // Regenerate T from the loaded values (MODE) and write it to the padded shared-memory tile.
 // OBJ: also copy T to sT2 and accumulate the entropy sum T (ln T - 1) into *ent;
 // on the Gibbs path ln T is the exponent itself (a ln 2), so no logarithm is taken.
-template <int MODE, bool OBJ = false>
+template <int MODE, bool OBJ = false, bool LNT = false>
 __device__ __forceinline__ void g2_stage(const G2Loader<MODE>& L, const TSrc2& S, float* __restrict__ sT, int64_t r0,
                                          int64_t c0, int64_t nl, int64_t m, int sub, float* __restrict__ sT2 = nullptr,
                                          float* ent = nullptr) {
@@ -93,12 +93,17 @@ __device__ __forceinline__ void g2_stage(const G2Loader<MODE>& L, const TSrc2& S
     for (int u = 0; u < 8; ++u) {
       const int rl = w + 4 * u;
       const int64_t i = r0 + sub * G2SUB + rl;
-      float4 t;
+      float4 t, lt = make_float4(0.f, 0.f, 0.f, 0.f);  // LNT: ln T
       if (MODE == T_EXPLICIT) {
         t = L.v[2 * u + h];
+        if (LNT) lt = make_float4(logf(t.x), logf(t.y), logf(t.z), logf(t.w));
       } else if (MODE == T_PRODUCT) {
         const float pi = i < nl ? S.fh[i] : 0.f;
         t = make_float4(pi * gh0.x, pi * gh0.y, pi * gh1.x, pi * gh1.y);
+        if (LNT) {
+          const float lpi = logf(pi);
+          lt = make_float4(lpi + logf(gh0.x), lpi + logf(gh0.y), lpi + logf(gh1.x), lpi + logf(gh1.y));
+        }
       } else {
         const float4 g = L.v[2 * u + h];
         const float Fh = i < nl ? S.fh[i] : 0.f, Fl = i < nl ? S.fl[i] : 0.f;
@@ -108,6 +113,10 @@ __device__ __forceinline__ void g2_stage(const G2Loader<MODE>& L, const TSrc2& S
         const float2 a0 = fadd2(fadd2(ffma2(g01, nch, gh0), F2), ffma2(g01, ncl, fadd2(gl0, Fl2)));
         const float2 a1 = fadd2(fadd2(ffma2(g23, nch, gh1), F2), ffma2(g23, ncl, fadd2(gl1, Fl2)));
         t = make_float4(ex2_ftz(a0.x), ex2_ftz(a0.y), ex2_ftz(a1.x), ex2_ftz(a1.y));
+        if (LNT) {
+          constexpr float ln2 = 0.6931471805599453f;
+          lt = make_float4(a0.x * ln2, a0.y * ln2, a1.x * ln2, a1.y * ln2);
+        }
         if (OBJ && i < nl) {
           constexpr float ln2 = 0.6931471805599453f;
           const float av[4] = {a0.x, a0.y, a1.x, a1.y}, tv[4] = {t.x, t.y, t.z, t.w};
@@ -122,15 +131,16 @@ __device__ __forceinline__ void g2_stage(const G2Loader<MODE>& L, const TSrc2& S
         for (int e = 0; e < 4; ++e)
           if (tv[e] > 0.f && q + e < m) *ent += tv[e] * (__logf(tv[e]) - 1.f);
       }
-      if (i >= nl) t = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (i >= nl) t = lt = make_float4(0.f, 0.f, 0.f, 0.f);
       if (q + 3 >= m) {
-        if (q >= m) t.x = 0.f;
-        if (q + 1 >= m) t.y = 0.f;
-        if (q + 2 >= m) t.z = 0.f;
-        if (q + 3 >= m) t.w = 0.f;
+        if (q >= m) t.x = lt.x = 0.f;
+        if (q + 1 >= m) t.y = lt.y = 0.f;
+        if (q + 2 >= m) t.z = lt.z = 0.f;
+        if (q + 3 >= m) t.w = lt.w = 0.f;
       }
       *reinterpret_cast<float4*>(sT + rl * G2RS + g2_phys(128 * h + 4 * lane)) = t;
       if (OBJ) *reinterpret_cast<float4*>(sT2 + rl * G2RS + g2_phys(128 * h + 4 * lane)) = t;
+      if (LNT) *reinterpret_cast<float4*>(sT2 + rl * G2RS + g2_phys(128 * h + 4 * lane)) = lt;
     }
   }
 }
@@ -153,7 +163,7 @@ __device__ __forceinline__ void g2_load_fast(G2Loader<MODE>& L, const TSrc2& S, 
   }
 }
 
-template <int MODE, bool OBJ>
+template <int MODE, bool OBJ, bool LNT = false>
 __device__ __forceinline__ void g2_stage_fast(const G2Loader<MODE>& L, const TSrc2& S, float* __restrict__ sT,
                                               const float2 (&gq)[2][2], const float2 (&gq2)[2][2],
                                               const float* __restrict__ sF, const float* __restrict__ sFl, int sub,
@@ -165,12 +175,18 @@ __device__ __forceinline__ void g2_stage_fast(const G2Loader<MODE>& L, const TSr
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int rl = w + 4 * u;
-      float4 t;
+      float4 t, lt = make_float4(0.f, 0.f, 0.f, 0.f);  // LNT: ln T
       if (MODE == T_EXPLICIT) {
         t = L.v[2 * u + h];
+        if (LNT) lt = make_float4(logf(t.x), logf(t.y), logf(t.z), logf(t.w));
       } else if (MODE == T_PRODUCT) {
         const float pi = sF[sub * G2SUB + rl];
         t = make_float4(pi * gq[h][0].x, pi * gq[h][0].y, pi * gq[h][1].x, pi * gq[h][1].y);
+        if (LNT) {
+          const float lpi = logf(pi);
+          lt = make_float4(lpi + logf(gq[h][0].x), lpi + logf(gq[h][0].y), lpi + logf(gq[h][1].x),
+                           lpi + logf(gq[h][1].y));
+        }
       } else {
         const float4 g = L.v[2 * u + h];
         const float Fh = sF[sub * G2SUB + rl], Fl = sFl[sub * G2SUB + rl];
@@ -180,6 +196,10 @@ __device__ __forceinline__ void g2_stage_fast(const G2Loader<MODE>& L, const TSr
         const float2 a0 = fadd2(fadd2(ffma2(g01, nch, gq[h][0]), F2), ffma2(g01, ncl, fadd2(gq2[h][0], Fl2)));
         const float2 a1 = fadd2(fadd2(ffma2(g23, nch, gq[h][1]), F2), ffma2(g23, ncl, fadd2(gq2[h][1], Fl2)));
         t = make_float4(ex2_ftz(a0.x), ex2_ftz(a0.y), ex2_ftz(a1.x), ex2_ftz(a1.y));
+        if (LNT) {
+          constexpr float ln2 = 0.6931471805599453f;
+          lt = make_float4(a0.x * ln2, a0.y * ln2, a1.x * ln2, a1.y * ln2);
+        }
         if (OBJ) {
           constexpr float ln2 = 0.6931471805599453f;
           const float av[4] = {a0.x, a0.y, a1.x, a1.y}, tv[4] = {t.x, t.y, t.z, t.w};
@@ -196,6 +216,7 @@ __device__ __forceinline__ void g2_stage_fast(const G2Loader<MODE>& L, const TSr
       }
       *reinterpret_cast<float4*>(sT + rl * G2RS + phys) = t;
       if (OBJ) *reinterpret_cast<float4*>(sT2 + rl * G2RS + phys) = t;
+      if (LNT) *reinterpret_cast<float4*>(sT2 + rl * G2RS + phys) = lt;
     }
   }
 }
@@ -290,7 +311,9 @@ __global__ void __launch_bounds__(G2T, 4) k_grad_moments2(TSrc2 S, int64_t nl, i
 // OBJ (the objective pass over the final plan): nothing is stored; per tile the fp64 sums
 // <G, T> (GW gradient, prescribed c), sum T (ln T - 1) and <(fx - fy)^2, T> go to
 // a.tile_obj / tile_ent / tile_cc for k_obj_partial (the constants are then not alpha-scaled).
-template <int MODE, bool FGW, bool OBJ = false>
+// TAU (tau != eps): the stored cost is G + beta ln T (beta = eps - tau) with ln T
+// of the plan the tile was regenerated from, kept in the dynamic buffer (a.beta).
+template <int MODE, bool FGW, bool OBJ = false, bool TAU = false>
 __global__ void __launch_bounds__(G2T, 3) k_grad_store2(MainArgs a, TSrc2 S) {
   __shared__ __align__(16) float sT[G2SUB * G2RS];  // T, then the local row scans (exclusive, per segment)
   extern __shared__ __align__(16) float sTobj[];     // OBJ: a copy of T (dynamic, G2SUB * G2RS floats)
@@ -405,8 +428,8 @@ __global__ void __launch_bounds__(G2T, 3) k_grad_store2(MainArgs a, TSrc2 S) {
     __syncthreads();  // previous sub-strip fully consumed; prologue smem visible
     {
       float ent = 0.f;
-      if (interior) g2_stage_fast<MODE, OBJ>(L, S, sT, gq, gq2, sF, sFl, sub, sTobj, &ent);
-      else g2_stage<MODE, OBJ>(L, S, sT, r0, c0, nl, m, sub, sTobj, &ent);
+      if (interior) g2_stage_fast<MODE, OBJ, TAU>(L, S, sT, gq, gq2, sF, sFl, sub, sTobj, &ent);
+      else g2_stage<MODE, OBJ, TAU>(L, S, sT, r0, c0, nl, m, sub, sTobj, &ent);
       if (OBJ) acc_ent += (double)ent;
     }
     if (sub + 1 < nsub) {
@@ -502,6 +525,11 @@ __global__ void __launch_bounds__(G2T, 3) k_grad_store2(MainArgs a, TSrc2 S) {
             const float fx = sFx[sub * G2SUB + rl];
             const float2 d = fadd2(make_float2(fx, fx), make_float2(-fy2.x, -fy2.y));
             g = ffma2(d, d, g);
+          }
+          if (TAU) {
+            const float2 lv = *reinterpret_cast<const float2*>(sTobj + rl * G2RS + cphys);
+            const float bt = (float)a.beta;
+            g = ffma2(lv, make_float2(bt, bt), g);
           }
             if (q1v) *reinterpret_cast<float2*>(Gp) = g;
           else if (q0v) Gp[0] = g.x;

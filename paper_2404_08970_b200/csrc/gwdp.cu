@@ -606,7 +606,7 @@ struct GradOut {
 // regeneration) so that its moments and its tile sums see bit-identical T values.
 static gw_status grad_pass_k1(gw_ctx* c, const Prepared& P, int mode, const TSrc& S, const TSrc2& S2, float* G,
                               int64_t ldG, bool store, bool obj, const double* fx, const double* fy, double alpha,
-                              double* objout_dev) {
+                              double* objout_dev, double beta = 0.0) {
   const int64_t nl = P.nl, m = P.m, n = P.n;
   const int R = P.R;
   if (nl == 0) return GW_OK;  // single rank only: prepare() rejects empty shards when R > 1
@@ -714,7 +714,7 @@ static gw_status grad_pass_k1(gw_ctx* c, const Prepared& P, int mode, const TSrc
   a.SAg = SAg; a.WAg = WAg;
   a.rP = rP; a.rA = rA; a.cS = cS; a.cX = cX; a.bs = bs; a.xlast = P.xlast; a.ylast = P.ylast;
   a.G = G; a.ldG = ldG; a.tile_obj = tobj; a.tile_ent = tent; a.tile_cc = tcc;
-  a.fx = fx ? fx + P.row0 : nullptr; a.fy = fy; a.alpha = alpha;
+  a.fx = fx ? fx + P.row0 : nullptr; a.fy = fy; a.alpha = alpha; a.beta = beta;
   PROF_BEGIN(c, pc_main);
 #define LAUNCH_MAIN(MODE, ST, OB)                                                                  \
   do {                                                                                             \
@@ -735,6 +735,17 @@ static gw_status grad_pass_k1(gw_ctx* c, const Prepared& P, int mode, const TSrc
         CU(cudaFuncSetAttribute(k_grad_store2<MODE, false, true>,                                     \
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, dsm));                   \
         k_grad_store2<MODE, false, true><<<grid, G2T, dsm, c->stream>>>(a, S2);                       \
+      }                                                                                               \
+    } else if (beta != 0.0) {                                                                         \
+      const int dsm = G2SUB * G2RS * (int)sizeof(float);                                              \
+      if (fx) {                                                                                       \
+        CU(cudaFuncSetAttribute(k_grad_store2<MODE, true, false, true>,                               \
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, dsm));                   \
+        k_grad_store2<MODE, true, false, true><<<grid, G2T, dsm, c->stream>>>(a, S2);                 \
+      } else {                                                                                        \
+        CU(cudaFuncSetAttribute(k_grad_store2<MODE, false, false, true>,                              \
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, dsm));                   \
+        k_grad_store2<MODE, false, false, true><<<grid, G2T, dsm, c->stream>>>(a, S2);                \
       }                                                                                               \
     } else if (fx) {                                                                                  \
       k_grad_store2<MODE, true><<<grid, G2T, 0, c->stream>>>(a, S2);                                  \
@@ -964,7 +975,10 @@ static gw_status grad_pass_gk(gw_ctx* c, const Prepared& P, int mode, const TSrc
 
 static gw_status grad_pass(gw_ctx* c, const Prepared& P, int mode, const TSrc& S, const TSrc2& S2, float* G,
                            int64_t ldG, bool store, bool obj, const double* fx, const double* fy, double alpha,
-                           double* objout_dev) {
+                           double* objout_dev, double beta = 0.0) {
+  if (beta != 0.0 && (P.grid2d || P.k != 1 || obj || !store))
+    return fail(GW_ERR_UNSUPPORTED, "tau != eps: only the k = 1 1-D gradient store carries the (eps - tau) ln T term");
+  if (beta != 0.0) return grad_pass_k1(c, P, mode, S, S2, G, ldG, store, obj, fx, fy, alpha, objout_dev, beta);
   if (P.grid2d) return grad_pass_2d(c, P, mode, S2, G, ldG, store, obj, fx, fy, alpha, objout_dev);
   if (P.k == 1) return grad_pass_k1(c, P, mode, S, S2, G, ldG, store, obj, fx, fy, alpha, objout_dev);
   if (P.k >= 3) {
@@ -1483,17 +1497,25 @@ static gw_status solve_impl(gw_ctx* c, const gw_problem* pb, const gw_solve_opts
                             double* g, gw_result* res, double* trace) {
   if (!c || !o || !res) return fail(GW_ERR_INVALID_ARG, "null ctx, opts or result");
   if (!(o->eps > 0)) return fail(GW_ERR_CONFIG, "eps must be > 0");
-  if (o->tau != o->eps && o->tau != 0)
-    return fail(GW_ERR_UNSUPPORTED, "tau != eps is not implemented (Remark 1, reading R6)");
+  // tau (0 means tau = eps, Remark 1): the Sinkhorn regulariser; tau != eps adds
+  // (eps - tau) ln T^l to the cost (k = 1, 1-D supports, T0 = p q^T)
+  const double tau = (o->tau == 0) ? o->eps : o->tau;
+  if (!(tau > 0)) return fail(GW_ERR_CONFIG, "tau must be > 0");
+  const bool tau_mode = tau != o->eps;
+  if (tau_mode && T0) return fail(GW_ERR_UNSUPPORTED, "tau != eps with an explicit T0 (ln T0) is not implemented");
   if (o->outer_iters < 0 || o->inner.max_iter < 0) return fail(GW_ERR_CONFIG, "iteration counts must be >= 0");
   if (!f || !g) return fail(GW_ERR_INVALID_ARG, "f and g (outputs) must be non-null");
   TRY(check_problem(pb));
   if (T0) TRY(check_matrix(T0, ldT, pb->m, "T0"));
   if (T_out) TRY(check_matrix(T_out, ldT, pb->m, "T_out"));
   CU(cudaSetDevice(c->device));
-  const double eps = o->eps;
+  const double eps = o->eps;  // the problem's regulariser (entropic objective E + eps H)
+  const double es = tau;      // the Sinkhorn regulariser (= eps unless tau != eps)
+  const double beta = tau_mode ? eps - tau : 0.0;
   Prepared P;
   TRY(prepare(c, pb, P));
+  if (tau_mode && (P.k != 1 || P.grid2d))
+    return fail(GW_ERR_UNSUPPORTED, "tau != eps: k = 1 on 1-D supports only");
   const int64_t nl = P.nl, m = P.m;
   const double* fx = nullptr;
   const double* fy = nullptr;
@@ -1559,18 +1581,23 @@ static gw_status solve_impl(gw_ctx* c, const gw_problem* pb, const gw_solve_opts
       }
     } else {
       mode = T_GIBBS;
-      k_scale<<<grid_for(nl), 256, 0, c->stream>>>(s.f, nl, GW_LOG2E / eps, Fs);
-      k_scale<<<grid_for(m), 256, 0, c->stream>>>(s.g, m, GW_LOG2E / eps, Gs2);
+      k_scale<<<grid_for(nl), 256, 0, c->stream>>>(s.f, nl, GW_LOG2E / es, Fs);
+      k_scale<<<grid_for(m), 256, 0, c->stream>>>(s.g, m, GW_LOG2E / es, Gs2);
       KCHECK();
-      S = TSrc{G, ldG, Fs, Gs2, GW_LOG2E / eps};
+      S = TSrc{G, ldG, Fs, Gs2, GW_LOG2E / es};
       // fp32 hi/lo split of the duals: the Sinkhorn state (fh, fl, gh, gl) is consistent with (f, g)
-      const double cc = GW_LOG2E / eps;
+      const double cc = GW_LOG2E / es;
       const float ch = (float)cc;
       S2 = TSrc2{G, ldG, s.fh, s.fl, s.gh, s.gl, ch, (float)(cc - (double)ch)};
     }
     const bool obj = (l > 0) && want_trace_obj;
     CU(cudaEventRecord(evs[2 * l], c->stream));
-    TRY(grad_pass(c, P, mode, S, S2, G, ldG, true, obj, fx, fy, alpha, objout));
+    if (tau_mode && obj) {  // objective of T^l first, then the cost over the buffer it reads
+      TRY(grad_pass(c, P, mode, S, S2, nullptr, 0, false, true, fx, fy, alpha, objout));
+      TRY(grad_pass(c, P, mode, S, S2, G, ldG, true, false, fx, fy, alpha, nullptr, beta));
+    } else {
+      TRY(grad_pass(c, P, mode, S, S2, G, ldG, true, obj, fx, fy, alpha, objout, beta));
+    }
     CU(cudaEventRecord(evs[2 * l + 1], c->stream));
     if (obj) {
       CU(cudaMemcpyAsync(c->hpin, objout, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -1580,9 +1607,9 @@ static gw_status solve_impl(gw_ctx* c, const gw_problem* pb, const gw_solve_opts
       tr[(size_t)(l - 1) * 4 + 1] = c->hpin[1];
     }
     // ---- Sinkhorn on G^{l+1} with warm-started duals ----
-    TRY(sink_split(c, P, s, eps));
+    TRY(sink_split(c, P, s, es));
     int used = 0, conv = 0;
-    TRY(sink_run(c, P, s, G, ldG, eps, o->inner.max_iter, o->inner.tol, o->inner.check_every, &used, &conv,
+    TRY(sink_run(c, P, s, G, ldG, es, o->inner.max_iter, o->inner.tol, o->inner.check_every, &used, &conv,
                  l == 0));
     inner_total += used;
     if (o->inner.tol > 0 && !conv) conv_all = 0;
@@ -1599,10 +1626,10 @@ static gw_status solve_impl(gw_ctx* c, const gw_problem* pb, const gw_solve_opts
       else { mode = T_PRODUCT; S = TSrc{nullptr, 0, P.pn + P.row0, P.qn, 0.0}; }
     } else {
       mode = T_GIBBS;
-      k_scale<<<grid_for(nl), 256, 0, c->stream>>>(s.f, nl, GW_LOG2E / eps, Fs);
-      k_scale<<<grid_for(m), 256, 0, c->stream>>>(s.g, m, GW_LOG2E / eps, Gs2);
+      k_scale<<<grid_for(nl), 256, 0, c->stream>>>(s.f, nl, GW_LOG2E / es, Fs);
+      k_scale<<<grid_for(m), 256, 0, c->stream>>>(s.g, m, GW_LOG2E / es, Gs2);
       KCHECK();
-      S = TSrc{G, ldG, Fs, Gs2, GW_LOG2E / eps};
+      S = TSrc{G, ldG, Fs, Gs2, GW_LOG2E / es};
     }
     TSrc2 S2{};
     if (mode == T_EXPLICIT) {
@@ -1610,7 +1637,7 @@ static gw_status solve_impl(gw_ctx* c, const gw_problem* pb, const gw_solve_opts
     } else if (mode == T_PRODUCT) {
       S2 = TSrc2{nullptr, 0, P.pnf + P.row0, nullptr, P.qnf, nullptr, 0.f, 0.f};
     } else {
-      const double cc = GW_LOG2E / eps;
+      const double cc = GW_LOG2E / es;
       const float ch = (float)cc;
       S2 = TSrc2{G, ldG, s.fh, s.fl, s.gh, s.gl, ch, (float)(cc - (double)ch)};
     }

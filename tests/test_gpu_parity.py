@@ -441,3 +441,32 @@ def test_k6_unsupported(gw):
         with pytest.raises(GwError) as e:
             gw.grad(x, x, p, p, T, k=k)
         assert e.value.code == "GW_ERR_UNSUPPORTED"
+
+
+# ----------------------------------------------------------------------------- tau != eps (Remark 1)
+
+@pytest.mark.parametrize("tau_ratio", [0.5, 2.0])
+def test_solver_general_tau(gw, tau_ratio):
+    """PAPER.md:102-110 with tau != eps: cost grad E + (eps - tau) ln T^l at regulariser tau, vs
+    oracle.entropic_gw(tau=...) (pinned against the KL-proximal step)."""
+    P = _c5_small(400, 300, 5, 100)
+    tau = tau_ratio * P.eps
+    r = gw.solve(P.x, P.y, P.p, P.q, P.eps, P.outer, P.inner, trace_objective=True, device=_dev(), tau=tau)
+    ro = O.entropic_gw(P.x, P.y, P.p, P.q, P.eps, P.outer, P.inner, tau=tau)
+    E = np.asarray(ro["E"])
+    assert np.max(np.abs(r.trace[:, 0] - E) / np.abs(E)) <= OBJ_TOL
+    assert abs(r.gw_objective - ro["gw_objective"]) <= OBJ_TOL * abs(ro["gw_objective"])
+    assert abs(r.entropic_objective - ro["entropic_objective"]) <= OBJ_TOL * abs(ro["entropic_objective"])
+    assert r.marginal_violation <= max(VIOL_TOL, 2 * ro["viol"][-1])
+
+
+def test_general_tau_fgw_and_unsupported(gw):
+    from paper_2404_08970_b200 import GwError
+    P = _c5_small(300, 256, 3, 60)
+    r = gw.solve(P.x, P.y, P.p, P.q, P.eps, P.outer, P.inner, fx=P.fx, fy=P.fy, alpha=0.5, device=_dev(),
+                 tau=0.5 * P.eps)
+    ro = O.entropic_fgw(P.x, P.y, P.p, P.q, P.fx, P.fy, 0.5, P.eps, P.outer, P.inner, tau=0.5 * P.eps)
+    assert abs(r.gw_objective - ro["gw_objective"]) <= OBJ_TOL * abs(ro["gw_objective"])
+    with pytest.raises(GwError) as e:
+        gw.solve(P.x, P.y, P.p, P.q, P.eps, 2, 10, device=_dev(), tau=0.5 * P.eps, k=2)
+    assert e.value.code == "GW_ERR_UNSUPPORTED"

@@ -495,3 +495,45 @@ def test_fgw_2d_bruteforce_and_reductions():
     r1 = O.entropic_fgw_2d(sx, sy, p, q, fx, fy, 1.0, 0.05, 2, 30)
     r2 = O.entropic_gw_2d(sx, sy, p, q, 0.05, 2, 30)
     np.testing.assert_allclose(r1["E"], r2["E"], rtol=1e-12)
+
+
+def test_mirror_descent_general_tau_is_the_kl_proximal_step():
+    """with tau != eps the oracle's step solves the cost Pi = G + (eps - tau) ln T^l at
+    regulariser tau; that must equal the KL-proximal step argmin <grad E + eps grad H(T^l), T> +
+    tau KL(T|T^l) over S(p,q), minimised directly (scipy, tiny instance)."""
+    from scipy.optimize import minimize
+    rng = np.random.default_rng(21)
+    n, m = 3, 4
+    x, y = np.sort(rng.random(n)), np.sort(rng.random(m))
+    p, q = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))
+    eps, tau = 0.08, 0.03
+    r1 = O.entropic_gw(x, y, p, q, eps, 1, 4000, tau=tau)
+    Tl = np.outer(p, q)
+    G = O.grad_prescribed(x, y, p, q, Tl)
+    C = G + eps * np.log(Tl)  # grad E + eps grad H(T^l)
+
+    # parametrise S(p, q) feasibly: T = T^l + B z with B spanning {sum rows = sum cols = 0}
+    basis = []
+    for i in range(n - 1):
+        for j in range(m - 1):
+            Bm = np.zeros((n, m))
+            Bm[i, j], Bm[i, m - 1], Bm[n - 1, j], Bm[n - 1, m - 1] = 1, -1, -1, 1
+            basis.append(Bm)
+    basis = np.array(basis)
+
+    def obj(z):
+        T = Tl + np.tensordot(z, basis, 1)
+        if np.any(T <= 0):
+            return 1e9, np.zeros_like(z)
+        val = np.sum(C * T) + tau * np.sum(T * np.log(T / Tl) - T + Tl)
+        dT = C + tau * np.log(T / Tl)
+        return val, np.tensordot(basis, dT, ([1, 2], [0, 1]))
+
+    r = minimize(obj, np.zeros(len(basis)), jac=True, method="L-BFGS-B",
+                 options={"ftol": 1e-15, "gtol": 1e-12, "maxiter": 5000})
+    Tp = Tl + np.tensordot(r.x, basis, 1)
+    np.testing.assert_allclose(r1["T"], Tp, atol=1e-8)
+    # tau = eps is the default path exactly
+    a = O.entropic_gw(x, y, p, q, eps, 3, 50)
+    b = O.entropic_gw(x, y, p, q, eps, 3, 50, tau=eps)
+    np.testing.assert_array_equal(a["T"], b["T"])
