@@ -61,6 +61,9 @@ def main():
     T64 = T32.double()
     ms64, Gref = timed(lambda: 2.0 * (c1[:, None] + c2[None, :]) - 4.0 * (DX @ T64 @ DY), reps=2)
     scale = Gref.abs().max().item()
+    print("diag: Gref finite %s max %r c1 max %r T max %r sum %r" % (
+        bool(torch.isfinite(Gref).all().item()), scale, c1.abs().max().item(), T32.max().item(),
+        T32.double().sum().item()), file=sys.stderr, flush=True)
     # tie the GPU fp64 reference to the CPU oracle on sampled rows: rows of D_X T D_Y by a
     # float64 NumPy product of the sampled rows of D_X with T, then with D_Y
     rng = np.random.default_rng(0)
