@@ -571,7 +571,6 @@ static gw_status prepare(gw_ctx* c, const gw_problem* pb, Prepared& P) {
   P.ylast = ends[3] - h[14];
   P.R = nranks_of(c);
   P.rank = c->comm ? c->comm->rank : 0;
-  if (P.k >= 3 && P.R > 1) return fail(GW_ERR_UNSUPPORTED, "k >= 3: row sharding is not implemented");
   P.tab.assign(2 * (size_t)P.R, 0);
   if (P.R > 1) {
     int64_t* dt;
@@ -904,11 +903,11 @@ template <int K, int MODE, bool STORE, bool OBJ, bool FGW>
 static gw_status gk_main_launch(gw_ctx* c, dim3 grid, const TSrc2& S2, int64_t nl, int64_t m, const double* xl,
                                 const double* yc, const double* rp, const double* rt, const double* Z,
                                 const double* ct, const double* cl, const double* c2, double alpha, const double* fx,
-                                const double* fy, float* G, int64_t ldG, double* tob) {
+                                const double* fy, float* G, int64_t ldG, double* tob, const double* carry) {
   auto kern = k_gk_main<K, MODE, STORE, OBJ, FGW>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gk_smem_bytes()));
   kern<<<grid, GK, gk_smem_bytes(), c->stream>>>(S2, nl, m, xl, yc, rp, rt, Z, ct, cl, c2, alpha, fx, fy, G, ldG,
-                                                    tob);
+                                                    tob, carry);
   KCHECK();
   return GW_OK;
 }
@@ -939,25 +938,51 @@ static gw_status grad_pass_gk_mode(gw_ctx* c, const Prepared& P, const TSrc2& S2
   KCHECK();
   k_gk_scan_tiles<<<grid_for((int64_t)K1 * m), 256, 0, c->stream>>>(Z, ntr, (int64_t)K1 * m, ct);
   KCHECK();
+  // multi-rank: the column sums of W over the rows of the ranks above (carry) and over all rows
+  // (ct, replaced by the global totals): one all-gather of (k+1) M fp64 per rank
+  double* carry = nullptr;
+  if (P.R > 1) {
+    double *g, *tot;
+    TRY(ws(c, c->xg1, K1 * (size_t)m * (P.R + 2), &g));
+    carry = g + K1 * (size_t)m * P.R;
+    tot = carry + K1 * (size_t)m;
+    TRY(comm_allgather(c, ct, g, sizeof(double) * K1 * (size_t)m));
+    k_gk_ranks<<<grid_for((int64_t)K1 * m), 256, 0, c->stream>>>(g, P.R, P.rank, (int64_t)K1 * m, carry, tot);
+    KCHECK();
+    ct = tot;
+  }
   PROF_END(c, PC_GRAD_CARRY, 3);
   const double* cl = P.cx + P.row0;
   if (obj) {
     TRY((gk_main_launch<K, MODE, false, true, false>(c, grid, S2, nl, m, xl, P.yc, rp, rt, Z, ct, cl, P.cy, 1.0,
-                                                     nullptr, nullptr, nullptr, 0, tob)));
-    // realised marginals: a = T 1 (row totals, power 0), b = T^T 1 (column totals of the plan)
+                                                     nullptr, nullptr, nullptr, 0, tob, carry)));
+    // realised marginals: a = T 1 (row totals, power 0; this rank's rows), b = T^T 1 (column
+    // totals of the plan over every rank: gathered and summed in rank order)
     k_gk_scan_tiles<<<grid_for((int64_t)K1 * m), 256, 0, c->stream>>>(cp, ntr, (int64_t)K1 * m, ctt);
     KCHECK();
-    k_gk_objective<K><<<1, 1024, 0, c->stream>>>(rt, xl, nl, ctt, P.yc, m, tob, (int64_t)ntc * ntr, objout_dev);
+    double *part, *gpart, *bg;
+    TRY(ws(c, c->xpart, (size_t)(2 * K + 2) * (P.R + 1), &part));
+    gpart = part + (2 * K + 2);
+    k_gk_obj_partial<K><<<1, 1024, 0, c->stream>>>(rt, xl, nl, tob, (int64_t)ntc * ntr, part);
+    KCHECK();
+    TRY(comm_allgather(c, part, gpart, sizeof(double) * (2 * K + 2)));
+    if (P.R > 1) {
+      TRY(ws(c, c->xg2, (size_t)m * P.R, &bg));
+      TRY(comm_allgather(c, ctt, bg, sizeof(double) * (size_t)m));  // power-0 row of ctt
+    } else {
+      bg = ctt;
+    }
+    k_gk_obj_final<K><<<1, 1024, 0, c->stream>>>(gpart, P.R, bg, P.yc, m, objout_dev);
     KCHECK();
   }
   if (store) {
     PROF_BEGIN(c, PC_GRAD_MAIN);
     if (fx)
-      TRY((gk_main_launch<K, MODE, true, false, true>(c, grid, S2, nl, m, xl, P.yc, rp, rt, Z, ct, cl, P.cy, alpha, fx,
-                                                      fy, G, ldG, nullptr)));
+      TRY((gk_main_launch<K, MODE, true, false, true>(c, grid, S2, nl, m, xl, P.yc, rp, rt, Z, ct, cl, P.cy, alpha,
+                                                      fx + P.row0, fy, G, ldG, nullptr, carry)));
     else
       TRY((gk_main_launch<K, MODE, true, false, false>(c, grid, S2, nl, m, xl, P.yc, rp, rt, Z, ct, cl, P.cy, alpha,
-                                                       nullptr, nullptr, G, ldG, nullptr)));
+                                                       nullptr, nullptr, G, ldG, nullptr, carry)));
     PROF_END(c, PC_GRAD_MAIN, 1);
   }
   return GW_OK;

@@ -295,7 +295,8 @@ __global__ void __launch_bounds__(256) k_gk_apply(const double* __restrict__ U, 
 // and / or the tile's <D_X T D_Y, T> (OBJ -> tile_obj[tile]).
 //   rowpre[tx][r][i], rowtot[r][i]: power sums of row i over the columns before tile tx / all columns
 //   colpre[ty][r][q], coltot[r][q]: power sums (weights x^r) of column q of W = T D_Y over the rows
-//                                   before row tile ty / all rows
+//                                   before row tile ty (this rank) / all rows (all ranks)
+//   colcarry[r][q] (nullable): the same sums over the rows of the ranks above
 template <int K, int MODE, bool STORE, bool OBJ, bool FGW>
 __global__ void __launch_bounds__(GK) k_gk_main(TSrc2 S, int64_t nl, int64_t m, const double* __restrict__ xl,
                                                 const double* __restrict__ yc, const double* __restrict__ rowpre,
@@ -303,7 +304,8 @@ __global__ void __launch_bounds__(GK) k_gk_main(TSrc2 S, int64_t nl, int64_t m, 
                                                 const double* __restrict__ coltot, const double* __restrict__ cl,
                                                 const double* __restrict__ c2, double alpha,
                                                 const double* __restrict__ fx, const double* __restrict__ fy,
-                                                float* __restrict__ G, int64_t ldG, double* __restrict__ tile_obj) {
+                                                float* __restrict__ G, int64_t ldG, double* __restrict__ tile_obj,
+                                                const double* __restrict__ colcarry) {
   extern __shared__ float4 gk_smem[];
   float* tile = reinterpret_cast<float*>(gk_smem);          // [GK][GKQ]
   double* xs = reinterpret_cast<double*>(tile + GK * GKQ);  // x of the tile's rows
@@ -350,7 +352,9 @@ __global__ void __launch_bounds__(GK) k_gk_main(TSrc2 S, int64_t nl, int64_t m, 
 #pragma unroll
     for (int r = 0; r <= K; ++r) {
       const double tt = coltot[(int64_t)r * m + q];
-      h[r] = gk_kappa<K>(r) * (ODD ? 2.0 * colpre[((int64_t)blockIdx.y * (K + 1) + r) * m + q] - tt : tt);
+      double pre = colpre[((int64_t)blockIdx.y * (K + 1) + r) * m + q];
+      if (colcarry) pre += colcarry[(int64_t)r * m + q];  // rows of the ranks above
+      h[r] = gk_kappa<K>(r) * (ODD ? 2.0 * pre - tt : tt);
     }
     const double c2q = 2.0 * alpha * c2[q];
     const double fyq = FGW ? fy[q] : 0.0;
@@ -418,20 +422,18 @@ __global__ void __launch_bounds__(1024) k_gk_const(const double* __restrict__ s,
   }
 }
 
-// E(T) = a^T (D_X o D_X) a + b^T (D_Y o D_Y) b - 2 <D_X T D_Y, T>  with a = T1, b = T^T 1 (realised)
-// -> out[0].  The power-2K quadratic forms by moments: sum_r C(P,r) (-1)^r mu_r mu_{P-r}.
+// E(T) = a^T (D_X o D_X) a + b^T (D_Y o D_Y) b - 2 <D_X T D_Y, T>  with a = T1, b = T^T 1 (realised).
+// The power-2K quadratic forms by moments: sum_r C(P,r) (-1)^r mu_r mu_{P-r}.
+// Partial (per rank): part = {mu_0(a) .. mu_P(a) over this rank's rows, sum of the tile <V, T> sums}.
 template <int K>
-__global__ void __launch_bounds__(1024) k_gk_objective(const double* __restrict__ a, const double* __restrict__ xl,
-                                                       int64_t nl, const double* __restrict__ b,
-                                                       const double* __restrict__ yc, int64_t m,
-                                                       const double* __restrict__ tile_obj, int64_t ntile,
-                                                       double* __restrict__ out) {
+__global__ void __launch_bounds__(1024) k_gk_obj_partial(const double* __restrict__ a, const double* __restrict__ xl,
+                                                         int64_t nl, const double* __restrict__ tile_obj,
+                                                         int64_t ntile, double* __restrict__ part) {
   constexpr int P = 2 * K;
   __shared__ double sm[32];
-  __shared__ double mua[P + 1], mub[P + 1];
-  double ua[P + 1], ub[P + 1];
+  double ua[P + 1];
 #pragma unroll
-  for (int r = 0; r <= P; ++r) ua[r] = ub[r] = 0.0;
+  for (int r = 0; r <= P; ++r) ua[r] = 0.0;
   for (int64_t i = threadIdx.x; i < nl; i += blockDim.x) {
     double v = a[i];
     const double x = xl[i];
@@ -441,8 +443,32 @@ __global__ void __launch_bounds__(1024) k_gk_objective(const double* __restrict_
       v *= x;
     }
   }
+  double go = 0.0;
+  for (int64_t i = threadIdx.x; i < ntile; i += blockDim.x) go += tile_obj[i];
+#pragma unroll
+  for (int r = 0; r <= P; ++r) {
+    const double v = block_sum<32>(ua[r], sm);
+    if (threadIdx.x == 0) part[r] = v;
+  }
+  go = block_sum<32>(go, sm);
+  if (threadIdx.x == 0) part[P + 1] = go;
+}
+
+// Final: the R ranks' partials (gathered [R][P + 2]) summed in rank order; b = T^T 1 over all
+// rows (bparts [R][m], summed in rank order) -> out[0] = E.
+template <int K>
+__global__ void __launch_bounds__(1024) k_gk_obj_final(const double* __restrict__ parts, int R,
+                                                       const double* __restrict__ bparts, const double* __restrict__ yc,
+                                                       int64_t m, double* __restrict__ out) {
+  constexpr int P = 2 * K;
+  __shared__ double sm[32];
+  __shared__ double mub[P + 1];
+  double ub[P + 1];
+#pragma unroll
+  for (int r = 0; r <= P; ++r) ub[r] = 0.0;
   for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
-    double v = b[i];
+    double v = 0.0;
+    for (int rk = 0; rk < R; ++rk) v += bparts[(int64_t)rk * m + i];
     const double y = yc[i];
 #pragma unroll
     for (int r = 0; r <= P; ++r) {
@@ -450,17 +476,19 @@ __global__ void __launch_bounds__(1024) k_gk_objective(const double* __restrict_
       v *= y;
     }
   }
-  double go = 0.0;
-  for (int64_t i = threadIdx.x; i < ntile; i += blockDim.x) go += tile_obj[i];
 #pragma unroll
   for (int r = 0; r <= P; ++r) {
-    const double va = block_sum<32>(ua[r], sm);
-    const double vb = block_sum<32>(ub[r], sm);
-    if (threadIdx.x == 0) { mua[r] = va; mub[r] = vb; }
+    const double v = block_sum<32>(ub[r], sm);
+    if (threadIdx.x == 0) mub[r] = v;
   }
-  go = block_sum<32>(go, sm);
   __syncthreads();
   if (threadIdx.x == 0) {
+    double mua[P + 1], go = 0.0;
+    for (int r = 0; r <= P; ++r) mua[r] = 0.0;
+    for (int rk = 0; rk < R; ++rk) {
+      for (int r = 0; r <= P; ++r) mua[r] += parts[(int64_t)rk * (P + 2) + r];
+      go += parts[(int64_t)rk * (P + 2) + P + 1];
+    }
     double Ea = 0.0, Eb = 0.0;
     for (int r = 0; r <= P; ++r) {
       const double cf = ((r & 1) ? -1.0 : 1.0) * gk_binom(P, r);
@@ -468,6 +496,22 @@ __global__ void __launch_bounds__(1024) k_gk_objective(const double* __restrict_
       Eb += cf * mub[r] * mub[P - r];
     }
     out[0] = Ea + Eb - 2.0 * go;
+  }
+}
+
+// Multi-rank column carries: g = [R][len] (each rank's column totals); carry = sum over the ranks
+// before `rank`, tot = sum over all (rank order).
+__global__ void k_gk_ranks(const double* __restrict__ g, int R, int rank, int64_t len, double* __restrict__ carry,
+                           double* __restrict__ tot) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < len; e += (int64_t)gridDim.x * blockDim.x) {
+    double c = 0.0, t = 0.0;
+    for (int r = 0; r < R; ++r) {
+      const double v = g[(int64_t)r * len + e];
+      if (r < rank) c += v;
+      t += v;
+    }
+    carry[e] = c;
+    tot[e] = t;
   }
 }
 

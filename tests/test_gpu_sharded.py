@@ -168,3 +168,53 @@ def test_sharded_k2_solve(gw):
     out = _run_ranks(3, fn)
     assert out[0] == out[1] == out[2]
     assert abs(out[0] - r1.gw_objective) <= 1e-6 * abs(r1.gw_objective)
+
+
+@pytest.mark.parametrize("k", [3, 4])
+def test_sharded_kgen_grad(gw, k):
+    """k >= 3 sharded: the column power sums of the ranks above arrive by one all-gather."""
+    import torch
+    api, dist = gw
+    rng = np.random.default_rng(40 + k)
+    n, m = 700, 390
+    x, y = np.sort(rng.random(n)), np.sort(rng.random(m))
+    p, q = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))
+    Tn = (rng.random((n, m)) / (n * m)).astype(np.float32)
+    dev = torch.device("cuda", 0)
+    T = api.plan_buffer(n, m, dev)
+    T.copy_(torch.from_numpy(Tn))
+    G1 = api.grad(x, y, p, q, T, k=k).cpu().numpy().astype(np.float64)
+
+    def fn(r, ctx, st):
+        r0, nl = dist.shard_rows(n, 3, r)
+        return r0, api.grad(x, y, p, q, T[r0:r0 + nl], ctx=ctx, row0=r0, k=k).cpu().numpy().astype(np.float64)
+
+    parts = _run_ranks(3, fn)
+    Gs = np.concatenate([g for _, g in sorted(parts, key=lambda t: t[0])])
+    Go = O.grad_prescribed(x, y, p, q, Tn.astype(np.float64), k=k)
+    scale = np.max(np.abs(Go))
+    assert np.max(np.abs(Gs - G1)) <= 2e-6 * scale
+    assert np.max(np.abs(Gs - Go)) <= 1e-5 * scale
+
+
+def test_sharded_k3_solve_and_fgw(gw):
+    api, dist = gw
+    P = _c5(300, 260, 4, 60)
+    r1 = api.solve(P.x, P.y, P.p, P.q, P.eps, P.outer, P.inner, k=3, trace_objective=True)
+    f1 = api.solve(P.x, P.y, P.p, P.q, P.eps, P.outer, P.inner, k=3, fx=P.fx, fy=P.fy, alpha=0.5)
+
+    def fn(r, ctx, st):
+        r0, nl = dist.shard_rows(P.x.size, 2, r)
+        a = api.solve(P.x, P.y, P.p, P.q, P.eps, P.outer, P.inner, ctx=ctx, row0=r0, n_local=nl, device=ctx.device,
+                      k=3, trace_objective=True)
+        b = api.solve(P.x, P.y, P.p, P.q, P.eps, P.outer, P.inner, ctx=ctx, row0=r0, n_local=nl, device=ctx.device,
+                      k=3, fx=P.fx, fy=P.fy, alpha=0.5)
+        return a.gw_objective, a.trace[:, 0].copy(), b.gw_objective
+
+    out = _run_ranks(2, fn)
+    assert out[0][0] == out[1][0] and out[0][2] == out[1][2]
+    assert abs(out[0][0] - r1.gw_objective) <= 1e-6 * abs(r1.gw_objective)
+    np.testing.assert_allclose(out[0][1], r1.trace[:, 0], rtol=1e-6)
+    assert abs(out[0][2] - f1.gw_objective) <= 1e-6 * abs(f1.gw_objective)
+    ro = O.entropic_gw(P.x, P.y, P.p, P.q, P.eps, P.outer, P.inner, k=3)
+    assert abs(out[0][0] - ro["gw_objective"]) <= 1e-4 * abs(ro["gw_objective"])
