@@ -202,9 +202,11 @@ __global__ void __launch_bounds__(G2D_MAXN) k_g2_rowred(TSrc2 S, int ny, double*
   }
 }
 
-// T^AC[a][c] = sum_b RC[(a,b)][c], T^BC[b][c] = sum_a RC, T^AD[a][d] = sum_b RD, T^BD[b][d] = sum_a RD
-__global__ void k_g2_marg(const double* __restrict__ RC, const double* __restrict__ RD, int nx, int ny,
-                          double* __restrict__ TAC, double* __restrict__ TAD, double* __restrict__ TBC,
+// T^AC[a][c] = sum_b RC[(a,b)][c], T^BC[b][c] = sum_a RC, T^AD[a][d] = sum_b RD, T^BD[b][d] = sum_a RD,
+// over this rank's rows [row0, row0 + nl) (RC, RD hold those rows; the ranks' partial matrices are
+// all-gathered and summed in rank order).
+__global__ void k_g2_marg(const double* __restrict__ RC, const double* __restrict__ RD, int nx, int ny, int64_t row0,
+                          int64_t nl, double* __restrict__ TAC, double* __restrict__ TAD, double* __restrict__ TBC,
                           double* __restrict__ TBD) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= 4 * nx * ny) return;
@@ -212,10 +214,9 @@ __global__ void k_g2_marg(const double* __restrict__ RC, const double* __restric
   const int r = k / ny, col = k - r * ny;
   const double* src = (which == 0 || which == 2) ? RC : RD;
   double v = 0.0;
-  if (which < 2) {  // sum over b for fixed a = r
-    for (int b = 0; b < nx; ++b) v += src[((int64_t)r * nx + b) * ny + col];
-  } else {          // sum over a for fixed b = r
-    for (int a = 0; a < nx; ++a) v += src[((int64_t)a * nx + r) * ny + col];
+  for (int o = 0; o < nx; ++o) {  // which < 2: sum over b for fixed a = r; else over a for fixed b = r
+    const int64_t i = which < 2 ? (int64_t)r * nx + o : (int64_t)o * nx + r;
+    if (i >= row0 && i < row0 + nl) v += src[(i - row0) * ny + col];
   }
   double* dst = which == 0 ? TAC : which == 1 ? TAD : which == 2 ? TBC : TBD;
   dst[k] = v;

@@ -393,8 +393,6 @@ static gw_status check_problem(const gw_problem* pb) {
       return fail(GW_ERR_UNSUPPORTED, "GW_GRID2D: grid side %lld / %lld exceeds %d", (long long)nx, (long long)ny,
                   G2D_MAXN);
     if (pb->k != 1) return fail(GW_ERR_UNSUPPORTED, "GW_GRID2D: only k = 1 (Manhattan distance) is implemented");
-    if (pb->row0 != 0 || pb->n_local != pb->n)
-      return fail(GW_ERR_UNSUPPORTED, "GW_GRID2D: row sharding is not implemented");
   }
   if (pb->loss != GW_LOSS_SQUARE) return fail(GW_ERR_UNSUPPORTED, "only the square loss is defined (PAPER.md:86)");
   if (pb->dtype != GW_F32) return fail(GW_ERR_UNSUPPORTED, "only fp32 matrix storage in ABI v1");
@@ -434,11 +432,36 @@ static gw_status g2_sqconst(gw_ctx* c, const double* axis, int na, const double*
   return GW_OK;
 }
 
+// The ranks' (row0, n_local) table (one all-gather), checked; P.R, P.rank, P.tab, P.dtab, P.maxnl.
+static gw_status shard_table(gw_ctx* c, Prepared& P) {
+  P.R = nranks_of(c);
+  P.rank = c->comm ? c->comm->rank : 0;
+  P.tab.assign(2 * (size_t)P.R, 0);
+  if (P.R > 1) {
+    int64_t* dt;
+    TRY(ws(c, c->xtab, 2 * (size_t)P.R + 2, &dt));
+    const int64_t mine[2] = {P.row0, P.nl};
+    CU(cudaMemcpyAsync(dt + 2 * P.R, mine, sizeof(mine), cudaMemcpyHostToDevice, c->stream));
+    TRY(comm_allgather(c, dt + 2 * P.R, dt, 2 * sizeof(int64_t)));
+    CU(cudaMemcpyAsync(P.tab.data(), dt, 2 * sizeof(int64_t) * P.R, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    TRY(gw_check_shards(P.tab.data(), P.R, P.n));
+    for (int r = 0; r < P.R; ++r)
+      if (P.tab[2 * r + 1] == 0) return fail(GW_ERR_DIM_MISMATCH, "rank %d holds no rows (n >= nranks required)", r);
+    P.dtab = dt;
+    for (int r = 0; r < P.R; ++r) P.maxnl = std::max(P.maxnl, P.tab[2 * r + 1]);
+  } else {
+    P.tab[0] = P.row0;
+    P.tab[1] = P.nl;
+    P.maxnl = P.nl;
+  }
+  return GW_OK;
+}
+
 static gw_status prepare_2d(gw_ctx* c, const gw_problem* pb, Prepared& P) {
   const int64_t n = pb->n, m = pb->m;
   const int nx = (int)llround(sqrt((double)n)), ny = (int)llround(sqrt((double)m));
-  P.n = n; P.m = m; P.row0 = 0; P.nl = n; P.k = 1; P.grid2d = true; P.nx = nx; P.ny = ny;
-  if (nranks_of(c) > 1) return fail(GW_ERR_UNSUPPORTED, "GW_GRID2D: multi-rank is not implemented");
+  P.n = n; P.m = m; P.row0 = pb->row0; P.nl = pb->n_local; P.k = 1; P.grid2d = true; P.nx = nx; P.ny = ny;
   const bool host = pb->flags & GW_HOST_VECTORS;
   if (host) {
     double* st;
@@ -487,11 +510,7 @@ static gw_status prepare_2d(gw_ctx* c, const gw_problem* pb, Prepared& P) {
   k_to_float<<<grid_for(m), 256, 0, c->stream>>>(qn, m, P.qnf);
   KCHECK();
   P.xlast = P.ylast = 0.0;
-  P.R = 1; P.rank = 0;
-  P.tab.assign(2, 0);
-  P.tab[1] = n;
-  P.maxnl = n;
-  return GW_OK;
+  return shard_table(c, P);
 }
 
 static gw_status prepare(gw_ctx* c, const gw_problem* pb, Prepared& P) {
@@ -569,28 +588,7 @@ static gw_status prepare(gw_ctx* c, const gw_problem* pb, Prepared& P) {
   CU(cudaStreamSynchronize(c->stream));
   P.xlast = ends[1] - h[6];
   P.ylast = ends[3] - h[14];
-  P.R = nranks_of(c);
-  P.rank = c->comm ? c->comm->rank : 0;
-  P.tab.assign(2 * (size_t)P.R, 0);
-  if (P.R > 1) {
-    int64_t* dt;
-    TRY(ws(c, c->xtab, 2 * (size_t)P.R + 2, &dt));
-    const int64_t mine[2] = {P.row0, P.nl};
-    CU(cudaMemcpyAsync(dt + 2 * P.R, mine, sizeof(mine), cudaMemcpyHostToDevice, c->stream));
-    TRY(comm_allgather(c, dt + 2 * P.R, dt, 2 * sizeof(int64_t)));
-    CU(cudaMemcpyAsync(P.tab.data(), dt, 2 * sizeof(int64_t) * P.R, cudaMemcpyDeviceToHost, c->stream));
-    CU(cudaStreamSynchronize(c->stream));
-    TRY(gw_check_shards(P.tab.data(), P.R, n));
-    for (int r = 0; r < P.R; ++r)
-      if (P.tab[2 * r + 1] == 0) return fail(GW_ERR_DIM_MISMATCH, "rank %d holds no rows (n >= nranks required)", r);
-    P.dtab = dt;
-    for (int r = 0; r < P.R; ++r) P.maxnl = std::max(P.maxnl, P.tab[2 * r + 1]);
-  } else {
-    P.tab[0] = P.row0;
-    P.tab[1] = P.nl;
-    P.maxnl = P.nl;
-  }
-  return GW_OK;
+  return shard_table(c, P);
 }
 
 // ------------------------------------------------------------------------------ gradient
@@ -830,32 +828,45 @@ static gw_status grad_pass_2d(gw_ctx* c, const Prepared& P, int mode, const TSrc
                               bool store, bool obj, const double* fx, const double* fy, double alpha,
                               double* objout_dev) {
   const int nx = P.nx, ny = P.ny;
-  const int64_t n = P.n, m = P.m;
+  const int64_t n = P.n, m = P.m, nl = P.nl;
   const int nn = nx * ny;
   double *RC, *RD, *Hr, *CCr, *TT, *VT, *tmp;
-  TRY(ws(c, c->g2rc, (size_t)n * ny, &RC)); TRY(ws(c, c->g2rd, (size_t)n * ny, &RD));
-  TRY(ws(c, c->g2h, n, &Hr)); TRY(ws(c, c->g2cc, n, &CCr));
+  TRY(ws(c, c->g2rc, (size_t)std::max<int64_t>(nl, 1) * ny, &RC));
+  TRY(ws(c, c->g2rd, (size_t)std::max<int64_t>(nl, 1) * ny, &RD));
+  TRY(ws(c, c->g2h, (size_t)std::max<int64_t>(nl, 1), &Hr)); TRY(ws(c, c->g2cc, (size_t)std::max<int64_t>(nl, 1), &CCr));
   TRY(ws(c, c->g2tt, 4 * (size_t)nn, &TT)); TRY(ws(c, c->g2vt, 4 * (size_t)nn, &VT));
   TRY(ws(c, c->g2tmp, (size_t)nn, &tmp));
   const int bt = (ny + 31) / 32 * 32;
+  const double* fxl = fx ? fx + P.row0 : nullptr;
   PROF_BEGIN(c, PC_GRAD_MOMENTS);
 #define LAUNCH_RR(MODE, OB)                                                                                   \
-  k_g2_rowred<MODE, OB><<<(unsigned)n, bt, 0, c->stream>>>(S2, ny, RC, RD, Hr, OB ? fx : nullptr, fy, CCr)
-  if (obj) {
-    if (mode == T_EXPLICIT) LAUNCH_RR(T_EXPLICIT, true);
-    else if (mode == T_GIBBS) LAUNCH_RR(T_GIBBS, true);
-    else LAUNCH_RR(T_PRODUCT, true);
-  } else {
-    if (mode == T_EXPLICIT) LAUNCH_RR(T_EXPLICIT, false);
-    else if (mode == T_GIBBS) LAUNCH_RR(T_GIBBS, false);
-    else LAUNCH_RR(T_PRODUCT, false);
+  k_g2_rowred<MODE, OB><<<(unsigned)nl, bt, 0, c->stream>>>(S2, ny, RC, RD, Hr, OB ? fxl : nullptr, fy, CCr)
+  if (nl > 0) {
+    if (obj) {
+      if (mode == T_EXPLICIT) LAUNCH_RR(T_EXPLICIT, true);
+      else if (mode == T_GIBBS) LAUNCH_RR(T_GIBBS, true);
+      else LAUNCH_RR(T_PRODUCT, true);
+    } else {
+      if (mode == T_EXPLICIT) LAUNCH_RR(T_EXPLICIT, false);
+      else if (mode == T_GIBBS) LAUNCH_RR(T_GIBBS, false);
+      else LAUNCH_RR(T_PRODUCT, false);
+    }
   }
 #undef LAUNCH_RR
   KCHECK();
   PROF_END(c, PC_GRAD_MOMENTS, obj ? 0 : 1);
   PROF_BEGIN(c, PC_GRAD_CARRY);
-  k_g2_marg<<<(4 * nn + 255) / 256, 256, 0, c->stream>>>(RC, RD, nx, ny, TT, TT + nn, TT + 2 * nn, TT + 3 * nn);
+  k_g2_marg<<<(4 * nn + 255) / 256, 256, 0, c->stream>>>(RC, RD, nx, ny, P.row0, nl, TT, TT + nn, TT + 2 * nn,
+                                                         TT + 3 * nn);
   KCHECK();
+  if (P.R > 1) {  // the four marginal matrices of the whole plan: partials summed in rank order
+    double* g;
+    TRY(ws(c, c->xg1, 4 * (size_t)nn * (P.R + 1), &g));
+    TRY(comm_allgather(c, TT, g, 4 * sizeof(double) * (size_t)nn));
+    k_gk_ranks<<<grid_for(4 * (int64_t)nn), 256, 0, c->stream>>>(g, P.R, P.rank, 4 * (int64_t)nn,
+                                                                 g + 4 * (size_t)nn * P.R, TT);
+    KCHECK();
+  }
   for (int k = 0; k < 4; ++k) {
     k_g2_mul_right<<<(nn + 255) / 256, 256, 0, c->stream>>>(TT + (size_t)k * nn, nx, ny, P.yc, tmp);
     KCHECK();
@@ -864,34 +875,63 @@ static gw_status grad_pass_2d(gw_ctx* c, const Prepared& P, int mode, const TSrc
   }
   PROF_END(c, PC_GRAD_CARRY, 4);
   if (obj) {
-    // realised marginals a = T 1 (from the row reductions), b = T^T 1 (column pass)
+    // realised marginals a = T 1 (from the row reductions), b = T^T 1 (column pass); with R > 1
+    // b's partials are summed and a, H, <C o C, T> per row are gathered into global vectors
     double *av, *bv, *cA, *cB, *part;
-    TRY(ws(c, c->g2a, n, &av)); TRY(ws(c, c->g2b, m, &bv));
-    TRY(ws(c, c->g2ca, n, &cA)); TRY(ws(c, c->g2cb, m, &cB));
-    const int nch = (int)((n + 255) / 256);
-    TRY(ws(c, c->g2part, (size_t)nch * m, &part));
-    k_g2_rowsum<<<grid_for(n), 256, 0, c->stream>>>(RC, n, ny, av);
+    TRY(ws(c, c->g2a, 3 * (size_t)n, &av)); TRY(ws(c, c->g2b, (size_t)m, &bv));
+    TRY(ws(c, c->g2ca, (size_t)n, &cA)); TRY(ws(c, c->g2cb, (size_t)m, &cB));
+    const int nch = (int)((nl + 255) / 256);
+    TRY(ws(c, c->g2part, (size_t)std::max(nch, 1) * m, &part));
+    double* al = av;  // this rank's rows (R == 1: the whole vector)
+    k_g2_rowsum<<<grid_for(nl), 256, 0, c->stream>>>(RC, nl, ny, al);
     KCHECK();
-    dim3 cg((unsigned)((m + 255) / 256), (unsigned)nch);
-    if (mode == T_EXPLICIT) k_g2_colsum<T_EXPLICIT><<<cg, 256, 0, c->stream>>>(S2, n, m, part);
-    else if (mode == T_GIBBS) k_g2_colsum<T_GIBBS><<<cg, 256, 0, c->stream>>>(S2, n, m, part);
-    else k_g2_colsum<T_PRODUCT><<<cg, 256, 0, c->stream>>>(S2, n, m, part);
-    KCHECK();
+    dim3 cg((unsigned)((m + 255) / 256), (unsigned)std::max(nch, 1));
+    if (nl > 0) {
+      if (mode == T_EXPLICIT) k_g2_colsum<T_EXPLICIT><<<cg, 256, 0, c->stream>>>(S2, nl, m, part);
+      else if (mode == T_GIBBS) k_g2_colsum<T_GIBBS><<<cg, 256, 0, c->stream>>>(S2, nl, m, part);
+      else k_g2_colsum<T_PRODUCT><<<cg, 256, 0, c->stream>>>(S2, nl, m, part);
+      KCHECK();
+    }
     k_g2_colsum_reduce<<<grid_for(m), 256, 0, c->stream>>>(part, nch, m, bv);
     KCHECK();
-    TRY(g2_sqconst(c, P.xc, nx, av, cA));
+    const double *aF = av, *HF = Hr, *CF = CCr;
+    if (P.R > 1) {
+      double *g, *pk;
+      const int64_t ml = P.maxnl;
+      TRY(ws(c, c->xg2, 3 * (size_t)ml * (P.R + 1), &g));
+      pk = g + 3 * (size_t)ml * P.R;
+      CU(cudaMemsetAsync(pk, 0, 3 * sizeof(double) * (size_t)ml, c->stream));
+      CU(cudaMemcpyAsync(pk, al, sizeof(double) * (size_t)nl, cudaMemcpyDeviceToDevice, c->stream));
+      CU(cudaMemcpyAsync(pk + ml, Hr, sizeof(double) * (size_t)nl, cudaMemcpyDeviceToDevice, c->stream));
+      if (fx) CU(cudaMemcpyAsync(pk + 2 * ml, CCr, sizeof(double) * (size_t)nl, cudaMemcpyDeviceToDevice, c->stream));
+      TRY(comm_allgather(c, pk, g, 3 * sizeof(double) * (size_t)ml));
+      double* full = av + n;  // [H | CC] after the first n entries of av's buffer
+      k_unpad<<<grid_for(ml), 256, 0, c->stream>>>(g, P.R, 3 * ml, P.dtab, av);
+      k_unpad<<<grid_for(ml), 256, 0, c->stream>>>(g + ml, P.R, 3 * ml, P.dtab, full);
+      k_unpad<<<grid_for(ml), 256, 0, c->stream>>>(g + 2 * ml, P.R, 3 * ml, P.dtab, full + n);
+      KCHECK();
+      HF = full;
+      CF = full + n;
+      // b: the ranks' column sums in rank order
+      double* gb;
+      TRY(ws(c, c->xvec, (size_t)m * (P.R + 1), &gb));
+      TRY(comm_allgather(c, bv, gb, sizeof(double) * (size_t)m));
+      k_gk_ranks<<<grid_for(m), 256, 0, c->stream>>>(gb, P.R, P.rank, m, gb + (size_t)m * P.R, bv);
+      KCHECK();
+    }
+    TRY(g2_sqconst(c, P.xc, nx, aF, cA));
     TRY(g2_sqconst(c, P.yc, ny, bv, cB));
-    k_g2_objective<<<1, 1024, 0, c->stream>>>(av, cA, P.pn, n, bv, cB, P.qn, m, VT, TT, 4 * nn, Hr,
-                                              fx ? CCr : nullptr, objout_dev);
+    k_g2_objective<<<1, 1024, 0, c->stream>>>(aF, cA, P.pn, n, bv, cB, P.qn, m, VT, TT, 4 * nn, HF,
+                                              fx ? CF : nullptr, objout_dev);
     KCHECK();
   }
-  if (store) {
+  if (store && nl > 0) {
     PROF_BEGIN(c, PC_GRAD_MAIN);
-    const dim3 sg((unsigned)((m + 256 * G2SC - 1) / (256 * G2SC)), (unsigned)((n + G2SR - 1) / G2SR));
-    if (fx) k_g2_store<true><<<sg, 256, 0, c->stream>>>(P.cx, P.cy, VT, VT + nn, VT + 2 * nn, VT + 3 * nn, nx, ny, 0, n,
-                                                       m, alpha, fx, fy, G, ldG);
-    else k_g2_store<false><<<sg, 256, 0, c->stream>>>(P.cx, P.cy, VT, VT + nn, VT + 2 * nn, VT + 3 * nn, nx, ny, 0, n,
-                                                     m, alpha, nullptr, nullptr, G, ldG);
+    const dim3 sg((unsigned)((m + 256 * G2SC - 1) / (256 * G2SC)), (unsigned)((nl + G2SR - 1) / G2SR));
+    if (fx) k_g2_store<true><<<sg, 256, 0, c->stream>>>(P.cx, P.cy, VT, VT + nn, VT + 2 * nn, VT + 3 * nn, nx, ny,
+                                                       P.row0, nl, m, alpha, fx, fy, G, ldG);
+    else k_g2_store<false><<<sg, 256, 0, c->stream>>>(P.cx, P.cy, VT, VT + nn, VT + 2 * nn, VT + 3 * nn, nx, ny,
+                                                     P.row0, nl, m, alpha, nullptr, nullptr, G, ldG);
     KCHECK();
     PROF_END(c, PC_GRAD_MAIN, 1);
   }

@@ -218,3 +218,45 @@ def test_sharded_k3_solve_and_fgw(gw):
     assert abs(out[0][2] - f1.gw_objective) <= 1e-6 * abs(f1.gw_objective)
     ro = O.entropic_gw(P.x, P.y, P.p, P.q, P.eps, P.outer, P.inner, k=3)
     assert abs(out[0][0] - ro["gw_objective"]) <= 1e-4 * abs(ro["gw_objective"])
+
+
+def test_sharded_grid2d_grad_and_solve(gw):
+    """2-D grids sharded by rows: the four marginal matrices' partials are all-gathered."""
+    import torch
+    api, dist = gw
+    rng = np.random.default_rng(77)
+    nx, ny = 13, 11
+    n, m = nx * nx, ny * ny
+    sx, sy = np.sort(rng.random(nx)), np.arange(ny) / (ny - 1.0)
+    p, q = rng.random(n) + 0.05, rng.random(m) + 0.05
+    p, q = p / p.sum(), q / q.sum()
+    Tn = (rng.random((n, m)) / (n * m)).astype(np.float32)
+    dev = torch.device("cuda", 0)
+    T = api.plan_buffer(n, m, dev)
+    T.copy_(torch.from_numpy(Tn))
+    G1 = api.grad(sx, sy, p, q, T, grid2d=True).cpu().numpy().astype(np.float64)
+    r1 = api.solve(sx, sy, p, q, 0.02, 4, 80, grid2d=True, trace_objective=True)
+    fx, fy = rng.random(n), rng.random(m)
+    f1 = api.solve(sx, sy, p, q, 0.02, 3, 60, grid2d=True, fx=fx, fy=fy, alpha=0.5)
+
+    def fn(r, ctx, st):
+        r0, nl = dist.shard_rows(n, 3, r)
+        g = api.grad(sx, sy, p, q, T[r0:r0 + nl], ctx=ctx, row0=r0, grid2d=True).cpu().numpy().astype(np.float64)
+        a = api.solve(sx, sy, p, q, 0.02, 4, 80, ctx=ctx, row0=r0, n_local=nl, device=ctx.device, grid2d=True,
+                      trace_objective=True)
+        b = api.solve(sx, sy, p, q, 0.02, 3, 60, ctx=ctx, row0=r0, n_local=nl, device=ctx.device, grid2d=True,
+                      fx=fx, fy=fy, alpha=0.5)
+        return r0, g, a.gw_objective, a.trace[:, 0].copy(), b.gw_objective
+
+    out = _run_ranks(3, fn)
+    Gs = np.concatenate([o[1] for o in sorted(out, key=lambda t: t[0])])
+    Go = O.grad_prescribed_2d(sx, sy, p, q, Tn.astype(np.float64))
+    scale = np.max(np.abs(Go))
+    assert np.max(np.abs(Gs - G1)) <= 2e-6 * scale
+    assert np.max(np.abs(Gs - Go)) <= 1e-5 * scale
+    assert out[0][2] == out[1][2] == out[2][2]
+    assert abs(out[0][2] - r1.gw_objective) <= 1e-6 * abs(r1.gw_objective)
+    np.testing.assert_allclose(out[0][3], r1.trace[:, 0], rtol=1e-6)
+    assert abs(out[0][4] - f1.gw_objective) <= 1e-6 * abs(f1.gw_objective)
+    ro = O.entropic_gw_2d(sx, sy, p, q, 0.02, 4, 80)
+    assert abs(out[0][2] - ro["gw_objective"]) <= 1e-4 * abs(ro["gw_objective"])
