@@ -78,10 +78,10 @@ typedef enum { GW_F32 = 0, GW_F64 = 1 } gw_dtype;  /* storage of every N x M mat
 /* 2-D tensor grids (Table 3): n = nx^2 points (a, b) -> row a nx + b
  * at (x[a], x[b]) with x the SORTED axis of length nx (likewise y with ny, m = ny^2), Manhattan
  * distance |x_a - x_a'| + |x_b - x_b'| (reading R31; the paper's uniform grid is x_a = a h).
- * k = 1, nx, ny <= 256, one rank; p (n) and q (m) as usual. */
+ * k = 1, nx, ny <= 256; p (n) and q (m) as usual; rows shard as in 1-D (row0, n_local). */
 #define GW_GRID2D          0x4u
 /* largest distance power: k = 1 (gap-weighted scans), k = 2 (moments), 3..5 (power-sum scans,
- * PAPER.md:229-259; one rank only for k >= 3) */
+ * PAPER.md:229-259) */
 #define GW_MAX_K           5
 
 typedef struct {
@@ -241,7 +241,8 @@ gw_status fgw_solve(gw_ctx *ctx, const gw_problem *prob, const double *fx, const
  *            marginal_violation = max(|G1 - u|, |G^T1 - v|) (informational: G is unbalanced).
  *   trace    [outer][4] = {F_eps, E, inner iterations, m(G)} per outer iteration (F_eps, E only
  *            with GW_SOLVE_TRACE_OBJECTIVE, and always for the last one).
- * One rank, 1-D supports (k = 1..GW_MAX_K); 2-D grids, sharding or tol > 0 -> GW_ERR_UNSUPPORTED. */
+ * 1-D supports (k = 1..GW_MAX_K), row-sharded like the other solvers; 2-D grids or tol > 0 ->
+ * GW_ERR_UNSUPPORTED. */
 gw_status ugw_solve(gw_ctx *ctx, const gw_problem *prob, double rho, const gw_solve_opts *opts,
                     const void *T0, void *T_out, int64_t ldT, double *f, double *g,
                     gw_result *res, double *trace);

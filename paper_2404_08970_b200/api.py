@@ -252,7 +252,7 @@ def solve_host(x, y, p, q, eps, outer, inner, tol=0.0, check_every=10, device=No
 
 
 def ugw_solve(x, y, u, v, rho, eps, outer, inner, trace_objective=False, return_plan=False, device=None, ctx=None,
-              k=1):
+              k=1, row0=0, n_local=None):
     """Entropic unbalanced GW (ugw_solve; Remark 3, readings R32-R35 in DESIGN.md)
     on device vectors.  Returns a Result: gw_objective = E(T), entropic_objective = F_eps(T),
     trace [outer, 4] = {F_eps, E, inner iterations, mass}."""
@@ -262,10 +262,12 @@ def ugw_solve(x, y, u, v, rho, eps, outer, inner, trace_objective=False, return_
     ctx = ctx or Context.get(dev)
     x, y, u, v = (_vec(t, dev) for t in (x, y, u, v))
     n, m = u.numel(), v.numel()
+    if n_local is not None:
+        n = int(n_local)
     f = torch.empty(n, dtype=torch.float64, device=dev)
     g = torch.empty(m, dtype=torch.float64, device=dev)
     T = plan_buffer(n, m, dev) if return_plan else None
-    pr = _problem(x, y, u, v, k=k)
+    pr = _problem(x, y, u, v, n_local=n, row0=row0, k=k)
     o = _opts(eps, outer, inner, 0.0, 10, trace_objective)
     res = L.gw_result()
     tr = np.zeros((max(int(outer), 1), 4), dtype=np.float64)

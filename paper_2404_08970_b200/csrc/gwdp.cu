@@ -1803,15 +1803,48 @@ static gw_status ugw_stats(gw_ctx* c, const Prepared& P, SinkState& s, const flo
   KCHECK();
   k_g2_colsum_reduce<<<grid_for(m), 256, 0, c->stream>>>(part, nch, m, b_out);
   KCHECK();
-  k_ugw_scalars<<<1, 1024, 0, c->stream>>>(a_out, P.lp, s.f, ct, nl, b_out, P.lq, s.g, m, sc);
+  if (P.R > 1) {  // b over every rank's rows, summed in rank order
+    double* gb;
+    TRY(ws(c, c->xvec, (size_t)m * (P.R + 1), &gb));
+    TRY(comm_allgather(c, b_out, gb, sizeof(double) * (size_t)m));
+    k_gk_ranks<<<grid_for(m), 256, 0, c->stream>>>(gb, P.R, P.rank, m, gb + (size_t)m * P.R, b_out);
+    KCHECK();
+  }
+  k_ugw_scalars<<<1, 1024, 0, c->stream>>>(a_out, P.lp + P.row0, s.f, ct, nl, b_out, P.lq, s.g, m, sc);
   KCHECK();
-  CU(cudaMemcpyAsync(c->hpin + 48, sc, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  // the row sums (entries 0, 1, 3, 5, 6) add over the ranks; the column sums (2, 4, 7) are replicated
+  double* gsc;
+  TRY(ws(c, c->xpart, 8 * (size_t)(P.R + 1), &gsc));
+  TRY(comm_allgather(c, sc, gsc, 8 * sizeof(double)));
+  CU(cudaMemcpyAsync(c->hpin, gsc, 8 * sizeof(double) * P.R, cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
-  const double* h = c->hpin + 48;
+  double h[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int r = 0; r < P.R; ++r)
+    for (int k : {0, 1, 3, 5, 6}) h[k] += c->hpin[8 * r + k];
+  for (int k : {2, 4, 7}) h[k] = c->hpin[k];
   st->mass = h[0];
   st->A1 = h[1];
   st->B1 = h[2];
   st->KL = (h[3] + h[4] - h[5]) / eps_t - h[6] - h[7];
+  return GW_OK;
+}
+
+// A per-row vector of this rank's rows -> the full vector on every rank (padded all-gather)
+static gw_status ugw_gather_rows(gw_ctx* c, const Prepared& P, const double* local, double* full) {
+  if (P.R == 1) {
+    if (local != full) CU(cudaMemcpyAsync(full, local, sizeof(double) * (size_t)P.nl, cudaMemcpyDeviceToDevice,
+                                          c->stream));
+    return GW_OK;
+  }
+  const int64_t ml = P.maxnl;
+  double* g;
+  TRY(ws(c, c->xg2, (size_t)ml * (P.R + 1), &g));
+  double* pk = g + (size_t)ml * P.R;
+  CU(cudaMemsetAsync(pk, 0, sizeof(double) * (size_t)ml, c->stream));
+  CU(cudaMemcpyAsync(pk, local, sizeof(double) * (size_t)P.nl, cudaMemcpyDeviceToDevice, c->stream));
+  TRY(comm_allgather(c, pk, g, sizeof(double) * (size_t)ml));
+  k_unpad<<<grid_for(ml), 256, 0, c->stream>>>(g, P.R, ml, P.dtab, full);
+  KCHECK();
   return GW_OK;
 }
 
@@ -1844,7 +1877,6 @@ static gw_status ugw_impl(gw_ctx* c, const gw_problem* pb, double rho, const gw_
   const double eps = o->eps;
   Prepared P;
   TRY(prepare(c, pb, P));
-  if (P.R > 1) return fail(GW_ERR_UNSUPPORTED, "ugw_solve: row sharding is not implemented");
   const int64_t nl = P.nl, m = P.m;
   const int64_t ldG = (m + 31) & ~int64_t(31);
   float* G;
@@ -1858,9 +1890,11 @@ static gw_status ugw_impl(gw_ctx* c, const gw_problem* pb, double rho, const gw_
     s.f = f;
     s.g = g;
   }
-  double *av, *bv, *ca, *cb, *fr, *gr, *Fs, *Gs2, *objout;
-  TRY(ws(c, c->uga, (size_t)std::max<int64_t>(nl, 1), &av)); TRY(ws(c, c->ugb, (size_t)m, &bv));
-  TRY(ws(c, c->ugca, (size_t)std::max<int64_t>(nl, 1), &ca)); TRY(ws(c, c->ugcb, (size_t)m, &cb));
+  double *av, *bv, *ca, *cb, *fr, *gr, *Fs, *Gs2, *objout, *afull;
+  const int64_t n = P.n;
+  TRY(ws(c, c->uga, (size_t)std::max<int64_t>(nl, 1) + (size_t)n, &av)); TRY(ws(c, c->ugb, (size_t)m, &bv));
+  afull = av + std::max<int64_t>(nl, 1);
+  TRY(ws(c, c->ugca, (size_t)n, &ca)); TRY(ws(c, c->ugcb, (size_t)m, &cb));
   TRY(ws(c, c->ugfr, (size_t)std::max<int64_t>(nl, 1), &fr)); TRY(ws(c, c->uggr, (size_t)m, &gr));
   TRY(ws(c, c->fsc, (size_t)std::max<int64_t>(nl, 1), &Fs)); TRY(ws(c, c->gsc, (size_t)m, &Gs2));
   TRY(ws(c, c->objout, 16, &objout));
@@ -1897,11 +1931,15 @@ static gw_status ugw_impl(gw_ctx* c, const gw_problem* pb, double rho, const gw_
   for (int l = 0; l < o->outer_iters; ++l) {
     // ---- cost C = grad E(T^) (realised a, b) + 2 g(T^) (R32) ----
     const double gconst = rho * st.A1 + rho * st.B1 + eps * st.KL;
-    const double* aw = (l == 0) ? P.pn : av;
+    const double* aw = P.pn;  // T^0: a = u (all rows)
+    if (l > 0) {
+      TRY(ugw_gather_rows(c, P, av, afull));
+      aw = afull;
+    }
     const double* bw = (l == 0) ? P.qn : bv;
-    TRY(dd_const(c, P.k, P.xc, aw, nl, ca));
+    TRY(dd_const(c, P.k, P.xc, aw, n, ca));
     TRY(dd_const(c, P.k, P.yc, bw, m, cb));
-    k_ugw_addc<<<grid_for(nl), 256, 0, c->stream>>>(ca, gconst, nl);
+    k_ugw_addc<<<grid_for(n), 256, 0, c->stream>>>(ca, gconst, n);
     KCHECK();
     Prepared P2 = P;
     P2.cx = ca;
@@ -1911,8 +1949,8 @@ static gw_status ugw_impl(gw_ctx* c, const gw_problem* pb, double rho, const gw_
     TSrc2 S2;
     if (l == 0) {
       mode = T_PRODUCT;
-      S = TSrc{nullptr, 0, P.pn, P.qn, 0.0};
-      S2 = TSrc2{nullptr, 0, P.pnf, nullptr, P.qnf, nullptr, 0.f, 0.f};
+      S = TSrc{nullptr, 0, P.pn + P.row0, P.qn, 0.0};
+      S2 = TSrc2{nullptr, 0, P.pnf + P.row0, nullptr, P.qnf, nullptr, 0.f, 0.f};
     } else {
       mode = T_GIBBS;
       const double cc = GW_LOG2E / eps_reg;
@@ -1928,25 +1966,26 @@ static gw_status ugw_impl(gw_ctx* c, const gw_problem* pb, double rho, const gw_
     const double eps_t = 2.0 * st.mass * eps, rho_t = 2.0 * st.mass * rho;
     const double kap = rho_t / (rho_t + eps_t);
     const float c2f = (float)(GW_LOG2E / eps_t);
-    k_ugw_axpy<<<grid_for(nl), 256, 0, c->stream>>>(fr, P.lp, eps_t, nl, s.f);
+    k_ugw_axpy<<<grid_for(nl), 256, 0, c->stream>>>(fr, P.lp + P.row0, eps_t, nl, s.f);
     k_ugw_axpy<<<grid_for(m), 256, 0, c->stream>>>(gr, P.lq, eps_t, m, s.g);
     KCHECK();
     TRY(sink_split(c, P, s, eps_t));
     for (int it = 0; it < o->inner.max_iter; ++it) {
-      k_sink_row<<<rgrid, 256, 0, c->stream>>>(G, ldG, nl, m, s.gh, s.gl, c2f, s.f, s.f, P.lp, eps_t, s.fh, s.fl,
-                                                nullptr, nullptr, nullptr, kap);
+      k_sink_row<<<rgrid, 256, 0, c->stream>>>(G, ldG, nl, m, s.gh, s.gl, c2f, s.f, s.f, P.lp + P.row0, eps_t,
+                                                s.fh, s.fl, nullptr, nullptr, nullptr, kap);
       KCHECK();
       k_sink_col<<<cgrid, 256, 0, c->stream>>>(G, ldG, nl, m, s.fh, s.fl, c2f, s.RB, s.part, nullptr, nullptr);
       KCHECK();
       k_sink_colmerge<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.part, s.nrb, m, s.lse, nullptr, nullptr);
       KCHECK();
-      k_sink_colfin<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.lse, 1, m, P.lq, eps_t, s.g, s.gh, s.gl,
+      TRY(comm_allgather(c, s.lse, s.lseg, 2 * sizeof(double) * (size_t)m));
+      k_sink_colfin<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.lseg, P.R, m, P.lq, eps_t, s.g, s.gh, s.gl,
                                                                        nullptr, nullptr, nullptr, kap);
       KCHECK();
     }
     inner_total += o->inner.max_iter;
     // relative duals for the warm start (R34), then the mass rescaling (R35)
-    k_ugw_axpy<<<grid_for(nl), 256, 0, c->stream>>>(s.f, P.lp, -eps_t, nl, fr);
+    k_ugw_axpy<<<grid_for(nl), 256, 0, c->stream>>>(s.f, P.lp + P.row0, -eps_t, nl, fr);
     k_ugw_axpy<<<grid_for(m), 256, 0, c->stream>>>(s.g, P.lq, -eps_t, m, gr);
     KCHECK();
     UgwStats sn;
@@ -1975,8 +2014,8 @@ static gw_status ugw_impl(gw_ctx* c, const gw_problem* pb, double rho, const gw_
   // ---- final plan: E, F, violation (vs u, v; informational) ----
   double E = 0.0, viol = 0.0;
   if (o->outer_iters == 0) {
-    const TSrc S{nullptr, 0, P.pn, P.qn, 0.0};
-    const TSrc2 S2{nullptr, 0, P.pnf, nullptr, P.qnf, nullptr, 0.f, 0.f};
+    const TSrc S{nullptr, 0, P.pn + P.row0, P.qn, 0.0};
+    const TSrc2 S2{nullptr, 0, P.pnf + P.row0, nullptr, P.qnf, nullptr, 0.f, 0.f};
     TRY(grad_pass(c, P, T_PRODUCT, S, S2, nullptr, 0, false, true, nullptr, nullptr, 1.0, objout));
     CU(cudaMemcpyAsync(c->hpin, objout, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));

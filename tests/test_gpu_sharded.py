@@ -260,3 +260,25 @@ def test_sharded_grid2d_grad_and_solve(gw):
     assert abs(out[0][4] - f1.gw_objective) <= 1e-6 * abs(f1.gw_objective)
     ro = O.entropic_gw_2d(sx, sy, p, q, 0.02, 4, 80)
     assert abs(out[0][2] - ro["gw_objective"]) <= 1e-4 * abs(ro["gw_objective"])
+
+
+def test_sharded_ugw(gw):
+    """UGW sharded by rows: the plan statistics' row parts add over the ranks, b and the column
+    LSE pairs are gathered; same trajectory as one rank."""
+    api, dist = gw
+    P = _c5(300, 260, 4, 40)
+    r1 = api.ugw_solve(P.x, P.y, P.p, P.q, 1.0, 0.01, P.outer, P.inner, trace_objective=True)
+
+    def fn(r, ctx, st):
+        r0, nl = dist.shard_rows(P.x.size, 3, r)
+        a = api.ugw_solve(P.x, P.y, P.p, P.q, 1.0, 0.01, P.outer, P.inner, trace_objective=True, ctx=ctx,
+                          device=ctx.device, row0=r0, n_local=nl)
+        return a.entropic_objective, a.trace.copy()
+
+    out = _run_ranks(3, fn)
+    assert out[0][0] == out[1][0] == out[2][0]
+    assert abs(out[0][0] - r1.entropic_objective) <= 1e-6 * abs(r1.entropic_objective)
+    np.testing.assert_allclose(out[0][1][:, 0], r1.trace[:, 0], rtol=1e-6)
+    np.testing.assert_allclose(out[0][1][:, 3], r1.trace[:, 3], rtol=1e-6)
+    ro = O.entropic_ugw(P.x, P.y, P.p, P.q, 1.0, 0.01, P.outer, P.inner)
+    assert abs(out[0][0] - ro["F"][-1]) <= 1e-4 * abs(ro["F"][-1])
