@@ -282,3 +282,37 @@ def test_sharded_ugw(gw):
     np.testing.assert_allclose(out[0][1][:, 3], r1.trace[:, 3], rtol=1e-6)
     ro = O.entropic_ugw(P.x, P.y, P.p, P.q, 1.0, 0.01, P.outer, P.inner)
     assert abs(out[0][0] - ro["F"][-1]) <= 1e-4 * abs(ro["F"][-1])
+
+
+def test_nccl_communicator_single_rank(gw):
+    """The NCCL transport's plumbing in-process: torch.distributed (nccl, world size 1) broadcasts
+    the unique id, gw_comm_init creates the communicator on the current device, a solve runs with it
+    and matches the communicator-less solve, and the handle is destroyed cleanly."""
+    import os
+    import socket
+    import torch
+    import torch.distributed as tdist
+    api, dist = gw
+    if tdist.is_initialized():
+        pytest.skip("a process group is already initialised")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dev = torch.device("cuda", 0)
+    tdist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    try:
+        comm = dist.nccl_comm()
+        assert comm.nranks == 1 and comm.rank == 0
+        st = torch.cuda.Stream(dev)
+        ctx = api.Context(dev, st, comm)
+        P = W.config5(200, 150)
+        with torch.cuda.stream(st):
+            a = api.solve(P.x, P.y, P.p, P.q, P.eps, 3, 40, ctx=ctx, device=dev)
+        b = api.solve(P.x, P.y, P.p, P.q, P.eps, 3, 40, device=dev)
+        assert a.gw_objective == b.gw_objective
+        ctx.close()
+        comm.close()
+    finally:
+        tdist.destroy_process_group()
