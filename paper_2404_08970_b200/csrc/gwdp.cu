@@ -21,6 +21,7 @@
 #include "grid2d.cuh"
 #include "polyk.cuh"
 #include "ugw.cuh"
+#include "small.cuh"
 #include "sink.cuh"
 #include "vec.cuh"
 
@@ -1313,6 +1314,49 @@ static gw_status sink_viol_global(gw_ctx* c, const Prepared& P, SinkState& s) {
   return GW_OK;
 }
 
+// Cluster-resident Sinkhorn (small.cuh) for a cost matrix that fits in one cluster's shared
+// memory.  The kernel is bound by its per-element fp64 / MUFU work on the cluster's SMs, so the
+// cluster is as wide as the rows allow (>= 16 rows per CTA, up to 16 CTAs) once it fits; 0 if none.
+static int small_cluster(gw_ctx* c, const Prepared& P, int* rows_out, size_t* bytes_out) {
+  if (P.nl <= 0 || P.m <= 0) return 0;
+  int want = 1;
+  while (want < 16 && P.nl >= 16 * 2 * (int64_t)want) want *= 2;
+  for (int CL : {1, 2, 4, 8, 16}) {
+    if (CL < want) continue;
+    const int64_t rows = (P.nl + CL - 1) / CL;
+    if (rows > (1 << 20)) continue;
+    const size_t bytes = small_smem_bytes((int)rows, (int)((P.m + 1) & ~int64_t(1)), P.m);
+    if (bytes > 220 * 1024) continue;
+    if (CL > 1 && rows * (CL - 1) >= P.nl) continue;  // every CTA holds at least one row
+    static int ok[32] = {0};  // occupancy verdict per CL (1 = fits, -1 = does not)
+    const int key = CL;
+    cudaFuncSetAttribute(k_sink_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (CL > 8) cudaFuncSetAttribute(k_sink_small, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (ok[key] == 0) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(CL);
+      cfg.blockDim = dim3(SNT);
+      cfg.dynamicSmemBytes = 220 * 1024;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      cudaFuncSetAttribute(k_sink_small, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      int ncl = 0;
+      const cudaError_t e = cudaOccupancyMaxActiveClusters(&ncl, (void*)k_sink_small, &cfg);
+      ok[key] = (e == cudaSuccess && ncl >= 1) ? 1 : -1;
+      cudaGetLastError();
+      cudaFuncSetAttribute(k_sink_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    }
+    if (ok[key] < 0) continue;
+    *rows_out = (int)rows;
+    *bytes_out = bytes;
+    return CL;
+  }
+  return 0;
+}
+
 // `iters` Sinkhorn iterations on G.  tol > 0: check every `check_every` iterations (one
 // host sync per check); returns the iterations used and whether tol was met.
 // Multi-rank: f is per-shard, g replicated; every column half-step gathers the ranks' column
@@ -1405,6 +1449,35 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
     KCHECK();
     return GW_OK;
   };
+  // Fixed iteration counts, one rank, G small enough for one cluster's shared memory: every
+  // iteration in ONE launch (small.cuh; GWDP_NO_SMALL=1 disables it)
+  const bool no_small = getenv("GWDP_NO_SMALL") != nullptr;  // read per call (tests compare both paths)
+  if (!tolmode && !no_small && P.R == 1 && iters > 0) {
+    int rows = 0;
+    size_t bytes = 0;
+    const int CL = small_cluster(c, P, &rows, &bytes);
+    if (CL > 0) {
+      // even smem row pitch: the fp64 arrays after the fp32 tile stay 8-byte aligned
+      SmallArgs sa{G, ldG, nl, m, rows, (int)((m + 1) & ~int64_t(1)), P.lp + P.row0, P.lq, eps, 1.0, iters, s.f, s.g};
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(CL);
+      cfg.blockDim = dim3(SNT);
+      cfg.dynamicSmemBytes = bytes;
+      cfg.stream = c->stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      PROF_BEGIN(c, PC_SINK_ROW);
+      CU(cudaLaunchKernelEx(&cfg, k_sink_small, sa));
+      KCHECK();
+      PROF_END(c, PC_SINK_ROW, 1);
+      TRY(sink_split(c, P, s, eps));
+      *used = iters;
+      return GW_OK;
+    }
+  }
   // Fixed iteration counts on one rank: the iteration's ~10 launches are captured once per solve
   // into a CUDA graph and replayed (the small configurations are launch-bound; GWDP_NO_GRAPH=1
   // disables it; not while per-kernel profiling is on, whose events time the launches).

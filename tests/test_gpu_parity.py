@@ -470,3 +470,25 @@ def test_general_tau_fgw_and_unsupported(gw):
     with pytest.raises(GwError) as e:
         gw.solve(P.x, P.y, P.p, P.q, P.eps, 2, 10, device=_dev(), tau=0.5 * P.eps, k=2)
     assert e.value.code == "GW_ERR_UNSUPPORTED"
+
+
+# ----------------------------------------------------------------------------- cluster-resident small path
+
+@pytest.mark.parametrize("n,m", [(256, 256), (400, 300), (37, 1000), (1, 9)])
+def test_small_cluster_path_matches_multikernel_path(gw, monkeypatch, n, m):
+    """small.cuh (one launch per inner loop, G in one cluster's shared memory) against the
+    multi-kernel path and the oracle on the same problem."""
+    rng = np.random.default_rng(n + m)
+    x, y = np.sort(rng.random(n)), np.sort(rng.random(m))
+    p, q = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))
+    eps = 0.02
+    a = gw.solve(x, y, p, q, eps, 4, 80, trace_objective=True, device=_dev())
+    monkeypatch.setenv("GWDP_NO_SMALL", "1")
+    b = gw.solve(x, y, p, q, eps, 4, 80, trace_objective=True, device=_dev())
+    monkeypatch.delenv("GWDP_NO_SMALL")
+    ro = O.entropic_gw(x, y, p, q, eps, 4, 80)
+    E = np.asarray(ro["E"])
+    for r in (a, b):
+        assert np.max(np.abs(r.trace[:, 0] - E) / np.abs(E)) <= OBJ_TOL
+        assert r.marginal_violation <= max(VIOL_TOL, 2 * ro["viol"][-1])
+    assert abs(a.gw_objective - b.gw_objective) <= 1e-5 * abs(b.gw_objective)
