@@ -253,9 +253,11 @@ def test_ugw_argument_errors(gw):
 
 @pytest.mark.parametrize("n,m,eps", [(300, 20000, 0.02), (64, 65536, 0.01), (500, 3000, 0.02), (257, 8193, 0.02),
                                      (1000, 8192, 0.01), (3, 70, 0.05)])
-def test_sinkhorn_fused_path_parity(gw, n, m, eps):
+def test_sinkhorn_fused_path_parity(gw, monkeypatch, n, m, eps):
     """The fused one-read iteration (clusters of 1-8 CTAs spanning a row, ragged last CTA,
-    CTAs entirely past m) against the oracle; and it must actually have run."""
+    CTAs entirely past m) against the oracle; and it must actually have run (the cluster-resident
+    small path, which would take the small shapes, is switched off)."""
+    monkeypatch.setenv("GWDP_NO_SMALL", "1")
     rng = np.random.default_rng(n * 7 + m)
     G = rng.random((n, m)).astype(np.float32)
     p, q = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))

@@ -26,6 +26,13 @@ def gw():
     return api, dist
 
 
+@pytest.fixture(autouse=True)
+def _multikernel_reference(monkeypatch):
+    """Sharded solves always take the multi-kernel path (the cluster-resident small path is single
+    rank); the single-rank references here take it too, so the comparisons isolate the exchanges."""
+    monkeypatch.setenv("GWDP_NO_SMALL", "1")
+
+
 def _run_ranks(R, fn):
     """fn(rank, ctx, stream) on R threads; returns the per-rank results in rank order."""
     import torch
