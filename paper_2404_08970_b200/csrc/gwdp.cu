@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <atomic>
 #include <vector>
 
 #include "../../include/gwdp.h"
@@ -1328,11 +1329,13 @@ static int small_cluster(gw_ctx* c, const Prepared& P, int* rows_out, size_t* by
     const size_t bytes = small_smem_bytes((int)rows, (int)((P.m + 1) & ~int64_t(1)), P.m);
     if (bytes > 220 * 1024) continue;
     if (CL > 1 && rows * (CL - 1) >= P.nl) continue;  // every CTA holds at least one row
-    static int ok[32] = {0};  // occupancy verdict per CL (1 = fits, -1 = does not)
-    const int key = CL;
-    cudaFuncSetAttribute(k_sink_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    static std::atomic<int> ok[32];  // occupancy verdict per CL (0 = unknown, 1 = fits, -1 = does not);
+    const int key = CL;               // contexts on several host threads may race benignly (same value)
+    // the attribute is the CAP (220 KB) for every launch: one value, so contexts on several host
+    // threads never shrink it under each other's launches
+    cudaFuncSetAttribute(k_sink_small, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     if (CL > 8) cudaFuncSetAttribute(k_sink_small, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (ok[key] == 0) {
+    if (ok[key].load() == 0) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(CL);
       cfg.blockDim = dim3(SNT);
@@ -1342,14 +1345,12 @@ static int small_cluster(gw_ctx* c, const Prepared& P, int* rows_out, size_t* by
       at[0].val.clusterDim.x = CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
       cfg.attrs = at;
       cfg.numAttrs = 1;
-      cudaFuncSetAttribute(k_sink_small, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
       int ncl = 0;
       const cudaError_t e = cudaOccupancyMaxActiveClusters(&ncl, (void*)k_sink_small, &cfg);
-      ok[key] = (e == cudaSuccess && ncl >= 1) ? 1 : -1;
+      ok[key].store((e == cudaSuccess && ncl >= 1) ? 1 : -1);
       cudaGetLastError();
-      cudaFuncSetAttribute(k_sink_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     }
-    if (ok[key] < 0) continue;
+    if (ok[key].load() < 0) continue;
     *rows_out = (int)rows;
     *bytes_out = bytes;
     return CL;
