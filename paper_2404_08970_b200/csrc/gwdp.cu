@@ -327,6 +327,12 @@ extern "C" gw_status gw_check_shards(const int64_t* table, int nranks, int64_t n
 
 static int nranks_of(const gw_ctx* c) { return c->comm ? c->comm->nranks : 1; }
 
+// Test-only fault injection (SURVEY §4.2 tier T6): GWDP_FAULT=<site> perturbs one value at that site.
+static bool fault_is(const char* site) {
+  const char* e = getenv("GWDP_FAULT");
+  return e && strcmp(e, site) == 0;
+}
+
 // All-gather of `bytes` per rank from device `dsend` into device `drecv` ([nranks][bytes], rank
 // order), ordered on ctx's stream.  Host transport: synchronises the stream around the callback.
 static gw_status comm_allgather(gw_ctx* c, const void* dsend, void* drecv, size_t bytes) {
@@ -657,6 +663,10 @@ static gw_status grad_pass_k1(gw_ctx* c, const Prepared& P, int mode, const TSrc
   KCHECK();
   k_rowcarry<<<nb, TR, 0, c->stream>>>(nl, m, ns, xl, P.yc, rP, rA, blk, Ptot, Aend);
   KCHECK();
+  if (fault_is("carry") && ns > 1 && nl > 0) {  // test-only: one row carry doubled
+    k_fault_scale<<<1, 32, 0, c->stream>>>(rP, (int64_t)1 * nl + nl / 2, 2.0);
+    KCHECK();
+  }
   double* tail = nullptr;
   if (R > 1) TRY(ws(c, c->xtail, 8 * (size_t)ns, &tail));
   k_blkscan<<<(ns + 31) / 32, 32, 0, c->stream>>>(nl, nb, ns, xl, blk, bs, tail);
@@ -1399,6 +1409,10 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
       KCHECK();
       k_sink_colsum<<<(unsigned)((m + 31) / 32), 256, 0, c->stream>>>(s.fpart, s.fncl, m, s.csl, s.mode, s.stop);
       KCHECK();
+      if (fault_is("colsum")) {  // test-only: one column sum of the half-step plan doubled
+        k_fault_scale<<<1, 32, 0, c->stream>>>(s.csl, m / 2, 2.0);
+        KCHECK();
+      }
       TRY(comm_allgather(c, s.csl, s.csg, sizeof(double) * (size_t)m));
       CU(cudaMemsetAsync(s.flag, 0, sizeof(int), c->stream));
       k_sink_fast_check<<<grid_for(std::max(m, nl), 256, 1 << 30), 256, 0, c->stream>>>(

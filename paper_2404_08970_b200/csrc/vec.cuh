@@ -163,6 +163,12 @@ __global__ void __launch_bounds__(1024) k_scan1d(Scan1DBatch B) {
   if (D.tot && threadIdx.x == 0) { D.tot[0] = V; D.tot[1] = Sv; }
 }
 
+// Test-only fault injection (SURVEY §4.2 tier T6, env GWDP_FAULT): perturb one entry so that the
+// parity tests must fail -- evidence that they would catch a wrong carry or column sum.
+__global__ void k_fault_scale(double* __restrict__ v, int64_t i, double f) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) v[i] *= f;
+}
+
 // fp32 hi/lo split of s * v (log2-domain dual scaling used by the Sinkhorn kernels)
 __global__ void k_split(const double* __restrict__ v, int64_t n, double scale, float* __restrict__ hi,
                         float* __restrict__ lo) {

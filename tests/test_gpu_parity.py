@@ -494,3 +494,30 @@ def test_small_cluster_path_matches_multikernel_path(gw, monkeypatch, n, m):
         assert np.max(np.abs(r.trace[:, 0] - E) / np.abs(E)) <= OBJ_TOL
         assert r.marginal_violation <= max(VIOL_TOL, 2 * ro["viol"][-1])
     assert abs(a.gw_objective - b.gw_objective) <= 1e-5 * abs(b.gw_objective)
+
+
+# ----------------------------------------------------------------------------- fault injection
+
+def test_fault_injection_is_caught(gw, monkeypatch):
+    """A test-only hook perturbs one tile carry of the gradient (GWDP_FAULT=carry) or one column sum
+    of the fused Sinkhorn iteration (GWDP_FAULT=colsum) by a factor 2: the parity checks must fail."""
+    rng = np.random.default_rng(5)
+    n, m = 600, 700
+    x, y = np.sort(rng.random(n)), np.sort(rng.random(m))
+    p, q = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))
+    T = (rng.random((n, m)) / (n * m)).astype(np.float32)
+    Go = O.grad_prescribed(x, y, p, q, T.astype(np.float64))
+    G = gw.grad(x, y, p, q, _to_dev(gw, T)).cpu().numpy().astype(np.float64)
+    assert _grad_err(G, Go) <= GRAD_TOL
+    monkeypatch.setenv("GWDP_FAULT", "carry")
+    Gf = gw.grad(x, y, p, q, _to_dev(gw, T)).cpu().numpy().astype(np.float64)
+    assert _grad_err(Gf, Go) > GRAD_TOL
+    monkeypatch.setenv("GWDP_FAULT", "colsum")
+    monkeypatch.setenv("GWDP_NO_SMALL", "1")
+    Gc = rng.random((300, 20000)).astype(np.float32)
+    pc, qc = rng.dirichlet(np.ones(300)), rng.dirichlet(np.ones(20000))
+    r = gw.sinkhorn(_to_dev(gw, Gc), pc, qc, 0.02, 60, return_plan=True)
+    f, g, _ = O.sinkhorn(Gc.astype(np.float64), pc, qc, 0.02, 60)
+    To = O.plan_from_duals(Gc.astype(np.float64), f, g, 0.02)
+    assert r["fused_iters"] > 0
+    assert np.max(np.abs(r["T"].cpu().numpy().astype(np.float64) - To)) > 1e-4 * np.max(To)
