@@ -218,7 +218,7 @@ def solve(x, y, p, q, eps, outer, inner, tol=0.0, check_every=10, T0=None, retur
 
 
 def solve_host(x, y, p, q, eps, outer, inner, tol=0.0, check_every=10, device=None, ctx=None,
-               fx=None, fy=None, alpha=None, row0=0, n_local=None, k=1, grid2d=False):
+               fx=None, fy=None, alpha=None, row0=0, n_local=None, k=1, grid2d=False, tau=None):
     """entropic_gw_solve with HOST vectors (GW_HOST_VECTORS): the library stages x, y, p, q
     host->device and copies the duals f, g back.  This is the end-to-end public call.
     Sharded: as solve() (f holds this rank's n_local rows)."""
@@ -235,7 +235,7 @@ def solve_host(x, y, p, q, eps, outer, inner, tol=0.0, check_every=10, device=No
     pr.x, pr.y, pr.p, pr.q = (a.ctypes.data for a in (xs, ys, ps, qs))
     pr.k, pr.loss, pr.dtype = int(k), L.GW_LOSS_SQUARE, L.GW_F32
     pr.flags = L.GW_HOST_VECTORS | (L.GW_GRID2D if grid2d else 0)
-    o = _opts(eps, outer, inner, tol, check_every, False)
+    o = _opts(eps, outer, inner, tol, check_every, False, tau)
     res = L.gw_result()
     tr = np.zeros((max(int(outer), 1), 4))
     fp = f.ctypes.data_as(C.c_void_p)
