@@ -651,19 +651,24 @@ __global__ void __launch_bounds__(NT, 1) k_sink_fused2(FusedArgs a) {
 // every column sum CS_p must be finite and above 2^-100 (no overflow of an exponential, no row or
 // column whose terms all underflowed).  Then the absorbed-dual update equals the log-domain one up
 // to fp32 rounding of sums of positive terms.  flag |= 1 otherwise (order-independent OR).
+// part: ncl payloads of `stride` doubles (the M column sums, then -- multi-rank -- the rank's row flag
+// as an int in the slot at M: rowflags_gathered).  One rank: the row sums are checked here.
 __global__ void k_sink_fast_check(const float* __restrict__ Srow, int64_t nl, const double* __restrict__ part,
-                                  int ncl, int64_t m, const double* __restrict__ lq, int* __restrict__ flag,
-                                  const int* __restrict__ mode, const int* __restrict__ stop) {
+                                  int ncl, int64_t stride, int64_t m, const double* __restrict__ lq,
+                                  int* __restrict__ flag, const int* __restrict__ mode, const int* __restrict__ stop,
+                                  bool rowflags_gathered) {
   if (*mode != 1 || (stop && *stop)) return;
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   bool bad = false;
-  if (q < nl) {
+  if (!rowflags_gathered && q < nl) {
     const float S = Srow[q];
     bad |= !(S > 7.9e-31f && S < 3.0e38f);
   }
+  if (rowflags_gathered && q == 0)
+    for (int c = 0; c < ncl; ++c) bad |= *reinterpret_cast<const int*>(part + (int64_t)c * stride + m) != 0;
   if (q < m && lq[q] != -INFINITY) {
     double CS = 0.0;
-    for (int c = 0; c < ncl; ++c) CS += part[(int64_t)c * m + q];
+    for (int c = 0; c < ncl; ++c) CS += part[(int64_t)c * stride + q];
     bad |= !(CS > 7.9e-31 && CS < 1e300);
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
@@ -680,7 +685,8 @@ __global__ void k_or_flags(int* __restrict__ flag, const int* __restrict__ gath,
 
 __global__ void k_sink_fin_fast(const float* __restrict__ Srow, int64_t nl, const double* __restrict__ lp,
                                 double* __restrict__ f, float* __restrict__ fh, float* __restrict__ fl,
-                                float* __restrict__ viol, const double* __restrict__ part, int ncl, int64_t m,
+                                float* __restrict__ viol, const double* __restrict__ part, int ncl, int64_t stride,
+                                int64_t m,
                                 const double* __restrict__ lq, double eps, double* __restrict__ g,
                                 float* __restrict__ gh, float* __restrict__ gl, int* __restrict__ mode,
                                 const int* __restrict__ stop, float* __restrict__ dev, const int* __restrict__ flag) {
@@ -695,7 +701,7 @@ __global__ void k_sink_fin_fast(const float* __restrict__ Srow, int64_t nl, cons
   float dv = 0.f, vv = 0.f;
   if (q < m) {
     double CS = 0.0;
-    for (int c = 0; c < ncl; ++c) CS += part[(int64_t)c * m + q];
+    for (int c = 0; c < ncl; ++c) CS += part[(int64_t)c * stride + q];
     const double d = lq[q] - log(CS);  // ln(q / CS)
     const double gn = (lq[q] == -INFINITY) ? -INFINITY : g[q] + eps * d;
     g[q] = gn;

@@ -1246,12 +1246,12 @@ static gw_status sink_alloc(gw_ctx* c, const Prepared& P, SinkState& s) {
   s.nrb = (int)std::max<int64_t>(1, (P.nl + RB - 1) / RB);
   TRY(ws(c, c->part, (size_t)s.nrb * P.m, &s.part));
   TRY(ws(c, c->slse, 2 * (size_t)P.m, &s.lse));
-  TRY(ws(c, c->scsl, (size_t)P.m, &s.csl));
+  TRY(ws(c, c->scsl, (size_t)P.m + 1, &s.csl));  // + the row-flag slot (multi-rank)
   TRY(ws(c, c->sflag, 4, &s.flag));
   TRY(ws(c, c->sflagg, (size_t)P.R + 4, &s.flagg));
   if (P.R > 1) {
     TRY(ws(c, c->slseg, 2 * (size_t)P.m * P.R, &s.lseg));
-    TRY(ws(c, c->scsg, (size_t)P.m * P.R, &s.csg));
+    TRY(ws(c, c->scsg, ((size_t)P.m + 1) * P.R, &s.csg));
     TRY(ws(c, c->sviolg, (size_t)P.R, &s.violg));
   } else {
     s.lseg = s.lse;
@@ -1407,24 +1407,26 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
       PROF_BEGIN(c, PC_SINK_FUSED);
       TRY(fused_launch(c, s.fK, s.fCL, s.fNT, fa, s.fncl));
       KCHECK();
-      k_sink_colsum<<<(unsigned)((m + 31) / 32), 256, 0, c->stream>>>(s.fpart, s.fncl, m, s.csl, s.mode, s.stop);
+      // one rank: column sums, check (rows + columns), commit.  R > 1: the rank's row check rides in
+      // the column-sum payload (slot M), so ONE all-gather per iteration carries everything.
+      const bool multi = P.R > 1;
+      const int64_t stride = multi ? m + 1 : m;
+      if (multi) CU(cudaMemsetAsync(s.csl + m, 0, sizeof(double), c->stream));
+      k_sink_colsum<<<(unsigned)((m + 31) / 32), 256, 0, c->stream>>>(
+          s.fpart, s.fncl, m, s.csl, s.mode, s.stop, multi ? s.Srow : nullptr, multi ? nl : 0,
+          multi ? reinterpret_cast<int*>(s.csl + m) : nullptr);
       KCHECK();
       if (fault_is("colsum")) {  // test-only: one column sum of the half-step plan doubled
         k_fault_scale<<<1, 32, 0, c->stream>>>(s.csl, m / 2, 2.0);
         KCHECK();
       }
-      TRY(comm_allgather(c, s.csl, s.csg, sizeof(double) * (size_t)m));
+      TRY(comm_allgather(c, s.csl, s.csg, sizeof(double) * (size_t)stride));
       CU(cudaMemsetAsync(s.flag, 0, sizeof(int), c->stream));
       k_sink_fast_check<<<grid_for(std::max(m, nl), 256, 1 << 30), 256, 0, c->stream>>>(
-          s.Srow, nl, s.csg, P.R, m, P.lq, s.flag, s.mode, s.stop);
+          s.Srow, nl, s.csg, P.R, stride, m, P.lq, s.flag, s.mode, s.stop, multi);
       KCHECK();
-      if (P.R > 1) {
-        TRY(comm_allgather(c, s.flag, s.flagg, sizeof(int)));
-        k_or_flags<<<1, 32, 0, c->stream>>>(s.flag, s.flagg, P.R);
-        KCHECK();
-      }
       k_sink_fin_fast<<<grid_for(std::max(m, nl), 256, 1 << 30), 256, 0, c->stream>>>(
-          s.Srow, nl, P.lp + P.row0, s.f, s.fh, s.fl, nullptr, s.csg, P.R, m, P.lq, eps, s.g, s.gh, s.gl,
+          s.Srow, nl, P.lp + P.row0, s.f, s.fh, s.fl, nullptr, s.csg, P.R, stride, m, P.lq, eps, s.g, s.gh, s.gl,
           s.mode, s.stop, s.dev, s.flag);
       KCHECK();
       PROF_END(c, PC_SINK_FUSED, 2);

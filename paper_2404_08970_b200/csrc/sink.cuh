@@ -266,12 +266,25 @@ __global__ void k_sink_colmergefin(const float2* __restrict__ part, int nrb, int
 // CTA = 32 columns x 8 warps: warp w sums clusters w, w + 8, ... for lane's column, then the 8
 // warp sums are added in warp order (deterministic; 8x the parallelism of a thread per column,
 // which matters when there are many clusters, i.e. small problems with one CTA per cluster).
+// Multi-rank (rowflag != null): the same launch also checks this rank's row sums S_i (finite, above
+// 2^-100, as k_sink_fast_check) and ORs a bad row into *rowflag -- an int in the payload slot after
+// the M column sums, so the speculation flag travels in the column-sum all-gather (one collective
+// per iteration).  Rows are covered grid-stride by all threads.
 __global__ void __launch_bounds__(256) k_sink_colsum(const double* __restrict__ part, int ncl, int64_t m,
                                                      double* __restrict__ out, const int* __restrict__ mode,
-                                                     const int* __restrict__ stop) {
+                                                     const int* __restrict__ stop, const float* __restrict__ Srow = nullptr,
+                                                     int64_t nl = 0, int* __restrict__ rowflag = nullptr) {
   if (*mode != 1 || (stop && *stop)) return;
   __shared__ double red[8][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (rowflag) {
+    bool bad = false;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nl; i += (int64_t)gridDim.x * blockDim.x) {
+      const float S = Srow[i];
+      bad |= !(S > 7.9e-31f && S < 3.0e38f);
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(rowflag, 1);
+  }
   const int64_t q = blockIdx.x * (int64_t)32 + lane;
   double CS = 0.0;
   if (q < m)
