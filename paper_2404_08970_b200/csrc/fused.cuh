@@ -746,4 +746,14 @@ __global__ void k_sink_mode(float* __restrict__ dev, int* __restrict__ mode, flo
   }
 }
 
+// Chunked multi-rank loop (sink_run): after a fused step the decision may only go 1 -> 0 (a failed
+// step, or a correction above the threshold, freezes the chunk until the host runs the safe
+// iteration, whose k_sink_mode may return to the fused path).
+__global__ void k_sink_mode_fused(float* __restrict__ dev, int* __restrict__ mode, float thresh) {
+  if (threadIdx.x == 0) {
+    if (*mode == 1 && !(*dev <= thresh)) *mode = 0;
+    *dev = 0.f;
+  }
+}
+
 }  // namespace gw

@@ -1397,13 +1397,13 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
     const char* pf = getenv("GWDP_L2_AHEAD");
     fa.l2_ahead = pf ? atoi(pf) : 0;
   }
-  // one iteration (check: the tolerance rule's violation check of the plan after `done` iterations)
-  auto iteration = [&](bool check, int done) -> gw_status {
+  // the fused one-read step of one iteration (speculative; a no-op unless *mode == 1)
+  auto fused_step = [&]() -> gw_status {
     // Every iteration first tries the fused one-read path when *mode == 1 (speculatively at the
     // start of a solve); k_sink_fast_check validates it before anything is committed, and on
     // failure k_sink_fin_fast leaves f, g untouched and sets *mode = 0 so that the robust
     // two-kernel path below runs this same iteration.  No host sync.
-    if (!check && s.fK > 0) {
+    if (s.fK > 0) {
       PROF_BEGIN(c, PC_SINK_FUSED);
       TRY(fused_launch(c, s.fK, s.fCL, s.fNT, fa, s.fncl));
       KCHECK();
@@ -1431,6 +1431,11 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
       KCHECK();
       PROF_END(c, PC_SINK_FUSED, 2);
     }
+    return GW_OK;
+  };
+  // one iteration (check: the tolerance rule's violation check of the plan after `done` iterations)
+  auto iteration = [&](bool check, int done) -> gw_status {
+    if (!check) TRY(fused_step());
     // iterations run the robust two-kernel path while *mode == 0 (decided on the device)
     const int* skip = check ? nullptr : s.mode;
     if (check) CU(cudaMemsetAsync(s.viol, 0, sizeof(float), c->stream));
@@ -1466,6 +1471,58 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
     KCHECK();
     return GW_OK;
   };
+  // Fixed iteration counts on several ranks: the device-skipped safe path would still issue its
+  // column all-gather every iteration (the host cannot see the device's path decision), so the
+  // iterations run as chunks of fused steps; after each chunk ONE host read of the committed-step
+  // counter tells every rank (identically: the counter follows gathered data) whether a step failed
+  // or asked for the safe path, which then runs exactly that iteration.  Same sequence of committed
+  // updates as the per-iteration form.
+  if (!tolmode && P.R > 1 && s.fK > 0) {
+    constexpr int CH = 10;
+    int* hc = reinterpret_cast<int*>(c->hpin + 40);
+    CU(cudaMemcpyAsync(hc, s.mode, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    int base = hc[1], done = 0;
+    while (done < iters) {
+      const int chunk = std::min(CH, iters - done);
+      for (int k = 0; k < chunk; ++k) {
+        TRY(fused_step());
+        k_sink_mode_fused<<<1, 32, 0, c->stream>>>(s.dev, s.mode, 20.f);
+        KCHECK();
+      }
+      CU(cudaMemcpyAsync(hc, s.mode, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      CU(cudaStreamSynchronize(c->stream));
+      const int committed = hc[1] - base;
+      base = hc[1];
+      done += committed;
+      // this iteration (and, while the decision stays on the safe path, the next ones) on the safe path
+      while (committed < chunk && done < iters) {
+        PROF_BEGIN(c, PC_SINK_ROW);
+        k_sink_row<<<rgrid, 256, 0, c->stream>>>(G, ldG, nl, m, s.gh, s.gl, c2f, s.f, s.f, P.lp + P.row0, eps,
+                                                  s.fh, s.fl, nullptr, s.stop, nullptr);
+        KCHECK();
+        PROF_END(c, PC_SINK_ROW, 1);
+        PROF_BEGIN(c, PC_SINK_COL);
+        k_sink_col<<<cgrid, 256, 0, c->stream>>>(G, ldG, nl, m, s.fh, s.fl, c2f, s.RB, s.part, s.stop, nullptr);
+        KCHECK();
+        k_sink_colmerge<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.part, s.nrb, m, s.lse, s.stop, nullptr);
+        KCHECK();
+        TRY(comm_allgather(c, s.lse, s.lseg, 2 * sizeof(double) * (size_t)m));
+        k_sink_colfin<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.lseg, P.R, m, P.lq, eps, s.g, s.gh,
+                                                                         s.gl, s.stop, nullptr, s.dev);
+        KCHECK();
+        PROF_END(c, PC_SINK_COL, 2);
+        k_sink_mode<<<1, 32, 0, c->stream>>>(s.dev, s.mode, 20.f);
+        KCHECK();
+        done += 1;
+        CU(cudaMemcpyAsync(hc, s.mode, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+        if (hc[0] == 1) break;  // back on the fused path (the safe path does not move the counter)
+      }
+    }
+    *used = iters;
+    return GW_OK;
+  }
   // Fixed iteration counts, one rank, G small enough for one cluster's shared memory: every
   // iteration in ONE launch (small.cuh; GWDP_NO_SMALL=1 disables it)
   const bool no_small = getenv("GWDP_NO_SMALL") != nullptr;  // read per call (tests compare both paths)
