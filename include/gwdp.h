@@ -12,8 +12,8 @@
  *   plan T (n x m, the paper's Gamma), row-major.
  *   GW gradient (transpose typo fixed, reading R3):
  *     G = 2 (c 1^T + 1 c'^T) - 4 D_X T D_Y,  c = (D_X o D_X) p,  c' = (D_Y o D_Y) q.
- *   Entropic GW by mirror descent with tau = eps
- *   (Remark 1 PAPER.md:127-133):
+ *   Entropic GW by mirror descent with tau = eps by default
+ *   (Remark 1 PAPER.md:127-133; tau != eps: gw_solve_opts):
  *     T^l = argmin_{T in S(p,q)} <G(T^{l-1}), T> + eps H(T),  solved by log-domain
  *     Sinkhorn: f_i = eps ln p_i - eps LSE_p((g_p - G_ip)/eps),
  *               g_p = eps ln q_p - eps LSE_i((f_i - G_ip)/eps),
@@ -39,6 +39,12 @@
  *     renormalised in an internal copy.
  *   - Results are bitwise reproducible for fixed inputs, sizes and world size
  *     (fixed-order reductions, no float atomics on result paths).
+ *   - Execution routes chosen inside (same results within the stated tolerances): the fused
+ *     one-read Sinkhorn iteration with a device-validated safe fallback; for fixed iteration
+ *     counts on one rank a cluster-resident kernel when G fits in one thread-block cluster's
+ *     shared memory, else one CUDA graph replay per iteration; chunks of fused steps on
+ *     several ranks.  Env switches (diagnostics only): GWDP_NO_SMALL, GWDP_NO_GRAPH,
+ *     GWDP_NO_FUSED; GWDP_FAULT=carry|colsum is a test-only fault injection.
  */
 #ifndef GWDP_H
 #define GWDP_H
@@ -92,7 +98,7 @@ typedef struct {
   int32_t k;              /* distance power |x - x'|^k: 1 (hot path) .. GW_MAX_K (R17, f2) */
   int32_t loss;           /* gw_loss */
   int32_t dtype;          /* gw_dtype; only GW_F32 in this ABI version                 */
-  uint32_t flags;         /* GW_NO_VALIDATE | GW_HOST_VECTORS                          */
+  uint32_t flags;         /* GW_NO_VALIDATE | GW_HOST_VECTORS | GW_GRID2D              */
 } gw_problem;
 
 /* Optional precomputed moments of T (device, fp64).  Not used in ABI v1
