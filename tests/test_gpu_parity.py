@@ -353,6 +353,25 @@ def test_solver_c2_fullsize_trajectory(gw):
     assert r.marginal_violation <= max(VIOL_TOL, 2 * ref["viol"][-1])
 
 
+@pytest.mark.slow
+def test_solver_c4_recipe_16384_trajectory(gw):
+    """SURVEY §8(c) C4 parity (i): C4's recipe (eps = 1e-3, K = 100 fixed, 10 outer) at N = M = 16384,
+    the GPU's objective trajectory against the oracle's (tests/golden/c4_n16384_trajectory.json,
+    written by scripts/make_golden.py from oracle/ only)."""
+    import json
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "c4_n16384_trajectory.json")
+    if not os.path.exists(path):
+        pytest.skip("golden trajectory not generated (python scripts/make_golden.py c4_16384)")
+    ref = json.load(open(path))
+    P = W.config4(16384)
+    r = gw.solve(P.x, P.y, P.p, P.q, P.eps, 10, 100, trace_objective=True, device=_dev())
+    E = np.asarray(ref["E"])
+    assert np.max(np.abs(r.trace[:, 0] - E) / np.abs(E)) <= OBJ_TOL
+    assert abs(r.gw_objective - ref["gw_objective"]) <= OBJ_TOL * abs(ref["gw_objective"])
+    assert r.marginal_violation <= max(VIOL_TOL, 2 * ref["viol"][-1])
+
+
 # ----------------------------------------------------------------------------- distance power k = 2 (f2)
 
 @pytest.mark.parametrize("n,m", [(1, 5), (64, 64), (300, 517), (1024, 777)])
