@@ -166,7 +166,7 @@ def reference_arm(args, world, rank, config):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)  # one C4 solve: BASELINE configs[3] runs 10 outer iterations
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=65536, help="N = M (default: BASELINE config 4)")
