@@ -10,6 +10,7 @@
 #include <cstring>
 #include <string>
 #include <atomic>
+#include <nvtx3/nvToolsExt.h>
 #include <vector>
 
 #include "../../include/gwdp.h"
@@ -325,6 +326,12 @@ extern "C" gw_status gw_check_shards(const int64_t* table, int nranks, int64_t n
   return GW_OK;
 }
 
+// NVTX ranges (host-side, for nsys / ncu --nvtx): solve, gradient, Sinkhorn, all-gather
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 static int nranks_of(const gw_ctx* c) { return c->comm ? c->comm->nranks : 1; }
 
 // Test-only fault injection (SURVEY §4.2 tier T6): GWDP_FAULT=<site> perturbs one value at that site.
@@ -336,6 +343,7 @@ static bool fault_is(const char* site) {
 // All-gather of `bytes` per rank from device `dsend` into device `drecv` ([nranks][bytes], rank
 // order), ordered on ctx's stream.  Host transport: synchronises the stream around the callback.
 static gw_status comm_allgather(gw_ctx* c, const void* dsend, void* drecv, size_t bytes) {
+  NvtxRange nv("gw.allgather");
   gw_comm* k = c->comm;
   if (!k || k->nranks == 1) {
     if (dsend != drecv) CU(cudaMemcpyAsync(drecv, dsend, bytes, cudaMemcpyDeviceToDevice, c->stream));
@@ -1053,6 +1061,7 @@ static gw_status grad_pass_gk(gw_ctx* c, const Prepared& P, int mode, const TSrc
 static gw_status grad_pass(gw_ctx* c, const Prepared& P, int mode, const TSrc& S, const TSrc2& S2, float* G,
                            int64_t ldG, bool store, bool obj, const double* fx, const double* fy, double alpha,
                            double* objout_dev, double beta = 0.0) {
+  NvtxRange nv(obj && !store ? "gw.objective" : "gw.grad");
   if (beta != 0.0 && (P.grid2d || P.k != 1 || obj || !store))
     return fail(GW_ERR_UNSUPPORTED, "tau != eps: only the k = 1 1-D gradient store carries the (eps - tau) ln T term");
   if (beta != 0.0) return grad_pass_k1(c, P, mode, S, S2, G, ldG, store, obj, fx, fy, alpha, objout_dev, beta);
@@ -1374,6 +1383,7 @@ static int small_cluster(gw_ctx* c, const Prepared& P, int* rows_out, size_t* by
 // sums (the only exchange), and every rank reaches the same path decision and stop flag.
 static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const float* G, int64_t ldG, double eps,
                           int iters, double tol, int check_every, int* used, int* converged, bool reset_count = true) {
+  NvtxRange nv("gw.sinkhorn");
   const int64_t nl = P.nl, m = P.m;
   const float c2f = (float)(GW_LOG2E / eps);
   // grid-stride launches: when the fused path runs, the skipped safe-path kernels cost one small wave
@@ -1709,6 +1719,7 @@ static gw_status solve_impl(gw_ctx* c, const gw_problem* pb, const gw_solve_opts
                             double* g, gw_result* res, double* trace) {
   if (!c || !o || !res) return fail(GW_ERR_INVALID_ARG, "null ctx, opts or result");
   if (!(o->eps > 0)) return fail(GW_ERR_CONFIG, "eps must be > 0");
+  NvtxRange nv("gw.solve");
   // tau (0 means tau = eps, Remark 1): the Sinkhorn regulariser; tau != eps adds
   // (eps - tau) ln T^l to the cost (k = 1, 1-D supports, T0 = p q^T)
   const double tau = (o->tau == 0) ? o->eps : o->tau;
@@ -1867,6 +1878,9 @@ static gw_status solve_impl(gw_ctx* c, const gw_problem* pb, const gw_solve_opts
   if (nl > 0) {
     E = c->hpin[0]; viol = c->hpin[1]; H = c->hpin[3]; ecc = c->hpin[6];
   }
+  if (nl > 0 && !(std::isfinite(E) && std::isfinite(H) && std::isfinite(viol)))
+    return fail(GW_ERR_NONFINITE, "non-finite result (E = %g, H = %g, violation = %g): eps too small for the "
+                "cost scale, or non-finite inputs", E, H, viol);
   const double Eout = fx ? (1.0 - alpha) * ecc + alpha * E : E;
   if (o->outer_iters > 0) {
     tr[(size_t)(o->outer_iters - 1) * 4 + 0] = Eout;
