@@ -2131,7 +2131,28 @@ static gw_status ugw_impl(gw_ctx* c, const gw_problem* pb, double rho, const gw_
     k_ugw_axpy<<<grid_for(m), 256, 0, c->stream>>>(gr, P.lq, eps_t, m, s.g);
     KCHECK();
     TRY(sink_split(c, P, s, eps_t));
-    for (int it = 0; it < o->inner.max_iter; ++it) {
+    int srows = 0;
+    size_t sbytes = 0;
+    const int sCL = (P.R == 1 && o->inner.max_iter > 0 && getenv("GWDP_NO_SMALL") == nullptr)
+                        ? small_cluster(c, P, &srows, &sbytes) : 0;
+    if (sCL > 0) {  // the whole inner loop in one cluster-resident launch (small.cuh), kappa included
+      SmallArgs sa{G, ldG, nl, m, srows, (int)((m + 1) & ~int64_t(1)), P.lp + P.row0, P.lq, eps_t, kap,
+                   o->inner.max_iter, s.f, s.g};
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(sCL);
+      cfg.blockDim = dim3(SNT);
+      cfg.dynamicSmemBytes = sbytes;
+      cfg.stream = c->stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = sCL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      CU(cudaLaunchKernelEx(&cfg, k_sink_small, sa));
+      KCHECK();
+      TRY(sink_split(c, P, s, eps_t));
+    }
+    for (int it = 0; it < (sCL > 0 ? 0 : o->inner.max_iter); ++it) {
       k_sink_row<<<rgrid, 256, 0, c->stream>>>(G, ldG, nl, m, s.gh, s.gl, c2f, s.f, s.f, P.lp + P.row0, eps_t,
                                                 s.fh, s.fl, nullptr, nullptr, nullptr, kap);
       KCHECK();
