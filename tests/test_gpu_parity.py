@@ -540,3 +540,8 @@ def test_fault_injection_is_caught(gw, monkeypatch):
     To = O.plan_from_duals(Gc.astype(np.float64), f, g, 0.02)
     assert r["fused_iters"] > 0
     assert np.max(np.abs(r["T"].cpu().numpy().astype(np.float64) - To)) > 1e-4 * np.max(To)
+
+
+def test_general_tau_degenerate_shapes(gw):
+    r = gw.solve([0.3], [0.7], [1.0], [1.0], 0.02, 3, 10, tau=0.01, return_plan=True, device=_dev())
+    assert r.T.cpu().numpy().tolist() == [[1.0]] and abs(r.gw_objective) < 1e-12

@@ -66,3 +66,16 @@ def test_ugw_large_rho_approaches_balanced_gw(gw):
     b = gw.solve(P.x, P.y, P.p, P.q, 0.04, 4, 300, return_plan=True, device=_dev())
     assert abs(r.gw_objective - b.gw_objective) <= 1e-3 * abs(b.gw_objective)
     assert abs(r.trace[-1, 3] - 1.0) <= 1e-4
+
+
+@pytest.mark.parametrize("n,m", [(1, 1), (1, 5), (6, 1)])
+def test_ugw_degenerate_shapes(gw, n, m):
+    """Single-point spaces: E = 0 (one row or column of a plan has no pair distances to mismatch);
+    the iteration still runs and matches the oracle's mass trajectory."""
+    rng = np.random.default_rng(n * 10 + m)
+    x, y = np.sort(rng.random(n)), np.sort(rng.random(m))
+    u, v = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))
+    r = gw.ugw_solve(x, y, u, v, 1.0, 0.05, 3, 30, trace_objective=True, device=_dev())
+    ro = O.entropic_ugw(x, y, u, v, 1.0, 0.05, 3, 30)
+    np.testing.assert_allclose(r.trace[:, 3], ro["mass"], rtol=1e-5)
+    assert abs(r.entropic_objective - ro["F"][-1]) <= 1e-4 * max(abs(ro["F"][-1]), 1e-12)
