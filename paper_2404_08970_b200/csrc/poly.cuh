@@ -51,45 +51,54 @@ __global__ void __launch_bounds__(PT) k_poly_moments(TSrc2 S, int64_t nl, int64_
     const float* row = S.T + j * S.ld;
     for (int64_t c0 = 4 * (int64_t)lane; c0 < m; c0 += 32 * 4 * 64) {
       float s32[PM + 1] = {0, 0, 0, 0, 0, 0};
-#pragma unroll 8
-      for (int u = 0; u < 64; ++u) {
-        const int64_t q = c0 + 128 * u;
-        const bool full = q + 3 < m;
-        float4 g = make_float4(0.f, 0.f, 0.f, 0.f), y4 = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (full) {
-          if (MODE != T_PRODUCT) g = __ldcs(reinterpret_cast<const float4*>(row + q));
-          y4 = *reinterpret_cast<const float4*>(yf + q);
-        } else if (q < m) {
-          float gt[4] = {0.f, 0.f, 0.f, 0.f}, yt[4] = {0.f, 0.f, 0.f, 0.f};
-          for (int e = 0; e < 4 && q + e < m; ++e) {
-            if (MODE != T_PRODUCT) gt[e] = row[q + e];
-            yt[e] = yf[q + e];
-          }
-          g = make_float4(gt[0], gt[1], gt[2], gt[3]);
-          y4 = make_float4(yt[0], yt[1], yt[2], yt[3]);
-        }
-        const float gv[4] = {g.x, g.y, g.z, g.w};
-        const float yv[4] = {y4.x, y4.y, y4.z, y4.w};
+      for (int u0 = 0; u0 < 64; u0 += 8) {
+        if (c0 + 128 * u0 >= m) break;  // uniform (all lanes' q differ by < 128)
+        // the loads of 8 steps first (independent: latency overlapped), then their arithmetic
+        float4 gv4[8], yv4[8];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          if (q + e < m) {
-            const float t = p_regen(MODE, S, gv[e], Fh, Fl, q + e);
-            const float y = yv[e];
-            float yp = t;
-            s32[0] += yp;
-            yp *= y; s32[1] += yp;
-            yp *= y; s32[2] += yp;
-            yp *= y; s32[3] += yp;
-            yp *= y; s32[4] += yp;
-            if (OBJ && t > 0.f) {
-              float lt;
-              if (MODE == T_GIBBS) {
-                lt = ((fmaf(gv[e], -S.ch, S.gh[q + e]) + Fh) + fmaf(gv[e], -S.cl, S.gl[q + e] + Fl)) *
-                     0.6931471805599453f;
-              } else {
-                lt = __logf(t);
+        for (int v = 0; v < 8; ++v) {
+          const int64_t q = c0 + 128 * (u0 + v);
+          gv4[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+          yv4[v] = gv4[v];
+          if (q + 3 < m) {
+            if (MODE != T_PRODUCT) gv4[v] = __ldcs(reinterpret_cast<const float4*>(row + q));
+            yv4[v] = *reinterpret_cast<const float4*>(yf + q);
+          } else if (q < m) {
+            float gt[4] = {0.f, 0.f, 0.f, 0.f}, yt[4] = {0.f, 0.f, 0.f, 0.f};
+            for (int e = 0; e < 4 && q + e < m; ++e) {
+              if (MODE != T_PRODUCT) gt[e] = row[q + e];
+              yt[e] = yf[q + e];
+            }
+            gv4[v] = make_float4(gt[0], gt[1], gt[2], gt[3]);
+            yv4[v] = make_float4(yt[0], yt[1], yt[2], yt[3]);
+          }
+        }
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const int64_t q = c0 + 128 * (u0 + v);
+          const float gv[4] = {gv4[v].x, gv4[v].y, gv4[v].z, gv4[v].w};
+          const float yv[4] = {yv4[v].x, yv4[v].y, yv4[v].z, yv4[v].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            if (q + e < m) {
+              const float t = p_regen(MODE, S, gv[e], Fh, Fl, q + e);
+              const float y = yv[e];
+              float yp = t;
+              s32[0] += yp;
+              yp *= y; s32[1] += yp;
+              yp *= y; s32[2] += yp;
+              yp *= y; s32[3] += yp;
+              yp *= y; s32[4] += yp;
+              if (OBJ && t > 0.f) {
+                float lt;
+                if (MODE == T_GIBBS) {
+                  lt = ((fmaf(gv[e], -S.ch, S.gh[q + e]) + Fh) + fmaf(gv[e], -S.cl, S.gl[q + e] + Fl)) *
+                       0.6931471805599453f;
+                } else {
+                  lt = __logf(t);
+                }
+                s32[5] += t * (lt - 1.f);
               }
-              s32[5] += t * (lt - 1.f);
             }
           }
         }
