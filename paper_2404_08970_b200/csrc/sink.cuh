@@ -47,33 +47,45 @@ __global__ void __launch_bounds__(256) k_sink_row(const float* __restrict__ G, i
       hv[k] = v ? gh[q + k] : -INFINITY;
       lv[k] = v ? gl[q + k] : 0.f;
     }
+    // rows in groups of 4: the group's 8 float4 loads are issued before their arithmetic
 #pragma unroll
-    for (int r = 0; r < RROWS; ++r) {
-      if (r < nr) {
-        const float* gr = G + (r0 + r) * ld + q;
-        const float4 x0 = __ldcs(reinterpret_cast<const float4*>(gr));
-        float4 x1 = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (q + 4 < m) x1 = __ldcs(reinterpret_cast<const float4*>(gr + 4));
-        const float gv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-        float av[8];
-        float cm = -INFINITY;
+    for (int r4 = 0; r4 < RROWS; r4 += 4) {
+      float4 x0[4], x1[4];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          av[k] = (q + k < m) ? fmaf(gv[k], -c2f, hv[k]) + lv[k] : -INFINITY;
-          cm = fmaxf(cm, av[k]);
+      for (int u = 0; u < 4; ++u) {
+        x0[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        x1[u] = x0[u];
+        if (r4 + u < nr) {
+          const float* gr = G + (r0 + r4 + u) * ld + q;
+          x0[u] = __ldcs(reinterpret_cast<const float4*>(gr));
+          if (q + 4 < m) x1[u] = __ldcs(reinterpret_cast<const float4*>(gr + 4));
         }
-        LSE2 s = st[r];
-        if (cm > s.m) {
-          s.s = (s.m == -INFINITY) ? 0.f : s.s * exp2f(s.m - cm);
-          s.m = cm;
-        }
-        if (s.m != -INFINITY) {
-          float acc = 0.f;
+      }
 #pragma unroll
-          for (int k = 0; k < 8; ++k) acc += exp2f(av[k] - s.m);
-          s.s += acc;
+      for (int u = 0; u < 4; ++u) {
+        const int r = r4 + u;
+        if (r < nr) {
+          const float gv[8] = {x0[u].x, x0[u].y, x0[u].z, x0[u].w, x1[u].x, x1[u].y, x1[u].z, x1[u].w};
+          float av[8];
+          float cm = -INFINITY;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            av[k] = (q + k < m) ? fmaf(gv[k], -c2f, hv[k]) + lv[k] : -INFINITY;
+            cm = fmaxf(cm, av[k]);
+          }
+          LSE2 s = st[r];
+          if (cm > s.m) {
+            s.s = (s.m == -INFINITY) ? 0.f : s.s * exp2f(s.m - cm);
+            s.m = cm;
+          }
+          if (s.m != -INFINITY) {
+            float acc = 0.f;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc += exp2f(av[k] - s.m);
+            s.s += acc;
+          }
+          st[r] = s;
         }
-        st[r] = s;
       }
     }
   }
@@ -130,34 +142,39 @@ __global__ void __launch_bounds__(256) k_sink_col(const float* __restrict__ G, i
   for (int k = 0; k < 4; ++k) st[k] = LSE2{-INFINITY, 0.f};
   const float* base = G + q0;
   int64_t r = rs;
-  for (; r + 4 <= re; r += 4) {
-    float4 x[4];
-    float fr[4];
+  for (; r + 8 <= re; r += 8) {  // 8 rows' loads in flight per thread
+    float4 x[8];
+    float fr[8], fo[8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      x[u] = __ldcs(reinterpret_cast<const float4*>(base + (r + u) * ld));
+    for (int u = 0; u < 8; ++u) x[u] = __ldcs(reinterpret_cast<const float4*>(base + (r + u) * ld));
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      fr[u] = fh[r + u];
+      fo[u] = fl[r + u];
     }
+    float a[8][4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) fr[u] = fh[r + u];
-    float a[4][4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const float lo = fl[r + u];
-      a[u][0] = fmaf(x[u].x, -c2f, fr[u]) + lo;
-      a[u][1] = fmaf(x[u].y, -c2f, fr[u]) + lo;
-      a[u][2] = fmaf(x[u].z, -c2f, fr[u]) + lo;
-      a[u][3] = fmaf(x[u].w, -c2f, fr[u]) + lo;
+    for (int u = 0; u < 8; ++u) {
+      a[u][0] = fmaf(x[u].x, -c2f, fr[u]) + fo[u];
+      a[u][1] = fmaf(x[u].y, -c2f, fr[u]) + fo[u];
+      a[u][2] = fmaf(x[u].z, -c2f, fr[u]) + fo[u];
+      a[u][3] = fmaf(x[u].w, -c2f, fr[u]) + fo[u];
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const float cm = fmaxf(fmaxf(a[0][k], a[1][k]), fmaxf(a[2][k], a[3][k]));
+      float cm = a[0][k];
+#pragma unroll
+      for (int u = 1; u < 8; ++u) cm = fmaxf(cm, a[u][k]);
       if (cm > st[k].m) {
         st[k].s = (st[k].m == -INFINITY) ? 0.f : st[k].s * exp2f(st[k].m - cm);
         st[k].m = cm;
       }
-      if (st[k].m != -INFINITY)
-        st[k].s += exp2f(a[0][k] - st[k].m) + exp2f(a[1][k] - st[k].m) + exp2f(a[2][k] - st[k].m) +
-                   exp2f(a[3][k] - st[k].m);
+      if (st[k].m != -INFINITY) {
+        float acc = 0.f;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc += exp2f(a[u][k] - st[k].m);
+        st[k].s += acc;
+      }
     }
   }
   for (; r < re; ++r) {
