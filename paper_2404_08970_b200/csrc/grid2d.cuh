@@ -303,17 +303,27 @@ __global__ void __launch_bounds__(256) k_g2_colsum(TSrc2 S, int64_t nl, int64_t 
   if (q >= m) return;
   const int64_t r1 = min(nl, r0 + 256);
   double acc = 0.0;
-  for (int64_t i = r0; i < r1; ++i) {
-    float t;
-    if (MODE == T_EXPLICIT) {
-      t = S.T[i * S.ld + q];
-    } else if (MODE == T_PRODUCT) {
-      t = S.fh[i] * S.gh[q];
-    } else {
-      const float g = S.T[i * S.ld + q];
-      t = ex2_ftz((fmaf(g, -S.ch, S.gh[q]) + S.fh[i]) + fmaf(g, -S.cl, S.gl[q] + S.fl[i]));
+  float ghq = 0.f, glq = 0.f;
+  if (MODE != T_EXPLICIT) ghq = S.gh[q];
+  if (MODE == T_GIBBS) glq = S.gl[q];
+  for (int64_t i0 = r0; i0 < r1; i0 += 8) {
+    float g8[8];  // 8 rows' loads first
+#pragma unroll
+    for (int v = 0; v < 8; ++v) g8[v] = (MODE != T_PRODUCT && i0 + v < r1) ? S.T[(i0 + v) * S.ld + q] : 0.f;
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const int64_t i = i0 + v;
+      if (i >= r1) break;
+      float t;
+      if (MODE == T_EXPLICIT) {
+        t = g8[v];
+      } else if (MODE == T_PRODUCT) {
+        t = S.fh[i] * ghq;
+      } else {
+        t = ex2_ftz((fmaf(g8[v], -S.ch, ghq) + S.fh[i]) + fmaf(g8[v], -S.cl, glq + S.fl[i]));
+      }
+      acc += (double)t;
     }
-    acc += (double)t;
   }
   part[(int64_t)blockIdx.y * m + q] = acc;
 }

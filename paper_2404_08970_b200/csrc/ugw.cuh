@@ -25,19 +25,33 @@ __global__ void __launch_bounds__(256) k_ugw_rowstats(TSrc2 S, int64_t nl, int64
     double sa = 0.0, sc = 0.0;
     for (int64_t c0 = 4 * (int64_t)lane; c0 < m; c0 += 128 * 64) {
       float pa = 0.f, pc = 0.f;
-#pragma unroll 4
-      for (int u = 0; u < 64; ++u) {
-        const int64_t q = c0 + 128 * u;
-        if (q >= m) break;
-        const float4 g4 = *reinterpret_cast<const float4*>(row + q);
-        const float gv[4] = {g4.x, g4.y, g4.z, g4.w};
+      for (int u0 = 0; u0 < 64; u0 += 8) {
+        if (c0 + 128 * u0 >= m) break;  // uniform
+        float4 g4[8];  // the loads of 8 steps first
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          if (q + e < m) {
-            const float g = gv[e];
-            const float t = ex2_ftz((fmaf(g, -S.ch, S.gh[q + e]) + Fh) + fmaf(g, -S.cl, S.gl[q + e] + Fl));
-            pa += t;
-            pc = fmaf(g, t, pc);
+        for (int v = 0; v < 8; ++v) {
+          const int64_t q = c0 + 128 * (u0 + v);
+          g4[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (q + 3 < m) {
+            g4[v] = *reinterpret_cast<const float4*>(row + q);
+          } else if (q < m) {
+            float gt[4] = {0.f, 0.f, 0.f, 0.f};
+            for (int e = 0; e < 4 && q + e < m; ++e) gt[e] = row[q + e];
+            g4[v] = make_float4(gt[0], gt[1], gt[2], gt[3]);
+          }
+        }
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const int64_t q = c0 + 128 * (u0 + v);
+          const float gv[4] = {g4[v].x, g4[v].y, g4[v].z, g4[v].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            if (q + e < m) {
+              const float g = gv[e];
+              const float t = ex2_ftz((fmaf(g, -S.ch, S.gh[q + e]) + Fh) + fmaf(g, -S.cl, S.gl[q + e] + Fl));
+              pa += t;
+              pc = fmaf(g, t, pc);
+            }
           }
         }
       }
