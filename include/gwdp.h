@@ -240,6 +240,9 @@ gw_status fgw_solve(gw_ctx *ctx, const gw_problem *prob, const double *fx, const
  * gradient with the REALISED marginals a = G^1, b = G^T1, unbalanced Sinkhorn with
  * kappa = rho~/(rho~+eps~) (opts->inner.max_iter fixed iterations; tol must be 0), G^0 = u v and
  * the mass rescaling sqrt(m(G^)/m(G)) after each subproblem.
+ *   prob     p = u, q = v: nonnegative measures of ANY positive mass (not normalised here; the
+ *            |sum - 1| check of the balanced solvers is skipped, m(u), m(v) > 0 is required);
+ *            G^0 = u v / sqrt(m(u) m(v)) (R35).
  *   rho      > 0 (finite); opts->eps > 0, opts->tau = eps or 0; T0 must be NULL.
  *   T_out    nullable: the final plan (fp32, ldT).  f, g: the subproblem's final duals in R34's
  *            convention (G = exp((f + g - C)/eps~) u v before the rescaling).

@@ -379,6 +379,7 @@ struct Prepared {
   double *xc, *yc, *pn, *qn, *lp, *lq, *cx, *cy;
   float *pnf, *qnf;  // fp32 copies of the normalised marginals (T^0 = p q^T on the fp32 gradient path)
   float* yf;         // fp32 centred y (k = 2 path)
+  double mass_p = 1.0, mass_q = 1.0;  // m(u), m(v): 1 except for ugw_solve (weights not normalised)
   double xlast, ylast;
   int k = 1;         // distance power
   bool grid2d = false;  // GW_GRID2D: xc / yc are the centred axes (nx, ny entries)
@@ -529,7 +530,9 @@ static gw_status prepare_2d(gw_ctx* c, const gw_problem* pb, Prepared& P) {
   return shard_table(c, P);
 }
 
-static gw_status prepare(gw_ctx* c, const gw_problem* pb, Prepared& P) {
+// unbalanced (ugw_solve only): p, q are positive measures of any mass; they are kept as given
+// (P.pn = p, P.lp = log p, P.cx = (D o D) p) and their masses recorded in P.mass_p / P.mass_q.
+static gw_status prepare(gw_ctx* c, const gw_problem* pb, Prepared& P, bool unbalanced = false) {
   TRY(check_problem(pb));
   if (pb->flags & GW_GRID2D) return prepare_2d(c, pb, P);
   const int64_t n = pb->n, m = pb->m;
@@ -562,13 +565,19 @@ static gw_status prepare(gw_ctx* c, const gw_problem* pb, Prepared& P) {
     if (h[2] != 0 || h[10] != 0) return fail(GW_ERR_NONFINITE, "non-finite entry in x, y, p or q");
     if (h[0] != 0 || h[8] != 0) return fail(GW_ERR_UNSORTED, "x and y must be non-decreasing (reading R16)");
     if (h[1] != 0 || h[9] != 0) return fail(GW_ERR_NEGATIVE_WEIGHT, "p and q must be >= 0");
-    if (fabs(h[3] - 1.0) > 1e-9 || fabs(h[11] - 1.0) > 1e-9)
+    if (!unbalanced && (fabs(h[3] - 1.0) > 1e-9 || fabs(h[11] - 1.0) > 1e-9))
       return fail(GW_ERR_NOT_NORMALIZED, "|sum p - 1| = %.3g, |sum q - 1| = %.3g exceed 1e-9 (SPEC.md:72)",
                   fabs(h[3] - 1.0), fabs(h[11] - 1.0));
   }
-  k_prep<<<grid_for(n), 256, 0, c->stream>>>(P.x, P.p, n, mom, xc, pn, lp, cx);
+  if (unbalanced) {
+    if (!(h[3] > 0.0) || !(h[11] > 0.0))
+      return fail(GW_ERR_NOT_NORMALIZED, "ugw_solve: the masses m(u) = %.3g, m(v) = %.3g must be > 0", h[3], h[11]);
+    P.mass_p = h[3];
+    P.mass_q = h[11];
+  }
+  k_prep<<<grid_for(n), 256, 0, c->stream>>>(P.x, P.p, n, mom, xc, pn, lp, cx, !unbalanced);
   KCHECK();
-  k_prep<<<grid_for(m), 256, 0, c->stream>>>(P.y, P.q, m, mom + 8, yc, qn, lq, cy);
+  k_prep<<<grid_for(m), 256, 0, c->stream>>>(P.y, P.q, m, mom + 8, yc, qn, lq, cy, !unbalanced);
   KCHECK();
   P.xc = xc; P.yc = yc; P.pn = pn; P.qn = qn; P.lp = lp; P.lq = lq; P.cx = cx; P.cy = cy;
   P.k = pb->k;
@@ -2010,10 +2019,11 @@ static gw_status ugw_gather_rows(gw_ctx* c, const Prepared& P, const double* loc
 }
 
 // F_eps (reading R33) from E and the plan statistics (m(u) = m(v) = 1)
-static double ugw_F(double E, const UgwStats& st, double rho, double eps) {
+// R33 with KL(x (x) x | y (x) y) = 2 m(x) <x, log(x/y)> - m(x)^2 + m(y)^2; mu = m(u), mv = m(v)
+static double ugw_F(double E, const UgwStats& st, double rho, double eps, double mu, double mv) {
   const double mm = st.mass;
-  return E + rho * (2.0 * mm * st.A1 - mm * mm + 1.0) + rho * (2.0 * mm * st.B1 - mm * mm + 1.0) +
-         eps * (2.0 * mm * st.KL - mm * mm + 1.0);
+  return E + rho * (2.0 * mm * st.A1 - mm * mm + mu * mu) + rho * (2.0 * mm * st.B1 - mm * mm + mv * mv) +
+         eps * (2.0 * mm * st.KL - mm * mm + (mu * mv) * (mu * mv));
 }
 
 // Entropic UGW (Remark 3) with readings R32-R35: per outer iteration
@@ -2037,7 +2047,8 @@ static gw_status ugw_impl(gw_ctx* c, const gw_problem* pb, double rho, const gw_
   CU(cudaSetDevice(c->device));
   const double eps = o->eps;
   Prepared P;
-  TRY(prepare(c, pb, P));
+  TRY(prepare(c, pb, P, true));
+  const double mu = P.mass_p, mv = P.mass_q, m0 = std::sqrt(mu * mv);
   const int64_t nl = P.nl, m = P.m;
   const int64_t ldG = (m + 31) & ~int64_t(31);
   float* G;
@@ -2069,8 +2080,18 @@ static gw_status ugw_impl(gw_ctx* c, const gw_problem* pb, double rho, const gw_
   CU(cudaEventRecord(ev0, c->stream));
   const unsigned cgrid = (unsigned)std::min<int64_t>(((m + 1023) / 1024) * s.nrb, 148 * 4);
   const unsigned rgrid = (unsigned)std::min<int64_t>((nl + RROWS - 1) / RROWS, 148 * 4);
-  // T^0 = u v (R35): a = u, b = v, m = 1, every log ratio 0
-  UgwStats st{1.0, 0.0, 0.0, 0.0};
+  // T^0 = u v / m0, m0 = sqrt(m(u) m(v)) (R35): a = u sqrt(mv/mu), b = v sqrt(mu/mv), m(T^0) = m0
+  UgwStats st{m0, 0.5 * m0 * std::log(mv / mu), 0.5 * m0 * std::log(mu / mv), -0.5 * m0 * std::log(mu * mv)};
+  // the product form of T^0 for the gradient kernels: rows u / m0 (local, fp64 in Fs and fp32 in s.fh,
+  // both free until the first Sinkhorn split), columns v
+  auto product_src = [&](TSrc& S, TSrc2& S2) -> gw_status {
+    k_scale<<<grid_for(nl), 256, 0, c->stream>>>(P.pn + P.row0, nl, 1.0 / m0, Fs);
+    k_scale_f<<<grid_for(nl), 256, 0, c->stream>>>(P.pn + P.row0, nl, 1.0 / m0, s.fh);
+    KCHECK();
+    S = TSrc{nullptr, 0, Fs, P.qn, 0.0};
+    S2 = TSrc2{nullptr, 0, s.fh, nullptr, P.qnf, nullptr, 0.f, 0.f};
+    return GW_OK;
+  };
   double eps_reg = 0.0;  // regulariser of the current implicit plan (l > 0)
   int inner_total = 0;
   // E of the current plan (objective pass on the Gibbs form, realised marginals)
@@ -2092,12 +2113,15 @@ static gw_status ugw_impl(gw_ctx* c, const gw_problem* pb, double rho, const gw_
   for (int l = 0; l < o->outer_iters; ++l) {
     // ---- cost C = grad E(T^) (realised a, b) + 2 g(T^) (R32) ----
     const double gconst = rho * st.A1 + rho * st.B1 + eps * st.KL;
-    const double* aw = P.pn;  // T^0: a = u (all rows)
     if (l > 0) {
       TRY(ugw_gather_rows(c, P, av, afull));
-      aw = afull;
+    } else {  // T^0: a = u sqrt(mv/mu) (all rows), b = v sqrt(mu/mv)
+      k_scale<<<grid_for(n), 256, 0, c->stream>>>(P.pn, n, std::sqrt(mv / mu), afull);
+      k_scale<<<grid_for(m), 256, 0, c->stream>>>(P.qn, m, std::sqrt(mu / mv), bv);
+      KCHECK();
     }
-    const double* bw = (l == 0) ? P.qn : bv;
+    const double* aw = afull;
+    const double* bw = bv;
     TRY(dd_const(c, P.k, P.xc, aw, n, ca));
     TRY(dd_const(c, P.k, P.yc, bw, m, cb));
     k_ugw_addc<<<grid_for(n), 256, 0, c->stream>>>(ca, gconst, n);
@@ -2110,8 +2134,7 @@ static gw_status ugw_impl(gw_ctx* c, const gw_problem* pb, double rho, const gw_
     TSrc2 S2;
     if (l == 0) {
       mode = T_PRODUCT;
-      S = TSrc{nullptr, 0, P.pn + P.row0, P.qn, 0.0};
-      S2 = TSrc2{nullptr, 0, P.pnf + P.row0, nullptr, P.qnf, nullptr, 0.f, 0.f};
+      TRY(product_src(S, S2));
     } else {
       mode = T_GIBBS;
       const double cc = GW_LOG2E / eps_reg;
@@ -2189,15 +2212,16 @@ static gw_status ugw_impl(gw_ctx* c, const gw_problem* pb, double rho, const gw_
     if (want_trace_obj && l + 1 < o->outer_iters) {
       double E;
       TRY(plan_E(&E, nullptr));
-      tr[(size_t)l * 4 + 0] = ugw_F(E, st, rho, eps);
+      tr[(size_t)l * 4 + 0] = ugw_F(E, st, rho, eps, mu, mv);
       tr[(size_t)l * 4 + 1] = E;
     }
   }
   // ---- final plan: E, F, violation (vs u, v; informational) ----
   double E = 0.0, viol = 0.0;
   if (o->outer_iters == 0) {
-    const TSrc S{nullptr, 0, P.pn + P.row0, P.qn, 0.0};
-    const TSrc2 S2{nullptr, 0, P.pnf + P.row0, nullptr, P.qnf, nullptr, 0.f, 0.f};
+    TSrc S;
+    TSrc2 S2;
+    TRY(product_src(S, S2));
     TRY(grad_pass(c, P, T_PRODUCT, S, S2, nullptr, 0, false, true, nullptr, nullptr, 1.0, objout));
     CU(cudaMemcpyAsync(c->hpin, objout, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
@@ -2208,7 +2232,7 @@ static gw_status ugw_impl(gw_ctx* c, const gw_problem* pb, double rho, const gw_
     TRY(plan_E(&E, &viol));
     if (T_out) TRY(materialize(c, P, T_GIBBS, TSrc{G, ldG, Fs, Gs2, GW_LOG2E / eps_reg}, T_out, ldT));
   }
-  const double F = ugw_F(E, st, rho, eps);
+  const double F = ugw_F(E, st, rho, eps, mu, mv);
   if (o->outer_iters > 0) {
     tr[(size_t)(o->outer_iters - 1) * 4 + 0] = F;
     tr[(size_t)(o->outer_iters - 1) * 4 + 1] = E;

@@ -51,16 +51,17 @@ __global__ void __launch_bounds__(1024) k_validate(const double* __restrict__ x0
 // ---------------------------------------------------------------------------------
 __global__ void k_prep(const double* __restrict__ x, const double* __restrict__ w, int64_t n,
                        const double* __restrict__ mom, double* __restrict__ xc, double* __restrict__ wn,
-                       double* __restrict__ lw, double* __restrict__ cvec) {
+                       double* __restrict__ lw, double* __restrict__ cvec, bool normalize = true) {
+  // normalize = false (unbalanced GW): wn = w as given (mass S0), cvec = (D o D) w = S0 (v^2 - 2 v mu1 + mu2)
   const double xmid = mom[6], S0 = mom[3];
-  const double mu1 = mom[4] / S0, mu2 = mom[5] / S0, inv = 1.0 / S0;
+  const double mu1 = mom[4] / S0, mu2 = mom[5] / S0, inv = normalize ? 1.0 / S0 : 1.0, cs = normalize ? 1.0 : S0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const double v = x[i] - xmid;
     const double wv = w[i] * inv;
     xc[i] = v;
     wn[i] = wv;
     lw[i] = log(wv);
-    cvec[i] = v * v - 2.0 * v * mu1 + mu2;
+    cvec[i] = cs * (v * v - 2.0 * v * mu1 + mu2);
   }
 }
 

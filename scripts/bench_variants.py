@@ -165,6 +165,35 @@ def main():
           "inner": 100, "ms": ms, "outer_iter_per_s": 2 / (ms / 1e3), "inner_fused": r.inner_fused_total,
           "algorithmic_bytes": 2 * (12 + 400) * nm3, "GBps": 2 * (12 + 400) * nm3 / ms / 1e6,
           "gw_objective": r.gw_objective})
+    # ---- unbalanced GW (row f4) at N = M = 16384, rho = 1, eps = 1e-2 (readings R32-R35) ----
+    u3 = rng.random(n3) + 0.5
+    u3 /= u3.sum()
+    v3 = rng.random(n3) + 0.5
+    v3 *= 1.3 / v3.sum()
+    with torch.cuda.stream(stream):
+        r = None
+
+        def runu():
+            nonlocal r
+            r = api.ugw_solve(x3, y3, u3, v3, 1.0, 1e-2, 2, 50, device=dev, ctx=ctx)
+        ms = timed(runu, 1, stream)
+    emit({"variant": "ugw_solve", "row": "f4", "N": n3, "M": n3, "rho": 1.0, "eps": 1e-2, "outer": 2,
+          "inner": 50, "ms": ms, "outer_iter_per_s": 2 / (ms / 1e3),
+          "algorithmic_bytes": 2 * (16 + 50 * 8) * nm3,
+          "bytes_note": "per outer: plan stats 4NM + gradient 12NM + 50 safe-path iterations (row read + column read) 8NM",
+          "GBps": 2 * (16 + 50 * 8) * nm3 / ms / 1e6})
+    # ---- tau != eps (reading R6) on the same problem: cost G + (eps - tau) ln T ----
+    with torch.cuda.stream(stream):
+        r = None
+
+        def runt():
+            nonlocal r
+            r = api.solve(x3, y3, p3, p3, 1e-2, 2, 100, device=dev, ctx=ctx, tau=5e-3)
+        ms = timed(runt, 1, stream)
+    emit({"variant": "entropic_gw_solve tau=eps/2", "row": "a (tau)", "N": n3, "M": n3, "eps": 1e-2, "tau": 5e-3,
+          "outer": 2, "inner": 100, "ms": ms, "outer_iter_per_s": 2 / (ms / 1e3), "inner_fused": r.inner_fused_total,
+          "algorithmic_bytes": 2 * (12 + 400) * nm3, "GBps": 2 * (12 + 400) * nm3 / ms / 1e6,
+          "gw_objective": r.gw_objective})
     ctx.close()
 
 

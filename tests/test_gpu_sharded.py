@@ -269,11 +269,13 @@ def test_sharded_grid2d_grad_and_solve(gw):
     assert abs(out[0][2] - ro["gw_objective"]) <= 1e-4 * abs(ro["gw_objective"])
 
 
-def test_sharded_ugw(gw):
+@pytest.mark.parametrize("su,sv", [(1.0, 1.0), (0.6, 1.7)])
+def test_sharded_ugw(gw, su, sv):
     """UGW sharded by rows: the plan statistics' row parts add over the ranks, b and the column
-    LSE pairs are gathered; same trajectory as one rank."""
+    LSE pairs are gathered; same trajectory as one rank (also for masses != 1)."""
     api, dist = gw
     P = _c5(300, 260, 4, 40)
+    P.p, P.q = su * P.p, sv * P.q
     r1 = api.ugw_solve(P.x, P.y, P.p, P.q, 1.0, 0.01, P.outer, P.inner, trace_objective=True)
 
     def fn(r, ctx, st):

@@ -79,3 +79,39 @@ def test_ugw_degenerate_shapes(gw, n, m):
     ro = O.entropic_ugw(x, y, u, v, 1.0, 0.05, 3, 30)
     np.testing.assert_allclose(r.trace[:, 3], ro["mass"], rtol=1e-5)
     assert abs(r.entropic_objective - ro["F"][-1]) <= 1e-4 * max(abs(ro["F"][-1]), 1e-12)
+
+
+@pytest.mark.parametrize("n,m,k,su,sv", [(300, 256, 1, 0.6, 1.7), (200, 180, 2, 2.5, 0.8), (150, 160, 3, 1.0, 0.4)])
+def test_ugw_trajectory_unequal_masses(gw, n, m, k, su, sv):
+    """Unbalanced inputs proper: u, v of masses != 1 (and != each other), G^0 = u v / sqrt(m(u) m(v))
+    (R35), KL constants m(u)^2, m(v)^2, (m(u) m(v))^2 in F_eps (R33)."""
+    P = W.config5(n, m)
+    u, v = su * P.p, sv * P.q
+    outer, inner = 4, 60
+    r = gw.ugw_solve(P.x, P.y, u, v, 1.0, 0.01, outer, inner, trace_objective=True, return_plan=True,
+                     device=_dev(), k=k)
+    ro = O.entropic_ugw(P.x, P.y, u, v, 1.0, 0.01, outer, inner, k=k)
+    F, E, mass = np.asarray(ro["F"]), np.asarray(ro["E"]), np.asarray(ro["mass"])
+    assert np.max(np.abs(r.trace[:, 0] - F) / np.abs(F)) <= OBJ_TOL
+    assert np.max(np.abs(r.trace[:, 1] - E) / np.abs(E)) <= OBJ_TOL
+    np.testing.assert_allclose(r.trace[:, 3], mass, rtol=1e-5)
+    T = r.T.cpu().numpy().astype(np.float64)
+    assert np.max(np.abs(T - ro["T"])) <= 1e-3 * np.max(ro["T"])
+
+
+def test_ugw_zero_outer_unequal_masses(gw):
+    P = W.config5(64, 48)
+    u, v = 0.5 * P.p, 3.0 * P.q
+    r = gw.ugw_solve(P.x, P.y, u, v, 1.0, 0.01, 0, 10, return_plan=True, device=_dev())
+    T0 = np.outer(u, v) / np.sqrt(u.sum() * v.sum())
+    np.testing.assert_allclose(r.T.cpu().numpy(), T0, rtol=1e-6, atol=1e-12)
+    assert abs(r.gw_objective - O.objective(P.x, P.y, T0)) <= 1e-6 * abs(r.gw_objective)
+    Fo = O.ugw_functional(P.x, P.y, u, v, T0, 1.0, 0.01)
+    assert abs(r.entropic_objective - Fo) <= 1e-6 * abs(Fo)
+
+
+def test_ugw_rejects_zero_mass(gw):
+    from paper_2404_08970_b200._lib import GwError
+    P = W.config5(16, 12)
+    with pytest.raises(GwError):
+        gw.ugw_solve(P.x, P.y, np.zeros(16), P.q, 1.0, 0.01, 1, 5, device=_dev())

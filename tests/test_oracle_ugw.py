@@ -33,12 +33,14 @@ def test_functional_closed_form_is_bruteforce():
         assert abs(a - b) <= 1e-12 * max(1.0, abs(b))
 
 
-@pytest.mark.parametrize("k", [1, 2])
-def test_ugw_cost_is_half_gradient_of_functional(k):
+@pytest.mark.parametrize("k,su,sv", [(1, 1.0, 1.0), (2, 1.0, 1.0), (1, 0.6, 1.7)])
+def test_ugw_cost_is_half_gradient_of_functional(k, su, sv):
     """R32: the subproblem's linearised objective L(G) = <C(G^), G> + m(G^) (rho KL(G1|u) +
     rho KL(G^T1|v) + eps KL(G|uv)) has gradient 1/2 grad F_eps at G = G^ (F_eps brute force,
-    central differences): this fixes g(G^) and the realised-marginal 1/2 grad E."""
+    central differences): this fixes g(G^) and the realised-marginal 1/2 grad E.  Also for
+    measures u, v of mass != 1 (unbalanced inputs)."""
     rng, x, y, u, v = _problem(2 + k, 4, 3)
+    u, v = su * u, sv * v
     Gh = rng.random((4, 3)) * 0.15 + 0.01
     rho, eps = 0.8, 0.07
     C = O.ugw_cost(x, y, u, v, Gh, rho, eps, k)
@@ -101,3 +103,20 @@ def test_ugw_mass_rescaling_and_symmetry():
     r2 = O.entropic_ugw(y, x, v, u, 0.5, 0.05, 3, 200)
     np.testing.assert_allclose(r1["F"], r2["F"], rtol=1e-10)
     assert all(0.0 < mm < 1.0 + 1e-9 for mm in r1["mass"])
+
+
+def test_ugw_start_and_masses():
+    """R35 for measures of any mass: the iteration starts from u v / sqrt(m(u) m(v)), so its first
+    functional value is the brute-force F_eps of that plan after one step of mass balance, and the
+    mass trajectory stays positive; scaling both u and v by the same s leaves the balanced-mass
+    plan's realised marginals proportional to u and v at G^0 (checked on the start plan)."""
+    _, x, y, u, v = _problem(7, 5, 4)
+    u, v = 0.6 * u, 1.7 * v
+    r0 = O.entropic_ugw(x, y, u, v, 0.5, 0.05, 0, 10)
+    G0 = np.asarray(r0["T"])
+    np.testing.assert_allclose(G0, np.outer(u, v) / math.sqrt(u.sum() * v.sum()), rtol=1e-15)
+    np.testing.assert_allclose(G0.sum(), math.sqrt(u.sum() * v.sum()), rtol=1e-14)
+    r = O.entropic_ugw(x, y, u, v, 0.5, 0.05, 2, 200)
+    assert all(mm > 0.0 for mm in r["mass"])
+    Fb = O.ugw_functional_bruteforce(x, y, u, v, r["T"], 0.5, 0.05, 1)
+    assert abs(r["F"][-1] - Fb) <= 1e-12 * max(1.0, abs(Fb))
