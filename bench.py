@@ -269,6 +269,9 @@ def main():
         units, byt = per_unit[name]
         ms_unit = ms_c[k] / units
         d = {"ms_total": ms_c[k], "units": units, "ms_per_unit": ms_unit}
+        if name in ("sink_row", "sink_col"):
+            d["note"] = ("ms_total includes the device-gated launches that exit at once in fused iterations "
+                         "(one per iteration); units = safe-path iterations only, so ms_per_unit overstates")
         if byt:
             d["GBps"] = byt / (ms_unit / 1e3) / 1e9
             d["frac"] = d["GBps"] / hbm
