@@ -276,9 +276,12 @@ def main():
             d["GBps"] = byt / (ms_unit / 1e3) / 1e9
             d["frac"] = d["GBps"] / hbm
         kern[name] = d
-    sf = kern["sink_fused"]
-    traffic = ncu_traffic("sink_fused_N%d_R%d" % (args.n, world))
-    roof = {"bound": "hbm", "kernel": "k_sink_fused (one-read Sinkhorn iteration)", "achieved": sf["GBps"],
+    if "sink_fused" in kern:
+        sf, kname = kern["sink_fused"], "k_sink_fused (one-read Sinkhorn iteration)"
+        traffic = ncu_traffic("sink_fused_N%d_R%d" % (args.n, world))
+    else:  # GWDP_NO_FUSED=1: the safe path's column half-step dominates
+        sf, kname, traffic = kern["sink_col"], "k_sink_col (safe-path column half-step)", None
+    roof = {"bound": "hbm", "kernel": kname, "achieved": sf["GBps"],
             "peak": hbm, "unit": "GB/s", "frac": sf["frac"], "traffic": traffic, "peak_source": peak_src,
             "algorithmic_bytes_per_launch": 4 * nm_bytes,
             "algorithmic_bytes_note": "4 B x N_local x M: one fp32 read of G per iteration (SURVEY §8d)",
@@ -288,7 +291,9 @@ def main():
     grad = {"ms_per_gradient": grad_ms, "algorithmic_bytes": 12 * nm_bytes,
             "GBps_algorithmic": 12 * nm_bytes / (grad_ms / 1e3) / 1e9,
             "frac_of_peak": 12 * nm_bytes / (grad_ms / 1e3) / 1e9 / hbm,
-            "note": "moments pass (4NM) + main pass (8NM: read T or the cost it is regenerated from, write G)"}
+            "note": "moments pass (4NM) + main pass (8NM: read T or the cost it is regenerated from, write G); "
+                    "averaged over the solve's gradients, the first of which is on the product plan p q^T "
+                    "(no plan read), so this slightly flatters the Gibbs-mode gradient"}
     sink_gbps_step = 4 * nm_bytes * args.inner / ((elapsed_ms - grad_ms * args.steps) / args.steps / 1e3) / 1e9
 
     # ---- e2e through the public host-vector call ----
