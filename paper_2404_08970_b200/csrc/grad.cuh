@@ -209,20 +209,37 @@ __global__ void __launch_bounds__(TR, 2) k_rowcarry(int64_t nl, int64_t m, int n
       ra[k] = (jv && k < cnt) ? rA[(int64_t)(sc + k) * nl + j] : 0.0;
       dy[k] = k < cnt ? yc[min((int64_t)(sc + k + 1) * TC, m - 1)] - yc[(int64_t)(sc + k) * TC] : 0.0;
     }
+    double vals[4 * U];  // [strip k][P, A, dxe P, dxe A] of this row, reduced over the warp below
 #pragma unroll
     for (int k = 0; k < U; ++k) {
+      vals[4 * k] = vals[4 * k + 1] = vals[4 * k + 2] = vals[4 * k + 3] = 0.0;
       if (k < cnt) {
         const int s = sc + k;
         if (jv) {
           rP[(int64_t)s * nl + j] = P;
           rA[(int64_t)s * nl + j] = A;
         }
-        const double v0 = warp_sum(P), v1 = warp_sum(A), v2 = warp_sum(dxe * P), v3 = warp_sum(dxe * A);
-        if (lane == 0) { red[k][w][0] = v0; red[k][w][1] = v1; red[k][w][2] = v2; red[k][w][3] = v3; }
+        vals[4 * k] = P; vals[4 * k + 1] = A; vals[4 * k + 2] = dxe * P; vals[4 * k + 3] = dxe * A;
         A = A + dy[k] * P + ra[k];
         P += rp[k];
       }
     }
+    // recursive halving over the warp (31 shuffles for the 32 sums instead of 32 x 5): afterwards
+    // lane L holds the warp sum of vals[L]; fixed lane structure => deterministic
+    static_assert(4 * U == 32, "one value per lane after the halving");
+#pragma unroll
+    for (int off = 16, h = 16; off >= 1; off >>= 1, h >>= 1) {
+      const bool hi = lane & off;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        if (i < h) {
+          const double send = hi ? vals[i] : vals[h + i];
+          const double keep = hi ? vals[h + i] : vals[i];
+          vals[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+      }
+    }
+    red[lane >> 2][w][lane & 3] = vals[0];
     __syncthreads();
     if (t < cnt * 4) {
       const int k = t >> 2, e = t & 3;
@@ -240,10 +257,9 @@ __global__ void __launch_bounds__(TR, 2) k_rowcarry(int64_t nl, int64_t m, int n
 //                sum_{j<r0} (x_{r0} - x_j) P_c0(j), sum_{j<r0} (x_{r0} - x_j) A_c0(j) }.
 // tail (nullable): [ns][4] the state after the last block (referenced at the last local row), the
 // per-rank payload of the multi-rank exchange (shard.cuh).
-__global__ void k_blkscan(int64_t nl, int nb, int ns, const double* __restrict__ xl, const double* __restrict__ blk,
-                          double* __restrict__ bs, double* __restrict__ tail) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= ns) return;
+__device__ __forceinline__ void blkscan_strip(int s, int64_t nl, int nb, int ns, const double* __restrict__ xl,
+                                              const double* __restrict__ blk, double* __restrict__ bs,
+                                              double* __restrict__ tail) {
   double SP = 0, SA = 0, XP = 0, XA = 0;
   constexpr int U = 16;
   for (int b0 = 0; b0 < nb; b0 += U) {
@@ -269,6 +285,12 @@ __global__ void k_blkscan(int64_t nl, int nb, int ns, const double* __restrict__
     }
   }
   if (tail) *reinterpret_cast<double4*>(tail + 4 * (int64_t)s) = make_double4(SP, SA, XP, XA);
+}
+
+__global__ void k_blkscan(int64_t nl, int nb, int ns, const double* __restrict__ xl, const double* __restrict__ blk,
+                          double* __restrict__ bs, double* __restrict__ tail) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < ns) blkscan_strip(s, nl, nb, ns, xl, blk, bs, tail);
 }
 
 // ---------------------------------------------------------------------------------

@@ -103,7 +103,7 @@ struct gw_ctx {
   Buf stage, mom, xc, yc, pn, qn, lp, lq, cvx, cvy;
   Buf fs, gs, fh, fl, gh, gl, ftmp, viol, stop, iters, part, fpart, mode, srow, pfl;
   // gradient aux
-  Buf rP, rA, cS, cX, blk, bs, btot, cxend, SAg, WAg, Ptot, Aend, DP, DA, tobj, tent, tcc, objout;
+  Buf rP, rA, cS, cX, blk, bs, btot, cxend, SAg, WAg, Ptot, Aend, DP, DA, tobj, tent, tcc, objout, scanwt;
   Buf fxs, fys;  // FGW features (staged)
   Buf pnf, qnf;  // fp32 marginals
   Buf yfb, pcoef, pc2s, pfx, pfy, ppart, pM;  // k = 2 path
@@ -119,7 +119,7 @@ struct gw_ctx {
   gw_ctx() {
     Buf* b[] = {&stage, &mom, &xc, &yc, &pn, &qn, &lp, &lq, &cvx, &cvy, &fs, &gs, &fh, &fl, &gh, &gl,
                 &ftmp, &viol, &stop, &iters, &part, &fpart, &mode, &srow, &pfl, &rP, &rA, &cS, &cX, &blk, &bs, &btot, &cxend,
-                &SAg, &WAg, &Ptot, &Aend, &DP, &DA, &tobj, &tent, &tcc, &objout, &fxs, &fys, &fsc, &gsc, &Gs,
+                &SAg, &WAg, &Ptot, &Aend, &DP, &DA, &tobj, &tent, &tcc, &objout, &scanwt, &fxs, &fys, &fsc, &gsc, &Gs,
                 &pnf, &qnf, &xtab, &xg1, &xg2, &xin, &xvec, &xtail, &xpart, &slse, &slseg, &scsl, &scsg,
                 &sviolg, &sflag, &sflagg, &yfb, &pcoef, &pc2s, &pfx, &pfy, &ppart, &pM,
                 &gkrp, &gkrt, &gkcp, &gkz, &gkct, &gkctt, &gkobj,
@@ -730,9 +730,17 @@ static gw_status grad_pass_k1(gw_ctx* c, const Prepared& P, int mode, const TSrc
   B.d[1] = Scan1D{cxend, P.yc, m, WAg, nullptr, nullptr};
   B.d[2] = Scan1D{DPsrc, xs_rows, nrows_dp, nullptr, DP, nullptr};
   B.d[3] = Scan1D{DAsrc, xs_rows, nrows_dp, nullptr, DA, nullptr};
-  k_scan1d<<<4, 1024, 0, c->stream>>>(B);
-  KCHECK();
-  PROF_END(c, PC_GRAD_CARRY, 4);
+  {  // the four 1-D programmes, each over K CTAs (k_scan1d_tot / k_scan1d_out)
+    const int64_t nmax = std::max<int64_t>(m, nrows_dp);
+    const int K = (int)std::min<int64_t>(SCAN_KMAX, std::max<int64_t>(1, (nmax + 4095) / 4096));
+    double* wt;
+    TRY(ws(c, c->scanwt, (size_t)4 * K * 32 * 3, &wt));
+    k_scan1d_tot<<<dim3(K, 4), 1024, 0, c->stream>>>(B, K, wt);
+    KCHECK();
+    k_scan1d_out<<<dim3(K, 4), 1024, 0, c->stream>>>(B, K, wt);
+    KCHECK();
+  }
+  PROF_END(c, PC_GRAD_CARRY, 5);
   MainArgs a;
   a.S = S; a.nl = nl; a.m = m; a.nb = nb; a.ns = ns;
   a.xl = xl; a.yc = P.yc; a.cl = P.cx + P.row0; a.c2 = P.cy;

@@ -164,6 +164,136 @@ __global__ void __launch_bounds__(1024) k_scan1d(Scan1DBatch B) {
   if (D.tot && threadIdx.x == 0) { D.tot[0] = V; D.tot[1] = Sv; }
 }
 
+// ---------------------------------------------------------------------------------
+// The same 1-D programme spread over K CTAs per vector (k_scan1d runs one CTA per vector: at
+// n = 65536 that is 4 CTAs on 148 SMs and a 64-step fp64 warp-scan chain per pass).  Segment k
+// of vector v is [k L, (k+1) L), L a multiple of 1024; warp w owns the contiguous 1/32 of it.
+//   k_scan1d_tot: each warp's total state -> wt[((v K) + k) 32 + w]   (3 doubles: P, A, s)
+//   k_scan1d_out: the warp's exclusive prefix = fixed-order fold of the warp totals before it,
+//                 the grand total = fold of all of them; then the output walk of k_scan1d.
+// ---------------------------------------------------------------------------------
+constexpr int SCAN_KMAX = 32;
+
+__device__ __forceinline__ void scan1d_seg(const Scan1D& D, int K, int k, int w, int64_t& i0, int64_t& i1) {
+  const int64_t L = ((D.n + K - 1) / K + 1023) / 1024 * 1024;
+  const int64_t C = L / 32;
+  i0 = (int64_t)k * L + (int64_t)w * C;
+  i1 = min(D.n, i0 + C);
+}
+
+__global__ void __launch_bounds__(1024) k_scan1d_tot(Scan1DBatch B, int K, double* __restrict__ wt) {
+  const int v = blockIdx.y, k = blockIdx.x;
+  if (k >= K) return;
+  const Scan1D D = B.d[v];
+  const int64_t n = D.n;
+  if (n <= 0) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int64_t i0, i1;
+  scan1d_seg(D, K, k, w, i0, i1);
+  constexpr int SU = 4;
+  PA<double> run{0.0, 0.0, i0 < n ? D.s[i0] : D.s[n - 1]};
+  for (int64_t b4 = i0; b4 < i1; b4 += 32 * SU) {
+    double sv[SU], vv[SU];
+#pragma unroll
+    for (int u = 0; u < SU; ++u) {
+      const int64_t i = b4 + 32 * u + lane;
+      sv[u] = D.s[min(i, i1 - 1)];
+      vv[u] = i < i1 ? D.v[i] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < SU; ++u) {
+      if (b4 + 32 * u >= i1) break;  // uniform across the warp
+      PA<double> ex;
+      const PA<double> inc = pa_warp_scan(PA<double>{vv[u], 0.0, sv[u]}, ex);
+      PA<double> st;
+      st.P = __shfl_sync(0xffffffffu, inc.P, 31);
+      st.A = __shfl_sync(0xffffffffu, inc.A, 31);
+      st.s = __shfl_sync(0xffffffffu, inc.s, 31);
+      run = pa_combine(run, st);
+    }
+  }
+  if (lane == 0) {
+    double* o = wt + 3 * (((int64_t)v * K + k) * 32 + w);
+    o[0] = run.P; o[1] = run.A; o[2] = run.s;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_scan1d_out(Scan1DBatch B, int K, const double* __restrict__ wt) {
+  __shared__ double sw[3 * 32 * SCAN_KMAX];
+  __shared__ double sseg[3 * SCAN_KMAX], spre[3 * 32], stot[3];
+  const int v = blockIdx.y, k = blockIdx.x;
+  const Scan1D D = B.d[v];
+  const int64_t n = D.n;
+  if (n <= 0) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nw = K * 32;
+  for (int e = threadIdx.x; e < 3 * nw; e += 1024) sw[e] = wt[3 * (int64_t)v * nw + e];
+  __syncthreads();
+  // fixed-order two-level fold (every CTA of the vector folds the same entries in the same order):
+  // lane j of warp 0 folds segment j's 32 warp totals; lane 0 folds the segment totals (-> the
+  // segment prefixes and the grand total); warp w's lane 0 adds its segment's warps before it.
+  if (w == 0) {
+    if (lane < K) {
+      const double* e = sw + 3 * 32 * lane;
+      PA<double> t{e[0], e[1], e[2]};
+#pragma unroll 4
+      for (int j = 1; j < 32; ++j) t = pa_combine(t, PA<double>{e[3 * j], e[3 * j + 1], e[3 * j + 2]});
+      sseg[3 * lane] = t.P; sseg[3 * lane + 1] = t.A; sseg[3 * lane + 2] = t.s;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      PA<double> run{0.0, 0.0, sw[2]}, segpre = run;
+      for (int j = 0; j < K; ++j) {
+        if (j == k) segpre = run;
+        run = pa_combine(run, PA<double>{sseg[3 * j], sseg[3 * j + 1], sseg[3 * j + 2]});
+      }
+      stot[0] = run.P; stot[1] = run.A; stot[2] = run.s;
+      spre[0] = segpre.P; spre[1] = segpre.A; spre[2] = segpre.s;
+    }
+  }
+  __syncthreads();
+  if (lane == 0 && w > 0) {
+    PA<double> pre{spre[0], spre[1], spre[2]};
+    const double* e = sw + 3 * 32 * k;
+    for (int j = 0; j < w; ++j) pre = pa_combine(pre, PA<double>{e[3 * j], e[3 * j + 1], e[3 * j + 2]});
+    spre[3 * w] = pre.P; spre[3 * w + 1] = pre.A; spre[3 * w + 2] = pre.s;
+  }
+  __syncthreads();
+  const double V = stot[0], Sv = stot[2] * stot[0] - stot[1];
+  int64_t i0, i1;
+  scan1d_seg(D, K, k, w, i0, i1);
+  PA<double> run{spre[3 * w], spre[3 * w + 1], spre[3 * w + 2]};
+  constexpr int SU = 4;
+  for (int64_t b4 = i0; b4 < i1; b4 += 32 * SU) {
+    double sv[SU], vv[SU];
+#pragma unroll
+    for (int u = 0; u < SU; ++u) {
+      const int64_t i = b4 + 32 * u + lane;
+      sv[u] = D.s[min(i, i1 - 1)];
+      vv[u] = i < i1 ? D.v[i] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < SU; ++u) {
+      if (b4 + 32 * u >= i1) break;  // uniform across the warp
+      const int64_t i = b4 + 32 * u + lane;
+      const double si = sv[u];
+      PA<double> ex;
+      const PA<double> inc = pa_warp_scan(PA<double>{vv[u], 0.0, si}, ex);
+      const double lo = pa_eval(pa_combine(run, ex), si);
+      if (i < i1) {
+        if (D.lower) D.lower[i] = lo;
+        if (D.dist) D.dist[i] = 2.0 * lo + Sv - si * V;
+      }
+      PA<double> st;
+      st.P = __shfl_sync(0xffffffffu, inc.P, 31);
+      st.A = __shfl_sync(0xffffffffu, inc.A, 31);
+      st.s = __shfl_sync(0xffffffffu, inc.s, 31);
+      run = pa_combine(run, st);
+    }
+  }
+  if (D.tot && k == 0 && threadIdx.x == 0) { D.tot[0] = V; D.tot[1] = Sv; }
+}
+
 // Test-only fault injection (SURVEY §4.2 tier T6, env GWDP_FAULT): perturb one entry so that the
 // parity tests must fail -- evidence that they would catch a wrong carry or column sum.
 __global__ void k_fault_scale(double* __restrict__ v, int64_t i, double f) {
