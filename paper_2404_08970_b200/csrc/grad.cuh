@@ -293,6 +293,65 @@ __global__ void k_blkscan(int64_t nl, int nb, int ns, const double* __restrict__
   if (s < ns) blkscan_strip(s, nl, nb, ns, xl, blk, bs, tail);
 }
 
+// The same carries with a warp per strip (k_blkscan walks the row blocks serially per thread: a
+// 256-step dependent chain).  Both recurrences are PA scans over the row blocks (element of block
+// b: {P, A} = {blk.x, blk.z} resp. {blk.y, blk.w}, positioned at X(b+1), X(b) = x of the block's
+// first row, X(nb) = x of the last local row): lane L folds blocks 8L .. 8L+7 of a round of 256,
+// a warp scan combines the lanes, and the outputs are evaluated at X(b) (pa_eval).
+__global__ void __launch_bounds__(256) k_blkscan_w(int64_t nl, int nb, int ns, const double* __restrict__ xl,
+                                                   const double* __restrict__ blk, double* __restrict__ bs,
+                                                   double* __restrict__ tail) {
+  constexpr int PER = 8;
+  const int lane = threadIdx.x & 31;
+  const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (s >= ns) return;  // uniform per warp
+  auto X = [&](int b) { return xl[min((int64_t)b * TR, nl - 1)]; };
+  PA<double> runP{0.0, 0.0, X(0)}, runA = runP;
+  for (int r0 = 0; r0 < nb; r0 += 32 * PER) {
+    const int b0 = r0 + lane * PER;
+    double4 tv[PER];
+    double xs[PER + 1];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int b = b0 + u;
+      tv[u] = b < nb ? *reinterpret_cast<const double4*>(blk + ((int64_t)b * ns + s) * 4) : make_double4(0, 0, 0, 0);
+      xs[u] = X(min(b, nb));
+    }
+    xs[PER] = X(min(b0 + PER, nb));
+    PA<double> lp{0.0, 0.0, xs[0]}, la = lp;
+#pragma unroll
+    for (int u = 0; u < PER; ++u)
+      if (b0 + u < nb) {
+        lp = pa_combine(lp, PA<double>{tv[u].x, tv[u].z, xs[u + 1]});
+        la = pa_combine(la, PA<double>{tv[u].y, tv[u].w, xs[u + 1]});
+      }
+    PA<double> exP, exA;
+    const PA<double> incP = pa_warp_scan(lp, exP);
+    const PA<double> incA = pa_warp_scan(la, exA);
+    PA<double> stP = pa_combine(runP, exP), stA = pa_combine(runA, exA);
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int b = b0 + u;
+      if (b < nb) {
+        *reinterpret_cast<double4*>(bs + ((int64_t)b * ns + s) * 4) =
+            make_double4(stP.P, stA.P, pa_eval(stP, xs[u]), pa_eval(stA, xs[u]));
+        stP = pa_combine(stP, PA<double>{tv[u].x, tv[u].z, xs[u + 1]});
+        stA = pa_combine(stA, PA<double>{tv[u].y, tv[u].w, xs[u + 1]});
+      }
+    }
+    const PA<double> tP{__shfl_sync(0xffffffffu, incP.P, 31), __shfl_sync(0xffffffffu, incP.A, 31),
+                        __shfl_sync(0xffffffffu, incP.s, 31)};
+    const PA<double> tA{__shfl_sync(0xffffffffu, incA.P, 31), __shfl_sync(0xffffffffu, incA.A, 31),
+                        __shfl_sync(0xffffffffu, incA.s, 31)};
+    runP = pa_combine(runP, tP);
+    runA = pa_combine(runA, tA);
+  }
+  if (tail && lane == 0) {
+    const double xe = X(nb);
+    *reinterpret_cast<double4*>(tail + 4 * (int64_t)s) = make_double4(runP.P, runA.P, pa_eval(runP, xe), pa_eval(runA, xe));
+  }
+}
+
 // ---------------------------------------------------------------------------------
 // Pass 3: main.  Tile (s, b).  Per element (i, p), tile-relative xh_i = x_i - x_r0,
 // yh_p = y_p - y_c0:

@@ -686,7 +686,7 @@ static gw_status grad_pass_k1(gw_ctx* c, const Prepared& P, int mode, const TSrc
   }
   double* tail = nullptr;
   if (R > 1) TRY(ws(c, c->xtail, 8 * (size_t)ns, &tail));
-  k_blkscan<<<(ns + 31) / 32, 32, 0, c->stream>>>(nl, nb, ns, xl, blk, bs, tail);
+  k_blkscan_w<<<(ns + 7) / 8, 256, 0, c->stream>>>(nl, nb, ns, xl, blk, bs, tail);
   KCHECK();
   const double* DPsrc = Ptot;
   const double* DAsrc = Aend;
