@@ -656,9 +656,9 @@ static gw_status grad_pass_k1(gw_ctx* c, const Prepared& P, int mode, const TSrc
   static const bool mom2 = getenv("GWDP_MOMENTS2") != nullptr;  // smem-staged variant (comparison)
   if (fast && !mom2) {
     switch (mode) {
-      case T_EXPLICIT: k_grad_moments3<T_EXPLICIT><<<grid, 256, 0, c->stream>>>(S2, nl, m, xl, P.yc, rP, rA, cS, cX); break;
+      case T_EXPLICIT: k_grad_moments3o<T_EXPLICIT><<<grid, 256, 0, c->stream>>>(S2, nl, m, xl, P.yc, rP, rA, cS, cX); break;
       case T_GIBBS: k_grad_moments3<T_GIBBS><<<grid, 256, 0, c->stream>>>(S2, nl, m, xl, P.yc, rP, rA, cS, cX); break;
-      default: k_grad_moments3<T_PRODUCT><<<grid, 256, 0, c->stream>>>(S2, nl, m, xl, P.yc, rP, rA, cS, cX); break;
+      default: k_grad_moments3o<T_PRODUCT><<<grid, 256, 0, c->stream>>>(S2, nl, m, xl, P.yc, rP, rA, cS, cX); break;
     }
   } else if (fast) {
     switch (mode) {
