@@ -12,7 +12,7 @@
 //
 // Tiles of TR x TC (rows x columns).  Three passes (12 N M bytes of fp32):
 //   k_grad_moments : per (row, strip) and (block, column) partial moments of T
-//   k_rowcarry / k_colcarry / k_blkscan : exclusive carries (fp64, in place)
+//   k_rowcarry / k_colcarry / k_blkscan_w : exclusive carries (fp64, in place)
 //   k_grad_main    : row scan (warp per row, fp32 in-tile, fp32-rounded fp64 carries),
 //                    column scan (thread per column), fp64 epilogue, fp32 store.
 // T is explicit (gw_grad_dp), regenerated from the Gibbs form exp((f+g-G)/eps) (solver),
@@ -257,44 +257,8 @@ __global__ void __launch_bounds__(TR, 2) k_rowcarry(int64_t nl, int64_t m, int n
 //                sum_{j<r0} (x_{r0} - x_j) P_c0(j), sum_{j<r0} (x_{r0} - x_j) A_c0(j) }.
 // tail (nullable): [ns][4] the state after the last block (referenced at the last local row), the
 // per-rank payload of the multi-rank exchange (shard.cuh).
-__device__ __forceinline__ void blkscan_strip(int s, int64_t nl, int nb, int ns, const double* __restrict__ xl,
-                                              const double* __restrict__ blk, double* __restrict__ bs,
-                                              double* __restrict__ tail) {
-  double SP = 0, SA = 0, XP = 0, XA = 0;
-  constexpr int U = 16;
-  for (int b0 = 0; b0 < nb; b0 += U) {
-    double4 tv[U];
-    double dxv[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int b = b0 + u;
-      tv[u] = b < nb ? *reinterpret_cast<const double4*>(blk + ((int64_t)b * ns + s) * 4) : make_double4(0, 0, 0, 0);
-      dxv[u] = b < nb ? xl[min((int64_t)(b + 1) * TR, nl - 1)] - xl[(int64_t)b * TR] : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int b = b0 + u;
-      if (b < nb) {
-        *reinterpret_cast<double4*>(bs + ((int64_t)b * ns + s) * 4) = make_double4(SP, SA, XP, XA);
-        const double dx = dxv[u];
-        XP = XP + dx * SP + tv[u].z;
-        XA = XA + dx * SA + tv[u].w;
-        SP += tv[u].x;
-        SA += tv[u].y;
-      }
-    }
-  }
-  if (tail) *reinterpret_cast<double4*>(tail + 4 * (int64_t)s) = make_double4(SP, SA, XP, XA);
-}
-
-__global__ void k_blkscan(int64_t nl, int nb, int ns, const double* __restrict__ xl, const double* __restrict__ blk,
-                          double* __restrict__ bs, double* __restrict__ tail) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s < ns) blkscan_strip(s, nl, nb, ns, xl, blk, bs, tail);
-}
-
-// The same carries with a warp per strip (k_blkscan walks the row blocks serially per thread: a
-// 256-step dependent chain).  Both recurrences are PA scans over the row blocks (element of block
+// Warp per strip (a serial walk over the row blocks per thread is a 256-step dependent chain at
+// N = 65536).  Both recurrences are PA scans over the row blocks (element of block
 // b: {P, A} = {blk.x, blk.z} resp. {blk.y, blk.w}, positioned at X(b+1), X(b) = x of the block's
 // first row, X(nb) = x of the last local row): lane L folds blocks 8L .. 8L+7 of a round of 256,
 // a warp scan combines the lanes, and the outputs are evaluated at X(b) (pa_eval).

@@ -7,7 +7,7 @@
 //
 //   column carries  : per column the state (sum_j T_jq, sum_j (x_ref - x_j) T_jq) of the ranks
 //                     above (gap-weighted pair combine, the k = 1 DP of PAPER.md:237-243 with gaps)
-//   block-strip     : the same for the per-strip sums of the row carries (k_blkscan tails)
+//   block-strip     : the same for the per-strip sums of the row carries (k_blkscan_w tails)
 //   row moments     : T 1 and the row-direction A_end are gathered whole (n doubles) and the 1-D
 //                     DPs D_X (.) run over the global support
 //   objective       : 8 partial sums per rank

@@ -66,10 +66,10 @@ __global__ void k_prep(const double* __restrict__ x, const double* __restrict__ 
 }
 
 // ---------------------------------------------------------------------------------
-// 1-D dynamic programme on a sorted support s (one CTA of 1024 threads per vector):
+// 1-D dynamic programme on a sorted support s (k_scan1d_tot / k_scan1d_out below):
 //   lower_i = sum_{j<i} (s_i - s_j) v_j                      (the paper's L v at k = 1,
 //   dist_i  = sum_j |s_i - s_j| v_j = 2 lower_i + Sv - s_i V   PAPER.md:219-243; D = L + L^T)
-// with V = sum v, Sv = sum s v.  Chunked: local pass, block scan of chunk states,
+// with V = sum v, Sv = sum s v.  Chunked: local pass, fixed-order scan of chunk states,
 // second local pass.  Either output may be null.  tot (nullable) = {V, Sv}.
 // ---------------------------------------------------------------------------------
 struct Scan1D {
@@ -84,93 +84,13 @@ struct Scan1DBatch {
   Scan1D d[6];
 };
 
-__global__ void __launch_bounds__(1024) k_scan1d(Scan1DBatch B) {
-  // Warp w owns the contiguous chunk [w C, (w+1) C), walked 32 elements at a time (lane =
-  // element: coalesced loads and stores); a warp scan of the elements' states per step, a
-  // fixed-order scan of the 32 warp totals, then the second (output) walk.
-  __shared__ double sm[3 * 32];
-  const Scan1D D = B.d[blockIdx.x];
-  const int64_t n = D.n;
-  if (n <= 0) return;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  constexpr int NW = 32;
-  const int64_t C = ((n + NW - 1) / NW + 31) / 32 * 32;
-  const int64_t i0 = (int64_t)w * C, i1 = min(n, i0 + C);
-  // pass 1: the warp's total state (the loads of 4 steps issued together)
-  constexpr int SU = 4;
-  PA<double> run{0.0, 0.0, i0 < n ? D.s[i0] : D.s[n - 1]};
-  for (int64_t b4 = i0; b4 < i1; b4 += 32 * SU) {
-    double sv[SU], vv[SU];
-#pragma unroll
-    for (int u = 0; u < SU; ++u) {
-      const int64_t i = b4 + 32 * u + lane;
-      sv[u] = D.s[min(i, i1 - 1)];
-      vv[u] = i < i1 ? D.v[i] : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < SU; ++u) {
-      if (b4 + 32 * u >= i1) break;  // uniform across the warp
-      PA<double> e{vv[u], 0.0, sv[u]};
-      PA<double> ex;
-      const PA<double> inc = pa_warp_scan(e, ex);
-      PA<double> st;  // the step's total (lane 31's inclusive state)
-      st.P = __shfl_sync(0xffffffffu, inc.P, 31);
-      st.A = __shfl_sync(0xffffffffu, inc.A, 31);
-      st.s = __shfl_sync(0xffffffffu, inc.s, 31);
-      run = pa_combine(run, st);
-    }
-  }
-  if (lane == 0) { sm[w] = run.P; sm[NW + w] = run.A; sm[2 * NW + w] = run.s; }
-  __syncthreads();
-  PA<double> pre{0.0, 0.0, sm[2 * NW]};
-  PA<double> tot = pre;
-  for (int k = 0; k < NW; ++k) {
-    const PA<double> t{sm[k], sm[NW + k], sm[2 * NW + k]};
-    if (k < w) pre = pa_combine(pre, t);
-    tot = pa_combine(tot, t);
-  }
-  const double V = tot.P, Sv = tot.s * tot.P - tot.A;
-  // pass 2: outputs
-  run = pre;
-  for (int64_t b4 = i0; b4 < i1; b4 += 32 * SU) {
-    double sv[SU], vv[SU];
-#pragma unroll
-    for (int u = 0; u < SU; ++u) {
-      const int64_t i = b4 + 32 * u + lane;
-      sv[u] = D.s[min(i, i1 - 1)];
-      vv[u] = i < i1 ? D.v[i] : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < SU; ++u) {
-      if (b4 + 32 * u >= i1) break;  // uniform across the warp
-      const int64_t i = b4 + 32 * u + lane;
-      const double si = sv[u];
-      PA<double> e{vv[u], 0.0, si};
-      PA<double> ex;
-      const PA<double> inc = pa_warp_scan(e, ex);
-      const PA<double> mine = pa_combine(run, ex);  // all elements before i
-      const double lo = pa_eval(mine, si);
-      if (i < i1) {
-        if (D.lower) D.lower[i] = lo;
-        if (D.dist) D.dist[i] = 2.0 * lo + Sv - si * V;
-    }
-    PA<double> st;
-    st.P = __shfl_sync(0xffffffffu, inc.P, 31);
-    st.A = __shfl_sync(0xffffffffu, inc.A, 31);
-    st.s = __shfl_sync(0xffffffffu, inc.s, 31);
-    run = pa_combine(run, st);
-    }
-  }
-  if (D.tot && threadIdx.x == 0) { D.tot[0] = V; D.tot[1] = Sv; }
-}
-
 // ---------------------------------------------------------------------------------
-// The same 1-D programme spread over K CTAs per vector (k_scan1d runs one CTA per vector: at
-// n = 65536 that is 4 CTAs on 148 SMs and a 64-step fp64 warp-scan chain per pass).  Segment k
+// Spread over K CTAs per vector (one CTA per vector would be 4 CTAs on 148 SMs and a 64-step
+// fp64 warp-scan chain per pass at n = 65536).  Segment k
 // of vector v is [k L, (k+1) L), L a multiple of 1024; warp w owns the contiguous 1/32 of it.
 //   k_scan1d_tot: each warp's total state -> wt[((v K) + k) 32 + w]   (3 doubles: P, A, s)
 //   k_scan1d_out: the warp's exclusive prefix = fixed-order fold of the warp totals before it,
-//                 the grand total = fold of all of them; then the output walk of k_scan1d.
+//                 the grand total = fold of all of them; then the output walk.
 // ---------------------------------------------------------------------------------
 constexpr int SCAN_KMAX = 32;
 
