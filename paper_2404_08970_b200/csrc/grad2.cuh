@@ -321,7 +321,9 @@ __global__ void __launch_bounds__(G2T, 3) k_grad_store2(MainArgs a, TSrc2 S) {
   __shared__ __align__(16) float2 sEx[G2SUB][4];    // per (row, segment): {P, A} exclusive state of the row
                                                     // before the segment (incl. the strip carry), at the
                                                     // segment's reference point
-  __shared__ __align__(16) float sDy[TC];           // gaps y_q - y_{q-1} inside a segment (0 at a segment start)
+  __shared__ __align__(16) float sDy[4 * G2SEG];    // gaps y_q - y_{q-1} inside a segment (0 at a segment start);
+                                                    // segments G2SEG apart: the row pass's 4 segments of a
+                                                    // quarter-warp then fall in distinct banks
   __shared__ float sFx[TR];
   __shared__ __align__(8) float2 sCar[TR];          // strip carry of each row: {P_c0, A_c0} (fp32)
   __shared__ float sSref[4];                        // y (tile-relative) of each segment's last column
@@ -393,7 +395,7 @@ __global__ void __launch_bounds__(G2T, 3) k_grad_store2(MainArgs a, TSrc2 S) {
     for (int e = 0; e < 2; ++e) {
       const int col = 2 * t + e;
       const int64_t q = c0 + col;
-      sDy[col] = ((col & 63) == 0 || q >= m) ? 0.f : (float)(a.yc[q] - a.yc[q - 1]);
+      sDy[(col >> 6) * G2SEG + (col & 63)] = ((col & 63) == 0 || q >= m) ? 0.f : (float)(a.yc[q] - a.yc[q - 1]);
       // yh_p - yh_ref(segment): distance from the previous segment's last column (ex-state
       // reference) to this column; for segment 0 the reference is y_c0 (strip carry)
       const int sgc = col >> 6;
@@ -440,7 +442,7 @@ __global__ void __launch_bounds__(G2T, 3) k_grad_store2(MainArgs a, TSrc2 S) {
     // ---- row pass: exclusive gap-weighted scan of this thread's segment, in place ----
     {
       float* rowp = sT + rrow * G2RS + sg * G2SEG;
-      const float* dyp = sDy + sg * 64;
+      const float* dyp = sDy + sg * G2SEG;
       float P = 0.f, A = 0.f;
 #pragma unroll 4
       for (int k = 0; k < 16; ++k) {
