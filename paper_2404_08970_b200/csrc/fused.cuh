@@ -41,7 +41,6 @@ struct FusedArgs {
   float* Srow;                // out: S_i = row sums of the plan entering the iteration
   double* part;               // [nclusters][m] column sums of the half-step plan
   int64_t rows_per_cluster;
-  int l2_ahead;               // rows beyond the ring to prefetch into L2 (0: none)
   int64_t wcol;               // columns per CTA (k_sink_fused2; <= the stage capacity 4 K NT)
   const int* mode;            // run only if *mode == 1
   const int* stop;
@@ -96,9 +95,6 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
-}
-__device__ __forceinline__ void prefetch_l2_bulk(const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -196,203 +192,26 @@ __device__ __forceinline__ float fused_exp_row(const float4* __restrict__ sp, co
   return ps[0].x + ps[0].y;
 }
 
-// One CTA = NT threads (NT/32 warps), each owning 4K columns (K float4 per row).  Per row j and
-// without any CTA-wide barrier every warp (a) exponentiates its columns from the ring stage,
-// (b) releases the stage -- the LAST warp to release it (shared counter) refills it by TMA with
-// the row FSTAGES further on, so FSTAGES-1 rows stay in flight whatever the warps' relative
-// progress -- (c) sends its partial of S_j to every cluster rank with st.async, then (d) waits
-// for row j-1's CL x NW partials, reduces them in a fixed order (bit-identical in every warp
-// of every CTA) and accumulates e_{j-1,p} w_{j-1}.
-//
-// Exponent (log2 units): a = fma(G_ip, -log2e/eps, gh_p) + F_i with the fp32 hi parts of the
-// scaled duals only (reading R30): the fma carries the one rounding of the large terms and
-// "+ F" cancels exactly; the dropped lo parts are per-row / per-column scalings that the
-// iteration's normalisations absorb.
-template <int K, int CL, int NT>
-__global__ void __launch_bounds__(NT, 1) k_sink_fused(FusedArgs a) {
-  if (*a.mode != 1 || (a.stop && *a.stop)) return;  // uniform across the cluster
-  constexpr int NW = NT / 32;
-  constexpr int W = 4 * K * NT;
-  constexpr int FSTAGES = fstages<NT>();
-  constexpr int NSLOT = 4;       // exchange slots (power of 2)
-  constexpr int NX = CL * NW;    // partials per row
-  extern __shared__ __align__(128) float ring[];  // [FSTAGES][W], then acc64 [K][4][NT] (fp64)
-  double* acc64 = reinterpret_cast<double*>(ring + (size_t)FSTAGES * W);
-  __shared__ __align__(8) uint64_t full[FSTAGES];
-  __shared__ unsigned int scnt[FSTAGES];
-  __shared__ __align__(8) uint64_t xbar[NSLOT];
-  __shared__ __align__(16) float xs[NSLOT][NX];  // [slot][rank * NW + warp]
-
-  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
-  // 1-D grid of 1-D clusters: rank and cluster index from blockIdx (provably warp-uniform)
-  const uint32_t cr = blockIdx.x % CL;
-  const int64_t cid = blockIdx.x / CL;
-  const int64_t m = a.m;
-  const int64_t c0 = (int64_t)cr * W;
-  const int64_t ncol = max((int64_t)0, min((int64_t)W, m - c0));  // valid columns of this CTA
-  const uint32_t bytes = (uint32_t)(((ncol + 3) & ~int64_t(3)) * 4);
-  const int64_t rb = cid * a.rows_per_cluster;
-  const int64_t re = min(a.nl, rb + a.rows_per_cluster);
-  const int nrows = (int)max((int64_t)0, re - rb);
-  constexpr uint32_t xbytes = 4u * NX;
-  const float* __restrict__ Gbase = a.G + rb * a.ld + c0;
-  const int64_t ld = a.ld;
-
-  if (t == 0) {
-    for (int s = 0; s < FSTAGES; ++s) {
-      mbar_init(&full[s], 1);
-      scnt[s] = 0u;
-    }
-    for (int s = 0; s < NSLOT; ++s) mbar_init(&xbar[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int s = 0; s < NSLOT && s < nrows; ++s) mbar_expect_tx(&xbar[s], xbytes);
-  }
-  __syncthreads();
-  cluster_arrive();
-  cluster_wait();  // every CTA's barriers are initialised and armed before any DSMEM traffic
-
-  if (t == 0 && bytes > 0) {
-    for (int r = 0; r < FSTAGES && r < nrows; ++r) {
-      mbar_expect_tx(&full[r], bytes);
-      tma_load_1d(ring + (size_t)r * W, Gbase + (int64_t)r * ld, bytes, &full[r]);
-    }
-    for (int r = FSTAGES; r < FSTAGES + a.l2_ahead && r < nrows; ++r) prefetch_l2_bulk(Gbase + (int64_t)r * ld, bytes);
-  }
-  const float* __restrict__ fh = a.fh + rb;
-  const float* __restrict__ pf = a.pf + rb;
-  float* __restrict__ Srow = a.Srow + rb;
-  // lane c < CL of every warp sends to rank c: remote address of this warp's slot-0 entry and
-  // of the slot-0 barrier (slot s sits at a fixed byte offset from slot 0 in every CTA)
-  const uint32_t peer = (uint32_t)min(lane, CL - 1);
-  const uint32_t rx0 = mapa(&xs[0][cr * NW + wid], peer), rb0 = mapa(&xbar[0], peer);
-  constexpr uint32_t XSTRIDE = sizeof(xs[0]), BSTRIDE = sizeof(uint64_t);
-  const bool full_tile = (ncol == W);
-
-  float2 ghv[K][2], acc[K][2];
-#pragma unroll
-  for (int k = 0; k < K; ++k)
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int64_t col = c0 + 4 * (t + NT * k) + 2 * h;
-      ghv[k][h].x = col < m ? a.gh[col] : 0.f;
-      ghv[k][h].y = col + 1 < m ? a.gh[col + 1] : 0.f;
-      acc[k][h] = make_float2(0.f, 0.f);
-      acc64[(k * 4 + 2 * h) * NT + t] = 0.0;
-      acc64[(k * 4 + 2 * h + 1) * NT + t] = 0.0;
-    }
-  const float2 nc2 = make_float2(-a.c2f, -a.c2f);
-  float2 eA[K][2], eB[K][2];
-  float pA = 0.f, pB = 0.f;
-  // the row's dual and marginal are loaded one row ahead (their L2 latency would otherwise sit on
-  // every row's critical path)
-  float Fnx = nrows > 0 ? fh[0] : 0.f, pnx = nrows > 0 ? pf[0] : 0.f;
-
-  // Step j: exponentiate row j and send its partial row sums, then consume row j-1 (its
-  // partials were sent one step ago, so the exchange latency hides behind row j's work).
-  auto step = [&](int j, float2 (&ecur)[K][2], float& pcur, float2 (&eprv)[K][2], float pprv) {
-    if (j < nrows) {
-      const int st = j % FSTAGES;
-      const float F = Fnx;
-      pcur = pnx;
-      if (j + 1 < nrows) {
-        Fnx = fh[j + 1];
-        pnx = pf[j + 1];
-      }
-      float psum = 0.f;
-      if (bytes > 0) {
-        mbar_wait(&full[st], (uint32_t)((j / FSTAGES) & 1));
-        const float4* sp = reinterpret_cast<const float4*>(ring + (size_t)st * W);
-        psum = full_tile ? fused_exp_row<K, NT, true>(sp, ghv, nc2, make_float2(F, F), ecur, t, c0, m)
-                         : fused_exp_row<K, NT, false>(sp, ghv, nc2, make_float2(F, F), ecur, t, c0, m);
-        __syncwarp();
-        if (lane == 0) {  // this warp is done with stage st; the last one refills it
-          const int nxt = j + FSTAGES;
-          if (atomicAdd(&scnt[st], 1u) == NW - 1) {
-            scnt[st] = 0u;
-            if (nxt < nrows) {
-              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-              mbar_expect_tx(&full[st], bytes);
-              tma_load_1d(ring + (size_t)st * W, Gbase + (int64_t)nxt * ld, bytes, &full[st]);
-              if (a.l2_ahead > 0 && nxt + a.l2_ahead < nrows)
-                prefetch_l2_bulk(Gbase + (int64_t)(nxt + a.l2_ahead) * ld, bytes);
-            }
-          }
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < K; ++k) { ecur[k][0] = make_float2(0.f, 0.f); ecur[k][1] = ecur[k][0]; }
-      }
-      psum = warp_sum_bfly(psum);
-      const int xsl = j & (NSLOT - 1);
-      if (lane < CL) st_async_f32(rx0 + XSTRIDE * xsl, psum, rb0 + BSTRIDE * xsl);
-    }
-    if (j > 0) {
-      const int jp = j - 1;
-      // row j-1: wait for its CL x NW partials and reduce them in a fixed order
-      const int psl = jp & (NSLOT - 1);
-      mbar_wait(&xbar[psl], (uint32_t)((jp / NSLOT) & 1));
-      float S = 0.f;
-      if (NX >= 32) {
-#pragma unroll
-        for (int i = 0; i < (NX + 31) / 32; ++i)
-          if (lane + 32 * i < NX) S += xs[psl][lane + 32 * i];
-      } else {
-        S = lane < NX ? xs[psl][lane] : 0.f;
-      }
-      S = warp_sum_bfly(S);
-      if (t == 0) {
-        Srow[jp] = S;
-        if (jp + NSLOT < nrows) mbar_expect_tx(&xbar[psl], xbytes);  // the slot now serves row j+3
-      }
-      const float wv = pprv * rcp_ftz(S);
-      const float2 w2 = make_float2(wv, wv);
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        acc[k][0] = ffma2(eprv[k][0], w2, acc[k][0]);
-        acc[k][1] = ffma2(eprv[k][1], w2, acc[k][1]);
-      }
-      if ((jp & (FFLUSH - 1)) == FFLUSH - 1) {
-#pragma unroll
-        for (int k = 0; k < K; ++k)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            acc64[(k * 4 + 2 * h) * NT + t] += (double)acc[k][h].x;
-            acc64[(k * 4 + 2 * h + 1) * NT + t] += (double)acc[k][h].y;
-            acc[k][h] = make_float2(0.f, 0.f);
-          }
-      }
-    }
-  };
-  // rows in pairs: the two e buffers swap roles, so no register copies
-  for (int j = 0; j <= nrows; j += 2) {
-    step(j, eA, pA, eB, pB);
-    if (j + 1 <= nrows) step(j + 1, eB, pB, eA, pA);
-  }
-#pragma unroll
-  for (int k = 0; k < K; ++k)
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int64_t col = c0 + 4 * (t + NT * k) + 2 * h;
-      const double v0 = acc64[(k * 4 + 2 * h) * NT + t] + (double)acc[k][h].x;
-      const double v1 = acc64[(k * 4 + 2 * h + 1) * NT + t] + (double)acc[k][h].y;
-      if (col < m) a.part[cid * m + col] = v0;
-      if (col + 1 < m) a.part[cid * m + col + 1] = v1;
-    }
-  // no CTA may exit while a peer can still address its shared memory
-  cluster_arrive();
-  cluster_wait();
-}
-
 __device__ __forceinline__ void st_async_v2f32(uint32_t raddr, float v0, float v1, uint32_t rbar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(raddr),
                "f"(v0), "f"(v1), "r"(rbar)
                : "memory");
 }
 
-// Row-pair variant of k_sink_fused: one step exponentiates TWO rows and exchanges both partial
-// row sums in one 8-byte st.async per peer, and the consumer reduces both in one pass, so the
-// per-row exchange, barrier and loop overhead (~2/3 of a warp's instructions per row at
-// K = 4) is paid once per two rows.  Same arithmetic per element, same fixed reduction order.
+// One CTA = NT threads (NT/32 warps), each owning 4K columns (K float4 per row).  Without any
+// CTA-wide barrier every warp (a) exponentiates its columns of a ring stage, (b) releases the stage
+// -- the LAST warp to release it (shared counter) refills it by TMA with the row FSTAGES further on,
+// so FSTAGES-1 rows stay in flight whatever the warps' relative progress -- (c) sends its partial row
+// sums to every cluster rank with st.async, then (d) waits for the previous step's CL x NW partials,
+// reduces them in a fixed order (bit-identical in every warp of every CTA) and accumulates e w.
+// Rows are processed in PAIRS: one step exponentiates two rows and exchanges both partial row sums
+// in one 8-byte st.async per peer, so the per-row exchange, barrier and loop overhead is paid once
+// per two rows.
+//
+// Exponent (log2 units): a = fma(G_ip, -log2e/eps, gh_p) + F_i with the fp32 hi parts of the
+// scaled duals only (reading R30): the fma carries the one rounding of the large terms and
+// "+ F" cancels exactly; the dropped lo parts are per-row / per-column scalings that the
+// iteration's normalisations absorb.
 template <int K, int CL, int NT>
 __global__ void __launch_bounds__(NT, 1) k_sink_fused2(FusedArgs a) {
   if (*a.mode != 1 || (a.stop && *a.stop)) return;  // uniform across the cluster

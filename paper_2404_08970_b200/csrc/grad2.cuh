@@ -1,5 +1,5 @@
 // grad2.cuh -- streaming kernels of the DP gradient (rows a1-a4 of SURVEY §8a):
-//   k_grad_moments2 : per (row, strip) row partials and per (block, column) column partials of T
+//   k_grad_moments3 : per (row, strip) row partials and per (block, column) column partials of T
 //   k_grad_store2   : the main pass, G = R_i + K'_p + xh_i u'_p + yh_p v_i - 16 A''_sub  (fp32 out)
 // Same tiling, carries and formulas as grad.cuh (TR x TC = 256 x 256 tiles; the derivation is in
 // grad.cuh and DESIGN.md §3), re-laid out so that every per-element step is a handful of fp32
@@ -219,82 +219,6 @@ __device__ __forceinline__ void g2_stage_fast(const G2Loader<MODE>& L, const TSr
       if (LNT) *reinterpret_cast<float4*>(sT2 + rl * G2RS + phys) = lt;
     }
   }
-}
-
-// ---------------------------------------------------------------------------------
-// Moments (outputs as k_grad_moments in grad.cuh):
-//   rP[s][j] = sum_{q in s} T_jq,   rA[s][j] = sum_{q in s} (ye_s - y_q) T_jq
-//   cS[b][q] = sum_{j in b} T_jq,   cX[b][q] = sum_{j in b} (xe_b - x_j) T_jq
-// ---------------------------------------------------------------------------------
-template <int MODE>
-__global__ void __launch_bounds__(G2T, 4) k_grad_moments2(TSrc2 S, int64_t nl, int64_t m, const double* __restrict__ xl,
-                                                       const double* __restrict__ yc, double* __restrict__ rP,
-                                                       double* __restrict__ rA, double* __restrict__ cS,
-                                                       double* __restrict__ cX) {
-  __shared__ __align__(16) float sT[G2SUB * G2RS];
-  __shared__ __align__(16) float sDyE[TC];    // ye_s - y_q (fp32)
-  __shared__ float sDx[TR];                   // xe_b - x_j (fp32)
-  const int s = blockIdx.x, b = blockIdx.y;
-  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  const int64_t c0 = (int64_t)s * TC, r0 = (int64_t)b * TR;
-  {
-    const double ye = yc[min(c0 + TC, m - 1)];
-    const double xe = xl[min(r0 + TR, nl - 1)];
-    for (int k = t; k < TC; k += G2T) sDyE[k] = c0 + k < m ? (float)(ye - yc[c0 + k]) : 0.f;
-    for (int k = t; k < TR; k += G2T) sDx[k] = r0 + k < nl ? (float)(xe - xl[r0 + k]) : 0.f;
-  }
-  const int nsub = (int)min((int64_t)(TR / G2SUB), (nl - r0 + G2SUB - 1) / G2SUB);
-  // row pass mapping: row rl = w * 8 + lane / 4, segment sg = lane % 4
-  const int rrow = w * 8 + (lane >> 2), sg = lane & 3;
-  // column pass: columns 2t, 2t+1
-  const int cphys = g2_phys(2 * t);
-  float2 cs = make_float2(0.f, 0.f), cx = cs;
-  G2Loader<MODE> L;
-  L.load(S, r0, c0, nl, m, 0);
-  for (int sub = 0; sub < nsub; ++sub) {
-    __syncthreads();  // previous sub-strip fully consumed
-    g2_stage<MODE>(L, S, sT, r0, c0, nl, m, sub);
-    if (sub + 1 < nsub) L.load(S, r0, c0, nl, m, sub + 1);
-    __syncthreads();
-    // ---- row partials over this thread's 64-column segment, then over the 4 segments ----
-    {
-      const float4* rowp = reinterpret_cast<const float4*>(sT + rrow * G2RS + sg * G2SEG);
-      const float4* dyp = reinterpret_cast<const float4*>(sDyE + sg * 64);
-      float2 P2 = make_float2(0.f, 0.f), A2 = P2;
-#pragma unroll 4
-      for (int k = 0; k < 16; ++k) {
-        const float4 v = rowp[k], d = dyp[k];
-        P2 = fadd2(P2, fadd2(make_float2(v.x, v.y), make_float2(v.z, v.w)));
-        A2 = ffma2(make_float2(d.x, d.y), make_float2(v.x, v.y), A2);
-        A2 = ffma2(make_float2(d.z, d.w), make_float2(v.z, v.w), A2);
-      }
-      float P = P2.x + P2.y, A = A2.x + A2.y;
-      // fixed-order sum over the 4 segment lanes (butterfly: identical bits in all 4)
-      P += __shfl_xor_sync(0xffffffffu, P, 1);
-      A += __shfl_xor_sync(0xffffffffu, A, 1);
-      P += __shfl_xor_sync(0xffffffffu, P, 2);
-      A += __shfl_xor_sync(0xffffffffu, A, 2);
-      const int64_t j = r0 + sub * G2SUB + rrow;
-      if (sg == 0 && j < nl) {
-        rP[(int64_t)s * nl + j] = (double)P;
-        rA[(int64_t)s * nl + j] = (double)A;
-      }
-    }
-    // ---- column partials ----
-    {
-      const float* dxs = sDx + sub * G2SUB;
-#pragma unroll 8
-      for (int rl = 0; rl < G2SUB; ++rl) {
-        const float2 v = *reinterpret_cast<const float2*>(sT + rl * G2RS + cphys);
-        const float dx = dxs[rl];
-        cs = fadd2(cs, v);
-        cx = ffma2(make_float2(dx, dx), v, cx);
-      }
-    }
-  }
-  const int64_t q = c0 + 2 * t;
-  if (q < m) { cS[b * m + q] = (double)cs.x; cX[b * m + q] = (double)cx.x; }
-  if (q + 1 < m) { cS[b * m + q + 1] = (double)cs.y; cX[b * m + q + 1] = (double)cx.y; }
 }
 
 // ---------------------------------------------------------------------------------
@@ -566,7 +490,9 @@ __global__ void __launch_bounds__(G2T, 3) k_grad_store2(MainArgs a, TSrc2 S) {
 namespace gw {
 
 // ---------------------------------------------------------------------------------
-// Moments without shared-memory staging (outputs as k_grad_moments / k_grad_moments2).
+// Moments without shared-memory staging (outputs as k_grad_moments in grad.cuh):
+//   rP[s][j] = sum_{q in s} T_jq,   rA[s][j] = sum_{q in s} (ye_s - y_q) T_jq
+//   cS[b][q] = sum_{j in b} T_jq,   cX[b][q] = sum_{j in b} (xe_b - x_j) T_jq
 // CTA = 256 threads, tile 256 x 256: warp w owns rows w, w+8, ..., lane L owns columns
 // c0 + 8L .. c0 + 8L + 7 (two coalesced float4 per row).  Per row the lane's 8 values give its
 // partial (P, A) of the row and feed its 8 column accumulators (fp32 over the tile's rows).

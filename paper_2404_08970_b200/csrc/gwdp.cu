@@ -468,6 +468,11 @@ static gw_status shard_table(gw_ctx* c, Prepared& P) {
     P.dtab = dt;
     for (int r = 0; r < P.R; ++r) P.maxnl = std::max(P.maxnl, P.tab[2 * r + 1]);
   } else {
+    // one rank holds the whole problem: a partial shard would silently treat the other rows of T as
+    // zero mass (the carries, moments and column sums are local-only when R == 1)
+    if (P.row0 != 0 || P.nl != P.n)
+      return fail(GW_ERR_DIM_MISMATCH, "single-rank context: the shard must be (row0, n_local) = (0, %lld), got "
+                  "(%lld, %lld)", (long long)P.n, (long long)P.row0, (long long)P.nl);
     P.tab[0] = P.row0;
     P.tab[1] = P.nl;
     P.maxnl = P.nl;
@@ -623,9 +628,11 @@ struct GradOut {
 
 // One DP gradient pass over the (local) plan given by `S` (mode `mode`):
 //   STORE -> G (ldG);  OBJ -> E(T), violation(T), H(T) via k_objective.
-// The STORE-only pass (every gradient of the solver and gw_grad_dp) runs the streaming fp32 kernels of
-// grad2.cuh with T supplied by S2; the objective pass (OBJ) runs grad.cuh's kernels with S (fp64
-// regeneration) so that its moments and its tile sums see bit-identical T values.
+// The STORE-only pass (every gradient of the solver and gw_grad_dp) AND the OBJ-only objective pass
+// run the streaming fp32 kernels of grad2.cuh with T supplied by S2 (fp32 hi/lo duals fh, fl, gh, gl);
+// only the rare STORE+OBJ pass (GW_SOLVE_TRACE_OBJECTIVE) runs grad.cuh's kernels with S (fp64
+// regeneration from the scaled duals).  Invariant relied on by the S2 passes: whenever sink_run returns,
+// fh/fl == split(f log2e/eps) and gh/gl == split(g log2e/eps) of the COMMITTED duals.
 static gw_status grad_pass_k1(gw_ctx* c, const Prepared& P, int mode, const TSrc& S, const TSrc2& S2, float* G,
                               int64_t ldG, bool store, bool obj, const double* fx, const double* fy, double alpha,
                               double* objout_dev, double beta = 0.0) {
@@ -653,18 +660,11 @@ static gw_status grad_pass_k1(gw_ctx* c, const Prepared& P, int mode, const TSrc
   // the objective pass is timed as its own class
   const int pc_mom = !obj ? PC_GRAD_MOMENTS : PC_OBJ, pc_main = !obj ? PC_GRAD_MAIN : PC_OBJ;
   PROF_BEGIN(c, pc_mom);
-  static const bool mom2 = getenv("GWDP_MOMENTS2") != nullptr;  // smem-staged variant (comparison)
-  if (fast && !mom2) {
+  if (fast) {
     switch (mode) {
       case T_EXPLICIT: k_grad_moments3o<T_EXPLICIT><<<grid, 256, 0, c->stream>>>(S2, nl, m, xl, P.yc, rP, rA, cS, cX); break;
       case T_GIBBS: k_grad_moments3<T_GIBBS><<<grid, 256, 0, c->stream>>>(S2, nl, m, xl, P.yc, rP, rA, cS, cX); break;
       default: k_grad_moments3o<T_PRODUCT><<<grid, 256, 0, c->stream>>>(S2, nl, m, xl, P.yc, rP, rA, cS, cX); break;
-    }
-  } else if (fast) {
-    switch (mode) {
-      case T_EXPLICIT: k_grad_moments2<T_EXPLICIT><<<grid, G2T, 0, c->stream>>>(S2, nl, m, xl, P.yc, rP, rA, cS, cX); break;
-      case T_GIBBS: k_grad_moments2<T_GIBBS><<<grid, G2T, 0, c->stream>>>(S2, nl, m, xl, P.yc, rP, rA, cS, cX); break;
-      default: k_grad_moments2<T_PRODUCT><<<grid, G2T, 0, c->stream>>>(S2, nl, m, xl, P.yc, rP, rA, cS, cX); break;
     }
   } else {
     switch (mode) {
@@ -1184,6 +1184,21 @@ static void sink_free(SinkState& s) {
   if (s.gexec) cudaGraphExecDestroy(s.gexec);
   s.gexec = nullptr;
 }
+// CUDA events owned by one call, destroyed on every exit path (errors included)
+struct EventSet {
+  std::vector<cudaEvent_t> v;
+  ~EventSet() {
+    for (auto e : v)
+      if (e) cudaEventDestroy(e);
+  }
+  cudaError_t make(cudaEvent_t* out) {
+    cudaEvent_t e = nullptr;
+    const cudaError_t r = cudaEventCreate(&e);
+    if (r == cudaSuccess) v.push_back(e);
+    *out = e;
+    return r;
+  }
+};
 struct SinkGuard {  // releases the captured graph on every exit path of a solve
   SinkState& s;
   ~SinkGuard() { sink_free(s); }
@@ -1191,14 +1206,9 @@ struct SinkGuard {  // releases the captured graph on every exit path of a solve
 
 template <int K, int CL, int NT>
 static gw_status fused_config_t(gw_ctx* c, int* ncl) {
-  auto kern = k_sink_fused<K, CL, NT>;
+  auto kern = k_sink_fused2<K, CL, NT>;
   const size_t dsm = fused_dyn_smem<K, NT>();
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
-  CU(cudaFuncSetAttribute(k_sink_fused2<K, CL, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
-  if (CL > 8) {  // non-portable cluster sizes (B200 allows up to 16)
-    CU(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    CU(cudaFuncSetAttribute(k_sink_fused2<K, CL, NT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(148 * CL);
   cfg.blockDim = dim3(NT);
@@ -1224,9 +1234,7 @@ static gw_status fused_launch_t(gw_ctx* c, const FusedArgs& fa, int ncl) {
   at[0].val.clusterDim.x = CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  static const bool v1 = getenv("GWDP_FUSED_V1") != nullptr;  // single-row variant (comparison)
-  if (v1) CU(cudaLaunchKernelEx(&cfg, k_sink_fused<K, CL, NT>, fa));
-  else CU(cudaLaunchKernelEx(&cfg, k_sink_fused2<K, CL, NT>, fa));
+  CU(cudaLaunchKernelEx(&cfg, k_sink_fused2<K, CL, NT>, fa));
   return GW_OK;
 }
 
@@ -1248,7 +1256,6 @@ static gw_status fused_launch_t(gw_ctx* c, const FusedArgs& fa, int ncl) {
     case 512 + 4 * 16 + 2: return FN<4, 2, 512>(__VA_ARGS__);                     \
     case 512 + 4 * 16 + 4: return FN<4, 4, 512>(__VA_ARGS__);                     \
     case 512 + 4 * 16 + 8: return FN<4, 8, 512>(__VA_ARGS__);                     \
-    case 256 + 8 * 16 + 9: return FN<8, 9, 256>(__VA_ARGS__);                     \
     default: return fail(GW_ERR_UNSUPPORTED, "fused path: no instance K=%d CL=%d NT=%d", K, CL, NT); \
   }
 static gw_status fused_config(gw_ctx* c, int K, int CL, int NT, int* ncl) { FUSED_DISPATCH(fused_config_t, c, ncl) }
@@ -1307,16 +1314,9 @@ static gw_status sink_alloc(gw_ctx* c, const Prepared& P, SinkState& s) {
     }
     if (CL == 3) CL = 4;
     if (CL > 4 && CL < 8) CL = 8;
-    int64_t wcol = 4 * (int64_t)K * NT;
-    // Clusters must fit in a GPC: on B200 clusters of 8 leave 28 SMs idle (15 clusters); clusters of
-    // 9 narrower CTAs (wcol = m / 9) use 135 SMs but still 15 clusters, and the per-row cost is set
-    // by the warp count, so it measured no faster (5.73 vs 5.79 TB/s at m = 65536): opt-in only.
-    const char* c9 = getenv("GWDP_FUSED_CL9");
-    if (c9 && c9[0] == '1' && !getenv("GWDP_FUSED_V1") && NT == 256 && CL == 8 && 9 * (wcol - 4) >= P.m) {
-      CL = 9;
-      wcol = ((P.m + 8) / 9 + 3) & ~int64_t(3);
-    }
-    if (CL <= 9) {
+    const int64_t wcol = 4 * (int64_t)K * NT;
+    // Clusters must fit in a GPC: on B200 clusters of 8 leave 28 SMs idle (15 clusters)
+    if (CL <= 8) {
       int ncl = 0;
       TRY(fused_config(c, K, CL, NT, &ncl));
       if (ncl > 0) {
@@ -1420,10 +1420,6 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
   fa.G = G; fa.ld = ldG; fa.nl = nl; fa.m = m; fa.c2f = c2f; fa.gh = s.gh; fa.gl = s.gl; fa.fh = s.fh;
   fa.fl = s.fl; fa.pf = s.pf; fa.Srow = s.Srow; fa.part = s.fpart; fa.rows_per_cluster = s.frpc;
   fa.mode = s.mode; fa.stop = s.stop; fa.wcol = s.fW;
-  {
-    const char* pf = getenv("GWDP_L2_AHEAD");
-    fa.l2_ahead = pf ? atoi(pf) : 0;
-  }
   // the fused one-read step of one iteration (speculative; a no-op unless *mode == 1)
   auto fused_step = [&]() -> gw_status {
     // Every iteration first tries the fused one-read path when *mode == 1 (speculatively at the
@@ -1620,6 +1616,10 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
       if (hs[0]) {
         *used = hs[1];
         *converged = 1;
+        // the measuring row half-step split the DISCARDED trial f' into fh/fl (k_sink_row always writes
+        // them); k_sink_commit kept f: re-split it so that fh/fl == split(f) on every return
+        k_split<<<grid_for(nl), 256, 0, c->stream>>>(s.f, nl, GW_LOG2E / eps, s.fh, s.fl);
+        KCHECK();
         return GW_OK;
       }
     }
@@ -1794,11 +1794,12 @@ static gw_status solve_impl(gw_ctx* c, const gw_problem* pb, const gw_solve_opts
   TRY(ws(c, c->gsc, (size_t)m, &Gs2));
   TRY(ws(c, c->objout, 16, &objout));
 
+  EventSet evset;
   cudaEvent_t ev0, ev1;
-  CU(cudaEventCreate(&ev0)); CU(cudaEventCreate(&ev1));
+  CU(evset.make(&ev0)); CU(evset.make(&ev1));
   CU(cudaEventRecord(ev0, c->stream));
   std::vector<cudaEvent_t> evs(2 * (size_t)o->outer_iters + 2);
-  for (auto& e : evs) CU(cudaEventCreate(&e));
+  for (auto& e : evs) CU(evset.make(&e));
 
   int inner_total = 0, conv_all = 1;
   float ms_grad = 0.f, ms_sink = 0.f;
@@ -1882,9 +1883,10 @@ static gw_status solve_impl(gw_ctx* c, const gw_problem* pb, const gw_solve_opts
       S2 = TSrc2{G, ldG, s.fh, s.fl, s.gh, s.gl, ch, (float)(cc - (double)ch)};
     }
     TRY(grad_pass(c, P, mode, S, S2, nullptr, 0, false, true, fx, fy, alpha, objout));
-    if (T_out) TRY(materialize(c, P, mode == T_EXPLICIT ? T_GIBBS : mode, S, T_out, ldT));
+    // outer_iters == 0 with an explicit T0: the returned plan IS T0 (S has no duals to regenerate from)
     if (T_out && mode == T_EXPLICIT) CU(cudaMemcpy2DAsync(T_out, ldT * 4, T0, ldT * 4, m * 4, nl,
                                                           cudaMemcpyDeviceToDevice, c->stream));
+    else if (T_out) TRY(materialize(c, P, mode, S, T_out, ldT));
     CU(cudaMemcpyAsync(c->hpin, objout, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   }
   int fused_total = 0;
@@ -1913,8 +1915,6 @@ static gw_status solve_impl(gw_ctx* c, const gw_problem* pb, const gw_solve_opts
   }
   float ms_total = 0.f;
   CU(cudaEventElapsedTime(&ms_total, ev0, ev1));
-  for (auto& e : evs) cudaEventDestroy(e);
-  cudaEventDestroy(ev0); cudaEventDestroy(ev1);
   res->gw_objective = Eout;
   res->entropic_objective = Eout + eps * H;
   res->marginal_violation = viol;
@@ -2083,8 +2083,9 @@ static gw_status ugw_impl(gw_ctx* c, const gw_problem* pb, double rho, const gw_
   KCHECK();
   const bool want_trace_obj = (o->flags & GW_SOLVE_TRACE_OBJECTIVE) != 0;
   std::vector<double> tr((size_t)std::max(o->outer_iters, 1) * 4, NAN);
+  EventSet evset;
   cudaEvent_t ev0, ev1;
-  CU(cudaEventCreate(&ev0)); CU(cudaEventCreate(&ev1));
+  CU(evset.make(&ev0)); CU(evset.make(&ev1));
   CU(cudaEventRecord(ev0, c->stream));
   const unsigned cgrid = (unsigned)std::min<int64_t>(((m + 1023) / 1024) * s.nrb, 148 * 4);
   const unsigned rgrid = (unsigned)std::min<int64_t>((nl + RROWS - 1) / RROWS, 148 * 4);
@@ -2252,7 +2253,6 @@ static gw_status ugw_impl(gw_ctx* c, const gw_problem* pb, double rho, const gw_
   CU(cudaStreamSynchronize(c->stream));
   float ms_total = 0.f;
   CU(cudaEventElapsedTime(&ms_total, ev0, ev1));
-  cudaEventDestroy(ev0); cudaEventDestroy(ev1);
   res->gw_objective = E;
   res->entropic_objective = F;
   res->marginal_violation = viol;

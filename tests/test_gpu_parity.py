@@ -545,3 +545,50 @@ def test_fault_injection_is_caught(gw, monkeypatch):
 def test_general_tau_degenerate_shapes(gw):
     r = gw.solve([0.3], [0.7], [1.0], [1.0], 0.02, 3, 10, tau=0.01, return_plan=True, device=_dev())
     assert r.T.cpu().numpy().tolist() == [[1.0]] and abs(r.gw_objective) < 1e-12
+
+
+# ----------------------------------------------------------------------------- regression (round-1 advice)
+
+def test_solver_zero_outer_with_T0_returns_T0(gw):
+    """outer_iters == 0 with an explicit T0 and a returned plan: the plan IS T0 and the objective is
+    E(T0) (no Gibbs regeneration from absent duals)."""
+    rng = np.random.default_rng(11)
+    n, m = 40, 33
+    x, y = np.sort(rng.random(n)), np.sort(rng.random(m))
+    p, q = np.full(n, 1.0 / n), np.full(m, 1.0 / m)
+    T0 = (np.outer(p, q) * rng.uniform(0.5, 1.5, (n, m))).astype(np.float32)
+    r = gw.solve(x, y, p, q, 0.05, 0, 10, T0=_to_dev(gw, T0), return_plan=True)
+    assert np.array_equal(r.T.cpu().numpy(), T0)
+    Eo = O.objective(x, y, T0.astype(np.float64))
+    assert abs(r.gw_objective - Eo) <= 1e-5 * abs(Eo)
+
+
+def test_solver_tolerance_early_stop_independent_of_trace(gw):
+    """tol > 0 with an early stop: fh/fl must be re-split from the COMMITTED f (not the measuring
+    half-step's trial f'), so the next gradient and the final objective do not depend on whether the
+    objective trace is on."""
+    P = W.config2(512)
+    a = gw.solve(P.x, P.y, P.p, P.q, 2e-2, 4, 2000, tol=1e-6, check_every=10, trace_objective=False,
+                 return_plan=True)
+    b = gw.solve(P.x, P.y, P.p, P.q, 2e-2, 4, 2000, tol=1e-6, check_every=10, trace_objective=True,
+                 return_plan=True)
+    assert list(a.trace[:, 2]) == list(b.trace[:, 2])
+    assert int(a.trace[0, 2]) < 2000  # the early stop happened
+    np.testing.assert_array_equal(a.f.cpu().numpy(), b.f.cpu().numpy())
+    assert a.gw_objective == b.gw_objective
+    # and both agree with the oracle replaying the same counts
+    counts = [int(c) for c in a.trace[:, 2]]
+    ro = O.entropic_gw(P.x, P.y, P.p, P.q, 2e-2, 4, counts)
+    assert abs(a.gw_objective - ro["gw_objective"]) <= OBJ_TOL * abs(ro["gw_objective"])
+
+
+def test_single_rank_rejects_partial_shard(gw):
+    """One rank: (row0, n_local) must be (0, n); a partial shard would silently drop rows."""
+    from paper_2404_08970_b200 import GwError
+    rng = np.random.default_rng(3)
+    x = np.sort(rng.random(64))
+    p = np.full(64, 1.0 / 64)
+    for row0, nl in [(0, 32), (16, 48), (0, 0)]:
+        with pytest.raises(GwError) as e:
+            gw.solve(x, x, p, p, 0.1, 1, 5, row0=row0, n_local=nl, device=_dev())
+        assert e.value.code == "GW_ERR_DIM_MISMATCH"

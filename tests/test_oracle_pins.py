@@ -391,6 +391,60 @@ def test_fgw_gradient_bruteforce():
     np.testing.assert_allclose(O.fgw_grad_prescribed(x, y, p, q, fx, fy, th, T), brute, atol=1e-12)
 
 
+def test_fgw_objective_closed_form_product_plan():
+    """E_bar(p (x) p) = (1 - theta) <C o C, p (x) p> + theta E(p (x) p) with both
+    parts in closed form: <(fx - fy)^2, p (x) q> = E_p[fx^2] - 2 E_p[fx] E_q[fy] + E_q[fy^2] (moments of
+    the product law) and E(p (x) p) on the uniform grid from P6.  Dropping the (1 - theta) factor, or
+    weighting the GW part by anything but theta, fails at theta in (0, 1)."""
+    rng = np.random.default_rng(41)
+    for n in [2, 7, 30]:
+        x = np.arange(n) / (n - 1)
+        p = np.full(n, 1.0 / n)
+        fx, fy = rng.standard_normal(n), rng.standard_normal(n)
+        cc = p @ fx ** 2 - 2 * (p @ fx) * (p @ fy) + p @ fy ** 2
+        e_gw = (n + 1) / (3 * (n - 1)) - 2 * ((n + 1) / (3 * n)) ** 2
+        for th in [0.0, 0.25, 0.5, 1.0]:
+            closed = (1 - th) * cc + th * e_gw
+            assert O.fgw_objective(x, x, fx, fy, th, np.outer(p, p)) == pytest.approx(closed, rel=1e-12, abs=1e-15)
+
+
+def test_fgw_objective_bruteforce_any_plan():
+    """E_bar(T) = (1 - theta) sum_ip (fx_i - fy_p)^2 T_ip + theta sum_ijpq (d_ij - d'_pq)^2 T_ip T_jq
+    by explicit loops over the entries on a non-feasible random plan."""
+    rng = np.random.default_rng(42)
+    n, m = 4, 3
+    x, y = _sorted(rng, n), _sorted(rng, m)
+    fx, fy = rng.standard_normal(n), rng.standard_normal(m)
+    T = rng.random((n, m))
+    lin = sum((fx[i] - fy[j]) ** 2 * T[i, j] for i in range(n) for j in range(m))
+    quad = sum((abs(x[i] - x[j]) - abs(y[a] - y[b])) ** 2 * T[i, a] * T[j, b]
+               for i in range(n) for j in range(n) for a in range(m) for b in range(m))
+    for th in [0.0, 0.4, 1.0]:
+        assert O.fgw_objective(x, y, fx, fy, th, T) == pytest.approx((1 - th) * lin + th * quad, rel=1e-12)
+
+
+def test_violation_is_two_sided():
+    """violation = max(||T1 - p||_inf, ||T^T 1 - q||_inf): on product plans the
+    marginals are known in closed form -- p' (x) q has row sums p' and column sums q exactly, p (x) q'
+    the reverse -- so a rows-only or columns-only check fails one of the two cases."""
+    rng = np.random.default_rng(43)
+    n, m = 9, 6
+    p, q = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))
+    p2, q2 = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))
+    assert O.violation(np.outer(p, q), p, q) == pytest.approx(0.0, abs=1e-16)
+    assert O.violation(np.outer(p2, q), p, q) == pytest.approx(np.max(np.abs(p2 - p)), abs=1e-16)
+    assert O.violation(np.outer(p, q2), p, q) == pytest.approx(np.max(np.abs(q2 - q)), abs=1e-16)
+    # a plan with exact row sums and one column off by d: the violation is d (loop sums)
+    T = np.outer(p, q)
+    d = 1e-3
+    T[0, 0] += d
+    T[0, 1] -= d
+    rows = max(abs(sum(T[i, :]) - p[i]) for i in range(n))
+    cols = max(abs(sum(T[:, j]) - q[j]) for j in range(m))
+    assert rows < 1e-15 and cols == pytest.approx(d, rel=1e-9)
+    assert O.violation(T, p, q) == pytest.approx(d, rel=1e-9)
+
+
 # --------------------------------------------------------------------------- workloads
 
 def test_workloads_deterministic_and_valid():
