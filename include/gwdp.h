@@ -225,6 +225,19 @@ gw_status entropic_gw_solve(gw_ctx *ctx, const gw_problem *prob, const gw_solve_
                             const void *T0, void *T_out, int64_t ldT, double *f, double *g,
                             gw_result *res, double *trace);
 
+/* Debug export for parity checks of the solver's own gradients.
+ * Arms a ONE-SHOT request consumed by the next entropic_gw_solve / fgw_solve on ctx: at outer
+ * iteration `outer_iter` (1-based; 0 clears the request) the library writes
+ *   T_prev (nullable): the plan T^{l-1} the l-th gradient is evaluated on (p q^T or T0 for l = 1,
+ *                      else exp((f + g - G^{l-1})/eps) materialised from the solver's duals), and
+ *   G_out  (nullable): the solver's stored cost G^l = grad E(T^{l-1}) (FGW:
+ *                      its cost) exactly as the Sinkhorn iterations consume it.
+ * Both are this rank's n_local x m rows, fp32 row-major with leading dimension ld (ld % 4 == 0,
+ * 16-byte aligned).  The request is taken by the next solve call whatever its outcome; a solve with
+ * fewer outer iterations writes nothing.  Errors: GW_ERR_INVALID_ARG (null ctx, both buffers null,
+ * bad ld / alignment), GW_ERR_CONFIG (outer_iter < 0).  Costs one extra N x M write each (debug only). */
+gw_status gw_solve_set_export(gw_ctx *ctx, int32_t outer_iter, void *T_prev, void *G_out, int64_t ld);
+
 /* Fused GW (Remark 2): cost (1-alpha) C o C + alpha G with the
  * feature cost C_ip = |fx_i - fy_p| (never stored), objective
  * (1-alpha) <C o C, T> + alpha E(T).  fx (n), fy (m).  Same conventions as

@@ -65,3 +65,11 @@ from .ugw import (  # noqa: F401
     unbalanced_plan,
     entropic_ugw,
 )
+from .streamed import (  # noqa: F401
+    const_term_blocked,
+    grad_rows_cols,
+    marginals_streamed,
+    violation_streamed,
+    objective_k1,
+    dist_apply_prefix,
+)

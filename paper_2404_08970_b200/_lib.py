@@ -27,7 +27,7 @@ GW_SOLVE_TRACE_OBJECTIVE = 0x1
 SYMBOLS = [
     "gw_ctx_create", "gw_ctx_destroy", "gw_ctx_trim", "gw_ctx_profile", "gw_last_error", "gw_abi_version",
     "gw_get_unique_id", "gw_comm_init", "gw_comm_init_host", "gw_comm_destroy", "gw_shard_rows", "gw_check_shards",
-    "gw_grad_dp", "sinkhorn_solve", "entropic_gw_solve", "fgw_solve", "ugw_solve",
+    "gw_grad_dp", "sinkhorn_solve", "entropic_gw_solve", "fgw_solve", "ugw_solve", "gw_solve_set_export",
 ]
 
 
@@ -108,6 +108,7 @@ def load(path=LIB_PATH):
                               C.POINTER(gw_result), P]
     lib.ugw_solve.argtypes = [P, C.POINTER(gw_problem), C.c_double, C.POINTER(gw_solve_opts), P, P, i64, P, P,
                               C.POINTER(gw_result), P]
+    lib.gw_solve_set_export.argtypes = [P, C.c_int32, P, P, i64]
     for name in SYMBOLS:
         f = getattr(lib, name)
         if f.restype is None or f.restype is C.c_int:

@@ -176,14 +176,17 @@ def _opts(eps, outer, inner, tol, check_every, trace_objective, tau=None):
 
 def solve(x, y, p, q, eps, outer, inner, tol=0.0, check_every=10, T0=None, return_plan=False,
           trace_objective=False, fx=None, fy=None, alpha=None, device=None, ctx=None, row0=0, n_local=None, k=1,
-          grid2d=False, tau=None):
+          grid2d=False, tau=None, export_iter=0, export_T=None, export_G=None):
     """Entropic GW (entropic_gw_solve) or, with fx/fy/alpha, entropic FGW (fgw_solve), on
     device vectors; tau = eps.  Sharded (ctx with a multi-rank
     comm): x, p (and fx) are full; this rank owns rows [row0, row0 + n_local): f, T0 and the
     returned plan hold those rows, g is replicated, the objective and violation are global.
     grid2d: x, y are 2-D grid axes (GW_GRID2D); p, q have len(x)**2, len(y)**2 entries.
     tau: the mirror-descent step's KL weight (default eps, Remark 1): the
-    subproblem is entropic OT of grad E + (eps - tau) ln T^l at regulariser tau (k = 1, 1-D)."""
+    subproblem is entropic OT of grad E + (eps - tau) ln T^l at regulariser tau (k = 1, 1-D).
+    export_iter / export_T / export_G (debug, gw_solve_set_export): at outer iteration export_iter
+    (1-based) write the plan T^{l-1} the gradient is evaluated on and the solver's own G^l into
+    caller buffers (plan_buffer-shaped, same leading dimension)."""
     dev = torch.device(device) if device is not None else (T0.device if T0 is not None else torch.device("cuda"))
     if dev.index is None:
         dev = torch.device("cuda", torch.cuda.current_device())
@@ -207,6 +210,13 @@ def solve(x, y, p, q, eps, outer, inner, tol=0.0, check_every=10, T0=None, retur
     res = L.gw_result()
     tr = np.zeros((max(int(outer), 1), 4), dtype=np.float64)
     trp = tr.ctypes.data_as(C.c_void_p)
+    if export_iter:
+        bufs = [b for b in (export_T, export_G) if b is not None]
+        eld = _check_mat(bufs[0], "export buffer") if bufs else 0
+        for b in bufs:
+            if b.stride(0) != eld:
+                raise ValueError("export_T and export_G must share the leading dimension")
+        L.check(ctx.lib.gw_solve_set_export(ctx.h, int(export_iter), _ptr(export_T), _ptr(export_G), eld))
     if fx is not None:
         fxv, fyv = _vec(fx, dev), _vec(fy, dev)
         L.check(ctx.lib.fgw_solve(ctx.h, C.byref(pr), _ptr(fxv), _ptr(fyv), float(alpha), C.byref(o), _ptr(T0),

@@ -24,6 +24,7 @@
 #include "polyk.cuh"
 #include "ugw.cuh"
 #include "small.cuh"
+#include "strip.cuh"
 #include "sink.cuh"
 #include "vec.cuh"
 
@@ -113,9 +114,16 @@ struct gw_ctx {
   Buf xtab, xg1, xg2, xin, xvec, xtail, xpart;  // multi-rank exchange buffers
   Buf slse, slseg, scsl, scsg, sviolg;          // Sinkhorn column-sum exchange
   Buf sflag, sflagg;
+  Buf stx, stc;  // strip Sinkhorn: row-sum exchange (partials, arrival counters)
   Buf fsc, gsc;  // scaled duals for the Gibbs regeneration
   Buf Gs;        // solver cost buffer
   double* hpin = nullptr;  // pinned host scratch (64 doubles)
+  // one-shot debug export for the next solve (gw_solve_set_export)
+  struct {
+    int iter = 0;
+    void *T = nullptr, *G = nullptr;
+    int64_t ld = 0;
+  } exp;
   gw_ctx() {
     Buf* b[] = {&stage, &mom, &xc, &yc, &pn, &qn, &lp, &lq, &cvx, &cvy, &fs, &gs, &fh, &fl, &gh, &gl,
                 &ftmp, &viol, &stop, &iters, &part, &fpart, &mode, &srow, &pfl, &rP, &rA, &cS, &cX, &blk, &bs, &btot, &cxend,
@@ -124,7 +132,8 @@ struct gw_ctx {
                 &sviolg, &sflag, &sflagg, &yfb, &pcoef, &pc2s, &pfx, &pfy, &ppart, &pM,
                 &gkrp, &gkrt, &gkcp, &gkz, &gkct, &gkctt, &gkobj,
                 &uga, &ugb, &ugct, &ugpart, &ugca, &ugcb, &ugfr, &uggr, &ugsc,
-                &g2rc, &g2rd, &g2h, &g2cc, &g2tt, &g2vt, &g2tmp, &g2s, &g2a, &g2b, &g2ca, &g2cb, &g2part};
+                &g2rc, &g2rd, &g2h, &g2cc, &g2tt, &g2vt, &g2tmp, &g2s, &g2a, &g2b, &g2ca, &g2cb, &g2part,
+                &stx, &stc};
     for (Buf* x : b) all.push_back(x);
   }
 };
@@ -1171,6 +1180,12 @@ struct SinkState {
   float* Srow;    // [nl]
   float* pf;      // [nl] p as fp32
   int fK = 0, fCL = 0, fNT = 256, fncl = 0;  // fK == 0: fast path unavailable for this shape
+  // strip variant of the fused iteration (strip.cuh): one CTA per SM, grid-wide row-sum exchange
+  bool strip = false;
+  int sKF = 0, snb = 0, snbuf = 0, slag = 0;
+  size_t sdsm = 0;
+  float* sxpart = nullptr;
+  unsigned* sxcnt = nullptr;
   int64_t fW = 0;                            // columns per CTA
   int64_t frpc = 0;
   // column-sum exchange: this rank's column LSE pairs / column sums, and all ranks' (gathered)
@@ -1263,6 +1278,74 @@ static gw_status fused_launch(gw_ctx* c, int K, int CL, int NT, const FusedArgs&
   FUSED_DISPATCH(fused_launch_t, c, fa, ncl)
 }
 
+template <int KF>
+static gw_status strip_launch_t(gw_ctx* c, const StripArgs& sa, size_t dsm) {
+  static std::atomic<size_t> attr_set[8];  // the dynamic smem attribute, raised monotonically
+  if (attr_set[KF].load() < dsm) {
+    CU(cudaFuncSetAttribute(k_sink_strip<KF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+    attr_set[KF].store(dsm);
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(sa.nb);
+  cfg.blockDim = dim3(SNTX);
+  cfg.dynamicSmemBytes = dsm;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;  // every CTA co-resident (grid-wide exchange)
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CU(cudaLaunchKernelEx(&cfg, k_sink_strip<KF>, sa));
+  return GW_OK;
+}
+static gw_status strip_launch(gw_ctx* c, int KF, const StripArgs& sa, size_t dsm) {
+  switch (KF) {
+    case 2: return strip_launch_t<2>(c, sa, dsm);
+    case 4: return strip_launch_t<4>(c, sa, dsm);
+    default: return fail(GW_ERR_UNSUPPORTED, "strip Sinkhorn: no instance KF=%d", KF);
+  }
+}
+
+// Strip variant eligibility (strip.cuh): wide rows (every SM gets >= 32 float4 per row), enough rows
+// for the exchange pipeline, and -- since its CTAs wait on each other -- one ctx per device at a time:
+// NCCL ranks (one GPU each) or a single rank; the host-transport shard tests drive several ctxs on one
+// GPU concurrently and keep the cluster kernel.  GWDP_STRIP=0/1 forces it off / on (where it fits).
+static bool strip_config(gw_ctx* c, const Prepared& P, SinkState& s) {
+  const char* e = getenv("GWDP_STRIP");
+  const int force = e ? atoi(e) : -1;
+  if (force != 1) return false;  // opt-in until measured faster than the cluster kernel
+  if (P.nl < 4 * SRB) return false;
+  const bool exclusive = P.R == 1 || (c->comm && c->comm->nccl);
+  if (!exclusive) return false;
+  int nsm = 0;
+  if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device) != cudaSuccess || nsm <= 0) {
+    cudaGetLastError();
+    return false;
+  }
+  if (nsm > SNBMAX) return false;
+  const int64_t M4 = (P.m + 3) / 4;
+  const int64_t nf4max = (M4 + nsm - 1) / nsm;
+  if (force != 1 && nf4max < 32) return false;  // narrow strips: the cluster kernel is the better fit
+  if (nf4max > 128) return false;
+  const int KF = nf4max <= 64 ? 2 : 4;
+  const size_t per = (size_t)SRB * nf4max * 16;
+  const size_t cap = 200 * 1024;
+  int nbuf = (int)std::min<size_t>(cap / per, 12);
+  const char* eb = getenv("GWDP_STRIP_NBUF");
+  if (eb) nbuf = std::min(nbuf, atoi(eb));
+  int lag = nbuf - 3;
+  const char* el = getenv("GWDP_STRIP_LAG");
+  if (el) lag = atoi(el);
+  if (nbuf < 3 || lag < 1 || lag > nbuf - 2 || lag > SPB - 2) return false;
+  s.strip = true;
+  s.sKF = KF;
+  s.snb = nsm;
+  s.snbuf = nbuf;
+  s.slag = lag;
+  s.sdsm = (size_t)nbuf * per;
+  return true;
+}
+
 static gw_status sink_alloc(gw_ctx* c, const Prepared& P, SinkState& s) {
   TRY(ws(c, c->fh, P.nl, &s.fh)); TRY(ws(c, c->fl, P.nl, &s.fl));
   TRY(ws(c, c->gh, P.m, &s.gh)); TRY(ws(c, c->gl, P.m, &s.gl));
@@ -1315,8 +1398,18 @@ static gw_status sink_alloc(gw_ctx* c, const Prepared& P, SinkState& s) {
     if (CL == 3) CL = 4;
     if (CL > 4 && CL < 8) CL = 8;
     const int64_t wcol = 4 * (int64_t)K * NT;
-    // Clusters must fit in a GPC: on B200 clusters of 8 leave 28 SMs idle (15 clusters)
-    if (CL <= 8) {
+    if (strip_config(c, P, s)) {
+      // the strip kernel: column sums complete per rank (one "cluster" payload), exchange scratch
+      s.fK = K; s.fCL = CL; s.fNT = NT; s.fncl = 1; s.fW = wcol;
+      s.frpc = P.nl;
+      TRY(ws(c, c->fpart, (size_t)P.m, &s.fpart));
+      TRY(ws(c, c->srow, (size_t)P.nl, &s.Srow));
+      TRY(ws(c, c->pfl, (size_t)P.nl, &s.pf));
+      TRY(ws(c, c->stx, (size_t)SPB * s.snb * SRB, &s.sxpart));
+      TRY(ws(c, c->stc, (size_t)SPB, &s.sxcnt));
+      k_to_float<<<grid_for(P.nl), 256, 0, c->stream>>>(P.pn + P.row0, P.nl, s.pf);
+      KCHECK();
+    } else if (CL <= 8) {  // clusters must fit in a GPC: on B200 clusters of 8 leave 28 SMs idle
       int ncl = 0;
       TRY(fused_config(c, K, CL, NT, &ncl));
       if (ncl > 0) {
@@ -1428,7 +1521,17 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
     // two-kernel path below runs this same iteration.  No host sync.
     if (s.fK > 0) {
       PROF_BEGIN(c, PC_SINK_FUSED);
-      TRY(fused_launch(c, s.fK, s.fCL, s.fNT, fa, s.fncl));
+      if (s.strip) {
+        StripArgs sa;
+        sa.G = G; sa.ld = ldG; sa.nl = nl; sa.m = m; sa.c2f = c2f; sa.gh = s.gh; sa.fh = s.fh; sa.pf = s.pf;
+        sa.Srow = s.Srow; sa.part = s.fpart; sa.xpart = s.sxpart; sa.xcnt = s.sxcnt;
+        sa.nb = s.snb; sa.nbuf = s.snbuf; sa.lag = s.slag;
+        sa.mode = s.mode; sa.stop = s.stop;
+        CU(cudaMemsetAsync(s.sxcnt, 0, SPB * sizeof(unsigned), c->stream));  // the arrival counters
+        TRY(strip_launch(c, s.sKF, sa, s.sdsm));
+      } else {
+        TRY(fused_launch(c, s.fK, s.fCL, s.fNT, fa, s.fncl));
+      }
       KCHECK();
       // one rank: column sums, check (rows + columns), commit.  R > 1: the rank's row check rides in
       // the column-sum payload (slot M), so ONE all-gather per iteration carries everything.
@@ -1735,6 +1838,10 @@ static gw_status solve_impl(gw_ctx* c, const gw_problem* pb, const gw_solve_opts
                             const double* fy_in, double alpha, const void* T0, void* T_out, int64_t ldT, double* f,
                             double* g, gw_result* res, double* trace) {
   if (!c || !o || !res) return fail(GW_ERR_INVALID_ARG, "null ctx, opts or result");
+  // the debug export request is one-shot: taken by this call whatever its outcome
+  const auto ex = c->exp;
+  c->exp.iter = 0;
+  c->exp.T = c->exp.G = nullptr;
   if (!(o->eps > 0)) return fail(GW_ERR_CONFIG, "eps must be > 0");
   NvtxRange nv("gw.solve");
   // tau (0 means tau = eps, Remark 1): the Sinkhorn regulariser; tau != eps adds
@@ -1832,6 +1939,16 @@ static gw_status solve_impl(gw_ctx* c, const gw_problem* pb, const gw_solve_opts
       S2 = TSrc2{G, ldG, s.fh, s.fl, s.gh, s.gl, ch, (float)(cc - (double)ch)};
     }
     const bool obj = (l > 0) && want_trace_obj;
+    const bool exporting = ex.iter == l + 1;
+    if (exporting && ex.T) {  // debug export: the plan T^{l} this gradient is evaluated on
+      if (mode == T_EXPLICIT) {
+        CU(cudaMemcpy2DAsync(ex.T, ex.ld * 4, T0, ldT * 4, m * 4, nl, cudaMemcpyDeviceToDevice, c->stream));
+      } else if (mode == T_PRODUCT) {
+        TRY(materialize(c, P, T_PRODUCT, S, ex.T, ex.ld));
+      } else {
+        TRY(materialize(c, P, T_GIBBS, S, ex.T, ex.ld));
+      }
+    }
     CU(cudaEventRecord(evs[2 * l], c->stream));
     if (tau_mode && obj) {  // objective of T^l first, then the cost over the buffer it reads
       TRY(grad_pass(c, P, mode, S, S2, nullptr, 0, false, true, fx, fy, alpha, objout));
@@ -1840,6 +1957,8 @@ static gw_status solve_impl(gw_ctx* c, const gw_problem* pb, const gw_solve_opts
       TRY(grad_pass(c, P, mode, S, S2, G, ldG, true, obj, fx, fy, alpha, objout, beta));
     }
     CU(cudaEventRecord(evs[2 * l + 1], c->stream));
+    if (exporting && ex.G)  // debug export: the solver's own stored cost G^{l+1} = grad E(T^l)
+      CU(cudaMemcpy2DAsync(ex.G, ex.ld * 4, G, ldG * 4, m * 4, nl, cudaMemcpyDeviceToDevice, c->stream));
     if (obj) {
       CU(cudaMemcpyAsync(c->hpin, objout, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
       CU(cudaStreamSynchronize(c->stream));
@@ -1927,6 +2046,21 @@ static gw_status solve_impl(gw_ctx* c, const gw_problem* pb, const gw_solve_opts
   res->ms_total = ms_total;
   if (trace) memcpy(trace, tr.data(), sizeof(double) * 4 * (size_t)o->outer_iters);
   TRY(stage_duals_out(c, pb, P, f, g, s.f, s.g));
+  return GW_OK;
+}
+
+extern "C" gw_status gw_solve_set_export(gw_ctx* c, int32_t outer_iter, void* T_prev, void* G_out, int64_t ld) {
+  if (!c) return fail(GW_ERR_INVALID_ARG, "null ctx");
+  if (outer_iter < 0) return fail(GW_ERR_CONFIG, "export: outer_iter must be >= 0 (0 clears)");
+  if (outer_iter > 0 && !T_prev && !G_out) return fail(GW_ERR_INVALID_ARG, "export: both buffers are null");
+  if (T_prev && (ld % 4 != 0 || (reinterpret_cast<uintptr_t>(T_prev) & 15)))
+    return fail(GW_ERR_INVALID_ARG, "export: T_prev needs ld %% 4 == 0 and a 16-byte aligned base");
+  if (G_out && (ld % 4 != 0 || (reinterpret_cast<uintptr_t>(G_out) & 15)))
+    return fail(GW_ERR_INVALID_ARG, "export: G_out needs ld %% 4 == 0 and a 16-byte aligned base");
+  c->exp.iter = outer_iter;
+  c->exp.T = T_prev;
+  c->exp.G = G_out;
+  c->exp.ld = ld;
   return GW_OK;
 }
 

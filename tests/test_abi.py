@@ -59,6 +59,7 @@ def test_host_only_entry_points(lib):
     assert _lib.STATUS[st] == "GW_ERR_INVALID_ARG"
     # null-argument validation happens before any device work
     assert _lib.STATUS[lib.gw_grad_dp(None, None, None, 0, None, 0, None)] == "GW_ERR_INVALID_ARG"
+    assert _lib.STATUS[lib.gw_solve_set_export(None, 1, None, None, 0)] == "GW_ERR_INVALID_ARG"
 
 
 def test_product_path_has_no_oracle_or_fallback():

@@ -445,6 +445,67 @@ def test_violation_is_two_sided():
     assert O.violation(T, p, q) == pytest.approx(d, rel=1e-9)
 
 
+# --------------------------------------------------------------------------- streamed (C4-size) evaluations
+
+def _blocks(T, b):
+    return [(j, T[j:j + b]) for j in range(0, T.shape[0], b)]
+
+
+def test_streamed_gradient_rows_cols_match_dense():
+    """grad_rows_cols (row blocks of T, D generated blockwise, the paper's recursion for the 1-D
+    products) equals the dense definition c3 on the sampled lines, ragged blocks, any plan."""
+    rng = np.random.default_rng(51)
+    n, m = 157, 131
+    x, y = _sorted(rng, n), _sorted(rng, m)
+    p, q = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))
+    T = rng.random((n, m)) / (n * m)
+    I = np.sort(rng.choice(n, 9, replace=False))
+    J = np.sort(rng.choice(m, 7, replace=False))
+    GI, GJ = O.grad_rows_cols(x, y, p, q, _blocks(T, 40), I, J)
+    Gd = O.grad_prescribed(x, y, p, q, T)
+    np.testing.assert_allclose(GI, Gd[I], rtol=0, atol=1e-13)
+    np.testing.assert_allclose(GJ, Gd[:, J], rtol=0, atol=1e-13)
+    c, c2 = O.const_term_blocked(x, y, p, q, block=33)
+    cd, c2d = O.const_term(x, y, p, q)
+    np.testing.assert_allclose(c, cd, rtol=1e-14)
+    np.testing.assert_allclose(c2, c2d, rtol=1e-14)
+
+
+def test_prefix_sum_distance_apply_matches_dense_and_recursion():
+    """D v by prefix sums (k = 1) equals the dense product and the paper's recursion
+    (PAPER.md:219-243), along either axis, with ties in the support."""
+    rng = np.random.default_rng(52)
+    s = np.sort(np.concatenate([rng.random(40), [0.5, 0.5, 0.5]]))
+    V = rng.random((7, s.size))
+    D = O.dist(s)
+    np.testing.assert_allclose(O.dist_apply_prefix(V, s, axis=1), V @ D, rtol=0, atol=1e-13)
+    np.testing.assert_allclose(O.dist_apply_prefix(V.T, s, axis=0), D @ V.T, rtol=0, atol=1e-13)
+    np.testing.assert_allclose(O.dist_apply_prefix(V, s, axis=1), O.ref_dp_distance(V, s), rtol=0, atol=1e-13)
+
+
+def test_streamed_objective_and_violation_match_dense():
+    """objective_k1 (two streamed passes) equals the dense objective and the
+    brute-force quadruple sum; violation_streamed equals the dense two-sided violation."""
+    rng = np.random.default_rng(53)
+    n, m = 211, 97
+    x, y = _sorted(rng, n), _sorted(rng, m)
+    p, q = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))
+    T = rng.random((n, m)) / (n * m)
+    E = O.objective_k1(x, y, _blocks(T, 50))
+    assert O.objective_k1(x, y, _blocks(T, 17), workers=4) == pytest.approx(E, rel=1e-13)
+    assert E == pytest.approx(O.objective(x, y, T), rel=1e-12)
+    Ts = T[:9, :8] / T[:9, :8].sum()
+    assert O.objective_k1(x[:9], y[:8], _blocks(Ts, 4)) == pytest.approx(
+        O.objective_bruteforce(x[:9], y[:8], Ts), rel=1e-12)
+    assert O.violation_streamed(_blocks(T, 64), p, q) == pytest.approx(O.violation(T, p, q), rel=1e-14)
+    # the closed form P6 of E(p (x) p) on the uniform grid
+    nn = 300
+    g = np.arange(nn) / (nn - 1)
+    pp = np.full(nn, 1.0 / nn)
+    closed = (nn + 1) / (3 * (nn - 1)) - 2 * ((nn + 1) / (3 * nn)) ** 2
+    assert O.objective_k1(g, g, _blocks(np.outer(pp, pp), 64)) == pytest.approx(closed, rel=1e-12)
+
+
 # --------------------------------------------------------------------------- workloads
 
 def test_workloads_deterministic_and_valid():
