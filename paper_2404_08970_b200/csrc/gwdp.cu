@@ -114,7 +114,7 @@ struct gw_ctx {
   Buf xtab, xg1, xg2, xin, xvec, xtail, xpart;  // multi-rank exchange buffers
   Buf slse, slseg, scsl, scsg, sviolg;          // Sinkhorn column-sum exchange
   Buf sflag, sflagg;
-  Buf stx, stc;  // strip Sinkhorn: row-sum exchange (partials, arrival counters)
+  Buf stx, sts, ste;  // strip Sinkhorn: row-sum exchange (partials, block sums, launch counter)
   Buf fsc, gsc;  // scaled duals for the Gibbs regeneration
   Buf Gs;        // solver cost buffer
   double* hpin = nullptr;  // pinned host scratch (64 doubles)
@@ -133,7 +133,7 @@ struct gw_ctx {
                 &gkrp, &gkrt, &gkcp, &gkz, &gkct, &gkctt, &gkobj,
                 &uga, &ugb, &ugct, &ugpart, &ugca, &ugcb, &ugfr, &uggr, &ugsc,
                 &g2rc, &g2rd, &g2h, &g2cc, &g2tt, &g2vt, &g2tmp, &g2s, &g2a, &g2b, &g2ca, &g2cb, &g2part,
-                &stx, &stc};
+                &stx, &sts, &ste};
     for (Buf* x : b) all.push_back(x);
   }
 };
@@ -1184,8 +1184,8 @@ struct SinkState {
   bool strip = false;
   int sKF = 0, snb = 0, snbuf = 0, slag = 0;
   size_t sdsm = 0;
-  float* sxpart = nullptr;
-  unsigned* sxcnt = nullptr;
+  unsigned long long *sxp = nullptr, *sxs = nullptr;
+  unsigned* sepoch = nullptr;
   int64_t fW = 0;                            // columns per CTA
   int64_t frpc = 0;
   // column-sum exchange: this rank's column LSE pairs / column sums, and all ranks' (gathered)
@@ -1314,7 +1314,7 @@ static bool strip_config(gw_ctx* c, const Prepared& P, SinkState& s) {
   const char* e = getenv("GWDP_STRIP");
   const int force = e ? atoi(e) : -1;
   if (force != 1) return false;  // opt-in until measured faster than the cluster kernel
-  if (P.nl < 4 * SRB) return false;
+  if (P.nl < 4 * SRB || (P.nl + SRB - 1) / SRB >= (1 << 20) - 1) return false;
   const bool exclusive = P.R == 1 || (c->comm && c->comm->nccl);
   if (!exclusive) return false;
   int nsm = 0;
@@ -1336,7 +1336,7 @@ static bool strip_config(gw_ctx* c, const Prepared& P, SinkState& s) {
   int lag = nbuf - 3;
   const char* el = getenv("GWDP_STRIP_LAG");
   if (el) lag = atoi(el);
-  if (nbuf < 3 || lag < 1 || lag > nbuf - 2 || lag > SPB - 2) return false;
+  if (nbuf < 3 || lag < 1 || lag > nbuf - 2 || lag > SPB - 2 || lag > SWB) return false;
   s.strip = true;
   s.sKF = KF;
   s.snb = nsm;
@@ -1405,8 +1405,12 @@ static gw_status sink_alloc(gw_ctx* c, const Prepared& P, SinkState& s) {
       TRY(ws(c, c->fpart, (size_t)P.m, &s.fpart));
       TRY(ws(c, c->srow, (size_t)P.nl, &s.Srow));
       TRY(ws(c, c->pfl, (size_t)P.nl, &s.pf));
-      TRY(ws(c, c->stx, (size_t)SPB * s.snb * SRB, &s.sxpart));
-      TRY(ws(c, c->stc, (size_t)SPB, &s.sxcnt));
+      TRY(ws(c, c->stx, (size_t)SPB * s.snb * SRB, &s.sxp));
+      TRY(ws(c, c->sts, (size_t)SPB * SRB, &s.sxs));
+      TRY(ws(c, c->ste, 1, &s.sepoch));
+      // tag 0xffffffff is never a block's tag (nblk < 2^20 - 1): no stale word looks published
+      CU(cudaMemsetAsync(s.sxp, 0xff, (size_t)SPB * s.snb * SRB * sizeof(unsigned long long), c->stream));
+      CU(cudaMemsetAsync(s.sxs, 0xff, (size_t)SPB * SRB * sizeof(unsigned long long), c->stream));
       k_to_float<<<grid_for(P.nl), 256, 0, c->stream>>>(P.pn + P.row0, P.nl, s.pf);
       KCHECK();
     } else if (CL <= 8) {  // clusters must fit in a GPC: on B200 clusters of 8 leave 28 SMs idle
@@ -1524,10 +1528,9 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
       if (s.strip) {
         StripArgs sa;
         sa.G = G; sa.ld = ldG; sa.nl = nl; sa.m = m; sa.c2f = c2f; sa.gh = s.gh; sa.fh = s.fh; sa.pf = s.pf;
-        sa.Srow = s.Srow; sa.part = s.fpart; sa.xpart = s.sxpart; sa.xcnt = s.sxcnt;
+        sa.Srow = s.Srow; sa.part = s.fpart; sa.xp = s.sxp; sa.xs = s.sxs; sa.epoch = s.sepoch;
         sa.nb = s.snb; sa.nbuf = s.snbuf; sa.lag = s.slag;
         sa.mode = s.mode; sa.stop = s.stop;
-        CU(cudaMemsetAsync(s.sxcnt, 0, SPB * sizeof(unsigned), c->stream));  // the arrival counters
         TRY(strip_launch(c, s.sKF, sa, s.sdsm));
       } else {
         TRY(fused_launch(c, s.fK, s.fCL, s.fNT, fa, s.fncl));

@@ -10,11 +10,11 @@
 // [c M/NB, (c+1) M/NB) of EVERY row (M/NB ~ 443 columns = 1.8 KB per row), so its column sums are
 // complete locally, and the row sums are exchanged across the grid.  Per block b of SRB rows:
 //   * compute warps (8): TMA bulk copies of the CTA's strip of the rows land in a ring buffer; e is
-//     computed in place (warp per row); per-row partial sums -> global xpart[b][c][.]; one arrival
-//     (release) on the block's counter;
-//   * the exchange warp (warp 8) runs ahead on its own: it waits (acquire) until all NB CTAs have
-//     arrived for a block, sums the NB partials of each row in a fixed order (so every CTA computes
-//     bit-identical S), forms w = p / S into a shared-memory slot and signals an mbarrier;
+//     computed in place (warp per row); per-row partial sums -> global {value, tag} words;
+//   * the reducer warp of CTA b mod NB waits for the NB partials of every row of block b, sums them
+//     in a fixed order (deterministic) and publishes S as {value, tag} words;
+//   * the consumer warp polls the published S of the next blocks (a 4-block window), forms
+//     w = p / S into a shared-memory slot and signals an mbarrier;
 //   * LAG blocks after exponentiating block b the compute warps accumulate e w of block b - LAG into
 //     their column sums (fp32 per block, fp64 across blocks) and release its buffer to the TMA.
 // The LAG blocks of e kept in shared memory hide the exchange latency.  All CTAs must be co-resident
@@ -26,11 +26,11 @@
 namespace gw {
 
 constexpr int SNTH = 256;            // compute threads per CTA (8 warps)
-constexpr int SNTX = SNTH + 32;      // + the exchange warp
+constexpr int SNTX = SNTH + 64;      // + the consumer warp and the reducer warp
 constexpr int SRB = 16;              // rows per block
-constexpr int SPB = 16;              // counter slots (ring of blocks; power of 2)
-constexpr int SWB = 4;               // w slots (blocks the exchange warp may run ahead)
-constexpr int SNBMAX = 160;          // CTAs (SMs) the exchange warp's unrolled loads cover
+constexpr int SPB = 16;              // exchange slots (ring of blocks; power of 2, >= lag + 2)
+constexpr int SWB = 8;               // w slots (blocks the consumer warp may run ahead)
+constexpr int SNBMAX = 160;          // CTAs (SMs) the reducer's unrolled loads cover
 
 struct StripArgs {
   const float* G;
@@ -41,23 +41,32 @@ struct StripArgs {
   const float* pf;       // p (fp32), local rows
   float* Srow;           // out: S_i
   double* part;          // out: [m] column sums of the half-step plan (this rank's rows)
-  float* xpart;          // [SPB][nb][SRB] partial row sums
-  unsigned* xcnt;        // [SPB] arrival counters, zeroed before every launch (slot s counts the
-                         // arrivals of blocks s, s + SPB, ...: block b is complete at NB (b/SPB + 1))
+  unsigned long long* xp;  // [SPB][nb][SRB] partial row sums as {value, tag} words
+  unsigned long long* xs;  // [SPB][SRB] row sums of a block as {value, tag} words (its reducer)
+  unsigned* epoch;       // launch counter (tags); CTA 0 increments it on exit
   int nb;                // CTAs in the grid (<= SNBMAX)
   int nbuf, lag;         // ring depth and exchange lag (blocks)
   const int* mode;
   const int* stop;
 };
 
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
+// {value, tag} words ("flag in data"): an aligned 64-bit store / load is single-copy atomic, so a
+// reader that sees the expected tag sees the value written with it -- no fences, no counters.
+// tag = (launch << 20) + block: unique between the block's current writer, the previous user of its
+// slot (block - SPB, same launch) and the previous launch (exchange buffers are zeroed per solve).
+__device__ __forceinline__ unsigned long long ll_pack(float v, unsigned tag) {
+  return ((unsigned long long)tag << 32) | __float_as_uint(v);
 }
-__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void ll_store(unsigned long long* p, unsigned long long w) {
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
 }
+__device__ __forceinline__ unsigned long long ll_load(const unsigned long long* p) {
+  unsigned long long w;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+  return w;
+}
+__device__ __forceinline__ unsigned ll_tag(unsigned long long w) { return (unsigned)(w >> 32); }
+__device__ __forceinline__ float ll_val(unsigned long long w) { return __uint_as_float((unsigned)w); }
 __device__ __forceinline__ void bar_compute() {  // named barrier over the 8 compute warps only
   asm volatile("bar.sync 1, %0;" ::"n"(SNTH) : "memory");
 }
@@ -71,10 +80,11 @@ __global__ void __launch_bounds__(SNTX, 1) k_sink_strip(StripArgs a) {
   extern __shared__ __align__(128) float sdyn[];  // [nbuf][SRB][nf4] float4
   float4* ring = reinterpret_cast<float4*>(sdyn);
   __shared__ __align__(8) uint64_t full[16];      // TMA landed (per ring buffer)
-  __shared__ __align__(8) uint64_t wready[SWB];   // w of a block is in sw[slot] (exchange warp)
+  __shared__ __align__(8) uint64_t wready[SWB];   // w of a block is in sw[slot] (consumer warp)
   __shared__ __align__(8) uint64_t wfree[SWB];    // sw[slot] consumed (compute warps)
   __shared__ float sw[SWB][SRB];
   __shared__ double sacc[128 * 4];                // final fixed-order merge of the two row halves
+  __shared__ unsigned sepoch;
 
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int cta = blockIdx.x, NB = a.nb;
@@ -94,49 +104,95 @@ __global__ void __launch_bounds__(SNTX, 1) k_sink_strip(StripArgs a) {
       mbar_init(&wfree[s], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    sepoch = *reinterpret_cast<volatile unsigned*>(a.epoch);
   }
   __syncthreads();
+  const unsigned tag0 = sepoch << 20;  // tag of block b: tag0 + b
 
-  if (wid == NW) {
-    // ================= exchange warp =================
-    // lanes 2r, 2r+1 own row r of a block and sum the CTAs c = lane & 1, lane & 1 + 2, ... in order
-    constexpr int NV = SNBMAX / 2;
-    const int r = lane >> 1, par = lane & 1;
-    for (int bc = 0; bc < nblk; ++bc) {
-      const int ws_ = bc % SWB;
-      if (bc >= SWB) mbar_wait(&wfree[ws_], (uint32_t)(((bc / SWB) - 1) & 1));
-      const int cslot = bc & (SPB - 1);
-      if (lane == 0) {
-        const unsigned want = (unsigned)NB * (unsigned)(bc / SPB + 1);  // the slot's (bc/SPB + 1)-th use
-        long long spins = 0;
-        while (ld_acquire_u32(a.xcnt + cslot) < want) {
-          __nanosleep(20);
-          if (++spins > (1ll << 28)) __trap();  // a lost CTA: fail loudly instead of hanging
-        }
-      }
-      __syncwarp();
-      const float* src = a.xpart + (size_t)cslot * NB * SRB + r;
-      float v[NV];
-#pragma unroll
-      for (int k = 0; k < NV; ++k) {
-        const int c = par + 2 * k;
-        v[k] = c < NB ? __ldcg(src + (size_t)c * SRB) : 0.f;
-      }
+  if (wid == NW + 1) {
+    // ================= reducer warp: the blocks b = cta (mod NB) =================
+    // lanes r and r + 16 own row r and sum the CTAs c = h, h + 2, ... (h = lane >> 4) in order
+    constexpr int NV = SNBMAX / 4;  // words per lane per chunk (two chunks: c < 2 NV and c >= 2 NV)
+    const int r = lane & 15, h = lane >> 4;
+    for (int b = cta; b < nblk; b += NB) {
+      const unsigned want = tag0 + (unsigned)b;
+      const unsigned long long* src = a.xp + (size_t)(b & (SPB - 1)) * NB * SRB + r;
       float S = 0.f;
+#pragma unroll 1
+      for (int ch = 0; ch < 2; ++ch) {
+        const int cb = h + 2 * NV * ch;
+        unsigned long long v[NV];
 #pragma unroll
-      for (int k = 0; k < NV; ++k) S += v[k];
-      S += __shfl_xor_sync(0xffffffffu, S, 1);
-      if (par == 0) {
-        const int64_t i = (int64_t)bc * SRB + r;
-        float w = 0.f;
-        if (i < nl) {
-          w = __fdiv_rn(a.pf[i], S);
-          if (cta == (bc % NB)) a.Srow[i] = S;
+        for (int k = 0; k < NV; ++k) {
+          const int c = cb + 2 * k;
+          v[k] = c < NB ? ll_load(src + (size_t)c * SRB) : ll_pack(0.f, want);
         }
-        sw[ws_][r] = w;
+        long long spins = 0;
+        for (;;) {
+          bool ok = true;
+#pragma unroll
+          for (int k = 0; k < NV; ++k) {
+            if (ll_tag(v[k]) != want) {
+              ok = false;
+              v[k] = ll_load(src + (size_t)(cb + 2 * k) * SRB);
+            }
+          }
+          if (__all_sync(0xffffffffu, ok)) break;
+          __nanosleep(32);
+          if (++spins > (1ll << 26)) __trap();  // a lost CTA: fail loudly instead of hanging
+        }
+#pragma unroll
+        for (int k = 0; k < NV; ++k) S += ll_val(v[k]);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&wready[ws_]);
+      S += __shfl_xor_sync(0xffffffffu, S, 16);
+      if (h == 0) {
+        ll_store(a.xs + (size_t)(b & (SPB - 1)) * SRB + r, ll_pack(S, want));
+        if ((int64_t)b * SRB + r < nl) a.Srow[(int64_t)b * SRB + r] = S;
+      }
+    }
+    return;
+  }
+  if (wid == NW) {
+    // ================= consumer warp: w = p / S of every block, in order =================
+    // lanes r and r + 16 poll row r of the two blocks b0 + h and b0 + 2 + h of a 4-block window
+    const int r = lane & 15, h = lane >> 4;
+    int b0 = 0;
+    long long spins = 0;
+    while (b0 < nblk) {
+      unsigned long long w2[2];
+      float p2[2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int b = b0 + 2 * j + h;
+        w2[j] = b < nblk ? ll_load(a.xs + (size_t)(b & (SPB - 1)) * SRB + r) : 0ull;
+        const int64_t i = (int64_t)b * SRB + r;
+        p2[j] = (b < nblk && i < nl) ? a.pf[i] : 0.f;
+      }
+      int done = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {  // blocks b0 + q, in order, while ready
+        const int b = b0 + q;
+        const int j = q >> 1, hq = q & 1;
+        if (b >= nblk) break;
+        const bool mine = h == hq;
+        const bool ok = ll_tag(w2[j]) == tag0 + (unsigned)b;
+        const unsigned ball = __ballot_sync(0xffffffffu, mine && ok);
+        if (__popc(ball) != 16) break;
+        const int ws_ = b % SWB;
+        if (b >= SWB) mbar_wait(&wfree[ws_], (uint32_t)(((b / SWB) - 1) & 1));
+        if (mine) {
+          const int64_t i = (int64_t)b * SRB + r;
+          sw[ws_][r] = i < nl ? __fdiv_rn(p2[j], ll_val(w2[j])) : 0.f;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&wready[ws_]);
+        ++done;
+      }
+      b0 += done;
+      if (done == 0) {
+        __nanosleep(20);
+        if (++spins > (1ll << 27)) __trap();
+      }
     }
     return;
   }
@@ -221,10 +277,9 @@ __global__ void __launch_bounds__(SNTX, 1) k_sink_strip(StripArgs a) {
       for (int u = 0; u < RPW; ++u) {
 #pragma unroll
         for (int d = 16; d > 0; d >>= 1) ps[u] += __shfl_xor_sync(0xffffffffu, ps[u], d);
-        if (lane == 0) __stcg(a.xpart + ((size_t)slot * NB + cta) * SRB + wid + NW * u, ps[u]);
+        if (lane == 0)
+          ll_store(a.xp + ((size_t)slot * NB + cta) * SRB + wid + NW * u, ll_pack(ps[u], tag0 + (unsigned)b));
       }
-      bar_compute();  // the CTA's partials of block b are stored
-      if (t == 0) red_release_add(a.xcnt + slot, 1u);
     }
     // ---- accumulate block bc = b - lag: e w into the column sums ----
     const int bc = b - lag;
@@ -272,6 +327,8 @@ __global__ void __launch_bounds__(SNTX, 1) k_sink_strip(StripArgs a) {
       if (col < m) a.part[col] = acc64[e] + sacc[kc * 4 + e];
     }
   }
+  // every CTA read the epoch at its start (CTA 0 consumed every block, so every CTA produced them)
+  if (cta == 0 && t == 0) atomicAdd(a.epoch, 1u);
 }
 
 }  // namespace gw
