@@ -565,12 +565,21 @@ __global__ void k_sink_mode(float* __restrict__ dev, int* __restrict__ mode, flo
   }
 }
 
-// Chunked multi-rank loop (sink_run): after a fused step the decision may only go 1 -> 0 (a failed
-// step, or a correction above the threshold, freezes the chunk until the host runs the safe
-// iteration, whose k_sink_mode may return to the fused path).
-__global__ void k_sink_mode_fused(float* __restrict__ dev, int* __restrict__ mode, float thresh) {
+// Multi-rank fixed-count loop (sink_run): end of one iteration slot, decided on the device (every rank
+// reaches the same decision: the flag and the column corrections follow gathered data).  The slot
+// committed an update unless its fused attempt failed the validity check (flag != 0: nothing was
+// committed and the next slot runs the safe path).  Next path: fused iff this slot committed and its
+// column correction was within 2^thresh.  stop once `target` updates are committed.
+//   md: [0] path of the next slot, [5] committed updates, [6] target
+__global__ void k_sink_slot_end(int* __restrict__ md, float* __restrict__ dev, const int* __restrict__ flag,
+                                int* __restrict__ stop, float thresh) {
   if (threadIdx.x == 0) {
-    if (*mode == 1 && !(*dev <= thresh)) *mode = 0;
+    if (!*stop) {
+      const bool ok = *flag == 0;
+      if (ok) md[5] += 1;
+      md[0] = (ok && *dev <= thresh) ? 1 : 0;
+      if (md[5] >= md[6]) *stop = 1;
+    }
     *dev = 0.f;
   }
 }

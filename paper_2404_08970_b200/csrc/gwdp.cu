@@ -24,7 +24,6 @@
 #include "polyk.cuh"
 #include "ugw.cuh"
 #include "small.cuh"
-#include "strip.cuh"
 #include "sink.cuh"
 #include "vec.cuh"
 
@@ -112,9 +111,8 @@ struct gw_ctx {
   Buf uga, ugb, ugct, ugpart, ugca, ugcb, ugfr, uggr, ugsc;  // UGW
   Buf g2rc, g2rd, g2h, g2cc, g2tt, g2vt, g2tmp, g2s, g2a, g2b, g2ca, g2cb, g2part;  // 2-D grids
   Buf xtab, xg1, xg2, xin, xvec, xtail, xpart;  // multi-rank exchange buffers
-  Buf slse, slseg, scsl, scsg, sviolg;          // Sinkhorn column-sum exchange
+  Buf slse, slseg, scsl, scsg, sviolg, sun, sung;  // Sinkhorn column-sum exchange
   Buf sflag, sflagg;
-  Buf stx, sts, ste;  // strip Sinkhorn: row-sum exchange (partials, block sums, launch counter)
   Buf fsc, gsc;  // scaled duals for the Gibbs regeneration
   Buf Gs;        // solver cost buffer
   double* hpin = nullptr;  // pinned host scratch (64 doubles)
@@ -128,12 +126,11 @@ struct gw_ctx {
     Buf* b[] = {&stage, &mom, &xc, &yc, &pn, &qn, &lp, &lq, &cvx, &cvy, &fs, &gs, &fh, &fl, &gh, &gl,
                 &ftmp, &viol, &stop, &iters, &part, &fpart, &mode, &srow, &pfl, &rP, &rA, &cS, &cX, &blk, &bs, &btot, &cxend,
                 &SAg, &WAg, &Ptot, &Aend, &DP, &DA, &tobj, &tent, &tcc, &objout, &scanwt, &fxs, &fys, &fsc, &gsc, &Gs,
-                &pnf, &qnf, &xtab, &xg1, &xg2, &xin, &xvec, &xtail, &xpart, &slse, &slseg, &scsl, &scsg,
+                &pnf, &qnf, &xtab, &xg1, &xg2, &xin, &xvec, &xtail, &xpart, &slse, &slseg, &scsl, &scsg, &sun, &sung,
                 &sviolg, &sflag, &sflagg, &yfb, &pcoef, &pc2s, &pfx, &pfy, &ppart, &pM,
                 &gkrp, &gkrt, &gkcp, &gkz, &gkct, &gkctt, &gkobj,
                 &uga, &ugb, &ugct, &ugpart, &ugca, &ugcb, &ugfr, &uggr, &ugsc,
-                &g2rc, &g2rd, &g2h, &g2cc, &g2tt, &g2vt, &g2tmp, &g2s, &g2a, &g2b, &g2ca, &g2cb, &g2part,
-                &stx, &sts, &ste};
+                &g2rc, &g2rd, &g2h, &g2cc, &g2tt, &g2vt, &g2tmp, &g2s, &g2a, &g2b, &g2ca, &g2cb, &g2part};
     for (Buf* x : b) all.push_back(x);
   }
 };
@@ -1174,22 +1171,18 @@ struct SinkState {
   int nrb;
   int64_t RB;
   // fused fast path
-  int* mode;      // [0] = path of the current iteration (1 = fused), [1] = fused iterations run
+  int* mode;      // [0] = path of the current iteration (1 = fused), [1] = fused iterations run,
+                  // [2] = dev (float), [5] / [6] = committed / target updates (multi-rank fixed-count loop)
   float* dev;     // max |log2(colsum/q)| of the last column half-step
   double* fpart;  // [ncl][m]
   float* Srow;    // [nl]
   float* pf;      // [nl] p as fp32
   int fK = 0, fCL = 0, fNT = 256, fncl = 0;  // fK == 0: fast path unavailable for this shape
-  // strip variant of the fused iteration (strip.cuh): one CTA per SM, grid-wide row-sum exchange
-  bool strip = false;
-  int sKF = 0, snb = 0, snbuf = 0, slag = 0;
-  size_t sdsm = 0;
-  unsigned long long *sxp = nullptr, *sxs = nullptr;
-  unsigned* sepoch = nullptr;
   int64_t fW = 0;                            // columns per CTA
   int64_t frpc = 0;
   // column-sum exchange: this rank's column LSE pairs / column sums, and all ranks' (gathered)
   double *lse, *lseg, *csl, *csg;
+  double *un = nullptr, *ung = nullptr;  // multi-rank fixed-count loop: payload (M + 1) and gathered
   float* violg;
   int *flag, *flagg;  // speculation validity flag (and the ranks' flags)
   cudaGraphExec_t gexec = nullptr;  // one fixed-count iteration, captured once per solve
@@ -1278,74 +1271,6 @@ static gw_status fused_launch(gw_ctx* c, int K, int CL, int NT, const FusedArgs&
   FUSED_DISPATCH(fused_launch_t, c, fa, ncl)
 }
 
-template <int KF>
-static gw_status strip_launch_t(gw_ctx* c, const StripArgs& sa, size_t dsm) {
-  static std::atomic<size_t> attr_set[8];  // the dynamic smem attribute, raised monotonically
-  if (attr_set[KF].load() < dsm) {
-    CU(cudaFuncSetAttribute(k_sink_strip<KF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
-    attr_set[KF].store(dsm);
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(sa.nb);
-  cfg.blockDim = dim3(SNTX);
-  cfg.dynamicSmemBytes = dsm;
-  cfg.stream = c->stream;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeCooperative;  // every CTA co-resident (grid-wide exchange)
-  at[0].val.cooperative = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  CU(cudaLaunchKernelEx(&cfg, k_sink_strip<KF>, sa));
-  return GW_OK;
-}
-static gw_status strip_launch(gw_ctx* c, int KF, const StripArgs& sa, size_t dsm) {
-  switch (KF) {
-    case 2: return strip_launch_t<2>(c, sa, dsm);
-    case 4: return strip_launch_t<4>(c, sa, dsm);
-    default: return fail(GW_ERR_UNSUPPORTED, "strip Sinkhorn: no instance KF=%d", KF);
-  }
-}
-
-// Strip variant eligibility (strip.cuh): wide rows (every SM gets >= 32 float4 per row), enough rows
-// for the exchange pipeline, and -- since its CTAs wait on each other -- one ctx per device at a time:
-// NCCL ranks (one GPU each) or a single rank; the host-transport shard tests drive several ctxs on one
-// GPU concurrently and keep the cluster kernel.  GWDP_STRIP=0/1 forces it off / on (where it fits).
-static bool strip_config(gw_ctx* c, const Prepared& P, SinkState& s) {
-  const char* e = getenv("GWDP_STRIP");
-  const int force = e ? atoi(e) : -1;
-  if (force != 1) return false;  // opt-in until measured faster than the cluster kernel
-  if (P.nl < 4 * SRB || (P.nl + SRB - 1) / SRB >= (1 << 20) - 1) return false;
-  const bool exclusive = P.R == 1 || (c->comm && c->comm->nccl);
-  if (!exclusive) return false;
-  int nsm = 0;
-  if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device) != cudaSuccess || nsm <= 0) {
-    cudaGetLastError();
-    return false;
-  }
-  if (nsm > SNBMAX) return false;
-  const int64_t M4 = (P.m + 3) / 4;
-  const int64_t nf4max = (M4 + nsm - 1) / nsm;
-  if (force != 1 && nf4max < 32) return false;  // narrow strips: the cluster kernel is the better fit
-  if (nf4max > 128) return false;
-  const int KF = nf4max <= 64 ? 2 : 4;
-  const size_t per = (size_t)SRB * nf4max * 16;
-  const size_t cap = 200 * 1024;
-  int nbuf = (int)std::min<size_t>(cap / per, 12);
-  const char* eb = getenv("GWDP_STRIP_NBUF");
-  if (eb) nbuf = std::min(nbuf, atoi(eb));
-  int lag = nbuf - 3;
-  const char* el = getenv("GWDP_STRIP_LAG");
-  if (el) lag = atoi(el);
-  if (nbuf < 3 || lag < 1 || lag > nbuf - 2 || lag > SPB - 2 || lag > SWB) return false;
-  s.strip = true;
-  s.sKF = KF;
-  s.snb = nsm;
-  s.snbuf = nbuf;
-  s.slag = lag;
-  s.sdsm = (size_t)nbuf * per;
-  return true;
-}
-
 static gw_status sink_alloc(gw_ctx* c, const Prepared& P, SinkState& s) {
   TRY(ws(c, c->fh, P.nl, &s.fh)); TRY(ws(c, c->fl, P.nl, &s.fl));
   TRY(ws(c, c->gh, P.m, &s.gh)); TRY(ws(c, c->gl, P.m, &s.gl));
@@ -1368,6 +1293,9 @@ static gw_status sink_alloc(gw_ctx* c, const Prepared& P, SinkState& s) {
   if (P.R > 1) {
     TRY(ws(c, c->slseg, 2 * (size_t)P.m * P.R, &s.lseg));
     TRY(ws(c, c->scsg, ((size_t)P.m + 1) * P.R, &s.csg));
+    // the fixed-count loop's one payload per iteration: column sums or packed LSE pairs + row flag
+    TRY(ws(c, c->sun, (size_t)P.m + 1, &s.un));
+    TRY(ws(c, c->sung, ((size_t)P.m + 1) * P.R, &s.ung));
     TRY(ws(c, c->sviolg, (size_t)P.R, &s.violg));
   } else {
     s.lseg = s.lse;
@@ -1376,7 +1304,7 @@ static gw_status sink_alloc(gw_ctx* c, const Prepared& P, SinkState& s) {
   }
   // fused fast path: cluster of CL CTAs x W = 1024 K columns spans a row
   int* md;
-  TRY(ws(c, c->mode, 4, &md));
+  TRY(ws(c, c->mode, 8, &md));
   s.mode = md;
   s.dev = reinterpret_cast<float*>(md + 2);
   s.fK = 0;
@@ -1398,22 +1326,7 @@ static gw_status sink_alloc(gw_ctx* c, const Prepared& P, SinkState& s) {
     if (CL == 3) CL = 4;
     if (CL > 4 && CL < 8) CL = 8;
     const int64_t wcol = 4 * (int64_t)K * NT;
-    if (strip_config(c, P, s)) {
-      // the strip kernel: column sums complete per rank (one "cluster" payload), exchange scratch
-      s.fK = K; s.fCL = CL; s.fNT = NT; s.fncl = 1; s.fW = wcol;
-      s.frpc = P.nl;
-      TRY(ws(c, c->fpart, (size_t)P.m, &s.fpart));
-      TRY(ws(c, c->srow, (size_t)P.nl, &s.Srow));
-      TRY(ws(c, c->pfl, (size_t)P.nl, &s.pf));
-      TRY(ws(c, c->stx, (size_t)SPB * s.snb * SRB, &s.sxp));
-      TRY(ws(c, c->sts, (size_t)SPB * SRB, &s.sxs));
-      TRY(ws(c, c->ste, 1, &s.sepoch));
-      // tag 0xffffffff is never a block's tag (nblk < 2^20 - 1): no stale word looks published
-      CU(cudaMemsetAsync(s.sxp, 0xff, (size_t)SPB * s.snb * SRB * sizeof(unsigned long long), c->stream));
-      CU(cudaMemsetAsync(s.sxs, 0xff, (size_t)SPB * SRB * sizeof(unsigned long long), c->stream));
-      k_to_float<<<grid_for(P.nl), 256, 0, c->stream>>>(P.pn + P.row0, P.nl, s.pf);
-      KCHECK();
-    } else if (CL <= 8) {  // clusters must fit in a GPC: on B200 clusters of 8 leave 28 SMs idle
+    if (CL <= 8) {  // clusters must fit in a GPC: on B200 clusters of 8 leave 28 SMs idle
       int ncl = 0;
       TRY(fused_config(c, K, CL, NT, &ncl));
       if (ncl > 0) {
@@ -1525,16 +1438,7 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
     // two-kernel path below runs this same iteration.  No host sync.
     if (s.fK > 0) {
       PROF_BEGIN(c, PC_SINK_FUSED);
-      if (s.strip) {
-        StripArgs sa;
-        sa.G = G; sa.ld = ldG; sa.nl = nl; sa.m = m; sa.c2f = c2f; sa.gh = s.gh; sa.fh = s.fh; sa.pf = s.pf;
-        sa.Srow = s.Srow; sa.part = s.fpart; sa.xp = s.sxp; sa.xs = s.sxs; sa.epoch = s.sepoch;
-        sa.nb = s.snb; sa.nbuf = s.snbuf; sa.lag = s.slag;
-        sa.mode = s.mode; sa.stop = s.stop;
-        TRY(strip_launch(c, s.sKF, sa, s.sdsm));
-      } else {
-        TRY(fused_launch(c, s.fK, s.fCL, s.fNT, fa, s.fncl));
-      }
+      TRY(fused_launch(c, s.fK, s.fCL, s.fNT, fa, s.fncl));
       KCHECK();
       // one rank: column sums, check (rows + columns), commit.  R > 1: the rank's row check rides in
       // the column-sum payload (slot M), so ONE all-gather per iteration carries everything.
@@ -1600,55 +1504,97 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
     KCHECK();
     return GW_OK;
   };
-  // Fixed iteration counts on several ranks: the device-skipped safe path would still issue its
-  // column all-gather every iteration (the host cannot see the device's path decision), so the
-  // iterations run as chunks of fused steps; after each chunk ONE host read of the committed-step
-  // counter tells every rank (identically: the counter follows gathered data) whether a step failed
-  // or asked for the safe path, which then runs exactly that iteration.  Same sequence of committed
-  // updates as the per-iteration form.
+  // Fixed iteration counts on several ranks: every iteration SLOT issues exactly one all-gather of one
+  // payload of M + 1 doubles: the fused path's column sums (+ this rank's row flag in slot M), or the
+  // safe path's column LSE pairs packed as 8-byte {float max, float sum}; the kernels of the path not
+  // taken exit at once (decided on the device, identically on every rank:
+  // the decision follows gathered data).  A slot whose fused attempt fails the validity check commits
+  // nothing and the next slot runs the safe path, so the committed updates are exactly those of the
+  // single-rank loop; slots are replayed (a CUDA graph per solve over NCCL) until `iters` updates are
+  // committed -- iters + SLACK slots per round, the device stops after the target, ONE host read per
+  // round (no host sync inside the inner loop unless more than SLACK fused attempts fail).
   if (!tolmode && P.R > 1 && s.fK > 0) {
-    constexpr int CH = 10;
-    int* hc = reinterpret_cast<int*>(c->hpin + 40);
-    CU(cudaMemcpyAsync(hc, s.mode, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    CU(cudaStreamSynchronize(c->stream));
-    int base = hc[1], done = 0;
-    while (done < iters) {
-      const int chunk = std::min(CH, iters - done);
-      for (int k = 0; k < chunk; ++k) {
-        TRY(fused_step());
-        k_sink_mode_fused<<<1, 32, 0, c->stream>>>(s.dev, s.mode, 20.f);
-        KCHECK();
+    const int64_t U = m + 1;
+    double* uc = s.un;           // [0, m): column sums (fused) or packed LSE pairs (safe), [m]: row flag
+    CU(cudaMemsetAsync(s.mode + 5, 0, 2 * sizeof(int), c->stream));
+    k_fill_int<<<1, 32, 0, c->stream>>>(s.mode + 6, iters);
+    KCHECK();
+    auto slot = [&]() -> gw_status {
+      CU(cudaMemsetAsync(s.flag, 0, sizeof(int), c->stream));
+      CU(cudaMemsetAsync(uc + m, 0, sizeof(double), c->stream));
+      PROF_BEGIN(c, PC_SINK_FUSED);
+      TRY(fused_launch(c, s.fK, s.fCL, s.fNT, fa, s.fncl));
+      KCHECK();
+      k_sink_colsum<<<(unsigned)((m + 31) / 32), 256, 0, c->stream>>>(s.fpart, s.fncl, m, uc, s.mode, s.stop, s.Srow,
+                                                                      nl, reinterpret_cast<int*>(uc + m));
+      KCHECK();
+      PROF_END(c, PC_SINK_FUSED, 2);
+      // the safe path's local half (skipped unless *mode == 0): row update, then column LSE pairs
+      PROF_BEGIN(c, PC_SINK_ROW);
+      k_sink_row<<<rgrid, 256, 0, c->stream>>>(G, ldG, nl, m, s.gh, s.gl, c2f, s.f, s.f, P.lp + P.row0, eps, s.fh,
+                                                s.fl, nullptr, s.stop, s.mode);
+      KCHECK();
+      PROF_END(c, PC_SINK_ROW, 1);
+      PROF_BEGIN(c, PC_SINK_COL);
+      k_sink_col<<<cgrid, 256, 0, c->stream>>>(G, ldG, nl, m, s.fh, s.fl, c2f, s.RB, s.part, s.stop, s.mode);
+      KCHECK();
+      k_sink_colmerge<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.part, s.nrb, m, uc, s.stop, s.mode, true);
+      KCHECK();
+      PROF_END(c, PC_SINK_COL, 1);
+      TRY(comm_allgather(c, s.un, s.ung, sizeof(double) * (size_t)U));
+      // safe path: g from the gathered LSE pairs (before the fused finish, which may switch *mode)
+      k_sink_colfin<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.ung, P.R, m, P.lq, eps, s.g, s.gh, s.gl,
+                                                                       s.stop, s.mode, s.dev, 1.0, U, true);
+      KCHECK();
+      // fused path: validity of the speculative iteration (all ranks' row flags, the gathered column
+      // sums), then commit -- or not, and switch to the safe path
+      k_sink_fast_check<<<grid_for(std::max(m, nl), 256, 1 << 30), 256, 0, c->stream>>>(
+          s.Srow, nl, s.ung, P.R, U, m, P.lq, s.flag, s.mode, s.stop, true);
+      KCHECK();
+      k_sink_fin_fast<<<grid_for(std::max(m, nl), 256, 1 << 30), 256, 0, c->stream>>>(
+          s.Srow, nl, P.lp + P.row0, s.f, s.fh, s.fl, nullptr, s.ung, P.R, U, m, P.lq, eps, s.g, s.gh, s.gl,
+          s.mode, s.stop, s.dev, s.flag);
+      KCHECK();
+      k_sink_slot_end<<<1, 32, 0, c->stream>>>(s.mode, s.dev, s.flag, s.stop, 20.f);
+      KCHECK();
+      return GW_OK;
+    };
+    static const bool no_graph_mr = getenv("GWDP_NO_GRAPH") != nullptr;
+    const bool graph = !no_graph_mr && !c->prof.on && c->comm && c->comm->nccl;  // host transport: not capturable
+    if (graph && !s.gexec) {
+      if (!c->cap) CU(cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking));
+      CU(cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal));
+      cudaStream_t saved = c->stream;
+      c->stream = c->cap;
+      const gw_status st = slot();
+      c->stream = saved;
+      cudaGraph_t gr = nullptr;
+      const cudaError_t e = cudaStreamEndCapture(c->cap, &gr);
+      if (st != GW_OK) {
+        if (gr) cudaGraphDestroy(gr);
+        return st;
       }
-      CU(cudaMemcpyAsync(hc, s.mode, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-      CU(cudaStreamSynchronize(c->stream));
-      const int committed = hc[1] - base;
-      base = hc[1];
-      done += committed;
-      // this iteration (and, while the decision stays on the safe path, the next ones) on the safe path
-      while (committed < chunk && done < iters) {
-        PROF_BEGIN(c, PC_SINK_ROW);
-        k_sink_row<<<rgrid, 256, 0, c->stream>>>(G, ldG, nl, m, s.gh, s.gl, c2f, s.f, s.f, P.lp + P.row0, eps,
-                                                  s.fh, s.fl, nullptr, s.stop, nullptr);
-        KCHECK();
-        PROF_END(c, PC_SINK_ROW, 1);
-        PROF_BEGIN(c, PC_SINK_COL);
-        k_sink_col<<<cgrid, 256, 0, c->stream>>>(G, ldG, nl, m, s.fh, s.fl, c2f, s.RB, s.part, s.stop, nullptr);
-        KCHECK();
-        k_sink_colmerge<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.part, s.nrb, m, s.lse, s.stop, nullptr);
-        KCHECK();
-        TRY(comm_allgather(c, s.lse, s.lseg, 2 * sizeof(double) * (size_t)m));
-        k_sink_colfin<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.lseg, P.R, m, P.lq, eps, s.g, s.gh,
-                                                                         s.gl, s.stop, nullptr, s.dev);
-        KCHECK();
-        PROF_END(c, PC_SINK_COL, 2);
-        k_sink_mode<<<1, 32, 0, c->stream>>>(s.dev, s.mode, 20.f);
-        KCHECK();
-        done += 1;
-        CU(cudaMemcpyAsync(hc, s.mode, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-        CU(cudaStreamSynchronize(c->stream));
-        if (hc[0] == 1) break;  // back on the fused path (the safe path does not move the counter)
-      }
+      if (e != cudaSuccess) return fail(GW_ERR_CUDA, "Sinkhorn graph capture (multi-rank): %s", cudaGetErrorString(e));
+      const cudaError_t ei = cudaGraphInstantiate(&s.gexec, gr, 0);
+      cudaGraphDestroy(gr);
+      if (ei != cudaSuccess) return fail(GW_ERR_CUDA, "Sinkhorn graph instantiate: %s", cudaGetErrorString(ei));
     }
+    constexpr int SLACK = 4;
+    int* hc = reinterpret_cast<int*>(c->hpin + 40);
+    int committed = 0;
+    for (int round = 0; committed < iters; ++round) {
+      const int nslots = (iters - committed) + SLACK;
+      for (int k = 0; k < nslots; ++k) {
+        if (graph) CU(cudaGraphLaunch(s.gexec, c->stream));
+        else TRY(slot());
+      }
+      CU(cudaMemcpyAsync(hc, s.mode + 5, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      CU(cudaStreamSynchronize(c->stream));
+      committed = hc[0];
+      if (round > 64) return fail(GW_ERR_CUDA, "multi-rank Sinkhorn: no progress (%d of %d updates)", committed, iters);
+    }
+    // the device stop flag is left set; later calls reset it
+    CU(cudaMemsetAsync(s.stop, 0, sizeof(int), c->stream));
     *used = iters;
     return GW_OK;
   }

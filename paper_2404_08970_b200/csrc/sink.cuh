@@ -193,8 +193,11 @@ __global__ void __launch_bounds__(256) k_sink_col(const float* __restrict__ G, i
 
 // Column half-step, pass 2a: merge this rank's row-block partials in fixed order, in fp64:
 // lse[q] = max_rb M, lse[m + q] = sum_rb S_rb 2^(M_rb - max).
+// pack: write the pair as ONE 8-byte {float M, float S} per column (M is a max of fp32 values, exact in
+// fp32; S in [1, nrb] rounded once to fp32), so the pairs fit the multi-rank loop's M-double payload.
 __global__ void k_sink_colmerge(const float2* __restrict__ part, int nrb, int64_t m, double* __restrict__ lse,
-                                const int* __restrict__ stop, const int* __restrict__ skip_if_fast) {
+                                const int* __restrict__ stop, const int* __restrict__ skip_if_fast,
+                                bool pack = false) {
   if (stop && *stop) return;
   if (skip_if_fast && *skip_if_fast) return;
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -207,27 +210,44 @@ __global__ void k_sink_colmerge(const float2* __restrict__ part, int nrb, int64_
       const float2 v = part[(int64_t)rb * m + q];
       if (v.x != -INFINITY) S += (double)v.y * exp2((double)v.x - M);
     }
-  lse[q] = M;
-  lse[m + q] = S;
+  if (pack) {
+    reinterpret_cast<float2*>(lse)[q] = make_float2((float)M, (float)S);
+  } else {
+    lse[q] = M;
+    lse[m + q] = S;
+  }
 }
 
 // Column half-step, pass 2b: merge the R ranks' (M, S) pairs (gath [R][2m]) in rank order and
 // update g (identical on every rank).
+// gstride: doubles between two ranks' payloads in gath (0: 2m; the multi-rank fixed-count loop gathers
+// the column sums and the LSE pairs in one payload, so its pairs sit at a larger stride).
 __global__ void k_sink_colfin(const double* __restrict__ gath, int R, int64_t m, const double* __restrict__ lq,
                               double eps, double* __restrict__ g, float* __restrict__ gh, float* __restrict__ gl,
                               const int* __restrict__ stop, const int* __restrict__ skip_if_fast,
-                              float* __restrict__ dev, double kappa = 1.0) {
+                              float* __restrict__ dev, double kappa = 1.0, int64_t gstride = 0,
+                              bool packed = false) {
   if (stop && *stop) return;
   if (skip_if_fast && *skip_if_fast) return;
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (q >= m) return;
+  const int64_t gs_ = gstride > 0 ? gstride : 2 * m;
+  // rank r's pair: {M, S} doubles at [r gs_ + q], [r gs_ + m + q], or packed {float M, float S} at
+  // 8-byte slot r gs_ + q (k_sink_colmerge's pack)
+  auto Mof = [&](int r) -> double {
+    return packed ? (double)reinterpret_cast<const float2*>(gath + (int64_t)r * gs_)[q].x : gath[(int64_t)r * gs_ + q];
+  };
+  auto Sof = [&](int r) -> double {
+    return packed ? (double)reinterpret_cast<const float2*>(gath + (int64_t)r * gs_)[q].y
+                  : gath[(int64_t)r * gs_ + m + q];
+  };
   double M = -INFINITY;
-  for (int r = 0; r < R; ++r) M = fmax(M, gath[(int64_t)r * 2 * m + q]);
+  for (int r = 0; r < R; ++r) M = fmax(M, Mof(r));
   double S = 0.0;
   if (M != -INFINITY)
     for (int r = 0; r < R; ++r) {
-      const double Mr = gath[(int64_t)r * 2 * m + q];
-      if (Mr != -INFINITY) S += gath[(int64_t)r * 2 * m + m + q] * exp2(Mr - M);
+      const double Mr = Mof(r);
+      if (Mr != -INFINITY) S += Sof(r) * exp2(Mr - M);
     }
   const double lse2 = M + log2(S);
   const double gn = (lq[q] == -INFINITY) ? -INFINITY : eps * lq[q] - kappa * (eps * GW_LN2 * lse2);

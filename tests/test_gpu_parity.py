@@ -269,32 +269,6 @@ def test_sinkhorn_fused_path_parity(gw, monkeypatch, n, m, eps):
     assert np.max(np.abs(T - To)) <= 1e-4 * np.max(To)
 
 
-@pytest.mark.parametrize("n,m,eps", [(300, 20000, 0.02), (64, 65536, 0.01), (1000, 40000, 0.01), (65, 70001, 0.02),
-                                     (2000, 9472, 0.02), (129, 75000, 0.01)])
-def test_sinkhorn_strip_path_parity(gw, monkeypatch, n, m, eps):
-    """The strip variant of the one-read iteration (strip.cuh: one CTA per SM owns a column strip of
-    every row, row sums exchanged grid-wide; ragged row blocks, m % 4 != 0, uneven strips) against the
-    oracle, and against the cluster kernel's result."""
-    monkeypatch.setenv("GWDP_NO_SMALL", "1")
-    rng = np.random.default_rng(n * 5 + m)
-    G = rng.random((n, m)).astype(np.float32)
-    p, q = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))
-    Gd = _to_dev(gw, G)
-    monkeypatch.setenv("GWDP_STRIP", "1")
-    r = gw.sinkhorn(Gd, p, q, eps, 60, return_plan=True)
-    assert r["fused_iters"] > 0
-    f, g, _ = O.sinkhorn(G.astype(np.float64), p, q, eps, 60)
-    To = O.plan_from_duals(G.astype(np.float64), f, g, eps)
-    T = r["T"].cpu().numpy().astype(np.float64)
-    assert np.max(np.abs(T - To)) <= 1e-4 * np.max(To)
-    # deterministic: the same bits again
-    r2 = gw.sinkhorn(Gd, p, q, eps, 60)
-    assert np.array_equal(r["g"].cpu().numpy(), r2["g"].cpu().numpy())
-    monkeypatch.setenv("GWDP_STRIP", "0")
-    c = gw.sinkhorn(Gd, p, q, eps, 60)
-    np.testing.assert_allclose(r["g"].cpu().numpy(), c["g"].cpu().numpy(), rtol=0, atol=1e-4 * eps)
-
-
 def test_fused_matches_safe_path(gw, monkeypatch):
     rng = np.random.default_rng(11)
     n, m, eps = 700, 12000, 0.02
