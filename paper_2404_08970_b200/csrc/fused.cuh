@@ -37,7 +37,8 @@ struct FusedArgs {
   const float* gl;
   const float* fh;            // f log2e/eps, fp32 hi / lo (local rows)
   const float* fl;
-  const float* pf;            // p (local rows, fp32)
+  const float* pf;            // balanced (kappa == 1): p (local rows, fp32); unbalanced: log2 u
+  float kappa;                // 1: balanced; < 1: unbalanced row factor (UGW, reading R34)
   float* Srow;                // out: S_i = row sums of the plan entering the iteration
   double* part;               // [nclusters][m] column sums of the half-step plan
   int64_t rows_per_cluster;
@@ -55,9 +56,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ float rcp_ftz(float x) {
+__device__ __forceinline__ float lg2_ftz(float x) {
   float y;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 __device__ __forceinline__ float ex2_ftz(float x) {
@@ -292,6 +293,8 @@ __global__ void __launch_bounds__(NT, 1) k_sink_fused2(FusedArgs a) {
       acc64[(k * 4 + 2 * h + 1) * NT + t] = 0.0;
     }
   const float2 nc2 = make_float2(-a.c2f, -a.c2f);
+  const bool ugw = a.kappa != 1.f;
+  const float km1 = a.kappa - 1.f;
   float2 eA0[K][2], eA1[K][2], eB0[K][2], eB1[K][2];
   float2 pA = make_float2(0.f, 0.f), pB = pA;  // marginals of the pair's two rows
   float2 Fnx = make_float2(nrows > 0 ? fh[0] : 0.f, nrows > 1 ? fh[1] : 0.f);
@@ -332,6 +335,10 @@ __global__ void __launch_bounds__(NT, 1) k_sink_fused2(FusedArgs a) {
     if (j0 < nrows) {
       const float2 F = Fnx;
       pcur = pnx;
+      if (ugw) {  // the row factor's constant part log2 u + (kappa - 1) F (F: the hi part the row uses)
+        pcur.x = fmaf(km1, F.x, pcur.x);
+        pcur.y = fmaf(km1, F.y, pcur.y);
+      }
       if (j0 + 2 < nrows) Fnx.x = fh[j0 + 2], pnx.x = pf[j0 + 2];
       if (j1 + 2 < nrows) Fnx.y = fh[j1 + 2], pnx.y = pf[j1 + 2];
       float s0, s1 = 0.f;
@@ -423,8 +430,16 @@ __global__ void __launch_bounds__(NT, 1) k_sink_fused2(FusedArgs a) {
         if (jp1 < nrows) Srow[jp1] = S1;
         if (Pp + NSLOT < npairs) mbar_expect_tx(&xbar[psl], xbytes);
       }
-      const float w0 = pprv.x * rcp_ftz(S0);
-      const float w1 = jp1 < nrows ? pprv.y * rcp_ftz(S1) : 0.f;
+      // half-step row factor: balanced w = p / S (IEEE division); unbalanced (R34, absorbed duals)
+      // w = 2^(log2 u + (kappa - 1) F - kappa log2 S), i.e. f'_new = eps~ ln u - kappa eps~ (ln S - F ln 2)
+      float w0, w1 = 0.f;
+      if (!ugw) {
+        w0 = __fdiv_rn(pprv.x, S0);
+        if (jp1 < nrows) w1 = __fdiv_rn(pprv.y, S1);
+      } else {
+        w0 = ex2_ftz(fmaf(-a.kappa, lg2_ftz(S0), pprv.x));
+        if (jp1 < nrows) w1 = ex2_ftz(fmaf(-a.kappa, lg2_ftz(S1), pprv.y));
+      }
       const float2 w02 = make_float2(w0, w0), w12 = make_float2(w1, w1);
 #pragma unroll
       for (int k = 0; k < K; ++k) {
@@ -508,7 +523,8 @@ __global__ void k_sink_fin_fast(const float* __restrict__ Srow, int64_t nl, cons
                                 int64_t m,
                                 const double* __restrict__ lq, double eps, double* __restrict__ g,
                                 float* __restrict__ gh, float* __restrict__ gl, int* __restrict__ mode,
-                                const int* __restrict__ stop, float* __restrict__ dev, const int* __restrict__ flag) {
+                                const int* __restrict__ stop, float* __restrict__ dev, const int* __restrict__ flag,
+                                double kappa = 1.0) {
   if (*mode != 1 || (stop && *stop)) return;
   if (*flag) {
     // speculation failed: nothing is committed and this iteration runs the safe path instead
@@ -521,8 +537,14 @@ __global__ void k_sink_fin_fast(const float* __restrict__ Srow, int64_t nl, cons
   if (q < m) {
     double CS = 0.0;
     for (int c = 0; c < ncl; ++c) CS += part[(int64_t)c * stride + q];
-    const double d = lq[q] - log(CS);  // ln(q / CS)
-    const double gn = (lq[q] == -INFINITY) ? -INFINITY : g[q] + eps * d;
+    double d = lq[q] - log(CS);  // ln(q / CS)
+    double gn;
+    if (kappa == 1.0) {
+      gn = (lq[q] == -INFINITY) ? -INFINITY : g[q] + eps * d;
+    } else {  // unbalanced (R34, absorbed duals): g'_new = eps~ ln v - kappa eps~ (ln CS - gh ln 2)
+      gn = (lq[q] == -INFINITY) ? -INFINITY : eps * lq[q] - kappa * eps * (log(CS) - (double)gh[q] * GW_LN2);
+      d = (gn - g[q]) / eps;
+    }
     g[q] = gn;
     const double gs = gn * (GW_LOG2E / eps);
     const float h = (float)gs;
@@ -536,7 +558,9 @@ __global__ void k_sink_fin_fast(const float* __restrict__ Srow, int64_t nl, cons
     // the kernel used only the fp32 hi part of f log2e/eps: S' = S 2^{-Fl}; the row
     // normalisation is then f <- f + eps (ln p - ln S') which absorbs the dropped lo part
     const double S = (double)Srow[q];
-    const double fn = (lp[q] == -INFINITY) ? -INFINITY : f[q] + eps * (lp[q] - log(S));
+    double fn;
+    if (kappa == 1.0) fn = (lp[q] == -INFINITY) ? -INFINITY : f[q] + eps * (lp[q] - log(S));
+    else fn = (lp[q] == -INFINITY) ? -INFINITY : eps * lp[q] - kappa * eps * (log(S) - (double)fh[q] * GW_LN2);
     f[q] = fn;
     const double fs = fn * (GW_LOG2E / eps);
     const float h = (float)fs;

@@ -1186,6 +1186,7 @@ struct SinkState {
   float* violg;
   int *flag, *flagg;  // speculation validity flag (and the ranks' flags)
   cudaGraphExec_t gexec = nullptr;  // one fixed-count iteration, captured once per solve
+  double g_eps = 0.0, g_kappa = 0.0;  // the scalars baked into gexec (UGW changes them per outer iteration)
 };
 
 static void sink_free(SinkState& s) {
@@ -1408,8 +1409,11 @@ static int small_cluster(gw_ctx* c, const Prepared& P, int* rows_out, size_t* by
 // host sync per check); returns the iterations used and whether tol was met.
 // Multi-rank: f is per-shard, g replicated; every column half-step gathers the ranks' column
 // sums (the only exchange), and every rank reaches the same path decision and stop flag.
+// kappa (UGW, reading R34): the unbalanced updates f' = eps ln u - kappa eps LSE, g' likewise, in the
+// absorbed-dual form (P.lp, P.lq = ln u, ln v); 1 = balanced.
 static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const float* G, int64_t ldG, double eps,
-                          int iters, double tol, int check_every, int* used, int* converged, bool reset_count = true) {
+                          int iters, double tol, int check_every, int* used, int* converged, bool reset_count = true,
+                          double kappa = 1.0) {
   NvtxRange nv("gw.sinkhorn");
   const int64_t nl = P.nl, m = P.m;
   const float c2f = (float)(GW_LOG2E / eps);
@@ -1430,6 +1434,11 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
   fa.G = G; fa.ld = ldG; fa.nl = nl; fa.m = m; fa.c2f = c2f; fa.gh = s.gh; fa.gl = s.gl; fa.fh = s.fh;
   fa.fl = s.fl; fa.pf = s.pf; fa.Srow = s.Srow; fa.part = s.fpart; fa.rows_per_cluster = s.frpc;
   fa.mode = s.mode; fa.stop = s.stop; fa.wcol = s.fW;
+  fa.kappa = (float)kappa;
+  if (kappa != 1.0 && s.fK > 0) {  // the fused kernel's row term: log2 u (fp32) instead of p
+    k_scale_f<<<grid_for(nl), 256, 0, c->stream>>>(P.lp + P.row0, nl, GW_LOG2E, s.pf);
+    KCHECK();
+  }
   // the fused one-read step of one iteration (speculative; a no-op unless *mode == 1)
   auto fused_step = [&]() -> gw_status {
     // Every iteration first tries the fused one-read path when *mode == 1 (speculatively at the
@@ -1460,7 +1469,7 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
       KCHECK();
       k_sink_fin_fast<<<grid_for(std::max(m, nl), 256, 1 << 30), 256, 0, c->stream>>>(
           s.Srow, nl, P.lp + P.row0, s.f, s.fh, s.fl, nullptr, s.csg, P.R, stride, m, P.lq, eps, s.g, s.gh, s.gl,
-          s.mode, s.stop, s.dev, s.flag);
+          s.mode, s.stop, s.dev, s.flag, kappa);
       KCHECK();
       PROF_END(c, PC_SINK_FUSED, 2);
     }
@@ -1476,7 +1485,7 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
     PROF_BEGIN(c, PC_SINK_ROW);
     k_sink_row<<<rgrid, 256, 0, c->stream>>>(
         G, ldG, nl, m, s.gh, s.gl, c2f, s.f, fout, P.lp + P.row0, eps, s.fh, s.fl, check ? s.viol : nullptr, s.stop,
-        skip);
+        skip, kappa);
     KCHECK();
     PROF_END(c, PC_SINK_ROW, 1);
     if (check) {
@@ -1489,14 +1498,14 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
     KCHECK();
     if (P.R == 1) {
       k_sink_colmergefin<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.part, s.nrb, m, P.lq, eps, s.g, s.gh,
-                                                                            s.gl, s.stop, skip, s.dev);
+                                                                            s.gl, s.stop, skip, s.dev, kappa);
       KCHECK();
     } else {
       k_sink_colmerge<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.part, s.nrb, m, s.lse, s.stop, skip);
       KCHECK();
       TRY(comm_allgather(c, s.lse, s.lseg, 2 * sizeof(double) * (size_t)m));
       k_sink_colfin<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.lseg, P.R, m, P.lq, eps, s.g, s.gh, s.gl,
-                                                                       s.stop, skip, s.dev);
+                                                                       s.stop, skip, s.dev, kappa);
       KCHECK();
     }
     PROF_END(c, PC_SINK_COL, 2);
@@ -1532,7 +1541,7 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
       // the safe path's local half (skipped unless *mode == 0): row update, then column LSE pairs
       PROF_BEGIN(c, PC_SINK_ROW);
       k_sink_row<<<rgrid, 256, 0, c->stream>>>(G, ldG, nl, m, s.gh, s.gl, c2f, s.f, s.f, P.lp + P.row0, eps, s.fh,
-                                                s.fl, nullptr, s.stop, s.mode);
+                                                s.fl, nullptr, s.stop, s.mode, kappa);
       KCHECK();
       PROF_END(c, PC_SINK_ROW, 1);
       PROF_BEGIN(c, PC_SINK_COL);
@@ -1544,7 +1553,7 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
       TRY(comm_allgather(c, s.un, s.ung, sizeof(double) * (size_t)U));
       // safe path: g from the gathered LSE pairs (before the fused finish, which may switch *mode)
       k_sink_colfin<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.ung, P.R, m, P.lq, eps, s.g, s.gh, s.gl,
-                                                                       s.stop, s.mode, s.dev, 1.0, U, true);
+                                                                       s.stop, s.mode, s.dev, kappa, U, true);
       KCHECK();
       // fused path: validity of the speculative iteration (all ranks' row flags, the gathered column
       // sums), then commit -- or not, and switch to the safe path
@@ -1553,7 +1562,7 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
       KCHECK();
       k_sink_fin_fast<<<grid_for(std::max(m, nl), 256, 1 << 30), 256, 0, c->stream>>>(
           s.Srow, nl, P.lp + P.row0, s.f, s.fh, s.fl, nullptr, s.ung, P.R, U, m, P.lq, eps, s.g, s.gh, s.gl,
-          s.mode, s.stop, s.dev, s.flag);
+          s.mode, s.stop, s.dev, s.flag, kappa);
       KCHECK();
       k_sink_slot_end<<<1, 32, 0, c->stream>>>(s.mode, s.dev, s.flag, s.stop, 20.f);
       KCHECK();
@@ -1561,7 +1570,10 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
     };
     static const bool no_graph_mr = getenv("GWDP_NO_GRAPH") != nullptr;
     const bool graph = !no_graph_mr && !c->prof.on && c->comm && c->comm->nccl;  // host transport: not capturable
+    if (graph && s.gexec && (s.g_eps != eps || s.g_kappa != kappa)) sink_free(s);
     if (graph && !s.gexec) {
+      s.g_eps = eps;
+      s.g_kappa = kappa;
       if (!c->cap) CU(cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking));
       CU(cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal));
       cudaStream_t saved = c->stream;
@@ -1607,7 +1619,8 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
     const int CL = small_cluster(c, P, &rows, &bytes);
     if (CL > 0) {
       // even smem row pitch: the fp64 arrays after the fp32 tile stay 8-byte aligned
-      SmallArgs sa{G, ldG, nl, m, rows, (int)((m + 1) & ~int64_t(1)), P.lp + P.row0, P.lq, eps, 1.0, iters, s.f, s.g};
+      SmallArgs sa{G, ldG, nl, m, rows, (int)((m + 1) & ~int64_t(1)), P.lp + P.row0, P.lq, eps, kappa, iters, s.f,
+                   s.g};
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(CL);
       cfg.blockDim = dim3(SNT);
@@ -1632,7 +1645,10 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
   // disables it; not while per-kernel profiling is on, whose events time the launches).
   static const bool no_graph = getenv("GWDP_NO_GRAPH") != nullptr;
   if (!tolmode && !no_graph && !c->prof.on && P.R == 1 && iters >= 3) {
+    if (s.gexec && (s.g_eps != eps || s.g_kappa != kappa)) sink_free(s);
     if (!s.gexec) {
+      s.g_eps = eps;
+      s.g_kappa = kappa;
       if (!c->cap) CU(cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking));
       CU(cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal));
       cudaStream_t saved = c->stream;
@@ -1682,7 +1698,7 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
     // final check of the plan after `done` iterations (row half-step into ftmp, not committed)
     CU(cudaMemsetAsync(s.viol, 0, sizeof(float), c->stream));
     k_sink_row<<<rgrid, 256, 0, c->stream>>>(
-        G, ldG, nl, m, s.gh, s.gl, c2f, s.f, s.ftmp, P.lp + P.row0, eps, s.fh, s.fl, s.viol, nullptr, nullptr);
+        G, ldG, nl, m, s.gh, s.gl, c2f, s.f, s.ftmp, P.lp + P.row0, eps, s.fh, s.fl, s.viol, nullptr, nullptr, kappa);
     KCHECK();
     TRY(sink_viol_global(c, P, s));
     float hv;
@@ -2170,8 +2186,6 @@ static gw_status ugw_impl(gw_ctx* c, const gw_problem* pb, double rho, const gw_
   cudaEvent_t ev0, ev1;
   CU(evset.make(&ev0)); CU(evset.make(&ev1));
   CU(cudaEventRecord(ev0, c->stream));
-  const unsigned cgrid = (unsigned)std::min<int64_t>(((m + 1023) / 1024) * s.nrb, 148 * 4);
-  const unsigned rgrid = (unsigned)std::min<int64_t>((nl + RROWS - 1) / RROWS, 148 * 4);
   // T^0 = u v / m0, m0 = sqrt(m(u) m(v)) (R35): a = u sqrt(mv/mu), b = v sqrt(mu/mv), m(T^0) = m0
   UgwStats st{m0, 0.5 * m0 * std::log(mv / mu), 0.5 * m0 * std::log(mu / mv), -0.5 * m0 * std::log(mu * mv)};
   // the product form of T^0 for the gradient kernels: rows u / m0 (local, fp64 in Fs and fp32 in s.fh,
@@ -2246,40 +2260,12 @@ static gw_status ugw_impl(gw_ctx* c, const gw_problem* pb, double rho, const gw_
     k_ugw_axpy<<<grid_for(m), 256, 0, c->stream>>>(gr, P.lq, eps_t, m, s.g);
     KCHECK();
     TRY(sink_split(c, P, s, eps_t));
-    int srows = 0;
-    size_t sbytes = 0;
-    const int sCL = (P.R == 1 && o->inner.max_iter > 0 && getenv("GWDP_NO_SMALL") == nullptr)
-                        ? small_cluster(c, P, &srows, &sbytes) : 0;
-    if (sCL > 0) {  // the whole inner loop in one cluster-resident launch (small.cuh), kappa included
-      SmallArgs sa{G, ldG, nl, m, srows, (int)((m + 1) & ~int64_t(1)), P.lp + P.row0, P.lq, eps_t, kap,
-                   o->inner.max_iter, s.f, s.g};
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(sCL);
-      cfg.blockDim = dim3(SNT);
-      cfg.dynamicSmemBytes = sbytes;
-      cfg.stream = c->stream;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = sCL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
-      cfg.attrs = at;
-      cfg.numAttrs = 1;
-      CU(cudaLaunchKernelEx(&cfg, k_sink_small, sa));
-      KCHECK();
-      TRY(sink_split(c, P, s, eps_t));
-    }
-    for (int it = 0; it < (sCL > 0 ? 0 : o->inner.max_iter); ++it) {
-      k_sink_row<<<rgrid, 256, 0, c->stream>>>(G, ldG, nl, m, s.gh, s.gl, c2f, s.f, s.f, P.lp + P.row0, eps_t,
-                                                s.fh, s.fl, nullptr, nullptr, nullptr, kap);
-      KCHECK();
-      k_sink_col<<<cgrid, 256, 0, c->stream>>>(G, ldG, nl, m, s.fh, s.fl, c2f, s.RB, s.part, nullptr, nullptr);
-      KCHECK();
-      k_sink_colmerge<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.part, s.nrb, m, s.lse, nullptr, nullptr);
-      KCHECK();
-      TRY(comm_allgather(c, s.lse, s.lseg, 2 * sizeof(double) * (size_t)m));
-      k_sink_colfin<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.lseg, P.R, m, P.lq, eps_t, s.g, s.gh, s.gl,
-                                                                       nullptr, nullptr, nullptr, kap);
-      KCHECK();
-    }
+    // the unbalanced subproblem on the hot path's Sinkhorn machinery: the one-read fused iteration
+    // (speculative, validated on the device, falling back to the safe two-kernel path), the
+    // cluster-resident loop for small problems, CUDA graphs / one collective per slot -- kappa
+    // carried through every update (R34)
+    int used = 0, conv = 0;
+    TRY(sink_run(c, P, s, G, ldG, eps_t, o->inner.max_iter, 0.0, 10, &used, &conv, l == 0, kap));
     inner_total += o->inner.max_iter;
     // relative duals for the warm start (R34), then the mass rescaling (R35)
     k_ugw_axpy<<<grid_for(nl), 256, 0, c->stream>>>(s.f, P.lp + P.row0, -eps_t, nl, fr);
@@ -2332,8 +2318,10 @@ static gw_status ugw_impl(gw_ctx* c, const gw_problem* pb, double rho, const gw_
   // the returned duals are the subproblem's final ones in R34's convention (relative to u v)
   CU(cudaMemcpyAsync(s.f, fr, nl * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   CU(cudaMemcpyAsync(s.g, gr, m * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  if (o->outer_iters > 0) CU(cudaMemcpyAsync(c->hpin + 32, s.mode, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CU(cudaEventRecord(ev1, c->stream));
   CU(cudaStreamSynchronize(c->stream));
+  const int ugw_fused = o->outer_iters > 0 ? reinterpret_cast<int*>(c->hpin + 32)[1] : 0;
   float ms_total = 0.f;
   CU(cudaEventElapsedTime(&ms_total, ev0, ev1));
   res->gw_objective = E;
@@ -2342,7 +2330,7 @@ static gw_status ugw_impl(gw_ctx* c, const gw_problem* pb, double rho, const gw_
   res->outer_iters = o->outer_iters;
   res->inner_iters_total = inner_total;
   res->converged = 0;
-  res->inner_fused_total = 0;
+  res->inner_fused_total = o->outer_iters > 0 ? ugw_fused : 0;
   res->ms_grad = 0.0;
   res->ms_sinkhorn = 0.0;
   res->ms_total = ms_total;
