@@ -69,7 +69,7 @@ def sinkhorn(G, p, q, eps, iters, f0=None, g0=None, tol=None, check_every=10):
 
 
 def entropic_gw(x, y, p, q, eps, outer, inner, k=1, T0=None, tol=None,
-                check_every=10, record_grads=False, grad_mode="dense", tau=None):
+                check_every=10, record_grads=False, grad_mode="dense", tau=None, cost_dtype=None):
     """Entropic GW by mirror descent with tau = eps.
 
     PAPER.md:102-114 (eqs. "GW proximal gradient", "GW sinkhorn") and Remark 1
@@ -85,6 +85,11 @@ def entropic_gw(x, y, p, q, eps, outer, inner, k=1, T0=None, tol=None,
     grad H(T) = ln T, i.e. entropic OT of the cost Pi = G + (eps - tau) ln T^l at
     regulariser tau; ln T^l is the log-domain plan (f + g - Pi_prev)/tau (ln p + ln q for
     T^0 = p (x) q), never log of an underflowed entry.
+
+    ``cost_dtype`` (diagnostic only, default None = float64 throughout): round the cost of every
+    subproblem to this storage type (e.g. np.float32, the matrix storage BASELINE.json's configs
+    prescribe) before the Sinkhorn iterations -- a model of a solver that STORES G in fp32; the
+    arithmetic stays float64.  Not the parity contract (the oracle is float64).
 
     Returns a dict: T, f, g, E (list, E(T^l) for l = 1..L), viol (list),
     inner_used (list), gw_objective, entropic_objective, and G (list) when
@@ -109,6 +114,8 @@ def entropic_gw(x, y, p, q, eps, outer, inner, k=1, T0=None, tol=None,
             G = grad_prescribed(x, y, p, q, T, k)
         if tau != eps:
             G = G + (eps - tau) * lnT  # the cost Pi of PAPER.md:110
+        if cost_dtype is not None:
+            G = G.astype(cost_dtype).astype(np.float64)
         f, g, used = sinkhorn(G, p, q, tau, counts[l], f, g, tol=tol, check_every=check_every)
         T = plan_from_duals(G, f, g, tau)
         if tau != eps:

@@ -1248,7 +1248,7 @@ static gw_status fused_launch_t(gw_ctx* c, const FusedArgs& fa, int ncl) {
 }
 
 // (K, CL, NT) dispatch: W = 4 K NT columns per CTA (W <= 8192); one cluster of CL CTAs spans a row.
-//   NT = 256: K in {1, 2, 4, 8} with CL = 1, K = 8 with CL in {2, 4, 8}
+//   NT = 256: K in {1, 2, 4, 8} with CL = 1, K = 8 with CL in {2, 4, 8}, K = 6 with CL in {4, 8}
 //   NT = 512: K in {1, 2, 4} with CL = 1, K = 4 with CL in {2, 4, 8}
 #define FUSED_DISPATCH(FN, ...)                                                   \
   switch ((NT / 256) * 256 + K * 16 + CL) {                                       \
@@ -1259,6 +1259,8 @@ static gw_status fused_launch_t(gw_ctx* c, const FusedArgs& fa, int ncl) {
     case 256 + 8 * 16 + 2: return FN<8, 2, 256>(__VA_ARGS__);                     \
     case 256 + 8 * 16 + 4: return FN<8, 4, 256>(__VA_ARGS__);                     \
     case 256 + 8 * 16 + 8: return FN<8, 8, 256>(__VA_ARGS__);                     \
+    case 256 + 6 * 16 + 4: return FN<6, 4, 256>(__VA_ARGS__);                     \
+    case 256 + 6 * 16 + 8: return FN<6, 8, 256>(__VA_ARGS__);                     \
     case 512 + 1 * 16 + 1: return FN<1, 1, 512>(__VA_ARGS__);                     \
     case 512 + 2 * 16 + 1: return FN<2, 1, 512>(__VA_ARGS__);                     \
     case 512 + 4 * 16 + 1: return FN<4, 1, 512>(__VA_ARGS__);                     \
@@ -1326,6 +1328,9 @@ static gw_status sink_alloc(gw_ctx* c, const Prepared& P, SinkState& s) {
     }
     if (CL == 3) CL = 4;
     if (CL > 4 && CL < 8) CL = 8;
+    // clusters rounded up to 4 or 8 CTAs: narrower CTAs (K = 6, 6144 columns) when they still cover the
+    // row, instead of idle CTAs (e.g. M = 24576: 4 x 6144 rather than 3 x 8192 + an empty fourth)
+    if (NT == 256 && CL >= 4 && (int64_t)CL * 6 * 1024 >= P.m) K = 6;
     const int64_t wcol = 4 * (int64_t)K * NT;
     if (CL <= 8) {  // clusters must fit in a GPC: on B200 clusters of 8 leave 28 SMs idle
       int ncl = 0;
