@@ -56,6 +56,12 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// MUFU reciprocal (<= 1 ulp; reading R19b): the fused iteration's per-row factor w = p / S
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float lg2_ftz(float x) {
   float y;
   asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -96,6 +102,10 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+// L2 prefetch of a 16-byte aligned range (bytes % 16 == 0): no registers, no completion to wait for
+__device__ __forceinline__ void prefetch_l2_bulk(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -213,7 +223,8 @@ __device__ __forceinline__ void st_async_v2f32(uint32_t raddr, float v0, float v
 // scaled duals only (reading R30): the fma carries the one rounding of the large terms and
 // "+ F" cancels exactly; the dropped lo parts are per-row / per-column scalings that the
 // iteration's normalisations absorb.
-template <int K, int CL, int NT>
+// UGW: the unbalanced row factor (a separate instantiation: the balanced kernel carries no trace of it)
+template <int K, int CL, int NT, bool UGW>
 __global__ void __launch_bounds__(NT, 1) k_sink_fused2(FusedArgs a) {
   if (*a.mode != 1 || (a.stop && *a.stop)) return;  // uniform across the cluster
   constexpr int NW = NT / 32;
@@ -293,7 +304,7 @@ __global__ void __launch_bounds__(NT, 1) k_sink_fused2(FusedArgs a) {
       acc64[(k * 4 + 2 * h + 1) * NT + t] = 0.0;
     }
   const float2 nc2 = make_float2(-a.c2f, -a.c2f);
-  const bool ugw = a.kappa != 1.f;
+  constexpr bool ugw = UGW;
   const float km1 = a.kappa - 1.f;
   float2 eA0[K][2], eA1[K][2], eB0[K][2], eB1[K][2];
   float2 pA = make_float2(0.f, 0.f), pB = pA;  // marginals of the pair's two rows
@@ -430,12 +441,14 @@ __global__ void __launch_bounds__(NT, 1) k_sink_fused2(FusedArgs a) {
         if (jp1 < nrows) Srow[jp1] = S1;
         if (Pp + NSLOT < npairs) mbar_expect_tx(&xbar[psl], xbytes);
       }
-      // half-step row factor: balanced w = p / S (IEEE division); unbalanced (R34, absorbed duals)
+      // half-step row factor: balanced w = p (1/S) with the MUFU reciprocal (<= 1 ulp, reading R19b: the
+      // IEEE __frcp_rn sequence on this latency-critical step cost 8% of the kernel); unbalanced (R34,
+      // absorbed duals)
       // w = 2^(log2 u + (kappa - 1) F - kappa log2 S), i.e. f'_new = eps~ ln u - kappa eps~ (ln S - F ln 2)
       float w0, w1 = 0.f;
       if (!ugw) {
-        w0 = __fdiv_rn(pprv.x, S0);
-        if (jp1 < nrows) w1 = __fdiv_rn(pprv.y, S1);
+        w0 = pprv.x * rcp_approx(S0);
+        if (jp1 < nrows) w1 = pprv.y * rcp_approx(S1);
       } else {
         w0 = ex2_ftz(fmaf(-a.kappa, lg2_ftz(S0), pprv.x));
         if (jp1 < nrows) w1 = ex2_ftz(fmaf(-a.kappa, lg2_ftz(S1), pprv.y));

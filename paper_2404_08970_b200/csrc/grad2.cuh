@@ -530,7 +530,6 @@ __device__ __forceinline__ void moments3_body(const TSrc2& S, int64_t nl, int64_
   const int nrows = (int)min((int64_t)TR, nl - r0);
   for (int rr = 0; rr < TR; rr += 32) {  // 4 rows per warp per group (8 warps x 4 = 32 rows)
     if (rr >= nrows) break;              // uniform
-    float v[8];
     float2 tv[4][4];                     // [row u][float2 k]
     float F[4], Fl[4], dxr[4];
 #pragma unroll

@@ -106,7 +106,7 @@ struct gw_ctx {
   Buf rP, rA, cS, cX, blk, bs, btot, cxend, SAg, WAg, Ptot, Aend, DP, DA, tobj, tent, tcc, objout, scanwt;
   Buf fxs, fys;  // FGW features (staged)
   Buf pnf, qnf;  // fp32 marginals
-  Buf yfb, pcoef, pc2s, pfx, pfy, ppart, pM;  // k = 2 path
+  Buf yfb, pcoef, pc2s, pfx, pfy, ppart, pM, p4coef, p4c2;  // k = 2 and k = 4 (moments) paths
   Buf gkrp, gkrt, gkcp, gkz, gkct, gkctt, gkobj;  // k >= 3 path
   Buf uga, ugb, ugct, ugpart, ugca, ugcb, ugfr, uggr, ugsc;  // UGW
   Buf g2rc, g2rd, g2h, g2cc, g2tt, g2vt, g2tmp, g2s, g2a, g2b, g2ca, g2cb, g2part;  // 2-D grids
@@ -127,7 +127,7 @@ struct gw_ctx {
                 &ftmp, &viol, &stop, &iters, &part, &fpart, &mode, &srow, &pfl, &rP, &rA, &cS, &cX, &blk, &bs, &btot, &cxend,
                 &SAg, &WAg, &Ptot, &Aend, &DP, &DA, &tobj, &tent, &tcc, &objout, &scanwt, &fxs, &fys, &fsc, &gsc, &Gs,
                 &pnf, &qnf, &xtab, &xg1, &xg2, &xin, &xvec, &xtail, &xpart, &slse, &slseg, &scsl, &scsg, &sun, &sung,
-                &sviolg, &sflag, &sflagg, &yfb, &pcoef, &pc2s, &pfx, &pfy, &ppart, &pM,
+                &sviolg, &sflag, &sflagg, &yfb, &pcoef, &pc2s, &pfx, &pfy, &ppart, &pM, &p4coef, &p4c2,
                 &gkrp, &gkrt, &gkcp, &gkz, &gkct, &gkctt, &gkobj,
                 &uga, &ugb, &ugct, &ugpart, &ugca, &ugcb, &ugfr, &uggr, &ugsc,
                 &g2rc, &g2rd, &g2h, &g2cc, &g2tt, &g2vt, &g2tmp, &g2s, &g2a, &g2b, &g2ca, &g2cb, &g2part};
@@ -1081,6 +1081,41 @@ static gw_status grad_pass_gk(gw_ctx* c, const Prepared& P, int mode, const TSrc
   return grad_pass_gk_mode<K, T_PRODUCT>(c, P, S2, G, ldG, store, obj, fx, fy, alpha, objout_dev);
 }
 
+// k = 4 gradient (store only): the k = 2 moments pass (M_rt, r, t <= 4) + a degree-4 polynomial per row
+// evaluated in fp64 (poly.cuh) -- 4NM read + 4NM write, no scans (the objective stays on polyk.cuh)
+static gw_status grad_store_poly4(gw_ctx* c, const Prepared& P, int mode, const TSrc2& S2, float* G, int64_t ldG,
+                                  const double* fx, const double* fy, double alpha) {
+  const int64_t nl = P.nl, m = P.m;
+  if (nl == 0) return GW_OK;
+  double* M;
+  PROF_BEGIN(c, PC_GRAD_MOMENTS);
+  TRY(poly_moments(c, P, mode, S2, false, &M));
+  PROF_END(c, PC_GRAD_MOMENTS, 1);
+  PROF_BEGIN(c, PC_GRAD_MAIN);
+  double *coef, *c2d;
+  float *fxs = nullptr, *fys = nullptr;
+  TRY(ws(c, c->p4coef, 5 * (size_t)std::max<int64_t>(nl, 1), &coef));
+  TRY(ws(c, c->p4c2, (size_t)m, &c2d));
+  k_poly4_rowcoef<<<grid_for(nl), 256, 0, c->stream>>>(M, P.xc + P.row0, P.cx + P.row0, nl, alpha, coef);
+  KCHECK();
+  k_scale<<<grid_for(m), 256, 0, c->stream>>>(P.cy, m, 2.0 * alpha, c2d);
+  KCHECK();
+  const dim3 grid((unsigned)((m + 1023) / 1024), (unsigned)((nl + PSR - 1) / PSR));
+  if (fx) {
+    TRY(ws(c, c->pfx, std::max<int64_t>(nl, 1), &fxs));
+    TRY(ws(c, c->pfy, m, &fys));
+    k_scale_f<<<grid_for(nl), 256, 0, c->stream>>>(fx + P.row0, nl, sqrt(1.0 - alpha), fxs);
+    k_scale_f<<<grid_for(m), 256, 0, c->stream>>>(fy, m, sqrt(1.0 - alpha), fys);
+    KCHECK();
+    k_poly4_store<true><<<grid, 256, 0, c->stream>>>(coef, c2d, P.yc, fxs, fys, nl, m, G, ldG);
+  } else {
+    k_poly4_store<false><<<grid, 256, 0, c->stream>>>(coef, c2d, P.yc, nullptr, nullptr, nl, m, G, ldG);
+  }
+  KCHECK();
+  PROF_END(c, PC_GRAD_MAIN, 1);
+  return GW_OK;
+}
+
 static gw_status grad_pass(gw_ctx* c, const Prepared& P, int mode, const TSrc& S, const TSrc2& S2, float* G,
                            int64_t ldG, bool store, bool obj, const double* fx, const double* fy, double alpha,
                            double* objout_dev, double beta = 0.0) {
@@ -1090,6 +1125,7 @@ static gw_status grad_pass(gw_ctx* c, const Prepared& P, int mode, const TSrc& S
   if (beta != 0.0) return grad_pass_k1(c, P, mode, S, S2, G, ldG, store, obj, fx, fy, alpha, objout_dev, beta);
   if (P.grid2d) return grad_pass_2d(c, P, mode, S2, G, ldG, store, obj, fx, fy, alpha, objout_dev);
   if (P.k == 1) return grad_pass_k1(c, P, mode, S, S2, G, ldG, store, obj, fx, fy, alpha, objout_dev);
+  if (P.k == 4 && store && !obj) return grad_store_poly4(c, P, mode, S2, G, ldG, fx, fy, alpha);
   if (P.k >= 3) {
     if (P.nl == 0) return GW_OK;
     if (obj)  // violation, entropy and <C o C, T> from the k = 1 objective machinery; E(T) below
@@ -1215,9 +1251,10 @@ struct SinkGuard {  // releases the captured graph on every exit path of a solve
 
 template <int K, int CL, int NT>
 static gw_status fused_config_t(gw_ctx* c, int* ncl) {
-  auto kern = k_sink_fused2<K, CL, NT>;
+  auto kern = k_sink_fused2<K, CL, NT, false>;
   const size_t dsm = fused_dyn_smem<K, NT>();
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+  CU(cudaFuncSetAttribute(k_sink_fused2<K, CL, NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(148 * CL);
   cfg.blockDim = dim3(NT);
@@ -1243,7 +1280,8 @@ static gw_status fused_launch_t(gw_ctx* c, const FusedArgs& fa, int ncl) {
   at[0].val.clusterDim.x = CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  CU(cudaLaunchKernelEx(&cfg, k_sink_fused2<K, CL, NT>, fa));
+  if (fa.kappa != 1.f) CU(cudaLaunchKernelEx(&cfg, k_sink_fused2<K, CL, NT, true>, fa));
+  else CU(cudaLaunchKernelEx(&cfg, k_sink_fused2<K, CL, NT, false>, fa));
   return GW_OK;
 }
 

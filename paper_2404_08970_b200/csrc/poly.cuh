@@ -197,6 +197,83 @@ __global__ void __launch_bounds__(256) k_poly_store(const float4* __restrict__ c
   }
 }
 
+// ---- k = 4 (even power: the distance is again a polynomial, PAPER.md:65-80 at k = 4) ----
+// (x_i - x_j)^4 = sum_r a_r(x_i) x_j^r, a_r(x) = C(4,r) (-1)^r x^{4-r} (same for y), so with the SAME
+// moments M_rt (r, t <= 4) as k = 2: D_X T D_Y = sum_{r,t} a_r(x_i) M_rt a_t(y_p), i.e. per row the
+// degree-4 polynomial in y_p
+//   G_ip = 2 c_i + 2 c'_p + sum_d B_d(i) y_p^d,   B_d = -4 C(4,d) (-1)^d u_{4-d}(i),  u_t = sum_r a_r M_rt.
+// The expansion cancels by up to ~200x on centred supports (terms ~4 W^8 against values ~W^8/50), so
+// the per-element evaluation is fp64 Horner (4 DFMA per element); coefficients in fp64.
+__global__ void k_poly4_rowcoef(const double* __restrict__ M, const double* __restrict__ xl,
+                                const double* __restrict__ cl, int64_t nl, double alpha, double* __restrict__ coef) {
+  const double C4[5] = {1, 4, 6, 4, 1};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nl; i += (int64_t)gridDim.x * blockDim.x) {
+    const double x = xl[i];
+    double a[5];
+    double xp = 1.0;  // x^{4-r} for r = 4 .. 0
+    for (int r = 4; r >= 0; --r) {
+      a[r] = C4[r] * ((r & 1) ? -1.0 : 1.0) * xp;
+      xp *= x;
+    }
+    double u[5];
+#pragma unroll
+    for (int t = 0; t < 5; ++t) {
+      double v = 0.0;
+#pragma unroll
+      for (int r = 0; r < 5; ++r) v += a[r] * M[r * PM + t];
+      u[t] = v;
+    }
+    double* co = coef + 5 * i;
+#pragma unroll
+    for (int d = 0; d < 5; ++d) co[d] = alpha * (-4.0 * C4[d] * ((d & 1) ? -1.0 : 1.0) * u[4 - d]);
+    co[0] += alpha * 2.0 * cl[i];
+  }
+}
+
+// G_ip = B_0(i) + 2 alpha c'_p + y_p (B_1 + y_p (B_2 + y_p (B_3 + y_p B_4))) [+ (1 - alpha)(fx_i - fy_p)^2],
+// fp64 Horner, one fp32 rounding; layout as k_poly_store (1024 columns x PSR rows per CTA).
+template <bool FGW>
+__global__ void __launch_bounds__(256) k_poly4_store(const double* __restrict__ coef, const double* __restrict__ c2d,
+                                                     const double* __restrict__ yd, const float* __restrict__ fxs,
+                                                     const float* __restrict__ fys, int64_t nl, int64_t m,
+                                                     float* __restrict__ G, int64_t ldG) {
+  const int64_t q = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+  if (q >= m) return;
+  double y[4], c2[4];
+  float fy[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int64_t qq = min(q + k, m - 1);
+    y[k] = yd[qq];
+    c2[k] = c2d[qq];
+    fy[k] = FGW ? fys[qq] : 0.f;
+  }
+  const int64_t i0 = (int64_t)blockIdx.y * PSR, i1 = min(nl, i0 + PSR);
+  for (int64_t i = i0; i < i1; ++i) {
+    const double* co = coef + 5 * i;
+    const double b0 = co[0], b1 = co[1], b2 = co[2], b3 = co[3], b4 = co[4];
+    const float fxi = FGW ? fxs[i] : 0.f;
+    float o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double yy = y[k];
+      const double v = fma(yy, fma(yy, fma(yy, fma(yy, b4, b3), b2), b1), b0 + c2[k]);
+      float fv = (float)v;
+      if (FGW) {
+        const float d = fxi - fy[k];
+        fv = fmaf(d, d, fv);
+      }
+      o[k] = fv;
+    }
+    float* dst = G + i * ldG + q;
+    if (q + 3 < m) {
+      __stcs(reinterpret_cast<float4*>(dst), make_float4(o[0], o[1], o[2], o[3]));
+    } else {
+      for (int k = 0; k < 4 && q + k < m; ++k) dst[k] = o[k];
+    }
+  }
+}
+
 // Objective at k = 2 from the global moments (k_obj_final supplies the violation and H):
 //   a^T (D_X o D_X) a = sum_r C(4,r) (-1)^r M_r0 M_{4-r,0},   b^T (D_Y o D_Y) b likewise with M_0t,
 //   <D_X T D_Y, T> = sum_{r,t<=2} M_rt atil_r atil_t M_{2-r,2-t}.   out[0] = E.

@@ -82,7 +82,8 @@ def main():
     for k, nbytes, note in [(1, 12, "moments read + main read + write (gap-weighted scans)"),
                             (2, 8, "moments read + write (polynomial moments)"),
                             (3, 12, "sums read + main read + write (power-sum scans)"),
-                            (4, 12, "as k = 3"), (5, 12, "as k = 3")]:
+                            (4, 8, "moments read + write (polynomial moments, fp64 per-row polynomial)"),
+                            (5, 12, "as k = 3")]:
         with torch.cuda.stream(stream):
             ms = timed(lambda: api.grad(x, x, p, p, T, out=G, ctx=ctx, k=k), args.reps, stream)
         d = {"variant": "gw_grad_dp k=%d" % k, "row": "a1-a4" if k == 1 else "f2", "N": n, "M": n,

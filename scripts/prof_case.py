@@ -1,0 +1,59 @@
+#!/usr/bin/env python
+"""Small driver for ncu captures of one kernel family (one case per run, sizes chosen so that ncu's
+replays stay short; HBM-bound behaviour is the same as at C4):
+
+  gibbs   entropic_gw_solve, N = M = 16384, 2 outer x 5 inner: the second gradient runs the solver's
+          Gibbs-mode kernels (k_grad_moments3<1>, k_grad_store2<1,...>)
+  k3      gw_grad_dp, k = 3, explicit plan, N = M = 16384 (k_gk_sums / k_gk_main)
+  k4      as k3 with k = 4
+  grid2d  gw_grad_dp GW_GRID2D, 128 x 128 grids (N = M = 16384) (k_g2_rowred / k_g2_store)
+
+    python scripts/prof_case.py gibbs
+"""
+
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    case = sys.argv[1]
+    import numpy as np
+    import torch
+    import workloads as W
+    from paper_2404_08970_b200 import api
+    dev = torch.device("cuda", 0)
+    n = 16384
+    rng = np.random.default_rng(0)
+    if case == "gibbs":
+        P = W.config4(n)
+        api.solve(P.x, P.y, P.p, P.q, P.eps, 2, 5, device=dev)
+    elif case in ("k3", "k4"):
+        k = int(case[1])
+        x = np.sort(rng.random(n))
+        p = np.full(n, 1.0 / n)
+        T = api.plan_buffer(n, n, dev)
+        T.copy_(torch.rand((n, n), device=dev) / (n * n))
+        G = torch.empty_like(T)
+        for _ in range(2):
+            api.grad(x, x, p, p, T, out=G, k=k)
+    elif case == "grid2d":
+        side = 128
+        s = np.arange(side) / (side - 1.0)
+        w = rng.random(side * side) + 0.05
+        w /= w.sum()
+        T = api.plan_buffer(side * side, side * side, dev)
+        T.copy_(torch.rand((side * side, side * side), device=dev) / (side ** 4))
+        G = torch.empty_like(T)
+        for _ in range(2):
+            api.grad(s, s, w, w, T, out=G, grid2d=True)
+    else:
+        raise SystemExit("unknown case %s" % case)
+    torch.cuda.synchronize()
+    print("ok", case)
+
+
+if __name__ == "__main__":
+    main()

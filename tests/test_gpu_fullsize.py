@@ -123,7 +123,8 @@ def test_fullsize_sinkhorn_step_and_marginals(full):
     # per-entry plan deviation of one step, in units of eps (reading R30 bounds it by ~1e-4)
     df = np.max(np.abs(f1 - fo)) / eps
     dg = np.max(np.abs(g1 - go)) / eps
-    assert df <= 5e-4 and dg <= 5e-4, (df, dg)
+    print("fullsize fused step: dual deviation / eps: f %.3e, g %.3e" % (df, dg))
+    assert df <= 5e-5 and dg <= 5e-5, (df, dg)  # ~3x the measured 1.7e-5 / 3.0e-6 (round 2)
     # after the g-update the plan's column sums are q (up to the fp32 cost): sampled columns
     rng = np.random.default_rng(5)
     J = rng.choice(N, 16, replace=False)

@@ -15,6 +15,10 @@ pytestmark = pytest.mark.gpu
 GRAD_TOL = 1e-5
 OBJ_TOL = 1e-4
 VIOL_TOL = 1e-6
+# Sinkhorn (60 iterations on an fp32 cost, fp32 exponents): plan error / max T and dual error / eps,
+# ~3x the largest values measured on a B200 (round 2: plan 1.0e-6 at 64 x 65536, duals 9.7e-7)
+PLAN_TOL = 3e-6
+DUAL_TOL = 3e-6
 
 
 @pytest.fixture(scope="module")
@@ -146,8 +150,10 @@ def test_sinkhorn_parity(gw, n, m, eps):
     f, g, _ = O.sinkhorn(G.astype(np.float64), p, q, eps, 50)
     To = O.plan_from_duals(G.astype(np.float64), f, g, eps)
     T = r["T"].cpu().numpy().astype(np.float64)
-    assert np.max(np.abs(T - To)) <= 1e-4 * np.max(To)
-    assert np.max(np.abs(r["g"].cpu().numpy() - g)) <= 1e-5 * eps * 10
+    eT = np.max(np.abs(T - To)) / np.max(To)
+    eg = np.max(np.abs(r["g"].cpu().numpy() - g)) / eps
+    print("sinkhorn_parity n=%d m=%d eps=%g: plan err/max T %.3e, dual err/eps %.3e" % (n, m, eps, eT, eg))
+    assert eT <= PLAN_TOL and eg <= DUAL_TOL
 
 
 def test_sinkhorn_tolerance_rule(gw):
@@ -252,7 +258,7 @@ def test_ugw_argument_errors(gw):
 # ----------------------------------------------------------------------------- fused path
 
 @pytest.mark.parametrize("n,m,eps", [(300, 20000, 0.02), (64, 65536, 0.01), (500, 3000, 0.02), (257, 8193, 0.02),
-                                     (1000, 8192, 0.01), (3, 70, 0.05)])
+                                     (1000, 8192, 0.01), (3, 70, 0.05), (200, 24576, 0.02), (150, 40001, 0.02)])
 def test_sinkhorn_fused_path_parity(gw, monkeypatch, n, m, eps):
     """The fused one-read iteration (clusters of 1-8 CTAs spanning a row, ragged last CTA,
     CTAs entirely past m) against the oracle; and it must actually have run (the cluster-resident
@@ -266,7 +272,9 @@ def test_sinkhorn_fused_path_parity(gw, monkeypatch, n, m, eps):
     f, g, _ = O.sinkhorn(G.astype(np.float64), p, q, eps, 60)
     To = O.plan_from_duals(G.astype(np.float64), f, g, eps)
     T = r["T"].cpu().numpy().astype(np.float64)
-    assert np.max(np.abs(T - To)) <= 1e-4 * np.max(To)
+    eT = np.max(np.abs(T - To)) / np.max(To)
+    print("fused_path_parity n=%d m=%d eps=%g: plan err/max T %.3e" % (n, m, eps, eT))
+    assert eT <= PLAN_TOL
 
 
 def test_fused_matches_safe_path(gw, monkeypatch):
@@ -420,6 +428,22 @@ def test_grad_kgen_random_plan(gw, k, n, m):
     G = gw.grad(x, y, p, q, _to_dev(gw, T), k=k).cpu().numpy().astype(np.float64)
     Go = O.grad_prescribed(x, y, p, q, T.astype(np.float64), k=k)
     assert _grad_err(G, Go) <= GRAD_TOL
+
+
+@pytest.mark.parametrize("n,m", [(2048, 2048), (1500, 16384)])
+def test_grad_k4_moments_path(gw, n, m):
+    """k = 4 runs the polynomial-moments path (poly.cuh: 25 plan moments + an fp64 degree-4 polynomial
+    per row; 4NM + 4NM bytes): wide, shifted supports and long rows (fp32 partial moment sums over many
+    columns) against the dense definition."""
+    rng = np.random.default_rng(n + m)
+    x, y = 10.0 * np.sort(rng.random(n)) - 3.0, 4.0 * np.sort(rng.random(m)) + 1.0
+    p, q = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))
+    T = (rng.exponential(size=(n, m)) / (n * m)).astype(np.float32)
+    G = gw.grad(x, y, p, q, _to_dev(gw, T), k=4).cpu().numpy().astype(np.float64)
+    Go = O.grad_prescribed(x, y, p, q, T.astype(np.float64), k=4)
+    err = _grad_err(G, Go)
+    print("k=4 moments path n=%d m=%d: gradient err / max|G| %.3e" % (n, m, err))
+    assert err <= GRAD_TOL
 
 
 def test_grad_k3_c3_recipe_2048(gw):
