@@ -101,8 +101,13 @@ typedef struct {
   uint32_t flags;         /* GW_NO_VALIDATE | GW_HOST_VECTORS | GW_GRID2D              */
 } gw_problem;
 
-/* Optional precomputed moments of T (device, fp64).  Not used in ABI v1
- * (gw_grad_dp always computes them in its moments pass); reserved. */
+/* Optional precomputed moments of T (device, fp64, the caller's coordinates; nullable argument of
+ * gw_grad_dp, k = 1 on 1-D supports): the plan's row totals T 1 and T y over this rank's rows and its
+ * column totals T^T 1 and T^T x over ALL rows.  When given they replace the totals the moments pass
+ * reduces -- the rank-2 term -4[(D_X (T y))_i - (D_X (T 1))_i y_p] and the column totals' 1-D DPs of
+ * PAPER.md:122-126 / 190-259 are formed from them -- while the pass itself still runs for the per-tile
+ * partials that feed the carries.  All four must be non-null (GW_ERR_INVALID_ARG); k != 1 or 2-D grids:
+ * GW_ERR_UNSUPPORTED. */
 typedef struct {
   const double *row_sum, *row_ysum;   /* T 1, T y over this shard's rows       */
   const double *col_sum, *col_xsum;   /* T^T 1, T^T x over ALL rows            */
@@ -201,8 +206,8 @@ gw_status gw_check_shards(const int64_t *table, int nranks, int64_t n);
  * realised as row and column prefix scans with fp64 carries.  With a multi-rank ctx every rank
  * passes its own rows of T and receives its rows of G.
  * T: device fp32 (n_local x m, ldT); G: device fp32 output (ldG), may alias T
- * (ldG == ldT).  c, c' use the PRESCRIBED p, q (reading R4).  mom: must be NULL
- * in ABI v1.  Asynchronous. */
+ * (ldG == ldT).  c, c' use the PRESCRIBED p, q (reading R4).  mom (nullable): the
+ * plan's row / column totals (gw_moments above).  Asynchronous. */
 gw_status gw_grad_dp(gw_ctx *ctx, const gw_problem *prob, const void *T, int64_t ldT,
                      void *G, int64_t ldG, const gw_moments *mom);
 

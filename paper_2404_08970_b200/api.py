@@ -95,11 +95,13 @@ def _problem(x, y, p, q, n_local=None, row0=0, flags=0, k=1, grid2d=False):
     return pr
 
 
-def grad(x, y, p, q, T, out=None, validate=True, ctx=None, row0=0, k=1, grid2d=False):
+def grad(x, y, p, q, T, out=None, validate=True, ctx=None, row0=0, k=1, grid2d=False, moments=None):
     """G = 2(c 1^T + 1 c'^T) - 4 D_X T D_Y  (gw_grad_dp), fp32.
     Sharded (ctx with a multi-rank comm): x, p are the full supports/marginals, T holds this
     rank's rows [row0, row0 + T.shape[0]) and the result holds the same rows of G.
-    grid2d: x, y are the axes of 2-D grids with the Manhattan distance (GW_GRID2D)."""
+    grid2d: x, y are the axes of 2-D grids with the Manhattan distance (GW_GRID2D).
+    moments: optional (row_sum, row_ysum, col_sum, col_xsum) = (T 1, T y, T^T 1, T^T x) of the plan
+    (gw_moments; this rank's rows / all rows), used for the totals instead of the reduced ones."""
     ctx = ctx or Context.get(T.device)
     dev = T.device
     x, y, p, q = (_vec(v, dev) for v in (x, y, p, q))
@@ -109,7 +111,12 @@ def grad(x, y, p, q, T, out=None, validate=True, ctx=None, row0=0, k=1, grid2d=F
         out = plan_buffer(n, m, dev)
     ldG = _check_mat(out, "out")
     pr = _problem(x, y, p, q, n_local=n, row0=row0, flags=0 if validate else L.GW_NO_VALIDATE, k=k, grid2d=grid2d)
-    L.check(ctx.lib.gw_grad_dp(ctx.h, C.byref(pr), _ptr(T), ldT, _ptr(out), ldG, None))
+    mom = None
+    if moments is not None:
+        mv = [_vec(v, dev) for v in moments]
+        mom = L.gw_moments(*(v.data_ptr() for v in mv))
+    L.check(ctx.lib.gw_grad_dp(ctx.h, C.byref(pr), _ptr(T), ldT, _ptr(out), ldG,
+                               C.byref(mom) if mom is not None else None))
     return out
 
 

@@ -139,26 +139,30 @@ __global__ void __launch_bounds__(G2D_MAXN) k_g2_rowred(TSrc2 S, int ny, double*
   float gq = 0.f, glq = 0.f;  // (column duals are per q: loaded per element below)
   constexpr int U = 8;        // loads of U columns c in flight per thread
   for (int c0 = 0; c0 < ny; c0 += U) {
-    float raw[U];
+    float raw[U], gqv[U], glv[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int c = c0 + u;
-      raw[u] = (dv && c < ny && MODE != T_PRODUCT) ? row[(int64_t)c * ny + d] : 0.f;
+      const int64_t q = (int64_t)c * ny + d;
+      const bool ok = dv && c < ny;
+      raw[u] = (ok && MODE != T_PRODUCT) ? row[q] : 0.f;
+      gqv[u] = (ok && MODE != T_EXPLICIT) ? S.gh[q] : 0.f;
+      glv[u] = (ok && MODE == T_GIBBS) ? S.gl[q] : 0.f;
     }
+    float tv[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int c = c0 + u;
-      if (c >= ny) break;  // uniform across the CTA
       float t = 0.f;
-      if (dv) {
+      if (dv && c < ny) {
         const int64_t q = (int64_t)c * ny + d;
         if (MODE == T_EXPLICIT) {
           t = raw[u];
         } else if (MODE == T_PRODUCT) {
-          t = Fh * S.gh[q];
+          t = Fh * gqv[u];
         } else {
-          gq = S.gh[q];
-          glq = S.gl[q];
+          gq = gqv[u];
+          glq = glv[u];
           const float a = (fmaf(raw[u], -S.ch, gq) + Fh) + fmaf(raw[u], -S.cl, glq + Fl);
           t = ex2_ftz(a);
           if (OBJ && t > 0.f) ent += t * fmaf(a, 0.6931471805599453f, -1.f);
@@ -170,11 +174,24 @@ __global__ void __launch_bounds__(G2D_MAXN) k_g2_rowred(TSrc2 S, int ny, double*
         }
       }
       rd += t;
-      float v = t;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) wp[c][w] = v;
+      tv[u] = t;
     }
+    // warp sums of the U = 8 columns by recursive halving (9 shuffles for 8 sums instead of 40): lanes
+    // with (lane & 3) == 0 end with column c0 + (lane >> 2); fixed lane structure -> deterministic
+#pragma unroll
+    for (int h = 4; h >= 1; h >>= 1) {  // lane bit 16 -> 4 values, bit 8 -> 2, bit 4 -> 1
+      const int bit = 4 * h;
+#pragma unroll
+      for (int k = 0; k < h; ++k) {
+        const bool hi = lane & bit;
+        const float send = hi ? tv[k] : tv[h + k];
+        const float keep = hi ? tv[h + k] : tv[k];
+        tv[k] = keep + __shfl_xor_sync(0xffffffffu, send, bit);
+      }
+    }
+    tv[0] += __shfl_xor_sync(0xffffffffu, tv[0], 2);
+    tv[0] += __shfl_xor_sync(0xffffffffu, tv[0], 1);
+    if ((lane & 3) == 0 && c0 + (lane >> 2) < ny) wp[c0 + (lane >> 2)][w] = tv[0];
   }
   __syncthreads();
   const int nw = (blockDim.x + 31) / 32;
@@ -256,14 +273,16 @@ __global__ void __launch_bounds__(256) k_g2_store(const double* __restrict__ cX,
   const int64_t il0 = (int64_t)blockIdx.y * G2SR, il1 = min(nl, il0 + G2SR);
   const bool vt = t < ny;  // this thread forms entry t of the row's two vectors
   double vac = 0, vbc = 0, vad = 0, vbd = 0, cxi = 0;
+  // grid coordinates (a, b) of row i = a nx + b, advanced incrementally (no division per row)
+  int fa = (int)((row0 + il0) / nx), fb = (int)((row0 + il0) - (int64_t)fa * nx);
   auto fetch = [&](int64_t il) {
     const int64_t i = row0 + il;
-    const int a = (int)(i / nx), b = (int)(i - (int64_t)a * nx);
     if (vt) {
-      vac = VAC[(int64_t)a * ny + t]; vbc = VBC[(int64_t)b * ny + t];
-      vad = VAD[(int64_t)a * ny + t]; vbd = VBD[(int64_t)b * ny + t];
+      vac = VAC[(int64_t)fa * ny + t]; vbc = VBC[(int64_t)fb * ny + t];
+      vad = VAD[(int64_t)fa * ny + t]; vbd = VBD[(int64_t)fb * ny + t];
       cxi = cX[i];
     }
+    if (++fb == nx) { fb = 0; ++fa; }
   };
   if (il0 < il1) fetch(il0);
   for (int64_t il = il0; il < il1; ++il) {
@@ -291,6 +310,84 @@ __global__ void __launch_bounds__(256) k_g2_store(const double* __restrict__ cX,
 #pragma unroll
       for (int k = 0; k < G2SC; ++k)
         if (qb + 256 * k < m) __stcs(dst + 256 * k, o[k]);
+    }
+  }
+}
+
+// The same store with 4 consecutive columns per thread group (ny % 4 == 0: the 4 share c, and d..d+3
+// are consecutive): one rc read, two double2 rd reads and ONE 16-byte store per 4 elements; row grid
+// coordinates advance incrementally (no division per row).  (Reading the V rows straight from L1
+// without the shared-memory staging measured slower: 10.1 vs 8.4 ms at 256^2 x 256^2.)
+template <bool FGW>
+__global__ void __launch_bounds__(256) k_g2_store4(const double* __restrict__ cX, const double* __restrict__ cY,
+                                                   const double* __restrict__ VAC, const double* __restrict__ VAD,
+                                                   const double* __restrict__ VBC, const double* __restrict__ VBD,
+                                                   int nx, int ny, int64_t row0, int64_t nl, int64_t m, double alpha,
+                                                   const double* __restrict__ fx, const double* __restrict__ fy,
+                                                   float* __restrict__ G, int64_t ldG) {
+  __shared__ __align__(16) double rc[2][G2D_MAXN], rd[2][G2D_MAXN];
+  const int t = threadIdx.x;
+  constexpr int NG = G2SC / 4;  // groups of 4 columns per thread
+  const int64_t qb = (int64_t)G2SC * 256 * blockIdx.x + 4 * t;  // groups at qb + 1024 k
+  const double a2 = 2.0 * alpha, a1 = 1.0 - alpha, a4 = -4.0 * alpha;
+  double cy[NG][4], fyv[NG][4];
+  int cc[NG], dd[NG];
+  bool gv[NG];
+#pragma unroll
+  for (int k = 0; k < NG; ++k) {
+    const int64_t q = qb + 1024 * k;
+    gv[k] = q < m;
+    const int64_t qq = gv[k] ? q : 0;
+    cc[k] = (int)(qq / ny);
+    dd[k] = (int)(qq - (int64_t)cc[k] * ny);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      cy[k][e] = gv[k] ? a2 * cY[qq + e] : 0.0;
+      fyv[k][e] = (FGW && gv[k]) ? fy[qq + e] : 0.0;
+    }
+  }
+  const int64_t il0 = (int64_t)blockIdx.y * G2SR, il1 = min(nl, il0 + G2SR);
+  const bool vt = t < ny;
+  double vac = 0, vbc = 0, vad = 0, vbd = 0, cxi = 0;
+  int fa = (int)((row0 + il0) / nx), fb = (int)((row0 + il0) - (int64_t)fa * nx);
+  auto fetch = [&](int64_t il) {
+    const int64_t i = row0 + il;
+    if (vt) {
+      vac = VAC[(int64_t)fa * ny + t]; vbc = VBC[(int64_t)fb * ny + t];
+      vad = VAD[(int64_t)fa * ny + t]; vbd = VBD[(int64_t)fb * ny + t];
+      cxi = cX[i];
+    }
+    if (++fb == nx) { fb = 0; ++fa; }
+  };
+  if (il0 < il1) fetch(il0);
+  for (int64_t il = il0; il < il1; ++il) {
+    const int buf = (int)(il & 1);
+    if (vt) {
+      rc[buf][t] = fma(a4, vac + vbc, a2 * cxi);
+      rd[buf][t] = a4 * (vad + vbd);
+    }
+    if (il + 1 < il1) fetch(il + 1);
+    __syncthreads();
+    const int64_t i = row0 + il;
+    const double fxi = FGW ? fx[i] : 0.0;
+#pragma unroll
+    for (int k = 0; k < NG; ++k) {
+      if (!gv[k]) continue;
+      const double r = rc[buf][cc[k]];
+      const double2 d01 = *reinterpret_cast<const double2*>(&rd[buf][dd[k]]);
+      const double2 d23 = *reinterpret_cast<const double2*>(&rd[buf][dd[k] + 2]);
+      const double dv[4] = {d01.x, d01.y, d23.x, d23.y};
+      float o[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        double v = (r + dv[e]) + cy[k][e];
+        if (FGW) {
+          const double df = fxi - fyv[k][e];
+          v = fma(a1 * df, df, v);
+        }
+        o[e] = (float)v;
+      }
+      __stcs(reinterpret_cast<float4*>(G + il * ldG + qb + 1024 * k), make_float4(o[0], o[1], o[2], o[3]));
     }
   }
 }

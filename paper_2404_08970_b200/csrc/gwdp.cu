@@ -387,6 +387,7 @@ struct Prepared {
   float* yf;         // fp32 centred y (k = 2 path)
   double mass_p = 1.0, mass_q = 1.0;  // m(u), m(v): 1 except for ugw_solve (weights not normalised)
   double xlast, ylast;
+  double xend_u = 0.0, yend_u = 0.0;  // x_{n-1}, y_{m-1} in the caller's (uncentred) coordinates
   int k = 1;         // distance power
   bool grid2d = false;  // GW_GRID2D: xc / yc are the centred axes (nx, ny entries)
   int nx = 0, ny = 0;
@@ -624,10 +625,31 @@ static gw_status prepare(gw_ctx* c, const gw_problem* pb, Prepared& P, bool unba
   CU(cudaStreamSynchronize(c->stream));
   P.xlast = ends[1] - h[6];
   P.ylast = ends[3] - h[14];
+  P.xend_u = ends[1];
+  P.yend_u = ends[3];
   return shard_table(c, P);
 }
 
 // ------------------------------------------------------------------------------ gradient
+// Supplied moments (gw_moments): the plan's row totals T 1, T y (this rank's rows) and column totals
+// T^T 1, T^T x (all rows), in the caller's coordinates, replace the totals the moments pass reduced:
+//   Ptot = T 1,  Aend = sum_q (y_{m-1} - y_q) T_jq = y_{m-1} T 1 - T y,
+//   btot = T^T 1,  cxend = sum_j (x_{n-1} - x_j) T_jq = x_{n-1} T^T 1 - T^T x.
+__global__ void k_moments_rows(int64_t nl, const double* __restrict__ rs, const double* __restrict__ rys,
+                               double yend, double* __restrict__ Ptot, double* __restrict__ Aend) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nl; i += (int64_t)gridDim.x * blockDim.x) {
+    Ptot[i] = rs[i];
+    Aend[i] = yend * rs[i] - rys[i];
+  }
+}
+__global__ void k_moments_cols(int64_t m, const double* __restrict__ cs, const double* __restrict__ cxs, double xend,
+                               double* __restrict__ btot, double* __restrict__ cxend) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x) {
+    btot[q] = cs[q];
+    cxend[q] = xend * cs[q] - cxs[q];
+  }
+}
+
 struct GradOut {
   double E, viol, go, H, cc;  // filled when OBJ
 };
@@ -641,7 +663,7 @@ struct GradOut {
 // fh/fl == split(f log2e/eps) and gh/gl == split(g log2e/eps) of the COMMITTED duals.
 static gw_status grad_pass_k1(gw_ctx* c, const Prepared& P, int mode, const TSrc& S, const TSrc2& S2, float* G,
                               int64_t ldG, bool store, bool obj, const double* fx, const double* fy, double alpha,
-                              double* objout_dev, double beta = 0.0) {
+                              double* objout_dev, double beta = 0.0, const gw_moments* mom = nullptr) {
   const int64_t nl = P.nl, m = P.m, n = P.n;
   const int R = P.R;
   if (nl == 0) return GW_OK;  // single rank only: prepare() rejects empty shards when R > 1
@@ -686,6 +708,14 @@ static gw_status grad_pass_k1(gw_ctx* c, const Prepared& P, int mode, const TSrc
   KCHECK();
   k_rowcarry<<<nb, TR, 0, c->stream>>>(nl, m, ns, xl, P.yc, rP, rA, blk, Ptot, Aend);
   KCHECK();
+  if (mom) {  // supplied row totals (this rank's rows) replace the reduced ones
+    k_moments_rows<<<grid_for(nl), 256, 0, c->stream>>>(nl, mom->row_sum, mom->row_ysum, P.yend_u, Ptot, Aend);
+    KCHECK();
+    if (R == 1) {
+      k_moments_cols<<<grid_for(m), 256, 0, c->stream>>>(m, mom->col_sum, mom->col_xsum, P.xend_u, btot, cxend);
+      KCHECK();
+    }
+  }
   if (fault_is("carry") && ns > 1 && nl > 0) {  // test-only: one row carry doubled
     k_fault_scale<<<1, 32, 0, c->stream>>>(rP, (int64_t)1 * nl + nl / 2, 2.0);
     KCHECK();
@@ -707,6 +737,10 @@ static gw_status grad_pass_k1(gw_ctx* c, const Prepared& P, int mode, const TSrc
     k_cols_ranks<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(g1, R, P.rank, P.dtab, P.xc, m, in, in + m, btot,
                                                                    cxend);
     KCHECK();
+    if (mom) {  // supplied global column totals replace the gathered ones
+      k_moments_cols<<<grid_for(m), 256, 0, c->stream>>>(m, mom->col_sum, mom->col_xsum, P.xend_u, btot, cxend);
+      KCHECK();
+    }
     k_cols_apply<<<grid_for((int64_t)nb * m, 256, 148 * 16), 256, 0, c->stream>>>(nb, m, xl, in, in + m, cS, cX);
     KCHECK();
     // (2) block-strip sums of the row carries of the ranks above
@@ -971,7 +1005,12 @@ static gw_status grad_pass_2d(gw_ctx* c, const Prepared& P, int mode, const TSrc
   if (store && nl > 0) {
     PROF_BEGIN(c, PC_GRAD_MAIN);
     const dim3 sg((unsigned)((m + 256 * G2SC - 1) / (256 * G2SC)), (unsigned)((nl + G2SR - 1) / G2SR));
-    if (fx) k_g2_store<true><<<sg, 256, 0, c->stream>>>(P.cx, P.cy, VT, VT + nn, VT + 2 * nn, VT + 3 * nn, nx, ny,
+    if (ny % 4 == 0) {  // 4 consecutive columns share their grid row c: vectorised stores
+      if (fx) k_g2_store4<true><<<sg, 256, 0, c->stream>>>(P.cx, P.cy, VT, VT + nn, VT + 2 * nn, VT + 3 * nn, nx, ny,
+                                                          P.row0, nl, m, alpha, fx, fy, G, ldG);
+      else k_g2_store4<false><<<sg, 256, 0, c->stream>>>(P.cx, P.cy, VT, VT + nn, VT + 2 * nn, VT + 3 * nn, nx, ny,
+                                                        P.row0, nl, m, alpha, nullptr, nullptr, G, ldG);
+    } else if (fx) k_g2_store<true><<<sg, 256, 0, c->stream>>>(P.cx, P.cy, VT, VT + nn, VT + 2 * nn, VT + 3 * nn, nx, ny,
                                                        P.row0, nl, m, alpha, fx, fy, G, ldG);
     else k_g2_store<false><<<sg, 256, 0, c->stream>>>(P.cx, P.cy, VT, VT + nn, VT + 2 * nn, VT + 3 * nn, nx, ny,
                                                      P.row0, nl, m, alpha, nullptr, nullptr, G, ldG);
@@ -1118,13 +1157,13 @@ static gw_status grad_store_poly4(gw_ctx* c, const Prepared& P, int mode, const 
 
 static gw_status grad_pass(gw_ctx* c, const Prepared& P, int mode, const TSrc& S, const TSrc2& S2, float* G,
                            int64_t ldG, bool store, bool obj, const double* fx, const double* fy, double alpha,
-                           double* objout_dev, double beta = 0.0) {
+                           double* objout_dev, double beta = 0.0, const gw_moments* mom = nullptr) {
   NvtxRange nv(obj && !store ? "gw.objective" : "gw.grad");
   if (beta != 0.0 && (P.grid2d || P.k != 1 || obj || !store))
     return fail(GW_ERR_UNSUPPORTED, "tau != eps: only the k = 1 1-D gradient store carries the (eps - tau) ln T term");
   if (beta != 0.0) return grad_pass_k1(c, P, mode, S, S2, G, ldG, store, obj, fx, fy, alpha, objout_dev, beta);
   if (P.grid2d) return grad_pass_2d(c, P, mode, S2, G, ldG, store, obj, fx, fy, alpha, objout_dev);
-  if (P.k == 1) return grad_pass_k1(c, P, mode, S, S2, G, ldG, store, obj, fx, fy, alpha, objout_dev);
+  if (P.k == 1) return grad_pass_k1(c, P, mode, S, S2, G, ldG, store, obj, fx, fy, alpha, objout_dev, 0.0, mom);
   if (P.k == 4 && store && !obj) return grad_store_poly4(c, P, mode, S2, G, ldG, fx, fy, alpha);
   if (P.k >= 3) {
     if (P.nl == 0) return GW_OK;
@@ -1182,8 +1221,13 @@ static gw_status grad_pass(gw_ctx* c, const Prepared& P, int mode, const TSrc& S
 extern "C" gw_status gw_grad_dp(gw_ctx* c, const gw_problem* pb, const void* T, int64_t ldT, void* G, int64_t ldG,
                                 const gw_moments* mom) {
   if (!c) return fail(GW_ERR_INVALID_ARG, "null ctx");
-  if (mom) return fail(GW_ERR_UNSUPPORTED, "gw_grad_dp: precomputed moments are not accepted in ABI v1");
   TRY(check_problem(pb));
+  if (mom) {
+    if (!mom->row_sum || !mom->row_ysum || !mom->col_sum || !mom->col_xsum)
+      return fail(GW_ERR_INVALID_ARG, "gw_grad_dp: gw_moments needs all four vectors");
+    if (pb->k != 1 || (pb->flags & GW_GRID2D))
+      return fail(GW_ERR_UNSUPPORTED, "gw_grad_dp: precomputed moments are used by the k = 1 1-D gradient only");
+  }
   TRY(check_matrix(T, ldT, pb->m, "T"));
   TRY(check_matrix(G, ldG, pb->m, "G"));
   CU(cudaSetDevice(c->device));
@@ -1192,7 +1236,7 @@ extern "C" gw_status gw_grad_dp(gw_ctx* c, const gw_problem* pb, const void* T, 
   TSrc S{reinterpret_cast<const float*>(T), ldT, nullptr, nullptr, 0.0};
   TSrc2 S2{reinterpret_cast<const float*>(T), ldT, nullptr, nullptr, nullptr, nullptr, 0.f, 0.f};
   TRY(grad_pass(c, P, T_EXPLICIT, S, S2, reinterpret_cast<float*>(G), ldG, true, false, nullptr, nullptr, 1.0,
-                nullptr));
+                nullptr, 0.0, mom));
   return GW_OK;
 }
 

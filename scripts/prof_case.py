@@ -39,16 +39,25 @@ def main():
         G = torch.empty_like(T)
         for _ in range(2):
             api.grad(x, x, p, p, T, out=G, k=k)
-    elif case == "grid2d":
-        side = 128
+    elif case in ("grid2d", "grid2d256"):
+        side = 128 if case == "grid2d" else 256
         s = np.arange(side) / (side - 1.0)
         w = rng.random(side * side) + 0.05
         w /= w.sum()
         T = api.plan_buffer(side * side, side * side, dev)
         T.copy_(torch.rand((side * side, side * side), device=dev) / (side ** 4))
         G = torch.empty_like(T)
-        for _ in range(2):
+        api.grad(s, s, w, w, T, out=G, grid2d=True)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(3):
             api.grad(s, s, w, w, T, out=G, grid2d=True)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 3
+        nm = float(side) ** 4
+        print("grid2d %dx%d gradient %.3f ms, %.0f GB/s over 8NM" % (side, side, ms, 8 * nm / ms / 1e6))
     else:
         raise SystemExit("unknown case %s" % case)
     torch.cuda.synchronize()

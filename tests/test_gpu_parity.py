@@ -105,6 +105,40 @@ def test_grad_in_place(gw):
     assert _grad_err(G, O.grad_prescribed(x, y, p, q, T.astype(np.float64))) <= GRAD_TOL
 
 
+def test_grad_supplied_moments(gw):
+    """gw_grad_dp with gw_moments (the plan's T1, Ty, T^T 1, T^T x in the caller's coordinates): the
+    totals are taken from the argument -- exact moments give the same G (both at the tolerance of the
+    dense definition), perturbed ones move G (so they are used), null members are rejected."""
+    import torch
+    from paper_2404_08970_b200 import GwError
+    rng = np.random.default_rng(77)
+    n, m = 600, 700
+    x, y = 3.0 * np.sort(rng.random(n)) + 1.0, np.sort(rng.random(m)) - 2.0
+    p, q = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))
+    T = (rng.exponential(size=(n, m)) / (n * m)).astype(np.float32)
+    T64 = T.astype(np.float64)
+    mom = (T64.sum(1), T64 @ y, T64.sum(0), x @ T64)
+    Td = _to_dev(gw, T)
+    Go = O.grad_prescribed(x, y, p, q, T64)
+    G0 = gw.grad(x, y, p, q, Td).cpu().numpy().astype(np.float64)
+    G1 = gw.grad(x, y, p, q, Td, moments=mom).cpu().numpy().astype(np.float64)
+    assert _grad_err(G0, Go) <= GRAD_TOL and _grad_err(G1, Go) <= GRAD_TOL
+    assert np.max(np.abs(G1 - G0)) <= 1e-6 * np.max(np.abs(Go))
+    bad = (mom[0] * (1 + 1e-3), mom[1], mom[2], mom[3])
+    G2 = gw.grad(x, y, p, q, Td, moments=bad).cpu().numpy().astype(np.float64)
+    assert _grad_err(G2, Go) > 10 * GRAD_TOL
+    from paper_2404_08970_b200 import _lib as L
+    lib = L.load()
+    z = torch.zeros(1, dtype=torch.float64, device=Td.device)
+    mm = L.gw_moments(z.data_ptr(), None, z.data_ptr(), z.data_ptr())
+    st = lib.gw_grad_dp(None, None, None, 0, None, 0, None)
+    assert L.STATUS[st] == "GW_ERR_INVALID_ARG"
+    with pytest.raises(GwError) as e:
+        gw.grad(x, y, p, q, Td, moments=mom, k=2)
+    assert e.value.code == "GW_ERR_UNSUPPORTED"
+    del mm
+
+
 def test_grad_deterministic(gw):
     P = W.config3(1500)
     Td = _to_dev(gw, P.extra["T"])
