@@ -537,7 +537,11 @@ __global__ void k_sink_fin_fast(const float* __restrict__ Srow, int64_t nl, cons
                                 const double* __restrict__ lq, double eps, double* __restrict__ g,
                                 float* __restrict__ gh, float* __restrict__ gl, int* __restrict__ mode,
                                 const int* __restrict__ stop, float* __restrict__ dev, const int* __restrict__ flag,
-                                double kappa = 1.0) {
+                                double kappa = 1.0, cudaGraphConditionalHandle cond = 0, int use_cond = 0) {
+  // inside a captured iteration: arm the conditional node that runs the safe path iff this iteration
+  // was not committed here (path already safe, or the speculation failed its check)
+  if (use_cond && blockIdx.x == 0 && threadIdx.x == 0)
+    cudaGraphSetConditional(cond, (!(stop && *stop) && (*mode != 1 || *flag)) ? 1u : 0u);
   if (*mode != 1 || (stop && *stop)) return;
   if (*flag) {
     // speculation failed: nothing is committed and this iteration runs the safe path instead

@@ -97,6 +97,7 @@ struct gw_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t cap = nullptr;  // CUDA-graph capture stream (created on first use)
+  cudaStream_t cap2 = nullptr;  // capture stream of a conditional node's body
   gw_comm* comm = nullptr;
   std::vector<Buf*> all;
   // vectors
@@ -107,7 +108,7 @@ struct gw_ctx {
   Buf fxs, fys;  // FGW features (staged)
   Buf pnf, qnf;  // fp32 marginals
   Buf yfb, pcoef, pc2s, pfx, pfy, ppart, pM, p4coef, p4c2;  // k = 2 and k = 4 (moments) paths
-  Buf gkrp, gkrt, gkcp, gkz, gkct, gkctt, gkobj;  // k >= 3 path
+  Buf gkrp, gkrt, gkcp, gkz, gkct, gkctt, gkobj, gkseg;  // k >= 3 path
   Buf uga, ugb, ugct, ugpart, ugca, ugcb, ugfr, uggr, ugsc;  // UGW
   Buf g2rc, g2rd, g2h, g2cc, g2tt, g2vt, g2tmp, g2s, g2a, g2b, g2ca, g2cb, g2part;  // 2-D grids
   Buf xtab, xg1, xg2, xin, xvec, xtail, xpart;  // multi-rank exchange buffers
@@ -128,7 +129,7 @@ struct gw_ctx {
                 &SAg, &WAg, &Ptot, &Aend, &DP, &DA, &tobj, &tent, &tcc, &objout, &scanwt, &fxs, &fys, &fsc, &gsc, &Gs,
                 &pnf, &qnf, &xtab, &xg1, &xg2, &xin, &xvec, &xtail, &xpart, &slse, &slseg, &scsl, &scsg, &sun, &sung,
                 &sviolg, &sflag, &sflagg, &yfb, &pcoef, &pc2s, &pfx, &pfy, &ppart, &pM, &p4coef, &p4c2,
-                &gkrp, &gkrt, &gkcp, &gkz, &gkct, &gkctt, &gkobj,
+                &gkrp, &gkrt, &gkcp, &gkz, &gkct, &gkctt, &gkobj, &gkseg,
                 &uga, &ugb, &ugct, &ugpart, &ugca, &ugcb, &ugfr, &uggr, &ugsc,
                 &g2rc, &g2rd, &g2h, &g2cc, &g2tt, &g2vt, &g2tmp, &g2s, &g2a, &g2b, &g2ca, &g2cb, &g2part};
     for (Buf* x : b) all.push_back(x);
@@ -1034,6 +1035,24 @@ static gw_status gk_main_launch(gw_ctx* c, dim3 grid, const TSrc2& S2, int64_t n
   return GW_OK;
 }
 
+// Exclusive prefix over the nt tiles of part[nt][len2] (+ totals): segmented when there are many tiles
+static gw_status gk_scan_tiles(gw_ctx* c, double* part, int nt, int64_t len2, double* tot) {
+  if (nt <= 32) {
+    k_gk_scan_tiles<<<grid_for(len2), 256, 0, c->stream>>>(part, nt, len2, tot);
+    KCHECK();
+    return GW_OK;
+  }
+  const int nseg = std::min(32, (nt + 15) / 16);
+  double* seg;
+  TRY(ws(c, c->gkseg, (size_t)nseg * len2, &seg));
+  const dim3 g((unsigned)((len2 + 255) / 256), (unsigned)nseg);
+  k_gk_scan_seg_a<<<g, 256, 0, c->stream>>>(part, nt, len2, nseg, seg);
+  KCHECK();
+  k_gk_scan_seg_b<<<g, 256, 0, c->stream>>>(part, nt, len2, nseg, seg, tot);
+  KCHECK();
+  return GW_OK;
+}
+
 template <int K, int MODE>
 static gw_status grad_pass_gk_mode(gw_ctx* c, const Prepared& P, const TSrc2& S2, float* G, int64_t ldG, bool store,
                                    bool obj, const double* fx, const double* fy, double alpha, double* objout_dev) {
@@ -1054,12 +1073,10 @@ static gw_status grad_pass_gk_mode(gw_ctx* c, const Prepared& P, const TSrc2& S2
   KCHECK();
   PROF_END(c, PC_GRAD_MOMENTS, 1);
   PROF_BEGIN(c, PC_GRAD_CARRY);
-  k_gk_scan_tiles<<<grid_for((int64_t)K1 * nl), 256, 0, c->stream>>>(rp, ntc, (int64_t)K1 * nl, rt);
-  KCHECK();
+  TRY(gk_scan_tiles(c, rp, ntc, (int64_t)K1 * nl, rt));
   k_gk_apply<K><<<(unsigned)(ntr * K1), 256, 0, c->stream>>>(cp, m, P.yc, Z);
   KCHECK();
-  k_gk_scan_tiles<<<grid_for((int64_t)K1 * m), 256, 0, c->stream>>>(Z, ntr, (int64_t)K1 * m, ct);
-  KCHECK();
+  TRY(gk_scan_tiles(c, Z, ntr, (int64_t)K1 * m, ct));
   // multi-rank: the column sums of W over the rows of the ranks above (carry) and over all rows
   // (ct, replaced by the global totals): one all-gather of (k+1) M fp64 per rank
   double* carry = nullptr;
@@ -1080,8 +1097,7 @@ static gw_status grad_pass_gk_mode(gw_ctx* c, const Prepared& P, const TSrc2& S2
                                                      nullptr, nullptr, nullptr, 0, tob, carry)));
     // realised marginals: a = T 1 (row totals, power 0; this rank's rows), b = T^T 1 (column
     // totals of the plan over every rank: gathered and summed in rank order)
-    k_gk_scan_tiles<<<grid_for((int64_t)K1 * m), 256, 0, c->stream>>>(cp, ntr, (int64_t)K1 * m, ctt);
-    KCHECK();
+    TRY(gk_scan_tiles(c, cp, ntr, (int64_t)K1 * m, ctt));
     double *part, *gpart, *bg;
     TRY(ws(c, c->xpart, (size_t)(2 * K + 2) * (P.R + 1), &part));
     gpart = part + (2 * K + 2);
@@ -1527,6 +1543,8 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
     KCHECK();
   }
   // the fused one-read step of one iteration (speculative; a no-op unless *mode == 1)
+  cudaGraphConditionalHandle cond_h = 0;  // set while capturing the single-rank iteration graph
+  int use_cond = 0;
   auto fused_step = [&]() -> gw_status {
     // Every iteration first tries the fused one-read path when *mode == 1 (speculatively at the
     // start of a solve); k_sink_fast_check validates it before anything is committed, and on
@@ -1556,7 +1574,7 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
       KCHECK();
       k_sink_fin_fast<<<grid_for(std::max(m, nl), 256, 1 << 30), 256, 0, c->stream>>>(
           s.Srow, nl, P.lp + P.row0, s.f, s.fh, s.fl, nullptr, s.csg, P.R, stride, m, P.lq, eps, s.g, s.gh, s.gl,
-          s.mode, s.stop, s.dev, s.flag, kappa);
+          s.mode, s.stop, s.dev, s.flag, kappa, cond_h, use_cond);
       KCHECK();
       PROF_END(c, PC_SINK_FUSED, 2);
     }
@@ -1737,13 +1755,65 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
       s.g_eps = eps;
       s.g_kappa = kappa;
       if (!c->cap) CU(cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking));
-      CU(cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal));
-      cudaStream_t saved = c->stream;
-      c->stream = c->cap;
-      const gw_status st = iteration(false, 0);
-      c->stream = saved;
+      static const bool no_cond = getenv("GWDP_NO_COND") != nullptr;
       cudaGraph_t graph = nullptr;
-      const cudaError_t e = cudaStreamEndCapture(c->cap, &graph);
+      gw_status st = GW_OK;
+      cudaError_t e = cudaSuccess;
+      cudaStream_t saved = c->stream;
+      if (s.fK > 0 && !no_cond) {
+        // fused step, then the safe path as the body of a conditional (IF) node armed by
+        // k_sink_fin_fast, then the path decision: a committed fused iteration launches nothing else
+        if (!c->cap2) CU(cudaStreamCreateWithFlags(&c->cap2, cudaStreamNonBlocking));
+        CU(cudaGraphCreate(&graph, 0));
+        CU(cudaGraphConditionalHandleCreate(&cond_h, graph, 0, cudaGraphCondAssignDefault));
+        CU(cudaStreamBeginCaptureToGraph(c->cap, graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        c->stream = c->cap;
+        use_cond = 1;
+        st = fused_step();
+        use_cond = 0;
+        if (st == GW_OK) {
+          cudaStreamCaptureStatus cs;
+          const cudaGraphNode_t* deps = nullptr;
+          size_t nd = 0;
+          cudaGraph_t cg = nullptr;
+          e = cudaStreamGetCaptureInfo(c->cap, &cs, nullptr, &cg, &deps, &nd);
+          cudaGraphNodeParams cp = {};
+          cp.type = cudaGraphNodeTypeConditional;
+          cp.conditional.handle = cond_h;
+          cp.conditional.type = cudaGraphCondTypeIf;
+          cp.conditional.size = 1;
+          cudaGraphNode_t cn = nullptr;
+          if (e == cudaSuccess) e = cudaGraphAddNode(&cn, cg, deps, nd, &cp);
+          if (e == cudaSuccess) e = cudaStreamUpdateCaptureDependencies(c->cap, &cn, 1, cudaStreamSetCaptureDependencies);
+          if (e == cudaSuccess) {
+            cudaGraph_t body = cp.conditional.phGraph_out[0];
+            e = cudaStreamBeginCaptureToGraph(c->cap2, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+            if (e == cudaSuccess) {
+              c->stream = c->cap2;
+              k_sink_row<<<rgrid, 256, 0, c->stream>>>(G, ldG, nl, m, s.gh, s.gl, c2f, s.f, s.f, P.lp + P.row0, eps,
+                                                        s.fh, s.fl, nullptr, s.stop, nullptr, kappa);
+              k_sink_col<<<cgrid, 256, 0, c->stream>>>(G, ldG, nl, m, s.fh, s.fl, c2f, s.RB, s.part, s.stop, nullptr);
+              k_sink_colmergefin<<<grid_for(m, 256, 1 << 30), 256, 0, c->stream>>>(s.part, s.nrb, m, P.lq, eps, s.g,
+                                                                                    s.gh, s.gl, s.stop, nullptr, s.dev,
+                                                                                    kappa);
+              cudaGraph_t bo = nullptr;
+              e = cudaStreamEndCapture(c->cap2, &bo);
+              c->stream = c->cap;
+            }
+          }
+          k_sink_mode<<<1, 32, 0, c->stream>>>(s.dev, s.mode, 20.f);
+        }
+        c->stream = saved;
+        cudaGraph_t go = nullptr;
+        const cudaError_t e2 = cudaStreamEndCapture(c->cap, &go);
+        if (e == cudaSuccess) e = e2;
+      } else {
+        CU(cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal));
+        c->stream = c->cap;
+        st = iteration(false, 0);
+        c->stream = saved;
+        e = cudaStreamEndCapture(c->cap, &graph);
+      }
       if (st != GW_OK) {
         if (graph) cudaGraphDestroy(graph);
         return st;

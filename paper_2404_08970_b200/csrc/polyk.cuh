@@ -201,6 +201,53 @@ __global__ void k_gk_scan_tiles(double* __restrict__ part, int nt, int64_t len2,
   }
 }
 
+// The same exclusive prefix over tiles, segmented for parallelism (the sequential walk over hundreds of
+// tiles per element is load-latency bound): the nt tiles are split into nseg segments; pass A sums each
+// segment (segtot[seg][e]), pass B adds the segments before it (fixed order) and walks its own tiles.
+// Fixed summation order -> deterministic.
+__global__ void k_gk_scan_seg_a(const double* __restrict__ part, int nt, int64_t len2, int nseg,
+                                double* __restrict__ segtot) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int sg = blockIdx.y;
+  if (e >= len2) return;
+  const int per = (nt + nseg - 1) / nseg, t0 = sg * per, t1 = min(nt, t0 + per);
+  constexpr int U = 8;
+  double run = 0.0;
+  for (int k0 = t0; k0 < t1; k0 += U) {
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = k0 + u < t1 ? part[(int64_t)(k0 + u) * len2 + e] : 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) run += v[u];
+  }
+  segtot[(int64_t)sg * len2 + e] = run;
+}
+__global__ void k_gk_scan_seg_b(double* __restrict__ part, int nt, int64_t len2, int nseg,
+                                const double* __restrict__ segtot, double* __restrict__ tot) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int sg = blockIdx.y;
+  if (e >= len2) return;
+  const int per = (nt + nseg - 1) / nseg, t0 = sg * per, t1 = min(nt, t0 + per);
+  double run = 0.0;
+  for (int s2 = 0; s2 < sg; ++s2) run += segtot[(int64_t)s2 * len2 + e];
+  constexpr int U = 8;
+  for (int k0 = t0; k0 < t1; k0 += U) {
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = k0 + u < t1 ? part[(int64_t)(k0 + u) * len2 + e] : 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (k0 + u < t1) part[(int64_t)(k0 + u) * len2 + e] = run;
+      run += v[u];
+    }
+  }
+  if (sg == nseg - 1) {
+    double all = 0.0;
+    for (int s2 = 0; s2 < nseg; ++s2) all += segtot[(int64_t)s2 * len2 + e];
+    tot[e] = all;
+  }
+}
+
 // Z[b] = D^(K) U[b] along a sorted centred support s (length m), one CTA per vector: a totals sweep,
 // then a chunked block scan of the K+1 power sums (8 consecutive entries per thread per step).
 template <int K>

@@ -30,8 +30,10 @@ def main():
     if case == "gibbs":
         P = W.config4(n)
         api.solve(P.x, P.y, P.p, P.q, P.eps, 2, 5, device=dev)
-    elif case in ("k3", "k4"):
+    elif case in ("k3", "k4", "k3big", "k5big"):
         k = int(case[1])
+        if case.endswith("big"):
+            n = 65536
         x = np.sort(rng.random(n))
         p = np.full(n, 1.0 / n)
         T = api.plan_buffer(n, n, dev)
