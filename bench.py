@@ -40,7 +40,7 @@ sys.path.insert(0, ROOT)
 METRIC = "DP GW-gradient GB/s (% of HBM peak) and entropic-GW outer iters/s at N=M=65536"
 UNIT = "outer_iter/s"
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
-TRAFFIC_PATH = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
+TRAFFIC_PATH = os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
 KERNELS = ["grad_moments", "grad_carry", "grad_main", "sink_row", "sink_col", "sink_fused", "objective_pass"]
 

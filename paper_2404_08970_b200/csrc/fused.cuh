@@ -599,10 +599,12 @@ __global__ void k_sink_fin_fast(const float* __restrict__ Srow, int64_t nl, cons
 // Path decision for the next iteration: fast (fused, absorbed duals) iff the last column
 // correction was within 2^20 -> then every plan entry e_ip <= 2^20 and every column sum of
 // the half-step plan stays within 2^{+-20} of q (no fp32 overflow or catastrophic underflow).
-__global__ void k_sink_mode(float* __restrict__ dev, int* __restrict__ mode, float thresh) {
+__global__ void k_sink_mode(float* __restrict__ dev, int* __restrict__ mode, float thresh,
+                            int* __restrict__ flag_reset = nullptr) {
   if (threadIdx.x == 0) {
     *mode = (*dev <= thresh) ? 1 : 0;
     *dev = 0.f;
+    if (flag_reset) *flag_reset = 0;  // the next speculative iteration's validity flag starts clear
   }
 }
 

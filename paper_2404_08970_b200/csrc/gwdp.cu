@@ -1037,7 +1037,9 @@ static gw_status gk_main_launch(gw_ctx* c, dim3 grid, const TSrc2& S2, int64_t n
 
 // Exclusive prefix over the nt tiles of part[nt][len2] (+ totals): segmented when there are many tiles
 static gw_status gk_scan_tiles(gw_ctx* c, double* part, int nt, int64_t len2, double* tot) {
-  if (nt <= 32) {
+  // one thread per element already fills the machine from ~128K elements (C4: 262144, where the segmented
+  // form measured slower: 2.1 vs 1.6 ms per gradient); below that, segments add the parallelism
+  if (nt <= 32 || len2 >= 131072) {
     k_gk_scan_tiles<<<grid_for(len2), 256, 0, c->stream>>>(part, nt, len2, tot);
     KCHECK();
     return GW_OK;
@@ -1524,6 +1526,7 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
   const unsigned cgrid = (unsigned)std::min<int64_t>(((m + 1023) / 1024) * s.nrb, 148 * 4);
   const unsigned rgrid = (unsigned)std::min<int64_t>((nl + RROWS - 1) / RROWS, 148 * 4);
   CU(cudaMemsetAsync(s.stop, 0, sizeof(int), c->stream));
+  CU(cudaMemsetAsync(s.flag, 0, sizeof(int), c->stream));  // the speculation flag starts clear
   if (reset_count) CU(cudaMemsetAsync(s.mode, 0, 4 * sizeof(int), c->stream));  // dev = 0; count = 0
   // first iteration: speculative fused path if available (validated before commit), else safe
   k_fill_int<<<1, 32, 0, c->stream>>>(s.mode, s.fK > 0 ? 1 : 0);
@@ -1558,20 +1561,26 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
       // the column-sum payload (slot M), so ONE all-gather per iteration carries everything.
       const bool multi = P.R > 1;
       const int64_t stride = multi ? m + 1 : m;
-      if (multi) CU(cudaMemsetAsync(s.csl + m, 0, sizeof(double), c->stream));
-      k_sink_colsum<<<(unsigned)((m + 31) / 32), 256, 0, c->stream>>>(
-          s.fpart, s.fncl, m, s.csl, s.mode, s.stop, multi ? s.Srow : nullptr, multi ? nl : 0,
-          multi ? reinterpret_cast<int*>(s.csl + m) : nullptr);
+      if (multi) {
+        CU(cudaMemsetAsync(s.csl + m, 0, sizeof(double), c->stream));
+        k_sink_colsum<<<(unsigned)((m + 31) / 32), 256, 0, c->stream>>>(
+            s.fpart, s.fncl, m, s.csl, s.mode, s.stop, s.Srow, nl, reinterpret_cast<int*>(s.csl + m));
+      } else {  // one rank: column sums + the whole validity check in one launch (flag cleared by k_sink_mode)
+        k_sink_colsum<<<(unsigned)((m + 31) / 32), 256, 0, c->stream>>>(
+            s.fpart, s.fncl, m, s.csl, s.mode, s.stop, s.Srow, nl, s.flag, s.flag, P.lq);
+      }
       KCHECK();
       if (fault_is("colsum")) {  // test-only: one column sum of the half-step plan doubled
         k_fault_scale<<<1, 32, 0, c->stream>>>(s.csl, m / 2, 2.0);
         KCHECK();
       }
       TRY(comm_allgather(c, s.csl, s.csg, sizeof(double) * (size_t)stride));
-      CU(cudaMemsetAsync(s.flag, 0, sizeof(int), c->stream));
-      k_sink_fast_check<<<grid_for(std::max(m, nl), 256, 1 << 30), 256, 0, c->stream>>>(
-          s.Srow, nl, s.csg, P.R, stride, m, P.lq, s.flag, s.mode, s.stop, multi);
-      KCHECK();
+      if (multi) {
+        CU(cudaMemsetAsync(s.flag, 0, sizeof(int), c->stream));
+        k_sink_fast_check<<<grid_for(std::max(m, nl), 256, 1 << 30), 256, 0, c->stream>>>(
+            s.Srow, nl, s.csg, P.R, stride, m, P.lq, s.flag, s.mode, s.stop, multi);
+        KCHECK();
+      }
       k_sink_fin_fast<<<grid_for(std::max(m, nl), 256, 1 << 30), 256, 0, c->stream>>>(
           s.Srow, nl, P.lp + P.row0, s.f, s.fh, s.fl, nullptr, s.csg, P.R, stride, m, P.lq, eps, s.g, s.gh, s.gl,
           s.mode, s.stop, s.dev, s.flag, kappa, cond_h, use_cond);
@@ -1581,6 +1590,7 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
     return GW_OK;
   };
   // one iteration (check: the tolerance rule's violation check of the plan after `done` iterations)
+  const int* commit_cnt = nullptr;  // graph-resident tolerance loop: the iteration count lives on the device
   auto iteration = [&](bool check, int done) -> gw_status {
     if (!check) TRY(fused_step());
     // iterations run the robust two-kernel path while *mode == 0 (decided on the device)
@@ -1595,7 +1605,8 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
     PROF_END(c, PC_SINK_ROW, 1);
     if (check) {
       TRY(sink_viol_global(c, P, s));
-      k_sink_commit<<<grid_for(nl), 256, 0, c->stream>>>(s.viol, tol, s.stop, s.ftmp, s.f, nl, s.iters, done);
+      k_sink_commit<<<grid_for(nl), 256, 0, c->stream>>>(s.viol, tol, s.stop, s.ftmp, s.f, nl, s.iters, done,
+                                                         commit_cnt);
       KCHECK();
     }
     PROF_BEGIN(c, PC_SINK_COL);
@@ -1614,7 +1625,7 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
       KCHECK();
     }
     PROF_END(c, PC_SINK_COL, 2);
-    k_sink_mode<<<1, 32, 0, c->stream>>>(s.dev, s.mode, s.fK > 0 ? 20.f : -1.f);
+    k_sink_mode<<<1, 32, 0, c->stream>>>(s.dev, s.mode, s.fK > 0 ? 20.f : -1.f, s.flag);
     KCHECK();
     return GW_OK;
   };
@@ -1801,7 +1812,7 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
               c->stream = c->cap;
             }
           }
-          k_sink_mode<<<1, 32, 0, c->stream>>>(s.dev, s.mode, 20.f);
+          k_sink_mode<<<1, 32, 0, c->stream>>>(s.dev, s.mode, 20.f, s.flag);
         }
         c->stream = saved;
         cudaGraph_t go = nullptr;
@@ -1826,6 +1837,89 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
     for (int k = 0; k < iters; ++k) CU(cudaGraphLaunch(s.gexec, c->stream));
     *used = iters;
     return GW_OK;
+  }
+  // Tolerance rule on one rank (reading R8), graph-resident: a prologue of check_every iterations, then a
+  // WHILE conditional node whose body is [the checking iteration (measure the violation of the current
+  // plan; stop, or commit the measured row update as this iteration's) + check_every - 1 iterations] and
+  // whose condition is set on the device (no stop, count below the cap): the same schedule as the host
+  // loop below, with no host synchronisation inside it.  GWDP_NO_DEVLOOP=1 keeps the host loop.
+  static const bool no_devloop = getenv("GWDP_NO_DEVLOOP") != nullptr;
+  if (tolmode && P.R == 1 && !no_graph && !no_devloop && !c->prof.on && iters >= 2 * check_every &&
+      iters % check_every == 0) {
+    int* cnt = s.mode + 3;  // iterations done (device)
+    if (!c->cap) CU(cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking));
+    if (!c->cap2) CU(cudaStreamCreateWithFlags(&c->cap2, cudaStreamNonBlocking));
+    cudaGraph_t graph = nullptr;
+    CU(cudaGraphCreate(&graph, 0));
+    cudaGraphConditionalHandle hw;
+    CU(cudaGraphConditionalHandleCreate(&hw, graph, 1, cudaGraphCondAssignDefault));
+    cudaStream_t saved = c->stream;
+    gw_status st = GW_OK;
+    cudaError_t e = cudaStreamBeginCaptureToGraph(c->cap, graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+      c->stream = c->cap;
+      k_fill_int<<<1, 32, 0, c->stream>>>(cnt, check_every);
+      for (int k = 0; k < check_every && st == GW_OK; ++k) st = iteration(false, 0);
+      if (st == GW_OK) {
+        cudaStreamCaptureStatus cs;
+        const cudaGraphNode_t* deps = nullptr;
+        size_t nd = 0;
+        cudaGraph_t cg = nullptr;
+        e = cudaStreamGetCaptureInfo(c->cap, &cs, nullptr, &cg, &deps, &nd);
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = hw;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t wn = nullptr;
+        if (e == cudaSuccess) e = cudaGraphAddNode(&wn, cg, deps, nd, &cp);
+        if (e == cudaSuccess) e = cudaStreamUpdateCaptureDependencies(c->cap, &wn, 1, cudaStreamSetCaptureDependencies);
+        if (e == cudaSuccess) {
+          e = cudaStreamBeginCaptureToGraph(c->cap2, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                            cudaStreamCaptureModeThreadLocal);
+          if (e == cudaSuccess) {
+            c->stream = c->cap2;
+            commit_cnt = cnt;
+            st = iteration(true, 0);
+            commit_cnt = nullptr;
+            for (int k = 1; k < check_every && st == GW_OK; ++k) st = iteration(false, 0);
+            k_tol_round_end<<<1, 32, 0, c->stream>>>(cnt, check_every, iters, s.stop, hw);
+            cudaGraph_t bo = nullptr;
+            const cudaError_t eb = cudaStreamEndCapture(c->cap2, &bo);
+            if (e == cudaSuccess) e = eb;
+          }
+        }
+      }
+      c->stream = saved;
+      cudaGraph_t go = nullptr;
+      const cudaError_t ee = cudaStreamEndCapture(c->cap, &go);
+      if (e == cudaSuccess) e = ee;
+    }
+    cudaGraphExec_t ex = nullptr;
+    if (st == GW_OK && e == cudaSuccess) e = cudaGraphInstantiate(&ex, graph, 0);
+    cudaGraphDestroy(graph);
+    if (st != GW_OK) {
+      if (ex) cudaGraphExecDestroy(ex);
+      return st;
+    }
+    if (e != cudaSuccess) return fail(GW_ERR_CUDA, "Sinkhorn tolerance-loop graph: %s", cudaGetErrorString(e));
+    const cudaError_t el = cudaGraphLaunch(ex, c->stream);
+    int hs[3];
+    CU(cudaMemcpyAsync(hs, s.stop, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaMemcpyAsync(hs + 1, s.iters, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaMemcpyAsync(hs + 2, cnt, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    const cudaError_t es = cudaStreamSynchronize(c->stream);
+    cudaGraphExecDestroy(ex);
+    if (el != cudaSuccess || es != cudaSuccess)
+      return fail(GW_ERR_CUDA, "Sinkhorn tolerance loop: %s", cudaGetErrorString(el != cudaSuccess ? el : es));
+    if (hs[0]) {
+      *used = hs[1];
+      *converged = 1;
+      k_split<<<grid_for(nl), 256, 0, c->stream>>>(s.f, nl, GW_LOG2E / eps, s.fh, s.fl);  // fh/fl == split(f)
+      KCHECK();
+      return GW_OK;
+    }
+    done = iters;  // the final check below
   }
   while (done < iters) {
     const int chunk = tolmode ? std::min(check_every, iters - done) : iters - done;

@@ -307,10 +307,15 @@ __global__ void k_sink_colmergefin(const float2* __restrict__ part, int nrb, int
 // 2^-100, as k_sink_fast_check) and ORs a bad row into *rowflag -- an int in the payload slot after
 // the M column sums, so the speculation flag travels in the column-sum all-gather (one collective
 // per iteration).  Rows are covered grid-stride by all threads.
+// csflag / lq (one rank): also validate the column sums here (k_sink_fast_check's column test, on the
+// columns with q > 0) and OR a failure into *csflag -- with rowflag == csflag the whole check of the
+// speculative iteration happens in this launch.
 __global__ void __launch_bounds__(256) k_sink_colsum(const double* __restrict__ part, int ncl, int64_t m,
                                                      double* __restrict__ out, const int* __restrict__ mode,
                                                      const int* __restrict__ stop, const float* __restrict__ Srow = nullptr,
-                                                     int64_t nl = 0, int* __restrict__ rowflag = nullptr) {
+                                                     int64_t nl = 0, int* __restrict__ rowflag = nullptr,
+                                                     int* __restrict__ csflag = nullptr,
+                                                     const double* __restrict__ lq = nullptr) {
   if (*mode != 1 || (stop && *stop)) return;
   __shared__ double red[8][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -328,29 +333,45 @@ __global__ void __launch_bounds__(256) k_sink_colsum(const double* __restrict__ 
     for (int c = w; c < ncl; c += 8) CS += part[(int64_t)c * m + q];
   red[w][lane] = CS;
   __syncthreads();
-  if (w == 0 && q < m) {
-    double v = 0.0;
+  if (w == 0) {
+    bool bad = false;
+    if (q < m) {
+      double v = 0.0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) v += red[k][lane];
-    out[q] = v;
+      for (int k = 0; k < 8; ++k) v += red[k][lane];
+      out[q] = v;
+      if (csflag && lq[q] != -INFINITY) bad = !(v > 7.9e-31 && v < 1e300);
+    }
+    if (csflag && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(csflag, 1);
   }
 }
 
 // Tolerance rule (reading R8): the row half-step of iteration k+1 measured the violation of
 // the plan after iteration k into *viol (written to ftmp).  If it is <= tol, stop with f
 // unchanged (iteration k+1 is discarded); otherwise commit ftmp -> f.
+// it_dev (nullable): the iteration count before this check, read from the device (graph-resident loop)
 __global__ void k_sink_commit(const float* __restrict__ viol, double tol, int* __restrict__ stop,
                               const double* __restrict__ ftmp, double* __restrict__ f, int64_t nl,
-                              int* __restrict__ iters, int it_before) {
+                              int* __restrict__ iters, int it_before, const int* __restrict__ it_dev = nullptr) {
   if (*stop) return;
   const bool done = (double)(*viol) <= tol;
   __syncthreads();
   if (done) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) { *stop = 1; *iters = it_before; }
+    if (blockIdx.x == 0 && threadIdx.x == 0) { *stop = 1; *iters = it_dev ? *it_dev : it_before; }
     return;
   }
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nl; i += (int64_t)gridDim.x * blockDim.x)
     f[i] = ftmp[i];
+}
+
+// End of one round of the graph-resident tolerance loop (reading R8): `step` more iterations done;
+// loop again unless the tolerance stopped the solve or the cap is reached (a device flag, no host sync).
+__global__ void k_tol_round_end(int* __restrict__ cnt, int step, int cap, const int* __restrict__ stop,
+                                cudaGraphConditionalHandle h) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    *cnt += step;
+    cudaGraphSetConditional(h, (!*stop && *cnt < cap) ? 1u : 0u);
+  }
 }
 
 }  // namespace gw
