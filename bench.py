@@ -321,6 +321,10 @@ def main():
     grad = {"ms_per_gradient": grad_ms, "algorithmic_bytes": 12 * nm_bytes,
             "GBps_algorithmic": 12 * nm_bytes / (grad_ms / 1e3) / 1e9,
             "frac_of_peak": 12 * nm_bytes / (grad_ms / 1e3) / 1e9 / hbm,
+            "frac_of_peak_at_8NM": 8 * nm_bytes / (grad_ms / 1e3) / 1e9 / hbm,
+            "bytes_note": "12NM is the floor of the exact gradient on the solver path (the row totals of T^l exist "
+                          "only after a read of the final plan: DESIGN.md 5.2b); frac_of_peak_at_8NM is SURVEY 8(d)'s "
+                          "accounting, which assumes the rank-2 term deferred into every Sinkhorn sweep",
             "note": "moments pass (4NM) + main pass (8NM: read T or the cost it is regenerated from, write G); "
                     "averaged over the solve's gradients, the first of which is on the product plan p q^T "
                     "(no plan read), so this slightly flatters the Gibbs-mode gradient"}

@@ -60,6 +60,36 @@ def main():
         ms = e0.elapsed_time(e1) / 3
         nm = float(side) ** 4
         print("grid2d %dx%d gradient %.3f ms, %.0f GB/s over 8NM" % (side, side, ms, 8 * nm / ms / 1e6))
+    elif case == "ugw":
+        # UGW at 16384^2 (rho = 1, eps = 1e-2, 2 outer x 50 inner): graph path vs instrumented breakdown
+        import ctypes as C
+        from paper_2404_08970_b200 import _lib
+        x3, y3 = np.sort(rng.random(n)), np.sort(rng.random(n))
+        u3 = rng.random(n) + 0.5
+        u3 /= u3.sum()
+        v3 = rng.random(n) + 0.5
+        v3 *= 1.3 / v3.sum()
+        ctx = api.Context.get(dev)
+        api.ugw_solve(x3, y3, u3, v3, 1.0, 1e-2, 2, 50, device=dev)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        r = api.ugw_solve(x3, y3, u3, v3, 1.0, 1e-2, 2, 50, device=dev)
+        e1.record()
+        torch.cuda.synchronize()
+        print("ugw graph path: %.3f ms, fused %d" % (e0.elapsed_time(e1), r.inner_fused_total))
+        lib = _lib.load()
+        ms_c = (C.c_double * 8)()
+        cnt_c = (C.c_int64 * 8)()
+        _lib.check(lib.gw_ctx_profile(ctx.h, 2, None, None, 0))
+        e0.record()
+        api.ugw_solve(x3, y3, u3, v3, 1.0, 1e-2, 2, 50, device=dev)
+        e1.record()
+        torch.cuda.synchronize()
+        _lib.check(lib.gw_ctx_profile(ctx.h, 0, C.cast(ms_c, C.c_void_p), C.cast(cnt_c, C.c_void_p), 8))
+        names = ["grad_moments", "grad_carry", "grad_main", "sink_row", "sink_col", "sink_fused", "objective"]
+        print("ugw instrumented: %.3f ms; classes: %s" % (e0.elapsed_time(e1),
+              {nm: round(ms_c[i], 3) for i, nm in enumerate(names)}))
     else:
         raise SystemExit("unknown case %s" % case)
     torch.cuda.synchronize()
