@@ -1028,8 +1028,8 @@ static gw_status gk_main_launch(gw_ctx* c, dim3 grid, const TSrc2& S2, int64_t n
                                 const double* ct, const double* cl, const double* c2, double alpha, const double* fx,
                                 const double* fy, float* G, int64_t ldG, double* tob, const double* carry) {
   auto kern = k_gk_main<K, MODE, STORE, OBJ, FGW>;
-  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gk_smem_bytes()));
-  kern<<<grid, GK, gk_smem_bytes(), c->stream>>>(S2, nl, m, xl, yc, rp, rt, Z, ct, cl, c2, alpha, fx, fy, G, ldG,
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gk_smem_bytes<K>()));
+  kern<<<grid, GK, gk_smem_bytes<K>(), c->stream>>>(S2, nl, m, xl, yc, rp, rt, Z, ct, cl, c2, alpha, fx, fy, G, ldG,
                                                     tob, carry);
   KCHECK();
   return GW_OK;
@@ -1059,7 +1059,7 @@ template <int K, int MODE>
 static gw_status grad_pass_gk_mode(gw_ctx* c, const Prepared& P, const TSrc2& S2, float* G, int64_t ldG, bool store,
                                    bool obj, const double* fx, const double* fy, double alpha, double* objout_dev) {
   const int64_t nl = P.nl, m = P.m;
-  const int ntc = (int)((m + GK - 1) / GK), ntr = (int)((nl + GK - 1) / GK);
+  const int ntc = (int)((m + GR - 1) / GR), ntr = (int)((nl + GR - 1) / GR);  // regions (polyk.cuh)
   const size_t K1 = K + 1;
   double *rp, *rt, *cp, *Z, *ct, *ctt, *tob;
   TRY(ws(c, c->gkrp, (size_t)ntc * K1 * nl, &rp)); TRY(ws(c, c->gkrt, K1 * nl, &rt));
@@ -1070,8 +1070,8 @@ static gw_status grad_pass_gk_mode(gw_ctx* c, const Prepared& P, const TSrc2& S2
   const dim3 grid((unsigned)ntc, (unsigned)ntr);
   PROF_BEGIN(c, PC_GRAD_MOMENTS);
   auto ks = k_gk_sums<K, MODE>;
-  CU(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gk_smem_bytes()));
-  ks<<<grid, GK, gk_smem_bytes(), c->stream>>>(S2, nl, m, xl, P.yc, rp, cp);
+  CU(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gk_smem_bytes<K>()));
+  ks<<<grid, GK, gk_smem_bytes<K>(), c->stream>>>(S2, nl, m, xl, P.yc, rp, cp);
   KCHECK();
   PROF_END(c, PC_GRAD_MOMENTS, 1);
   PROF_BEGIN(c, PC_GRAD_CARRY);

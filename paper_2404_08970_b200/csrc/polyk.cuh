@@ -11,14 +11,14 @@
 // gap-shifted binomial states: on centred supports every term of the recombination is O(width^k)
 // (bounded cancellation), and every state and product is fp64.
 //
-// D_X T D_Y on GK x GK tiles:
-//   k_gk_sums   per tile: row power sums (weights y^r) and column power sums (weights x^r) of T;
-//   carries     exclusive prefix over column tiles per row (k_gk_scan_tiles); the column power sums of
-//               W = T D_Y over row tiles are D_Y applied to T's column power sums (k_gk_apply on
-//               (N/GK)(k+1) vectors of length M), then an exclusive prefix over row tiles;
-//   k_gk_main   the tile in shared memory: a thread-per-row scan forms W (fp32, in place), then a
+// D_X T D_Y on GR x GR regions (one CTA each, staged through shared memory as 2 x 2 tiles of GK x GK):
+//   k_gk_sums   per region: row power sums (weights y^r) and column power sums (weights x^r) of T;
+//   carries     exclusive prefix over column regions per row (k_gk_scan_tiles); the column power sums
+//               of W = T D_Y over row regions are D_Y applied to T's column power sums (k_gk_apply on
+//               (N/GR)(k+1) vectors of length M), then an exclusive prefix over row regions;
+//   k_gk_main   per tile in shared memory: a thread-per-row scan forms W (fp32, in place), then a
 //               thread-per-column scan forms V = D_X W and G = 2c + 2c' - 4V (coalesced stores).
-// Bytes: 2 reads + 1 write of the N x M matrix, plus ~3 (k+1) N M / GK fp64 carries.
+// Bytes: 2 reads + 1 write of the N x M matrix, plus ~3 (k+1) N M / GR fp64 carries.
 #pragma once
 #include "common.cuh"
 #include "fused.cuh"  // ex2_ftz
@@ -66,44 +66,73 @@ __device__ __forceinline__ void gk_powers(double s, double* pw, double* cf, int 
 template <int K>
 __device__ __forceinline__ double gk_kappa(int r) { return ((r & 1) ? -1.0 : 1.0) * gk_binom(K, r); }
 
-// acc_r += v s^r  (r = 0..K)
+// Tile-centred fp32 arithmetic.  Inside a GK x GK tile every power and every state is taken about the
+// centre of the tile's own coordinate range (cx: the tile's rows, cy: its columns), so |x - cx| is at
+// most half the tile's width: the recombination sum_j a_j s^j of a tile-centred polynomial has no
+// cancellation beyond the terms' own size (a_0 = the value at the centre dominates), and fp32 state +
+// fp32 FFMA give errors of a few fp32 ulps of (width^k x mass), far inside the gradient tolerance.  The
+// cross-tile carries stay in fp64 about the global centre; each thread converts them to its tile's
+// centre once per tile (a Taylor shift, O(k^2) fp64 operations per row or column per tile).
+//
+// per-coordinate table stride in floats (K + 1 values, padded for 8-B / 16-B shared loads)
 template <int K>
-__device__ __forceinline__ void gk_accum(double (&acc)[K + 1], double v, double s) {
+__host__ __device__ constexpr int gk_kp() { return (K + 1 + 1) & ~1; }
+
+// dynamic smem: the fp32 tile [GK][GKQ] first (16-B aligned), then one fp32 table [GK][KP] (rebuilt
+// between the row and the column pass) and five fp32 per-coordinate vectors [GK]; with the static
+// shared memory at most 73.5 KB (k = 5): three CTAs per SM
+template <int K>
+constexpr size_t gk_smem_bytes() { return sizeof(float) * (GK * GKQ + GK * gk_kp<K>() + 5 * GK); }
+
+// Taylor shift in fp64: c[0..K] ascending coefficients of P(y) -> those of P(c + s) in s
+template <int K>
+__device__ __forceinline__ void gk_shift(double (&a)[K + 1], double c) {
 #pragma unroll
-  for (int r = 0; r <= K; ++r) {
-    acc[r] += v;
-    v *= s;
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = K - 1; j >= i; --j) a[j] = fma(c, a[j + 1], a[j]);
+}
+
+// KP consecutive fp32 table entries (16-B loads when KP % 4 == 0, else 8-B)
+template <int KP>
+__device__ __forceinline__ void gk_ld_tab(const float* p, float (&v)[KP]) {
+  if constexpr (KP % 4 == 0) {
+#pragma unroll
+    for (int i = 0; i < KP; i += 4) {
+      const float4 t = *reinterpret_cast<const float4*>(p + i);
+      v[i] = t.x; v[i + 1] = t.y; v[i + 2] = t.z; v[i + 3] = t.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < KP; i += 2) {
+      const float2 t = *reinterpret_cast<const float2*>(p + i);
+      v[i] = t.x; v[i + 1] = t.y;
+    }
   }
 }
-// sum_r h~_r s^{K-r}
+
+// sum_j a_j s^j (fp32 Horner)
 template <int K>
-__device__ __forceinline__ double gk_horner(const double (&h)[K + 1], double s) {
-  double v = h[0];
+__device__ __forceinline__ float gk_horner_f(const float (&a)[K + 1], float s) {
+  float v = a[K];
 #pragma unroll
-  for (int r = 1; r <= K; ++r) v = fma(v, s, h[r]);
+  for (int j = K - 1; j >= 0; --j) v = fmaf(v, s, a[j]);
   return v;
 }
-// h~_r += kappa_r v s^r
-template <int K>
-__device__ __forceinline__ void gk_update(double (&h)[K + 1], double v, double s) {
-#pragma unroll
-  for (int r = 0; r <= K; ++r) {
-    h[r] = fma(gk_kappa<K>(r), v, h[r]);
-    v *= s;
-  }
+
+// centre of the sorted coordinates v[i0 .. i0 + cnt) (0 for an empty range)
+__device__ __forceinline__ double gk_centre(const double* __restrict__ v, int64_t i0, int cnt) {
+  return cnt > 0 ? 0.5 * (v[i0] + v[i0 + cnt - 1]) : 0.0;
 }
 
-// dynamic smem: the fp32 tile [GK][GKQ] first (16-B aligned), then fp64 per-row / per-column values
-constexpr size_t gk_smem_bytes() { return sizeof(float) * GK * GKQ + sizeof(double) * 4 * GK; }
-
 // The plan tile [r0, r0 + GK) x [c0, c0 + GK) into shared memory, zero outside the matrix.  EXPLICIT /
-// GIBBS: one bulk copy (cp.async.bulk, complete_tx on an mbarrier) per row, so the whole 64 KB tile is
-// in flight at once; then each thread regenerates its column in place (GIBBS: the same fp32
-// expression as every other pass).  PRODUCT: p_i q_q directly.
+// GIBBS: one bulk copy (cp.async.bulk, complete_tx on the mbarrier `bar`, phase `parity`) per row, so
+// the whole 64 KB tile is in flight at once; then each thread regenerates its column in place (GIBBS:
+// the same fp32 expression as every other pass).  PRODUCT: p_i q_q directly.  The caller has passed a
+// barrier after every thread's last access to `tile` (and fenced its generic writes to the async proxy).
 template <int MODE>
 __device__ __forceinline__ void gk_load_tile(const TSrc2& S, int64_t nl, int64_t m, int64_t r0, int64_t c0,
-                                             float* tile) {
-  __shared__ uint64_t bar;
+                                             float* tile, uint64_t* bar, uint32_t parity) {
   __shared__ float fhs[GK], fls[GK];
   const int t = threadIdx.x;
   const int rows = (int)(nl - r0 < GK ? nl - r0 : GK);
@@ -112,28 +141,30 @@ __device__ __forceinline__ void gk_load_tile(const TSrc2& S, int64_t nl, int64_t
   if (MODE == T_GIBBS) fls[t] = t < rows ? S.fl[r0 + t] : 0.f;
   if (MODE != T_PRODUCT) {
     const uint32_t rb = 4u * (uint32_t)((cols + 3) & ~3);  // ld % 4 == 0: stays inside the row
-    if (t == 0) {
-      mbar_init(&bar, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      mbar_expect_tx(&bar, rb * (uint32_t)rows);
-    }
+    if (t == 0) mbar_expect_tx(bar, rb * (uint32_t)rows);
     __syncthreads();
-    if (t < rows) tma_load_1d(tile + t * GKQ, S.T + (r0 + t) * S.ld + c0, rb, &bar);
-    mbar_wait(&bar, 0);
+    if (t < rows) tma_load_1d(tile + t * GKQ, S.T + (r0 + t) * S.ld + c0, rb, bar);
+    mbar_wait(bar, parity);
   } else {
     __syncthreads();
   }
   const bool qv = t < cols;
+  if (MODE == T_EXPLICIT) {
+    // the bulk copies filled [0, rows) x [0, 4 ceil(cols / 4)); only a ragged tile has entries to zero
+    if (rows < GK || cols < GK) {
+      for (int rr = 0; rr < GK; ++rr)
+        if (!qv || rr >= rows) tile[rr * GKQ + t] = 0.f;
+    }
+    return;
+  }
   float gq = 0.f, glq = 0.f;
-  if (qv && MODE != T_EXPLICIT) gq = S.gh[c0 + t];
+  if (qv) gq = S.gh[c0 + t];
   if (qv && MODE == T_GIBBS) glq = S.gl[c0 + t];
 #pragma unroll 4
   for (int rr = 0; rr < GK; ++rr) {
     float v = 0.f;
     if (qv && rr < rows) {
-      if (MODE == T_EXPLICIT) {
-        v = tile[rr * GKQ + t];
-      } else if (MODE == T_PRODUCT) {
+      if (MODE == T_PRODUCT) {
         v = fhs[rr] * gq;
       } else {
         const float g = tile[rr * GKQ + t];
@@ -144,41 +175,130 @@ __device__ __forceinline__ void gk_load_tile(const TSrc2& S, int64_t nl, int64_t
   }
 }
 
-// Pass 1: per tile (blockIdx.x = column tile, blockIdx.y = row tile)
-//   colpart[ty][r][q] = sum_{i in tile rows} x_i^r T_iq,   rowpart[tx][r][i] = sum_{q in tile cols} y_q^r T_iq
+// A CTA owns a GR x GR region (2 x 2 tiles of GK x GK, staged through shared memory one tile at a
+// time): the carries between CTAs are per region, half as many as per tile, and the states are taken
+// about the region's centres (|x - cx| <= half the region's width).
+constexpr int GR = 2 * GK;
+
+// before a tile buffer is refilled: generic-proxy writes to it ordered before the async-proxy (TMA)
+// writes, and every thread past its last read
+__device__ __forceinline__ void gk_tile_release() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+}
+
+// sum_j C(r,j) c^{r-j} d_j for r = 0..K (the power sums of the centred coordinates about 0)
+template <int K>
+__device__ __forceinline__ void gk_uncentre(const float (&u)[K + 1], double c, double (&o)[K + 1]) {
+#pragma unroll
+  for (int r = 0; r <= K; ++r) {
+    double v = 0.0, cp = 1.0;
+#pragma unroll
+    for (int j = r; j >= 0; --j) {
+      v = fma(gk_binom(r, j) * cp, (double)u[j], v);
+      cp *= c;
+    }
+    o[r] = v;
+  }
+}
+
+// Pass 1: per region (blockIdx.x = column region, blockIdx.y = row region)
+//   colpart[ry][r][q] = sum_{i in region rows} x_i^r T_iq,   rowpart[rx][r][i] = sum_{q in region cols} y_q^r T_iq
+// (global centred coordinates, fp64), accumulated in fp32 about the region's centres and shifted back:
+//   sum_i x_i^r T_iq = sum_j C(r,j) cx^{r-j} U_j,  U_j = sum_i (x_i - cx)^j T_iq.
 template <int K, int MODE>
 __global__ void __launch_bounds__(GK) k_gk_sums(TSrc2 S, int64_t nl, int64_t m, const double* __restrict__ xl,
                                                 const double* __restrict__ yc, double* __restrict__ rowpart,
                                                 double* __restrict__ colpart) {
+  constexpr int KP = gk_kp<K>();
   extern __shared__ float4 gk_smem[];
-  float* tile = reinterpret_cast<float*>(gk_smem);            // [GK][GKQ]
-  double* xs = reinterpret_cast<double*>(tile + GK * GKQ);    // [GK] x of the tile's rows
-  double* ys = xs + GK;                                       // [GK] y of the tile's columns
+  __shared__ uint64_t bar;
+  float* tile = reinterpret_cast<float*>(gk_smem);  // [GK][GKQ]
+  float* pwt = tile + GK * GKQ;                      // [GK][KP] (x_i - cx)^j, then (y_q - cy)^j
   const int t = threadIdx.x;
-  const int64_t r0 = (int64_t)blockIdx.y * GK, c0 = (int64_t)blockIdx.x * GK;
-  xs[t] = r0 + t < nl ? xl[r0 + t] : 0.0;
-  ys[t] = c0 + t < m ? yc[c0 + t] : 0.0;
-  gk_load_tile<MODE>(S, nl, m, r0, c0, tile);
-  __syncthreads();
-  double U[K + 1];
-#pragma unroll
-  for (int r = 0; r <= K; ++r) U[r] = 0.0;
-  for (int rr = 0; rr < GK; ++rr) gk_accum<K>(U, (double)tile[rr * GKQ + t], xs[rr]);
-  if (c0 + t < m)
-#pragma unroll
-    for (int r = 0; r <= K; ++r) colpart[((int64_t)blockIdx.y * (K + 1) + r) * m + c0 + t] = U[r];
-#pragma unroll
-  for (int r = 0; r <= K; ++r) U[r] = 0.0;
-  for (int c = 0; c < GK; c += 4) {
-    const float4 t4 = *reinterpret_cast<const float4*>(tile + t * GKQ + c);
-    gk_accum<K>(U, (double)t4.x, ys[c]);
-    gk_accum<K>(U, (double)t4.y, ys[c + 1]);
-    gk_accum<K>(U, (double)t4.z, ys[c + 2]);
-    gk_accum<K>(U, (double)t4.w, ys[c + 3]);
+  const int64_t R0 = (int64_t)blockIdx.y * GR, C0 = (int64_t)blockIdx.x * GR;
+  const double cx = gk_centre(xl, R0, (int)min((int64_t)GR, nl - R0));
+  const double cy = gk_centre(yc, C0, (int)min((int64_t)GR, m - C0));
+  if (t == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (r0 + t < nl)
+  auto powers = [&](float sv) {
+    float pv = 1.f;
 #pragma unroll
-    for (int r = 0; r <= K; ++r) rowpart[((int64_t)blockIdx.x * (K + 1) + r) * nl + r0 + t] = U[r];
+    for (int j = 0; j < KP; ++j) {
+      pwt[t * KP + j] = j <= K ? pv : 0.f;
+      pv *= sv;
+    }
+  };
+  float U[2][K + 1];  // column sums of the two column tiles, over both row tiles
+#pragma unroll
+  for (int cs = 0; cs < 2; ++cs)
+#pragma unroll
+    for (int j = 0; j <= K; ++j) U[cs][j] = 0.f;
+  uint32_t ph = 0;
+#pragma unroll
+  for (int rs = 0; rs < 2; ++rs) {
+    const int64_t r0 = R0 + rs * GK;
+    if (r0 >= nl) break;  // uniform
+    const int rows = (int)min((int64_t)GK, nl - r0);
+    float R[K + 1];  // row sums of row r0 + t over both column tiles
+#pragma unroll
+    for (int j = 0; j <= K; ++j) R[j] = 0.f;
+#pragma unroll
+    for (int cs = 0; cs < 2; ++cs) {
+      const int64_t c0 = C0 + cs * GK;
+      if (c0 >= m) break;  // uniform
+      const int cols = (int)min((int64_t)GK, m - c0);
+      gk_tile_release();
+      powers(t < rows ? (float)(xl[r0 + t] - cx) : 0.f);
+      gk_load_tile<MODE>(S, nl, m, r0, c0, tile, &bar, ph);
+      if (MODE != T_PRODUCT) ph ^= 1u;
+      __syncthreads();
+      // thread = column t: U_j += sum_rr (x_rr - cx)^j T[rr][t]
+#pragma unroll 4
+      for (int rr = 0; rr < GK; ++rr) {
+        float pw[KP];
+        gk_ld_tab<KP>(pwt + rr * KP, pw);
+        const float v = tile[rr * GKQ + t];
+#pragma unroll
+        for (int j = 0; j <= K; ++j) U[cs][j] = fmaf(v, pw[j], U[cs][j]);
+      }
+      __syncthreads();
+      powers(t < cols ? (float)(yc[c0 + t] - cy) : 0.f);
+      __syncthreads();
+      // thread = row t: R_j += sum_c (y_c - cy)^j T[t][c]
+      const float* trow = tile + t * GKQ;
+#pragma unroll 2
+      for (int cc = 0; cc < GK; cc += 4) {
+        const float4 t4 = *reinterpret_cast<const float4*>(trow + cc);
+        const float tv[4] = {t4.x, t4.y, t4.z, t4.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float pw[KP];
+          gk_ld_tab<KP>(pwt + (cc + e) * KP, pw);
+#pragma unroll
+          for (int j = 0; j <= K; ++j) R[j] = fmaf(tv[e], pw[j], R[j]);
+        }
+      }
+    }
+    if (t < rows) {
+      double o[K + 1];
+      gk_uncentre<K>(R, cy, o);
+#pragma unroll
+      for (int r = 0; r <= K; ++r) rowpart[((int64_t)blockIdx.x * (K + 1) + r) * nl + r0 + t] = o[r];
+    }
+  }
+#pragma unroll
+  for (int cs = 0; cs < 2; ++cs) {
+    const int64_t q = C0 + cs * GK + t;
+    if (q < m) {
+      double o[K + 1];
+      gk_uncentre<K>(U[cs], cx, o);
+#pragma unroll
+      for (int r = 0; r <= K; ++r) colpart[((int64_t)blockIdx.y * (K + 1) + r) * m + q] = o[r];
+    }
+  }
 }
 
 // In-place exclusive prefix over the tile index of part[nt][len2] (fixed order); totals -> tot[len2].
@@ -339,11 +459,15 @@ __global__ void __launch_bounds__(256) k_gk_apply(const double* __restrict__ U, 
 }
 
 // Pass 2: G = alpha (2c 1^T + 2 1 c'^T - 4 D_X T D_Y) [+ (1 - alpha)(fx_i - fy_q)^2]  (STORE)
-// and / or the tile's <D_X T D_Y, T> (OBJ -> tile_obj[tile]).
-//   rowpre[tx][r][i], rowtot[r][i]: power sums of row i over the columns before tile tx / all columns
-//   colpre[ty][r][q], coltot[r][q]: power sums (weights x^r) of column q of W = T D_Y over the rows
-//                                   before row tile ty (this rank) / all rows (all ranks)
+// and / or the region's <D_X T D_Y, T> (OBJ -> tile_obj[region]).
+//   rowpre[rx][r][i], rowtot[r][i]: power sums of row i over the columns before region rx / all columns
+//   colpre[ry][r][q], coltot[r][q]: power sums (weights x^r) of column q of W = T D_Y over the rows
+//                                   before row region ry (this rank) / all rows (all ranks)
 //   colcarry[r][q] (nullable): the same sums over the rows of the ranks above
+// Each thread turns its fp64 carry polynomial sum_r h_r y^{K-r} into fp32 coefficients a_j about the
+// region's centre (gk_shift), then walks the region's two tiles in order: W = sum_j a_j s^j, and (odd
+// k) crossing column c flips that column's sign: a_j += 2 T_c C(K,j) (-s_c)^{K-j}  (the table tab[c][j]).
+// The column states of both column tiles stay in registers from the upper row tile to the lower one.
 template <int K, int MODE, bool STORE, bool OBJ, bool FGW>
 __global__ void __launch_bounds__(GK) k_gk_main(TSrc2 S, int64_t nl, int64_t m, const double* __restrict__ xl,
                                                 const double* __restrict__ yc, const double* __restrict__ rowpre,
@@ -353,76 +477,147 @@ __global__ void __launch_bounds__(GK) k_gk_main(TSrc2 S, int64_t nl, int64_t m, 
                                                 const double* __restrict__ fx, const double* __restrict__ fy,
                                                 float* __restrict__ G, int64_t ldG, double* __restrict__ tile_obj,
                                                 const double* __restrict__ colcarry) {
-  extern __shared__ float4 gk_smem[];
-  float* tile = reinterpret_cast<float*>(gk_smem);          // [GK][GKQ]
-  double* xs = reinterpret_cast<double*>(tile + GK * GKQ);  // x of the tile's rows
-  double* ys = xs + GK;                                     // y of the tile's columns
-  double* crow = ys + GK;                                   // 2 alpha c_i
-  double* frow = crow + GK;                                 // fx_i
+  constexpr int KP = gk_kp<K>();
   constexpr bool ODD = K & 1;
+  extern __shared__ float4 gk_smem[];
+  __shared__ uint64_t bar;
+  float* tile = reinterpret_cast<float*>(gk_smem);  // [GK][GKQ]
+  float* tab = tile + GK * GKQ;                      // [GK][KP] crossing table: columns, then rows
+  float* sys = tab + GK * KP;                        // [GK] y_q - cy
+  float* sxs = sys + GK;                             // [GK] x_i - cx
+  float2* sxc = reinterpret_cast<float2*>(sxs + GK);  // [GK] {x_i - cx, 2 alpha c_i} (8-B aligned)
+  float* fxs = sxs + 3 * GK;                         // [GK] fx_i (FGW)
   const int t = threadIdx.x;
-  const int64_t r0 = (int64_t)blockIdx.y * GK, c0 = (int64_t)blockIdx.x * GK;
-  const int64_t i_t = r0 + t, q = c0 + t;
-  xs[t] = i_t < nl ? xl[i_t] : 0.0;
-  ys[t] = q < m ? yc[q] : 0.0;
-  crow[t] = i_t < nl ? 2.0 * alpha * cl[i_t] : 0.0;
-  frow[t] = (FGW && i_t < nl) ? fx[i_t] : 0.0;
-  gk_load_tile<MODE>(S, nl, m, r0, c0, tile);
-  __syncthreads();
-  // thread = row: W_iq = sum_r kappa_r y_q^{K-r} h_r,  h_r = 2 S_r^<(q) - S_r (odd k) or S_r (even k)
-  if (i_t < nl) {
-    double h[K + 1];
-#pragma unroll
-    for (int r = 0; r <= K; ++r) {
-      const double tt = rowtot[(int64_t)r * nl + i_t];
-      h[r] = gk_kappa<K>(r) * (ODD ? 2.0 * rowpre[((int64_t)blockIdx.x * (K + 1) + r) * nl + i_t] - tt : tt);
-    }
-    float* trow = tile + t * GKQ;
-    for (int c = 0; c < GK; c += 4) {
-      const float4 t4 = *reinterpret_cast<const float4*>(trow + c);
-      const double tv[4] = {(double)t4.x, (double)t4.y, (double)t4.z, (double)t4.w};
-      float wo[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const double y = ys[c + e];
-        wo[e] = (float)gk_horner<K>(h, y);
-        if (ODD) gk_update<K>(h, 2.0 * tv[e], y);
-      }
-      *reinterpret_cast<float4*>(trow + c) = make_float4(wo[0], wo[1], wo[2], wo[3]);
-    }
+  const int64_t R0 = (int64_t)blockIdx.y * GR, C0 = (int64_t)blockIdx.x * GR;
+  const double cx = gk_centre(xl, R0, (int)min((int64_t)GR, nl - R0));
+  const double cy = gk_centre(yc, C0, (int)min((int64_t)GR, m - C0));
+  if (t == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();
-  // thread = column: V_iq = sum_r kappa_r x_i^{K-r} h'_r,  h'_r from the column power sums of W
-  double acc = 0.0;
-  if (q < m) {
-    double h[K + 1];
+  auto crossing = [&](float sv) {  // 2 C(K,j) (-s)^{K-j}
 #pragma unroll
-    for (int r = 0; r <= K; ++r) {
-      const double tt = coltot[(int64_t)r * m + q];
-      double pre = colpre[((int64_t)blockIdx.y * (K + 1) + r) * m + q];
-      if (colcarry) pre += colcarry[(int64_t)r * m + q];  // rows of the ranks above
-      h[r] = gk_kappa<K>(r) * (ODD ? 2.0 * pre - tt : tt);
+    for (int j = 0; j < KP; ++j) {
+      float v = 0.f;
+      if (j <= K) {
+        v = (float)(2.0 * gk_binom(K, j));
+        for (int e = j; e < K; ++e) v *= -sv;
+      }
+      tab[t * KP + j] = v;
     }
-    const double c2q = 2.0 * alpha * c2[q];
-    const double fyq = FGW ? fy[q] : 0.0;
-    const double a4 = -4.0 * alpha, a1 = 1.0 - alpha;
-    float gq = 0.f, glq = 0.f;
-    if (OBJ && MODE != T_EXPLICIT) gq = S.gh[q];
-    if (OBJ && MODE == T_GIBBS) glq = S.gl[q];
-    const int rows = (int)(nl - r0 < GK ? nl - r0 : GK);
-    for (int rr = 0; rr < rows; ++rr) {
-      const double x = xs[rr];
-      const double v = gk_horner<K>(h, x);
-      if (ODD) gk_update<K>(h, 2.0 * (double)tile[rr * GKQ + t], x);
-      const int64_t i = r0 + rr;
-      if (OBJ) acc = fma(v, (double)gk_regen<MODE>(S, i, q, gq, glq), acc);
-      if (STORE) {
-        double g = fma(a4, v, crow[rr] + c2q);
-        if (FGW) {
-          const double d = frow[rr] - fyq;
-          g = fma(a1 * d, d, g);
+  };
+  const float a4 = (float)(-4.0 * alpha), a1 = (float)(1.0 - alpha);
+  float b[2][K + 1];  // column states of the two column tiles
+  double acc = 0.0;
+  uint32_t ph = 0;
+#pragma unroll
+  for (int rs = 0; rs < 2; ++rs) {
+    const int64_t r0 = R0 + rs * GK;
+    if (r0 >= nl) break;  // uniform
+    const int rows = (int)min((int64_t)GK, nl - r0);
+    const int64_t i_t = r0 + t;
+    float a[K + 1];  // row state of row r0 + t
+#pragma unroll
+    for (int cs = 0; cs < 2; ++cs) {
+      const int64_t c0 = C0 + cs * GK;
+      if (c0 >= m) break;  // uniform
+      const int cols = (int)min((int64_t)GK, m - c0);
+      const int64_t q = c0 + t;
+      gk_tile_release();
+      {
+        const float sx = t < rows ? (float)(xl[i_t] - cx) : 0.f;
+        const float sy = t < cols ? (float)(yc[q] - cy) : 0.f;
+        sxs[t] = sx;
+        sys[t] = sy;
+        sxc[t] = make_float2(sx, t < rows ? (float)(2.0 * alpha * cl[i_t]) : 0.f);
+        if (FGW) fxs[t] = t < rows ? (float)fx[i_t] : 0.f;
+        if (ODD) crossing(sy);
+      }
+      gk_load_tile<MODE>(S, nl, m, r0, c0, tile, &bar, ph);
+      if (MODE != T_PRODUCT) ph ^= 1u;
+      __syncthreads();
+      // thread = row: W_iq for the tile's columns, in place
+      if (t < rows) {
+        if (cs == 0) {
+          double h[K + 1];  // ascending in y: P(y) = sum_d h_d y^d, h_d = kappa_{K-d} (2 S^<_{K-d} - S_{K-d})
+#pragma unroll
+          for (int d = 0; d <= K; ++d) {
+            const int r = K - d;
+            const double tt = rowtot[(int64_t)r * nl + i_t];
+            h[d] = gk_kappa<K>(r) * (ODD ? 2.0 * rowpre[((int64_t)blockIdx.x * (K + 1) + r) * nl + i_t] - tt : tt);
+          }
+          gk_shift<K>(h, cy);
+#pragma unroll
+          for (int j = 0; j <= K; ++j) a[j] = (float)h[j];
         }
-        G[i * ldG + q] = (float)g;
+        float* trow = tile + t * GKQ;
+#pragma unroll 2
+        for (int cc = 0; cc < GK; cc += 4) {
+          const float4 t4 = *reinterpret_cast<const float4*>(trow + cc);
+          const float tv[4] = {t4.x, t4.y, t4.z, t4.w};
+          float wo[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            wo[e] = gk_horner_f<K>(a, sys[cc + e]);
+            if (ODD) {
+              float tb[KP];
+              gk_ld_tab<KP>(tab + (cc + e) * KP, tb);
+#pragma unroll
+              for (int j = 0; j <= K; ++j) a[j] = fmaf(tv[e], tb[j], a[j]);
+            }
+          }
+          *reinterpret_cast<float4*>(trow + cc) = make_float4(wo[0], wo[1], wo[2], wo[3]);
+        }
+      }
+      __syncthreads();
+      if (ODD) {
+        crossing(sxs[t]);
+        __syncthreads();
+      }
+      // thread = column: V_iq = D_X W over the tile's rows, G
+      if (t < cols) {
+        if (rs == 0) {
+          double h[K + 1];
+#pragma unroll
+          for (int d = 0; d <= K; ++d) {
+            const int r = K - d;
+            const double tt = coltot[(int64_t)r * m + q];
+            double pre = colpre[((int64_t)blockIdx.y * (K + 1) + r) * m + q];
+            if (colcarry) pre += colcarry[(int64_t)r * m + q];  // rows of the ranks above
+            h[d] = gk_kappa<K>(r) * (ODD ? 2.0 * pre - tt : tt);
+          }
+          gk_shift<K>(h, cx);
+#pragma unroll
+          for (int j = 0; j <= K; ++j) b[cs][j] = (float)h[j];
+        }
+        const float c2q = (float)(2.0 * alpha * c2[q]);
+        const float fyq = FGW ? (float)fy[q] : 0.f;
+        float gq = 0.f, glq = 0.f;
+        if (OBJ && MODE != T_EXPLICIT) gq = S.gh[q];
+        if (OBJ && MODE == T_GIBBS) glq = S.gl[q];
+        float* gp = G + r0 * ldG + q;
+#pragma unroll 2
+        for (int rr = 0; rr < rows; ++rr, gp += ldG) {
+          const float2 xc = sxc[rr];
+          const float v = gk_horner_f<K>(b[cs], xc.x);
+          if (ODD) {
+            float tb[KP];
+            gk_ld_tab<KP>(tab + rr * KP, tb);
+            const float w = tile[rr * GKQ + t];
+#pragma unroll
+            for (int j = 0; j <= K; ++j) b[cs][j] = fmaf(w, tb[j], b[cs][j]);
+          }
+          if (OBJ) acc = fma((double)v, (double)gk_regen<MODE>(S, r0 + rr, q, gq, glq), acc);
+          if (STORE) {
+            // the constant 2 alpha (c_i + c'_q) in fp32: one rounding of a term no larger than ~max|G|
+            float g = fmaf(a4, v, xc.y + c2q);
+            if (FGW) {
+              const float d = fxs[rr] - fyq;
+              g = fmaf(a1 * d, d, g);
+            }
+            __stcs(gp, g);
+          }
+        }
       }
     }
   }

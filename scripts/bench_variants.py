@@ -51,6 +51,7 @@ def main():
     ap.add_argument("--n", type=int, default=65536)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--no-oracle", action="store_true")
+    ap.add_argument("--grads-only", action="store_true", help="only the explicit-plan gradients k = 1..5")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -99,6 +100,8 @@ def main():
         emit(d)
     del T, G
     torch.cuda.empty_cache()
+    if args.grads_only:
+        return
 
     # ---- 2-D grids: side 256 (N = M = 65536), Table-3 style weights ----
     side = int(round(n ** 0.5))

@@ -464,6 +464,33 @@ def test_grad_kgen_random_plan(gw, k, n, m):
     assert _grad_err(G, Go) <= GRAD_TOL
 
 
+@pytest.mark.parametrize("k", [3, 5])
+@pytest.mark.parametrize("shape", ["wide", "clustered", "long"])
+def test_grad_kgen_tile_centred_fp32(gw, k, shape):
+    """k = 3, 5 run fp32 arithmetic about each 128-wide tile's own centre, with fp64 carries between
+    tiles (polyk.cuh): wide shifted supports, a tight cluster holding most of the mass beside far
+    outliers (a big carry next to small local terms), and long rows (64 column tiles' carries summed
+    into one row) -- each against the dense definition at the gradient tolerance."""
+    rng = np.random.default_rng(100 * k + len(shape))
+    if shape == "wide":
+        n, m = 1500, 1300
+        x, y = 10.0 * np.sort(rng.random(n)) - 3.0, 4.0 * np.sort(rng.random(m)) + 1.0
+    elif shape == "clustered":
+        n, m = 1100, 900
+        x = np.sort(np.concatenate([0.5 + 1e-3 * rng.random(n - 20), rng.random(20) * 3.0 - 1.0]))
+        y = np.sort(np.concatenate([0.2 + 1e-3 * rng.random(m - 10), rng.random(10) * 2.0]))
+    else:
+        n, m = 300, 8192
+        x, y = np.sort(rng.random(n)), np.sort(rng.random(m))
+    p, q = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))
+    T = (rng.exponential(size=(n, m)) / (n * m)).astype(np.float32)
+    G = gw.grad(x, y, p, q, _to_dev(gw, T), k=k).cpu().numpy().astype(np.float64)
+    Go = O.grad_prescribed(x, y, p, q, T.astype(np.float64), k=k)
+    err = _grad_err(G, Go)
+    print("k=%d %s n=%d m=%d: gradient err / max|G| %.3e" % (k, shape, n, m, err))
+    assert err <= GRAD_TOL
+
+
 @pytest.mark.parametrize("n,m", [(2048, 2048), (1500, 16384)])
 def test_grad_k4_moments_path(gw, n, m):
     """k = 4 runs the polynomial-moments path (poly.cuh: 25 plan moments + an fp64 degree-4 polynomial
