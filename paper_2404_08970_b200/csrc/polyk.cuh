@@ -175,10 +175,11 @@ __device__ __forceinline__ void gk_load_tile(const TSrc2& S, int64_t nl, int64_t
   }
 }
 
-// A CTA owns a GR x GR region (2 x 2 tiles of GK x GK, staged through shared memory one tile at a
-// time): the carries between CTAs are per region, half as many as per tile, and the states are taken
+// A CTA owns a GR x GR region (GNS x GNS tiles of GK x GK, staged through shared memory one tile at a
+// time): the carries between CTAs are per region, 1 / GNS as many as per tile, and the states are taken
 // about the region's centres (|x - cx| <= half the region's width).
-constexpr int GR = 2 * GK;
+constexpr int GNS = 4;        // tiles per region side
+constexpr int GR = GNS * GK;  // region side
 
 // before a tile buffer is refilled: generic-proxy writes to it ordered before the async-proxy (TMA)
 // writes, and every thread past its last read
@@ -189,13 +190,13 @@ __device__ __forceinline__ void gk_tile_release() {
 
 // sum_j C(r,j) c^{r-j} d_j for r = 0..K (the power sums of the centred coordinates about 0)
 template <int K>
-__device__ __forceinline__ void gk_uncentre(const float (&u)[K + 1], double c, double (&o)[K + 1]) {
+__device__ __forceinline__ void gk_uncentre(const double (&u)[K + 1], double c, double (&o)[K + 1]) {
 #pragma unroll
   for (int r = 0; r <= K; ++r) {
     double v = 0.0, cp = 1.0;
 #pragma unroll
     for (int j = r; j >= 0; --j) {
-      v = fma(gk_binom(r, j) * cp, (double)u[j], v);
+      v = fma(gk_binom(r, j) * cp, u[j], v);
       cp *= c;
     }
     o[r] = v;
@@ -231,22 +232,24 @@ __global__ void __launch_bounds__(GK) k_gk_sums(TSrc2 S, int64_t nl, int64_t m, 
       pv *= sv;
     }
   };
-  float U[2][K + 1];  // column sums of the two column tiles, over both row tiles
+  // column sums of the region's column tiles over all its row tiles: each tile's fp32 partial is folded
+  // into an fp64 accumulator (the fp32 sums run over 128 terms at most)
+  double U[GNS][K + 1];
 #pragma unroll
-  for (int cs = 0; cs < 2; ++cs)
+  for (int cs = 0; cs < GNS; ++cs)
 #pragma unroll
-    for (int j = 0; j <= K; ++j) U[cs][j] = 0.f;
+    for (int j = 0; j <= K; ++j) U[cs][j] = 0.0;
   uint32_t ph = 0;
-#pragma unroll
-  for (int rs = 0; rs < 2; ++rs) {
+#pragma unroll 1
+  for (int rs = 0; rs < GNS; ++rs) {
     const int64_t r0 = R0 + rs * GK;
     if (r0 >= nl) break;  // uniform
     const int rows = (int)min((int64_t)GK, nl - r0);
-    float R[K + 1];  // row sums of row r0 + t over both column tiles
+    double R[K + 1];  // row sums of row r0 + t over the region's column tiles (fp64 fold per tile)
 #pragma unroll
-    for (int j = 0; j <= K; ++j) R[j] = 0.f;
+    for (int j = 0; j <= K; ++j) R[j] = 0.0;
 #pragma unroll
-    for (int cs = 0; cs < 2; ++cs) {
+    for (int cs = 0; cs < GNS; ++cs) {
       const int64_t c0 = C0 + cs * GK;
       if (c0 >= m) break;  // uniform
       const int cols = (int)min((int64_t)GK, m - c0);
@@ -256,30 +259,44 @@ __global__ void __launch_bounds__(GK) k_gk_sums(TSrc2 S, int64_t nl, int64_t m, 
       if (MODE != T_PRODUCT) ph ^= 1u;
       __syncthreads();
       // thread = column t: U_j += sum_rr (x_rr - cx)^j T[rr][t]
-#pragma unroll 4
-      for (int rr = 0; rr < GK; ++rr) {
-        float pw[KP];
-        gk_ld_tab<KP>(pwt + rr * KP, pw);
-        const float v = tile[rr * GKQ + t];
+      {
+        float u[K + 1];
 #pragma unroll
-        for (int j = 0; j <= K; ++j) U[cs][j] = fmaf(v, pw[j], U[cs][j]);
+        for (int j = 0; j <= K; ++j) u[j] = 0.f;
+#pragma unroll 4
+        for (int rr = 0; rr < GK; ++rr) {
+          float pw[KP];
+          gk_ld_tab<KP>(pwt + rr * KP, pw);
+          const float v = tile[rr * GKQ + t];
+#pragma unroll
+          for (int j = 0; j <= K; ++j) u[j] = fmaf(v, pw[j], u[j]);
+        }
+#pragma unroll
+        for (int j = 0; j <= K; ++j) U[cs][j] += (double)u[j];
       }
       __syncthreads();
       powers(t < cols ? (float)(yc[c0 + t] - cy) : 0.f);
       __syncthreads();
       // thread = row t: R_j += sum_c (y_c - cy)^j T[t][c]
-      const float* trow = tile + t * GKQ;
+      {
+        float u[K + 1];
+#pragma unroll
+        for (int j = 0; j <= K; ++j) u[j] = 0.f;
+        const float* trow = tile + t * GKQ;
 #pragma unroll 2
-      for (int cc = 0; cc < GK; cc += 4) {
-        const float4 t4 = *reinterpret_cast<const float4*>(trow + cc);
-        const float tv[4] = {t4.x, t4.y, t4.z, t4.w};
+        for (int cc = 0; cc < GK; cc += 4) {
+          const float4 t4 = *reinterpret_cast<const float4*>(trow + cc);
+          const float tv[4] = {t4.x, t4.y, t4.z, t4.w};
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          float pw[KP];
-          gk_ld_tab<KP>(pwt + (cc + e) * KP, pw);
+          for (int e = 0; e < 4; ++e) {
+            float pw[KP];
+            gk_ld_tab<KP>(pwt + (cc + e) * KP, pw);
 #pragma unroll
-          for (int j = 0; j <= K; ++j) R[j] = fmaf(tv[e], pw[j], R[j]);
+            for (int j = 0; j <= K; ++j) u[j] = fmaf(tv[e], pw[j], u[j]);
+          }
         }
+#pragma unroll
+        for (int j = 0; j <= K; ++j) R[j] += (double)u[j];
       }
     }
     if (t < rows) {
@@ -290,7 +307,7 @@ __global__ void __launch_bounds__(GK) k_gk_sums(TSrc2 S, int64_t nl, int64_t m, 
     }
   }
 #pragma unroll
-  for (int cs = 0; cs < 2; ++cs) {
+  for (int cs = 0; cs < GNS; ++cs) {
     const int64_t q = C0 + cs * GK + t;
     if (q < m) {
       double o[K + 1];
@@ -467,7 +484,7 @@ __global__ void __launch_bounds__(256) k_gk_apply(const double* __restrict__ U, 
 // Each thread turns its fp64 carry polynomial sum_r h_r y^{K-r} into fp32 coefficients a_j about the
 // region's centre (gk_shift), then walks the region's two tiles in order: W = sum_j a_j s^j, and (odd
 // k) crossing column c flips that column's sign: a_j += 2 T_c C(K,j) (-s_c)^{K-j}  (the table tab[c][j]).
-// The column states of both column tiles stay in registers from the upper row tile to the lower one.
+// The column states of the region's column tiles stay in registers from one row tile to the next.
 template <int K, int MODE, bool STORE, bool OBJ, bool FGW>
 __global__ void __launch_bounds__(GK) k_gk_main(TSrc2 S, int64_t nl, int64_t m, const double* __restrict__ xl,
                                                 const double* __restrict__ yc, const double* __restrict__ rowpre,
@@ -507,18 +524,22 @@ __global__ void __launch_bounds__(GK) k_gk_main(TSrc2 S, int64_t nl, int64_t m, 
     }
   };
   const float a4 = (float)(-4.0 * alpha), a1 = (float)(1.0 - alpha);
-  float b[2][K + 1];  // column states of the two column tiles
+  float b[GNS][K + 1], e0[GNS];  // column states of the region's column tiles (constant term split as for a)
   double acc = 0.0;
   uint32_t ph = 0;
-#pragma unroll
-  for (int rs = 0; rs < 2; ++rs) {
+#pragma unroll 1
+  for (int rs = 0; rs < GNS; ++rs) {
     const int64_t r0 = R0 + rs * GK;
     if (r0 >= nl) break;  // uniform
     const int rows = (int)min((int64_t)GK, nl - r0);
     const int64_t i_t = r0 + t;
-    float a[K + 1];  // row state of row r0 + t
+    // row state of row r0 + t.  The constant coefficient is split: a[0] keeps the carried value, d0
+    // collects the crossings' constant terms 2 T_c (-s_c)^K -- hundreds of increments far smaller than
+    // a[0] would each round at a[0]'s ulp (a random walk of ~sqrt(GR) ulps); apart they do not.  The
+    // higher coefficients meet powers of |s| <= half the region's width, where that rounding is negligible.
+    float a[K + 1], d0 = 0.f;
 #pragma unroll
-    for (int cs = 0; cs < 2; ++cs) {
+    for (int cs = 0; cs < GNS; ++cs) {
       const int64_t c0 = C0 + cs * GK;
       if (c0 >= m) break;  // uniform
       const int cols = (int)min((int64_t)GK, m - c0);
@@ -549,6 +570,7 @@ __global__ void __launch_bounds__(GK) k_gk_main(TSrc2 S, int64_t nl, int64_t m, 
           gk_shift<K>(h, cy);
 #pragma unroll
           for (int j = 0; j <= K; ++j) a[j] = (float)h[j];
+          d0 = 0.f;
         }
         float* trow = tile + t * GKQ;
 #pragma unroll 2
@@ -558,12 +580,13 @@ __global__ void __launch_bounds__(GK) k_gk_main(TSrc2 S, int64_t nl, int64_t m, 
           float wo[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            wo[e] = gk_horner_f<K>(a, sys[cc + e]);
+            wo[e] = gk_horner_f<K>(a, sys[cc + e]) + d0;
             if (ODD) {
               float tb[KP];
               gk_ld_tab<KP>(tab + (cc + e) * KP, tb);
+              d0 = fmaf(tv[e], tb[0], d0);
 #pragma unroll
-              for (int j = 0; j <= K; ++j) a[j] = fmaf(tv[e], tb[j], a[j]);
+              for (int j = 1; j <= K; ++j) a[j] = fmaf(tv[e], tb[j], a[j]);
             }
           }
           *reinterpret_cast<float4*>(trow + cc) = make_float4(wo[0], wo[1], wo[2], wo[3]);
@@ -589,6 +612,7 @@ __global__ void __launch_bounds__(GK) k_gk_main(TSrc2 S, int64_t nl, int64_t m, 
           gk_shift<K>(h, cx);
 #pragma unroll
           for (int j = 0; j <= K; ++j) b[cs][j] = (float)h[j];
+          e0[cs] = 0.f;
         }
         const float c2q = (float)(2.0 * alpha * c2[q]);
         const float fyq = FGW ? (float)fy[q] : 0.f;
@@ -599,13 +623,14 @@ __global__ void __launch_bounds__(GK) k_gk_main(TSrc2 S, int64_t nl, int64_t m, 
 #pragma unroll 2
         for (int rr = 0; rr < rows; ++rr, gp += ldG) {
           const float2 xc = sxc[rr];
-          const float v = gk_horner_f<K>(b[cs], xc.x);
+          const float v = gk_horner_f<K>(b[cs], xc.x) + e0[cs];
           if (ODD) {
             float tb[KP];
             gk_ld_tab<KP>(tab + rr * KP, tb);
             const float w = tile[rr * GKQ + t];
+            e0[cs] = fmaf(w, tb[0], e0[cs]);
 #pragma unroll
-            for (int j = 0; j <= K; ++j) b[cs][j] = fmaf(w, tb[j], b[cs][j]);
+            for (int j = 1; j <= K; ++j) b[cs][j] = fmaf(w, tb[j], b[cs][j]);
           }
           if (OBJ) acc = fma((double)v, (double)gk_regen<MODE>(S, r0 + rr, q, gq, glq), acc);
           if (STORE) {
