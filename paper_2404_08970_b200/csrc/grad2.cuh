@@ -427,6 +427,9 @@ __global__ void __launch_bounds__(G2T, 3) k_grad_store2(MainArgs a, TSrc2 S) {
       float* Gp = a.G + (r0 + sub * G2SUB) * a.ldG + c0 + 2 * t;
       const bool q0v = c0 + 2 * t < m, q1v = c0 + 2 * t + 1 < m;
       const int nr = (int)min((int64_t)G2SUB, nl - (r0 + sub * G2SUB));
+      // OBJ: the sub-strip's <G, T> and feature terms in fp32 (<= G2SUB non-negative products per
+      // lane, relative rounding <= G2SUB ulps), folded into the fp64 sums after the sub-strip
+      float2 ob = make_float2(0.f, 0.f), oc = ob;
 #pragma unroll 4
       for (int rl = 0; rl < nr; ++rl) {
         const float2 loc = *reinterpret_cast<const float2*>(sT + rl * G2RS + cphys);
@@ -440,11 +443,11 @@ __global__ void __launch_bounds__(G2T, 3) k_grad_store2(MainArgs a, TSrc2 S) {
         g = ffma2(AA, m162, g);
         if (OBJ) {
           const float2 tv = *reinterpret_cast<const float2*>(sTobj + rl * G2RS + cphys);
-          acc_obj += (double)(g.x * tv.x) + (double)(g.y * tv.y);
+          ob = ffma2(g, tv, ob);
           if (FGW) {
             const float fx = sFx[sub * G2SUB + rl];
-            const float d0 = fx - fy2.x, d1 = fx - fy2.y;
-            acc_cc += (double)(d0 * d0 * tv.x) + (double)(d1 * d1 * tv.y);
+            const float2 d = fadd2(make_float2(fx, fx), make_float2(-fy2.x, -fy2.y));
+            oc = ffma2(make_float2(d.x * d.x, d.y * d.y), tv, oc);
           }
         } else {
           if (FGW) {
@@ -463,6 +466,10 @@ __global__ void __launch_bounds__(G2T, 3) k_grad_store2(MainArgs a, TSrc2 S) {
         }
         SA = fadd2(SA, Av);
         AA = ffma2(make_float2(rc.w, rc.w), SA, AA);
+      }
+      if (OBJ) {
+        acc_obj += (double)ob.x + (double)ob.y;
+        if (FGW) acc_cc += (double)oc.x + (double)oc.y;
       }
       // fold the sub-strip into the fp64 column state: AAtop(i0 + 32) = AAtop + (x_end - x_i0) SAtop + AAsub
       const float xend = nr > 0 ? sRow[sub * G2SUB + nr - 1].y + sRow[sub * G2SUB + nr - 1].w : xh0;
@@ -499,7 +506,7 @@ namespace gw {
 // Rows are taken 4 at a time: the 8 lane partials (4 rows x {P, A}) are reduced over the warp by
 // recursive halving (9 shuffles instead of 40); fixed lane structure => deterministic.
 // ---------------------------------------------------------------------------------
-template <int MODE>
+template <int MODE, bool COSTW = false>
 __device__ __forceinline__ void moments3_body(const TSrc2& S, int64_t nl, int64_t m, const double* __restrict__ xl,
                                               const double* __restrict__ yc, double* __restrict__ rP,
                                               double* __restrict__ rA, double* __restrict__ cS,
@@ -560,7 +567,8 @@ __device__ __forceinline__ void moments3_body(const TSrc2& S, int64_t nl, int64_
       float2 P2 = make_float2(0.f, 0.f), A2 = P2;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        float2 t = tv[u][k];
+        const float2 graw = tv[u][k];  // the loaded value (GIBBS: the cost)
+        float2 t = graw;
         if (MODE == T_GIBBS) {
           const float2 aa = fadd2(fadd2(ffma2(t, nch, gh[k]), make_float2(F[u], F[u])),
                                   ffma2(t, ncl, fadd2(gl[k], make_float2(Fl[u], Fl[u]))));
@@ -575,9 +583,9 @@ __device__ __forceinline__ void moments3_body(const TSrc2& S, int64_t nl, int64_
           if (q + 1 >= m) t.y = 0.f;
         }
         P2 = fadd2(P2, t);
-        A2 = ffma2(dy[k], t, A2);
+        A2 = ffma2(COSTW ? graw : dy[k], t, A2);
         cs[k] = fadd2(cs[k], t);
-        cx[k] = ffma2(make_float2(dxr[u], dxr[u]), t, cx[k]);
+        if (!COSTW) cx[k] = ffma2(make_float2(dxr[u], dxr[u]), t, cx[k]);
       }
       part[2 * u] = P2.x + P2.y;
       part[2 * u + 1] = A2.x + A2.y;
@@ -621,8 +629,10 @@ __device__ __forceinline__ void moments3_body(const TSrc2& S, int64_t nl, int64_
   for (int k = 0; k < 4; ++k) {
     red[0][w][8 * lane + 2 * k] = cs[k].x;
     red[0][w][8 * lane + 2 * k + 1] = cs[k].y;
-    red[1][w][8 * lane + 2 * k] = cx[k].x;
-    red[1][w][8 * lane + 2 * k + 1] = cx[k].y;
+    if (!COSTW) {
+      red[1][w][8 * lane + 2 * k] = cx[k].x;
+      red[1][w][8 * lane + 2 * k + 1] = cx[k].y;
+    }
   }
   __syncthreads();
   const int t = threadIdx.x;
@@ -630,9 +640,12 @@ __device__ __forceinline__ void moments3_body(const TSrc2& S, int64_t nl, int64_
   if (q < m) {
     double a = 0.0, bx = 0.0;
 #pragma unroll
-    for (int ww = 0; ww < 8; ++ww) { a += red[0][ww][t]; bx += red[1][ww][t]; }
+    for (int ww = 0; ww < 8; ++ww) {
+      a += red[0][ww][t];
+      if (!COSTW) bx += red[1][ww][t];
+    }
     cS[b * m + q] = a;
-    cX[b * m + q] = bx;
+    if (!COSTW) cX[b * m + q] = bx;
   }
 }
 
@@ -653,6 +666,15 @@ __global__ void __launch_bounds__(256, 3) k_grad_moments3o(TSrc2 S, int64_t nl, 
                                                            double* __restrict__ rA, double* __restrict__ cS,
                                                            double* __restrict__ cX) {
   moments3_body<MODE>(S, nl, m, xl, yc, rP, rA, cS, cX);
+}
+
+// UGW plan statistics in one read of the cost (Remark 3, reading R33; ugw.cuh): per (row, strip)
+//   rP[s][j] = sum_{q in s} T_jq,  rC[s][j] = sum_{q in s} C_jq T_jq,  and per (block, column)
+//   cS[b][q] = sum_{j in b} T_jq  of the Gibbs plan T = exp2(...) regenerated from the cost C.
+__global__ void __launch_bounds__(256) k_ugw_moments(TSrc2 S, int64_t nl, int64_t m, const double* __restrict__ xl,
+                                                     const double* __restrict__ yc, double* __restrict__ rP,
+                                                     double* __restrict__ rC, double* __restrict__ cS) {
+  moments3_body<T_GIBBS, true>(S, nl, m, xl, yc, rP, rC, cS, nullptr);
 }
 
 }  // namespace gw

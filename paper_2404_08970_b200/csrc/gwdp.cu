@@ -109,7 +109,7 @@ struct gw_ctx {
   Buf pnf, qnf;  // fp32 marginals
   Buf yfb, pcoef, pc2s, pfx, pfy, ppart, pM, p4coef, p4c2;  // k = 2 and k = 4 (moments) paths
   Buf gkrp, gkrt, gkcp, gkz, gkct, gkctt, gkobj, gkseg;  // k >= 3 path
-  Buf uga, ugb, ugct, ugpart, ugca, ugcb, ugfr, uggr, ugsc;  // UGW
+  Buf uga, ugb, ugct, ugpart, ugca, ugcb, ugfr, uggr, ugsc, ugrpart;  // UGW
   Buf g2rc, g2rd, g2h, g2cc, g2tt, g2vt, g2tmp, g2s, g2a, g2b, g2ca, g2cb, g2part;  // 2-D grids
   Buf xtab, xg1, xg2, xin, xvec, xtail, xpart;  // multi-rank exchange buffers
   Buf slse, slseg, scsl, scsg, sviolg, sun, sung;  // Sinkhorn column-sum exchange
@@ -130,7 +130,7 @@ struct gw_ctx {
                 &pnf, &qnf, &xtab, &xg1, &xg2, &xin, &xvec, &xtail, &xpart, &slse, &slseg, &scsl, &scsg, &sun, &sung,
                 &sviolg, &sflag, &sflagg, &yfb, &pcoef, &pc2s, &pfx, &pfy, &ppart, &pM, &p4coef, &p4c2,
                 &gkrp, &gkrt, &gkcp, &gkz, &gkct, &gkctt, &gkobj, &gkseg,
-                &uga, &ugb, &ugct, &ugpart, &ugca, &ugcb, &ugfr, &uggr, &ugsc,
+                &uga, &ugb, &ugct, &ugpart, &ugca, &ugcb, &ugfr, &uggr, &ugsc, &ugrpart,
                 &g2rc, &g2rd, &g2h, &g2cc, &g2tt, &g2vt, &g2tmp, &g2s, &g2a, &g2b, &g2ca, &g2cb, &g2part};
     for (Buf* x : b) all.push_back(x);
   }
@@ -2320,16 +2320,23 @@ static gw_status ugw_stats(gw_ctx* c, const Prepared& P, SinkState& s, const flo
   const double cc = GW_LOG2E / eps_t;
   const float ch = (float)cc;
   const TSrc2 S2{C, ldC, s.fh, s.fl, s.gh, s.gl, ch, (float)(cc - (double)ch)};
-  double *ct, *part, *sc;
+  double *ct, *part, *rpart, *sc;
   TRY(ws(c, c->ugct, (size_t)std::max<int64_t>(nl, 1), &ct));
-  const int nch = (int)((nl + 255) / 256);
-  TRY(ws(c, c->ugpart, (size_t)std::max(nch, 1) * m, &part));
+  // one read of the cost (k_ugw_moments): per 256-column strip row partials of a and ct, per 256-row
+  // block column partials of b, then fixed-order sums over the strips / blocks
+  const int nblk = (int)((nl + TR - 1) / TR), nstr = (int)((m + TC - 1) / TC);
+  TRY(ws(c, c->ugpart, (size_t)std::max(nblk, 1) * m, &part));
+  TRY(ws(c, c->ugrpart, 2 * (size_t)nstr * (size_t)std::max<int64_t>(nl, 1), &rpart));
   TRY(ws(c, c->ugsc, 8, &sc));
-  k_ugw_rowstats<<<(unsigned)((nl + 8 * URPW - 1) / (8 * URPW)), 256, 0, c->stream>>>(S2, nl, m, a_out, ct);
-  KCHECK();
-  k_g2_colsum<T_GIBBS><<<dim3((unsigned)((m + 255) / 256), (unsigned)nch), 256, 0, c->stream>>>(S2, nl, m, part);
-  KCHECK();
-  k_g2_colsum_reduce<<<grid_for(m), 256, 0, c->stream>>>(part, nch, m, b_out);
+  if (nl > 0) {
+    k_ugw_moments<<<dim3((unsigned)nstr, (unsigned)nblk), 256, 0, c->stream>>>(S2, nl, m, P.xc + P.row0, P.yc, rpart,
+                                                                                rpart + (size_t)nstr * nl, part);
+    KCHECK();
+    k_g2_colsum_reduce<<<grid_for(nl), 256, 0, c->stream>>>(rpart, nstr, nl, a_out);
+    k_g2_colsum_reduce<<<grid_for(nl), 256, 0, c->stream>>>(rpart + (size_t)nstr * nl, nstr, nl, ct);
+    KCHECK();
+  }
+  k_g2_colsum_reduce<<<grid_for(m), 256, 0, c->stream>>>(part, nl > 0 ? nblk : 0, m, b_out);
   KCHECK();
   if (P.R > 1) {  // b over every rank's rows, summed in rank order
     double* gb;

@@ -46,6 +46,16 @@ def oracle_time(fn):
     return time.perf_counter() - t0
 
 
+SOLVE_BYTES_NOTE = ("2 outer iterations: gradient on T^0 = p q^T 4NM (write only) + gradient on the Gibbs plan "
+                    "12NM + 4NM per one-read Sinkhorn iteration + the final objective 8NM")
+
+
+def solve_bytes(inner, nm, outer=2, stats=0):
+    """Algorithmic bytes of an `outer`-iteration solve with `inner` fused iterations per outer iteration
+    (NM = N x M elements; 4NM = one fp32 pass over the matrix)."""
+    return (4 + 12 * (outer - 1) + 4 * inner * outer + stats * outer + 8) * nm
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=65536)
@@ -150,8 +160,8 @@ def main():
     nm5 = float(P.n) * P.m
     emit({"variant": "fgw_solve (C5)", "row": "f1", "N": P.n, "M": P.m, "alpha": 0.5, "eps": P.eps, "outer": 2,
           "inner": 100, "ms": ms, "outer_iter_per_s": 2 / (ms / 1e3), "inner_fused": r.inner_fused_total,
-          "algorithmic_bytes": 2 * (12 + 400) * nm5, "bytes_note": "per outer: gradient 12NM + 100 fused sweeps 4NM",
-          "GBps": 2 * (12 + 400) * nm5 / ms / 1e6, "gw_objective": r.gw_objective,
+          "algorithmic_bytes": solve_bytes(100, nm5), "bytes_note": SOLVE_BYTES_NOTE,
+          "GBps": solve_bytes(100, nm5) / ms / 1e6, "gw_objective": r.gw_objective,
           "marginal_violation": r.marginal_violation})
     # ---- k = 3 solve at C3 size ----
     n3 = 16384
@@ -167,8 +177,8 @@ def main():
     nm3 = float(n3) * n3
     emit({"variant": "entropic_gw_solve k=3", "row": "f2", "N": n3, "M": n3, "eps": 1e-2, "outer": 2,
           "inner": 100, "ms": ms, "outer_iter_per_s": 2 / (ms / 1e3), "inner_fused": r.inner_fused_total,
-          "algorithmic_bytes": 2 * (12 + 400) * nm3, "GBps": 2 * (12 + 400) * nm3 / ms / 1e6,
-          "gw_objective": r.gw_objective})
+          "algorithmic_bytes": solve_bytes(100, nm3), "bytes_note": SOLVE_BYTES_NOTE,
+          "GBps": solve_bytes(100, nm3) / ms / 1e6, "gw_objective": r.gw_objective})
     # ---- unbalanced GW (row f4) at N = M = 16384, rho = 1, eps = 1e-2 (readings R32-R35) ----
     u3 = rng.random(n3) + 0.5
     u3 /= u3.sum()
@@ -183,10 +193,9 @@ def main():
         ms = timed(runu, 1, stream)
     emit({"variant": "ugw_solve", "row": "f4", "N": n3, "M": n3, "rho": 1.0, "eps": 1e-2, "outer": 2,
           "inner": 50, "ms": ms, "outer_iter_per_s": 2 / (ms / 1e3), "inner_fused": r.inner_fused_total,
-          "algorithmic_bytes": 2 * (8 + 12 + 50 * 4) * nm3,
-          "bytes_note": "per outer: plan statistics 8NM (row pass + column pass) + gradient 12NM + 50 fused "
-                        "one-read iterations 4NM",
-          "GBps": 2 * (8 + 12 + 50 * 4) * nm3 / ms / 1e6})
+          "algorithmic_bytes": solve_bytes(50, nm3, stats=4),
+          "bytes_note": SOLVE_BYTES_NOTE + "; plan statistics 4NM per outer (one read of the cost)",
+          "GBps": solve_bytes(50, nm3, stats=4) / ms / 1e6})
     # ---- unbalanced GW on the C5 recipe at full size (N = 32768, M = 24576, rho = 1.0, BASELINE configs[4]) ----
     with torch.cuda.stream(stream):
         r = None
@@ -197,9 +206,9 @@ def main():
         ms = timed(runu5, 1, stream)
     emit({"variant": "ugw_solve (C5)", "row": "f4", "N": P.n, "M": P.m, "rho": 1.0, "eps": P.eps, "outer": 2,
           "inner": 100, "ms": ms, "outer_iter_per_s": 2 / (ms / 1e3), "inner_fused": r.inner_fused_total,
-          "algorithmic_bytes": 2 * (8 + 12 + 100 * 4) * nm5,
-          "bytes_note": "per outer: plan statistics 8NM + gradient 12NM + 100 fused one-read iterations 4NM",
-          "GBps": 2 * (8 + 12 + 100 * 4) * nm5 / ms / 1e6, "gw_objective": r.gw_objective})
+          "algorithmic_bytes": solve_bytes(100, nm5, stats=4),
+          "bytes_note": SOLVE_BYTES_NOTE + "; plan statistics 4NM per outer (one read of the cost)",
+          "GBps": solve_bytes(100, nm5, stats=4) / ms / 1e6, "gw_objective": r.gw_objective})
     torch.cuda.empty_cache()
     # ---- tau != eps (reading R6) on the same problem: cost G + (eps - tau) ln T ----
     with torch.cuda.stream(stream):
@@ -211,8 +220,8 @@ def main():
         ms = timed(runt, 1, stream)
     emit({"variant": "entropic_gw_solve tau=eps/2", "row": "a (tau)", "N": n3, "M": n3, "eps": 1e-2, "tau": 5e-3,
           "outer": 2, "inner": 100, "ms": ms, "outer_iter_per_s": 2 / (ms / 1e3), "inner_fused": r.inner_fused_total,
-          "algorithmic_bytes": 2 * (12 + 400) * nm3, "GBps": 2 * (12 + 400) * nm3 / ms / 1e6,
-          "gw_objective": r.gw_objective})
+          "algorithmic_bytes": solve_bytes(100, nm3), "bytes_note": SOLVE_BYTES_NOTE,
+          "GBps": solve_bytes(100, nm3) / ms / 1e6, "gw_objective": r.gw_objective})
     ctx.close()
 
 
