@@ -219,6 +219,110 @@ __global__ void __launch_bounds__(G2D_MAXN) k_g2_rowred(TSrc2 S, int ny, double*
   }
 }
 
+// The same row reductions (no OBJ terms) for ny = 4 TPR with TPR in {32, 64}: 128-bit loads.  Thread
+// (phase, j) of the 256 covers d = 4j .. 4j + 3 of the c-rows c = phase + P k (P = 256 / TPR phases),
+// eight c-rows' float4 in flight per thread (4x the bytes per load of the scalar kernel, which is
+// load-latency bound); the 8 per-thread c-row partials are reduced over the warp by recursive halving,
+// the TPR / 32 warps of a c-row and the P phases of a d are combined through shared memory in fixed
+// order -> deterministic.
+template <int MODE, int TPR>
+__global__ void __launch_bounds__(256) k_g2_rowred4(TSrc2 S, double* __restrict__ RC, double* __restrict__ RD) {
+  constexpr int NY = 4 * TPR, P = 256 / TPR, WPR = TPR / 32;  // WPR warps per c-row
+  // c-rows per thread per batch (GIBBS loads the cost and both column-dual words: 4 keep the double
+  // buffer in registers)
+  constexpr int B = MODE == T_GIBBS ? 4 : 8;
+  constexpr int LB = B == 8 ? 3 : 2;
+  __shared__ float wp[NY][WPR];
+  __shared__ float4 rdp[P][TPR];
+  const int64_t i = blockIdx.x;
+  const int t = threadIdx.x, lane = t & 31;
+  const int phase = t / TPR, j = t % TPR, wr = j / 32;  // wr: this warp's index within its c-row
+  float Fh = 0.f, Fl = 0.f;
+  if (MODE != T_EXPLICIT) Fh = S.fh[i];
+  if (MODE == T_GIBBS) Fl = S.fl[i];
+  const float4* row = (MODE == T_PRODUCT) ? nullptr : reinterpret_cast<const float4*>(S.T + i * S.ld);
+  float4 rd = make_float4(0.f, 0.f, 0.f, 0.f);
+  // software pipeline: the next batch's loads are issued before this batch's arithmetic (left to
+  // itself the compiler sinks each load to its use at 32 registers: 4 loads in flight, not 8)
+  float4 nraw[B], ng1[B], ng2[B];
+  auto load = [&](int cb) {
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      const int c = cb + phase + P * k;
+      const int64_t q4 = (int64_t)c * TPR + j;  // float4 index of (c, 4j)
+      nraw[k] = MODE != T_PRODUCT ? __ldcs(row + q4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (MODE != T_EXPLICIT) ng1[k] = reinterpret_cast<const float4*>(S.gh)[q4];
+      if (MODE == T_GIBBS) ng2[k] = reinterpret_cast<const float4*>(S.gl)[q4];
+    }
+  };
+  load(0);
+  for (int cb = 0; cb < NY; cb += P * B) {
+    float4 raw[B], g1[B], g2[B];
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      raw[k] = nraw[k];
+      if (MODE != T_EXPLICIT) g1[k] = ng1[k];
+      if (MODE == T_GIBBS) g2[k] = ng2[k];
+    }
+    if (cb + P * B < NY) load(cb + P * B);
+    float v[B];
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      float4 tt;
+      if (MODE == T_EXPLICIT) {
+        tt = raw[k];
+      } else if (MODE == T_PRODUCT) {
+        tt = make_float4(Fh * g1[k].x, Fh * g1[k].y, Fh * g1[k].z, Fh * g1[k].w);
+      } else {
+        const float2 nch = make_float2(-S.ch, -S.ch), ncl = make_float2(-S.cl, -S.cl);
+        const float2 F2 = make_float2(Fh, Fh), Fl2 = make_float2(Fl, Fl);
+        const float2 a0 = fadd2(fadd2(ffma2(make_float2(raw[k].x, raw[k].y), nch, make_float2(g1[k].x, g1[k].y)), F2),
+                                ffma2(make_float2(raw[k].x, raw[k].y), ncl, fadd2(make_float2(g2[k].x, g2[k].y), Fl2)));
+        const float2 a1 = fadd2(fadd2(ffma2(make_float2(raw[k].z, raw[k].w), nch, make_float2(g1[k].z, g1[k].w)), F2),
+                                ffma2(make_float2(raw[k].z, raw[k].w), ncl, fadd2(make_float2(g2[k].z, g2[k].w), Fl2)));
+        tt = make_float4(ex2_ftz(a0.x), ex2_ftz(a0.y), ex2_ftz(a1.x), ex2_ftz(a1.y));
+      }
+      rd.x += tt.x; rd.y += tt.y; rd.z += tt.z; rd.w += tt.w;
+      v[k] = (tt.x + tt.y) + (tt.z + tt.w);
+    }
+    // the warp's sums of the B c-rows by recursive halving: lanes whose low 5 - LB bits are zero end
+    // with k = lane >> (5 - LB)
+    int bit = 16;
+#pragma unroll
+    for (int h = B / 2; h >= 1; h >>= 1, bit >>= 1) {
+#pragma unroll
+      for (int k = 0; k < h; ++k) {
+        const bool hi = lane & bit;
+        const float send = hi ? v[k] : v[h + k];
+        const float keep = hi ? v[h + k] : v[k];
+        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, bit);
+      }
+    }
+#pragma unroll
+    for (int bb = 16 >> LB; bb >= 1; bb >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], bb);
+    if ((lane & ((1 << (5 - LB)) - 1)) == 0) wp[cb + phase + P * (lane >> (5 - LB))][wr] = v[0];
+  }
+  rdp[phase][j] = rd;
+  __syncthreads();
+  // RC[c] = sum of the c-row's warp partials; RD[d] = sum over the phases (fixed order)
+  for (int c = t; c < NY; c += 256) {
+    double a = 0.0;
+#pragma unroll
+    for (int w = 0; w < WPR; ++w) a += (double)wp[c][w];
+    RC[i * NY + c] = a;
+  }
+  for (int d = t; d < NY; d += 256) {
+    double a = 0.0;
+#pragma unroll
+    for (int ph = 0; ph < P; ++ph) {
+      const float4 r4 = rdp[ph][d >> 2];
+      const int e = d & 3;
+      a += (double)(e == 0 ? r4.x : e == 1 ? r4.y : e == 2 ? r4.z : r4.w);
+    }
+    RD[i * NY + d] = a;
+  }
+}
+
 // T^AC[a][c] = sum_b RC[(a,b)][c], T^BC[b][c] = sum_a RC, T^AD[a][d] = sum_b RD, T^BD[b][d] = sum_a RD,
 // over this rank's rows [row0, row0 + nl) (RC, RD hold those rows; the ranks' partial matrices are
 // all-gathered and summed in rank order).

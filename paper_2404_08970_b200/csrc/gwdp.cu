@@ -924,6 +924,19 @@ static gw_status grad_pass_2d(gw_ctx* c, const Prepared& P, int mode, const TSrc
       if (mode == T_EXPLICIT) LAUNCH_RR(T_EXPLICIT, true);
       else if (mode == T_GIBBS) LAUNCH_RR(T_GIBBS, true);
       else LAUNCH_RR(T_PRODUCT, true);
+    } else if ((ny == 128 || ny == 256) && !getenv("GWDP_G2_SCALAR")) {
+      // 128-bit loads (k_g2_rowred4): rows of 128^2 or 256^2 columns
+#define LAUNCH_RR4(MODE, TPR) k_g2_rowred4<MODE, TPR><<<(unsigned)nl, 256, 0, c->stream>>>(S2, RC, RD)
+      if (ny == 256) {
+        if (mode == T_EXPLICIT) LAUNCH_RR4(T_EXPLICIT, 64);
+        else if (mode == T_GIBBS) LAUNCH_RR4(T_GIBBS, 64);
+        else LAUNCH_RR4(T_PRODUCT, 64);
+      } else {
+        if (mode == T_EXPLICIT) LAUNCH_RR4(T_EXPLICIT, 32);
+        else if (mode == T_GIBBS) LAUNCH_RR4(T_GIBBS, 32);
+        else LAUNCH_RR4(T_PRODUCT, 32);
+      }
+#undef LAUNCH_RR4
     } else {
       if (mode == T_EXPLICIT) LAUNCH_RR(T_EXPLICIT, false);
       else if (mode == T_GIBBS) LAUNCH_RR(T_GIBBS, false);

@@ -99,6 +99,59 @@ def test_grad_2d_max_side(gw):
         assert np.max(np.abs(G[i] - Go)) <= GRAD_TOL * np.max(np.abs(Go)), i
 
 
+def _grad_2d_rows_oracle(sx, sy, p, q, T64, rows):
+    """Rows of the 2-D gradient by the oracle's Kronecker products (apply_distance_2d, pinned to the
+    dense definition): W = T D_Y row by row, then (D_X W)_i with the dense D_X."""
+    W = np.stack([O.apply_distance_2d(T64[j], sy) for j in range(T64.shape[0])])  # T D_Y (D_Y symmetric)
+    DX = O.dist2d(sx)
+    Px, Py = O.grid_points(sx), O.grid_points(sy)
+    out = []
+    for i in rows:
+        dxi = np.abs(Px[i, 0] - Px[:, 0]) + np.abs(Px[i, 1] - Px[:, 1])
+        c_i = np.sum(dxi * dxi * p)
+        out.append((i, c_i, DX[i] @ W))
+    DYq = np.array([np.sum((np.abs(Py[j, 0] - Py[:, 0]) + np.abs(Py[j, 1] - Py[:, 1])) ** 2 * q)
+                    for j in range(Py.shape[0])])
+    return {i: 2.0 * (c_i + DYq) - 4.0 * v for i, c_i, v in out}
+
+
+@pytest.mark.parametrize("nx,ny", [(8, 128), (6, 256)])
+def test_grad_2d_wide_rows(gw, nx, ny):
+    """Rows of 128^2 / 256^2 columns take the 128-bit reduction kernel (k_g2_rowred4): every row vs the
+    oracle's Kronecker route."""
+    rng, sx, sy, p, q = _problem(5 * nx + ny, nx, ny, False)
+    n, m = nx * nx, ny * ny
+    T = (rng.random((n, m)) / (n * m)).astype(np.float32)
+    G = gw.grad(sx, sy, p, q, _to_dev(gw, T), grid2d=True).cpu().numpy().astype(np.float64)
+    ref = _grad_2d_rows_oracle(sx, sy, p, q, T.astype(np.float64), range(n))
+    scale = max(np.max(np.abs(v)) for v in ref.values())
+    err = max(np.max(np.abs(G[i] - v)) for i, v in ref.items()) / scale
+    print("2-D wide rows nx=%d ny=%d: gradient err / max|G| %.3e" % (nx, ny, err))
+    assert err <= GRAD_TOL
+
+
+def test_solver_2d_wide_rows_gibbs_gradient(gw, monkeypatch):
+    """The solver's own gradient on a Gibbs plan (T^1 regenerated from G^1 and the duals) through the
+    128-bit reduction kernel: exported G^2 vs the oracle on the exported T^1; and the whole solve with
+    the scalar kernel (GWDP_G2_SCALAR=1) agrees."""
+    _, sx, sy, p, q = _problem(77, 12, 128, False)
+    n, m = 144, 128 * 128
+    Tb, Gb = gw.plan_buffer(n, m, _dev()), gw.plan_buffer(n, m, _dev())
+    r = gw.solve(sx, sy, p, q, 0.01, 2, 50, device=_dev(), grid2d=True, export_iter=2, export_T=Tb, export_G=Gb)
+    T64 = Tb.cpu().numpy().astype(np.float64)
+    G = Gb.cpu().numpy().astype(np.float64)
+    rows = np.random.default_rng(0).choice(n, 24, replace=False)
+    ref = _grad_2d_rows_oracle(sx, sy, p, q, T64, rows)
+    scale = max(np.max(np.abs(v)) for v in ref.values())
+    err = max(np.max(np.abs(G[i] - v)) for i, v in ref.items()) / scale
+    monkeypatch.setenv("GWDP_G2_SCALAR", "1")
+    r2 = gw.solve(sx, sy, p, q, 0.01, 2, 50, device=_dev(), grid2d=True)
+    rel = abs(r.gw_objective - r2.gw_objective) / abs(r2.gw_objective)
+    print("2-D Gibbs gradient err / max|G| %.3e; objective vector vs scalar kernel %.3e" % (err, rel))
+    assert err <= GRAD_TOL
+    assert rel <= 1e-5
+
+
 def test_grad_2d_product_plan_closed_form(gw):
     """T = p q^T: D_X T D_Y = (D_X p)(D_Y q)^T, each factor by the oracle's dense D."""
     rng, sx, sy, p, q = _problem(3, 12, 9, False)
