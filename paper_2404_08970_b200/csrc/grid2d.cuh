@@ -352,6 +352,10 @@ __global__ void k_g2_marg(const double* __restrict__ RC, const double* __restric
 // smaller than c_i), so each element is summed in fp64 and rounded to fp32 once.
 constexpr int G2SR = 32;
 constexpr int G2SC = 8;  // columns per thread
+// k_g2_store4: columns per thread (more columns per barrier; FGW keeps 16: its feature terms double the
+// per-column registers)
+template <bool FGW>
+__host__ __device__ constexpr int g2sc4() { return FGW ? 16 : 32; }
 template <bool FGW>
 __global__ void __launch_bounds__(256) k_g2_store(const double* __restrict__ cX, const double* __restrict__ cY,
                                                   const double* __restrict__ VAC, const double* __restrict__ VAD,
@@ -420,8 +424,10 @@ __global__ void __launch_bounds__(256) k_g2_store(const double* __restrict__ cX,
 
 // The same store with 4 consecutive columns per thread group (ny % 4 == 0: the 4 share c, and d..d+3
 // are consecutive): one rc read, two double2 rd reads and ONE 16-byte store per 4 elements; row grid
-// coordinates advance incrementally (no division per row).  (Reading the V rows straight from L1
-// without the shared-memory staging measured slower: 10.1 vs 8.4 ms at 256^2 x 256^2.)
+// coordinates advance incrementally (no division per row).  A CTA covers 256 g2sc4 columns: 32 per
+// thread (16 with FGW) amortise each row's barrier and shared-memory staging over 8192 stores (3.78 ->
+// 3.22 ms per store pass in ncu at 256^2 x 256^2, 8 columns per thread before).  (Reading the V rows straight
+// from L1 without the shared-memory staging measured slower: 10.1 vs 8.4 ms per gradient.)
 template <bool FGW>
 __global__ void __launch_bounds__(256) k_g2_store4(const double* __restrict__ cX, const double* __restrict__ cY,
                                                    const double* __restrict__ VAC, const double* __restrict__ VAD,
@@ -431,8 +437,8 @@ __global__ void __launch_bounds__(256) k_g2_store4(const double* __restrict__ cX
                                                    float* __restrict__ G, int64_t ldG) {
   __shared__ __align__(16) double rc[2][G2D_MAXN], rd[2][G2D_MAXN];
   const int t = threadIdx.x;
-  constexpr int NG = G2SC / 4;  // groups of 4 columns per thread
-  const int64_t qb = (int64_t)G2SC * 256 * blockIdx.x + 4 * t;  // groups at qb + 1024 k
+  constexpr int NG = g2sc4<FGW>() / 4;  // groups of 4 columns per thread
+  const int64_t qb = (int64_t)g2sc4<FGW>() * 256 * blockIdx.x + 4 * t;  // groups at qb + 1024 k
   const double a2 = 2.0 * alpha, a1 = 1.0 - alpha, a4 = -4.0 * alpha;
   double cy[NG][4], fyv[NG][4];
   int cc[NG], dd[NG];

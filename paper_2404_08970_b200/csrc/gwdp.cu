@@ -1019,10 +1019,12 @@ static gw_status grad_pass_2d(gw_ctx* c, const Prepared& P, int mode, const TSrc
   if (store && nl > 0) {
     PROF_BEGIN(c, PC_GRAD_MAIN);
     const dim3 sg((unsigned)((m + 256 * G2SC - 1) / (256 * G2SC)), (unsigned)((nl + G2SR - 1) / G2SR));
+    const int sc4 = fx ? g2sc4<true>() : g2sc4<false>();
+    const dim3 sg4((unsigned)((m + 256 * sc4 - 1) / (256 * sc4)), (unsigned)((nl + G2SR - 1) / G2SR));
     if (ny % 4 == 0) {  // 4 consecutive columns share their grid row c: vectorised stores
-      if (fx) k_g2_store4<true><<<sg, 256, 0, c->stream>>>(P.cx, P.cy, VT, VT + nn, VT + 2 * nn, VT + 3 * nn, nx, ny,
+      if (fx) k_g2_store4<true><<<sg4, 256, 0, c->stream>>>(P.cx, P.cy, VT, VT + nn, VT + 2 * nn, VT + 3 * nn, nx, ny,
                                                           P.row0, nl, m, alpha, fx, fy, G, ldG);
-      else k_g2_store4<false><<<sg, 256, 0, c->stream>>>(P.cx, P.cy, VT, VT + nn, VT + 2 * nn, VT + 3 * nn, nx, ny,
+      else k_g2_store4<false><<<sg4, 256, 0, c->stream>>>(P.cx, P.cy, VT, VT + nn, VT + 2 * nn, VT + 3 * nn, nx, ny,
                                                         P.row0, nl, m, alpha, nullptr, nullptr, G, ldG);
     } else if (fx) k_g2_store<true><<<sg, 256, 0, c->stream>>>(P.cx, P.cy, VT, VT + nn, VT + 2 * nn, VT + 3 * nn, nx, ny,
                                                        P.row0, nl, m, alpha, fx, fy, G, ldG);
