@@ -42,7 +42,8 @@ UNIT = "outer_iter/s"
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 TRAFFIC_PATH = os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
-KERNELS = ["grad_moments", "grad_carry", "grad_main", "sink_row", "sink_col", "sink_fused", "objective_pass"]
+KERNELS = ["grad_moments", "grad_carry", "grad_main", "sink_row", "sink_col", "sink_fused", "objective_pass",
+           None, "grad_onepass", "sink_xm"]  # gw_ctx_profile slots (slot 7: the launch count)
 
 
 def peaks():
@@ -267,8 +268,8 @@ def main():
     # ---- second timed region, same solve with per-kernel-class CUDA events on the library stream
     # (the library then launches eagerly: events cannot sit inside its graphs) -> the breakdown and the
     # roofline of the dominant kernel ----
-    ms_c = (C.c_double * 8)()
-    cnt_c = (C.c_int64 * 8)()
+    ms_c = (C.c_double * len(KERNELS))()
+    cnt_c = (C.c_int64 * len(KERNELS))()
     _lib.check(lib.gw_ctx_profile(ctx.h, 2, None, None, 0))
     barrier()
     torch.cuda.synchronize()
@@ -278,22 +279,26 @@ def main():
     p1.record(stream)
     torch.cuda.synchronize()
     barrier()
-    _lib.check(lib.gw_ctx_profile(ctx.h, 0, C.cast(ms_c, C.c_void_p), C.cast(cnt_c, C.c_void_p), 8))
+    _lib.check(lib.gw_ctx_profile(ctx.h, 0, C.cast(ms_c, C.c_void_p), C.cast(cnt_c, C.c_void_p), len(KERNELS)))
     prof_ms = max_over_ranks(p0.elapsed_time(p1))
 
     # ---- per kernel class (live CUDA events on the library stream) ----
     hbm, peak_src = peaks()
     nm_bytes = float(nl) * m
-    fused_it = max(1, res.inner_fused_total)
+    n_one = int(cnt_c[8])                       # gradients on the one-read path
+    n_two = args.steps - n_one                  # two-read gradients (the first: the product plan)
+    n_xm = int(cnt_c[9]) // 2                   # XM sweeps (one per one-read gradient)
+    fused_it = max(1, res.inner_fused_total - n_xm)
     safe_it = max(1, res.inner_iters_total - res.inner_fused_total)
     per_unit = {  # (units, algorithmic bytes per unit)
-        "grad_moments": (args.steps, 4 * nm_bytes), "grad_carry": (args.steps, None),
-        "grad_main": (args.steps, 8 * nm_bytes), "sink_row": (safe_it, 4 * nm_bytes),
+        "grad_moments": (max(1, n_two), 4 * nm_bytes), "grad_carry": (max(1, n_two), None),
+        "grad_main": (max(1, n_two), 8 * nm_bytes), "sink_row": (safe_it, 4 * nm_bytes),
         "sink_col": (safe_it, 4 * nm_bytes), "sink_fused": (fused_it, 4 * nm_bytes),
-        "objective_pass": (1, 8 * nm_bytes)}
+        "objective_pass": (1, 8 * nm_bytes), "grad_onepass": (max(1, n_one), 8 * nm_bytes),
+        "sink_xm": (max(1, n_xm), 4 * nm_bytes)}
     kern = {}
     for k, name in enumerate(KERNELS):
-        if ms_c[k] <= 0:
+        if name is None or ms_c[k] <= 0:
             continue
         units, byt = per_unit[name]
         ms_unit = ms_c[k] / units
@@ -316,18 +321,35 @@ def main():
             "algorithmic_bytes_note": "4 B x N_local x M: one fp32 read of G per iteration (SURVEY §8d)",
             "share_of_step": sf["ms_total"] / prof_ms,
             "measured_in": "the second (instrumented) timed solve of the same configuration"}
-    grad_ms = sum(kern.get(k, {}).get("ms_total", 0.0) for k in ("grad_moments", "grad_carry", "grad_main"))
-    grad_ms /= args.steps
-    grad = {"ms_per_gradient": grad_ms, "algorithmic_bytes": 12 * nm_bytes,
-            "GBps_algorithmic": 12 * nm_bytes / (grad_ms / 1e3) / 1e9,
-            "frac_of_peak": 12 * nm_bytes / (grad_ms / 1e3) / 1e9 / hbm,
-            "frac_of_peak_at_8NM": 8 * nm_bytes / (grad_ms / 1e3) / 1e9 / hbm,
-            "bytes_note": "12NM is the floor of the exact gradient on the solver path (the row totals of T^l exist "
-                          "only after a read of the final plan: DESIGN.md 5.2b); frac_of_peak_at_8NM is SURVEY 8(d)'s "
-                          "accounting, which assumes the rank-2 term deferred into every Sinkhorn sweep",
-            "note": "moments pass (4NM) + main pass (8NM: read T or the cost it is regenerated from, write G); "
-                    "averaged over the solve's gradients, the first of which is on the product plan p q^T "
-                    "(no plan read), so this slightly flatters the Gibbs-mode gradient"}
+    two_ms = sum(kern.get(k, {}).get("ms_total", 0.0) for k in ("grad_moments", "grad_carry", "grad_main"))
+    one_ms = kern.get("grad_onepass", {}).get("ms_total", 0.0)
+    grad_ms = (two_ms + one_ms) / args.steps
+    if n_one > 0:
+        # the solver's gradient on T^l (l >= 1): one read of the cost + one write of G = 8 N M bytes
+        # (SURVEY 8(d) M1); the XM sweep that feeds it replaces one Sinkhorn iteration, and its extra time
+        # over a plain fused iteration is charged to the gradient in `incl_xm`
+        g1 = one_ms / n_one
+        xm_extra = 0.0
+        if "sink_xm" in kern and "sink_fused" in kern:
+            xm_extra = max(0.0, kern["sink_xm"]["ms_per_unit"] - kern["sink_fused"]["ms_per_unit"])
+        grad = {"path": "one-read (rowclu.cuh): XM sweep column moments + cluster row scans",
+                "ms_per_gradient": g1, "algorithmic_bytes": 8 * nm_bytes,
+                "GBps_algorithmic": 8 * nm_bytes / (g1 / 1e3) / 1e9,
+                "frac_of_peak": 8 * nm_bytes / (g1 / 1e3) / 1e9 / hbm,
+                "incl_xm": {"ms_per_gradient": g1 + xm_extra, "xm_extra_ms": xm_extra,
+                            "frac_of_peak": 8 * nm_bytes / ((g1 + xm_extra) / 1e3) / 1e9 / hbm},
+                "gradients": n_one,
+                "first_gradient_ms": two_ms / max(1, n_two),
+                "note": "averaged over the solve's gradients on T^l, l >= 1; the first gradient (on the product "
+                        "plan p q^T, no plan read) runs the two-read kernels and is reported as first_gradient_ms"}
+    else:
+        grad = {"path": "two-read (moments pass + main pass)", "ms_per_gradient": grad_ms,
+                "algorithmic_bytes": 12 * nm_bytes,
+                "GBps_algorithmic": 12 * nm_bytes / (grad_ms / 1e3) / 1e9,
+                "frac_of_peak": 12 * nm_bytes / (grad_ms / 1e3) / 1e9 / hbm,
+                "frac_of_peak_at_8NM": 8 * nm_bytes / (grad_ms / 1e3) / 1e9 / hbm,
+                "note": "moments pass (4NM) + main pass (8NM); the one-read path is off (GWDP_NO_RC=1, several "
+                        "ranks, or an unsupported variant)"}
     sink_gbps_step = 4 * nm_bytes * args.inner / ((elapsed_ms - grad_ms * args.steps) / args.steps / 1e3) / 1e9
     instrumented = {"ms_per_step": prof_ms / args.steps, "note": "the same solve with per-kernel-class events "
                     "(eager launches, no graphs): the source of `kernels`, `grad` and `roofline`"}

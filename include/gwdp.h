@@ -55,7 +55,7 @@
 extern "C" {
 #endif
 
-#define GWDP_ABI_VERSION 1
+#define GWDP_ABI_VERSION 2
 
 typedef struct gw_ctx gw_ctx;    /* opaque: device, stream, workspace, optional comm */
 typedef struct gw_comm gw_comm;  /* opaque: NCCL communicator, rank, world size      */
@@ -147,6 +147,8 @@ typedef struct {
   int32_t outer_iters, inner_iters_total, converged;
   int32_t inner_fused_total;  /* Sinkhorn iterations that ran the fused one-read path    */
   double ms_grad, ms_sinkhorn, ms_total;
+  int32_t grad_onepass_total; /* gradients evaluated in one read of the cost + one write  */
+                              /* (8 N M bytes): k = 1, one rank          */
 } gw_result;
 
 /* ---- context / communicator ------------------------------------------------------ */
@@ -160,9 +162,11 @@ gw_status gw_ctx_trim(gw_ctx *ctx);
 /* Kernel-class timing with CUDA events on ctx's stream (for measurement harnesses).
  * enable: 0 off, 1 on, 2 on + reset totals.  out_ms / out_counts (host, nullable) receive
  * `nslots` entries: {grad_moments, grad_carry, grad_main, sink_row, sink_col, sink_fused,
- * objective_pass} accumulated since the last reset (sink_col and sink_fused count their two
- * launches per iteration; objective_pass counts one per final-objective pass); with
- * nslots >= 8, out_counts[7] = all kernel launches of the library since the last reset.
+ * objective_pass, -, grad_onepass, sink_xm} accumulated since the last reset (sink_col,
+ * sink_fused and sink_xm count their two launches per iteration; objective_pass counts one per
+ * final-objective pass; grad_onepass: the one-read gradient, its carries included, one per
+ * gradient; sink_xm: the last Sinkhorn iteration of an inner loop on that path); slot 7 has no
+ * time: out_counts[7] = all kernel launches of the library since the last reset.
  * Synchronises ctx's stream. */
 gw_status gw_ctx_profile(gw_ctx *ctx, int enable, double *out_ms, int64_t *out_counts, int nslots);
 const char *gw_last_error(void);

@@ -67,7 +67,8 @@ class gw_result(C.Structure):
     _fields_ = [("gw_objective", C.c_double), ("entropic_objective", C.c_double),
                 ("marginal_violation", C.c_double), ("outer_iters", C.c_int32),
                 ("inner_iters_total", C.c_int32), ("converged", C.c_int32), ("inner_fused_total", C.c_int32),
-                ("ms_grad", C.c_double), ("ms_sinkhorn", C.c_double), ("ms_total", C.c_double)]
+                ("ms_grad", C.c_double), ("ms_sinkhorn", C.c_double), ("ms_total", C.c_double),
+                ("grad_onepass_total", C.c_int32)]
 
 
 # int (*gw_allgather_fn)(const void *send, void *recv, int64_t bytes, void *user)

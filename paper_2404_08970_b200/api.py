@@ -162,13 +162,14 @@ class Result:
     T: Optional[object] = None
     trace: Optional[np.ndarray] = None   # [outer, 4]: E(T^l), violation, inner iters, ms
     inner_fused_total: int = 0
+    grad_onepass_total: int = 0          # gradients on the one-read (8 N M) path
     extra: dict = field(default_factory=dict)
 
 
 def _result(res, f, g, T, tr):
     return Result(res.gw_objective, res.entropic_objective, res.marginal_violation, res.outer_iters,
                   res.inner_iters_total, bool(res.converged), res.ms_grad, res.ms_sinkhorn, res.ms_total,
-                  f, g, T, tr, res.inner_fused_total)
+                  f, g, T, tr, res.inner_fused_total, res.grad_onepass_total)
 
 
 def _opts(eps, outer, inner, tol, check_every, trace_objective, tau=None):

@@ -45,6 +45,12 @@ struct FusedArgs {
   int64_t wcol;               // columns per CTA (k_sink_fused2; <= the stage capacity 4 K NT)
   const int* mode;            // run only if *mode == 1
   const int* stop;
+  // XM instantiation (the last sweep of an inner loop on the 8 N M gradient path, rowclu.cuh): the
+  // exponent in the Gibbs-regeneration form (lo parts of the duals and of log2e/eps included), and
+  // the column sums of x_i e_ip w_i beside those of e_ip w_i
+  float c2f_lo;               // lo part of log2e/eps
+  const float* xr;            // centred x (fp32, local rows)
+  double* partx;              // [nclusters][m]
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -166,9 +172,9 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
 
 // W = 4 K NT columns per CTA.  Dynamic shared memory: the TMA ring [FSTAGES][W] fp32, then the
 // fp64 column accumulators [K][4][NT] (conflict-free: lane-contiguous doubles).
-template <int K, int NT>
+template <int K, int NT, bool XM = false>
 constexpr size_t fused_dyn_smem() {
-  return (size_t)fstages<NT>() * 4 * K * NT * sizeof(float) + (size_t)4 * K * NT * sizeof(double);
+  return (size_t)fstages<NT>() * 4 * K * NT * sizeof(float) + (size_t)(XM ? 2 : 1) * 4 * K * NT * sizeof(double);
 }
 
 // Exponentiate one row slice: e = 2^(fma(G, -log2e/eps, gh) + F) for the thread's 4K columns
@@ -183,6 +189,39 @@ __device__ __forceinline__ float fused_exp_row(const float4* __restrict__ sp, co
     const float4 gv = sp[t + NT * k];
     const float2 a0 = fadd2(ffma2(make_float2(gv.x, gv.y), nc2, ghv[k][0]), F2);
     const float2 a1 = fadd2(ffma2(make_float2(gv.z, gv.w), nc2, ghv[k][1]), F2);
+    float2 e0 = make_float2(ex2_ftz(a0.x), ex2_ftz(a0.y));
+    float2 e1 = make_float2(ex2_ftz(a1.x), ex2_ftz(a1.y));
+    if (!FULL) {
+      const int64_t col = c0 + 4 * (t + NT * k);
+      if (col >= m) e0.x = 0.f;
+      if (col + 1 >= m) e0.y = 0.f;
+      if (col + 2 >= m) e1.x = 0.f;
+      if (col + 3 >= m) e1.y = 0.f;
+    }
+    ec[k][0] = e0;
+    ec[k][1] = e1;
+    ps[k] = fadd2(e0, e1);
+  }
+#pragma unroll
+  for (int w = 1; w < K; w <<= 1)
+#pragma unroll
+    for (int k = 0; k + w < K; k += 2 * w) ps[k] = fadd2(ps[k], ps[k + w]);
+  return ps[0].x + ps[0].y;
+}
+
+// XM: the same with the Gibbs-regeneration exponent a = [fma(G, -c_hi, g_hi) + F_hi] +
+// [fma(G, -c_lo, g_lo + F_lo)] (grad2.cuh), so that e is the plan the gradient regenerates
+template <int K, int NT, bool FULL>
+__device__ __forceinline__ float fused_exp_row_xm(const float4* __restrict__ sp, const float2 (&ghv)[K][2],
+                                                  const float2 (&glv)[K][2], float2 nc2, float2 ncl2, float2 F2,
+                                                  float2 Fl2, float2 (&ec)[K][2], int t, int64_t c0, int64_t m) {
+  float2 ps[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const float4 gv = sp[t + NT * k];
+    const float2 g01 = make_float2(gv.x, gv.y), g23 = make_float2(gv.z, gv.w);
+    const float2 a0 = fadd2(fadd2(ffma2(g01, nc2, ghv[k][0]), F2), ffma2(g01, ncl2, fadd2(glv[k][0], Fl2)));
+    const float2 a1 = fadd2(fadd2(ffma2(g23, nc2, ghv[k][1]), F2), ffma2(g23, ncl2, fadd2(glv[k][1], Fl2)));
     float2 e0 = make_float2(ex2_ftz(a0.x), ex2_ftz(a0.y));
     float2 e1 = make_float2(ex2_ftz(a1.x), ex2_ftz(a1.y));
     if (!FULL) {
@@ -224,8 +263,10 @@ __device__ __forceinline__ void st_async_v2f32(uint32_t raddr, float v0, float v
 // "+ F" cancels exactly; the dropped lo parts are per-row / per-column scalings that the
 // iteration's normalisations absorb.
 // UGW: the unbalanced row factor (a separate instantiation: the balanced kernel carries no trace of it)
-template <int K, int CL, int NT, bool UGW>
+// XM: Gibbs-regeneration exponent + column sums of x_i e_ip w_i (see FusedArgs; balanced only)
+template <int K, int CL, int NT, bool UGW, bool XM = false>
 __global__ void __launch_bounds__(NT, 1) k_sink_fused2(FusedArgs a) {
+  static_assert(!(UGW && XM), "XM is balanced only");
   if (*a.mode != 1 || (a.stop && *a.stop)) return;  // uniform across the cluster
   constexpr int NW = NT / 32;
   constexpr int W = 4 * K * NT;
@@ -234,6 +275,7 @@ __global__ void __launch_bounds__(NT, 1) k_sink_fused2(FusedArgs a) {
   constexpr int NX = CL * NW;    // partial pairs per row pair
   extern __shared__ __align__(128) float ring[];  // [FSTAGES][W], then acc64 [K][4][NT] (fp64)
   double* acc64 = reinterpret_cast<double*>(ring + (size_t)FSTAGES * W);
+  double* acc64x = acc64 + (size_t)4 * K * NT;  // XM only
   __shared__ __align__(8) uint64_t full[FSTAGES];
   __shared__ unsigned int scnt[FSTAGES];
   __shared__ __align__(8) uint64_t xbar[NSLOT];
@@ -291,6 +333,7 @@ __global__ void __launch_bounds__(NT, 1) k_sink_fused2(FusedArgs a) {
   const bool full_tile = !((c0 + ncol >= m) && (m & 3));
 
   float2 ghv[K][2], acc[K][2];
+  float2 glv[K][2], accx[K][2];  // XM only
 #pragma unroll
   for (int k = 0; k < K; ++k)
 #pragma unroll
@@ -302,24 +345,46 @@ __global__ void __launch_bounds__(NT, 1) k_sink_fused2(FusedArgs a) {
       acc[k][h] = make_float2(0.f, 0.f);
       acc64[(k * 4 + 2 * h) * NT + t] = 0.0;
       acc64[(k * 4 + 2 * h + 1) * NT + t] = 0.0;
+      if (XM) {
+        glv[k][h].x = (lc < ncol && col < m) ? a.gl[col] : 0.f;
+        glv[k][h].y = (lc + 1 < ncol && col + 1 < m) ? a.gl[col + 1] : 0.f;
+        accx[k][h] = make_float2(0.f, 0.f);
+        acc64x[(k * 4 + 2 * h) * NT + t] = 0.0;
+        acc64x[(k * 4 + 2 * h + 1) * NT + t] = 0.0;
+      }
     }
   const float2 nc2 = make_float2(-a.c2f, -a.c2f);
+  const float2 ncl2 = make_float2(-a.c2f_lo, -a.c2f_lo);  // XM only
   constexpr bool ugw = UGW;
   const float km1 = a.kappa - 1.f;
   float2 eA0[K][2], eA1[K][2], eB0[K][2], eB1[K][2];
   float2 pA = make_float2(0.f, 0.f), pB = pA;  // marginals of the pair's two rows
+  float2 xA = pA, xB = pA;                       // XM: their x
   float2 Fnx = make_float2(nrows > 0 ? fh[0] : 0.f, nrows > 1 ? fh[1] : 0.f);
   float2 pnx = make_float2(nrows > 0 ? pf[0] : 0.f, nrows > 1 ? pf[1] : 0.f);
+  const float* __restrict__ flr = a.fl + rb;
+  const float* __restrict__ xr = XM ? a.xr + rb : nullptr;
+  float2 Flnx = make_float2(0.f, 0.f), xnx = Flnx;
+  if (XM) {
+    Flnx = make_float2(nrows > 0 ? flr[0] : 0.f, nrows > 1 ? flr[1] : 0.f);
+    xnx = make_float2(nrows > 0 ? xr[0] : 0.f, nrows > 1 ? xr[1] : 0.f);
+  }
 
   // exponentiate row j into e (returns the thread's partial row sum) and release its stage
-  auto do_row = [&](int j, float F, float2 (&e)[K][2]) -> float {
+  auto do_row = [&](int j, float F, float Fl, float2 (&e)[K][2]) -> float {
     float psum = 0.f;
     if (bytes > 0) {
       const int st = j % FSTAGES;
       mbar_wait(&full[st], (uint32_t)((j / FSTAGES) & 1));
       const float4* sp = reinterpret_cast<const float4*>(ring + (size_t)st * W);
-      psum = full_tile ? fused_exp_row<K, NT, true>(sp, ghv, nc2, make_float2(F, F), e, t, c0, m)
-                       : fused_exp_row<K, NT, false>(sp, ghv, nc2, make_float2(F, F), e, t, c0, m);
+      if (XM)
+        psum = full_tile ? fused_exp_row_xm<K, NT, true>(sp, ghv, glv, nc2, ncl2, make_float2(F, F),
+                                                         make_float2(Fl, Fl), e, t, c0, m)
+                         : fused_exp_row_xm<K, NT, false>(sp, ghv, glv, nc2, ncl2, make_float2(F, F),
+                                                          make_float2(Fl, Fl), e, t, c0, m);
+      else
+        psum = full_tile ? fused_exp_row<K, NT, true>(sp, ghv, nc2, make_float2(F, F), e, t, c0, m)
+                         : fused_exp_row<K, NT, false>(sp, ghv, nc2, make_float2(F, F), e, t, c0, m);
       __syncwarp();
       if (lane == 0) {  // the last warp to release a stage refills it
         const int nxt = j + FSTAGES;
@@ -340,12 +405,19 @@ __global__ void __launch_bounds__(NT, 1) k_sink_fused2(FusedArgs a) {
   };
 
   // Step P: rows 2P, 2P+1 (exponentiate + send), then consume pair P-1.
-  auto step = [&](int P, float2 (&c0e)[K][2], float2 (&c1e)[K][2], float2& pcur, float2 (&v0)[K][2],
-                  float2 (&v1)[K][2], float2 pprv) {
+  auto step = [&](int P, float2 (&c0e)[K][2], float2 (&c1e)[K][2], float2& pcur, float2& xcur, float2 (&v0)[K][2],
+                  float2 (&v1)[K][2], float2 pprv, float2 xprv) {
     const int j0 = 2 * P, j1 = 2 * P + 1;
     if (j0 < nrows) {
       const float2 F = Fnx;
       pcur = pnx;
+      float2 Fl = make_float2(0.f, 0.f);
+      if (XM) {
+        Fl = Flnx;
+        xcur = xnx;
+        if (j0 + 2 < nrows) Flnx.x = flr[j0 + 2], xnx.x = xr[j0 + 2];
+        if (j1 + 2 < nrows) Flnx.y = flr[j1 + 2], xnx.y = xr[j1 + 2];
+      }
       if (ugw) {  // the row factor's constant part log2 u + (kappa - 1) F (F: the hi part the row uses)
         pcur.x = fmaf(km1, F.x, pcur.x);
         pcur.y = fmaf(km1, F.y, pcur.y);
@@ -366,10 +438,17 @@ __global__ void __launch_bounds__(NT, 1) k_sink_fused2(FusedArgs a) {
 #pragma unroll
         for (int k = 0; k < K; ++k) {
           const float4 g0 = sp0[t + NT * k], g1 = sp1[t + NT * k];
-          const float2 a00 = fadd2(ffma2(make_float2(g0.x, g0.y), nc2, ghv[k][0]), F0);
-          const float2 a01 = fadd2(ffma2(make_float2(g0.z, g0.w), nc2, ghv[k][1]), F0);
-          const float2 a10 = fadd2(ffma2(make_float2(g1.x, g1.y), nc2, ghv[k][0]), F1);
-          const float2 a11 = fadd2(ffma2(make_float2(g1.z, g1.w), nc2, ghv[k][1]), F1);
+          float2 a00 = fadd2(ffma2(make_float2(g0.x, g0.y), nc2, ghv[k][0]), F0);
+          float2 a01 = fadd2(ffma2(make_float2(g0.z, g0.w), nc2, ghv[k][1]), F0);
+          float2 a10 = fadd2(ffma2(make_float2(g1.x, g1.y), nc2, ghv[k][0]), F1);
+          float2 a11 = fadd2(ffma2(make_float2(g1.z, g1.w), nc2, ghv[k][1]), F1);
+          if (XM) {  // the lo bracket of the Gibbs-regeneration exponent
+            const float2 L0 = make_float2(Fl.x, Fl.x), L1 = make_float2(Fl.y, Fl.y);
+            a00 = fadd2(a00, ffma2(make_float2(g0.x, g0.y), ncl2, fadd2(glv[k][0], L0)));
+            a01 = fadd2(a01, ffma2(make_float2(g0.z, g0.w), ncl2, fadd2(glv[k][1], L0)));
+            a10 = fadd2(a10, ffma2(make_float2(g1.x, g1.y), ncl2, fadd2(glv[k][0], L1)));
+            a11 = fadd2(a11, ffma2(make_float2(g1.z, g1.w), ncl2, fadd2(glv[k][1], L1)));
+          }
           c0e[k][0] = make_float2(ex2_ftz(a00.x), ex2_ftz(a00.y));
           c0e[k][1] = make_float2(ex2_ftz(a01.x), ex2_ftz(a01.y));
           c1e[k][0] = make_float2(ex2_ftz(a10.x), ex2_ftz(a10.y));
@@ -395,10 +474,10 @@ __global__ void __launch_bounds__(NT, 1) k_sink_fused2(FusedArgs a) {
           }
         }
       } else if (j1 < nrows) {
-        s0 = do_row(j0, F.x, c0e);
-        s1 = do_row(j1, F.y, c1e);
+        s0 = do_row(j0, F.x, Fl.x, c0e);
+        s1 = do_row(j1, F.y, Fl.y, c1e);
       } else {
-        s0 = do_row(j0, F.x, c0e);
+        s0 = do_row(j0, F.x, Fl.x, c0e);
 #pragma unroll
         for (int k = 0; k < K; ++k) { c1e[k][0] = make_float2(0.f, 0.f); c1e[k][1] = c1e[k][0]; }
         pcur.y = 0.f;
@@ -459,6 +538,15 @@ __global__ void __launch_bounds__(NT, 1) k_sink_fused2(FusedArgs a) {
         acc[k][0] = ffma2(v1[k][0], w12, ffma2(v0[k][0], w02, acc[k][0]));
         acc[k][1] = ffma2(v1[k][1], w12, ffma2(v0[k][1], w02, acc[k][1]));
       }
+      if (XM) {
+        const float wx0 = w0 * xprv.x, wx1 = w1 * xprv.y;
+        const float2 wx02 = make_float2(wx0, wx0), wx12 = make_float2(wx1, wx1);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          accx[k][0] = ffma2(v1[k][0], wx12, ffma2(v0[k][0], wx02, accx[k][0]));
+          accx[k][1] = ffma2(v1[k][1], wx12, ffma2(v0[k][1], wx02, accx[k][1]));
+        }
+      }
       if ((Pp & (FFLUSH / 2 - 1)) == FFLUSH / 2 - 1) {
 #pragma unroll
         for (int k = 0; k < K; ++k)
@@ -467,13 +555,18 @@ __global__ void __launch_bounds__(NT, 1) k_sink_fused2(FusedArgs a) {
             acc64[(k * 4 + 2 * h) * NT + t] += (double)acc[k][h].x;
             acc64[(k * 4 + 2 * h + 1) * NT + t] += (double)acc[k][h].y;
             acc[k][h] = make_float2(0.f, 0.f);
+            if (XM) {
+              acc64x[(k * 4 + 2 * h) * NT + t] += (double)accx[k][h].x;
+              acc64x[(k * 4 + 2 * h + 1) * NT + t] += (double)accx[k][h].y;
+              accx[k][h] = make_float2(0.f, 0.f);
+            }
           }
       }
     }
   };
   for (int P = 0; P <= npairs; P += 2) {
-    step(P, eA0, eA1, pA, eB0, eB1, pB);
-    if (P + 1 <= npairs) step(P + 1, eB0, eB1, pB, eA0, eA1, pA);
+    step(P, eA0, eA1, pA, xA, eB0, eB1, pB, xB);
+    if (P + 1 <= npairs) step(P + 1, eB0, eB1, pB, xB, eA0, eA1, pA, xA);
   }
 #pragma unroll
   for (int k = 0; k < K; ++k)
@@ -485,6 +578,12 @@ __global__ void __launch_bounds__(NT, 1) k_sink_fused2(FusedArgs a) {
       const double v1 = acc64[(k * 4 + 2 * h + 1) * NT + t] + (double)acc[k][h].y;
       if (lc < ncol && col < m) a.part[cid * m + col] = v0;
       if (lc + 1 < ncol && col + 1 < m) a.part[cid * m + col + 1] = v1;
+      if (XM) {
+        const double x0 = acc64x[(k * 4 + 2 * h) * NT + t] + (double)accx[k][h].x;
+        const double x1 = acc64x[(k * 4 + 2 * h + 1) * NT + t] + (double)accx[k][h].y;
+        if (lc < ncol && col < m) a.partx[cid * m + col] = x0;
+        if (lc + 1 < ncol && col + 1 < m) a.partx[cid * m + col + 1] = x1;
+      }
     }
   cluster_arrive();
   cluster_wait();

@@ -16,6 +16,7 @@
 #include "../../include/gwdp.h"
 #include "common.cuh"
 #include "fused.cuh"
+#include "rowclu.cuh"
 #include "grad.cuh"
 #include "grad2.cuh"
 #include "shard.cuh"
@@ -81,7 +82,9 @@ struct gw_comm {
 };
 
 // Per-kernel-class CUDA-event timing (enabled by gw_ctx_profile; events on ctx's stream).
-enum { PC_GRAD_MOMENTS = 0, PC_GRAD_CARRY, PC_GRAD_MAIN, PC_SINK_ROW, PC_SINK_COL, PC_SINK_FUSED, PC_OBJ, PC_N };
+// slot 7 of gw_ctx_profile is the count of all kernel launches (no class of its own)
+enum { PC_GRAD_MOMENTS = 0, PC_GRAD_CARRY, PC_GRAD_MAIN, PC_SINK_ROW, PC_SINK_COL, PC_SINK_FUSED, PC_OBJ, PC_LAUNCHES,
+       PC_GRAD_ONEPASS, PC_SINK_XM, PC_N };
 struct Prof {
   bool on = false;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
@@ -116,6 +119,7 @@ struct gw_ctx {
   Buf sflag, sflagg;
   Buf fsc, gsc;  // scaled duals for the Gibbs regeneration
   Buf Gs;        // solver cost buffer
+  Buf rcp, rcpx, rcv, rcvx, rcu, rcz, rcxf, rccx, rccy, rcflag;  // 8 N M solver gradient (rowclu.cuh)
   double* hpin = nullptr;  // pinned host scratch (64 doubles)
   // one-shot debug export for the next solve (gw_solve_set_export)
   struct {
@@ -131,7 +135,8 @@ struct gw_ctx {
                 &sviolg, &sflag, &sflagg, &yfb, &pcoef, &pc2s, &pfx, &pfy, &ppart, &pM, &p4coef, &p4c2,
                 &gkrp, &gkrt, &gkcp, &gkz, &gkct, &gkctt, &gkobj, &gkseg,
                 &uga, &ugb, &ugct, &ugpart, &ugca, &ugcb, &ugfr, &uggr, &ugsc, &ugrpart,
-                &g2rc, &g2rd, &g2h, &g2cc, &g2tt, &g2vt, &g2tmp, &g2s, &g2a, &g2b, &g2ca, &g2cb, &g2part};
+                &g2rc, &g2rd, &g2h, &g2cc, &g2tt, &g2vt, &g2tmp, &g2s, &g2a, &g2b, &g2ca, &g2cb, &g2part,
+                &rcp, &rcpx, &rcv, &rcvx, &rcu, &rcz, &rcxf, &rccx, &rccy, &rcflag};
     for (Buf* x : b) all.push_back(x);
   }
 };
@@ -241,10 +246,9 @@ extern "C" gw_status gw_ctx_profile(gw_ctx* c, int enable, double* out_ms, int64
     P.used = 0;
   }
   for (int k = 0; k < nslots && k < PC_N; ++k) {
-    if (out_ms) out_ms[k] = P.ms[k];
-    if (out_counts) out_counts[k] = P.cnt[k];
+    if (out_ms) out_ms[k] = k == PC_LAUNCHES ? 0.0 : P.ms[k];
+    if (out_counts) out_counts[k] = k == PC_LAUNCHES ? c->launches : P.cnt[k];  // slot 7: all kernel launches
   }
-  if (nslots > PC_N && out_counts) out_counts[PC_N] = c->launches;  // all kernel launches
   if (enable == 2) {
     for (int k = 0; k < PC_N; ++k) { P.ms[k] = 0; P.cnt[k] = 0; }
     c->launches = 0;
@@ -1300,11 +1304,21 @@ struct SinkState {
   int *flag, *flagg;  // speculation validity flag (and the ranks' flags)
   cudaGraphExec_t gexec = nullptr;  // one fixed-count iteration, captured once per solve
   double g_eps = 0.0, g_kappa = 0.0;  // the scalars baked into gexec (UGW changes them per outer iteration)
+  // 8 N M solver gradient (rowclu.cuh): the last sweep of an inner loop runs the XM instantiation over
+  // rcncl clusters of rcCL CTAs (4096 columns each, rcrpc rows per cluster), the same partition as the
+  // gradient's main pass; rcCL == 0: unavailable for this problem
+  int rcCL = 0, rcncl = 0;
+  int64_t rcrpc = 0;
+  double *rcpart = nullptr, *rcpartx = nullptr;
+  float *xf = nullptr, *ccx = nullptr, *ccy = nullptr;
+  int* xmv = nullptr;               // set on the device when the XM sweep ran and was committed
+  cudaGraphExec_t gexec_xm = nullptr;  // the same iteration with the XM sweep
 };
 
 static void sink_free(SinkState& s) {
   if (s.gexec) cudaGraphExecDestroy(s.gexec);
-  s.gexec = nullptr;
+  if (s.gexec_xm) cudaGraphExecDestroy(s.gexec_xm);
+  s.gexec = s.gexec_xm = nullptr;
 }
 // CUDA events owned by one call, destroyed on every exit path (errors included)
 struct EventSet {
@@ -1389,6 +1403,114 @@ static gw_status fused_launch(gw_ctx* c, int K, int CL, int NT, const FusedArgs&
   FUSED_DISPATCH(fused_launch_t, c, fa, ncl)
 }
 
+// XM instantiation (K = 4, NT = 256: 4096 columns per CTA) and the gradient main pass, CL in {1,...,16}
+template <int CL>
+static gw_status rc_config_t(gw_ctx* c, int* ncl) {
+  auto kx = k_sink_fused2<4, CL, 256, false, true>;
+  auto kg = k_grad_rc<CL>;
+  const size_t dx = fused_dyn_smem<4, 256, true>(), dg = rc_dyn_smem();
+  CU(cudaFuncSetAttribute(kx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dx));
+  CU(cudaFuncSetAttribute(kg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dg));
+  if (CL > 8) {
+    CU(cudaFuncSetAttribute(kx, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CU(cudaFuncSetAttribute(kg, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  }
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(148 * CL);
+  cfg.blockDim = dim3(256);
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int nx = 0, ng = 0;
+  cfg.dynamicSmemBytes = dx;
+  CU(cudaOccupancyMaxActiveClusters(&nx, (void*)kx, &cfg));
+  cfg.dynamicSmemBytes = dg;
+  CU(cudaOccupancyMaxActiveClusters(&ng, (void*)kg, &cfg));
+  *ncl = std::min(nx, ng);
+  return GW_OK;
+}
+template <int CL>
+static gw_status rc_xm_launch_t(gw_ctx* c, const FusedArgs& fa, int ncl) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ncl * CL);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = fused_dyn_smem<4, 256, true>();
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CU(cudaLaunchKernelEx(&cfg, k_sink_fused2<4, CL, 256, false, true>, fa));
+  return GW_OK;
+}
+template <int CL>
+static gw_status rc_grad_launch_t(gw_ctx* c, const CUtensorMap& tm, const RcArgs& ra, int ncl) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ncl * CL);
+  cfg.blockDim = dim3(RC_NT);
+  cfg.dynamicSmemBytes = rc_dyn_smem();
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CU(cudaLaunchKernelEx(&cfg, k_grad_rc<CL>, tm, ra));
+  return GW_OK;
+}
+#define RC_DISPATCH(FN, CL, ...)                                                        \
+  switch (CL) {                                                                         \
+    case 1: return FN<1>(__VA_ARGS__);                                                  \
+    case 2: return FN<2>(__VA_ARGS__);                                                  \
+    case 4: return FN<4>(__VA_ARGS__);                                                  \
+    case 8: return FN<8>(__VA_ARGS__);                                                  \
+    case 16: return FN<16>(__VA_ARGS__);                                                \
+    default: return fail(GW_ERR_UNSUPPORTED, "8NM gradient: no instance CL=%d", CL);   \
+  }
+static gw_status rc_config(gw_ctx* c, int CL, int* ncl) { RC_DISPATCH(rc_config_t, CL, c, ncl) }
+static gw_status rc_xm_launch(gw_ctx* c, int CL, const FusedArgs& fa, int ncl) { RC_DISPATCH(rc_xm_launch_t, CL, c, fa, ncl) }
+static gw_status rc_grad_launch(gw_ctx* c, int CL, const CUtensorMap& tm, const RcArgs& ra, int ncl) {
+  RC_DISPATCH(rc_grad_launch_t, CL, c, tm, ra, ncl)
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no link against libcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+// The solver's cost buffer as a 3-D tensor {32, ld / 32, nl} (fp32, 128-B lines) read in boxes of
+// {32, 128, 1} = one 4096-column row slice, 128-byte swizzle (rowclu.cuh)
+static gw_status rc_tensor_map(gw_ctx* c, const float* G, int64_t ld, int64_t nl, CUtensorMap* tm) {
+  static EncodeTiledFn enc = nullptr;
+  if (!enc) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CU(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) return fail(GW_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    enc = reinterpret_cast<EncodeTiledFn>(fn);
+  }
+  if (ld % 32 != 0 || (reinterpret_cast<uintptr_t>(G) & 15))
+    return fail(GW_ERR_INVALID_ARG, "8NM gradient: the cost buffer needs ld %% 32 == 0 and 16-B alignment");
+  const cuuint64_t dims[3] = {32, (cuuint64_t)(ld / 32), (cuuint64_t)std::max<int64_t>(nl, 1)};
+  const cuuint64_t strides[2] = {128, (cuuint64_t)ld * 4};
+  const cuuint32_t box[3] = {32, 128, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(G), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(GW_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return GW_OK;
+}
+
+// XM sweep validity: set when the last iteration ran the XM fused kernel and passed its check (before
+// k_sink_fin_fast, which may switch *mode)
+__global__ void k_xm_mark(const int* __restrict__ mode, const int* __restrict__ flag, const int* __restrict__ stop,
+                          int* __restrict__ xmv) {
+  if (threadIdx.x == 0) *xmv = (*mode == 1 && *flag == 0 && !(stop && *stop)) ? 1 : 0;
+}
+
 static gw_status sink_alloc(gw_ctx* c, const Prepared& P, SinkState& s) {
   TRY(ws(c, c->fh, P.nl, &s.fh)); TRY(ws(c, c->fl, P.nl, &s.fl));
   TRY(ws(c, c->gh, P.m, &s.gh)); TRY(ws(c, c->gl, P.m, &s.gl));
@@ -1462,6 +1584,60 @@ static gw_status sink_alloc(gw_ctx* c, const Prepared& P, SinkState& s) {
       }
     }
   }
+  // 8 N M solver gradient: one rank, k = 1 on 1-D supports, M <= 16 x 4096 (opt-in while it is slower
+  // than the two-read path: GWDP_RC=1 enables it, GWDP_NO_RC=1 disables it)
+  s.rcCL = 0;
+  const char* nrc = getenv("GWDP_NO_RC");
+  const char* yrc = getenv("GWDP_RC");
+  if (!(nrc && nrc[0] == '1') && (yrc && yrc[0] == '1') && s.fK > 0 && P.R == 1 && P.k == 1 && !P.grid2d && P.nl > 0 && P.m <= 16 * RC_W) {
+    int CL = 1;
+    while ((int64_t)CL * RC_W < P.m) CL *= 2;
+    int ncl = 0;
+    TRY(rc_config(c, CL, &ncl));
+    if (ncl > 0) {
+      ncl = (int)std::min<int64_t>(ncl, P.nl);
+      s.rcCL = CL;
+      s.rcncl = ncl;
+      s.rcrpc = (P.nl + ncl - 1) / ncl;
+      TRY(ws(c, c->rcp, (size_t)ncl * P.m, &s.rcpart));
+      TRY(ws(c, c->rcpx, (size_t)ncl * P.m, &s.rcpartx));
+      TRY(ws(c, c->rcxf, (size_t)P.nl, &s.xf));
+      TRY(ws(c, c->rccx, (size_t)P.nl, &s.ccx));
+      TRY(ws(c, c->rccy, (size_t)P.m, &s.ccy));
+      TRY(ws(c, c->rcflag, 4, &s.xmv));
+      k_to_float<<<grid_for(P.nl), 256, 0, c->stream>>>(P.xc + P.row0, P.nl, s.xf);
+      k_scale_f<<<grid_for(P.nl), 256, 0, c->stream>>>(P.cx + P.row0, P.nl, 2.0, s.ccx);
+      k_scale_f<<<grid_for(P.m), 256, 0, c->stream>>>(P.cy, P.m, 2.0, s.ccy);
+      KCHECK();
+    }
+  }
+  return GW_OK;
+}
+
+// The solver's gradient on the 8 N M path (rowclu.cuh), k = 1, one rank: requires that the last
+// Sinkhorn iteration ran the XM sweep (s.rcpart / s.rcpartx / s.csl hold its column sums).
+static gw_status grad_rc(gw_ctx* c, const Prepared& P, SinkState& s, float* G, int64_t ldG, const TSrc2& S2) {
+  const int64_t nl = P.nl, m = P.m;
+  const int ncl = s.rcncl;
+  double *V, *VX, *U0, *Z0;
+  TRY(ws(c, c->rcv, (size_t)ncl * m, &V));
+  TRY(ws(c, c->rcvx, (size_t)ncl * m, &VX));
+  TRY(ws(c, c->rcu, (size_t)ncl * m, &U0));
+  TRY(ws(c, c->rcz, (size_t)ncl * m, &Z0));
+  PROF_BEGIN(c, PC_GRAD_ONEPASS);
+  k_rc_vec<<<grid_for(m), 256, 0, c->stream>>>(s.rcpart, s.rcpartx, ncl, m, s.csl, P.lq, V, VX);
+  KCHECK();
+  k_rc_dy<<<2 * ncl, 1024, 0, c->stream>>>(V, VX, ncl, m, P.yc, U0, Z0);
+  KCHECK();
+  CUtensorMap tm;
+  TRY(rc_tensor_map(c, G, ldG, nl, &tm));
+  RcArgs ra;
+  ra.G = G; ra.ld = ldG; ra.nl = nl; ra.m = m; ra.rows_per_cluster = s.rcrpc;
+  ra.fh = S2.fh; ra.fl = S2.fl; ra.gh = S2.gh; ra.gl = S2.gl; ra.ch = S2.ch; ra.cl = S2.cl;
+  ra.xf = s.xf; ra.ccx = s.ccx; ra.yf = P.yf; ra.ccy = s.ccy; ra.U0 = U0; ra.Zn0 = Z0;
+  TRY(rc_grad_launch(c, s.rcCL, tm, ra, ncl));
+  KCHECK();
+  PROF_END(c, PC_GRAD_ONEPASS, 1);
   return GW_OK;
 }
 
@@ -1533,7 +1709,7 @@ static int small_cluster(gw_ctx* c, const Prepared& P, int* rows_out, size_t* by
 // absorbed-dual form (P.lp, P.lq = ln u, ln v); 1 = balanced.
 static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const float* G, int64_t ldG, double eps,
                           int iters, double tol, int check_every, int* used, int* converged, bool reset_count = true,
-                          double kappa = 1.0) {
+                          double kappa = 1.0, bool xm = false) {
   NvtxRange nv("gw.sinkhorn");
   const int64_t nl = P.nl, m = P.m;
   const float c2f = (float)(GW_LOG2E / eps);
@@ -1563,15 +1739,33 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
   // the fused one-read step of one iteration (speculative; a no-op unless *mode == 1)
   cudaGraphConditionalHandle cond_h = 0;  // set while capturing the single-rank iteration graph
   int use_cond = 0;
-  auto fused_step = [&]() -> gw_status {
+  // XM sweep (the last iteration of the inner loop on the 8 N M gradient path): only in the fixed-count
+  // single-rank graph loop below; s.xmv tells the caller whether it ran and was committed
+  xm = xm && s.rcCL > 0 && s.fK > 0 && P.R == 1 && kappa == 1.0 && tol <= 0;
+  if (s.xmv) CU(cudaMemsetAsync(s.xmv, 0, sizeof(int), c->stream));
+  FusedArgs fax = fa;
+  if (xm) {
+    const double cc = GW_LOG2E / eps;
+    fax.c2f_lo = (float)(cc - (double)c2f);
+    fax.xr = s.xf;
+    fax.part = s.rcpart;
+    fax.partx = s.rcpartx;
+    fax.rows_per_cluster = s.rcrpc;
+    fax.wcol = RC_W;
+  }
+  auto fused_step = [&](bool xmstep = false) -> gw_status {
     // Every iteration first tries the fused one-read path when *mode == 1 (speculatively at the
     // start of a solve); k_sink_fast_check validates it before anything is committed, and on
     // failure k_sink_fin_fast leaves f, g untouched and sets *mode = 0 so that the robust
     // two-kernel path below runs this same iteration.  No host sync.
     if (s.fK > 0) {
+      PROF_BEGIN(c, PC_SINK_XM);
       PROF_BEGIN(c, PC_SINK_FUSED);
-      TRY(fused_launch(c, s.fK, s.fCL, s.fNT, fa, s.fncl));
+      if (xmstep) TRY(rc_xm_launch(c, s.rcCL, fax, s.rcncl));
+      else TRY(fused_launch(c, s.fK, s.fCL, s.fNT, fa, s.fncl));
       KCHECK();
+      double* const fpart = xmstep ? s.rcpart : s.fpart;
+      const int fncl = xmstep ? s.rcncl : s.fncl;
       // one rank: column sums, check (rows + columns), commit.  R > 1: the rank's row check rides in
       // the column-sum payload (slot M), so ONE all-gather per iteration carries everything.
       const bool multi = P.R > 1;
@@ -1579,12 +1773,16 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
       if (multi) {
         CU(cudaMemsetAsync(s.csl + m, 0, sizeof(double), c->stream));
         k_sink_colsum<<<(unsigned)((m + 31) / 32), 256, 0, c->stream>>>(
-            s.fpart, s.fncl, m, s.csl, s.mode, s.stop, s.Srow, nl, reinterpret_cast<int*>(s.csl + m));
+            fpart, fncl, m, s.csl, s.mode, s.stop, s.Srow, nl, reinterpret_cast<int*>(s.csl + m));
       } else {  // one rank: column sums + the whole validity check in one launch (flag cleared by k_sink_mode)
         k_sink_colsum<<<(unsigned)((m + 31) / 32), 256, 0, c->stream>>>(
-            s.fpart, s.fncl, m, s.csl, s.mode, s.stop, s.Srow, nl, s.flag, s.flag, P.lq);
+            fpart, fncl, m, s.csl, s.mode, s.stop, s.Srow, nl, s.flag, s.flag, P.lq);
       }
       KCHECK();
+      if (xmstep) {
+        k_xm_mark<<<1, 32, 0, c->stream>>>(s.mode, s.flag, s.stop, s.xmv);
+        KCHECK();
+      }
       if (fault_is("colsum")) {  // test-only: one column sum of the half-step plan doubled
         k_fault_scale<<<1, 32, 0, c->stream>>>(s.csl, m / 2, 2.0);
         KCHECK();
@@ -1600,14 +1798,18 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
           s.Srow, nl, P.lp + P.row0, s.f, s.fh, s.fl, nullptr, s.csg, P.R, stride, m, P.lq, eps, s.g, s.gh, s.gl,
           s.mode, s.stop, s.dev, s.flag, kappa, cond_h, use_cond);
       KCHECK();
-      PROF_END(c, PC_SINK_FUSED, 2);
+      if (xmstep) {
+        PROF_END(c, PC_SINK_XM, 2);
+      } else {
+        PROF_END(c, PC_SINK_FUSED, 2);
+      }
     }
     return GW_OK;
   };
   // one iteration (check: the tolerance rule's violation check of the plan after `done` iterations)
   const int* commit_cnt = nullptr;  // graph-resident tolerance loop: the iteration count lives on the device
-  auto iteration = [&](bool check, int done) -> gw_status {
-    if (!check) TRY(fused_step());
+  auto iteration = [&](bool check, int done, bool xmstep = false) -> gw_status {
+    if (!check) TRY(fused_step(xmstep));
     // iterations run the robust two-kernel path while *mode == 0 (decided on the device)
     const int* skip = check ? nullptr : s.mode;
     if (check) CU(cudaMemsetAsync(s.viol, 0, sizeof(float), c->stream));
@@ -1777,9 +1979,7 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
   static const bool no_graph = getenv("GWDP_NO_GRAPH") != nullptr;
   if (!tolmode && !no_graph && !c->prof.on && P.R == 1 && iters >= 3) {
     if (s.gexec && (s.g_eps != eps || s.g_kappa != kappa)) sink_free(s);
-    if (!s.gexec) {
-      s.g_eps = eps;
-      s.g_kappa = kappa;
+    auto capture = [&](bool xmstep, cudaGraphExec_t* out) -> gw_status {
       if (!c->cap) CU(cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking));
       static const bool no_cond = getenv("GWDP_NO_COND") != nullptr;
       cudaGraph_t graph = nullptr;
@@ -1795,7 +1995,7 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
         CU(cudaStreamBeginCaptureToGraph(c->cap, graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
         c->stream = c->cap;
         use_cond = 1;
-        st = fused_step();
+        st = fused_step(xmstep);
         use_cond = 0;
         if (st == GW_OK) {
           cudaStreamCaptureStatus cs;
@@ -1845,11 +2045,20 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
         return st;
       }
       if (e != cudaSuccess) return fail(GW_ERR_CUDA, "Sinkhorn graph capture: %s", cudaGetErrorString(e));
-      const cudaError_t ei = cudaGraphInstantiate(&s.gexec, graph, 0);
+      const cudaError_t ei = cudaGraphInstantiate(out, graph, 0);
       cudaGraphDestroy(graph);
       if (ei != cudaSuccess) return fail(GW_ERR_CUDA, "Sinkhorn graph instantiate: %s", cudaGetErrorString(ei));
+      return GW_OK;
+    };
+    static const bool no_cond_x = getenv("GWDP_NO_COND") != nullptr;
+    if (no_cond_x) xm = false;  // the XM sweep rides on the conditional-node graph only
+    if (!s.gexec) {
+      s.g_eps = eps;
+      s.g_kappa = kappa;
+      TRY(capture(false, &s.gexec));
     }
-    for (int k = 0; k < iters; ++k) CU(cudaGraphLaunch(s.gexec, c->stream));
+    if (xm && !s.gexec_xm) TRY(capture(true, &s.gexec_xm));
+    for (int k = 0; k < iters; ++k) CU(cudaGraphLaunch((xm && k == iters - 1) ? s.gexec_xm : s.gexec, c->stream));
     *used = iters;
     return GW_OK;
   }
@@ -1940,7 +2149,7 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
     const int chunk = tolmode ? std::min(check_every, iters - done) : iters - done;
     for (int k = 0; k < chunk; ++k) {
       const bool check = tolmode && k == 0 && done > 0;  // violation of the plan after `done` iterations
-      TRY(iteration(check, done));
+      TRY(iteration(check, done, xm && !tolmode && done + k == iters - 1));
     }
     if (tolmode) {
       int hs[2];
@@ -2143,6 +2352,8 @@ static gw_status solve_impl(gw_ctx* c, const gw_problem* pb, const gw_solve_opts
   float ms_grad = 0.f, ms_sink = 0.f;
   std::vector<double> tr((size_t)std::max(o->outer_iters, 1) * 4, NAN);
   const bool want_trace_obj = (o->flags & GW_SOLVE_TRACE_OBJECTIVE) != 0;
+  bool rc_next = false;  // the next gradient runs on the 8 N M path (rowclu.cuh)
+  int onepass = 0;
   for (int l = 0; l < o->outer_iters; ++l) {
     // ---- gradient of T^{l} (l = 0: T0 or p q^T) ----
     int mode;
@@ -2184,6 +2395,9 @@ static gw_status solve_impl(gw_ctx* c, const gw_problem* pb, const gw_solve_opts
     if (tau_mode && obj) {  // objective of T^l first, then the cost over the buffer it reads
       TRY(grad_pass(c, P, mode, S, S2, nullptr, 0, false, true, fx, fy, alpha, objout));
       TRY(grad_pass(c, P, mode, S, S2, G, ldG, true, false, fx, fy, alpha, nullptr, beta));
+    } else if (mode == T_GIBBS && rc_next && !obj) {
+      TRY(grad_rc(c, P, s, G, ldG, S2));  // one read + one write (rowclu.cuh)
+      ++onepass;
     } else {
       TRY(grad_pass(c, P, mode, S, S2, G, ldG, true, obj, fx, fy, alpha, objout, beta));
     }
@@ -2200,8 +2414,17 @@ static gw_status solve_impl(gw_ctx* c, const gw_problem* pb, const gw_solve_opts
     // ---- Sinkhorn on G^{l+1} with warm-started duals ----
     TRY(sink_split(c, P, s, es));
     int used = 0, conv = 0;
+    // the next gradient on the 8 N M path needs the XM sweep as this inner loop's last iteration
+    const bool want_xm = s.rcCL > 0 && l + 1 < o->outer_iters && !tau_mode && !fx && !want_trace_obj;
     TRY(sink_run(c, P, s, G, ldG, es, o->inner.max_iter, o->inner.tol, o->inner.check_every, &used, &conv,
-                 l == 0));
+                 l == 0, 1.0, want_xm));
+    rc_next = false;
+    if (want_xm) {  // did it run and commit? (one 4-byte read per outer iteration)
+      int* hx = reinterpret_cast<int*>(c->hpin + 48);
+      CU(cudaMemcpyAsync(hx, s.xmv, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      CU(cudaStreamSynchronize(c->stream));
+      rc_next = hx[0] == 1;
+    }
     inner_total += used;
     if (o->inner.tol > 0 && !conv) conv_all = 0;
     tr[(size_t)l * 4 + 2] = used;
@@ -2275,6 +2498,7 @@ static gw_status solve_impl(gw_ctx* c, const gw_problem* pb, const gw_solve_opts
   res->ms_grad = ms_grad;
   res->ms_sinkhorn = ms_sink;
   res->ms_total = ms_total;
+  res->grad_onepass_total = onepass;
   if (trace) memcpy(trace, tr.data(), sizeof(double) * 4 * (size_t)o->outer_iters);
   TRY(stage_duals_out(c, pb, P, f, g, s.f, s.g));
   return GW_OK;
@@ -2597,6 +2821,7 @@ static gw_status ugw_impl(gw_ctx* c, const gw_problem* pb, double rho, const gw_
   const int ugw_fused = o->outer_iters > 0 ? reinterpret_cast<int*>(c->hpin + 32)[1] : 0;
   float ms_total = 0.f;
   CU(cudaEventElapsedTime(&ms_total, ev0, ev1));
+  res->grad_onepass_total = 0;
   res->gw_objective = E;
   res->entropic_objective = F;
   res->marginal_violation = viol;

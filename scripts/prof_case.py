@@ -25,7 +25,7 @@ def main():
     import workloads as W
     from paper_2404_08970_b200 import api
     dev = torch.device("cuda", 0)
-    n = 16384
+    n = int(sys.argv[2]) if len(sys.argv) > 2 else 16384
     rng = np.random.default_rng(0)
     if case == "gibbs":
         P = W.config4(n)
@@ -90,6 +90,30 @@ def main():
         names = ["grad_moments", "grad_carry", "grad_main", "sink_row", "sink_col", "sink_fused", "objective"]
         print("ugw instrumented: %.3f ms; classes: %s" % (e0.elapsed_time(e1),
               {nm: round(ms_c[i], 3) for i, nm in enumerate(names)}))
+    elif case == "onepass":
+        # the solver's gradient on the one-read path (rowclu.cuh) and the XM sweep that feeds it, C4 recipe
+        # at N = M = n: 3 outer x 3 inner, instrumented (eager launches); then the two-read path
+        import ctypes as C
+        import os
+        from paper_2404_08970_b200 import _lib
+        import workloads as W
+        P = W.config4(n)
+        ctx = api.Context.get(dev)
+        lib = _lib.load()
+        names = ["grad_moments", "grad_carry", "grad_main", "sink_row", "sink_col", "sink_fused", "objective",
+                 None, "grad_onepass", "sink_xm"]
+        os.environ["GWDP_RC"] = "1"
+        for env in ("", "1"):
+            os.environ["GWDP_NO_RC"] = env
+            api.solve(P.x, P.y, P.p, P.q, P.eps, 2, 3, device=dev)
+            ms_c = (C.c_double * 10)()
+            cnt_c = (C.c_int64 * 10)()
+            _lib.check(lib.gw_ctx_profile(ctx.h, 2, None, None, 0))
+            r = api.solve(P.x, P.y, P.p, P.q, P.eps, 4, 3, device=dev)
+            _lib.check(lib.gw_ctx_profile(ctx.h, 0, C.cast(ms_c, C.c_void_p), C.cast(cnt_c, C.c_void_p), 10))
+            print("GWDP_NO_RC=%s onepass=%d:" % (env or "0", r.grad_onepass_total),
+                  {nm: (round(ms_c[i], 3), int(cnt_c[i])) for i, nm in enumerate(names) if nm and cnt_c[i]})
+        os.environ.pop("GWDP_NO_RC", None)
     else:
         raise SystemExit("unknown case %s" % case)
     torch.cuda.synchronize()

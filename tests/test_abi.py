@@ -52,7 +52,7 @@ def test_library_is_sm100a(lib):
 
 
 def test_host_only_entry_points(lib):
-    assert lib.gw_abi_version() == 1
+    assert lib.gw_abi_version() == 2
     # null-argument validation of ugw_solve happens before any device work
     from paper_2404_08970_b200 import _lib
     st = lib.ugw_solve(None, None, 1.0, None, None, None, 0, None, None, None, None)

@@ -287,7 +287,9 @@ def test_sharded_ugw(gw, su, sv):
     out = _run_ranks(3, fn)
     assert out[0][0] == out[1][0] == out[2][0]
     assert abs(out[0][0] - r1.entropic_objective) <= 1e-6 * abs(r1.entropic_objective)
-    np.testing.assert_allclose(out[0][1][:, 0], r1.trace[:, 0], rtol=1e-6)
+    # per-outer trace of two GPU paths with different summation orders (3 row shards vs one rank):
+    # measured up to 1.23e-6 relative on one box (GPUTEST, round 2); the oracle bound below is 1e-4
+    np.testing.assert_allclose(out[0][1][:, 0], r1.trace[:, 0], rtol=5e-6)
     np.testing.assert_allclose(out[0][1][:, 3], r1.trace[:, 3], rtol=1e-6)
     ro = O.entropic_ugw(P.x, P.y, P.p, P.q, 1.0, 0.01, P.outer, P.inner)
     assert abs(out[0][0] - ro["F"][-1]) <= 1e-4 * abs(ro["F"][-1])
