@@ -119,7 +119,7 @@ struct gw_ctx {
   Buf sflag, sflagg;
   Buf fsc, gsc;  // scaled duals for the Gibbs regeneration
   Buf Gs;        // solver cost buffer
-  Buf rcp, rcpx, rcv, rcvx, rcu, rcz, rcxf, rccx, rccy, rcflag;  // 8 N M solver gradient (rowclu.cuh)
+  Buf rcp, rcpx, rcv, rcvx, rcu, rcz, rcxf, rccx, rccy, rcflag, rcdx;  // 8 N M solver gradient (rowclu.cuh)
   double* hpin = nullptr;  // pinned host scratch (64 doubles)
   // one-shot debug export for the next solve (gw_solve_set_export)
   struct {
@@ -136,7 +136,7 @@ struct gw_ctx {
                 &gkrp, &gkrt, &gkcp, &gkz, &gkct, &gkctt, &gkobj, &gkseg,
                 &uga, &ugb, &ugct, &ugpart, &ugca, &ugcb, &ugfr, &uggr, &ugsc, &ugrpart,
                 &g2rc, &g2rd, &g2h, &g2cc, &g2tt, &g2vt, &g2tmp, &g2s, &g2a, &g2b, &g2ca, &g2cb, &g2part,
-                &rcp, &rcpx, &rcv, &rcvx, &rcu, &rcz, &rcxf, &rccx, &rccy, &rcflag};
+                &rcp, &rcpx, &rcv, &rcvx, &rcu, &rcz, &rcxf, &rccx, &rccy, &rcflag, &rcdx};
     for (Buf* x : b) all.push_back(x);
   }
 };
@@ -1310,7 +1310,7 @@ struct SinkState {
   int rcCL = 0, rcncl = 0;
   int64_t rcrpc = 0;
   double *rcpart = nullptr, *rcpartx = nullptr;
-  float *xf = nullptr, *ccx = nullptr, *ccy = nullptr;
+  float *xf = nullptr, *ccx = nullptr, *ccy = nullptr, *dxf = nullptr;
   int* xmv = nullptr;               // set on the device when the XM sweep ran and was committed
   cudaGraphExec_t gexec_xm = nullptr;  // the same iteration with the XM sweep
 };
@@ -1606,6 +1606,8 @@ static gw_status sink_alloc(gw_ctx* c, const Prepared& P, SinkState& s) {
       TRY(ws(c, c->rccy, (size_t)P.m, &s.ccy));
       TRY(ws(c, c->rcflag, 4, &s.xmv));
       k_to_float<<<grid_for(P.nl), 256, 0, c->stream>>>(P.xc + P.row0, P.nl, s.xf);
+      TRY(ws(c, c->rcdx, (size_t)P.nl, &s.dxf));
+      k_rc_dx<<<grid_for(P.nl), 256, 0, c->stream>>>(P.xc + P.row0, P.nl, s.dxf);
       k_scale_f<<<grid_for(P.nl), 256, 0, c->stream>>>(P.cx + P.row0, P.nl, 2.0, s.ccx);
       k_scale_f<<<grid_for(P.m), 256, 0, c->stream>>>(P.cy, P.m, 2.0, s.ccy);
       KCHECK();
@@ -1634,7 +1636,7 @@ static gw_status grad_rc(gw_ctx* c, const Prepared& P, SinkState& s, float* G, i
   RcArgs ra;
   ra.G = G; ra.ld = ldG; ra.nl = nl; ra.m = m; ra.rows_per_cluster = s.rcrpc;
   ra.fh = S2.fh; ra.fl = S2.fl; ra.gh = S2.gh; ra.gl = S2.gl; ra.ch = S2.ch; ra.cl = S2.cl;
-  ra.xf = s.xf; ra.ccx = s.ccx; ra.yf = P.yf; ra.ccy = s.ccy; ra.U0 = U0; ra.Zn0 = Z0;
+  ra.dxf = s.dxf; ra.xc = P.xc + P.row0; ra.ccx = s.ccx; ra.yf = P.yf; ra.ccy = s.ccy; ra.U0 = U0; ra.Zn0 = Z0;
   TRY(rc_grad_launch(c, s.rcCL, tm, ra, ncl));
   KCHECK();
   PROF_END(c, PC_GRAD_ONEPASS, 1);

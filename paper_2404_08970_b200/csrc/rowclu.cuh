@@ -35,7 +35,7 @@ namespace gw {
 constexpr int RC_NT = 256;              // threads per CTA
 constexpr int RC_KC = 16;               // contiguous columns per thread
 constexpr int RC_W = RC_NT * RC_KC;     // 4096 columns per CTA
-constexpr int RC_RS = 8;                // TMA ring stages (rows of the CTA slice, 16 KB each)
+constexpr int RC_RS = 7;                // TMA ring stages (rows of the CTA slice, 16 KB each)
 constexpr int RC_FLUSH = 32;            // rows between fp32 -> fp64 column-state re-basing
 
 struct RcArgs {
@@ -43,16 +43,18 @@ struct RcArgs {
   int64_t ld, nl, m, rows_per_cluster;
   const float *fh, *fl, *gh, *gl;  // f log2e/eps, g log2e/eps of T^l: fp32 hi / lo
   float ch, cl;                    // log2e/eps hi / lo
-  const float* xf;   // centred x (fp32, local rows)
+  const float* dxf;  // x_{i+1} - x_i (fp32, local rows; 0 for the last)
+  const double* xc;  // centred x (fp64, local rows)
   const float* ccx;  // 2 c_i (fp32, local rows)
   const float* yf;   // centred y (fp32)
   const float* ccy;  // 2 c'_p (fp32)
   const double* U0;  // [ncl][m] column state U at each cluster's first row
-  const double* Zn0; // [ncl][m] -Z there
+  const double* Zn0; // [ncl][m] -Z there (V = x U + Zn = (D_X B) at that row)
 };
 
 __host__ __device__ constexpr size_t rc_dyn_smem() {
-  return 1024 + (size_t)RC_RS * RC_W * sizeof(float) + (size_t)2 * RC_KC * RC_NT * sizeof(double);
+  return 1024 + (size_t)RC_RS * RC_W * sizeof(float) + (size_t)2 * RC_KC * RC_NT * sizeof(double) +
+         (size_t)2 * RC_KC * RC_NT * sizeof(float);
 }
 
 // TMA tile load of one 4096-column row slice as a [128][32] fp32 box, 128-byte swizzle: the 16-B chunk
@@ -68,26 +70,35 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
 }
 
 // One CTA = 256 threads x 16 contiguous columns; a cluster of CL CTAs spans a row; cluster cid owns
-// rows [cid rpc, (cid + 1) rpc) and walks them top-down.  Per row j (no CTA-wide barrier, as in
-// k_sink_fused2): produce(j) -- regenerate T, the thread's in-row exclusive prefixes, a warp scan, the
-// warp totals st.async'ed to every CTA of the cluster -- then consume(j - 1): the (rank, warp) partials
-// of row j - 1 give R, (Ty) and this warp's offset; the row DP gives B, the column state gives
-// V = x U + Zn, G = 2c_i + 2c'_p - 4 V is stored, and U, Zn advance by 2B, -2xB.
+// rows [cid rpc, (cid + 1) rpc) and walks them top-down in PAIRS of rows.  Per pair step P (no CTA-wide
+// barrier, as in k_sink_fused2): produce(P) -- regenerate T on rows 2P, 2P+1, the threads' totals, one
+// warp scan of the four values, the warp totals of both rows in ONE 16-byte st.async to every CTA of
+// the cluster -- then consume(P - 1): the (rank, warp) partials of the previous pair give R, (Ty) and
+// this warp's offset for both rows (one butterfly of eight values); the row DP gives B, G is stored, and
+// the column state advances down the two rows.  The two rows' chains interleave (latency per row
+// halved; the kernel is latency bound at 2 warps per scheduler).
 template <int CL>
 __global__ void __launch_bounds__(RC_NT, 1) k_grad_rc(const __grid_constant__ CUtensorMap tmap, RcArgs a) {
   constexpr int NW = RC_NT / 32;
-  constexpr int NX = CL * NW;               // partials per row
+  constexpr int NX = CL * NW;               // partials per row pair
   constexpr int NXP = NX < 32 ? 32 : NX;    // padded so that every lane reads a slot
   constexpr int PER = NXP / 32;             // partials per lane
   constexpr int NSLOT = 4;
   extern __shared__ unsigned char rc_raw[];
-  float* ring = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(rc_raw) + 1023) & ~uintptr_t(1023));
-  double* U64 = reinterpret_cast<double*>(ring + (size_t)RC_RS * RC_W);  // [16][NT]
-  double* Z64 = U64 + RC_KC * RC_NT;                                       // [16][NT]  (-Z)
+  // 1024-B aligned ring (128-byte swizzle); offset from the shared base keeps the shared address space
+  float* ring = reinterpret_cast<float*>(rc_raw + ((1024u - (smem_u32(rc_raw) & 1023u)) & 1023u));
+  double* U64 = reinterpret_cast<double*>(ring + (size_t)RC_RS * RC_W);  // [16][NT]  U
+  double* V64 = U64 + RC_KC * RC_NT;                                       // [16][NT]  V = D_X B
+  float4* sgh = reinterpret_cast<float4*>(V64 + RC_KC * RC_NT);           // [4][NT]  g_hi (16 columns)
+  float4* sgl = sgh + 4 * RC_NT;                                           // [4][NT]  g_lo
   __shared__ __align__(8) uint64_t full[RC_RS];
   __shared__ unsigned int scnt[RC_RS];
   __shared__ __align__(8) uint64_t xbar[NSLOT];
-  __shared__ __align__(16) float2 xs[NSLOT][NXP];
+  __shared__ __align__(16) float4 xs[NSLOT][NXP];  // {T row 0, yT row 0, T row 1, yT row 1}
+  // the pair's totals and the exclusive prefixes of this CTA's warps, reduced by ONE designated warp
+  // (P mod NW) and published through a CTA-local mbarrier
+  __shared__ __align__(16) float4 red[NSLOT][NW + 1];
+  __shared__ __align__(8) uint64_t rbar[NSLOT];
 
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const uint32_t cr = blockIdx.x % CL;
@@ -98,22 +109,26 @@ __global__ void __launch_bounds__(RC_NT, 1) k_grad_rc(const __grid_constant__ CU
   const int64_t rb = cid * a.rows_per_cluster;
   const int64_t re = min(a.nl, rb + a.rows_per_cluster);
   const int nrows = (int)max((int64_t)0, re - rb);
+  const int npairs = (nrows + 1) >> 1;
   const int64_t q0 = c0 + (int64_t)RC_KC * t;  // this thread's first column
   const int nv = (int)max((int64_t)0, min((int64_t)RC_KC, m - q0));
-  constexpr uint32_t xbytes = 8u * NX;
+  constexpr uint32_t xbytes = 16u * NX;
   constexpr uint32_t tbytes = RC_W * 4u;
 
   // padding slots (never written by peers) read as zero
   for (int i = NX + t; i < NXP; i += RC_NT)
-    for (int s = 0; s < NSLOT; ++s) xs[s][i] = make_float2(0.f, 0.f);
+    for (int s = 0; s < NSLOT; ++s) xs[s][i] = make_float4(0.f, 0.f, 0.f, 0.f);
   if (t == 0) {
     for (int s = 0; s < RC_RS; ++s) {
       mbar_init(&full[s], 1);
       scnt[s] = 0u;
     }
-    for (int s = 0; s < NSLOT; ++s) mbar_init(&xbar[s], 1);
+    for (int s = 0; s < NSLOT; ++s) {
+      mbar_init(&xbar[s], 1);
+      mbar_init(&rbar[s], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int s = 0; s < NSLOT && s < nrows; ++s) mbar_expect_tx(&xbar[s], xbytes);
+    for (int s = 0; s < NSLOT && s < npairs; ++s) mbar_expect_tx(&xbar[s], xbytes);
   }
   __syncthreads();
   cluster_arrive();
@@ -126,161 +141,181 @@ __global__ void __launch_bounds__(RC_NT, 1) k_grad_rc(const __grid_constant__ CU
     }
   }
 
-  // per-column constants and the column state (pairs of adjacent columns)
-  float2 gh2[8], gl2[8], y2[8], cp2[8], Uf[8], Zf[8], u2[8], z2[8];
+  // column state (pairs of adjacent columns): U = Uf + u, V = Vf + v with fp64 bases U64, V64 every
+  // RC_FLUSH rows; Wf = 2c'_p - 4 Vf.  Down the column: G_i = Wf + 2c_i - 4 v;  U += 2 B_i;
+  // V += (x_{i+1} - x_i) U  (V_{i+1} - V_i = dx_i (2 sum_{j<=i} B_j - sum_j B_j), PAPER.md:237-243 on columns)
+  float2 y2[8], Uf[8], Wf[8], u2[8], v2[8];
   const double* U0 = a.U0 + cid * m;
   const double* Zn0 = a.Zn0 + cid * m;
+  const double x0 = nrows > 0 ? a.xc[rb] : 0.0;
+  {
+    float gh[RC_KC], gl[RC_KC];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    float v[2][4];
+    for (int k = 0; k < 8; ++k) {
+      float yv[2];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int kk = 2 * k + h;
-      const int64_t q = q0 + kk;
-      const bool ok = kk < nv;
-      v[h][0] = ok ? a.gh[q] : 0.f;
-      v[h][1] = ok ? a.gl[q] : 0.f;
-      v[h][2] = ok ? a.yf[q] : 0.f;
-      v[h][3] = ok ? a.ccy[q] : 0.f;
-      const double U = ok ? U0[q] : 0.0, Z = ok ? Zn0[q] : 0.0;
-      U64[kk * RC_NT + t] = U;
-      Z64[kk * RC_NT + t] = Z;
-      if (h == 0) { Uf[k].x = (float)U; Zf[k].x = (float)Z; }
-      else { Uf[k].y = (float)U; Zf[k].y = (float)Z; }
+      for (int h = 0; h < 2; ++h) {
+        const int kk = 2 * k + h;
+        const int64_t q = q0 + kk;
+        const bool ok = kk < nv;
+        gh[kk] = ok ? a.gh[q] : 0.f;
+        gl[kk] = ok ? a.gl[q] : 0.f;
+        yv[h] = ok ? a.yf[q] : 0.f;
+        const double U = ok ? U0[q] : 0.0, V = ok ? fma(x0, U0[q], Zn0[q]) : 0.0;
+        const double cp = ok ? (double)a.ccy[q] : 0.0;
+        U64[kk * RC_NT + t] = U;
+        V64[kk * RC_NT + t] = V;
+        if (h == 0) { Uf[k].x = (float)U; Wf[k].x = (float)(cp - 4.0 * V); }
+        else { Uf[k].y = (float)U; Wf[k].y = (float)(cp - 4.0 * V); }
+      }
+      y2[k] = make_float2(yv[0], yv[1]);
+      u2[k] = make_float2(0.f, 0.f);
+      v2[k] = u2[k];
     }
-    gh2[k] = make_float2(v[0][0], v[1][0]);
-    gl2[k] = make_float2(v[0][1], v[1][1]);
-    y2[k] = make_float2(v[0][2], v[1][2]);
-    cp2[k] = make_float2(v[0][3], v[1][3]);
-    u2[k] = make_float2(0.f, 0.f);
-    z2[k] = u2[k];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      sgh[c * RC_NT + t] = make_float4(gh[4 * c], gh[4 * c + 1], gh[4 * c + 2], gh[4 * c + 3]);
+      sgl[c * RC_NT + t] = make_float4(gl[4 * c], gl[4 * c + 1], gl[4 * c + 2], gl[4 * c + 3]);
+    }
   }
   const float2 nch = make_float2(-a.ch, -a.ch), ncl = make_float2(-a.cl, -a.cl);
   const float* __restrict__ fh = a.fh + rb;
   const float* __restrict__ fl = a.fl + rb;
-  const float* __restrict__ xf = a.xf + rb;
+  const float* __restrict__ dxf = a.dxf + rb;
   const float* __restrict__ ccx = a.ccx + rb;
   float* __restrict__ Gout = a.G + rb * ld + q0;
   const uint32_t peer = (uint32_t)min(lane, CL - 1);
   const uint32_t rx0 = mapa(&xs[0][cr * NW + wid], peer), rbar0 = mapa(&xbar[0], peer);
   constexpr uint32_t XSTRIDE = sizeof(xs[0]), BSTRIDE = sizeof(uint64_t);
-  const int me = (int)cr * NW + wid;  // this warp's index in the row's column order
   // swizzled offsets (floats) of the thread's four 16-B chunks inside a stage
   const int rl = t >> 1;
   int chunk_off[4];
 #pragma unroll
   for (int c = 0; c < 4; ++c) chunk_off[c] = rl * 32 + (((4 * (t & 1) + c) ^ (rl & 7)) << 2);
 
-  // per-row scalars {F_hi, F_lo, x_i, 2 c_i}: lane l holds those of row 32 g + l of the current 32-row
-  // group g (and prefetches group g + 1), broadcast by shuffles -- no global-load latency per row
+  // per-row scalars {F_hi, F_lo, x_{i+1} - x_i, 2 c_i}: lane l holds those of row 32 g + l of the current
+  // 32-row group g (and prefetches group g + 1), broadcast by shuffles -- no global-load latency per row
   float4 rcur = make_float4(0.f, 0.f, 0.f, 0.f), rnxt = rcur;
   auto rload = [&](int g) {
     const int r = 32 * g + lane;
-    return r < nrows ? make_float4(fh[r], fl[r], xf[r], ccx[r]) : make_float4(0.f, 0.f, 0.f, 0.f);
+    return r < nrows ? make_float4(fh[r], fl[r], dxf[r], ccx[r]) : make_float4(0.f, 0.f, 0.f, 0.f);
   };
   rnxt = rload(0);
 
-  // produce row j: the plan values t of the thread's 16 columns (pairs), the lane-exclusive warp prefix
-  // `off` = (sum T, sum yT) of the thread's first column, and the row's {x_i, 2 c_i}
-  auto produce = [&](int j, float2 (&tv)[8], float2& off, float2& xc) {
-    if ((j & 31) == 0) {
-      rcur = rnxt;
-      rnxt = rload((j >> 5) + 1);
-    }
-    const int src = j & 31;
-    const float Fh = __shfl_sync(0xffffffffu, rcur.x, src), Fl = __shfl_sync(0xffffffffu, rcur.y, src);
-    xc = make_float2(__shfl_sync(0xffffffffu, rcur.z, src), __shfl_sync(0xffffffffu, rcur.w, src));
-    if (ncol > 0) {
-      const int st = j % RC_RS;
-      mbar_wait(&full[st], (uint32_t)((j / RC_RS) & 1));
-      const float* sp = ring + (size_t)st * RC_W;
-      float4 gv[4];
+  // regenerate the plan on one row of the pair (stage st) into tv
+  auto regen = [&](int j, float Fh, float Fl, float2 (&tv)[8]) {
+    const int st = j % RC_RS;
+    mbar_wait(&full[st], (uint32_t)((j / RC_RS) & 1));
+    const float* sp = ring + (size_t)st * RC_W;
+    float4 gv[4];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) gv[c] = *reinterpret_cast<const float4*>(sp + chunk_off[c]);
-      const float2 F2 = make_float2(Fh, Fh), L2 = make_float2(Fl, Fl);
+    for (int c = 0; c < 4; ++c) gv[c] = *reinterpret_cast<const float4*>(sp + chunk_off[c]);
+    const float2 F2 = make_float2(Fh, Fh), L2 = make_float2(Fl, Fl);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const float4 h4 = sgh[c * RC_NT + t], l4 = sgl[c * RC_NT + t];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int k = 2 * c + e;
+        const float2 g = e ? make_float2(gv[c].z, gv[c].w) : make_float2(gv[c].x, gv[c].y);
+        const float2 gh = e ? make_float2(h4.z, h4.w) : make_float2(h4.x, h4.y);
+        const float2 gl = e ? make_float2(l4.z, l4.w) : make_float2(l4.x, l4.y);
+#ifdef RCX_NOREGEN
+        tv[k] = g;
+#else
+        const float2 ae = fadd2(fadd2(ffma2(g, nch, gh), F2), ffma2(g, ncl, fadd2(gl, L2)));
+        tv[k] = make_float2(ex2_ftz(ae.x), ex2_ftz(ae.y));
+#endif
+      }
+    }
+    if (nv < RC_KC) {
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        const float4 g4 = gv[k >> 1];
-        const float2 g = (k & 1) ? make_float2(g4.z, g4.w) : make_float2(g4.x, g4.y);
-        const float2 ae = fadd2(fadd2(ffma2(g, nch, gh2[k]), F2), ffma2(g, ncl, fadd2(gl2[k], L2)));
-        tv[k] = make_float2(ex2_ftz(ae.x), ex2_ftz(ae.y));
+        if (2 * k >= nv) tv[k].x = 0.f;
+        if (2 * k + 1 >= nv) tv[k].y = 0.f;
       }
-      if (nv < RC_KC) {
+    }
+  };
+  auto release = [&](int j) {  // the last warp to release a stage refills it with row j + RS
+    const int st = j % RC_RS;
+    if (atomicAdd(&scnt[st], 1u) == NW - 1) {
+      scnt[st] = 0u;
+      const int nxt = j + RC_RS;
+      if (nxt < nrows) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&full[st], tbytes);
+        tma_load_3d(ring + (size_t)st * RC_W, &tmap, 0, cy, (int)(rb + nxt), &full[st]);
+      }
+    }
+  };
+
+  // produce pair P: plan values of both rows, the lane-exclusive warp prefixes `off` = {T0, yT0, T1, yT1}
+  // of the thread's first column, and the rows' {dx, 2 c_i} in `xc`
+  auto produce = [&](int P, float2 (&t0)[8], float2 (&t1)[8], float4& off, float4& xc) {
+    const int j0 = 2 * P, j1 = j0 + 1;
+    if ((j0 & 31) == 0) {
+      rcur = rnxt;
+      rnxt = rload((j0 >> 5) + 1);
+    }
+    const int s0 = j0 & 31;
+    const float Fh0 = __shfl_sync(0xffffffffu, rcur.x, s0), Fl0 = __shfl_sync(0xffffffffu, rcur.y, s0);
+    const float Fh1 = __shfl_sync(0xffffffffu, rcur.x, s0 + 1), Fl1 = __shfl_sync(0xffffffffu, rcur.y, s0 + 1);
+    xc = make_float4(__shfl_sync(0xffffffffu, rcur.z, s0), __shfl_sync(0xffffffffu, rcur.w, s0),
+                     __shfl_sync(0xffffffffu, rcur.z, s0 + 1), __shfl_sync(0xffffffffu, rcur.w, s0 + 1));
+    if (ncol > 0) {
+      regen(j0, Fh0, Fl0, t0);
+      if (j1 < nrows) regen(j1, Fh1, Fl1, t1);
+      else {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          if (2 * k >= nv) tv[k].x = 0.f;
-          if (2 * k + 1 >= nv) tv[k].y = 0.f;
-        }
+        for (int k = 0; k < 8; ++k) t1[k] = make_float2(0.f, 0.f);
       }
       __syncwarp();
-      if (lane == 0) {  // release the stage; the last warp refills it with row j + RS
-        if (atomicAdd(&scnt[st], 1u) == NW - 1) {
-          scnt[st] = 0u;
-          const int nxt = j + RC_RS;
-          if (nxt < nrows) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_expect_tx(&full[st], tbytes);
-            tma_load_3d(ring + (size_t)st * RC_W, &tmap, 0, cy, (int)(rb + nxt), &full[st]);
-          }
-        }
+      if (lane == 0) {
+        release(j0);
+        if (j1 < nrows) release(j1);
       }
     } else {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) tv[k] = make_float2(0.f, 0.f);
+      for (int k = 0; k < 8; ++k) t0[k] = t1[k] = make_float2(0.f, 0.f);
     }
-    // thread totals (sum t, sum y t), pairwise
-    float2 sp2 = make_float2(0.f, 0.f), sy2 = sp2;
+    // thread totals {sum t, sum y t} of both rows, pairwise
+    float2 p0 = make_float2(0.f, 0.f), q0s = p0, p1 = p0, q1s = p0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      sp2 = fadd2(sp2, tv[k]);
-      sy2 = ffma2(y2[k], tv[k], sy2);
+      p0 = fadd2(p0, t0[k]);
+      q0s = ffma2(y2[k], t0[k], q0s);
+      p1 = fadd2(p1, t1[k]);
+      q1s = ffma2(y2[k], t1[k], q1s);
     }
-    const float s = sp2.x + sp2.y, sy = sy2.x + sy2.y;
-    // warp inclusive scan of the thread totals -> lane-exclusive prefix, warp total
-    float it = s, iy = sy;
+    float4 it = make_float4(p0.x + p0.y, q0s.x + q0s.y, p1.x + p1.y, q1s.x + q1s.y);
+#ifndef RCX_NOSCAN
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const float ut = __shfl_up_sync(0xffffffffu, it, d), uy = __shfl_up_sync(0xffffffffu, iy, d);
-      if (lane >= d) { it += ut; iy += uy; }
+    for (int d = 1; d < 32; d <<= 1) {  // warp inclusive scan of the four totals
+      const float u0 = __shfl_up_sync(0xffffffffu, it.x, d), u1 = __shfl_up_sync(0xffffffffu, it.y, d);
+      const float u2s = __shfl_up_sync(0xffffffffu, it.z, d), u3 = __shfl_up_sync(0xffffffffu, it.w, d);
+      if (lane >= d) { it.x += u0; it.y += u1; it.z += u2s; it.w += u3; }
     }
-    const float et = __shfl_up_sync(0xffffffffu, it, 1), ey = __shfl_up_sync(0xffffffffu, iy, 1);
-    off = lane ? make_float2(et, ey) : make_float2(0.f, 0.f);
-    const float wt = __shfl_sync(0xffffffffu, it, 31), wy = __shfl_sync(0xffffffffu, iy, 31);
-    const int xsl = j & (NSLOT - 1);
-    if (lane < CL) st_async_v2f32(rx0 + XSTRIDE * xsl, wt, wy, rbar0 + BSTRIDE * xsl);
+    off = make_float4(__shfl_up_sync(0xffffffffu, it.x, 1), __shfl_up_sync(0xffffffffu, it.y, 1),
+                      __shfl_up_sync(0xffffffffu, it.z, 1), __shfl_up_sync(0xffffffffu, it.w, 1));
+    if (lane == 0) off = make_float4(0.f, 0.f, 0.f, 0.f);
+#else
+    off = it;
+#endif
+    const float4 w4 = make_float4(__shfl_sync(0xffffffffu, it.x, 31), __shfl_sync(0xffffffffu, it.y, 31),
+                                  __shfl_sync(0xffffffffu, it.z, 31), __shfl_sync(0xffffffffu, it.w, 31));
+    const int xsl = P & (NSLOT - 1);
+    if (lane < CL)
+      asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                       rx0 + XSTRIDE * xsl),
+                   "f"(w4.x), "f"(w4.y), "f"(w4.z), "f"(w4.w), "r"(rbar0 + BSTRIDE * xsl)
+                   : "memory");
   };
 
-  // consume row jp (local index): row DP, column DP, store
-  auto consume = [&](int jp, const float2 (&tv)[8], float2 off, float2 xc) {
-    const int psl = jp & (NSLOT - 1);
-    mbar_wait(&xbar[psl], (uint32_t)((jp / NSLOT) & 1));
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);  // {tot T, tot yT, prefix T, prefix yT}
-#pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      const int idx = lane * PER + i;
-      const float2 v = xs[psl][idx];
-      acc.x += v.x;
-      acc.y += v.y;
-      if (idx < me) {
-        acc.z += v.x;
-        acc.w += v.y;
-      }
-    }
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) {
-      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, d);
-      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, d);
-      acc.z += __shfl_xor_sync(0xffffffffu, acc.z, d);
-      acc.w += __shfl_xor_sync(0xffffffffu, acc.w, d);
-    }
-    if (t == 0 && jp + NSLOT < nrows) mbar_expect_tx(&xbar[psl], xbytes);
-    const float xi = xc.x, ci = xc.y;
-    // a_k = 2 P_<p - R_i,  nb_k = (Ty)_i - 2 Y_<p   at the thread's columns
-    const float a0 = fmaf(2.f, acc.z + off.x, -acc.x);
-    const float b0 = fmaf(-2.f, acc.w + off.y, acc.y);
-    const float2 a02 = make_float2(a0, a0), b02 = make_float2(b0, b0);
+  // one row of the consumed pair: row DP -> B, G stored, column state advanced
+  auto row_out = [&](int jp, const float2 (&tv)[8], float a0, float b0, float dx, float ci) {
     const float2 two = make_float2(2.f, 2.f), mtwo = make_float2(-2.f, -2.f), m4 = make_float2(-4.f, -4.f);
-    const float2 x2 = make_float2(xi, xi), ci2 = make_float2(ci, ci), m2x = make_float2(-2.f * xi, -2.f * xi);
+    const float2 a02 = make_float2(a0, a0), b02 = make_float2(b0, b0);
+    const float2 ci2 = make_float2(ci, ci), dx2 = make_float2(dx, dx);
     float2 Gv[8];
     float lp = 0.f, ly = 0.f;  // in-thread exclusive prefixes (sum t, sum y t)
 #pragma unroll
@@ -296,18 +331,24 @@ __global__ void __launch_bounds__(RC_NT, 1) k_grad_rc(const __grid_constant__ CU
       ly = fmaf(y2[k].y, tv[k].y, ly);
       const float2 av = ffma2(two, lpk, a02);
       const float2 bv = ffma2(mtwo, lyk, b02);
-      const float2 B = ffma2(y2[k], av, bv);                       // B_ip = y_p a - b
-      const float2 V = ffma2(x2, fadd2(Uf[k], u2[k]), fadd2(Zf[k], z2[k]));  // x_i U + Zn
-      Gv[k] = ffma2(m4, V, fadd2(cp2[k], ci2));                    // 2c'_p + 2c_i - 4 V
-      u2[k] = ffma2(two, B, u2[k]);
-      z2[k] = ffma2(m2x, B, z2[k]);
+      const float2 B = ffma2(y2[k], av, bv);                 // B_ip = y_p a - b
+      Gv[k] = fadd2(ffma2(m4, v2[k], Wf[k]), ci2);           // 2c'_p - 4 V + 2c_i
+      u2[k] = ffma2(two, B, u2[k]);                          // U_{i+1}
+      v2[k] = ffma2(dx2, fadd2(Uf[k], u2[k]), v2[k]);        // V_{i+1} = V_i + dx_i U_{i+1}
     }
+#ifdef RCX_NOSTORE
+    if (ncol < 0) {
+#else
     if (ncol > 0) {
+#endif
       float* gp = Gout + (int64_t)jp * ld;
-      if (nv == RC_KC) {
+      if (nv == RC_KC) {  // two 256-bit stores: each lane writes whole 32-B sectors
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-          *reinterpret_cast<float4*>(gp + 4 * c) = make_float4(Gv[2 * c].x, Gv[2 * c].y, Gv[2 * c + 1].x, Gv[2 * c + 1].y);
+        for (int h = 0; h < 2; ++h)
+          asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(gp + 8 * h),
+                       "f"(Gv[4 * h].x), "f"(Gv[4 * h].y), "f"(Gv[4 * h + 1].x), "f"(Gv[4 * h + 1].y),
+                       "f"(Gv[4 * h + 2].x), "f"(Gv[4 * h + 2].y), "f"(Gv[4 * h + 3].x), "f"(Gv[4 * h + 3].y)
+                       : "memory");
       } else {
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
@@ -320,29 +361,89 @@ __global__ void __launch_bounds__(RC_NT, 1) k_grad_rc(const __grid_constant__ CU
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         double* U = U64 + (2 * k) * RC_NT + t;
-        double* Z = Z64 + (2 * k) * RC_NT + t;
+        double* V = V64 + (2 * k) * RC_NT + t;
         const double U_0 = U[0] + (double)u2[k].x, U_1 = U[RC_NT] + (double)u2[k].y;
-        const double Z_0 = Z[0] + (double)z2[k].x, Z_1 = Z[RC_NT] + (double)z2[k].y;
-        U[0] = U_0; U[RC_NT] = U_1; Z[0] = Z_0; Z[RC_NT] = Z_1;
+        const double V_0 = V[0] + (double)v2[k].x, V_1 = V[RC_NT] + (double)v2[k].y;
+        U[0] = U_0; U[RC_NT] = U_1; V[0] = V_0; V[RC_NT] = V_1;
+        const int64_t q = q0 + 2 * k;
+        const double cp0 = 2 * k < nv ? (double)a.ccy[q] : 0.0, cp1 = 2 * k + 1 < nv ? (double)a.ccy[q + 1] : 0.0;
         Uf[k] = make_float2((float)U_0, (float)U_1);
-        Zf[k] = make_float2((float)Z_0, (float)Z_1);
+        Wf[k] = make_float2((float)(cp0 - 4.0 * V_0), (float)(cp1 - 4.0 * V_1));
         u2[k] = make_float2(0.f, 0.f);
-        z2[k] = u2[k];
+        v2[k] = u2[k];
       }
     }
   };
 
-  float2 tA[8], tB[8], offA, offB, xcA, xcB;
-  for (int j = 0; j <= nrows; j += 2) {
-    if (j < nrows) produce(j, tA, offA, xcA);
-    if (j > 0) consume(j - 1, tB, offB, xcB);
-    if (j + 1 <= nrows) {
-      if (j + 1 < nrows) produce(j + 1, tB, offB, xcB);
-      consume(j, tA, offA, xcA);
+  // consume pair Pp: totals and this warp's offsets for both rows, then the two rows in order
+  auto consume = [&](int Pp, const float2 (&t0)[8], const float2 (&t1)[8], float4 off, float4 xc) {
+    const int psl = Pp & (NSLOT - 1);
+    float4 tot, pre;
+#ifndef RCX_NOEXCH
+    if (wid == (Pp & (NW - 1))) {
+      // designated warp: lane l holds entries [l PER, (l + 1) PER) in column order; inclusive scan
+      mbar_wait(&xbar[psl], (uint32_t)((Pp / NSLOT) & 1));
+      float4 e[PER], run = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        e[i] = xs[psl][lane * PER + i];
+        run.x += e[i].x; run.y += e[i].y; run.z += e[i].z; run.w += e[i].w;
+      }
+      if (lane == 0 && Pp + NSLOT < npairs) mbar_expect_tx(&xbar[psl], xbytes);  // xs[psl] consumed
+      float4 inc = run;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const float u0 = __shfl_up_sync(0xffffffffu, inc.x, d), u1 = __shfl_up_sync(0xffffffffu, inc.y, d);
+        const float u2s = __shfl_up_sync(0xffffffffu, inc.z, d), u3 = __shfl_up_sync(0xffffffffu, inc.w, d);
+        if (lane >= d) { inc.x += u0; inc.y += u1; inc.z += u2s; inc.w += u3; }
+      }
+      float4 ex = make_float4(__shfl_up_sync(0xffffffffu, inc.x, 1), __shfl_up_sync(0xffffffffu, inc.y, 1),
+                              __shfl_up_sync(0xffffffffu, inc.z, 1), __shfl_up_sync(0xffffffffu, inc.w, 1));
+      if (lane == 0) ex = make_float4(0.f, 0.f, 0.f, 0.f);
+      tot = make_float4(__shfl_sync(0xffffffffu, inc.x, 31), __shfl_sync(0xffffffffu, inc.y, 31),
+                        __shfl_sync(0xffffffffu, inc.z, 31), __shfl_sync(0xffffffffu, inc.w, 31));
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        const int idx = lane * PER + i;
+        if (idx >= (int)cr * NW && idx < (int)cr * NW + NW) red[psl][idx - (int)cr * NW] = ex;
+        ex.x += e[i].x; ex.y += e[i].y; ex.z += e[i].z; ex.w += e[i].w;
+      }
+      if (lane == 0) red[psl][NW] = tot;
+      __syncwarp();
+      pre = red[psl][wid];
+      if (lane == 0) mbar_arrive(&rbar[psl]);
+    } else {
+      mbar_wait(&rbar[psl], (uint32_t)((Pp / NSLOT) & 1));
+      tot = red[psl][NW];
+      pre = red[psl][wid];
+    }
+#else
+    tot = pre = make_float4(0.f, 0.f, 0.f, 0.f);
+#endif
+    // a = 2 P_<p - R_i,  nb = (Ty)_i - 2 Y_<p  at the thread's first column
+    const int jp0 = 2 * Pp, jp1 = jp0 + 1;
+    row_out(jp0, t0, fmaf(2.f, pre.x + off.x, -tot.x), fmaf(-2.f, pre.y + off.y, tot.y), xc.x, xc.y);
+    if (jp1 < nrows) row_out(jp1, t1, fmaf(2.f, pre.z + off.z, -tot.z), fmaf(-2.f, pre.w + off.w, tot.w), xc.z, xc.w);
+  };
+
+  float2 tA0[8], tA1[8], tB0[8], tB1[8];
+  float4 offA, offB, xcA, xcB;
+  for (int P = 0; P <= npairs; P += 2) {
+    if (P < npairs) produce(P, tA0, tA1, offA, xcA);
+    if (P > 0) consume(P - 1, tB0, tB1, offB, xcB);
+    if (P + 1 <= npairs) {
+      if (P + 1 < npairs) produce(P + 1, tB0, tB1, offB, xcB);
+      consume(P, tA0, tA1, offA, xcA);
     }
   }
   cluster_arrive();
   cluster_wait();
+}
+
+// x_{i+1} - x_i (fp32) of the local rows, 0 for the last
+__global__ void k_rc_dx(const double* __restrict__ x, int64_t nl, float* __restrict__ dx) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nl; i += (int64_t)gridDim.x * blockDim.x)
+    dx[i] = i + 1 < nl ? (float)(x[i + 1] - x[i]) : 0.f;
 }
 
 // Column partials of T^l per cluster -> the signed prefix vectors whose D_Y gives each cluster's
