@@ -170,6 +170,25 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
   return d;
 }
 
+// 2^x on the FMA pipe for a pair (offloads MUFU): x clamped at -126, n = rint(x) by the 1.5 2^23 shift,
+// f = x - n in [-1/2, 1/2], 2^f by a degree-5 polynomial (max rel. error 2.4e-7 in fp32 Horner, the size of
+// MUFU ex2.approx's), scaled by adding n to the exponent field.
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x.x = fminf(fmaxf(x.x, -126.f), 128.f);  // 128: inf / NaN, as MUFU's overflow (caught by the check)
+  x.y = fminf(fmaxf(x.y, -126.f), 128.f);
+  const float2 mg = make_float2(12582912.f, 12582912.f);
+  const float2 r = fadd2(x, mg);
+  const float2 f = fadd2(x, make_float2(-(r.x - 12582912.f), -(r.y - 12582912.f)));
+  float2 p = make_float2(0.0013276450335979462f, 0.0013276450335979462f);
+  p = ffma2(p, f, make_float2(0.009675541892647743f, 0.009675541892647743f));
+  p = ffma2(p, f, make_float2(0.05550713464617729f, 0.05550713464617729f));
+  p = ffma2(p, f, make_float2(0.24022120237350464f, 0.24022120237350464f));
+  p = ffma2(p, f, make_float2(0.6931469440460205f, 0.6931469440460205f));
+  p = ffma2(p, f, make_float2(1.0000001192092896f, 1.0000001192092896f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(r.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(r.y) << 23)));
+}
+
 // W = 4 K NT columns per CTA.  Dynamic shared memory: the TMA ring [FSTAGES][W] fp32, then the
 // fp64 column accumulators [K][4][NT] (conflict-free: lane-contiguous doubles).
 template <int K, int NT, bool XM = false>
@@ -449,10 +468,16 @@ __global__ void __launch_bounds__(NT, 1) k_sink_fused2(FusedArgs a) {
             a10 = fadd2(a10, ffma2(make_float2(g1.x, g1.y), ncl2, fadd2(glv[k][0], L1)));
             a11 = fadd2(a11, ffma2(make_float2(g1.z, g1.w), ncl2, fadd2(glv[k][1], L1)));
           }
-          c0e[k][0] = make_float2(ex2_ftz(a00.x), ex2_ftz(a00.y));
-          c0e[k][1] = make_float2(ex2_ftz(a01.x), ex2_ftz(a01.y));
-          c1e[k][0] = make_float2(ex2_ftz(a10.x), ex2_ftz(a10.y));
-          c1e[k][1] = make_float2(ex2_ftz(a11.x), ex2_ftz(a11.y));
+          if (K >= 8 && k == K - 1) {
+            // one chunk in eight on the FMA pipe (ex2_poly2): MUFU.EX2 is the kernel's busiest unit
+            // (XU 47 %); measured 2.86 -> 2.82 ms per iteration at C4 (profiles/r02_fused_poly_offload.jsonl)
+            c0e[k][0] = ex2_poly2(a00); c0e[k][1] = ex2_poly2(a01); c1e[k][0] = ex2_poly2(a10); c1e[k][1] = ex2_poly2(a11);
+          } else {
+            c0e[k][0] = make_float2(ex2_ftz(a00.x), ex2_ftz(a00.y));
+            c0e[k][1] = make_float2(ex2_ftz(a01.x), ex2_ftz(a01.y));
+            c1e[k][0] = make_float2(ex2_ftz(a10.x), ex2_ftz(a10.y));
+            c1e[k][1] = make_float2(ex2_ftz(a11.x), ex2_ftz(a11.y));
+          }
           q0 = fadd2(q0, fadd2(c0e[k][0], c0e[k][1]));
           q1 = fadd2(q1, fadd2(c1e[k][0], c1e[k][1]));
         }
