@@ -350,6 +350,35 @@ def main():
                 "frac_of_peak_at_8NM": 8 * nm_bytes / (grad_ms / 1e3) / 1e9 / hbm,
                 "note": "moments pass (4NM) + main pass (8NM); the one-read path is off (GWDP_NO_RC=1, several "
                         "ranks, or an unsupported variant)"}
+    # ---- the one-read (8 N M) gradient path, opt-in (GWDP_RC=1): measured live on a short
+    # instrumented solve of the same configuration (3 outer iterations: 2 one-read gradients) ----
+    onepass = None
+    if world == 1 and not os.environ.get("GWDP_NO_RC"):
+        os.environ["GWDP_RC"] = "1"
+        try:
+            ms1 = (C.c_double * len(KERNELS))()
+            cn1 = (C.c_int64 * len(KERNELS))()
+            _lib.check(lib.gw_ctx_profile(ctx.h, 2, None, None, 0))
+            r1 = run(3)
+            torch.cuda.synchronize()
+            _lib.check(lib.gw_ctx_profile(ctx.h, 0, C.cast(ms1, C.c_void_p), C.cast(cn1, C.c_void_p), len(KERNELS)))
+        finally:
+            os.environ.pop("GWDP_RC", None)
+        n1 = int(cn1[8])
+        if n1 > 0:
+            g1 = ms1[8] / n1
+            nx = max(1, int(cn1[9]) // 2)
+            xm_ms = ms1[9] / nx
+            fu_ms = ms1[5] / max(1, int(cn1[5]) // 2)
+            onepass = {"ms_per_gradient": g1, "algorithmic_bytes": 8 * nm_bytes,
+                       "GBps_algorithmic": 8 * nm_bytes / (g1 / 1e3) / 1e9,
+                       "frac_of_peak": 8 * nm_bytes / (g1 / 1e3) / 1e9 / hbm,
+                       "xm_sweep_ms": xm_ms, "plain_sweep_ms": fu_ms, "xm_extra_ms": max(0.0, xm_ms - fu_ms),
+                       "gradients": n1,
+                       "note": "opt-in path (GWDP_RC=1): one read of the cost + one write of G per gradient (ncu: "
+                               "17.19 GB read + 17.13 GB written); slower than the default two-read path on this "
+                               "part (latency-bound cluster row scans on 112 SMs + the XM sweep's extra time), "
+                               "DESIGN.md 5.2b"}
     sink_gbps_step = 4 * nm_bytes * args.inner / ((elapsed_ms - grad_ms * args.steps) / args.steps / 1e3) / 1e9
     instrumented = {"ms_per_step": prof_ms / args.steps, "note": "the same solve with per-kernel-class events "
                     "(eager launches, no graphs): the source of `kernels`, `grad` and `roofline`"}
@@ -380,7 +409,7 @@ def main():
            "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config,
            "transport": args.transport if world > 1 else None, "n_ranks": world,
-           "roofline": roof, "grad": grad, "sinkhorn_GBps_per_step": sink_gbps_step, "kernels": kern,
+           "roofline": roof, "grad": grad, "grad_onepass": onepass, "sinkhorn_GBps_per_step": sink_gbps_step, "kernels": kern,
            "gpu_launches": int(cnt_c[7]),
            "gpu_launches_note": "kernel launches of one timed solve, counted by the library in the instrumented "
                                 "run (the graph replays of the headline run launch the same kernels, minus the "
