@@ -25,6 +25,9 @@
 // partials; every term non-negative) and one rounding of each prefix against the row total; the column
 // state is fp64 (shared memory) re-based every RC_FLUSH rows with fp32 increments in between; the
 // assembly V = x_i U + Zn is one fp32 fma on O(max|G|) terms.
+//
+// RCX_* macros are timing-only switches of the standalone harness scripts/rc_bench.cu (they remove one
+// part of the kernel, giving wrong results); the product build never defines them.
 #pragma once
 #include <cuda.h>
 #include "common.cuh"
