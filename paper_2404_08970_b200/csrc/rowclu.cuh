@@ -35,9 +35,15 @@
 
 namespace gw {
 
-constexpr int RC_NT = 256;              // threads per CTA
-constexpr int RC_KC = 16;               // contiguous columns per thread
-constexpr int RC_W = RC_NT * RC_KC;     // 4096 columns per CTA
+#ifndef RC_NT_DEF
+#define RC_NT_DEF 256
+#endif
+constexpr int RC_NT = RC_NT_DEF;        // threads per CTA
+constexpr int RC_W = 4096;              // columns per CTA
+constexpr int RC_KC = RC_W / RC_NT;     // contiguous columns per thread (16 or 8)
+constexpr int RC_KP = RC_KC / 2;        // column pairs per thread
+constexpr int RC_NCH = RC_KC / 4;       // 16-B chunks per thread and row
+constexpr int RC_TPL = 32 / RC_KC;      // threads per 128-B line
 constexpr int RC_RS = 7;                // TMA ring stages (rows of the CTA slice, 16 KB each)
 constexpr int RC_FLUSH = 32;            // rows between fp32 -> fp64 column-state re-basing
 
@@ -93,7 +99,7 @@ __global__ void __launch_bounds__(RC_NT, 1) k_grad_rc(const __grid_constant__ CU
   double* U64 = reinterpret_cast<double*>(ring + (size_t)RC_RS * RC_W);  // [16][NT]  U
   double* V64 = U64 + RC_KC * RC_NT;                                       // [16][NT]  V = D_X B
   float4* sgh = reinterpret_cast<float4*>(V64 + RC_KC * RC_NT);           // [4][NT]  g_hi (16 columns)
-  float4* sgl = sgh + 4 * RC_NT;                                           // [4][NT]  g_lo
+  float4* sgl = sgh + RC_NCH * RC_NT;                                      // [NCH][NT]  g_lo
   __shared__ __align__(8) uint64_t full[RC_RS];
   __shared__ unsigned int scnt[RC_RS];
   __shared__ __align__(8) uint64_t xbar[NSLOT];
@@ -147,14 +153,14 @@ __global__ void __launch_bounds__(RC_NT, 1) k_grad_rc(const __grid_constant__ CU
   // column state (pairs of adjacent columns): U = Uf + u, V = Vf + v with fp64 bases U64, V64 every
   // RC_FLUSH rows; Wf = 2c'_p - 4 Vf.  Down the column: G_i = Wf + 2c_i - 4 v;  U += 2 B_i;
   // V += (x_{i+1} - x_i) U  (V_{i+1} - V_i = dx_i (2 sum_{j<=i} B_j - sum_j B_j), PAPER.md:237-243 on columns)
-  float2 y2[8], Uf[8], Wf[8], u2[8], v2[8];
+  float2 y2[RC_KP], Uf[RC_KP], Wf[RC_KP], u2[RC_KP], v2[RC_KP];
   const double* U0 = a.U0 + cid * m;
   const double* Zn0 = a.Zn0 + cid * m;
   const double x0 = nrows > 0 ? a.xc[rb] : 0.0;
   {
     float gh[RC_KC], gl[RC_KC];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < RC_KP; ++k) {
       float yv[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -176,7 +182,7 @@ __global__ void __launch_bounds__(RC_NT, 1) k_grad_rc(const __grid_constant__ CU
       v2[k] = u2[k];
     }
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < RC_NCH; ++c) {
       sgh[c * RC_NT + t] = make_float4(gh[4 * c], gh[4 * c + 1], gh[4 * c + 2], gh[4 * c + 3]);
       sgl[c * RC_NT + t] = make_float4(gl[4 * c], gl[4 * c + 1], gl[4 * c + 2], gl[4 * c + 3]);
     }
@@ -191,10 +197,10 @@ __global__ void __launch_bounds__(RC_NT, 1) k_grad_rc(const __grid_constant__ CU
   const uint32_t rx0 = mapa(&xs[0][cr * NW + wid], peer), rbar0 = mapa(&xbar[0], peer);
   constexpr uint32_t XSTRIDE = sizeof(xs[0]), BSTRIDE = sizeof(uint64_t);
   // swizzled offsets (floats) of the thread's four 16-B chunks inside a stage
-  const int rl = t >> 1;
-  int chunk_off[4];
+  const int rl = t / RC_TPL;
+  int chunk_off[RC_NCH];
 #pragma unroll
-  for (int c = 0; c < 4; ++c) chunk_off[c] = rl * 32 + (((4 * (t & 1) + c) ^ (rl & 7)) << 2);
+  for (int c = 0; c < RC_NCH; ++c) chunk_off[c] = rl * 32 + (((RC_NCH * (t % RC_TPL) + c) ^ (rl & 7)) << 2);
 
   // per-row scalars {F_hi, F_lo, x_{i+1} - x_i, 2 c_i}: lane l holds those of row 32 g + l of the current
   // 32-row group g (and prefetches group g + 1), broadcast by shuffles -- no global-load latency per row
@@ -206,16 +212,16 @@ __global__ void __launch_bounds__(RC_NT, 1) k_grad_rc(const __grid_constant__ CU
   rnxt = rload(0);
 
   // regenerate the plan on one row of the pair (stage st) into tv
-  auto regen = [&](int j, float Fh, float Fl, float2 (&tv)[8]) {
+  auto regen = [&](int j, float Fh, float Fl, float2 (&tv)[RC_KP]) {
     const int st = j % RC_RS;
     mbar_wait(&full[st], (uint32_t)((j / RC_RS) & 1));
     const float* sp = ring + (size_t)st * RC_W;
-    float4 gv[4];
+    float4 gv[RC_NCH];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) gv[c] = *reinterpret_cast<const float4*>(sp + chunk_off[c]);
+    for (int c = 0; c < RC_NCH; ++c) gv[c] = *reinterpret_cast<const float4*>(sp + chunk_off[c]);
     const float2 F2 = make_float2(Fh, Fh), L2 = make_float2(Fl, Fl);
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < RC_NCH; ++c) {
       const float4 h4 = sgh[c * RC_NT + t], l4 = sgl[c * RC_NT + t];
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
@@ -233,7 +239,7 @@ __global__ void __launch_bounds__(RC_NT, 1) k_grad_rc(const __grid_constant__ CU
     }
     if (nv < RC_KC) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
+      for (int k = 0; k < RC_KP; ++k) {
         if (2 * k >= nv) tv[k].x = 0.f;
         if (2 * k + 1 >= nv) tv[k].y = 0.f;
       }
@@ -254,7 +260,7 @@ __global__ void __launch_bounds__(RC_NT, 1) k_grad_rc(const __grid_constant__ CU
 
   // produce pair P: plan values of both rows, the lane-exclusive warp prefixes `off` = {T0, yT0, T1, yT1}
   // of the thread's first column, and the rows' {dx, 2 c_i} in `xc`
-  auto produce = [&](int P, float2 (&t0)[8], float2 (&t1)[8], float4& off, float4& xc) {
+  auto produce = [&](int P, float2 (&t0)[RC_KP], float2 (&t1)[RC_KP], float4& off, float4& xc) {
     const int j0 = 2 * P, j1 = j0 + 1;
     if ((j0 & 31) == 0) {
       rcur = rnxt;
@@ -270,7 +276,7 @@ __global__ void __launch_bounds__(RC_NT, 1) k_grad_rc(const __grid_constant__ CU
       if (j1 < nrows) regen(j1, Fh1, Fl1, t1);
       else {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) t1[k] = make_float2(0.f, 0.f);
+        for (int k = 0; k < RC_KP; ++k) t1[k] = make_float2(0.f, 0.f);
       }
       __syncwarp();
       if (lane == 0) {
@@ -279,12 +285,12 @@ __global__ void __launch_bounds__(RC_NT, 1) k_grad_rc(const __grid_constant__ CU
       }
     } else {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) t0[k] = t1[k] = make_float2(0.f, 0.f);
+      for (int k = 0; k < RC_KP; ++k) t0[k] = t1[k] = make_float2(0.f, 0.f);
     }
     // thread totals {sum t, sum y t} of both rows, pairwise
     float2 p0 = make_float2(0.f, 0.f), q0s = p0, p1 = p0, q1s = p0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < RC_KP; ++k) {
       p0 = fadd2(p0, t0[k]);
       q0s = ffma2(y2[k], t0[k], q0s);
       p1 = fadd2(p1, t1[k]);
@@ -315,14 +321,14 @@ __global__ void __launch_bounds__(RC_NT, 1) k_grad_rc(const __grid_constant__ CU
   };
 
   // one row of the consumed pair: row DP -> B, G stored, column state advanced
-  auto row_out = [&](int jp, const float2 (&tv)[8], float a0, float b0, float dx, float ci) {
+  auto row_out = [&](int jp, const float2 (&tv)[RC_KP], float a0, float b0, float dx, float ci) {
     const float2 two = make_float2(2.f, 2.f), mtwo = make_float2(-2.f, -2.f), m4 = make_float2(-4.f, -4.f);
     const float2 a02 = make_float2(a0, a0), b02 = make_float2(b0, b0);
     const float2 ci2 = make_float2(ci, ci), dx2 = make_float2(dx, dx);
-    float2 Gv[8];
+    float2 Gv[RC_KP];
     float lp = 0.f, ly = 0.f;  // in-thread exclusive prefixes (sum t, sum y t)
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < RC_KP; ++k) {
       float2 lpk, lyk;
       lpk.x = lp;
       lyk.x = ly;
@@ -347,14 +353,14 @@ __global__ void __launch_bounds__(RC_NT, 1) k_grad_rc(const __grid_constant__ CU
       float* gp = Gout + (int64_t)jp * ld;
       if (nv == RC_KC) {  // two 256-bit stores: each lane writes whole 32-B sectors
 #pragma unroll
-        for (int h = 0; h < 2; ++h)
+        for (int h = 0; h < RC_KC / 8; ++h)
           asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(gp + 8 * h),
                        "f"(Gv[4 * h].x), "f"(Gv[4 * h].y), "f"(Gv[4 * h + 1].x), "f"(Gv[4 * h + 1].y),
                        "f"(Gv[4 * h + 2].x), "f"(Gv[4 * h + 2].y), "f"(Gv[4 * h + 3].x), "f"(Gv[4 * h + 3].y)
                        : "memory");
       } else {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < RC_KP; ++k) {
           if (2 * k < nv) gp[2 * k] = Gv[k].x;
           if (2 * k + 1 < nv) gp[2 * k + 1] = Gv[k].y;
         }
@@ -362,7 +368,7 @@ __global__ void __launch_bounds__(RC_NT, 1) k_grad_rc(const __grid_constant__ CU
     }
     if ((jp & (RC_FLUSH - 1)) == RC_FLUSH - 1) {  // re-base the column state in fp64
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
+      for (int k = 0; k < RC_KP; ++k) {
         double* U = U64 + (2 * k) * RC_NT + t;
         double* V = V64 + (2 * k) * RC_NT + t;
         const double U_0 = U[0] + (double)u2[k].x, U_1 = U[RC_NT] + (double)u2[k].y;
@@ -379,7 +385,7 @@ __global__ void __launch_bounds__(RC_NT, 1) k_grad_rc(const __grid_constant__ CU
   };
 
   // consume pair Pp: totals and this warp's offsets for both rows, then the two rows in order
-  auto consume = [&](int Pp, const float2 (&t0)[8], const float2 (&t1)[8], float4 off, float4 xc) {
+  auto consume = [&](int Pp, const float2 (&t0)[RC_KP], const float2 (&t1)[RC_KP], float4 off, float4 xc) {
     const int psl = Pp & (NSLOT - 1);
     float4 tot, pre;
 #ifndef RCX_NOEXCH
@@ -429,7 +435,7 @@ __global__ void __launch_bounds__(RC_NT, 1) k_grad_rc(const __grid_constant__ CU
     if (jp1 < nrows) row_out(jp1, t1, fmaf(2.f, pre.z + off.z, -tot.z), fmaf(-2.f, pre.w + off.w, tot.w), xc.z, xc.w);
   };
 
-  float2 tA0[8], tA1[8], tB0[8], tB1[8];
+  float2 tA0[RC_KP], tA1[RC_KP], tB0[RC_KP], tB1[RC_KP];
   float4 offA, offB, xcA, xcB;
   for (int P = 0; P <= npairs; P += 2) {
     if (P < npairs) produce(P, tA0, tA1, offA, xcA);
