@@ -592,9 +592,11 @@ static gw_status prepare(gw_ctx* c, const gw_problem* pb, Prepared& P, bool unba
     P.mass_p = h[3];
     P.mass_q = h[11];
   }
-  k_prep<<<grid_for(n), 256, 0, c->stream>>>(P.x, P.p, n, mom, xc, pn, lp, cx, !unbalanced);
+  TRY(ws(c, c->yfb, m, &P.yf));
+  TRY(ws(c, c->pnf, n, &P.pnf)); TRY(ws(c, c->qnf, m, &P.qnf));
+  k_prep<<<grid_for(n), 256, 0, c->stream>>>(P.x, P.p, n, mom, xc, pn, lp, cx, !unbalanced, P.pnf);
   KCHECK();
-  k_prep<<<grid_for(m), 256, 0, c->stream>>>(P.y, P.q, m, mom + 8, yc, qn, lq, cy, !unbalanced);
+  k_prep<<<grid_for(m), 256, 0, c->stream>>>(P.y, P.q, m, mom + 8, yc, qn, lq, cy, !unbalanced, P.qnf, P.yf);
   KCHECK();
   P.xc = xc; P.yc = yc; P.pn = pn; P.qn = qn; P.lp = lp; P.lq = lq; P.cx = cx; P.cy = cy;
   P.k = pb->k;
@@ -612,26 +614,12 @@ static gw_status prepare(gw_ctx* c, const gw_problem* pb, Prepared& P, bool unba
     k_poly_const<<<1, 1024, 0, c->stream>>>(yc, qn, m, cy);
     KCHECK();
   }
-  TRY(ws(c, c->yfb, m, &P.yf));
-  k_to_float<<<grid_for(m), 256, 0, c->stream>>>(yc, m, P.yf);
-  KCHECK();
-  TRY(ws(c, c->pnf, n, &P.pnf)); TRY(ws(c, c->qnf, m, &P.qnf));
-  k_to_float<<<grid_for(n), 256, 0, c->stream>>>(pn, n, P.pnf);
-  KCHECK();
-  k_to_float<<<grid_for(m), 256, 0, c->stream>>>(qn, m, P.qnf);
-  KCHECK();
-  P.xlast = h[6] * 0.0;  // filled below from host copies of the endpoints
-  // endpoints in centred coordinates: x_{n-1} - xmid = (x_{n-1} - x_0) / 2
-  double ends[4];
-  CU(cudaMemcpyAsync(&ends[0], P.x, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  CU(cudaMemcpyAsync(&ends[1], P.x + n - 1, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  CU(cudaMemcpyAsync(&ends[2], P.y, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  CU(cudaMemcpyAsync(&ends[3], P.y + m - 1, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  CU(cudaStreamSynchronize(c->stream));
-  P.xlast = ends[1] - h[6];
-  P.ylast = ends[3] - h[14];
-  P.xend_u = ends[1];
-  P.yend_u = ends[3];
+  // endpoints (k_validate's slot 7, read with the moments): x_{n-1} in the caller's coordinates and,
+  // centred, x_{n-1} - xmid = (x_{n-1} - x_0) / 2
+  P.xlast = h[7] - h[6];
+  P.ylast = h[15] - h[14];
+  P.xend_u = h[7];
+  P.yend_u = h[15];
   return shard_table(c, P);
 }
 

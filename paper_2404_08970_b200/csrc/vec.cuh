@@ -7,7 +7,7 @@ namespace gw {
 // ---------------------------------------------------------------------------------
 // Validation + moments of one (support, marginal) pair, one CTA of 1024 threads.
 // out[0..7] = {unsorted, negative, nonfinite, S0 = sum w, S1 = sum xc w, S2 = sum xc^2 w,
-//              xmid, unused}, xc = x - xmid, xmid = (x_0 + x_{n-1}) / 2.
+//              xmid, x_{n-1}}, xc = x - xmid, xmid = (x_0 + x_{n-1}) / 2.
 // Fixed-order reduction => deterministic (SPEC.md:68-76 validate_measure).
 // ---------------------------------------------------------------------------------
 __global__ void __launch_bounds__(1024) k_validate(const double* __restrict__ x0, const double* __restrict__ w0,
@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(1024) k_validate(const double* __restrict__ x0
   s1 = block_sum<32>(s1, sm);
   s2 = block_sum<32>(s2, sm);
   if (threadIdx.x == 0) {
-    o[0] = uns; o[1] = neg; o[2] = nf; o[3] = s0; o[4] = s1; o[5] = s2; o[6] = xmid; o[7] = 0;
+    o[0] = uns; o[1] = neg; o[2] = nf; o[3] = s0; o[4] = s1; o[5] = s2; o[6] = xmid; o[7] = x[n - 1];
   }
 }
 
@@ -51,7 +51,8 @@ __global__ void __launch_bounds__(1024) k_validate(const double* __restrict__ x0
 // ---------------------------------------------------------------------------------
 __global__ void k_prep(const double* __restrict__ x, const double* __restrict__ w, int64_t n,
                        const double* __restrict__ mom, double* __restrict__ xc, double* __restrict__ wn,
-                       double* __restrict__ lw, double* __restrict__ cvec, bool normalize = true) {
+                       double* __restrict__ lw, double* __restrict__ cvec, bool normalize = true,
+                       float* __restrict__ wf = nullptr, float* __restrict__ xf = nullptr) {
   // normalize = false (unbalanced GW): wn = w as given (mass S0), cvec = (D o D) w = S0 (v^2 - 2 v mu1 + mu2)
   const double xmid = mom[6], S0 = mom[3];
   const double mu1 = mom[4] / S0, mu2 = mom[5] / S0, inv = normalize ? 1.0 / S0 : 1.0, cs = normalize ? 1.0 : S0;
@@ -62,6 +63,8 @@ __global__ void k_prep(const double* __restrict__ x, const double* __restrict__ 
     wn[i] = wv;
     lw[i] = log(wv);
     cvec[i] = cs * (v * v - 2.0 * v * mu1 + mu2);
+    if (wf) wf[i] = (float)wv;  // fp32 copies (the fp32 gradient path's T^0 = p q^T, centred y)
+    if (xf) xf[i] = (float)v;
   }
 }
 

@@ -90,6 +90,33 @@ def main():
         names = ["grad_moments", "grad_carry", "grad_main", "sink_row", "sink_col", "sink_fused", "objective"]
         print("ugw instrumented: %.3f ms; classes: %s" % (e0.elapsed_time(e1),
               {nm: round(ms_c[i], 3) for i, nm in enumerate(names)}))
+    elif case == "c3grad":
+        # gw_grad_dp on an explicit plan at N = M = n (C3: 16384), per kernel class (instrumented) + plain
+        import ctypes as C
+        from paper_2404_08970_b200 import _lib
+        x, y = np.sort(rng.random(n)), np.sort(rng.random(n))
+        p = np.full(n, 1.0 / n)
+        T = api.plan_buffer(n, n, dev)
+        T.copy_(torch.rand((n, n), device=dev) / (n * n))
+        ctx = api.Context.get(dev)
+        lib = _lib.load()
+        for _ in range(3):
+            api.grad(x, y, p, p, T)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10):
+            api.grad(x, y, p, p, T)
+        e1.record()
+        torch.cuda.synchronize()
+        print("gw_grad_dp %d^2: %.4f ms per call" % (n, e0.elapsed_time(e1) / 10))
+        ms_c = (C.c_double * 10)()
+        cnt_c = (C.c_int64 * 10)()
+        _lib.check(lib.gw_ctx_profile(ctx.h, 2, None, None, 0))
+        for _ in range(10):
+            api.grad(x, y, p, p, T)
+        _lib.check(lib.gw_ctx_profile(ctx.h, 0, C.cast(ms_c, C.c_void_p), C.cast(cnt_c, C.c_void_p), 10))
+        print({nm: round(ms_c[i] / 10, 4) for i, nm in enumerate(["moments", "carry", "main"])})
     elif case == "onepass":
         # the solver's gradient on the one-read path (rowclu.cuh) and the XM sweep that feeds it, C4 recipe
         # at N = M = n: 3 outer x 3 inner, instrumented (eager launches); then the two-read path
