@@ -173,14 +173,20 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
   return d;
 }
 
-// 2^x on the FMA pipe for a pair (offloads MUFU): x clamped at -126, n = rint(x) by the 1.5 2^23 shift,
-// f = x - n in [-1/2, 1/2], 2^f by a degree-5 polynomial (max rel. error 2.4e-7 in fp32 Horner, the size of
-// MUFU ex2.approx's), scaled by adding n to the exponent field.
+// 2^x on the FMA pipe for a pair (offloads MUFU): x clamped to [-126, 128] (the lower bound NaN-propagating,
+// so a NaN argument becomes 128), n = rint(x) by the 1.5 2^23 shift, f = x - n in [-1/2, 1/2], 2^f by a
+// degree-5 polynomial (max rel. error 2.4e-7 in fp32 Horner, the size of MUFU ex2.approx's), n added to the
+// exponent field.  n = 128 (overflow, or a NaN argument) gives inf / NaN, which the iteration's validity
+// check rejects exactly as it rejects MUFU's inf / NaN.
+__device__ __forceinline__ float clamp_ex2(float x) {
+  float y;
+  asm("{\n\t.reg .f32 t;\n\tmax.NaN.f32 t, %1, 0fC2FC0000;\n\tmin.f32 %0, t, 0f43000000;\n\t}"
+      : "=f"(y) : "f"(x));  // max(x, -126) keeping NaN, then min(., 128) turning NaN into 128
+  return y;
+}
 __device__ __forceinline__ float2 ex2_poly2(float2 x) {
-  x.x = fminf(fmaxf(x.x, -126.f), 128.f);  // 128: inf / NaN, as MUFU's overflow (caught by the check)
-  x.y = fminf(fmaxf(x.y, -126.f), 128.f);
-  const float2 mg = make_float2(12582912.f, 12582912.f);
-  const float2 r = fadd2(x, mg);
+  x = make_float2(clamp_ex2(x.x), clamp_ex2(x.y));
+  const float2 r = fadd2(x, make_float2(12582912.f, 12582912.f));
   const float2 f = fadd2(x, make_float2(-(r.x - 12582912.f), -(r.y - 12582912.f)));
   float2 p = make_float2(0.0013276450335979462f, 0.0013276450335979462f);
   p = ffma2(p, f, make_float2(0.009675541892647743f, 0.009675541892647743f));
@@ -188,6 +194,7 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   p = ffma2(p, f, make_float2(0.24022120237350464f, 0.24022120237350464f));
   p = ffma2(p, f, make_float2(0.6931469440460205f, 0.6931469440460205f));
   p = ffma2(p, f, make_float2(1.0000001192092896f, 1.0000001192092896f));
+  // the low bits of r are n + 2^22 + 2^23, which the shift by 23 drops
   return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(r.x) << 23)),
                      __int_as_float(__float_as_int(p.y) + (__float_as_int(r.y) << 23)));
 }
