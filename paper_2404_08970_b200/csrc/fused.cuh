@@ -153,6 +153,9 @@ __device__ __forceinline__ float warp_sum_bfly(float v) {
 #ifndef FUSED_POLY_K
 #define FUSED_POLY_K 5  // the chunk (of K = 8) whose exponentials run on the FMA pipe
 #endif
+#ifndef FUSED_POLY_K6
+#define FUSED_POLY_K6 5  // K = 6 instances (rows of 24576, C5): one chunk in six (0.584 -> 0.568 ms)
+#endif
 // packed fp32x2 arithmetic (sm_100: FFMA2 / FADD2 -- two lanes per instruction)
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
   float2 d;
@@ -478,7 +481,7 @@ __global__ void __launch_bounds__(NT, 1) k_sink_fused2(FusedArgs a) {
             a10 = fadd2(a10, ffma2(make_float2(g1.x, g1.y), ncl2, fadd2(glv[k][0], L1)));
             a11 = fadd2(a11, ffma2(make_float2(g1.z, g1.w), ncl2, fadd2(glv[k][1], L1)));
           }
-          if (K >= 8 && k == FUSED_POLY_K) {
+          if ((K >= 8 && k == FUSED_POLY_K) || (FUSED_POLY_K6 >= 0 && K == 6 && k == FUSED_POLY_K6)) {
             // one chunk in eight on the FMA pipe (ex2_poly2): MUFU.EX2 is the kernel's busiest unit
             // (XU 47 %); measured 2.86 -> 2.82 ms per iteration at C4 (profiles/r02_fused_poly_offload.jsonl)
             c0e[k][0] = ex2_poly2(a00); c0e[k][1] = ex2_poly2(a01); c1e[k][0] = ex2_poly2(a10); c1e[k][1] = ex2_poly2(a11);
