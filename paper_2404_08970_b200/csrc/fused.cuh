@@ -27,7 +27,13 @@ namespace gw {
 // slots would not leave room for a fifth next to the 64 KB of fp64 column accumulators
 template <int NT>
 __host__ __device__ constexpr int fstages() { return NT >= 512 ? 4 : 5; }
-constexpr int FFLUSH = 32;             // rows between fp32 -> fp64 column-accumulator flushes
+#ifndef FFLUSH_DEF
+#define FFLUSH_DEF 64
+#endif
+// rows between fp32 -> fp64 column-accumulator flushes: a fp32 sum of <= 64 positive terms (relative error
+// <= 63 u = 3.8e-6 worst case, ~sqrt(64) u typical), folded in fp64; the flush (F2F conversions) cost 2 %
+// of the iteration at 32 rows, 1 % at 64 (profiles/r02_fused_poly_offload.jsonl)
+constexpr int FFLUSH = FFLUSH_DEF;
 
 struct FusedArgs {
   const float* G;
