@@ -157,7 +157,10 @@ __device__ __forceinline__ float warp_sum_bfly(float v) {
 }
 
 #ifndef FUSED_POLY_K
-#define FUSED_POLY_K 5  // the chunk (of K = 8) whose exponentials run on the FMA pipe
+#define FUSED_POLY_K 5  // a chunk (of K = 8) whose exponentials run on the FMA pipe
+#endif
+#ifndef FUSED_POLY_K2
+#define FUSED_POLY_K2 2  // a second chunk: {2, 5} measured best of the pairs (2.778 -> 2.767 ms; {1,5}, {5,7}: slower)
 #endif
 #ifndef FUSED_POLY_K6
 #define FUSED_POLY_K6 5  // K = 6 instances (rows of 24576, C5): one chunk in six (0.584 -> 0.568 ms)
@@ -487,9 +490,10 @@ __global__ void __launch_bounds__(NT, 1) k_sink_fused2(FusedArgs a) {
             a10 = fadd2(a10, ffma2(make_float2(g1.x, g1.y), ncl2, fadd2(glv[k][0], L1)));
             a11 = fadd2(a11, ffma2(make_float2(g1.z, g1.w), ncl2, fadd2(glv[k][1], L1)));
           }
-          if ((K >= 8 && k == FUSED_POLY_K) || (FUSED_POLY_K6 >= 0 && K == 6 && k == FUSED_POLY_K6)) {
-            // one chunk in eight on the FMA pipe (ex2_poly2): MUFU.EX2 is the kernel's busiest unit
-            // (XU 47 %); measured 2.86 -> 2.82 ms per iteration at C4 (profiles/r02_fused_poly_offload.jsonl)
+          if ((K >= 8 && (k == FUSED_POLY_K || k == FUSED_POLY_K2)) || (FUSED_POLY_K6 >= 0 && K == 6 && k == FUSED_POLY_K6)) {
+            // chunks 2 and 5 of 8 (K = 8), 5 of 6 (K = 6) on the FMA pipe (ex2_poly2): MUFU.EX2 is the
+            // kernel's busiest unit (XU 47 %); with the 64-row flush 2.86 -> 2.77 ms per iteration at C4
+            // (profiles/r02_fused_poly_offload.jsonl)
             c0e[k][0] = ex2_poly2(a00); c0e[k][1] = ex2_poly2(a01); c1e[k][0] = ex2_poly2(a10); c1e[k][1] = ex2_poly2(a11);
           } else {
             c0e[k][0] = make_float2(ex2_ftz(a00.x), ex2_ftz(a00.y));
