@@ -9,9 +9,17 @@ int main(int argc, char** argv) {
 #ifdef FU_K6  // C5's shape: K = 6, clusters of 4 CTAs of 6144 columns
   const int64_t n = 32768, m = 24576, ld = m;
   constexpr int KK = 6, CLL = 4;
+#elif defined(FU_NT512)
+  const int64_t n = 65536, m = 65536, ld = m;
+  constexpr int KK = 4, CLL = 8;
 #else
   const int64_t n = 65536, m = 65536, ld = m;
   constexpr int KK = 8, CLL = 8;
+#endif
+#ifdef FU_NT512
+  constexpr int NTT = 512;
+#else
+  constexpr int NTT = 256;
 #endif
   float* G; cudaMalloc(&G, n * ld * 4);
   fillf<<<1184, 256>>>(G, n * ld, 0.01f, 0.f);
@@ -20,20 +28,20 @@ int main(int argc, char** argv) {
   cudaMalloc(&pf, n * 4); cudaMalloc(&Srow, n * 4); cudaMalloc(&part, 160 * m * 8); cudaMalloc(&mode, 16);
   fillf<<<64, 256>>>(fh, n, 1.f, -17.f); fillf<<<64, 256>>>(fl, n, 0.f, 0.f); fillf<<<64, 256>>>(gh, m, 1.f, 0.f);
   fillf<<<64, 256>>>(pf, n, 0.f, 1.f / n); filli<<<1, 1>>>(mode, 1);
-  auto k = k_sink_fused2<KK, CLL, 256, false>;
-  const size_t dsm = fused_dyn_smem<KK, 256>();
+  auto k = k_sink_fused2<KK, CLL, NTT, false>;
+  const size_t dsm = fused_dyn_smem<KK, NTT>();
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = CLL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
   cudaLaunchConfig_t cfg = {};
-  cfg.blockDim = dim3(256); cfg.dynamicSmemBytes = dsm; cfg.attrs = at; cfg.numAttrs = 1;
+  cfg.blockDim = dim3(NTT); cfg.dynamicSmemBytes = dsm; cfg.attrs = at; cfg.numAttrs = 1;
   cfg.gridDim = dim3(148 * CLL);
   int ncl = 0; cudaOccupancyMaxActiveClusters(&ncl, (void*)k, &cfg);
   cfg.gridDim = dim3(ncl * CLL);
   FusedArgs a = {};
   a.G = G; a.ld = ld; a.nl = n; a.m = m; a.c2f = 1442.7f; a.gh = gh; a.gl = gl; a.fh = fh; a.fl = fl; a.pf = pf;
-  a.kappa = 1.f; a.Srow = Srow; a.part = part; a.rows_per_cluster = (n + ncl - 1) / ncl; a.wcol = 4 * KK * 256; a.mode = mode; a.stop = nullptr;
+  a.kappa = 1.f; a.Srow = Srow; a.part = part; a.rows_per_cluster = (n + ncl - 1) / ncl; a.wcol = 4 * KK * NTT; a.mode = mode; a.stop = nullptr;
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   cudaLaunchKernelEx(&cfg, k, a);
   cudaDeviceSynchronize();
