@@ -30,6 +30,12 @@
 
 using namespace gw;
 
+// The next Sinkhorn iteration tries the fused (absorbed-dual) path iff the last column correction
+// |log2(CS/q)| was within 2^FUSED_THRESH (§5.3); a failed attempt is caught by k_sink_fast_check
+#ifndef FUSED_THRESH
+#define FUSED_THRESH 20.f
+#endif
+
 // ------------------------------------------------------------------------------ errors
 static thread_local std::string g_err;
 
@@ -1832,7 +1838,7 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
       KCHECK();
     }
     PROF_END(c, PC_SINK_COL, 2);
-    k_sink_mode<<<1, 32, 0, c->stream>>>(s.dev, s.mode, s.fK > 0 ? 20.f : -1.f, s.flag);
+    k_sink_mode<<<1, 32, 0, c->stream>>>(s.dev, s.mode, s.fK > 0 ? FUSED_THRESH : -1.f, s.flag);
     KCHECK();
     return GW_OK;
   };
@@ -1887,7 +1893,7 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
           s.Srow, nl, P.lp + P.row0, s.f, s.fh, s.fl, nullptr, s.ung, P.R, U, m, P.lq, eps, s.g, s.gh, s.gl,
           s.mode, s.stop, s.dev, s.flag, kappa);
       KCHECK();
-      k_sink_slot_end<<<1, 32, 0, c->stream>>>(s.mode, s.dev, s.flag, s.stop, 20.f);
+      k_sink_slot_end<<<1, 32, 0, c->stream>>>(s.mode, s.dev, s.flag, s.stop, FUSED_THRESH);
       KCHECK();
       return GW_OK;
     };
@@ -2017,7 +2023,7 @@ static gw_status sink_run(gw_ctx* c, const Prepared& P, SinkState& s, const floa
               c->stream = c->cap;
             }
           }
-          k_sink_mode<<<1, 32, 0, c->stream>>>(s.dev, s.mode, 20.f, s.flag);
+          k_sink_mode<<<1, 32, 0, c->stream>>>(s.dev, s.mode, FUSED_THRESH, s.flag);
         }
         c->stream = saved;
         cudaGraph_t go = nullptr;
