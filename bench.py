@@ -129,8 +129,14 @@ def oracle_sample(n_s, n_full, inner=100, sweeps=3):
     t0 = time.perf_counter()
     O.sinkhorn(G, P.p, P.q, P.eps, sweeps)
     t_sweep = (time.perf_counter() - t0) / sweeps
+    # the oracle's O(N^2) dynamic-programme gradient (the paper's algorithm, grad_prescribed_dp: pinned
+    # against the dense one) -- the like-for-like algorithm on the host cores, reported beside
+    t0 = time.perf_counter()
+    O.grad_prescribed_dp(P.x, P.y, P.p, P.q, T)
+    t_grad_dp = time.perf_counter() - t0
     r = n_full / n_s
     t_outer = t_grad * r ** 3 + inner * t_sweep * r ** 2
+    t_outer_dp = (t_grad_dp + inner * t_sweep) * r ** 2
     cores = len(os.sched_getaffinity(0))
     try:
         from threadpoolctl import threadpool_info
@@ -142,7 +148,11 @@ def oracle_sample(n_s, n_full, inner=100, sweeps=3):
                        "%d Sinkhorn iterations at %.4f s each, extrapolated to N=M=%d as "
                        "t_grad*(N/%d)^3 + %d*t_sweep*(N/%d)^2" % (n_s, t_grad, sweeps, t_sweep, n_full, n_s, inner,
                                                                    n_s)),
-            "t_grad_s": t_grad, "t_sweep_s": t_sweep,
+            "t_grad_s": t_grad, "t_sweep_s": t_sweep, "t_grad_dp_s": t_grad_dp,
+            "value_with_dp_gradient": 1.0 / t_outer_dp,
+            "value_with_dp_gradient_note": ("the same outer iteration with the oracle's O(N^2) DP gradient "
+                                            "(grad_prescribed_dp, PAPER.md:203-259), extrapolated (N/%d)^2: "
+                                            "GPU vs CPU on the same algorithm" % n_s),
             "note": ("the oracle's gradient is the DENSE definition (O(N^3)): a GPU/oracle ratio mixes the DP's "
                      "O(N^2) vs O(N^3) advantage with GPU vs CPU, so it is context, not a measure of kernel "
                      "quality (the roofline fraction is)")}
