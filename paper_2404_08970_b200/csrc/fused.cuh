@@ -160,7 +160,7 @@ __device__ __forceinline__ float warp_sum_bfly(float v) {
 #define FUSED_POLY_K 5  // a chunk (of K = 8) whose exponentials run on the FMA pipe
 #endif
 #ifndef FUSED_POLY_K2
-#define FUSED_POLY_K2 2  // a second chunk: {2, 5} measured best of the pairs (2.778 -> 2.767 ms; {1,5}, {5,7}: slower)
+#define FUSED_POLY_K2 -1  // a second chunk: {2, 5} gained 0.4 % at full clocks but lost 2 % under sw_power_cap (sustained harness)
 #endif
 #ifndef FUSED_POLY_K6
 #define FUSED_POLY_K6 5  // K = 6 instances (rows of 24576, C5): one chunk in six (0.584 -> 0.568 ms)
@@ -491,9 +491,9 @@ __global__ void __launch_bounds__(NT, 1) k_sink_fused2(FusedArgs a) {
             a11 = fadd2(a11, ffma2(make_float2(g1.z, g1.w), ncl2, fadd2(glv[k][1], L1)));
           }
           if ((K >= 8 && (k == FUSED_POLY_K || k == FUSED_POLY_K2)) || (FUSED_POLY_K6 >= 0 && K == 6 && k == FUSED_POLY_K6)) {
-            // chunks 2 and 5 of 8 (K = 8), 5 of 6 (K = 6) on the FMA pipe (ex2_poly2): MUFU.EX2 is the
-            // kernel's busiest unit (XU 47 %); with the 64-row flush 2.86 -> 2.77 ms per iteration at C4
-            // (profiles/r02_fused_poly_offload.jsonl)
+            // chunk 5 of 8 (K = 8), 5 of 6 (K = 6) on the FMA pipe (ex2_poly2): MUFU.EX2 is the kernel's
+            // busiest unit (XU 47 %); with the 64-row flush 2.86 -> 2.78 ms per iteration at C4 at full
+            // clocks, 3.11 -> 3.07 ms under sw_power_cap (profiles/r02_fused_poly_offload.jsonl)
             c0e[k][0] = ex2_poly2(a00); c0e[k][1] = ex2_poly2(a01); c1e[k][0] = ex2_poly2(a10); c1e[k][1] = ex2_poly2(a11);
           } else {
             c0e[k][0] = make_float2(ex2_ftz(a00.x), ex2_ftz(a00.y));

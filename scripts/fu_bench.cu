@@ -1,6 +1,7 @@
 // standalone timing harness for k_sink_fused2<8,8,256> at N = M = 65536 (random inputs; experiments only):
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 scripts/fu_bench.cu -o fu
 #include <cstdio>
+#include <cstdlib>
 #include "../paper_2404_08970_b200/csrc/fused.cuh"
 using namespace gw;
 __global__ void fillf(float* p, size_t n, float v, float o) { for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = o + v * (float)((i * 2654435761u) % 1000) * 1e-3f; }
@@ -46,7 +47,7 @@ int main(int argc, char** argv) {
   cudaLaunchKernelEx(&cfg, k, a);
   cudaDeviceSynchronize();
   cudaEventRecord(e0);
-  const int R = 10;
+  const int R = argc > 2 ? atoi(argv[2]) : 10;  // >= 500: sustained (power-capped) load
   for (int i = 0; i < R; ++i) cudaLaunchKernelEx(&cfg, k, a);
   cudaEventRecord(e1); cudaEventSynchronize(e1);
   float ms; cudaEventElapsedTime(&ms, e0, e1);
