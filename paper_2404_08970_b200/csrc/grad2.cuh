@@ -678,3 +678,41 @@ __global__ void __launch_bounds__(256) k_ugw_moments(TSrc2 S, int64_t nl, int64_
 }
 
 }  // namespace gw
+
+namespace gw {
+
+// ---------------------------------------------------------------------------------
+// The gradient on the product plan T^0 = p q^T (the first outer iteration, PAPER.md:120-126 with a
+// rank-1 plan): D_X T D_Y = (D_X p)(D_Y q)^T, so
+//   G_ip = 2 c_i + 2 c'_p - 4 a_i b_p,   a = D_X p,  b = D_Y q   (1-D DPs)
+// -- one write of G (4 N M bytes) instead of the general moments + main passes.  Thread: one float4 of
+// columns x 32 rows; fp32 assembly of O(max|G|) terms as in the main pass (two roundings).
+// ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_grad_product(float* __restrict__ G, int64_t ld, int64_t nl, int64_t m,
+                                                      const double* __restrict__ a, const double* __restrict__ c,
+                                                      const double* __restrict__ b, const double* __restrict__ c2) {
+  const int64_t q = 4 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+  const int64_t i0 = (int64_t)blockIdx.y * 32;
+  if (q >= m) return;
+  float bq[4], dq[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    bq[e] = q + e < m ? (float)b[q + e] : 0.f;
+    dq[e] = q + e < m ? (float)(2.0 * c2[q + e]) : 0.f;
+  }
+  const bool full = q + 3 < m;
+  const int nr = (int)min((int64_t)32, nl - i0);
+  for (int r = 0; r < nr; ++r) {
+    const int64_t i = i0 + r;
+    const float A = (float)(-4.0 * a[i]), C = (float)(2.0 * c[i]);
+    float g[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) g[e] = fmaf(A, bq[e], C + dq[e]);
+    float* gp = G + i * ld + q;
+    if (full) __stcs(reinterpret_cast<float4*>(gp), make_float4(g[0], g[1], g[2], g[3]));
+    else
+      for (int e = 0; e < 4 && q + e < m; ++e) gp[e] = g[e];
+  }
+}
+
+}  // namespace gw

@@ -1610,6 +1610,35 @@ static gw_status sink_alloc(gw_ctx* c, const Prepared& P, SinkState& s) {
   return GW_OK;
 }
 
+// The gradient on the product plan T^0 = p q^T (k = 1, 1-D supports, GW): the closed form of
+// k_grad_product (a = D_X p over all n rows, b = D_Y q by the 1-D programmes), one write of G.
+static gw_status grad_product(gw_ctx* c, const Prepared& P, float* G, int64_t ldG) {
+  const int64_t n = P.n, m = P.m, nl = P.nl;
+  if (nl == 0) return GW_OK;
+  double *a, *b;
+  TRY(ws(c, c->DP, (size_t)n, &a));
+  TRY(ws(c, c->DA, (size_t)m, &b));
+  PROF_BEGIN(c, PC_GRAD_CARRY);
+  Scan1DBatch B;
+  memset(&B, 0, sizeof(B));
+  B.d[0] = Scan1D{P.pn, P.xc, n, nullptr, a, nullptr};
+  B.d[1] = Scan1D{P.qn, P.yc, m, nullptr, b, nullptr};
+  const int K = (int)std::min<int64_t>(SCAN_KMAX, std::max<int64_t>(1, (std::max(n, m) + 4095) / 4096));
+  double* wt;
+  TRY(ws(c, c->scanwt, (size_t)4 * K * 32 * 3, &wt));
+  k_scan1d_tot<<<dim3(K, 2), 1024, 0, c->stream>>>(B, K, wt);
+  KCHECK();
+  k_scan1d_out<<<dim3(K, 2), 1024, 0, c->stream>>>(B, K, wt);
+  KCHECK();
+  PROF_END(c, PC_GRAD_CARRY, 2);
+  PROF_BEGIN(c, PC_GRAD_MAIN);
+  const dim3 grid((unsigned)((m + 1023) / 1024), (unsigned)((nl + 31) / 32));
+  k_grad_product<<<grid, 256, 0, c->stream>>>(G, ldG, nl, m, a + P.row0, P.cx + P.row0, b, P.cy);
+  KCHECK();
+  PROF_END(c, PC_GRAD_MAIN, 1);
+  return GW_OK;
+}
+
 // The solver's gradient on the 8 N M path (rowclu.cuh), k = 1, one rank: requires that the last
 // Sinkhorn iteration ran the XM sweep (s.rcpart / s.rcpartx / s.csl hold its column sums).
 static gw_status grad_rc(gw_ctx* c, const Prepared& P, SinkState& s, float* G, int64_t ldG, const TSrc2& S2) {
@@ -2394,6 +2423,8 @@ static gw_status solve_impl(gw_ctx* c, const gw_problem* pb, const gw_solve_opts
     } else if (mode == T_GIBBS && rc_next && !obj) {
       TRY(grad_rc(c, P, s, G, ldG, S2));  // one read + one write (rowclu.cuh)
       ++onepass;
+    } else if (mode == T_PRODUCT && P.k == 1 && !P.grid2d && !fx && !tau_mode && !obj) {
+      TRY(grad_product(c, P, G, ldG));  // closed form on T^0 = p q^T: one write
     } else {
       TRY(grad_pass(c, P, mode, S, S2, G, ldG, true, obj, fx, fy, alpha, objout, beta));
     }

@@ -127,3 +127,18 @@ def test_onepass_not_taken_where_unsupported(gw):
     assert r.grad_onepass_total == 0
     r = gw.solve(x, y, p, q, 0.02, 3, 40, k=2, device=_dev())
     assert r.grad_onepass_total == 0
+
+
+@pytest.mark.parametrize("n,m", [(1, 1), (5, 300), (300, 517), (777, 5003), (2048, 1031)])
+def test_product_plan_gradient_closed_form(gw, n, m):
+    """The first outer iteration's gradient on T^0 = p q^T: the solver writes the closed form
+    2c_i + 2c'_p - 4 (D_X p)_i (D_Y q)_p (k_grad_product); exported G^1 vs the oracle on p q^T."""
+    x, y, p, q = _problem(n + 3 * m, n, m)
+    r, Tb, Gb = _export(gw, x, y, p, q, 0.02, 1, 10, 1)
+    T = Tb.cpu().numpy().astype(np.float64)
+    np.testing.assert_allclose(T, np.outer(p, q), rtol=2e-7, atol=1e-30)
+    G = Gb.cpu().numpy().astype(np.float64)
+    Go = O.grad_prescribed(x, y, p, q, np.outer(p, q))
+    err = np.max(np.abs(G - Go)) / max(np.max(np.abs(Go)), 1e-300)
+    print("product-plan gradient %dx%d: %.3e of max|G|" % (n, m, err))
+    assert err <= GRAD_TOL, err
