@@ -169,6 +169,7 @@ __device__ __forceinline__ void g2_stage_fast(const G2Loader<MODE>& L, const TSr
                                               const float* __restrict__ sF, const float* __restrict__ sFl, int sub,
                                               float* __restrict__ sT2, float* ent) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float2 entv = make_float2(0.f, 0.f);  // OBJ, Gibbs: two interleaved fp32 partial sums of T (ln T - 1)
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int phys = g2_phys(128 * h + 4 * lane);
@@ -201,11 +202,13 @@ __device__ __forceinline__ void g2_stage_fast(const G2Loader<MODE>& L, const TSr
           lt = make_float4(a0.x * ln2, a0.y * ln2, a1.x * ln2, a1.y * ln2);
         }
         if (OBJ) {
-          constexpr float ln2 = 0.6931471805599453f;
-          const float av[4] = {a0.x, a0.y, a1.x, a1.y}, tv[4] = {t.x, t.y, t.z, t.w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            if (tv[e] > 0.f) *ent += tv[e] * fmaf(av[e], ln2, -1.f);
+          // T (ln T - 1) with ln T = a ln 2, packed, no branch: a clamped at -200 (T = 0 there) so that a
+          // zero-mass column's a = -inf contributes 0 x finite
+          const float2 l2 = make_float2(0.6931471805599453f, 0.6931471805599453f), m1 = make_float2(-1.f, -1.f);
+          const float2 A0 = make_float2(fmaxf(a0.x, -200.f), fmaxf(a0.y, -200.f));
+          const float2 A1 = make_float2(fmaxf(a1.x, -200.f), fmaxf(a1.y, -200.f));
+          entv = ffma2(make_float2(t.x, t.y), ffma2(A0, l2, m1), entv);
+          entv = ffma2(make_float2(t.z, t.w), ffma2(A1, l2, m1), entv);
         }
       }
       if (OBJ && MODE != T_GIBBS) {
@@ -219,6 +222,7 @@ __device__ __forceinline__ void g2_stage_fast(const G2Loader<MODE>& L, const TSr
       if (LNT) *reinterpret_cast<float4*>(sT2 + rl * G2RS + phys) = lt;
     }
   }
+  if (OBJ && MODE == T_GIBBS) *ent += entv.x + entv.y;
 }
 
 // ---------------------------------------------------------------------------------
