@@ -69,14 +69,20 @@ typedef enum {
   GW_ERR_NOT_NORMALIZED = 5,  /* |sum - 1| > 1e-9                        */
   GW_ERR_NONFINITE = 6,       /* NaN/Inf in inputs or produced          */
   GW_ERR_CONFIG = 7,          /* invalid options                                       */
-  GW_ERR_UNSUPPORTED = 8,     /* k > GW_MAX_K, loss != square, fp64 storage, tau != eps off k = 1, ... */
+  GW_ERR_UNSUPPORTED = 8,     /* k > GW_MAX_K, loss != square, GW_F64 off k = 1 / 1-D, tau != eps off k = 1, ... */
   GW_ERR_OOM = 9,
   GW_ERR_CUDA = 10,
   GW_ERR_NCCL = 11
 } gw_status;
 
 typedef enum { GW_LOSS_SQUARE = 0 } gw_loss;       /* the only loss the paper defines */
-typedef enum { GW_F32 = 0, GW_F64 = 1 } gw_dtype;  /* storage of every N x M matrix */
+/* Storage of every N x M matrix (T, G, T0, T_out, export buffers) of a call.  GW_F32: the bandwidth
+ * path (C2-C5).  GW_F64 (C1 = BASELINE configs[0], SURVEY.md §8 sizes table): every matrix float64 and
+ * every step in fp64 (the DP gradient as a row scan and a column scan, the log-domain Sinkhorn updates,
+ * the objective) -- parity ~1e-12 with the float64 oracle; k = 1 on 1-D supports only (other k, 2-D
+ * grids, ugw_solve, tau != eps: GW_ERR_UNSUPPORTED).  The solver keeps its plan explicit then (two
+ * fp64 N x M buffers).  Any other value: GW_ERR_INVALID_ARG. */
+typedef enum { GW_F32 = 0, GW_F64 = 1 } gw_dtype;
 
 /* problem flags */
 #define GW_NO_VALIDATE     0x1u  /* skip sortedness / marginal checks (caller guarantees them) */
@@ -97,7 +103,7 @@ typedef struct {
   const double *p, *q;    /* marginals, >= 0, sum 1 within 1e-9 (length n and m)       */
   int32_t k;              /* distance power |x - x'|^k: 1 (hot path) .. GW_MAX_K (R17, f2) */
   int32_t loss;           /* gw_loss */
-  int32_t dtype;          /* gw_dtype; only GW_F32 in this ABI version                 */
+  int32_t dtype;          /* gw_dtype: GW_F32, or GW_F64 (k = 1, 1-D)                   */
   uint32_t flags;         /* GW_NO_VALIDATE | GW_HOST_VECTORS | GW_GRID2D              */
 } gw_problem;
 
@@ -209,7 +215,7 @@ gw_status gw_check_shards(const int64_t *table, int nranks, int64_t n);
  * in O(n m) by the paper's dynamic programme
  * realised as row and column prefix scans with fp64 carries.  With a multi-rank ctx every rank
  * passes its own rows of T and receives its rows of G.
- * T: device fp32 (n_local x m, ldT); G: device fp32 output (ldG), may alias T
+ * T: device fp32 (n_local x m, ldT); G: device fp32 output (ldG), may alias T; both fp64 with GW_F64
  * (ldG == ldT).  c, c' use the PRESCRIBED p, q (reading R4).  mom (nullable): the
  * plan's row / column totals (gw_moments above).  Asynchronous. */
 gw_status gw_grad_dp(gw_ctx *ctx, const gw_problem *prob, const void *T, int64_t ldT,
@@ -218,14 +224,14 @@ gw_status gw_grad_dp(gw_ctx *ctx, const gw_problem *prob, const void *T, int64_t
 /* Log-domain Sinkhorn on cost G, never materialising
  * exp(-G/eps).  f (n_local) and g (m) are in/out fp64 duals (warm start; pass
  * zeros for a cold start).  T_out (nullable): the plan exp((f+g-G)/eps), fp32,
- * ldT.  info (host, nullable).  Iteration = f-update then g-update (reading R7). */
+ * ldT (G and T_out fp64 with GW_F64).  info (host, nullable).  Iteration = f-update then g-update (reading R7). */
 gw_status sinkhorn_solve(gw_ctx *ctx, const gw_problem *prob, const void *G, int64_t ldG,
                          const gw_sinkhorn_opts *opts, double *f, double *g,
                          void *T_out, int64_t ldT, gw_sinkhorn_info *info);
 
 /* Entropic GW by mirror descent (tau = eps unless opts->tau says otherwise).
  * T0: initial plan (device fp32, nullable -> p (x) q, reading R5); T_out: final plan
- * (nullable).  f, g: final duals (f has n_local entries, g has m).  res (host,
+ * (nullable); both fp64 with GW_F64.  f, g: final duals (f has n_local entries, g has m).  res (host,
  * required).  trace (host, nullable): [outer_iters x 4] doubles per outer l:
  * {E(T^l) (NaN unless GW_SOLVE_TRACE_OBJECTIVE), violation of T^l,
  *  Sinkhorn iterations used, milliseconds}.  The iteration counts let the oracle
@@ -241,8 +247,8 @@ gw_status entropic_gw_solve(gw_ctx *ctx, const gw_problem *prob, const gw_solve_
  *                      else exp((f + g - G^{l-1})/eps) materialised from the solver's duals), and
  *   G_out  (nullable): the solver's stored cost G^l = grad E(T^{l-1}) (FGW:
  *                      its cost) exactly as the Sinkhorn iterations consume it.
- * Both are this rank's n_local x m rows, fp32 row-major with leading dimension ld (ld % 4 == 0,
- * 16-byte aligned).  The request is taken by the next solve call whatever its outcome; a solve with
+ * Both are this rank's n_local x m rows, fp32 (fp64 when the solve's problem is GW_F64) row-major
+ * with leading dimension ld in elements (ld % 4 == 0, 16-byte aligned).  The request is taken by the next solve call whatever its outcome; a solve with
  * fewer outer iterations writes nothing.  Errors: GW_ERR_INVALID_ARG (null ctx, both buffers null,
  * bad ld / alignment), GW_ERR_CONFIG (outer_iter < 0).  Costs one extra N x M write each (debug only). */
 gw_status gw_solve_set_export(gw_ctx *ctx, int32_t outer_iter, void *T_prev, void *G_out, int64_t ld);

@@ -36,9 +36,15 @@ def plan_buffer(n, m, device=None, dtype=torch.float32):
     return buf[:, :m]
 
 
-def _check_mat(t, name):
-    if t.dtype != torch.float32 or not t.is_cuda or t.dim() != 2 or t.stride(1) != 1:
-        raise ValueError("%s must be a 2-D row-major float32 CUDA tensor" % name)
+_GW_DTYPE = {torch.float32: L.GW_F32, torch.float64: L.GW_F64}
+
+
+def _check_mat(t, name, dtype=None):
+    """Leading dimension of a 2-D row-major float32 / float64 (GW_F64) CUDA matrix; `dtype`: required type."""
+    if t.dtype not in _GW_DTYPE or not t.is_cuda or t.dim() != 2 or t.stride(1) != 1:
+        raise ValueError("%s must be a 2-D row-major float32 or float64 CUDA tensor" % name)
+    if dtype is not None and t.dtype != dtype:
+        raise ValueError("%s must be %s like the other matrices of the call" % (name, dtype))
     return t.stride(0)
 
 
@@ -79,7 +85,7 @@ class Context:
             self.h = None
 
 
-def _problem(x, y, p, q, n_local=None, row0=0, flags=0, k=1, grid2d=False):
+def _problem(x, y, p, q, n_local=None, row0=0, flags=0, k=1, grid2d=False, dtype=torch.float32):
     pr = L.gw_problem()
     if grid2d:  # x, y are the grid axes (GW_GRID2D): n = len(p) = len(x)^2
         if p.numel() != x.numel() ** 2 or q.numel() != y.numel() ** 2:
@@ -91,12 +97,13 @@ def _problem(x, y, p, q, n_local=None, row0=0, flags=0, k=1, grid2d=False):
     pr.row0 = row0
     pr.n_local = pr.n if n_local is None else n_local
     pr.x, pr.y, pr.p, pr.q = x.data_ptr(), y.data_ptr(), p.data_ptr(), q.data_ptr()
-    pr.k, pr.loss, pr.dtype, pr.flags = int(k), L.GW_LOSS_SQUARE, L.GW_F32, flags
+    pr.k, pr.loss, pr.dtype, pr.flags = int(k), L.GW_LOSS_SQUARE, _GW_DTYPE[dtype], flags
     return pr
 
 
 def grad(x, y, p, q, T, out=None, validate=True, ctx=None, row0=0, k=1, grid2d=False, moments=None):
-    """G = 2(c 1^T + 1 c'^T) - 4 D_X T D_Y  (gw_grad_dp), fp32.
+    """G = 2(c 1^T + 1 c'^T) - 4 D_X T D_Y  (gw_grad_dp), in T's dtype (float32, or
+    float64 = GW_F64 storage: k = 1 on 1-D supports).
     Sharded (ctx with a multi-rank comm): x, p are the full supports/marginals, T holds this
     rank's rows [row0, row0 + T.shape[0]) and the result holds the same rows of G.
     grid2d: x, y are the axes of 2-D grids with the Manhattan distance (GW_GRID2D).
@@ -108,9 +115,10 @@ def grad(x, y, p, q, T, out=None, validate=True, ctx=None, row0=0, k=1, grid2d=F
     ldT = _check_mat(T, "T")
     n, m = T.shape
     if out is None:
-        out = plan_buffer(n, m, dev)
-    ldG = _check_mat(out, "out")
-    pr = _problem(x, y, p, q, n_local=n, row0=row0, flags=0 if validate else L.GW_NO_VALIDATE, k=k, grid2d=grid2d)
+        out = plan_buffer(n, m, dev, T.dtype)
+    ldG = _check_mat(out, "out", T.dtype)
+    pr = _problem(x, y, p, q, n_local=n, row0=row0, flags=0 if validate else L.GW_NO_VALIDATE, k=k, grid2d=grid2d,
+                  dtype=T.dtype)
     mom = None
     if moments is not None:
         mv = [_vec(v, dev) for v in moments]
@@ -122,7 +130,7 @@ def grad(x, y, p, q, T, out=None, validate=True, ctx=None, row0=0, k=1, grid2d=F
 
 def sinkhorn(G, p, q, eps, max_iter, tol=0.0, check_every=10, f=None, g=None, return_plan=False, ctx=None):
     """Log-domain Sinkhorn on cost G (sinkhorn_solve).  Returns a dict with
-    f, g (fp64 CUDA), iters, converged, violation and optionally T."""
+    f, g (fp64 CUDA), iters, converged, violation and optionally T (G's dtype; float64 = GW_F64)."""
     ctx = ctx or Context.get(G.device)
     dev = G.device
     n, m = G.shape
@@ -133,8 +141,8 @@ def sinkhorn(G, p, q, eps, max_iter, tol=0.0, check_every=10, f=None, g=None, re
     ys = torch.arange(m, dtype=torch.float64, device=dev)
     f = torch.zeros(n, dtype=torch.float64, device=dev) if f is None else _vec(f, dev).clone()
     g = torch.zeros(m, dtype=torch.float64, device=dev) if g is None else _vec(g, dev).clone()
-    T = plan_buffer(n, m, dev) if return_plan else None
-    pr = _problem(xs, ys, p, q)
+    T = plan_buffer(n, m, dev, G.dtype) if return_plan else None
+    pr = _problem(xs, ys, p, q, dtype=G.dtype)
     o = L.gw_sinkhorn_opts(eps, int(max_iter), float(tol), int(check_every))
     info = L.gw_sinkhorn_info()
     L.check(ctx.lib.sinkhorn_solve(ctx.h, C.byref(pr), _ptr(G), ldG, C.byref(o), _ptr(f), _ptr(g), _ptr(T),
@@ -184,7 +192,7 @@ def _opts(eps, outer, inner, tol, check_every, trace_objective, tau=None):
 
 def solve(x, y, p, q, eps, outer, inner, tol=0.0, check_every=10, T0=None, return_plan=False,
           trace_objective=False, fx=None, fy=None, alpha=None, device=None, ctx=None, row0=0, n_local=None, k=1,
-          grid2d=False, tau=None, export_iter=0, export_T=None, export_G=None):
+          grid2d=False, tau=None, export_iter=0, export_T=None, export_G=None, dtype=torch.float32):
     """Entropic GW (entropic_gw_solve) or, with fx/fy/alpha, entropic FGW (fgw_solve), on
     device vectors; tau = eps.  Sharded (ctx with a multi-rank
     comm): x, p (and fx) are full; this rank owns rows [row0, row0 + n_local): f, T0 and the
@@ -194,7 +202,9 @@ def solve(x, y, p, q, eps, outer, inner, tol=0.0, check_every=10, T0=None, retur
     subproblem is entropic OT of grad E + (eps - tau) ln T^l at regulariser tau (k = 1, 1-D).
     export_iter / export_T / export_G (debug, gw_solve_set_export): at outer iteration export_iter
     (1-based) write the plan T^{l-1} the gradient is evaluated on and the solver's own G^l into
-    caller buffers (plan_buffer-shaped, same leading dimension)."""
+    caller buffers (plan_buffer-shaped, same leading dimension).
+    dtype: matrix storage, torch.float32 (default) or torch.float64 (GW_F64: T0, the returned plan and
+    the export buffers are float64; k = 1 on 1-D supports; taken from T0 when given)."""
     dev = torch.device(device) if device is not None else (T0.device if T0 is not None else torch.device("cuda"))
     if dev.index is None:
         dev = torch.device("cuda", torch.cuda.current_device())
@@ -203,24 +213,26 @@ def solve(x, y, p, q, eps, outer, inner, tol=0.0, check_every=10, T0=None, retur
     n, m = p.numel(), q.numel()
     if n_local is not None:
         n = int(n_local)
+    if T0 is not None:
+        dtype = T0.dtype
     f = torch.empty(n, dtype=torch.float64, device=dev)
     g = torch.empty(m, dtype=torch.float64, device=dev)
-    T = plan_buffer(n, m, dev) if return_plan else None
+    T = plan_buffer(n, m, dev, dtype) if return_plan else None
     ld = 0
     if T0 is not None:
         ld = _check_mat(T0, "T0")
         if T is not None and T.stride(0) != ld:
-            T = torch.empty((n, ld), dtype=torch.float32, device=dev)[:, :m]
+            T = torch.empty((n, ld), dtype=dtype, device=dev)[:, :m]
     elif T is not None:
         ld = T.stride(0)
-    pr = _problem(x, y, p, q, n_local=n, row0=row0, k=k, grid2d=grid2d)
+    pr = _problem(x, y, p, q, n_local=n, row0=row0, k=k, grid2d=grid2d, dtype=dtype)
     o = _opts(eps, outer, inner, tol, check_every, trace_objective, tau)
     res = L.gw_result()
     tr = np.zeros((max(int(outer), 1), 4), dtype=np.float64)
     trp = tr.ctypes.data_as(C.c_void_p)
     if export_iter:
         bufs = [b for b in (export_T, export_G) if b is not None]
-        eld = _check_mat(bufs[0], "export buffer") if bufs else 0
+        eld = _check_mat(bufs[0], "export buffer", dtype) if bufs else 0
         for b in bufs:
             if b.stride(0) != eld:
                 raise ValueError("export_T and export_G must share the leading dimension")
@@ -236,7 +248,7 @@ def solve(x, y, p, q, eps, outer, inner, tol=0.0, check_every=10, T0=None, retur
 
 
 def solve_host(x, y, p, q, eps, outer, inner, tol=0.0, check_every=10, device=None, ctx=None,
-               fx=None, fy=None, alpha=None, row0=0, n_local=None, k=1, grid2d=False, tau=None):
+               fx=None, fy=None, alpha=None, row0=0, n_local=None, k=1, grid2d=False, tau=None, dtype=torch.float32):
     """entropic_gw_solve with HOST vectors (GW_HOST_VECTORS): the library stages x, y, p, q
     host->device and copies the duals f, g back.  This is the end-to-end public call.
     Sharded: as solve() (f holds this rank's n_local rows)."""
@@ -251,7 +263,7 @@ def solve_host(x, y, p, q, eps, outer, inner, tol=0.0, check_every=10, device=No
     pr = L.gw_problem()
     pr.n, pr.m, pr.row0, pr.n_local = n, m, int(row0), nl
     pr.x, pr.y, pr.p, pr.q = (a.ctypes.data for a in (xs, ys, ps, qs))
-    pr.k, pr.loss, pr.dtype = int(k), L.GW_LOSS_SQUARE, L.GW_F32
+    pr.k, pr.loss, pr.dtype = int(k), L.GW_LOSS_SQUARE, _GW_DTYPE[dtype]
     pr.flags = L.GW_HOST_VECTORS | (L.GW_GRID2D if grid2d else 0)
     o = _opts(eps, outer, inner, tol, check_every, False, tau)
     res = L.gw_result()

@@ -1,0 +1,482 @@
+// fp64 matrix storage (GW_F64; C1 = configs[0] runs with fp64 matrices, reading
+// R28 as revised in round 2).  Every N x M matrix (T, G) is float64 and every step of the hot path
+// runs in fp64: the paper's dynamic programme for G = 2(c 1^T + 1 c'^T) - 4 D_X T D_Y
+// as a row scan (B = T D_Y) and a column scan (D_X B), and the
+// log-domain Sinkhorn updates with max-shifted fp64 LSEs.
+// k = 1 (|x - x'|) on 1-D supports.  This is the precision path (C1: parity ~1e-12 with the
+// float64 oracle), not the bandwidth path: the plan is kept explicit (one more N x M buffer), rows
+// are one warp each, columns one thread each over 64-row blocks, all loads coalesced.
+#pragma once
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace gw {
+
+constexpr int F64_RB = 64;  // rows per column block (column scans and column LSE partials)
+constexpr int F64_CH = 16;  // rows whose loads a column thread issues before consuming them
+
+// a marginal deviation for a max-reduction: NaN counts as +inf (fmax would drop it)
+__device__ __forceinline__ double dev64(double d) { return d == d ? fabs(d) : INFINITY; }
+
+// T^0 = p q^T (reading R5)
+__global__ void k64_product(const double* __restrict__ pl, const double* __restrict__ q, int64_t nl, int64_t m,
+                            double* __restrict__ T, int64_t ldT) {
+  for (int64_t i = blockIdx.x; i < nl; i += gridDim.x) {
+    const double pi = pl[i];
+    for (int64_t p = threadIdx.x; p < m; p += blockDim.x) T[i * ldT + p] = pi * q[p];
+  }
+}
+
+// T_ip = exp((f_i + g_p - G_ip) / eps): the Gibbs form of the subproblem's solution
+__global__ void k64_gibbs(const double* __restrict__ G, int64_t ldG, const double* __restrict__ f,
+                          const double* __restrict__ g, double eps, int64_t nl, int64_t m, double* __restrict__ T,
+                          int64_t ldT) {
+  for (int64_t i = blockIdx.x; i < nl; i += gridDim.x) {
+    const double fi = f[i];
+    for (int64_t p = threadIdx.x; p < m; p += blockDim.x) T[i * ldT + p] = exp((fi + g[p] - G[i * ldG + p]) / eps);
+  }
+}
+
+// Supplied moments (gw_moments): row totals in the centred y coordinates, Q_c = T y - ymid T 1.
+__global__ void k64_momrows(const double* __restrict__ rs, const double* __restrict__ rys, double ymid, int64_t nl,
+                            double* __restrict__ rin) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nl; i += (int64_t)gridDim.x * blockDim.x) {
+    rin[i] = rs[i];
+    rin[nl + i] = rys[i] - ymid * rs[i];
+  }
+}
+// ... and the column totals' sources for the 1-D DPs over y: T^T 1 and T^T x_c = T^T x - xmid T^T 1.
+__global__ void k64_momcols(const double* __restrict__ cs, const double* __restrict__ cxs, double xmid, int64_t m,
+                            double* __restrict__ v) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x) {
+    v[p] = cs[p];
+    v[m + p] = cxs[p] - xmid * cs[p];
+  }
+}
+
+// a2, the row direction (PAPER.md:194-243 at k = 1): B = T D_Y row by row,
+//   B_ip = sum_q |y_p - y_q| T_iq = 2 (y_p P_<p - Q_<p) + Q_tot - y_p P_tot,
+//   P_<p = sum_{q<p} T_iq,  Q_<p = sum_{q<p} y_q T_iq  (fp64 warp scans with a running carry).
+// One warp per row.  B may alias T (each lane reads its element before writing it).  rin (nullable):
+// supplied totals [P_tot | Q_tot]; rtot (out): [P_tot | Q_tot] of every row.
+__global__ void k64_row(const double* T, int64_t ldT, int64_t nl, int64_t m, const double* __restrict__ yc,
+                        const double* __restrict__ rin, double* B, int64_t ldB, double* __restrict__ rtot) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (i >= nl) return;
+  const double* t = T + i * ldT;
+  double* b = B + i * ldB;
+  double Pt, Qt;
+  if (rin) {
+    Pt = rin[i];
+    Qt = rin[nl + i];
+  } else {
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll 4
+    for (int64_t p = lane; p < m; p += 32) {
+      const double v = t[p];
+      s0 += v;
+      s1 += yc[p] * v;
+    }
+    Pt = warp_sum(s0);
+    Qt = warp_sum(s1);
+  }
+  double cP = 0.0, cQ = 0.0;
+  constexpr int U = 4;  // chunks of 32 columns loaded ahead of the (serial) scans
+  for (int64_t p0 = 0; p0 < m; p0 += 32 * U) {
+    double v[U], yv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t p = p0 + 32 * u + lane;
+      v[u] = p < m ? t[p] : 0.0;
+      yv[u] = p < m ? yc[p] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t p = p0 + 32 * u + lane;
+      double a = v[u], c = yv[u] * v[u];  // inclusive warp scans
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const double oa = __shfl_up_sync(0xffffffffu, a, d), oc = __shfl_up_sync(0xffffffffu, c, d);
+        if (lane >= d) {
+          a += oa;
+          c += oc;
+        }
+      }
+      double ae = __shfl_up_sync(0xffffffffu, a, 1), ce = __shfl_up_sync(0xffffffffu, c, 1);
+      if (lane == 0) ae = ce = 0.0;
+      if (p < m) b[p] = 2.0 * (yv[u] * (cP + ae) - (cQ + ce)) + Qt - yv[u] * Pt;
+      cP += __shfl_sync(0xffffffffu, a, 31);
+      cQ += __shfl_sync(0xffffffffu, c, 31);
+    }
+  }
+  if (lane == 0) {
+    rtot[i] = Pt;
+    rtot[nl + i] = Qt;
+  }
+}
+
+// a3, the column direction: per 64-row block and column, S = sum_j B_jp and
+// U = sum_j x_j B_jp over the block's rows.  part: [nb][2][m].
+__global__ void k64_colpart(const double* __restrict__ B, int64_t ldB, int64_t nl, int64_t m,
+                            const double* __restrict__ xl, double* __restrict__ part) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t blk = blockIdx.y;
+  if (p >= m) return;
+  const int64_t i0 = blk * F64_RB, i1 = min(nl, i0 + F64_RB);
+  double S = 0.0, U = 0.0;
+  for (int64_t c0 = i0; c0 < i1; c0 += F64_CH) {  // F64_CH loads in flight per thread
+    double b[F64_CH];
+#pragma unroll
+    for (int u = 0; u < F64_CH; ++u) b[u] = c0 + u < i1 ? B[(c0 + u) * ldB + p] : 0.0;
+#pragma unroll
+    for (int u = 0; u < F64_CH; ++u) {
+      S += b[u];
+      if (c0 + u < i1) U += xl[c0 + u] * b[u];
+    }
+  }
+  part[(2 * blk) * m + p] = S;
+  part[(2 * blk + 1) * m + p] = U;
+}
+
+// Exclusive prefix of the block partials over blocks (in place, block order); tot = this rank's totals.
+__global__ void k64_colscan(double* __restrict__ part, int nb, int64_t m, double* __restrict__ tot) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= m) return;
+  double S = 0.0, U = 0.0;
+  for (int k = 0; k < nb; ++k) {
+    const double s = part[(2 * (int64_t)k) * m + p], u = part[(2 * (int64_t)k + 1) * m + p];
+    part[(2 * (int64_t)k) * m + p] = S;
+    part[(2 * (int64_t)k + 1) * m + p] = U;
+    S += s;
+    U += u;
+  }
+  tot[p] = S;
+  tot[m + p] = U;
+}
+
+// Row shards: off = sum of the ranks before this one, glob = sum over all ranks (rank order).
+// gath: [R][2][m]; glob_set: the global totals were supplied (gw_moments): only off is written.
+__global__ void k64_rankoff(const double* __restrict__ gath, int R, int rank, int64_t m, double* __restrict__ off,
+                            double* __restrict__ glob, bool glob_set) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= 2 * m) return;
+  double o = 0.0, t = 0.0;
+  for (int r = 0; r < R; ++r) {
+    const double v = gath[(int64_t)r * 2 * m + e];
+    if (r < rank) o += v;
+    t += v;
+  }
+  off[e] = o;
+  if (!glob_set) glob[e] = t;
+}
+
+// a3 + a4: (D_X B)_ip = 2 (x_i S_<i - U_<i) + U_tot - x_i S_tot (S, U column prefixes of B and x B,
+// PAPER.md:211-219), then G_ip = 2 (c_i + c'_p) - 4 (D_X T D_Y)_ip or, with the
+// feature cost (Remark 2), (1 - alpha) C_ip^2 + alpha (2 (c_i + c'_p) - 4 (D_X T D_Y)_ip).
+// G holds B on entry and is overwritten in place.  OBJ: per (block, column) partials of
+// sum T (D_X T D_Y), sum T, sum T (ln T - 1), sum T C^2 into obj [nb][4][m] (T explicit, not aliased).
+template <bool OBJ, bool FGW>
+__global__ void k64_colapply(double* G, int64_t ldG, const double* __restrict__ T, int64_t ldT, int64_t nl,
+                             int64_t m, const double* __restrict__ xl, const double* __restrict__ part,
+                             const double* __restrict__ off, const double* __restrict__ glob,
+                             const double* __restrict__ cl, const double* __restrict__ c2,
+                             const double* __restrict__ fxl, const double* __restrict__ fy, double alpha,
+                             double* __restrict__ obj) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t blk = blockIdx.y;
+  if (p >= m) return;
+  const int64_t i0 = blk * F64_RB, i1 = min(nl, i0 + F64_RB);
+  double S = off[p] + part[(2 * blk) * m + p], U = off[m + p] + part[(2 * blk + 1) * m + p];
+  const double St = glob[p], Ut = glob[m + p], cp = c2[p];
+  const double fyp = FGW ? fy[p] : 0.0;
+  double o0 = 0.0, o1 = 0.0, o2 = 0.0, o3 = 0.0;
+  for (int64_t c0 = i0; c0 < i1; c0 += F64_CH) {
+  double bv[F64_CH], tv[F64_CH];
+#pragma unroll
+  for (int u = 0; u < F64_CH; ++u) {
+    bv[u] = c0 + u < i1 ? G[(c0 + u) * ldG + p] : 0.0;
+    if (OBJ) tv[u] = c0 + u < i1 ? T[(c0 + u) * ldT + p] : 0.0;
+  }
+#pragma unroll
+  for (int u = 0; u < F64_CH; ++u) {
+    const int64_t i = c0 + u;
+    if (i >= i1) break;
+    const double x = xl[i];
+    double* gp = G + i * ldG + p;
+    const double b = bv[u];
+    const double db = 2.0 * (x * S - U) + Ut - x * St;
+    S += b;
+    U += x * b;
+    double gv = 2.0 * (cl[i] + cp) - 4.0 * db;
+    double cc = 0.0;
+    if (FGW) {
+      const double d = fxl[i] - fyp;
+      cc = d * d;
+      gv = (1.0 - alpha) * cc + alpha * gv;
+    }
+    *gp = gv;
+    if (OBJ) {
+      const double t = tv[u];
+      o0 += t * db;
+      o1 += t;
+      if (t > 0.0) o2 += t * (log(t) - 1.0);
+      o3 += t * cc;
+    }
+  }
+  }
+  if (OBJ) {
+    obj[(4 * blk + 0) * m + p] = o0;
+    obj[(4 * blk + 1) * m + p] = o1;
+    obj[(4 * blk + 2) * m + p] = o2;
+    obj[(4 * blk + 3) * m + p] = o3;
+  }
+}
+
+// Objective pieces, step 1: per column, the block partials summed in block order.
+// pay[p] = (T^T 1)_p over this rank's rows; tmp[k][p] (k = 0, 1, 2) = the column's sums of
+// T (D_X T D_Y), T (ln T - 1), T C^2.
+__global__ void k64_objcols(const double* __restrict__ obj, int nb, int64_t m, double* __restrict__ pay,
+                            double* __restrict__ tmp) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= m) return;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  for (int k = 0; k < nb; ++k) {
+    s0 += obj[(4 * (int64_t)k + 0) * m + p];
+    s1 += obj[(4 * (int64_t)k + 1) * m + p];
+    s2 += obj[(4 * (int64_t)k + 2) * m + p];
+    s3 += obj[(4 * (int64_t)k + 3) * m + p];
+  }
+  pay[p] = s1;
+  tmp[p] = s0;
+  tmp[m + p] = s2;
+  tmp[2 * m + p] = s3;
+}
+
+__device__ __forceinline__ double bsum1024(double v, double* sm) { return block_sum<32, double>(v, sm); }
+__device__ __forceinline__ double bmax1024(double v, double* sm) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  v = warp_max(v);
+  if (lane == 0) sm[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (w == 0) {
+    t = warp_max(sm[lane]);
+    if (lane == 0) sm[0] = t;
+  }
+  __syncthreads();
+  t = sm[0];
+  __syncthreads();
+  return t;
+}
+
+// Objective pieces, step 2 (one CTA of 1024): this rank's scalars into pay[m .. m + 8):
+//   {sum T DTD, sum T (ln T - 1), sum T C^2, A0, A1, A2, max_i |a_i - p_i|, 0}
+// with a = T 1 (the row pass's P_tot) and A_k = sum_i a_i x_i^k (centred x).
+__global__ void k64_objlocal(const double* __restrict__ tmp, int64_t m, const double* __restrict__ a,
+                             const double* __restrict__ xl, const double* __restrict__ pl, int64_t nl,
+                             double* __restrict__ pay) {
+  __shared__ double sm[32];
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  for (int64_t p = threadIdx.x; p < m; p += blockDim.x) {
+    s0 += tmp[p];
+    s1 += tmp[m + p];
+    s2 += tmp[2 * m + p];
+  }
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, dv = 0.0;
+  for (int64_t i = threadIdx.x; i < nl; i += blockDim.x) {
+    const double v = a[i], x = xl[i];
+    a0 += v;
+    a1 += v * x;
+    a2 += v * x * x;
+    dv = fmax(dv, dev64(v - pl[i]));
+  }
+  s0 = bsum1024(s0, sm); s1 = bsum1024(s1, sm); s2 = bsum1024(s2, sm);
+  a0 = bsum1024(a0, sm); a1 = bsum1024(a1, sm); a2 = bsum1024(a2, sm);
+  dv = bmax1024(dv, sm);
+  if (threadIdx.x == 0) {
+    double* o = pay + m;
+    o[0] = s0; o[1] = s1; o[2] = s2; o[3] = a0; o[4] = a1; o[5] = a2; o[6] = dv; o[7] = 0.0;
+  }
+}
+
+// Objective pieces, step 3 (one CTA of 1024): the ranks' payloads [R][m + 8] combined in rank order;
+//   E(T) = a (D_X o D_X) a + b (D_Y o D_Y) b - 2 <D_X T D_Y, T>
+// with sum_ij (x_i - x_j)^2 a_i a_j = 2 (A0 A2 - A1^2) (likewise b over y), b = T^T 1.
+// out: [0] E, [1] max(|T1 - p|, |T^T 1 - q|), [3] H = sum T (ln T - 1), [6] sum T C^2 (FGW).
+__global__ void k64_objglobal(const double* __restrict__ gath, int R, int64_t m, const double* __restrict__ yc,
+                              const double* __restrict__ qn, double* __restrict__ out) {
+  __shared__ double sm[32];
+  const int64_t st = m + 8;
+  double b0 = 0.0, b1 = 0.0, b2 = 0.0, dv = 0.0;
+  for (int64_t p = threadIdx.x; p < m; p += blockDim.x) {
+    double b = 0.0;
+    for (int r = 0; r < R; ++r) b += gath[r * st + p];
+    const double y = yc[p];
+    b0 += b;
+    b1 += b * y;
+    b2 += b * y * y;
+    dv = fmax(dv, dev64(b - qn[p]));
+  }
+  b0 = bsum1024(b0, sm); b1 = bsum1024(b1, sm); b2 = bsum1024(b2, sm);
+  dv = bmax1024(dv, sm);
+  if (threadIdx.x == 0) {
+    double s[7] = {0, 0, 0, 0, 0, 0, 0};
+    for (int r = 0; r < R; ++r) {
+      const double* o = gath + r * st + m;
+      for (int k = 0; k < 6; ++k) s[k] += o[k];
+      s[6] = fmax(s[6], o[6]);
+    }
+    const double Ea = 2.0 * (s[3] * s[5] - s[4] * s[4]);
+    const double Eb = 2.0 * (b0 * b2 - b1 * b1);
+    out[0] = Ea + Eb - 2.0 * s[0];
+    out[1] = fmax(s[6], dv);
+    out[2] = 0.0;
+    out[3] = s[1];
+    out[4] = out[5] = 0.0;
+    out[6] = s[2];
+    out[7] = 0.0;
+  }
+}
+
+// ---- Sinkhorn, max-shifted log-sum-exp in fp64 ----------------
+struct L64 {
+  double m, s;  // max and sum of 2^(v - m), v in log2 units
+};
+__device__ __forceinline__ L64 l64_merge(L64 a, L64 b) {
+  const double mx = fmax(a.m, b.m);
+  if (mx == -INFINITY) return L64{-INFINITY, 0.0};
+  return L64{mx, a.s * exp2(a.m - mx) + b.s * exp2(b.m - mx)};
+}
+
+// F values at once: one max, one rescale of the running sum, F exponentials
+template <int F>
+__device__ __forceinline__ void l64_chunk(L64& a, const double (&v)[F]) {
+  double mx = v[0];
+#pragma unroll
+  for (int u = 1; u < F; ++u) mx = fmax(mx, v[u]);
+  if (mx == -INFINITY) return;
+  if (mx > a.m) {
+    a.s *= exp2(a.m - mx);  // a.m = -inf: 0
+    a.m = mx;
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int u = 0; u < F; ++u) s += exp2(v[u] - a.m);
+  a.s += s;
+}
+
+// The exponents are formed as (f_i + g_p - G_ip) * c2, c2 = log2(e) / eps (no fp64 division per element;
+// 2^x instead of e^x), LSE = ln 2 (m + log2 s): within ~|v| ulp of the oracle's (.)/eps and exp.
+// Rows, one warp each: LSE_p of v_p = (f_i + g_p - G_ip) / eps.
+//   mode 0 (a5, f-update): f_i = eps ln p_i - eps LSE_p((g_p - G_ip) / eps)
+//   mode 1 (violation):    dev_i = |sum_p T_ip - p_i| with T = exp((f + g - G) / eps)
+__global__ void k64_rowlse(const double* __restrict__ G, int64_t ldG, int64_t nl, int64_t m,
+                           const double* __restrict__ g, double eps, double* __restrict__ f,
+                           const double* __restrict__ lpl, const double* __restrict__ pl, int mode,
+                           double* __restrict__ dev) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (i >= nl) return;
+  const double fi = mode == 1 ? f[i] : 0.0;
+  const double c2 = GW_LOG2E / eps;
+  const double* Gi = G + i * ldG;
+  L64 a{-INFINITY, 0.0};
+  constexpr int U = 4;  // 4 coalesced warp loads in flight
+  for (int64_t p0 = lane; p0 < m; p0 += 32 * U) {
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t p = p0 + 32 * u;
+      v[u] = p < m ? Gi[p] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t p = p0 + 32 * u;
+      v[u] = p < m ? (fi + g[p] - v[u]) * c2 : -INFINITY;
+    }
+    l64_chunk<U>(a, v);
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    L64 o{__shfl_xor_sync(0xffffffffu, a.m, d), __shfl_xor_sync(0xffffffffu, a.s, d)};
+    a = l64_merge(a, o);
+  }
+  if (lane == 0) {
+    const double lse = (a.m + log2(a.s)) * GW_LN2;
+    if (mode == 0) f[i] = eps * lpl[i] - eps * lse;
+    else dev[i] = dev64(exp(lse) - pl[i]);
+  }
+}
+
+// Columns: per (column, 64-row block) LSE pair of v_i = (f_i + g_p - G_ip) / eps (g nullable: 0).
+__global__ void k64_colpart_lse(const double* __restrict__ G, int64_t ldG, int64_t nl, int64_t m,
+                                const double* __restrict__ f, const double* __restrict__ g, double eps,
+                                double2* __restrict__ part) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t blk = blockIdx.y;
+  if (p >= m) return;
+  const int64_t i0 = blk * F64_RB, i1 = min(nl, i0 + F64_RB);
+  const double gp = g ? g[p] : 0.0;
+  const double c2 = GW_LOG2E / eps;
+  L64 a{-INFINITY, 0.0};
+  for (int64_t c0 = i0; c0 < i1; c0 += F64_CH) {
+    double v[F64_CH];
+#pragma unroll
+    for (int u = 0; u < F64_CH; ++u) v[u] = c0 + u < i1 ? G[(c0 + u) * ldG + p] : 0.0;
+#pragma unroll
+    for (int u = 0; u < F64_CH; ++u) v[u] = c0 + u < i1 ? (f[c0 + u] + gp - v[u]) * c2 : -INFINITY;
+    l64_chunk<F64_CH>(a, v);
+  }
+  part[blk * m + p] = make_double2(a.m, a.s);
+}
+// The blocks' pairs merged in block order: pay[p] = max, pay[m + p] = sum (this rank's rows).
+__global__ void k64_colcomb(const double2* __restrict__ part, int nb, int64_t m, double* __restrict__ pay) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= m) return;
+  L64 a{-INFINITY, 0.0};
+  for (int k = 0; k < nb; ++k) {
+    const double2 v = part[(int64_t)k * m + p];
+    a = l64_merge(a, L64{v.x, v.y});
+  }
+  pay[p] = a.m;
+  pay[m + p] = a.s;
+}
+// The ranks' pairs [R][stride] merged in rank order.
+//   mode 0 (a6, g-update): g_p = eps ln q_p - eps LSE_i((f_i - G_ip) / eps)
+//   mode 1 (violation):    dev_p = |sum_i T_ip - q_p|
+__global__ void k64_colfinal(const double* __restrict__ gath, int R, int64_t stride, int64_t m, double eps,
+                             const double* __restrict__ lq, const double* __restrict__ qn, double* __restrict__ g,
+                             int mode, double* __restrict__ dev) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= m) return;
+  L64 a{-INFINITY, 0.0};
+  for (int r = 0; r < R; ++r) a = l64_merge(a, L64{gath[r * stride + p], gath[r * stride + m + p]});
+  const double lse = (a.m + log2(a.s)) * GW_LN2;
+  if (mode == 0) g[p] = eps * lq[p] - eps * lse;
+  else dev[p] = dev64(exp(lse) - qn[p]);
+}
+
+// max of v[0 .. n) into *out (one CTA of 1024)
+__global__ void k64_max(const double* __restrict__ v, int64_t n, double* __restrict__ out) {
+  __shared__ double sm[32];
+  double d = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) d = fmax(d, v[i]);
+  d = bmax1024(d, sm);
+  if (threadIdx.x == 0) *out = d;
+}
+// violation = max(column deviations, every rank's row maximum gath[r * stride + 2m]) (one CTA of 1024)
+__global__ void k64_viol(const double* __restrict__ coldev, int64_t m, const double* __restrict__ gath, int R,
+                         int64_t stride, double* __restrict__ out) {
+  __shared__ double sm[32];
+  double d = 0.0;
+  for (int64_t p = threadIdx.x; p < m; p += blockDim.x) d = fmax(d, coldev[p]);
+  d = bmax1024(d, sm);
+  if (threadIdx.x == 0) {
+    for (int r = 0; r < R; ++r) d = fmax(d, gath[r * stride + 2 * m]);
+    *out = d;
+  }
+}
+
+}  // namespace gw

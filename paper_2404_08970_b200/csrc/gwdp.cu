@@ -27,6 +27,7 @@
 #include "small.cuh"
 #include "sink.cuh"
 #include "vec.cuh"
+#include "f64.cuh"
 
 using namespace gw;
 
@@ -126,6 +127,8 @@ struct gw_ctx {
   Buf fsc, gsc;  // scaled duals for the Gibbs regeneration
   Buf Gs;        // solver cost buffer
   Buf rcp, rcpx, rcv, rcvx, rcu, rcz, rcxf, rccx, rccy, rcflag, rcdx;  // 8 N M solver gradient (rowclu.cuh)
+  Buf d64T, d64G, d64rt, d64part, d64tot, d64gath, d64obj, d64tmp, d64pay, d64pg, d64mc;  // GW_F64 (f64.cuh)
+  Buf s64pay, s64gath, s64part, s64rdev, s64cdev;                                      // GW_F64 Sinkhorn
   double* hpin = nullptr;  // pinned host scratch (64 doubles)
   // one-shot debug export for the next solve (gw_solve_set_export)
   struct {
@@ -142,7 +145,9 @@ struct gw_ctx {
                 &gkrp, &gkrt, &gkcp, &gkz, &gkct, &gkctt, &gkobj, &gkseg,
                 &uga, &ugb, &ugct, &ugpart, &ugca, &ugcb, &ugfr, &uggr, &ugsc, &ugrpart,
                 &g2rc, &g2rd, &g2h, &g2cc, &g2tt, &g2vt, &g2tmp, &g2s, &g2a, &g2b, &g2ca, &g2cb, &g2part,
-                &rcp, &rcpx, &rcv, &rcvx, &rcu, &rcz, &rcxf, &rccx, &rccy, &rcflag, &rcdx};
+                &rcp, &rcpx, &rcv, &rcvx, &rcu, &rcz, &rcxf, &rccx, &rccy, &rcflag, &rcdx,
+                &d64T, &d64G, &d64rt, &d64part, &d64tot, &d64gath, &d64obj, &d64tmp, &d64pay, &d64pg, &d64mc,
+                &s64pay, &s64gath, &s64part, &s64rdev, &s64cdev};
     for (Buf* x : b) all.push_back(x);
   }
 };
@@ -430,7 +435,9 @@ static gw_status check_problem(const gw_problem* pb) {
     if (pb->k != 1) return fail(GW_ERR_UNSUPPORTED, "GW_GRID2D: only k = 1 (Manhattan distance) is implemented");
   }
   if (pb->loss != GW_LOSS_SQUARE) return fail(GW_ERR_UNSUPPORTED, "only the square loss is defined (PAPER.md:86)");
-  if (pb->dtype != GW_F32) return fail(GW_ERR_UNSUPPORTED, "only fp32 matrix storage in ABI v1");
+  if (pb->dtype != GW_F32 && pb->dtype != GW_F64) return fail(GW_ERR_INVALID_ARG, "dtype %d is not a gw_dtype", pb->dtype);
+  if (pb->dtype == GW_F64 && (pb->k != 1 || (pb->flags & GW_GRID2D)))
+    return fail(GW_ERR_UNSUPPORTED, "GW_F64 storage: k = 1 on 1-D supports (f64.cuh)");
   return GW_OK;
 }
 
@@ -1249,6 +1256,188 @@ static gw_status grad_pass(gw_ctx* c, const Prepared& P, int mode, const TSrc& S
   return GW_OK;
 }
 
+// ------------------------------------------------------------------------------ fp64 storage (GW_F64)
+// f64.cuh: the same gradient and Sinkhorn steps with float64 matrices (C1 = configs[0]).  Multi-rank:
+// the column prefixes / totals and the column LSE pairs are all-gathered and combined in rank order
+// (as shard.cuh does for the fp32 path), so one and several ranks agree up to summation order.
+
+// G = 2(c 1^T + 1 c'^T) - 4 D_X T D_Y (alpha, fx, fy: the FGW cost, Remark 2) for this rank's rows.
+// G may alias T unless obj.  obj: objout (device, 8 doubles) = {E, violation, -, H, -, -, sum T C^2, -}
+// of the plan T (over all ranks).  mom (nullable): supplied totals (gw_moments).
+static gw_status grad64(gw_ctx* c, const Prepared& P, const double* T, int64_t ldT, double* G, int64_t ldG, bool obj,
+                        const double* fx, const double* fy, double alpha, const gw_moments* mom, double* objout) {
+  const int64_t nl = P.nl, m = P.m;
+  const int R = P.R;
+  if (nl == 0) return GW_OK;  // single rank only: prepare() rejects empty shards when R > 1
+  const int64_t nb = (nl + F64_RB - 1) / F64_RB;
+  if (nb > 65535) return fail(GW_ERR_UNSUPPORTED, "GW_F64: at most %lld rows per rank", (long long)65535 * F64_RB);
+  double *rtot, *part, *tot, *gath;
+  TRY(ws(c, c->d64rt, 4 * (size_t)nl, &rtot));
+  TRY(ws(c, c->d64part, (size_t)nb * 2 * m, &part));
+  TRY(ws(c, c->d64tot, 6 * (size_t)m, &tot));
+  TRY(ws(c, c->d64gath, (size_t)R * 2 * m, &gath));
+  double* rin = rtot + 2 * nl;
+  double* off = tot + 2 * m;
+  double* glob = tot + 4 * m;
+  const double* xl = P.xc + P.row0;
+  NvtxRange nv("gw.grad64");
+  PROF_BEGIN(c, PC_GRAD_MAIN);
+  if (mom) {
+    k64_momrows<<<grid_for(nl), 256, 0, c->stream>>>(mom->row_sum, mom->row_ysum, P.yend_u - P.ylast, nl, rin);
+    KCHECK();
+  }
+  // a2: B = T D_Y into G (one warp per row)
+  k64_row<<<(unsigned)((nl * 32 + 255) / 256), 256, 0, c->stream>>>(T, ldT, nl, m, P.yc, mom ? rin : nullptr, G, ldG,
+                                                                     rtot);
+  KCHECK();
+  // a3: column block partials of B and x B, their exclusive prefix, the ranks' offsets and totals
+  const dim3 cg((unsigned)((m + 127) / 128), (unsigned)nb);
+  k64_colpart<<<cg, 128, 0, c->stream>>>(G, ldG, nl, m, xl, part);
+  KCHECK();
+  k64_colscan<<<(unsigned)((m + 255) / 256), 256, 0, c->stream>>>(part, (int)nb, m, tot);
+  KCHECK();
+  TRY(comm_allgather(c, tot, gath, 2 * (size_t)m * sizeof(double)));
+  if (mom) {  // column totals of B = T D_Y from the supplied T^T 1, T^T x by 1-D DPs over y
+    double* v;
+    TRY(ws(c, c->d64mc, 2 * (size_t)m, &v));
+    k64_momcols<<<grid_for(m), 256, 0, c->stream>>>(mom->col_sum, mom->col_xsum, P.xend_u - P.xlast, m, v);
+    KCHECK();
+    Scan1DBatch B;
+    memset(&B, 0, sizeof(B));
+    B.d[0] = Scan1D{v, P.yc, m, nullptr, glob, nullptr};
+    B.d[1] = Scan1D{v + m, P.yc, m, nullptr, glob + m, nullptr};
+    const int K = (int)std::min<int64_t>(SCAN_KMAX, std::max<int64_t>(1, (m + 4095) / 4096));
+    double* wt;
+    TRY(ws(c, c->scanwt, (size_t)4 * K * 32 * 3, &wt));
+    k_scan1d_tot<<<dim3(K, 2), 1024, 0, c->stream>>>(B, K, wt);
+    KCHECK();
+    k_scan1d_out<<<dim3(K, 2), 1024, 0, c->stream>>>(B, K, wt);
+    KCHECK();
+  }
+  k64_rankoff<<<(unsigned)((2 * m + 255) / 256), 256, 0, c->stream>>>(gath, R, P.rank, m, off, glob, mom != nullptr);
+  KCHECK();
+  // a3 + a4: D_X B by the column scan, assembled into G in place
+  double* ob = nullptr;
+  if (obj) TRY(ws(c, c->d64obj, (size_t)nb * 4 * m, &ob));
+  const double* fxl = fx ? fx + P.row0 : nullptr;
+#define K64_APPLY(O, F)                                                                                        \
+  k64_colapply<O, F><<<cg, 128, 0, c->stream>>>(G, ldG, T, ldT, nl, m, xl, part, off, glob, P.cx + P.row0, P.cy, \
+                                                 fxl, fy, alpha, ob)
+  if (obj) {
+    if (fx) K64_APPLY(true, true); else K64_APPLY(true, false);
+  } else {
+    if (fx) K64_APPLY(false, true); else K64_APPLY(false, false);
+  }
+#undef K64_APPLY
+  KCHECK();
+  PROF_END(c, PC_GRAD_MAIN, 5);
+  if (obj) {  // a8: E(T), violation, H, sum T C^2
+    double *tmp, *pay, *pg;
+    const int64_t st = m + 8;
+    TRY(ws(c, c->d64tmp, 3 * (size_t)m, &tmp));
+    TRY(ws(c, c->d64pay, (size_t)st, &pay));
+    TRY(ws(c, c->d64pg, (size_t)R * st, &pg));
+    k64_objcols<<<(unsigned)((m + 255) / 256), 256, 0, c->stream>>>(ob, (int)nb, m, pay, tmp);
+    KCHECK();
+    k64_objlocal<<<1, 1024, 0, c->stream>>>(tmp, m, rtot, xl, P.pn + P.row0, nl, pay);
+    KCHECK();
+    TRY(comm_allgather(c, pay, pg, (size_t)st * sizeof(double)));
+    k64_objglobal<<<1, 1024, 0, c->stream>>>(pg, R, m, P.yc, P.qn, objout);
+    KCHECK();
+  }
+  return GW_OK;
+}
+
+// fp64 Sinkhorn state: the column exchange payload {max[m], sum[m], row deviation, pad} per rank.
+struct Sink64 {
+  double *pay, *gath, *rdev, *cdev, *vout;
+  double2* part;
+  int64_t stride = 0, nb = 0;
+};
+static gw_status sink64_alloc(gw_ctx* c, const Prepared& P, Sink64& s) {
+  s.stride = 2 * P.m + 2;
+  s.nb = (std::max<int64_t>(P.nl, 1) + F64_RB - 1) / F64_RB;
+  if (s.nb > 65535) return fail(GW_ERR_UNSUPPORTED, "GW_F64: at most %lld rows per rank", (long long)65535 * F64_RB);
+  TRY(ws(c, c->s64pay, (size_t)s.stride + 2, &s.pay));
+  s.vout = s.pay + s.stride;
+  TRY(ws(c, c->s64gath, (size_t)P.R * s.stride, &s.gath));
+  TRY(ws(c, c->s64part, (size_t)s.nb * P.m, &s.part));
+  TRY(ws(c, c->s64rdev, (size_t)std::max<int64_t>(P.nl, 1), &s.rdev));
+  TRY(ws(c, c->s64cdev, (size_t)P.m, &s.cdev));
+  return GW_OK;
+}
+// column LSE pairs of (f_i + g_p - G_ip)/eps over this rank's rows, all-gathered (g nullable: 0)
+static gw_status sink64_cols(gw_ctx* c, const Prepared& P, Sink64& s, const double* G, int64_t ldG, const double* f,
+                             const double* g, double eps) {
+  const int64_t m = P.m;
+  k64_colpart_lse<<<dim3((unsigned)((m + 127) / 128), (unsigned)s.nb), 128, 0, c->stream>>>(G, ldG, P.nl, m, f, g,
+                                                                                          eps, s.part);
+  KCHECK();
+  k64_colcomb<<<(unsigned)((m + 255) / 256), 256, 0, c->stream>>>(s.part, (int)s.nb, m, s.pay);
+  KCHECK();
+  TRY(comm_allgather(c, s.pay, s.gath, (size_t)s.stride * sizeof(double)));
+  return GW_OK;
+}
+// one iteration: f-update (a5) then g-update (a6), reading R7
+static gw_status sink64_iter(gw_ctx* c, const Prepared& P, Sink64& s, const double* G, int64_t ldG, double* f,
+                             double* g, double eps) {
+  const int64_t nl = P.nl, m = P.m;
+  k64_rowlse<<<(unsigned)((nl * 32 + 255) / 256), 256, 0, c->stream>>>(G, ldG, nl, m, g, eps, f, P.lp + P.row0,
+                                                                       P.pn + P.row0, 0, nullptr);
+  KCHECK();
+  TRY(sink64_cols(c, P, s, G, ldG, f, nullptr, eps));
+  k64_colfinal<<<(unsigned)((m + 255) / 256), 256, 0, c->stream>>>(s.gath, P.R, s.stride, m, eps, P.lq, P.qn, g, 0,
+                                                                   nullptr);
+  KCHECK();
+  return GW_OK;
+}
+// violation max(|T1 - p|, |T^T 1 - q|) of the plan (f, g) into s.vout (device); host != null: read back
+static gw_status sink64_viol(gw_ctx* c, const Prepared& P, Sink64& s, const double* G, int64_t ldG, const double* f,
+                             const double* g, double eps, double* host) {
+  const int64_t nl = P.nl, m = P.m;
+  k64_rowlse<<<(unsigned)((nl * 32 + 255) / 256), 256, 0, c->stream>>>(G, ldG, nl, m, g, eps, const_cast<double*>(f),
+                                                                       nullptr, P.pn + P.row0, 1, s.rdev);
+  KCHECK();
+  k64_max<<<1, 1024, 0, c->stream>>>(s.rdev, nl, s.pay + 2 * m);
+  KCHECK();
+  TRY(sink64_cols(c, P, s, G, ldG, f, g, eps));
+  k64_colfinal<<<(unsigned)((m + 255) / 256), 256, 0, c->stream>>>(s.gath, P.R, s.stride, m, eps, P.lq, P.qn, nullptr,
+                                                                   1, s.cdev);
+  KCHECK();
+  k64_viol<<<1, 1024, 0, c->stream>>>(s.cdev, m, s.gath, P.R, s.stride, s.vout);
+  KCHECK();
+  if (host) {
+    CU(cudaMemcpyAsync(c->hpin + 56, s.vout, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    *host = c->hpin[56];
+  }
+  return GW_OK;
+}
+// `iters` iterations; tol > 0: the plan's violation checked every check_every iterations, stop when
+// <= tol (reading R8; the oracle's schedule exactly)
+static gw_status sink64_run(gw_ctx* c, const Prepared& P, Sink64& s, const double* G, int64_t ldG, double* f,
+                            double* g, double eps, int iters, double tol, int check_every, int* used, int* conv) {
+  NvtxRange nv("gw.sinkhorn64");
+  *used = 0;
+  *conv = 0;
+  if (check_every < 1) check_every = 10;
+  for (int it = 1; it <= iters; ++it) {
+    PROF_BEGIN(c, PC_SINK_ROW);
+    TRY(sink64_iter(c, P, s, G, ldG, f, g, eps));
+    PROF_END(c, PC_SINK_ROW, 4);
+    *used = it;
+    if (tol > 0 && it % check_every == 0) {
+      double v = 0.0;
+      TRY(sink64_viol(c, P, s, G, ldG, f, g, eps, &v));
+      if (v <= tol) {
+        *conv = 1;
+        break;
+      }
+    }
+  }
+  return GW_OK;
+}
+
 extern "C" gw_status gw_grad_dp(gw_ctx* c, const gw_problem* pb, const void* T, int64_t ldT, void* G, int64_t ldG,
                                 const gw_moments* mom) {
   if (!c) return fail(GW_ERR_INVALID_ARG, "null ctx");
@@ -1264,6 +1453,9 @@ extern "C" gw_status gw_grad_dp(gw_ctx* c, const gw_problem* pb, const void* T, 
   CU(cudaSetDevice(c->device));
   Prepared P;
   TRY(prepare(c, pb, P));
+  if (pb->dtype == GW_F64)
+    return grad64(c, P, reinterpret_cast<const double*>(T), ldT, reinterpret_cast<double*>(G), ldG, false, nullptr,
+                  nullptr, 1.0, mom, nullptr);
   TSrc S{reinterpret_cast<const float*>(T), ldT, nullptr, nullptr, 0.0};
   TSrc2 S2{reinterpret_cast<const float*>(T), ldT, nullptr, nullptr, nullptr, nullptr, 0.f, 0.f};
   TRY(grad_pass(c, P, T_EXPLICIT, S, S2, reinterpret_cast<float*>(G), ldG, true, false, nullptr, nullptr, 1.0,
@@ -2256,6 +2448,30 @@ extern "C" gw_status sinkhorn_solve(gw_ctx* c, const gw_problem* pb, const void*
   CU(cudaSetDevice(c->device));
   Prepared P;
   TRY(prepare(c, pb, P));
+  if (pb->dtype == GW_F64) {  // fp64 storage (f64.cuh)
+    Sink64 s;
+    TRY(sink64_alloc(c, P, s));
+    double *fd, *gd;
+    TRY(stage_duals_in(c, pb, P, f, g, &fd, &gd));
+    const double* Gd = reinterpret_cast<const double*>(G);
+    int used = 0, conv = 0;
+    TRY(sink64_run(c, P, s, Gd, ldG, fd, gd, o->eps, o->max_iter, o->tol, o->check_every, &used, &conv));
+    if (T_out) {
+      k64_gibbs<<<grid_for(P.nl * P.m, 256, 148 * 32), 256, 0, c->stream>>>(Gd, ldG, fd, gd, o->eps, P.nl, P.m,
+                                                                            reinterpret_cast<double*>(T_out), ldT);
+      KCHECK();
+    }
+    if (info) {
+      double v = 0.0;
+      TRY(sink64_viol(c, P, s, Gd, ldG, fd, gd, o->eps, &v));
+      info->iters = used;
+      info->converged = o->tol > 0 ? (v <= o->tol) : 0;
+      info->fused_iters = 0;
+      info->marginal_violation = v;
+    }
+    TRY(stage_duals_out(c, pb, P, f, g, fd, gd));
+    return GW_OK;
+  }
   SinkState s;
   SinkGuard sguard{s};
   TRY(sink_alloc(c, P, s));
@@ -2295,6 +2511,109 @@ extern "C" gw_status sinkhorn_solve(gw_ctx* c, const gw_problem* pb, const void*
     info->marginal_violation = hv;
   }
   TRY(stage_duals_out(c, pb, P, f, g, s.f, s.g));
+  return GW_OK;
+}
+
+// Entropic (F)GW with fp64 storage (f64.cuh): the same mirror-descent schedule as solve_impl
+// (Remark 1; Remark 2 for FGW; readings R5, R7, R8) with the plan kept explicit:
+// T^l (fp64, one N x M buffer) and G^{l+1} (fp64, one N x M buffer); T^{l+1} = exp((f + g - G^{l+1})/eps).
+static gw_status solve64(gw_ctx* c, const gw_problem* pb, const Prepared& P, const gw_solve_opts* o, const double* fx,
+                         const double* fy, double alpha, const void* T0, void* T_out, int64_t ldT, double* f, double* g,
+                         gw_result* res, double* trace, int ex_iter, void* ex_T, void* ex_G, int64_t ex_ld) {
+  const int64_t nl = P.nl, m = P.m;
+  const double eps = o->eps;
+  const int64_t ld = (m + 31) & ~int64_t(31);
+  double *Tb, *Gb, *objout;
+  TRY(ws(c, c->d64T, (size_t)std::max<int64_t>(nl, 1) * ld, &Tb));
+  TRY(ws(c, c->d64G, (size_t)std::max<int64_t>(nl, 1) * ld, &Gb));
+  TRY(ws(c, c->objout, 16, &objout));
+  Sink64 s;
+  TRY(sink64_alloc(c, P, s));
+  double *fd, *gd;
+  if (pb->flags & GW_HOST_VECTORS) {
+    TRY(stage_duals_in(c, pb, P, nullptr, nullptr, &fd, &gd));
+  } else {
+    fd = f;
+    gd = g;
+  }
+  k_fill<<<grid_for(nl), 256, 0, c->stream>>>(fd, nl, 0.0);  // f = g = 0 before the first sweep (R7)
+  k_fill<<<grid_for(m), 256, 0, c->stream>>>(gd, m, 0.0);
+  KCHECK();
+  EventSet evset;
+  cudaEvent_t ev0, ev1;
+  CU(evset.make(&ev0)); CU(evset.make(&ev1));
+  CU(cudaEventRecord(ev0, c->stream));
+  std::vector<cudaEvent_t> evs(2 * (size_t)o->outer_iters + 2);
+  for (auto& e : evs) CU(evset.make(&e));
+  const int eg = grid_for(nl * m, 256, 148 * 32);
+  // T^0: the caller's T0 or p q^T (reading R5)
+  if (T0) CU(cudaMemcpy2DAsync(Tb, ld * 8, T0, ldT * 8, m * 8, nl, cudaMemcpyDeviceToDevice, c->stream));
+  else k64_product<<<eg, 256, 0, c->stream>>>(P.pn + P.row0, P.qn, nl, m, Tb, ld);
+  KCHECK();
+  const bool want_trace_obj = (o->flags & GW_SOLVE_TRACE_OBJECTIVE) != 0;
+  std::vector<double> tr((size_t)std::max(o->outer_iters, 1) * 4, NAN);
+  int inner_total = 0, conv_all = 1;
+  for (int l = 0; l < o->outer_iters; ++l) {
+    const bool exporting = ex_iter == l + 1;
+    if (exporting && ex_T) CU(cudaMemcpy2DAsync(ex_T, ex_ld * 8, Tb, ld * 8, m * 8, nl, cudaMemcpyDeviceToDevice, c->stream));
+    const bool obj = l > 0 && want_trace_obj;
+    CU(cudaEventRecord(evs[2 * l], c->stream));
+    TRY(grad64(c, P, Tb, ld, Gb, ld, obj, fx, fy, alpha, nullptr, objout));  // G^{l+1} = grad E(T^l)
+    CU(cudaEventRecord(evs[2 * l + 1], c->stream));
+    if (exporting && ex_G) CU(cudaMemcpy2DAsync(ex_G, ex_ld * 8, Gb, ld * 8, m * 8, nl, cudaMemcpyDeviceToDevice, c->stream));
+    if (obj) {
+      CU(cudaMemcpyAsync(c->hpin, objout, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CU(cudaStreamSynchronize(c->stream));
+      tr[(size_t)(l - 1) * 4 + 0] = fx ? (1.0 - alpha) * c->hpin[6] + alpha * c->hpin[0] : c->hpin[0];
+      tr[(size_t)(l - 1) * 4 + 1] = c->hpin[1];
+    }
+    int used = 0, conv = 0;
+    TRY(sink64_run(c, P, s, Gb, ld, fd, gd, eps, o->inner.max_iter, o->inner.tol, o->inner.check_every, &used, &conv));
+    k64_gibbs<<<eg, 256, 0, c->stream>>>(Gb, ld, fd, gd, eps, nl, m, Tb, ld);  // T^{l+1}
+    KCHECK();
+    inner_total += used;
+    if (o->inner.tol > 0 && !conv) conv_all = 0;
+    tr[(size_t)l * 4 + 2] = used;
+  }
+  CU(cudaEventRecord(evs[2 * (size_t)o->outer_iters], c->stream));
+  // final plan: objective, violation, entropy (one gradient pass; G is scratch now)
+  TRY(grad64(c, P, Tb, ld, Gb, ld, true, fx, fy, alpha, nullptr, objout));
+  if (T_out) CU(cudaMemcpy2DAsync(T_out, ldT * 8, Tb, ld * 8, m * 8, nl, cudaMemcpyDeviceToDevice, c->stream));
+  CU(cudaMemcpyAsync(c->hpin, objout, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaEventRecord(ev1, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  const double E = c->hpin[0], viol = c->hpin[1], H = c->hpin[3], ecc = c->hpin[6];
+  if (!(std::isfinite(E) && std::isfinite(H) && std::isfinite(viol)))
+    return fail(GW_ERR_NONFINITE, "non-finite result (E = %g, H = %g, violation = %g): eps too small for the "
+                "cost scale, or non-finite inputs", E, H, viol);
+  const double Eout = fx ? (1.0 - alpha) * ecc + alpha * E : E;
+  if (o->outer_iters > 0) {
+    tr[(size_t)(o->outer_iters - 1) * 4 + 0] = Eout;
+    tr[(size_t)(o->outer_iters - 1) * 4 + 1] = viol;
+  }
+  float ms_grad = 0.f, ms_sink = 0.f, ms_total = 0.f;
+  for (int l = 0; l < o->outer_iters; ++l) {
+    float a = 0.f, b = 0.f;
+    CU(cudaEventElapsedTime(&a, evs[2 * l], evs[2 * l + 1]));
+    CU(cudaEventElapsedTime(&b, evs[2 * l + 1], evs[2 * l + 2]));
+    ms_grad += a;
+    ms_sink += b;
+    tr[(size_t)l * 4 + 3] = a + b;
+  }
+  CU(cudaEventElapsedTime(&ms_total, ev0, ev1));
+  res->gw_objective = Eout;
+  res->entropic_objective = Eout + eps * H;
+  res->marginal_violation = viol;
+  res->outer_iters = o->outer_iters;
+  res->inner_iters_total = inner_total;
+  res->converged = (o->inner.tol > 0) ? conv_all : 0;
+  res->inner_fused_total = 0;
+  res->ms_grad = ms_grad;
+  res->ms_sinkhorn = ms_sink;
+  res->ms_total = ms_total;
+  res->grad_onepass_total = 0;
+  if (trace) memcpy(trace, tr.data(), sizeof(double) * 4 * (size_t)o->outer_iters);
+  TRY(stage_duals_out(c, pb, P, f, g, fd, gd));
   return GW_OK;
 }
 
@@ -2342,6 +2661,10 @@ static gw_status solve_impl(gw_ctx* c, const gw_problem* pb, const gw_solve_opts
     } else {
       fx = fx_in; fy = fy_in;
     }
+  }
+  if (pb->dtype == GW_F64) {
+    if (tau_mode) return fail(GW_ERR_UNSUPPORTED, "GW_F64 storage: tau != eps is not implemented");
+    return solve64(c, pb, P, o, fx, fy, alpha, T0, T_out, ldT, f, g, res, trace, ex.iter, ex.T, ex.G, ex.ld);
   }
   // cost buffer
   const int64_t ldG = (m + 31) & ~int64_t(31);
@@ -2674,6 +2997,7 @@ static gw_status ugw_impl(gw_ctx* c, const gw_problem* pb, double rho, const gw_
   if (o->inner.tol > 0) return fail(GW_ERR_UNSUPPORTED, "ugw_solve: fixed inner iteration counts only");
   TRY(check_problem(pb));
   if (pb->flags & GW_GRID2D) return fail(GW_ERR_UNSUPPORTED, "ugw_solve: 2-D grids are not implemented");
+  if (pb->dtype != GW_F32) return fail(GW_ERR_UNSUPPORTED, "ugw_solve: fp32 storage only");
   if (T_out) TRY(check_matrix(T_out, ldT, pb->m, "T_out"));
   CU(cudaSetDevice(c->device));
   const double eps = o->eps;
