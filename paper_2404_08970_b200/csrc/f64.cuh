@@ -58,8 +58,10 @@ __global__ void k64_momcols(const double* __restrict__ cs, const double* __restr
 // a2, the row direction (PAPER.md:194-243 at k = 1): B = T D_Y row by row,
 //   B_ip = sum_q |y_p - y_q| T_iq = 2 (y_p P_<p - Q_<p) + Q_tot - y_p P_tot,
 //   P_<p = sum_{q<p} T_iq,  Q_<p = sum_{q<p} y_q T_iq  (fp64 warp scans with a running carry).
-// One warp per row.  B may alias T (each lane reads its element before writing it).  rin (nullable):
-// supplied totals [P_tot | Q_tot]; rtot (out): [P_tot | Q_tot] of every row.
+// One warp per row, ONE read of the row: the kernel writes B'_ip = 2 (y_p P_<p - Q_<p) and the row totals
+// (the final carries); the column kernels add the rank-2 term Q_tot_i - y_p P_tot_i when they read B'
+// (b64 below).  B may alias T (each lane reads its element before writing it).  rin (nullable): supplied
+// totals [P_tot | Q_tot] (copied to rtot); rtot (out): [P_tot | Q_tot] of every row.
 __global__ void k64_row(const double* T, int64_t ldT, int64_t nl, int64_t m, const double* __restrict__ yc,
                         const double* __restrict__ rin, double* B, int64_t ldB, double* __restrict__ rtot) {
   const int lane = threadIdx.x & 31;
@@ -67,21 +69,6 @@ __global__ void k64_row(const double* T, int64_t ldT, int64_t nl, int64_t m, con
   if (i >= nl) return;
   const double* t = T + i * ldT;
   double* b = B + i * ldB;
-  double Pt, Qt;
-  if (rin) {
-    Pt = rin[i];
-    Qt = rin[nl + i];
-  } else {
-    double s0 = 0.0, s1 = 0.0;
-#pragma unroll 4
-    for (int64_t p = lane; p < m; p += 32) {
-      const double v = t[p];
-      s0 += v;
-      s1 += yc[p] * v;
-    }
-    Pt = warp_sum(s0);
-    Qt = warp_sum(s1);
-  }
   double cP = 0.0, cQ = 0.0;
   constexpr int U = 4;  // chunks of 32 columns loaded ahead of the (serial) scans
   for (int64_t p0 = 0; p0 < m; p0 += 32 * U) {
@@ -106,25 +93,32 @@ __global__ void k64_row(const double* T, int64_t ldT, int64_t nl, int64_t m, con
       }
       double ae = __shfl_up_sync(0xffffffffu, a, 1), ce = __shfl_up_sync(0xffffffffu, c, 1);
       if (lane == 0) ae = ce = 0.0;
-      if (p < m) b[p] = 2.0 * (yv[u] * (cP + ae) - (cQ + ce)) + Qt - yv[u] * Pt;
+      if (p < m) b[p] = 2.0 * (yv[u] * (cP + ae) - (cQ + ce));
       cP += __shfl_sync(0xffffffffu, a, 31);
       cQ += __shfl_sync(0xffffffffu, c, 31);
     }
   }
   if (lane == 0) {
-    rtot[i] = Pt;
-    rtot[nl + i] = Qt;
+    rtot[i] = rin ? rin[i] : cP;
+    rtot[nl + i] = rin ? rin[nl + i] : cQ;
   }
+}
+
+// B_ip from the row pass's B'_ip and the row totals (the deferred rank-2 term)
+__device__ __forceinline__ double b64(double bp, const double* __restrict__ rtot, int64_t nl, int64_t i, double y) {
+  return bp + rtot[nl + i] - y * rtot[i];
 }
 
 // a3, the column direction: per 64-row block and column, S = sum_j B_jp and
 // U = sum_j x_j B_jp over the block's rows.  part: [nb][2][m].
 __global__ void k64_colpart(const double* __restrict__ B, int64_t ldB, int64_t nl, int64_t m,
-                            const double* __restrict__ xl, double* __restrict__ part) {
+                            const double* __restrict__ xl, const double* __restrict__ yc,
+                            const double* __restrict__ rtot, double* __restrict__ part) {
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t blk = blockIdx.y;
   if (p >= m) return;
   const int64_t i0 = blk * F64_RB, i1 = min(nl, i0 + F64_RB);
+  const double yp = yc[p];
   double S = 0.0, U = 0.0;
   for (int64_t c0 = i0; c0 < i1; c0 += F64_CH) {  // F64_CH loads in flight per thread
     double b[F64_CH];
@@ -132,8 +126,11 @@ __global__ void k64_colpart(const double* __restrict__ B, int64_t ldB, int64_t n
     for (int u = 0; u < F64_CH; ++u) b[u] = c0 + u < i1 ? B[(c0 + u) * ldB + p] : 0.0;
 #pragma unroll
     for (int u = 0; u < F64_CH; ++u) {
-      S += b[u];
-      if (c0 + u < i1) U += xl[c0 + u] * b[u];
+      if (c0 + u < i1) {
+        const double bb = b64(b[u], rtot, nl, c0 + u, yp);
+        S += bb;
+        U += xl[c0 + u] * bb;
+      }
     }
   }
   part[(2 * blk) * m + p] = S;
@@ -141,16 +138,30 @@ __global__ void k64_colpart(const double* __restrict__ B, int64_t ldB, int64_t n
 }
 
 // Exclusive prefix of the block partials over blocks (in place, block order); tot = this rank's totals.
+// One thread per column (coalesced across the warp), 16 blocks' loads in flight before they are consumed.
 __global__ void k64_colscan(double* __restrict__ part, int nb, int64_t m, double* __restrict__ tot) {
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= m) return;
+  constexpr int CH = 16;
   double S = 0.0, U = 0.0;
-  for (int k = 0; k < nb; ++k) {
-    const double s = part[(2 * (int64_t)k) * m + p], u = part[(2 * (int64_t)k + 1) * m + p];
-    part[(2 * (int64_t)k) * m + p] = S;
-    part[(2 * (int64_t)k + 1) * m + p] = U;
-    S += s;
-    U += u;
+  for (int k0 = 0; k0 < nb; k0 += CH) {
+    double s[CH], u[CH];
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      const int64_t k = k0 + j;
+      s[j] = k < nb ? part[(2 * k) * m + p] : 0.0;
+      u[j] = k < nb ? part[(2 * k + 1) * m + p] : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      const int64_t k = k0 + j;
+      if (k < nb) {
+        part[(2 * k) * m + p] = S;
+        part[(2 * k + 1) * m + p] = U;
+      }
+      S += s[j];
+      U += u[j];
+    }
   }
   tot[p] = S;
   tot[m + p] = U;
@@ -175,7 +186,7 @@ __global__ void k64_rankoff(const double* __restrict__ gath, int R, int rank, in
 // a3 + a4: (D_X B)_ip = 2 (x_i S_<i - U_<i) + U_tot - x_i S_tot (S, U column prefixes of B and x B,
 // PAPER.md:211-219), then G_ip = 2 (c_i + c'_p) - 4 (D_X T D_Y)_ip or, with the
 // feature cost (Remark 2), (1 - alpha) C_ip^2 + alpha (2 (c_i + c'_p) - 4 (D_X T D_Y)_ip).
-// G holds B on entry and is overwritten in place.  OBJ: per (block, column) partials of
+// G holds B' (k64_row) on entry and is overwritten in place.  OBJ: per (block, column) partials of
 // sum T (D_X T D_Y), sum T, sum T (ln T - 1), sum T C^2 into obj [nb][4][m] (T explicit, not aliased).
 template <bool OBJ, bool FGW>
 __global__ void k64_colapply(double* G, int64_t ldG, const double* __restrict__ T, int64_t ldT, int64_t nl,
@@ -183,29 +194,30 @@ __global__ void k64_colapply(double* G, int64_t ldG, const double* __restrict__ 
                              const double* __restrict__ off, const double* __restrict__ glob,
                              const double* __restrict__ cl, const double* __restrict__ c2,
                              const double* __restrict__ fxl, const double* __restrict__ fy, double alpha,
-                             double* __restrict__ obj) {
+                             const double* __restrict__ yc, const double* __restrict__ rtot, double* __restrict__ obj) {
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t blk = blockIdx.y;
   if (p >= m) return;
   const int64_t i0 = blk * F64_RB, i1 = min(nl, i0 + F64_RB);
   double S = off[p] + part[(2 * blk) * m + p], U = off[m + p] + part[(2 * blk + 1) * m + p];
-  const double St = glob[p], Ut = glob[m + p], cp = c2[p];
+  const double St = glob[p], Ut = glob[m + p], cp = c2[p], yp = yc[p];
   const double fyp = FGW ? fy[p] : 0.0;
   double o0 = 0.0, o1 = 0.0, o2 = 0.0, o3 = 0.0;
-  for (int64_t c0 = i0; c0 < i1; c0 += F64_CH) {
-  double bv[F64_CH], tv[F64_CH];
+  constexpr int CHA = 8;  // (16 rows: 168 registers, 18 % of the warps resident)
+  for (int64_t c0 = i0; c0 < i1; c0 += CHA) {
+  double bv[CHA], tv[CHA];
 #pragma unroll
-  for (int u = 0; u < F64_CH; ++u) {
+  for (int u = 0; u < CHA; ++u) {
     bv[u] = c0 + u < i1 ? G[(c0 + u) * ldG + p] : 0.0;
     if (OBJ) tv[u] = c0 + u < i1 ? T[(c0 + u) * ldT + p] : 0.0;
   }
 #pragma unroll
-  for (int u = 0; u < F64_CH; ++u) {
+  for (int u = 0; u < CHA; ++u) {
     const int64_t i = c0 + u;
     if (i >= i1) break;
     const double x = xl[i];
     double* gp = G + i * ldG + p;
-    const double b = bv[u];
+    const double b = b64(bv[u], rtot, nl, i, yp);
     const double db = 2.0 * (x * S - U) + Ut - x * St;
     S += b;
     U += x * b;
@@ -421,27 +433,37 @@ __global__ void k64_colpart_lse(const double* __restrict__ G, int64_t ldG, int64
   const double gp = g ? g[p] : 0.0;
   const double c2 = GW_LOG2E / eps;
   L64 a{-INFINITY, 0.0};
-  for (int64_t c0 = i0; c0 < i1; c0 += F64_CH) {
-    double v[F64_CH];
+  constexpr int CH = 8;
+  for (int64_t c0 = i0; c0 < i1; c0 += CH) {
+    double v[CH];
 #pragma unroll
-    for (int u = 0; u < F64_CH; ++u) v[u] = c0 + u < i1 ? G[(c0 + u) * ldG + p] : 0.0;
+    for (int u = 0; u < CH; ++u) v[u] = c0 + u < i1 ? G[(c0 + u) * ldG + p] : 0.0;
 #pragma unroll
-    for (int u = 0; u < F64_CH; ++u) v[u] = c0 + u < i1 ? (f[c0 + u] + gp - v[u]) * c2 : -INFINITY;
-    l64_chunk<F64_CH>(a, v);
+    for (int u = 0; u < CH; ++u) v[u] = c0 + u < i1 ? (f[c0 + u] + gp - v[u]) * c2 : -INFINITY;
+    l64_chunk<CH>(a, v);
   }
   part[blk * m + p] = make_double2(a.m, a.s);
 }
-// The blocks' pairs merged in block order: pay[p] = max, pay[m + p] = sum (this rank's rows).
+// The blocks' pairs merged (one warp per column: lane segments, then a fixed butterfly):
+// pay[p] = max, pay[m + p] = sum (this rank's rows).
 __global__ void k64_colcomb(const double2* __restrict__ part, int nb, int64_t m, double* __restrict__ pay) {
-  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t p = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (p >= m) return;
   L64 a{-INFINITY, 0.0};
-  for (int k = 0; k < nb; ++k) {
+  for (int k = lane; k < nb; k += 32) {
     const double2 v = part[(int64_t)k * m + p];
     a = l64_merge(a, L64{v.x, v.y});
   }
-  pay[p] = a.m;
-  pay[m + p] = a.s;
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    L64 o{__shfl_xor_sync(0xffffffffu, a.m, d), __shfl_xor_sync(0xffffffffu, a.s, d)};
+    a = l64_merge(a, o);
+  }
+  if (lane == 0) {
+    pay[p] = a.m;
+    pay[m + p] = a.s;
+  }
 }
 // The ranks' pairs [R][stride] merged in rank order.
 //   mode 0 (a6, g-update): g_p = eps ln q_p - eps LSE_i((f_i - G_ip) / eps)

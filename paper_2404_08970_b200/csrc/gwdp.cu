@@ -1292,9 +1292,9 @@ static gw_status grad64(gw_ctx* c, const Prepared& P, const double* T, int64_t l
   KCHECK();
   // a3: column block partials of B and x B, their exclusive prefix, the ranks' offsets and totals
   const dim3 cg((unsigned)((m + 127) / 128), (unsigned)nb);
-  k64_colpart<<<cg, 128, 0, c->stream>>>(G, ldG, nl, m, xl, part);
+  k64_colpart<<<cg, 128, 0, c->stream>>>(G, ldG, nl, m, xl, P.yc, rtot, part);
   KCHECK();
-  k64_colscan<<<(unsigned)((m + 255) / 256), 256, 0, c->stream>>>(part, (int)nb, m, tot);
+  k64_colscan<<<(unsigned)((m + 127) / 128), 128, 0, c->stream>>>(part, (int)nb, m, tot);
   KCHECK();
   TRY(comm_allgather(c, tot, gath, 2 * (size_t)m * sizeof(double)));
   if (mom) {  // column totals of B = T D_Y from the supplied T^T 1, T^T x by 1-D DPs over y
@@ -1322,7 +1322,7 @@ static gw_status grad64(gw_ctx* c, const Prepared& P, const double* T, int64_t l
   const double* fxl = fx ? fx + P.row0 : nullptr;
 #define K64_APPLY(O, F)                                                                                        \
   k64_colapply<O, F><<<cg, 128, 0, c->stream>>>(G, ldG, T, ldT, nl, m, xl, part, off, glob, P.cx + P.row0, P.cy, \
-                                                 fxl, fy, alpha, ob)
+                                                 fxl, fy, alpha, P.yc, rtot, ob)
   if (obj) {
     if (fx) K64_APPLY(true, true); else K64_APPLY(true, false);
   } else {
@@ -1373,7 +1373,7 @@ static gw_status sink64_cols(gw_ctx* c, const Prepared& P, Sink64& s, const doub
   k64_colpart_lse<<<dim3((unsigned)((m + 127) / 128), (unsigned)s.nb), 128, 0, c->stream>>>(G, ldG, P.nl, m, f, g,
                                                                                           eps, s.part);
   KCHECK();
-  k64_colcomb<<<(unsigned)((m + 255) / 256), 256, 0, c->stream>>>(s.part, (int)s.nb, m, s.pay);
+  k64_colcomb<<<(unsigned)((m * 32 + 255) / 256), 256, 0, c->stream>>>(s.part, (int)s.nb, m, s.pay);
   KCHECK();
   TRY(comm_allgather(c, s.pay, s.gath, (size_t)s.stride * sizeof(double)));
   return GW_OK;
