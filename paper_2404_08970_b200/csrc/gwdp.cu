@@ -1353,6 +1353,11 @@ struct Sink64 {
   double *pay, *gath, *rdev, *cdev, *vout;
   double2* part;
   int64_t stride = 0, nb = 0;
+  cudaGraphExec_t gexec = nullptr;  // fixed-count loops: `gchunk` iterations captured once per solve
+  int gchunk = 0;
+  ~Sink64() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+  }
 };
 static gw_status sink64_alloc(gw_ctx* c, const Prepared& P, Sink64& s) {
   s.stride = 2 * P.m + 2;
@@ -1416,11 +1421,47 @@ static gw_status sink64_viol(gw_ctx* c, const Prepared& P, Sink64& s, const doub
 // `iters` iterations; tol > 0: the plan's violation checked every check_every iterations, stop when
 // <= tol (reading R8; the oracle's schedule exactly)
 static gw_status sink64_run(gw_ctx* c, const Prepared& P, Sink64& s, const double* G, int64_t ldG, double* f,
-                            double* g, double eps, int iters, double tol, int check_every, int* used, int* conv) {
+                            double* g, double eps, int iters, double tol, int check_every, int* used, int* conv,
+                            bool graph_ok = false) {
   NvtxRange nv("gw.sinkhorn64");
   *used = 0;
   *conv = 0;
   if (check_every < 1) check_every = 10;
+  // Fixed-count loop inside a solve (the same G, f, g, eps every outer iteration): up to 100 iterations
+  // captured once as a CUDA graph and replayed (C1's 256 x 256 iterations are launch bound: 4 kernels
+  // each).  Host-transport all-gathers are not capturable.
+  static const bool no_graph = getenv("GWDP_NO_GRAPH") != nullptr;
+  if (graph_ok && tol <= 0 && iters > 0 && !no_graph && !c->prof.on &&
+      (P.R == 1 || (c->comm && c->comm->nccl))) {
+    const int chunk = std::min(iters, 100);
+    if (!s.gexec || s.gchunk != chunk) {
+      if (s.gexec) cudaGraphExecDestroy(s.gexec);
+      s.gexec = nullptr;
+      if (!c->cap) CU(cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking));
+      CU(cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal));
+      cudaStream_t saved = c->stream;
+      c->stream = c->cap;
+      gw_status st = GW_OK;
+      for (int k = 0; k < chunk && st == GW_OK; ++k) st = sink64_iter(c, P, s, G, ldG, f, g, eps);
+      c->stream = saved;
+      cudaGraph_t gr = nullptr;
+      const cudaError_t e = cudaStreamEndCapture(c->cap, &gr);
+      if (st != GW_OK) {
+        if (gr) cudaGraphDestroy(gr);
+        return st;
+      }
+      if (e != cudaSuccess) return fail(GW_ERR_CUDA, "fp64 Sinkhorn graph capture: %s", cudaGetErrorString(e));
+      const cudaError_t ei = cudaGraphInstantiate(&s.gexec, gr, 0);
+      cudaGraphDestroy(gr);
+      if (ei != cudaSuccess) return fail(GW_ERR_CUDA, "fp64 Sinkhorn graph instantiate: %s", cudaGetErrorString(ei));
+      s.gchunk = chunk;
+    }
+    int done = 0;
+    for (; done + s.gchunk <= iters; done += s.gchunk) CU(cudaGraphLaunch(s.gexec, c->stream));
+    for (; done < iters; ++done) TRY(sink64_iter(c, P, s, G, ldG, f, g, eps));
+    *used = iters;
+    return GW_OK;
+  }
   for (int it = 1; it <= iters; ++it) {
     PROF_BEGIN(c, PC_SINK_ROW);
     TRY(sink64_iter(c, P, s, G, ldG, f, g, eps));
@@ -2568,7 +2609,8 @@ static gw_status solve64(gw_ctx* c, const gw_problem* pb, const Prepared& P, con
       tr[(size_t)(l - 1) * 4 + 1] = c->hpin[1];
     }
     int used = 0, conv = 0;
-    TRY(sink64_run(c, P, s, Gb, ld, fd, gd, eps, o->inner.max_iter, o->inner.tol, o->inner.check_every, &used, &conv));
+    TRY(sink64_run(c, P, s, Gb, ld, fd, gd, eps, o->inner.max_iter, o->inner.tol, o->inner.check_every, &used, &conv,
+                   true));
     k64_gibbs<<<eg, 256, 0, c->stream>>>(Gb, ld, fd, gd, eps, nl, m, Tb, ld);  // T^{l+1}
     KCHECK();
     inner_total += used;

@@ -304,3 +304,29 @@ def test_sharded64(gw, R, monkeypatch):
     eo = abs(out[0][1] - ro["gw_objective"]) / abs(ro["gw_objective"])
     _log(test="sharded64", R=R, ef=ef, eo=eo, eg=_rel(Gs, Go))
     assert ef <= SINK64_TOL
+
+
+def test_solver64_degenerate(gw):
+    """Degenerate inputs on the fp64 path: zero-mass rows and columns (ln 0 = -inf duals, empty plan rows),
+    a single point on either side (n = 1 or m = 1: the plan is p q^T), against the oracle."""
+    import torch
+    rng = np.random.default_rng(9)
+    n, m = 70, 45
+    x, y = np.sort(rng.random(n)), np.sort(rng.random(m))
+    p, q = rng.random(n), rng.random(m)
+    p[[0, 13, 69]] = 0.0
+    q[[5, 44]] = 0.0
+    p, q = p / p.sum(), q / q.sum()
+    r = gw.solve(x, y, p, q, 0.05, 3, 40, trace_objective=True, return_plan=True, dtype=torch.float64)
+    ro = O.entropic_gw(x, y, p, q, 0.05, 3, 40)
+    T = _np(r.T)
+    assert np.all(T[[0, 13, 69], :] == 0.0) and np.all(T[:, [5, 44]] == 0.0)
+    assert _rel(T, ro["T"]) <= OBJ64_TOL
+    assert np.max(np.abs(r.trace[:, 0] - ro["E"]) / np.abs(ro["E"])) <= OBJ64_TOL
+    assert abs(r.entropic_objective - ro["entropic_objective"]) <= OBJ64_TOL * abs(ro["entropic_objective"])
+    for (a, b) in [(1, 9), (9, 1)]:
+        xa, yb = np.sort(rng.random(a)), np.sort(rng.random(b))
+        pa, qb = rng.dirichlet(np.ones(a)), rng.dirichlet(np.ones(b))
+        r1 = gw.solve(xa, yb, pa, qb, 0.05, 2, 10, return_plan=True, dtype=torch.float64)
+        assert _rel(_np(r1.T), np.outer(pa, qb)) <= 1e-14
+        assert abs(r1.gw_objective - O.objective(xa, yb, np.outer(pa, qb))) <= 1e-14 + 1e-12 * abs(r1.gw_objective)
