@@ -54,6 +54,20 @@ def main():
     api.solve(s, s, u, u[::-1].copy(), 0.02, 2, 20, device=dev, grid2d=True, trace_objective=True)
     api.ugw_solve(x, y, p, q, 1.0, 0.02, 2, 10, device=dev, trace_objective=True)
     torch.cuda.synchronize()
+    # fp64 storage (GW_F64, f64.cuh): gradient (in place and with supplied moments), Sinkhorn with the
+    # tolerance rule, a graph-captured solve with the objective trace, FGW
+    n, m = 133, 70
+    x, y, p, q = prob(n, m)
+    T64 = api.plan_buffer(n, m, dev, torch.float64)
+    T64.copy_(torch.from_numpy(rng.random((n, m)) / (n * m)))
+    Tn = T64.cpu().numpy()
+    api.grad(x, y, p, q, T64, moments=(Tn.sum(1), Tn @ y, Tn.sum(0), Tn.T @ x))
+    api.grad(x, y, p, q, T64, out=T64)
+    api.sinkhorn(T64, p, q, 0.05, 25, tol=1e-12, check_every=5, return_plan=True)
+    api.solve(x, y, p, q, 0.02, 2, 20, device=dev, trace_objective=True, return_plan=True, dtype=torch.float64)
+    api.solve(x, y, p, q, 0.02, 2, 20, device=dev, fx=rng.random(n), fy=rng.random(m), alpha=0.5,
+              dtype=torch.float64)
+    torch.cuda.synchronize()
     print("sanitize workload ok")
 
 
