@@ -69,7 +69,7 @@ typedef enum {
   GW_ERR_NOT_NORMALIZED = 5,  /* |sum - 1| > 1e-9                        */
   GW_ERR_NONFINITE = 6,       /* NaN/Inf in inputs or produced          */
   GW_ERR_CONFIG = 7,          /* invalid options                                       */
-  GW_ERR_UNSUPPORTED = 8,     /* k > GW_MAX_K, loss != square, GW_F64 off k = 1 / 1-D, tau != eps off k = 1, ... */
+  GW_ERR_UNSUPPORTED = 8,     /* k > GW_MAX_K, loss != square, GW_F64 on 2-D grids, tau != eps off k = 1, ... */
   GW_ERR_OOM = 9,
   GW_ERR_CUDA = 10,
   GW_ERR_NCCL = 11
@@ -79,8 +79,8 @@ typedef enum { GW_LOSS_SQUARE = 0 } gw_loss;       /* the only loss the paper de
 /* Storage of every N x M matrix (T, G, T0, T_out, export buffers) of a call.  GW_F32: the bandwidth
  * path (C2-C5).  GW_F64 (C1 = BASELINE configs[0], SURVEY.md §8 sizes table): every matrix float64 and
  * every step in fp64 (the DP gradient as a row scan and a column scan, the log-domain Sinkhorn updates,
- * the objective) -- parity ~1e-12 with the float64 oracle; k = 1 on 1-D supports only (other k, 2-D
- * grids, ugw_solve, tau != eps: GW_ERR_UNSUPPORTED).  The solver keeps its plan explicit then (two
+ * the objective) -- parity ~1e-12 with the float64 oracle; 1-D supports, k = 1..GW_MAX_K (2-D grids,
+ * ugw_solve, tau != eps: GW_ERR_UNSUPPORTED).  The solver keeps its plan explicit then (two
  * fp64 N x M buffers).  Any other value: GW_ERR_INVALID_ARG. */
 typedef enum { GW_F32 = 0, GW_F64 = 1 } gw_dtype;
 
@@ -103,7 +103,7 @@ typedef struct {
   const double *p, *q;    /* marginals, >= 0, sum 1 within 1e-9 (length n and m)       */
   int32_t k;              /* distance power |x - x'|^k: 1 (hot path) .. GW_MAX_K (R17, f2) */
   int32_t loss;           /* gw_loss */
-  int32_t dtype;          /* gw_dtype: GW_F32, or GW_F64 (k = 1, 1-D)                   */
+  int32_t dtype;          /* gw_dtype: GW_F32, or GW_F64 (1-D supports)                 */
   uint32_t flags;         /* GW_NO_VALIDATE | GW_HOST_VECTORS | GW_GRID2D              */
 } gw_problem;
 

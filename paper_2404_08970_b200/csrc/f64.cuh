@@ -55,127 +55,186 @@ __global__ void k64_momcols(const double* __restrict__ cs, const double* __restr
   }
 }
 
-// a2, the row direction (PAPER.md:194-243 at k = 1): B = T D_Y row by row,
-//   B_ip = sum_q |y_p - y_q| T_iq = 2 (y_p P_<p - Q_<p) + Q_tot - y_p P_tot,
-//   P_<p = sum_{q<p} T_iq,  Q_<p = sum_{q<p} y_q T_iq  (fp64 warp scans with a running carry).
-// One warp per row, ONE read of the row: the kernel writes B'_ip = 2 (y_p P_<p - Q_<p) and the row totals
-// (the final carries); the column kernels add the rank-2 term Q_tot_i - y_p P_tot_i when they read B'
-// (b64 below).  B may alias T (each lane reads its element before writing it).  rin (nullable): supplied
-// totals [P_tot | Q_tot] (copied to rtot); rtot (out): [P_tot | Q_tot] of every row.
+// Distance power k (|x - x'|^k, PAPER.md:229-259 / reading R17), with kappa_r = C(k, r) (-1)^r:
+//   (D v)_p = sum_q |y_p - y_q|^k v_q = sum_r kappa_r y_p^(k-r) [S_r^<(p) + (-1)^k (S_r^tot - S_r^<(p))],
+//   S_r^<(p) = sum_{q<p} y_q^r v_q   (the q = p term vanishes),
+// i.e. odd k: sum_r kappa_r y_p^(k-r) (2 S_r^< - S_r^tot); even k: sum_r kappa_r y_p^(k-r) S_r^tot (no scan).
+// k = 1 is the paper's gap recursion: 2 (y_p P_< - Q_<) + Q_tot - y_p P_tot.  Supports are centred.
+__host__ __device__ constexpr double kappa64(int k, int r) {
+  double c = 1.0;
+  for (int j = 0; j < r; ++j) c = c * (k - j) / (j + 1);
+  return (r & 1) ? -c : c;
+}
+template <int K>
+__device__ __forceinline__ void pow64(double x, double (&v)[K + 1]) {
+  v[0] = 1.0;
+#pragma unroll
+  for (int r = 1; r <= K; ++r) v[r] = v[r - 1] * x;
+}
+
+// a2, the row direction: B = T D_Y row by row, one warp per row, ONE read of the row.  Odd k: fp64
+// warp scans of the k + 1 power sums with running carries; the kernel writes
+// B'_ip = 2 sum_r kappa_r y_p^(k-r) S_r^<(p) and the row totals S_r^tot (the final carries); the column
+// kernels add the deferred term -sum_r kappa_r y_p^(k-r) S_r^tot(i) when they read B' (b64 below).
+// Even k: only the totals (B is then the deferred term alone; nothing is written).  B may alias T (each
+// lane reads its element before writing it).  rin (nullable, k = 1): supplied totals [P_tot | Q_tot];
+// rtot (out): [k + 1][nl].
+template <int K>
 __global__ void k64_row(const double* T, int64_t ldT, int64_t nl, int64_t m, const double* __restrict__ yc,
                         const double* __restrict__ rin, double* B, int64_t ldB, double* __restrict__ rtot) {
+  constexpr int NS = K + 1;
   const int lane = threadIdx.x & 31;
   const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (i >= nl) return;
   const double* t = T + i * ldT;
   double* b = B + i * ldB;
-  double cP = 0.0, cQ = 0.0;
-  constexpr int U = 4;  // chunks of 32 columns loaded ahead of the (serial) scans
-  for (int64_t p0 = 0; p0 < m; p0 += 32 * U) {
-    double v[U], yv[U];
+  double cr[NS];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t p = p0 + 32 * u + lane;
-      v[u] = p < m ? t[p] : 0.0;
-      yv[u] = p < m ? yc[p] : 0.0;
+  for (int r = 0; r < NS; ++r) cr[r] = 0.0;
+  if (K % 2 == 0) {  // totals only
+#pragma unroll 4
+    for (int64_t p = lane; p < m; p += 32) {
+      const double v = t[p], y = yc[p];
+      double yp = 1.0;
+#pragma unroll
+      for (int r = 0; r < NS; ++r) {
+        cr[r] += yp * v;
+        yp *= y;
+      }
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t p = p0 + 32 * u + lane;
-      double a = v[u], c = yv[u] * v[u];  // inclusive warp scans
+    for (int r = 0; r < NS; ++r) cr[r] = warp_sum(cr[r]);
+  } else {
+    constexpr int U = K == 1 ? 4 : 2;  // chunks of 32 columns loaded ahead of the (serial) scans
+    for (int64_t p0 = 0; p0 < m; p0 += 32 * U) {
+      double v[U], yv[U];
 #pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const double oa = __shfl_up_sync(0xffffffffu, a, d), oc = __shfl_up_sync(0xffffffffu, c, d);
-        if (lane >= d) {
-          a += oa;
-          c += oc;
-        }
+      for (int u = 0; u < U; ++u) {
+        const int64_t p = p0 + 32 * u + lane;
+        v[u] = p < m ? t[p] : 0.0;
+        yv[u] = p < m ? yc[p] : 0.0;
       }
-      double ae = __shfl_up_sync(0xffffffffu, a, 1), ce = __shfl_up_sync(0xffffffffu, c, 1);
-      if (lane == 0) ae = ce = 0.0;
-      if (p < m) b[p] = 2.0 * (yv[u] * (cP + ae) - (cQ + ce));
-      cP += __shfl_sync(0xffffffffu, a, 31);
-      cQ += __shfl_sync(0xffffffffu, c, 31);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t p = p0 + 32 * u + lane;
+        double yp[NS], a[NS];
+        pow64<K>(yv[u], yp);
+#pragma unroll
+        for (int r = 0; r < NS; ++r) a[r] = yp[r] * v[u];
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {  // inclusive warp scans
+#pragma unroll
+          for (int r = 0; r < NS; ++r) {
+            const double o = __shfl_up_sync(0xffffffffu, a[r], d);
+            if (lane >= d) a[r] += o;
+          }
+        }
+        double acc = 0.0;
+#pragma unroll
+        for (int r = 0; r < NS; ++r) {
+          double e = __shfl_up_sync(0xffffffffu, a[r], 1);
+          if (lane == 0) e = 0.0;
+          acc += kappa64(K, r) * yp[K - r] * (cr[r] + e);
+          cr[r] += __shfl_sync(0xffffffffu, a[r], 31);
+        }
+        if (p < m) b[p] = 2.0 * acc;
+      }
     }
   }
   if (lane == 0) {
-    rtot[i] = rin ? rin[i] : cP;
-    rtot[nl + i] = rin ? rin[nl + i] : cQ;
+#pragma unroll
+    for (int r = 0; r < NS; ++r) rtot[r * nl + i] = (K == 1 && rin) ? rin[r * nl + i] : cr[r];
   }
 }
 
-// B_ip from the row pass's B'_ip and the row totals (the deferred rank-2 term)
-__device__ __forceinline__ double b64(double bp, const double* __restrict__ rtot, int64_t nl, int64_t i, double y) {
-  return bp + rtot[nl + i] - y * rtot[i];
+// B_ip: (odd k) B'_ip plus the deferred term, or (even k) the term alone; yq = powers of y_p
+template <int K>
+__device__ __forceinline__ double b64(double bp, const double* __restrict__ rtot, int64_t nl, int64_t i,
+                                      const double (&yq)[K + 1]) {
+  double d = 0.0;
+#pragma unroll
+  for (int r = 0; r <= K; ++r) d += kappa64(K, r) * yq[K - r] * rtot[r * nl + i];
+  return (K & 1) ? bp - d : d;
 }
 
-// a3, the column direction: per 64-row block and column, S = sum_j B_jp and
-// U = sum_j x_j B_jp over the block's rows.  part: [nb][2][m].
+// a3, the column direction: per 64-row block and column, the power sums
+// S_r = sum_j x_j^r B_jp (r = 0..k) over the block's rows.  part: [nb][k + 1][m].
+template <int K>
 __global__ void k64_colpart(const double* __restrict__ B, int64_t ldB, int64_t nl, int64_t m,
                             const double* __restrict__ xl, const double* __restrict__ yc,
                             const double* __restrict__ rtot, double* __restrict__ part) {
+  constexpr int NS = K + 1, CH = K == 1 ? F64_CH : 8;
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t blk = blockIdx.y;
   if (p >= m) return;
   const int64_t i0 = blk * F64_RB, i1 = min(nl, i0 + F64_RB);
-  const double yp = yc[p];
-  double S = 0.0, U = 0.0;
-  for (int64_t c0 = i0; c0 < i1; c0 += F64_CH) {  // F64_CH loads in flight per thread
-    double b[F64_CH];
+  double yq[NS];
+  pow64<K>(yc[p], yq);
+  double S[NS];
 #pragma unroll
-    for (int u = 0; u < F64_CH; ++u) b[u] = c0 + u < i1 ? B[(c0 + u) * ldB + p] : 0.0;
+  for (int r = 0; r < NS; ++r) S[r] = 0.0;
+  for (int64_t c0 = i0; c0 < i1; c0 += CH) {  // CH loads in flight per thread
+    double bv[CH];
 #pragma unroll
-    for (int u = 0; u < F64_CH; ++u) {
+    for (int u = 0; u < CH; ++u) bv[u] = ((K & 1) && c0 + u < i1) ? B[(c0 + u) * ldB + p] : 0.0;
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
       if (c0 + u < i1) {
-        const double bb = b64(b[u], rtot, nl, c0 + u, yp);
-        S += bb;
-        U += xl[c0 + u] * bb;
+        const double bb = b64<K>(bv[u], rtot, nl, c0 + u, yq);
+        const double x = xl[c0 + u];
+        double xp = 1.0;
+#pragma unroll
+        for (int r = 0; r < NS; ++r) {
+          S[r] += xp * bb;
+          xp *= x;
+        }
       }
     }
   }
-  part[(2 * blk) * m + p] = S;
-  part[(2 * blk + 1) * m + p] = U;
+#pragma unroll
+  for (int r = 0; r < NS; ++r) part[(NS * blk + r) * m + p] = S[r];
 }
 
-// Exclusive prefix of the block partials over blocks (in place, block order); tot = this rank's totals.
-// One thread per column (coalesced across the warp), 16 blocks' loads in flight before they are consumed.
+// Exclusive prefix of the block partials over blocks (in place, block order); tot = this rank's totals
+// [NS][m].  One thread per column (coalesced across the warp), several blocks' loads in flight.
+template <int NS>
 __global__ void k64_colscan(double* __restrict__ part, int nb, int64_t m, double* __restrict__ tot) {
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= m) return;
-  constexpr int CH = 16;
-  double S = 0.0, U = 0.0;
+  constexpr int CH = NS <= 2 ? 16 : 4;
+  double S[NS];
+#pragma unroll
+  for (int r = 0; r < NS; ++r) S[r] = 0.0;
   for (int k0 = 0; k0 < nb; k0 += CH) {
-    double s[CH], u[CH];
+    double v[CH][NS];
+#pragma unroll
+    for (int j = 0; j < CH; ++j)
+#pragma unroll
+      for (int r = 0; r < NS; ++r) v[j][r] = k0 + j < nb ? part[(NS * (int64_t)(k0 + j) + r) * m + p] : 0.0;
 #pragma unroll
     for (int j = 0; j < CH; ++j) {
-      const int64_t k = k0 + j;
-      s[j] = k < nb ? part[(2 * k) * m + p] : 0.0;
-      u[j] = k < nb ? part[(2 * k + 1) * m + p] : 0.0;
-    }
+      if (k0 + j < nb) {
 #pragma unroll
-    for (int j = 0; j < CH; ++j) {
-      const int64_t k = k0 + j;
-      if (k < nb) {
-        part[(2 * k) * m + p] = S;
-        part[(2 * k + 1) * m + p] = U;
+        for (int r = 0; r < NS; ++r) {
+          part[(NS * (int64_t)(k0 + j) + r) * m + p] = S[r];
+          S[r] += v[j][r];
+        }
       }
-      S += s[j];
-      U += u[j];
     }
   }
-  tot[p] = S;
-  tot[m + p] = U;
+#pragma unroll
+  for (int r = 0; r < NS; ++r) tot[r * m + p] = S[r];
 }
 
 // Row shards: off = sum of the ranks before this one, glob = sum over all ranks (rank order).
-// gath: [R][2][m]; glob_set: the global totals were supplied (gw_moments): only off is written.
-__global__ void k64_rankoff(const double* __restrict__ gath, int R, int rank, int64_t m, double* __restrict__ off,
+// gath: [R][len]; glob_set: the global totals were supplied (gw_moments): only off is written.
+__global__ void k64_rankoff(const double* __restrict__ gath, int R, int rank, int64_t len, double* __restrict__ off,
                             double* __restrict__ glob, bool glob_set) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e >= 2 * m) return;
+  if (e >= len) return;
   double o = 0.0, t = 0.0;
   for (int r = 0; r < R; ++r) {
-    const double v = gath[(int64_t)r * 2 * m + e];
+    const double v = gath[(int64_t)r * len + e];
     if (r < rank) o += v;
     t += v;
   }
@@ -183,60 +242,71 @@ __global__ void k64_rankoff(const double* __restrict__ gath, int R, int rank, in
   if (!glob_set) glob[e] = t;
 }
 
-// a3 + a4: (D_X B)_ip = 2 (x_i S_<i - U_<i) + U_tot - x_i S_tot (S, U column prefixes of B and x B,
-// PAPER.md:211-219), then G_ip = 2 (c_i + c'_p) - 4 (D_X T D_Y)_ip or, with the
-// feature cost (Remark 2), (1 - alpha) C_ip^2 + alpha (2 (c_i + c'_p) - 4 (D_X T D_Y)_ip).
-// G holds B' (k64_row) on entry and is overwritten in place.  OBJ: per (block, column) partials of
-// sum T (D_X T D_Y), sum T, sum T (ln T - 1), sum T C^2 into obj [nb][4][m] (T explicit, not aliased).
-template <bool OBJ, bool FGW>
+// a3 + a4: (D_X B)_ip = sum_r kappa_r x_i^(k-r) (odd k: 2 S_r^<(i) - S_r^tot; even k: S_r^tot) with the
+// column power sums S_r of B, then G_ip = 2 (c_i + c'_p) - 4 (D_X T D_Y)_ip
+// or, with the feature cost (Remark 2),
+// (1 - alpha) C_ip^2 + alpha (2 (c_i + c'_p) - 4 (D_X T D_Y)_ip).  G holds B' (k64_row, odd k) on entry and
+// is overwritten in place.  OBJ: per (block, column) partials of sum T (D_X T D_Y), sum T,
+// sum T (ln T - 1), sum T C^2 into obj [nb][4][m] (T explicit, not aliased).
+template <int K, bool OBJ, bool FGW>
 __global__ void k64_colapply(double* G, int64_t ldG, const double* __restrict__ T, int64_t ldT, int64_t nl,
                              int64_t m, const double* __restrict__ xl, const double* __restrict__ part,
                              const double* __restrict__ off, const double* __restrict__ glob,
                              const double* __restrict__ cl, const double* __restrict__ c2,
                              const double* __restrict__ fxl, const double* __restrict__ fy, double alpha,
                              const double* __restrict__ yc, const double* __restrict__ rtot, double* __restrict__ obj) {
+  constexpr int NS = K + 1;
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t blk = blockIdx.y;
   if (p >= m) return;
   const int64_t i0 = blk * F64_RB, i1 = min(nl, i0 + F64_RB);
-  double S = off[p] + part[(2 * blk) * m + p], U = off[m + p] + part[(2 * blk + 1) * m + p];
-  const double St = glob[p], Ut = glob[m + p], cp = c2[p], yp = yc[p];
+  double S[NS], St[NS], yq[NS];
+#pragma unroll
+  for (int r = 0; r < NS; ++r) {
+    S[r] = off[r * m + p] + part[(NS * blk + r) * m + p];
+    St[r] = glob[r * m + p];
+  }
+  pow64<K>(yc[p], yq);
+  const double cp = c2[p];
   const double fyp = FGW ? fy[p] : 0.0;
   double o0 = 0.0, o1 = 0.0, o2 = 0.0, o3 = 0.0;
-  constexpr int CHA = 8;  // (16 rows: 168 registers, 18 % of the warps resident)
+  constexpr int CHA = K == 1 ? 8 : 4;  // (16 rows at k = 1: 168 registers, 18 % of the warps resident)
   for (int64_t c0 = i0; c0 < i1; c0 += CHA) {
-  double bv[CHA], tv[CHA];
+    double bv[CHA], tv[CHA];
 #pragma unroll
-  for (int u = 0; u < CHA; ++u) {
-    bv[u] = c0 + u < i1 ? G[(c0 + u) * ldG + p] : 0.0;
-    if (OBJ) tv[u] = c0 + u < i1 ? T[(c0 + u) * ldT + p] : 0.0;
-  }
+    for (int u = 0; u < CHA; ++u) {
+      bv[u] = c0 + u < i1 ? G[(c0 + u) * ldG + p] : 0.0;
+      if (OBJ) tv[u] = c0 + u < i1 ? T[(c0 + u) * ldT + p] : 0.0;
+    }
 #pragma unroll
-  for (int u = 0; u < CHA; ++u) {
-    const int64_t i = c0 + u;
-    if (i >= i1) break;
-    const double x = xl[i];
-    double* gp = G + i * ldG + p;
-    const double b = b64(bv[u], rtot, nl, i, yp);
-    const double db = 2.0 * (x * S - U) + Ut - x * St;
-    S += b;
-    U += x * b;
-    double gv = 2.0 * (cl[i] + cp) - 4.0 * db;
-    double cc = 0.0;
-    if (FGW) {
-      const double d = fxl[i] - fyp;
-      cc = d * d;
-      gv = (1.0 - alpha) * cc + alpha * gv;
+    for (int u = 0; u < CHA; ++u) {
+      const int64_t i = c0 + u;
+      if (i >= i1) break;
+      const double x = xl[i];
+      const double b = b64<K>(bv[u], rtot, nl, i, yq);
+      double xp[NS];
+      pow64<K>(x, xp);
+      double db = 0.0;
+#pragma unroll
+      for (int r = 0; r < NS; ++r) db += kappa64(K, r) * xp[K - r] * ((K & 1) ? 2.0 * S[r] - St[r] : St[r]);
+#pragma unroll
+      for (int r = 0; r < NS; ++r) S[r] += xp[r] * b;
+      double gv = 2.0 * (cl[i] + cp) - 4.0 * db;
+      double cc = 0.0;
+      if (FGW) {
+        const double d = fxl[i] - fyp;
+        cc = d * d;
+        gv = (1.0 - alpha) * cc + alpha * gv;
+      }
+      G[i * ldG + p] = gv;
+      if (OBJ) {
+        const double t = tv[u];
+        o0 += t * db;
+        o1 += t;
+        if (t > 0.0) o2 += t * (log(t) - 1.0);
+        o3 += t * cc;
+      }
     }
-    *gp = gv;
-    if (OBJ) {
-      const double t = tv[u];
-      o0 += t * db;
-      o1 += t;
-      if (t > 0.0) o2 += t * (log(t) - 1.0);
-      o3 += t * cc;
-    }
-  }
   }
   if (OBJ) {
     obj[(4 * blk + 0) * m + p] = o0;
@@ -283,10 +353,13 @@ __device__ __forceinline__ double bmax1024(double v, double* sm) {
   return t;
 }
 
-// Objective pieces, step 2 (one CTA of 1024): this rank's scalars into pay[m .. m + 8):
-//   {sum T DTD, sum T (ln T - 1), sum T C^2, A0, A1, A2, max_i |a_i - p_i|, 0}
-// with a = T 1 (the row pass's P_tot) and A_k = sum_i a_i x_i^k (centred x).
-__global__ void k64_objlocal(const double* __restrict__ tmp, int64_t m, const double* __restrict__ a,
+constexpr int F64_PAYS = 16;  // scalars after the m column sums in the objective payload
+
+// Objective pieces, step 2 (one CTA of 1024): this rank's scalars into pay[m .. m + 16):
+//   {sum T DTD, sum T (ln T - 1), sum T C^2, max_i |a_i - p_i|, A_0 .. A_2k}
+// with a = T 1 (the row pass's S_0^tot) and A_r = sum_i a_i x_i^r (centred x).
+template <int K>
+__global__ void __launch_bounds__(1024) k64_objlocal(const double* __restrict__ tmp, int64_t m, const double* __restrict__ a,
                              const double* __restrict__ xl, const double* __restrict__ pl, int64_t nl,
                              double* __restrict__ pay) {
   __shared__ double sm[32];
@@ -296,54 +369,72 @@ __global__ void k64_objlocal(const double* __restrict__ tmp, int64_t m, const do
     s1 += tmp[m + p];
     s2 += tmp[2 * m + p];
   }
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0, dv = 0.0;
+  double A[2 * K + 1], dv = 0.0;
+#pragma unroll
+  for (int r = 0; r <= 2 * K; ++r) A[r] = 0.0;
   for (int64_t i = threadIdx.x; i < nl; i += blockDim.x) {
     const double v = a[i], x = xl[i];
-    a0 += v;
-    a1 += v * x;
-    a2 += v * x * x;
+    double xp = v;
+#pragma unroll
+    for (int r = 0; r <= 2 * K; ++r) {
+      A[r] += xp;
+      xp *= x;
+    }
     dv = fmax(dv, dev64(v - pl[i]));
   }
   s0 = bsum1024(s0, sm); s1 = bsum1024(s1, sm); s2 = bsum1024(s2, sm);
-  a0 = bsum1024(a0, sm); a1 = bsum1024(a1, sm); a2 = bsum1024(a2, sm);
+#pragma unroll
+  for (int r = 0; r <= 2 * K; ++r) A[r] = bsum1024(A[r], sm);
   dv = bmax1024(dv, sm);
   if (threadIdx.x == 0) {
     double* o = pay + m;
-    o[0] = s0; o[1] = s1; o[2] = s2; o[3] = a0; o[4] = a1; o[5] = a2; o[6] = dv; o[7] = 0.0;
+    o[0] = s0; o[1] = s1; o[2] = s2; o[3] = dv;
+#pragma unroll
+    for (int r = 0; r <= 2 * K; ++r) o[4 + r] = A[r];
   }
 }
 
-// Objective pieces, step 3 (one CTA of 1024): the ranks' payloads [R][m + 8] combined in rank order;
+// Objective pieces, step 3 (one CTA of 1024): the ranks' payloads [R][m + 16] combined in rank order;
 //   E(T) = a (D_X o D_X) a + b (D_Y o D_Y) b - 2 <D_X T D_Y, T>
-// with sum_ij (x_i - x_j)^2 a_i a_j = 2 (A0 A2 - A1^2) (likewise b over y), b = T^T 1.
-// out: [0] E, [1] max(|T1 - p|, |T^T 1 - q|), [3] H = sum T (ln T - 1), [6] sum T C^2 (FGW).
-__global__ void k64_objglobal(const double* __restrict__ gath, int R, int64_t m, const double* __restrict__ yc,
+// with sum_ij |x_i - x_j|^2k a_i a_j = sum_r kappa_r(2k) A_(2k-r) A_r (an even power: no split), likewise
+// b = T^T 1 over y.  out: [0] E, [1] max(|T1 - p|, |T^T 1 - q|), [3] H = sum T (ln T - 1), [6] sum T C^2.
+template <int K>
+__global__ void __launch_bounds__(1024) k64_objglobal(const double* __restrict__ gath, int R, int64_t m, const double* __restrict__ yc,
                               const double* __restrict__ qn, double* __restrict__ out) {
   __shared__ double sm[32];
-  const int64_t st = m + 8;
-  double b0 = 0.0, b1 = 0.0, b2 = 0.0, dv = 0.0;
+  const int64_t st = m + F64_PAYS;
+  double B[2 * K + 1], dv = 0.0;
+#pragma unroll
+  for (int r = 0; r <= 2 * K; ++r) B[r] = 0.0;
   for (int64_t p = threadIdx.x; p < m; p += blockDim.x) {
     double b = 0.0;
     for (int r = 0; r < R; ++r) b += gath[r * st + p];
     const double y = yc[p];
-    b0 += b;
-    b1 += b * y;
-    b2 += b * y * y;
+    double yp = b;
+#pragma unroll
+    for (int r = 0; r <= 2 * K; ++r) {
+      B[r] += yp;
+      yp *= y;
+    }
     dv = fmax(dv, dev64(b - qn[p]));
   }
-  b0 = bsum1024(b0, sm); b1 = bsum1024(b1, sm); b2 = bsum1024(b2, sm);
+#pragma unroll
+  for (int r = 0; r <= 2 * K; ++r) B[r] = bsum1024(B[r], sm);
   dv = bmax1024(dv, sm);
   if (threadIdx.x == 0) {
-    double s[7] = {0, 0, 0, 0, 0, 0, 0};
+    double s[4 + 2 * K + 1];
+    for (int k = 0; k < 4 + 2 * K + 1; ++k) s[k] = 0.0;
     for (int r = 0; r < R; ++r) {
       const double* o = gath + r * st + m;
-      for (int k = 0; k < 6; ++k) s[k] += o[k];
-      s[6] = fmax(s[6], o[6]);
+      for (int k = 0; k < 4 + 2 * K + 1; ++k) s[k] = k == 3 ? fmax(s[3], o[3]) : s[k] + o[k];
     }
-    const double Ea = 2.0 * (s[3] * s[5] - s[4] * s[4]);
-    const double Eb = 2.0 * (b0 * b2 - b1 * b1);
+    double Ea = 0.0, Eb = 0.0;
+    for (int r = 0; r <= 2 * K; ++r) {
+      Ea += kappa64(2 * K, r) * s[4 + 2 * K - r] * s[4 + r];
+      Eb += kappa64(2 * K, r) * B[2 * K - r] * B[r];
+    }
     out[0] = Ea + Eb - 2.0 * s[0];
-    out[1] = fmax(s[6], dv);
+    out[1] = fmax(s[3], dv);
     out[2] = 0.0;
     out[3] = s[1];
     out[4] = out[5] = 0.0;
@@ -481,7 +572,7 @@ __global__ void k64_colfinal(const double* __restrict__ gath, int R, int64_t str
 }
 
 // max of v[0 .. n) into *out (one CTA of 1024)
-__global__ void k64_max(const double* __restrict__ v, int64_t n, double* __restrict__ out) {
+__global__ void __launch_bounds__(1024) k64_max(const double* __restrict__ v, int64_t n, double* __restrict__ out) {
   __shared__ double sm[32];
   double d = 0.0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) d = fmax(d, v[i]);
@@ -489,7 +580,7 @@ __global__ void k64_max(const double* __restrict__ v, int64_t n, double* __restr
   if (threadIdx.x == 0) *out = d;
 }
 // violation = max(column deviations, every rank's row maximum gath[r * stride + 2m]) (one CTA of 1024)
-__global__ void k64_viol(const double* __restrict__ coldev, int64_t m, const double* __restrict__ gath, int R,
+__global__ void __launch_bounds__(1024) k64_viol(const double* __restrict__ coldev, int64_t m, const double* __restrict__ gath, int R,
                          int64_t stride, double* __restrict__ out) {
   __shared__ double sm[32];
   double d = 0.0;

@@ -436,8 +436,8 @@ static gw_status check_problem(const gw_problem* pb) {
   }
   if (pb->loss != GW_LOSS_SQUARE) return fail(GW_ERR_UNSUPPORTED, "only the square loss is defined (PAPER.md:86)");
   if (pb->dtype != GW_F32 && pb->dtype != GW_F64) return fail(GW_ERR_INVALID_ARG, "dtype %d is not a gw_dtype", pb->dtype);
-  if (pb->dtype == GW_F64 && (pb->k != 1 || (pb->flags & GW_GRID2D)))
-    return fail(GW_ERR_UNSUPPORTED, "GW_F64 storage: k = 1 on 1-D supports (f64.cuh)");
+  if (pb->dtype == GW_F64 && (pb->flags & GW_GRID2D))
+    return fail(GW_ERR_UNSUPPORTED, "GW_F64 storage: 1-D supports only (f64.cuh)");
   return GW_OK;
 }
 
@@ -1261,43 +1261,46 @@ static gw_status grad_pass(gw_ctx* c, const Prepared& P, int mode, const TSrc& S
 // the column prefixes / totals and the column LSE pairs are all-gathered and combined in rank order
 // (as shard.cuh does for the fp32 path), so one and several ranks agree up to summation order.
 
-// G = 2(c 1^T + 1 c'^T) - 4 D_X T D_Y (alpha, fx, fy: the FGW cost, Remark 2) for this rank's rows.
-// G may alias T unless obj.  obj: objout (device, 8 doubles) = {E, violation, -, H, -, -, sum T C^2, -}
-// of the plan T (over all ranks).  mom (nullable): supplied totals (gw_moments).
-static gw_status grad64(gw_ctx* c, const Prepared& P, const double* T, int64_t ldT, double* G, int64_t ldG, bool obj,
-                        const double* fx, const double* fy, double alpha, const gw_moments* mom, double* objout) {
+// G = 2(c 1^T + 1 c'^T) - 4 D_X T D_Y (alpha, fx, fy: the FGW cost, Remark 2) for this rank's rows,
+// distance power K (f64.cuh).  G may alias T unless obj.  obj: objout (device, 8 doubles) =
+// {E, violation, -, H, -, -, sum T C^2, -} of the plan T (over all ranks).  mom (nullable, K = 1):
+// supplied totals (gw_moments).
+template <int K>
+static gw_status grad64_k(gw_ctx* c, const Prepared& P, const double* T, int64_t ldT, double* G, int64_t ldG, bool obj,
+                          const double* fx, const double* fy, double alpha, const gw_moments* mom, double* objout) {
+  constexpr int NS = K + 1;
   const int64_t nl = P.nl, m = P.m;
   const int R = P.R;
   if (nl == 0) return GW_OK;  // single rank only: prepare() rejects empty shards when R > 1
   const int64_t nb = (nl + F64_RB - 1) / F64_RB;
   if (nb > 65535) return fail(GW_ERR_UNSUPPORTED, "GW_F64: at most %lld rows per rank", (long long)65535 * F64_RB);
   double *rtot, *part, *tot, *gath;
-  TRY(ws(c, c->d64rt, 4 * (size_t)nl, &rtot));
-  TRY(ws(c, c->d64part, (size_t)nb * 2 * m, &part));
-  TRY(ws(c, c->d64tot, 6 * (size_t)m, &tot));
-  TRY(ws(c, c->d64gath, (size_t)R * 2 * m, &gath));
-  double* rin = rtot + 2 * nl;
-  double* off = tot + 2 * m;
-  double* glob = tot + 4 * m;
+  TRY(ws(c, c->d64rt, (size_t)(NS + 2) * nl, &rtot));
+  TRY(ws(c, c->d64part, (size_t)nb * NS * m, &part));
+  TRY(ws(c, c->d64tot, 3 * (size_t)NS * m, &tot));
+  TRY(ws(c, c->d64gath, (size_t)R * NS * m, &gath));
+  double* rin = rtot + NS * nl;
+  double* off = tot + NS * m;
+  double* glob = tot + 2 * NS * m;
   const double* xl = P.xc + P.row0;
   NvtxRange nv("gw.grad64");
   PROF_BEGIN(c, PC_GRAD_MAIN);
-  if (mom) {
+  if (K == 1 && mom) {
     k64_momrows<<<grid_for(nl), 256, 0, c->stream>>>(mom->row_sum, mom->row_ysum, P.yend_u - P.ylast, nl, rin);
     KCHECK();
   }
-  // a2: B = T D_Y into G (one warp per row)
-  k64_row<<<(unsigned)((nl * 32 + 255) / 256), 256, 0, c->stream>>>(T, ldT, nl, m, P.yc, mom ? rin : nullptr, G, ldG,
-                                                                     rtot);
+  // a2: B' = (T D_Y)' into G (odd K) and the row power sums (one warp per row)
+  k64_row<K><<<(unsigned)((nl * 32 + 255) / 256), 256, 0, c->stream>>>(T, ldT, nl, m, P.yc,
+                                                                        (K == 1 && mom) ? rin : nullptr, G, ldG, rtot);
   KCHECK();
-  // a3: column block partials of B and x B, their exclusive prefix, the ranks' offsets and totals
+  // a3: column block power sums of B, their exclusive prefix, the ranks' offsets and totals
   const dim3 cg((unsigned)((m + 127) / 128), (unsigned)nb);
-  k64_colpart<<<cg, 128, 0, c->stream>>>(G, ldG, nl, m, xl, P.yc, rtot, part);
+  k64_colpart<K><<<cg, 128, 0, c->stream>>>(G, ldG, nl, m, xl, P.yc, rtot, part);
   KCHECK();
-  k64_colscan<<<(unsigned)((m + 127) / 128), 128, 0, c->stream>>>(part, (int)nb, m, tot);
+  k64_colscan<NS><<<(unsigned)((m + 127) / 128), 128, 0, c->stream>>>(part, (int)nb, m, tot);
   KCHECK();
-  TRY(comm_allgather(c, tot, gath, 2 * (size_t)m * sizeof(double)));
-  if (mom) {  // column totals of B = T D_Y from the supplied T^T 1, T^T x by 1-D DPs over y
+  TRY(comm_allgather(c, tot, gath, (size_t)NS * m * sizeof(double)));
+  if (K == 1 && mom) {  // column totals of B = T D_Y from the supplied T^T 1, T^T x by 1-D DPs over y
     double* v;
     TRY(ws(c, c->d64mc, 2 * (size_t)m, &v));
     k64_momcols<<<grid_for(m), 256, 0, c->stream>>>(mom->col_sum, mom->col_xsum, P.xend_u - P.xlast, m, v);
@@ -1306,23 +1309,24 @@ static gw_status grad64(gw_ctx* c, const Prepared& P, const double* T, int64_t l
     memset(&B, 0, sizeof(B));
     B.d[0] = Scan1D{v, P.yc, m, nullptr, glob, nullptr};
     B.d[1] = Scan1D{v + m, P.yc, m, nullptr, glob + m, nullptr};
-    const int K = (int)std::min<int64_t>(SCAN_KMAX, std::max<int64_t>(1, (m + 4095) / 4096));
+    const int KS = (int)std::min<int64_t>(SCAN_KMAX, std::max<int64_t>(1, (m + 4095) / 4096));
     double* wt;
-    TRY(ws(c, c->scanwt, (size_t)4 * K * 32 * 3, &wt));
-    k_scan1d_tot<<<dim3(K, 2), 1024, 0, c->stream>>>(B, K, wt);
+    TRY(ws(c, c->scanwt, (size_t)4 * KS * 32 * 3, &wt));
+    k_scan1d_tot<<<dim3(KS, 2), 1024, 0, c->stream>>>(B, KS, wt);
     KCHECK();
-    k_scan1d_out<<<dim3(K, 2), 1024, 0, c->stream>>>(B, K, wt);
+    k_scan1d_out<<<dim3(KS, 2), 1024, 0, c->stream>>>(B, KS, wt);
     KCHECK();
   }
-  k64_rankoff<<<(unsigned)((2 * m + 255) / 256), 256, 0, c->stream>>>(gath, R, P.rank, m, off, glob, mom != nullptr);
+  k64_rankoff<<<(unsigned)((NS * m + 255) / 256), 256, 0, c->stream>>>(gath, R, P.rank, NS * m, off, glob,
+                                                                       K == 1 && mom != nullptr);
   KCHECK();
   // a3 + a4: D_X B by the column scan, assembled into G in place
   double* ob = nullptr;
   if (obj) TRY(ws(c, c->d64obj, (size_t)nb * 4 * m, &ob));
   const double* fxl = fx ? fx + P.row0 : nullptr;
-#define K64_APPLY(O, F)                                                                                        \
-  k64_colapply<O, F><<<cg, 128, 0, c->stream>>>(G, ldG, T, ldT, nl, m, xl, part, off, glob, P.cx + P.row0, P.cy, \
-                                                 fxl, fy, alpha, P.yc, rtot, ob)
+#define K64_APPLY(O, F)                                                                                           \
+  k64_colapply<K, O, F><<<cg, 128, 0, c->stream>>>(G, ldG, T, ldT, nl, m, xl, part, off, glob, P.cx + P.row0, P.cy, \
+                                                    fxl, fy, alpha, P.yc, rtot, ob)
   if (obj) {
     if (fx) K64_APPLY(true, true); else K64_APPLY(true, false);
   } else {
@@ -1333,19 +1337,31 @@ static gw_status grad64(gw_ctx* c, const Prepared& P, const double* T, int64_t l
   PROF_END(c, PC_GRAD_MAIN, 5);
   if (obj) {  // a8: E(T), violation, H, sum T C^2
     double *tmp, *pay, *pg;
-    const int64_t st = m + 8;
+    const int64_t st = m + F64_PAYS;
     TRY(ws(c, c->d64tmp, 3 * (size_t)m, &tmp));
     TRY(ws(c, c->d64pay, (size_t)st, &pay));
     TRY(ws(c, c->d64pg, (size_t)R * st, &pg));
     k64_objcols<<<(unsigned)((m + 255) / 256), 256, 0, c->stream>>>(ob, (int)nb, m, pay, tmp);
     KCHECK();
-    k64_objlocal<<<1, 1024, 0, c->stream>>>(tmp, m, rtot, xl, P.pn + P.row0, nl, pay);
+    k64_objlocal<K><<<1, 1024, 0, c->stream>>>(tmp, m, rtot, xl, P.pn + P.row0, nl, pay);
     KCHECK();
     TRY(comm_allgather(c, pay, pg, (size_t)st * sizeof(double)));
-    k64_objglobal<<<1, 1024, 0, c->stream>>>(pg, R, m, P.yc, P.qn, objout);
+    k64_objglobal<K><<<1, 1024, 0, c->stream>>>(pg, R, m, P.yc, P.qn, objout);
     KCHECK();
   }
   return GW_OK;
+}
+
+static gw_status grad64(gw_ctx* c, const Prepared& P, const double* T, int64_t ldT, double* G, int64_t ldG, bool obj,
+                        const double* fx, const double* fy, double alpha, const gw_moments* mom, double* objout) {
+  switch (P.k) {
+    case 1: return grad64_k<1>(c, P, T, ldT, G, ldG, obj, fx, fy, alpha, mom, objout);
+    case 2: return grad64_k<2>(c, P, T, ldT, G, ldG, obj, fx, fy, alpha, mom, objout);
+    case 3: return grad64_k<3>(c, P, T, ldT, G, ldG, obj, fx, fy, alpha, mom, objout);
+    case 4: return grad64_k<4>(c, P, T, ldT, G, ldG, obj, fx, fy, alpha, mom, objout);
+    case 5: return grad64_k<5>(c, P, T, ldT, G, ldG, obj, fx, fy, alpha, mom, objout);
+    default: return fail(GW_ERR_UNSUPPORTED, "GW_F64: distance power k = %d", P.k);
+  }
 }
 
 // fp64 Sinkhorn state: the column exchange payload {max[m], sum[m], row deviation, pad} per rank.

@@ -242,7 +242,7 @@ def test_solver64_export_and_host(gw):
 
 
 def test_f64_unsupported(gw):
-    """GW_F64 is k = 1 on 1-D supports: other distance powers, 2-D grids and tau != eps are rejected."""
+    """GW_F64 is 1-D supports (k = 1..5): 2-D grids and tau != eps are rejected."""
     import torch
     from paper_2404_08970_b200 import _lib as L
     rng = np.random.default_rng(0)
@@ -250,7 +250,7 @@ def test_f64_unsupported(gw):
     p = q = np.full(16, 1 / 16)
     T = _to_dev64(gw, np.outer(p, q))
     with pytest.raises(L.GwError) as e:
-        gw.grad(x, y, p, q, T, k=2)
+        gw.grad(np.arange(4.0), np.arange(4.0), p, q, T, grid2d=True)
     assert e.value.code == "GW_ERR_UNSUPPORTED"
     with pytest.raises(L.GwError) as e:
         gw.solve(x, y, p, q, 0.1, 1, 5, tau=0.05, dtype=torch.float64)
@@ -330,3 +330,32 @@ def test_solver64_degenerate(gw):
         r1 = gw.solve(xa, yb, pa, qb, 0.05, 2, 10, return_plan=True, dtype=torch.float64)
         assert _rel(_np(r1.T), np.outer(pa, qb)) <= 1e-14
         assert abs(r1.gw_objective - O.objective(xa, yb, np.outer(pa, qb))) <= 1e-14 + 1e-12 * abs(r1.gw_objective)
+
+
+@pytest.mark.parametrize("k", [2, 3, 4, 5])
+@pytest.mark.parametrize("n,m", [(1, 1), (7, 3), (65, 129), (300, 257)])
+def test_grad64_power_k(gw, k, n, m):
+    """Distance powers k = 2..5 (reading R17) with fp64 storage: the k + 1 power-sum
+    scans (odd k) or totals (even k) vs grad_prescribed(k) (two dense DGEMMs)."""
+    rng = np.random.default_rng(100 * k + n + m)
+    x, y = np.sort(rng.random(n)), np.sort(rng.random(m))
+    p, q = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))
+    Tn = rng.exponential(size=(n, m)) / (n * m)
+    G = _np(gw.grad(x, y, p, q, _to_dev64(gw, Tn), k=k))
+    Go = O.grad_prescribed(x, y, p, q, Tn, k)
+    err = _rel(G, Go)
+    _log(test="grad64_k", k=k, n=n, m=m, err=err)
+    assert err <= GRAD64_TOL
+
+
+@pytest.mark.parametrize("k", [2, 3, 5])
+def test_solver64_power_k(gw, k):
+    """Entropic GW with |x - x'|^k (k = 2, 3, 5) and fp64 storage: trajectory against the oracle."""
+    import torch
+    P = W.config5(150, 120)
+    r = gw.solve(P.x, P.y, P.p, P.q, 0.02, 4, 60, k=k, trace_objective=True, dtype=torch.float64)
+    ro = O.entropic_gw(P.x, P.y, P.p, P.q, 0.02, 4, 60, k=k)
+    eE = float(np.max(np.abs(r.trace[:, 0] - ro["E"]) / np.abs(ro["E"])))
+    _log(test="solver64_k", k=k, eE=eE)
+    assert eE <= OBJ64_TOL
+    assert abs(r.entropic_objective - ro["entropic_objective"]) <= OBJ64_TOL * abs(ro["entropic_objective"])
