@@ -2,7 +2,7 @@
 """Randomised parity sweep (beyond the committed tests): many seeded random shapes, ties, marginals
 and distance powers through the C ABI against the float64 oracle.
 
-    python scripts/stress_parity.py [--cases 300] [--seed 0]
+    python scripts/stress_parity.py [--cases 300] [--seed 0] [--f64]
 
 Prints one line per failure and a summary; exit status 1 if any case fails.
 """
@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--cases", type=int, default=300)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--dump", default=None, help="directory for the inputs of failing solve cases")
+    ap.add_argument("--f64", action="store_true", help="also GW_F64 (fp64 storage) gradients and solves")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -53,7 +54,7 @@ def main():
         return w
 
     for case in range(args.cases):
-        kind = rng.choice(["grad", "grad", "grad", "solve", "grid"])
+        kind = rng.choice(["grad", "grad", "grad", "solve", "grid"] + (["grad64", "solve64"] if args.f64 else []))
         try:
             if kind == "grad":
                 n, m = int(rng.integers(1, 1500)), int(rng.integers(1, 1500))
@@ -101,6 +102,35 @@ def main():
                     if args.dump:
                         np.savez(os.path.join(args.dump, "fail_%d.npz" % case), x=x, y=y, p=p, q=q, eps=eps, k=k)
                 note("solve k=%d" % k, err, 1e-4, info)
+            elif kind == "grad64":  # fp64 storage: rounding-level parity
+                n, m = int(rng.integers(1, 1500)), int(rng.integers(1, 1500))
+                k = int(rng.choice([1, 1, 2, 3, 4, 5]))
+                x, y, p, q = supports(n), supports(m), marg(n), marg(m)
+                T = rng.random((n, m)) ** rng.choice([1, 3])
+                T /= T.sum()
+                Td = api.plan_buffer(n, m, dev, torch.float64)
+                Td.copy_(torch.from_numpy(T))
+                G = api.grad(x, y, p, q, Td, k=k).cpu().numpy()
+                Go = O.grad_prescribed(x, y, p, q, T, k=k)
+                note("grad64 k=%d" % k, np.max(np.abs(G - Go)) / max(np.max(np.abs(Go)), 1e-300), 1e-13,
+                     "n=%d m=%d" % (n, m))
+            elif kind == "solve64":
+                n, m = int(rng.integers(2, 400)), int(rng.integers(2, 400))
+                k = int(rng.choice([1, 1, 2, 3]))
+                iid = rng.random() < 0.5
+                if iid:
+                    x, y = np.sort(rng.random(n)), np.sort(rng.random(m))
+                else:
+                    x, y = np.sort(rng.beta(2, 5, n)), np.sort(rng.beta(5, 2, m))
+                p, q = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))
+                eps = float(rng.choice([0.01, 0.02, 0.05]))
+                r = api.solve(x, y, p, q, eps, 3, 60, device=dev, k=k, dtype=torch.float64)
+                ro = O.entropic_gw(x, y, p, q, eps, 3, 60, k=k)
+                E = ro["gw_objective"]
+                err = abs(r.gw_objective - E) / abs(E)
+                cls = "f64 " + ("iid" if iid else "beta")
+                devs.setdefault(cls, []).append(err)
+                note("solve64 k=%d" % k, err, 1e-10, "case=%d %s n=%d m=%d eps=%g k=%d" % (case, cls, n, m, eps, k))
             else:
                 nx, ny = int(rng.integers(1, 20)), int(rng.integers(1, 20))
                 sx, sy = np.sort(rng.random(nx)), np.sort(rng.random(ny))
