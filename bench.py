@@ -427,6 +427,18 @@ def main():
            "instrumented": instrumented, "clocks": ck, "e2e": e2e,
            "result": {"gw_objective": res.gw_objective, "marginal_violation": res.marginal_violation,
                       "inner_iters": res.inner_iters_total, "inner_fused": res.inner_fused_total}}
+    if rank == 0 and world == 1:
+        # configs[0] (C1) with the fp64 matrices SURVEY §8 gives it (GW_F64): context, not
+        # the headline; device time of the library's own events, after one warm-up solve
+        P1 = W.config1()
+        with torch.cuda.stream(stream):
+            api.solve(P1.x, P1.y, P1.p, P1.q, P1.eps, P1.outer, P1.inner, ctx=ctx, dtype=torch.float64)
+            r1 = api.solve(P1.x, P1.y, P1.p, P1.q, P1.eps, P1.outer, P1.inner, ctx=ctx, dtype=torch.float64)
+        torch.cuda.synchronize()
+        out["configs0_fp64"] = {"workload": "C1 (BASELINE configs[0]): N=M=256, eps=1e-2, 20 outer x 100 inner, "
+                                            "T0 = p q^T, fp64 matrix storage (GW_F64)",
+                                "outer_it_per_s": P1.outer / (r1.ms_total / 1e3), "ms_per_solve": r1.ms_total,
+                                "gw_objective": r1.gw_objective, "marginal_violation": r1.marginal_violation}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = oracle_sample(n_s=min(2048, args.n), n_full=args.n, inner=args.inner)
     if rank == 0:
