@@ -10,6 +10,7 @@
 #include <cstdint>
 
 #include "common.cuh"
+#include "small.cuh"  // cluster helpers, SNT, ld_dsmem_f64
 
 namespace gw {
 
@@ -590,6 +591,94 @@ __global__ void __launch_bounds__(1024) k64_viol(const double* __restrict__ cold
     for (int r = 0; r < R; ++r) d = fmax(d, gath[r * stride + 2 * m]);
     *out = d;
   }
+}
+
+
+// ---- cluster-resident fp64 Sinkhorn (small problems; C1) --------------------------------------------
+// The fp64 analogue of small.cuh: G (this CTA's rows, fp64) in shared memory, ALL `iters` iterations of
+// a fixed-count inner loop in one launch; per iteration the f-update (warp per own row, two-pass
+// max-shifted LSE) and the g-update (thread per column: (max, sum) over the CTA's rows, one cluster
+// barrier, the CL partials merged in CTA order through DSMEM, so g is bit-identical in every CTA).
+// Same formulas as k64_rowlse / k64_colfinal: exponent (g_p - G_ip) log2e/eps in fp64, exp2 in fp64,
+// LSE = ln 2 (max + log2 sum).
+struct Small64Args {
+  const double* G;
+  int64_t ld, nl, m;
+  int rows;  // rows per CTA (the last CTA may hold fewer)
+  const double *lp, *lq;
+  double eps;
+  int iters;
+  double *f, *g;  // in: warm start, out: final duals
+};
+
+// dynamic smem: Gs [rows][m] | gS [m] | part [2][2][m] (max, sum; double-buffered) | fS [rows] | lpS [rows]
+__host__ __device__ inline size_t small64_smem_bytes(int rows, int64_t m) {
+  return sizeof(double) * ((size_t)rows * m + 5 * (size_t)m + 2 * (size_t)rows);
+}
+
+__global__ void __launch_bounds__(SNT, 1) k64_sink_small(Small64Args a) {
+  extern __shared__ __align__(16) double dsm[];
+  const uint32_t cr = cluster_rank();
+  const uint32_t CL = gridDim.x;  // one cluster: every CTA of the grid
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  constexpr int NWp = SNT / 32;
+  const int64_t m = a.m;
+  const int64_t r0 = (int64_t)cr * a.rows;
+  const int nr = (int)max((int64_t)0, min((int64_t)a.rows, a.nl - r0));
+  double* Gs = dsm;
+  double* gS = Gs + (size_t)a.rows * m;
+  double* part = gS + m;  // [2 buffers][2 (max, sum)][m]
+  double* fS = part + 4 * m;
+  double* lpS = fS + a.rows;
+  const double c2 = GW_LOG2E / a.eps;
+  for (int r = 0; r < nr; ++r)
+    for (int64_t q = t; q < m; q += SNT) Gs[(size_t)r * m + q] = a.G[(r0 + r) * a.ld + q];
+  for (int64_t q = t; q < m; q += SNT) gS[q] = a.g[q];
+  for (int r = t; r < nr; r += SNT) {
+    fS[r] = a.f[r0 + r];
+    lpS[r] = a.lp[r0 + r];
+  }
+  __syncthreads();
+  cluster_arrive();
+  cluster_wait();  // every CTA's shared memory is live before any DSMEM access
+  for (int it = 0; it < a.iters; ++it) {
+    for (int r = w; r < nr; r += NWp) {  // f-update
+      const double* row = Gs + (size_t)r * m;
+      double mx = -INFINITY;
+      for (int64_t q = lane; q < m; q += 32) mx = fmax(mx, (gS[q] - row[q]) * c2);
+      mx = warp_max(mx);
+      double sm = 0.0;
+      if (mx != -INFINITY)
+        for (int64_t q = lane; q < m; q += 32) sm += exp2((gS[q] - row[q]) * c2 - mx);
+      sm = warp_sum(sm);
+      if (lane == 0) fS[r] = a.eps * lpS[r] - a.eps * ((mx + log2(sm)) * GW_LN2);
+    }
+    __syncthreads();
+    double* pb = part + (size_t)(it & 1) * 2 * m;
+    for (int64_t q = t; q < m; q += SNT) {  // g-update: this CTA's column partials
+      double mx = -INFINITY;
+      for (int r = 0; r < nr; ++r) mx = fmax(mx, (fS[r] - Gs[(size_t)r * m + q]) * c2);
+      double sm = 0.0;
+      if (mx != -INFINITY)
+        for (int r = 0; r < nr; ++r) sm += exp2((fS[r] - Gs[(size_t)r * m + q]) * c2 - mx);
+      pb[q] = mx;
+      pb[m + q] = sm;
+    }
+    cluster_arrive();
+    cluster_wait();  // every CTA's partials of this iteration are written
+    for (int64_t q = t; q < m; q += SNT) {
+      L64 acc{-INFINITY, 0.0};
+      for (uint32_t k = 0; k < CL; ++k)
+        acc = l64_merge(acc, L64{ld_dsmem_f64(mapa(pb + q, k)), ld_dsmem_f64(mapa(pb + m + q, k))});
+      gS[q] = a.eps * a.lq[q] - a.eps * ((acc.m + log2(acc.s)) * GW_LN2);
+    }
+    __syncthreads();
+  }
+  for (int r = t; r < nr; r += SNT) a.f[r0 + r] = fS[r];
+  if (cr == 0)
+    for (int64_t q = t; q < m; q += SNT) a.g[q] = gS[q];
+  cluster_arrive();
+  cluster_wait();  // no CTA exits while a peer may still read its partials
 }
 
 }  // namespace gw

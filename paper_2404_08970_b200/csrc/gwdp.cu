@@ -1434,6 +1434,44 @@ static gw_status sink64_viol(gw_ctx* c, const Prepared& P, Sink64& s, const doub
   }
   return GW_OK;
 }
+// Cluster size for the cluster-resident fp64 Sinkhorn (f64.cuh k64_sink_small): G's rows in one cluster's
+// shared memory, >= 16 rows per CTA where the rows allow (up to 16 CTAs); 0 if it does not fit.
+static int small64_cluster(const Prepared& P, int* rows_out, size_t* bytes_out) {
+  if (P.nl <= 0 || P.m <= 0) return 0;
+  int want = 1;
+  while (want < 16 && P.nl >= 16 * 2 * (int64_t)want) want *= 2;
+  for (int CL : {1, 2, 4, 8, 16}) {
+    if (CL < want) continue;
+    const int64_t rows = (P.nl + CL - 1) / CL;
+    const size_t bytes = small64_smem_bytes((int)std::min<int64_t>(rows, 1 << 20), P.m);
+    if (rows > (1 << 20) || bytes > 220 * 1024) continue;
+    if (CL > 1 && rows * (CL - 1) >= P.nl) continue;  // every CTA holds at least one row
+    static std::atomic<int> ok[32];  // occupancy verdict per CL (0 = unknown, 1 = fits, -1 = does not)
+    cudaFuncSetAttribute(k64_sink_small, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    if (CL > 8) cudaFuncSetAttribute(k64_sink_small, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (ok[CL].load() == 0) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(CL);
+      cfg.blockDim = dim3(SNT);
+      cfg.dynamicSmemBytes = 220 * 1024;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int ncl = 0;
+      const cudaError_t e = cudaOccupancyMaxActiveClusters(&ncl, (void*)k64_sink_small, &cfg);
+      ok[CL].store((e == cudaSuccess && ncl >= 1) ? 1 : -1);
+      cudaGetLastError();
+    }
+    if (ok[CL].load() < 0) continue;
+    *rows_out = (int)rows;
+    *bytes_out = bytes;
+    return CL;
+  }
+  return 0;
+}
+
 // `iters` iterations; tol > 0: the plan's violation checked every check_every iterations, stop when
 // <= tol (reading R8; the oracle's schedule exactly)
 static gw_status sink64_run(gw_ctx* c, const Prepared& P, Sink64& s, const double* G, int64_t ldG, double* f,
@@ -1443,6 +1481,32 @@ static gw_status sink64_run(gw_ctx* c, const Prepared& P, Sink64& s, const doubl
   *used = 0;
   *conv = 0;
   if (check_every < 1) check_every = 10;
+  // Fixed-count loop on one rank with G small enough for one cluster's shared memory: every iteration in
+  // ONE launch (k64_sink_small; GWDP_NO_SMALL=1 disables it)
+  if (tol <= 0 && iters > 0 && P.R == 1 && getenv("GWDP_NO_SMALL") == nullptr) {
+    int rows = 0;
+    size_t bytes = 0;
+    const int CL = small64_cluster(P, &rows, &bytes);
+    if (CL > 0) {
+      Small64Args sa{G, ldG, P.nl, P.m, rows, P.lp + P.row0, P.lq, eps, iters, f, g};
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(CL);
+      cfg.blockDim = dim3(SNT);
+      cfg.dynamicSmemBytes = bytes;
+      cfg.stream = c->stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      PROF_BEGIN(c, PC_SINK_ROW);
+      CU(cudaLaunchKernelEx(&cfg, k64_sink_small, sa));
+      KCHECK();
+      PROF_END(c, PC_SINK_ROW, 1);
+      *used = iters;
+      return GW_OK;
+    }
+  }
   // Fixed-count loop inside a solve (the same G, f, g, eps every outer iteration): up to 100 iterations
   // captured once as a CUDA graph and replayed (C1's 256 x 256 iterations are launch bound: 4 kernels
   // each).  Host-transport all-gathers are not capturable.

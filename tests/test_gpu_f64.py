@@ -359,3 +359,24 @@ def test_solver64_power_k(gw, k):
     _log(test="solver64_k", k=k, eE=eE)
     assert eE <= OBJ64_TOL
     assert abs(r.entropic_objective - ro["entropic_objective"]) <= OBJ64_TOL * abs(ro["entropic_objective"])
+
+
+@pytest.mark.parametrize("n,m", [(256, 256), (37, 300), (300, 5)])
+def test_solver64_small_vs_multikernel(gw, n, m, monkeypatch):
+    """The cluster-resident fp64 Sinkhorn (k64_sink_small: every inner iteration in one launch) and the
+    multi-kernel route (GWDP_NO_SMALL=1: row LSE, column partials, merge; graph-replayed) against each
+    other and the oracle."""
+    import torch
+    rng = np.random.default_rng(n + 7 * m)
+    x, y = np.sort(rng.random(n)), np.sort(rng.random(m))
+    p, q = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))
+    r_small = gw.solve(x, y, p, q, 0.01, 5, 100, trace_objective=True, dtype=torch.float64)
+    monkeypatch.setenv("GWDP_NO_SMALL", "1")
+    r_multi = gw.solve(x, y, p, q, 0.01, 5, 100, trace_objective=True, dtype=torch.float64)
+    ro = O.entropic_gw(x, y, p, q, 0.01, 5, 100)
+    es = float(np.max(np.abs(r_small.trace[:, 0] - ro["E"]) / np.abs(ro["E"])))
+    em = float(np.max(np.abs(r_multi.trace[:, 0] - ro["E"]) / np.abs(ro["E"])))
+    ef = float(np.max(np.abs(_np(r_small.f) - _np(r_multi.f))) / 0.01)
+    _log(test="small_vs_multi64", n=n, m=m, es=es, em=em, ef=ef)
+    assert max(es, em) <= OBJ64_TOL
+    assert ef <= OBJ64_TOL
