@@ -14,8 +14,9 @@ other than itself: worked examples (tests/golden/), closed forms, brute force,
 invariants and finite differences.  Functions without such a pin would say
 "parity unpinned".  ``ugw`` (Remark 3) follows readings R32-R35 (the paper leaves g(G^)
 undefined): its pieces are pinned (finite differences of the functional,
-direct minimisation of the subproblem, the balanced rho -> infinity limit), the reading itself
-is parity unpinned.
+direct minimisation of the subproblem, the balanced rho -> infinity limit) and so is the loop's
+fixed point (a critical point of the functional Remark 3 minimises); the per-iteration trajectory
+of the reading has no worked example in the paper and is parity unpinned.
 """
 
 from .gw import (  # noqa: F401

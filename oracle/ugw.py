@@ -27,8 +27,15 @@ R34  the subproblem is solved by unbalanced Sinkhorn in log form:
 R35  G^0 = u v / sqrt(m(u) m(v)), and after each subproblem the plan is rescaled by
      sqrt(m(G^) / m(G)) (mass balance of the UGW iteration).
 The rho -> infinity limit is balanced entropic GW at 2 eps with realised-marginal gradients
-(pinned against oracle.entropic_gw).  Beyond these pins the reading itself is "parity unpinned":
-the paper gives no worked example for UGW.
+(pinned against oracle.entropic_gw).  The loop as a whole (R32-R35 together) is pinned by what the
+functional fixes: Remark 3 minimises F_eps over all positive measures, so a fixed point of the
+iteration must have grad F_eps = 0 entrywise -- checked by central differences of the brute-force
+functional with m(u) != m(v) != 1 (tests/test_oracle_ugw.py::
+test_ugw_fixed_point_is_a_critical_point_of_the_functional; the mutations "rho~ = rho", "no square
+root in R35", "eps for rho in g" all move the fixed point off the critical set,
+profiles/r02_oracle_mutations.log).  What stays without a pin is the TRAJECTORY towards that fixed
+point (the paper gives no worked example for UGW and several iterations share the fixed point): for
+the per-iteration values the reading is still "parity unpinned".
 """
 
 import math

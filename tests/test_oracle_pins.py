@@ -615,8 +615,7 @@ def test_fgw_2d_bruteforce_and_reductions():
 def test_mirror_descent_general_tau_is_the_kl_proximal_step():
     """with tau != eps the oracle's step solves the cost Pi = G + (eps - tau) ln T^l at
     regulariser tau; that must equal the KL-proximal step argmin <grad E + eps grad H(T^l), T> +
-    tau KL(T|T^l) over S(p,q), minimised directly (scipy, tiny instance)."""
-    from scipy.optimize import minimize
+    tau KL(T|T^l) over S(p,q), minimised directly (scipy, tiny instance), at the first TWO steps."""
     rng = np.random.default_rng(21)
     n, m = 3, 4
     x, y = np.sort(rng.random(n)), np.sort(rng.random(m))
@@ -624,6 +623,23 @@ def test_mirror_descent_general_tau_is_the_kl_proximal_step():
     eps, tau = 0.08, 0.03
     r1 = O.entropic_gw(x, y, p, q, eps, 1, 4000, tau=tau)
     Tl = np.outer(p, q)
+    _check_kl_proximal_step(x, y, p, q, eps, tau, Tl, r1["T"])
+    # second step: ln T^1 is no longer separable (on T^0 = p (x) q the (eps - tau) ln T^0 term only shifts
+    # the duals, so the first step alone cannot see its sign)
+    r2 = O.entropic_gw(x, y, p, q, eps, 2, 4000, tau=tau)
+    _check_kl_proximal_step(x, y, p, q, eps, tau, r1["T"], r2["T"])
+    for t2 in (0.03, 0.2):  # and the sign matters: tau on either side of eps gives different plans
+        assert np.max(np.abs(O.entropic_gw(x, y, p, q, eps, 2, 4000, tau=t2)["T"]
+                             - O.entropic_gw(x, y, p, q, eps, 2, 4000)["T"])) > 1e-4
+    # tau = eps is the default path exactly
+    a = O.entropic_gw(x, y, p, q, eps, 3, 50)
+    b = O.entropic_gw(x, y, p, q, eps, 3, 50, tau=eps)
+    np.testing.assert_array_equal(a["T"], b["T"])
+
+
+def _check_kl_proximal_step(x, y, p, q, eps, tau, Tl, T_next):
+    from scipy.optimize import minimize
+    n, m = Tl.shape
     G = O.grad_prescribed(x, y, p, q, Tl)
     C = G + eps * np.log(Tl)  # grad E + eps grad H(T^l)
 
@@ -647,8 +663,90 @@ def test_mirror_descent_general_tau_is_the_kl_proximal_step():
     r = minimize(obj, np.zeros(len(basis)), jac=True, method="L-BFGS-B",
                  options={"ftol": 1e-15, "gtol": 1e-12, "maxiter": 5000})
     Tp = Tl + np.tensordot(r.x, basis, 1)
-    np.testing.assert_allclose(r1["T"], Tp, atol=1e-8)
-    # tau = eps is the default path exactly
-    a = O.entropic_gw(x, y, p, q, eps, 3, 50)
-    b = O.entropic_gw(x, y, p, q, eps, 3, 50, tau=eps)
-    np.testing.assert_array_equal(a["T"], b["T"])
+    np.testing.assert_allclose(T_next, Tp, atol=1e-8)
+
+
+# --------------------------------------------------------------------------- result fields / wiring
+
+def test_entropic_objective_field_closed_form_and_duality():
+    """The reported entropic objective is E(T) + eps H(T), H = sum T (ln T - 1).
+    (i) outer = 0: T = p (x) p uniform on the uniform grid, where E has the closed form P6 and
+    H(p (x) p) = -2 ln N - 1.  (ii) after converged inner loops T = exp((f + g - G)/eps) is feasible, so
+    eps H(T) = <f, p> + <g, q> - <G, T> - eps (Gibbs form + marginals; no logarithm of T taken here)."""
+    n, eps = 10, 0.07
+    x = np.arange(n) / (n - 1)
+    p = np.full(n, 1.0 / n)
+    r0 = O.entropic_gw(x, x, p, p, eps, 0, 5)
+    closed = (n + 1) / (3 * (n - 1)) - 2 * ((n + 1) / (3 * n)) ** 2
+    assert r0["entropic_objective"] == pytest.approx(closed + eps * (-2 * math.log(n) - 1), rel=1e-12)
+    rng = np.random.default_rng(31)
+    n, m = 7, 5
+    x, y = _sorted(rng, n), _sorted(rng, m)
+    p, q = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))
+    fx, fy = rng.standard_normal(n), rng.standard_normal(m)
+    r = O.entropic_gw(x, y, p, q, eps, 3, 3000, record_grads=True)
+    G, T = r["G"][-1], r["T"]
+    dual = r["f"] @ p + r["g"] @ q - np.sum(G * T) - eps
+    assert r["entropic_objective"] - r["gw_objective"] == pytest.approx(dual, rel=1e-9)
+    assert r["entropic_objective"] - r["gw_objective"] < 0 < r["gw_objective"]
+    # FGW: same identity with the FGW gradient of the previous plan as the cost
+    alpha = 0.4
+    rf2 = O.entropic_fgw(x, y, p, q, fx, fy, alpha, eps, 2, 3000)
+    rf3 = O.entropic_fgw(x, y, p, q, fx, fy, alpha, eps, 3, 3000)
+    Gf = O.fgw_grad_prescribed(x, y, p, q, fx, fy, alpha, rf2["T"])
+    dual = rf3["f"] @ p + rf3["g"] @ q - np.sum(Gf * rf3["T"]) - eps
+    assert rf3["entropic_objective"] - rf3["gw_objective"] == pytest.approx(dual, rel=1e-9)
+
+
+def test_entropic_fgw_wiring_intermediate_alpha():
+    """Remark 2: every FGW outer step is the entropic OT problem of the cost
+    grad E_bar(T^l).  With converged inner loops the step's plan is the unique minimiser, so it must
+    equal the Sinkhorn fixed point of that cost from a cold start, with the features on the right
+    sides (fx on rows, fy on columns: N != M makes a swap an error, equal sizes would hide it, so both)."""
+    rng = np.random.default_rng(33)
+    for n, m in ((6, 6), (7, 4)):
+        x, y = _sorted(rng, n), _sorted(rng, m)
+        p, q = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))
+        fx, fy = rng.standard_normal(n), rng.standard_normal(m)
+        alpha, eps = 0.3, 0.08
+        T = np.outer(p, q)
+        for l in range(1, 3):
+            C = np.empty((n, m))
+            for i in range(n):
+                for j in range(m):
+                    C[i, j] = (1 - alpha) * (fx[i] - fy[j]) ** 2
+            C += alpha * O.grad_entrywise(x, y, T)  # T in S(p, q): realised = prescribed marginals
+            f, g, _ = O.sinkhorn(C, p, q, eps, 4000)
+            T = O.plan_from_duals(C, f, g, eps)
+            r = O.entropic_fgw(x, y, p, q, fx, fy, alpha, eps, l, 4000)
+            np.testing.assert_allclose(r["T"], T, atol=1e-10)
+            val = (1 - alpha) * sum((fx[i] - fy[j]) ** 2 * T[i, j] for i in range(n) for j in range(m)) \
+                + alpha * O.objective_bruteforce(x, y, T)
+            assert r["gw_objective"] == pytest.approx(val, rel=1e-8)
+
+
+def test_grid_points_flattening():
+    """Row i = a n + b of a 2-D grid is the point (axis[a], axis[b]) (reading R31)."""
+    P = O.grid_points([0.0, 0.5, 2.0])
+    assert P.shape == (9, 2)
+    assert tuple(P[1]) == (0.0, 0.5) and tuple(P[3]) == (0.5, 0.0) and tuple(P[5]) == (0.5, 2.0)
+
+
+def test_entropic_gw_restart_from_T0_is_the_next_step():
+    """T0 (reading R5) is the plan the first gradient is evaluated on: with converged inner loops each
+    step's plan is the unique minimiser of PAPER.md:108-114, so two steps from p (x) q equal one step
+    restarted from the first step's plan (the duals restart from zero; the minimiser does not care)."""
+    rng = np.random.default_rng(35)
+    n, m = 6, 8
+    x, y = _sorted(rng, n), _sorted(rng, m)
+    p, q = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))
+    eps = 0.06
+    r1 = O.entropic_gw(x, y, p, q, eps, 1, 4000)
+    r2 = O.entropic_gw(x, y, p, q, eps, 2, 4000)
+    rr = O.entropic_gw(x, y, p, q, eps, 1, 4000, T0=r1["T"])
+    np.testing.assert_allclose(rr["T"], r2["T"], atol=1e-11)
+    assert np.max(np.abs(r2["T"] - r1["T"])) > 1e-4
+    rf1 = O.entropic_fgw(x, y, p, q, x[::-1], y, 0.5, eps, 1, 4000)
+    rf2 = O.entropic_fgw(x, y, p, q, x[::-1], y, 0.5, eps, 2, 4000)
+    rfr = O.entropic_fgw(x, y, p, q, x[::-1], y, 0.5, eps, 1, 4000, T0=rf1["T"])
+    np.testing.assert_allclose(rfr["T"], rf2["T"], atol=1e-11)

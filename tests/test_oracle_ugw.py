@@ -1,6 +1,7 @@
 """Pins for the UGW oracle (oracle/ugw.py; Remark 3; readings R32-R35).
-The paper leaves g(G^) undefined, so the reading is parity unpinned; these tests pin every
-piece of it to something other than itself."""
+The paper leaves g(G^) undefined; these tests pin every piece of the reading to something other
+than itself and the whole loop by its fixed point (a critical point of the functional Remark 3
+minimises).  The per-iteration trajectory has no worked example in the paper: parity unpinned."""
 
 import math
 
@@ -103,6 +104,36 @@ def test_ugw_mass_rescaling_and_symmetry():
     r2 = O.entropic_ugw(y, x, v, u, 0.5, 0.05, 3, 200)
     np.testing.assert_allclose(r1["F"], r2["F"], rtol=1e-10)
     assert all(0.0 < mm < 1.0 + 1e-9 for mm in r1["mass"])
+
+
+@pytest.mark.parametrize("rho,eps", [(1.0, 0.1), (0.5, 0.05)])
+def test_ugw_fixed_point_is_a_critical_point_of_the_functional(rho, eps):
+    """Remark 3 minimises F_eps over all positive measures (no constraint), by
+    alternate minimisation of the bi-convex relaxation; a fixed point G = G^ of the whole iteration
+    (readings R32-R35: cost 1/2 grad E + g, the mass-scaled rho~, eps~, the square-root rescaling)
+    therefore has grad F_eps(G) = 0 entrywise.  Checked by central differences of the BRUTE-FORCE
+    functional; any mistake in the loop's scalings (rho~ = rho, no square root, a wrong g(G^)) moves
+    the fixed point off the critical set.  Masses of u, v differ from 1 and from each other."""
+    rng, x, y, u, v = _problem(3, 5, 4)
+    u, v = 0.8 * u, 1.3 * v
+    r = O.entropic_ugw(x, y, u, v, rho, eps, 300, 300)
+    T = np.asarray(r["T"])
+    assert abs(r["F"][-1] - r["F"][-2]) <= 1e-13
+
+    def grad_fd(Z):
+        g = np.zeros_like(Z)
+        for i in range(Z.shape[0]):
+            for j in range(Z.shape[1]):
+                h = 1e-6 * Z[i, j]
+                Zp, Zm = Z.copy(), Z.copy()
+                Zp[i, j] += h
+                Zm[i, j] -= h
+                g[i, j] = (O.ugw_functional_bruteforce(x, y, u, v, Zp, rho, eps, 1)
+                           - O.ugw_functional_bruteforce(x, y, u, v, Zm, rho, eps, 1)) / (2 * h)
+        return g
+    g0 = np.abs(grad_fd(np.outer(u, v) / math.sqrt(u.sum() * v.sum()))).max()
+    assert g0 > 0.1                                   # the start plan is far from critical
+    assert np.abs(grad_fd(T)).max() <= 1e-6 * g0      # measured 3e-8 / 0.35
 
 
 def test_ugw_start_and_masses():
