@@ -73,4 +73,7 @@ from .streamed import (  # noqa: F401
     violation_streamed,
     objective_k1,
     dist_apply_prefix,
+    fgw_rows_cols,
+    fgw_objective_k1,
+    ugw_functional_k1,
 )

@@ -17,6 +17,11 @@ by block); objective_k1 iterates them twice, so it takes a sequence (e.g. views 
   with both factors formed by the k = 1 definition written as prefix sums,
       sum_j |s_i - s_j| v_j = s_i (P_<i - P_>i) - (Q_<i - Q_>i),  P = cumsum(v), Q = cumsum(s v),
   (distributivity of the lower / upper triangular sums), in float64.
+* fgw_rows_cols / fgw_objective_k1 (C5: 32768 x 24576): Remark 2's gradient and objective
+   from the GW pieces above and the feature cost (fx_i - fy_p)^2 (reading R29).
+* ugw_functional_k1: F_eps of reading R33 (PAPER.md:150-153 + the entropic term) for a streamed plan:
+  E by objective_k1, the three tensorised KLs by KL(x (x) x | y (x) y) = 2 m(x) <log(x/y), x> - m(x)^2
+  + m(y)^2 with the plan's <log(T/(u v)), T> accumulated block by block (0 log 0 = 0).
 """
 
 import numpy as np
@@ -24,7 +29,7 @@ import numpy as np
 from .gw import _f64, ref_dp_distance
 
 __all__ = ["const_term_blocked", "grad_rows_cols", "marginals_streamed", "violation_streamed",
-           "objective_k1", "dist_apply_prefix"]
+           "objective_k1", "dist_apply_prefix", "fgw_rows_cols", "fgw_objective_k1", "ugw_functional_k1"]
 
 BLK = 2048
 
@@ -156,3 +161,47 @@ def objective_k1(x, y, T_blocks, workers=1):
         m0, m1, m2 = w.sum(), w @ s, w @ (s * s)
         return 2.0 * (m0 * m2 - m1 * m1)
     return float(quad(x, a) + quad(y, b) - 2.0 * total)
+
+
+def fgw_rows_cols(x, y, p, q, fx, fy, alpha, T_blocks, I, J, const=None):
+    """Rows I and columns J of grad E_bar = (1 - theta) C o C + theta (2(c 1^T + 1 c'^T) - 4 D_X T D_Y)
+    (PAPER.md:141-145 with theta = alpha, transpose typo fixed as in R3; C o C = (fx_i - fy_p)^2)."""
+    fx, fy = _f64(fx), _f64(fy)
+    I, J = np.asarray(I), np.asarray(J)
+    GI, GJ = grad_rows_cols(x, y, p, q, T_blocks, I, J, 1, const)
+    return ((1.0 - alpha) * (fx[I, None] - fy[None, :]) ** 2 + alpha * GI,
+            (1.0 - alpha) * (fx[:, None] - fy[None, J]) ** 2 + alpha * GJ)
+
+
+def fgw_objective_k1(x, y, fx, fy, alpha, T_blocks, workers=1):
+    """E_bar(T) = (1 - theta) sum_ip (fx_i - fy_p)^2 T_ip + theta E(T), streamed."""
+    fx, fy = _f64(fx), _f64(fy)
+    blocks = list(T_blocks)
+    lin = 0.0
+    for j0, Tb in blocks:
+        Tb = _f64(Tb)
+        lin += float(np.sum((fx[j0:j0 + Tb.shape[0], None] - fy[None, :]) ** 2 * Tb))
+    return (1.0 - alpha) * lin + alpha * objective_k1(x, y, blocks, workers)
+
+
+def ugw_functional_k1(x, y, u, v, T_blocks, rho, eps, workers=1):
+    """F_eps(G) (reading R33) for a streamed plan, k = 1.  Returns (F, E, mass)."""
+    u, v = _f64(u), _f64(v)
+    blocks = list(T_blocks)
+    a, b = marginals_streamed(blocks, u.size, v.size)
+
+    def xlogy_sum(w, ref):       # <log(w/ref), w>, 0 log 0 = 0
+        pos = w > 0
+        return float(np.sum(w[pos] * np.log(w[pos] / ref[pos])))
+
+    def kl_sq(w, ref):           # KL(w (x) w | ref (x) ref)
+        return 2.0 * w.sum() * xlogy_sum(w, ref) - w.sum() ** 2 + ref.sum() ** 2
+
+    ent = 0.0
+    for j0, Tb in blocks:
+        Tb = _f64(Tb)
+        ent += xlogy_sum(Tb, u[j0:j0 + Tb.shape[0], None] * v[None, :])
+    mass = float(a.sum())
+    kl_plan = 2.0 * mass * ent - mass ** 2 + (u.sum() * v.sum()) ** 2
+    E = objective_k1(x, y, blocks, workers)
+    return E + rho * kl_sq(a, u) + rho * kl_sq(b, v) + eps * kl_plan, E, mass

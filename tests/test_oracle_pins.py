@@ -506,6 +506,35 @@ def test_streamed_objective_and_violation_match_dense():
     assert O.objective_k1(g, g, _blocks(np.outer(pp, pp), 64)) == pytest.approx(closed, rel=1e-12)
 
 
+def test_streamed_fgw_and_ugw_match_dense():
+    """C5-size evaluations: fgw_rows_cols / fgw_objective_k1 equal the dense FGW gradient (itself pinned
+    by brute force) and objective; ugw_functional_k1 equals the BRUTE-FORCE functional with every
+    tensor product formed (tiny) and the dense closed form (larger), zero entries and masses != 1
+    included."""
+    rng = np.random.default_rng(57)
+    n, m = 83, 61
+    x, y = _sorted(rng, n), _sorted(rng, m)
+    p, q = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))
+    fx, fy = rng.standard_normal(n), rng.standard_normal(m)
+    T = rng.random((n, m)) / (n * m)
+    T[rng.random((n, m)) < 0.1] = 0.0
+    I, J = np.array([0, 5, 40, n - 1]), np.array([1, 2, 33, m - 1])
+    for alpha in (0.0, 0.3, 1.0):
+        G = O.fgw_grad_prescribed(x, y, p, q, fx, fy, alpha, T)
+        GI, GJ = O.fgw_rows_cols(x, y, p, q, fx, fy, alpha, _blocks(T, 20), I, J)
+        np.testing.assert_allclose(GI, G[I], atol=1e-13)
+        np.testing.assert_allclose(GJ, G[:, J], atol=1e-13)
+        assert O.fgw_objective_k1(x, y, fx, fy, alpha, _blocks(T, 20), workers=2) == pytest.approx(
+            O.fgw_objective(x, y, fx, fy, alpha, T), rel=1e-12)
+    u, v = 0.7 * p, 1.4 * q
+    F, E, mass = O.ugw_functional_k1(x, y, u, v, _blocks(T, 20), 0.8, 0.05)
+    assert F == pytest.approx(O.ugw_functional(x, y, u, v, T, 0.8, 0.05), rel=1e-12)
+    assert E == pytest.approx(O.objective(x, y, T), rel=1e-12) and mass == pytest.approx(T.sum(), rel=1e-14)
+    Ts = T[:5, :4] * 300
+    Fs, _, _ = O.ugw_functional_k1(x[:5], y[:4], u[:5], v[:4], _blocks(Ts, 2), 0.8, 0.05)
+    assert Fs == pytest.approx(O.ugw_functional_bruteforce(x[:5], y[:4], u[:5], v[:4], Ts, 0.8, 0.05), rel=1e-11)
+
+
 # --------------------------------------------------------------------------- workloads
 
 def test_workloads_deterministic_and_valid():
