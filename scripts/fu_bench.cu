@@ -22,8 +22,15 @@ int main(int argc, char** argv) {
 #else
   constexpr int NTT = 256;
 #endif
+#ifdef FU_LD0  // every row reads the SAME M floats (L2 resident): the iteration's floor without HBM traffic
+  const int64_t ldk = 0;
+  float* G; cudaMalloc(&G, m * 4);
+  fillf<<<1184, 256>>>(G, m, 0.01f, 0.f);
+#else
+  const int64_t ldk = ld;
   float* G; cudaMalloc(&G, n * ld * 4);
   fillf<<<1184, 256>>>(G, n * ld, 0.01f, 0.f);
+#endif
   float *fh, *fl, *gh, *gl, *pf, *Srow; double* part; int* mode;
   cudaMalloc(&fh, n * 4); cudaMalloc(&fl, n * 4); cudaMalloc(&gh, m * 4); cudaMalloc(&gl, m * 4);
   cudaMalloc(&pf, n * 4); cudaMalloc(&Srow, n * 4); cudaMalloc(&part, 160 * m * 8); cudaMalloc(&mode, 16);
@@ -41,7 +48,7 @@ int main(int argc, char** argv) {
   int ncl = 0; cudaOccupancyMaxActiveClusters(&ncl, (void*)k, &cfg);
   cfg.gridDim = dim3(ncl * CLL);
   FusedArgs a = {};
-  a.G = G; a.ld = ld; a.nl = n; a.m = m; a.c2f = 1442.7f; a.gh = gh; a.gl = gl; a.fh = fh; a.fl = fl; a.pf = pf;
+  a.G = G; a.ld = ldk; a.nl = n; a.m = m; a.c2f = 1442.7f; a.gh = gh; a.gl = gl; a.fh = fh; a.fl = fl; a.pf = pf;
   a.kappa = 1.f; a.Srow = Srow; a.part = part; a.rows_per_cluster = (n + ncl - 1) / ncl; a.wcol = 4 * KK * NTT; a.mode = mode; a.stop = nullptr;
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   cudaLaunchKernelEx(&cfg, k, a);
