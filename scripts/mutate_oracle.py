@@ -121,8 +121,15 @@ def run_one(idx, mut):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--jobs", type=int, default=8)
+    ap.add_argument("--only", default=None, help="comma-separated substrings of 'function: mistake' to select mutations")
     a = ap.parse_args()
     muts = list(MUTATIONS)
+    if a.only:
+        keys = [k.strip() for k in a.only.split(",")]
+        muts = [m for m in muts if any(k in "%s: %s" % (m[1], m[4]) for k in keys)]
+        if not muts:
+            print("no mutation selected")
+            return 2
     res = []
     with cf.ThreadPoolExecutor(a.jobs) as ex:
         for r in ex.map(lambda im: run_one(*im), enumerate(muts)):
