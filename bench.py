@@ -19,7 +19,7 @@ e2e         : the same metric through the public host-vector call (api.solve_hos
               copies of x, y, p, q and the D2H copies of the duals are inside the timed region.
 roofline    : the dominant kernel (the fused one-read Sinkhorn sweep): algorithmic bytes 4 N_local M
               per iteration / its live event-timed duration, against MEASURED_PEAKS.json hbm_gbs;
-              traffic from the committed ncu capture (profiles/r01_ncu_traffic.json).
+              traffic from the committed ncu capture (profiles/r02_ncu_traffic.json).
 grad        : the DP gradient (metric M1): 12 N_local M bytes / its event-timed duration.
 cpu_baseline / --impl reference : the float64 NumPy oracle (oracle/) on the host cores, a bounded
               sample extrapolated to the metric's unit (see "sample").
