@@ -26,7 +26,9 @@
  *     The caller owns every argument; the library never frees or retains them.
  *   - N x M matrices: row-major fp32 (gw_dtype GW_F32), leading dimension
  *     ld >= m, ld % 4 == 0, 16-byte aligned base.  A rank holds only its
- *     n_local rows [row0, row0 + n_local).
+ *     n_local rows [row0, row0 + n_local).  Only the elements [0, n_local) x
+ *     [0, m) of an output matrix are written: its padding columns [m, ld) and
+ *     anything outside its rows are left untouched (tests/test_gpu_canary.py).
  *   - Work is enqueued on ctx's stream.  Calls that fill host structs
  *     (info, res, trace) synchronise that stream before returning.
  *   - Errors: a status is returned; no exception or abort crosses the ABI;

@@ -60,7 +60,8 @@ def _plan(rng, n, m):
     return T / T.sum()
 
 
-@pytest.mark.parametrize("n,m", [(1, 1), (37, 53), (300, 517), (1000, 777), (130, 9001)])
+@pytest.mark.parametrize("n,m", [(1, 1), (37, 53), (300, 517), (1000, 777), (130, 9001), (64, 1003), (50, 1002),
+                                 (513, 4099)])
 @pytest.mark.parametrize("k", [1, 2, 3])
 def test_grad_fp32_canaries(gw, n, m, k):
     import torch
@@ -79,7 +80,8 @@ def test_grad_fp32_canaries(gw, n, m, k):
     assert bool(torch.isfinite(G.view).all())
 
 
-@pytest.mark.parametrize("n,m,k", [(1, 1, 1), (133, 70, 1), (300, 257, 1), (257, 300, 3), (64, 1000, 2)])
+@pytest.mark.parametrize("n,m,k", [(1, 1, 1), (133, 70, 1), (300, 257, 1), (257, 300, 3), (64, 1000, 2),
+                                   (90, 1003, 1), (90, 1003, 2)])
 def test_grad_fp64_canaries(gw, n, m, k):
     import torch
     dev = torch.device("cuda", 0)
