@@ -153,3 +153,36 @@ def test_sinkhorn_and_solve_canaries(gw, n, m, dtype):
         torch.cuda.synchronize()
         assert eG2.guards_intact() and eG2.padding_intact()
         assert bool(torch.isfinite(eG2.view).all())
+
+
+def test_validation_errors_write_nothing(gw):
+    """include/gwdp.h: "Argument and validation errors are detected before any output is written"."""
+    import torch
+    from paper_2404_08970_b200 import GwError
+    dev = torch.device("cuda", 0)
+    n, m = 120, 77
+    rng = np.random.default_rng(5)
+    x, y = np.sort(rng.random(n)), np.sort(rng.random(m))
+    p, q = rng.dirichlet(np.ones(n)), rng.dirichlet(np.ones(m))
+    T, G = Guarded(n, m, torch.float32, dev), Guarded(n, m, torch.float32, dev)
+    T.view.copy_(torch.from_numpy(_plan(rng, n, m)))
+    g0 = G.snapshot()
+    bad_x = x.copy()
+    bad_x[[3, 4]] = bad_x[[4, 3]]                      # unsorted support
+    bad_p = p.copy()
+    bad_p[7] = -bad_p[7]                               # negative mass
+    for args in ((bad_x, y, p, q), (x, y, bad_p, q), (x, y, 2.0 * p, q)):
+        with pytest.raises(GwError):
+            gw.grad(*args, T.view, out=G.view)
+        torch.cuda.synchronize()
+        assert G.unchanged(g0), "gw_grad_dp wrote into G before rejecting its arguments"
+    eT, eG = Guarded(n, m, torch.float32, dev), Guarded(n, m, torch.float32, dev)
+    t0, g1 = eT.snapshot(), eG.snapshot()
+    with pytest.raises(GwError):
+        gw.solve(bad_x, y, p, q, 0.02, 2, 10, device=dev, export_iter=1, export_T=eT.view, export_G=eG.view)
+    torch.cuda.synchronize()
+    assert eT.unchanged(t0) and eG.unchanged(g1)
+    # the rejected call consumed its one-shot export request: the next valid solve exports nothing
+    gw.solve(x, y, p, q, 0.02, 2, 10, device=dev)
+    torch.cuda.synchronize()
+    assert eT.unchanged(t0) and eG.unchanged(g1)
